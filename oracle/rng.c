@@ -1,0 +1,187 @@
+/*
+ * CPU ORACLE -- test infrastructure only.  Never linked into the product.
+ *
+ * Plain-C restatement of the random-number arithmetic the reference relies
+ * on.  The reference builds every stream as
+ *     numpy.random.Generator(numpy.random.Philox(key=blake2b(...)))
+ * (sm/core.py:119-126) and draws with `integers` (sm/core.py:128-129),
+ * `normal` (:131-132), `uniform` (:134-135) and `poisson` (:137-138).  That
+ * arithmetic lives in the third-party dependency numpy, pinned at 2.3.5,
+ * which is not part of /root/reference; restated here from numpy's published
+ * algorithms:
+ *   - Philox4x64-10 (Random123, as vendored by numpy/random/src/philox):
+ *     counter pre-incremented before each 4-word block, key bumped by the
+ *     Weyl constants between rounds;
+ *   - next_uint32: low half of a 64-bit word first, high half buffered
+ *     (`has_uint32`), the buffer persisting across calls;
+ *   - next_double: (w >> 11) * 2^-53;
+ *   - integers(lo, hi) for hi-lo <= 2^32: 32-bit Lemire with the rejection
+ *     threshold (2^32 - ex) % ex; hi-lo == 1 consumes nothing;
+ *   - standard normal: 256-layer ziggurat on next_uint64 with the tables
+ *     lifted from libnpyrandom.a (tools/extract_ziggurat.py);
+ *   - poisson(lam < 10): multiplication method on next_double.
+ * Pinned against numpy itself by tests/test_oracle_rng.py and against the
+ * committed golden vectors in tests/golden/.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "ziggurat_tables.h"
+
+#define PHILOX_M0 0xD2E7470EE14C6C93ULL
+#define PHILOX_M1 0xCA5A826395121157ULL
+#define PHILOX_W0 0x9E3779B97F4A7C15ULL
+#define PHILOX_W1 0xBB67AE8584CAA73BULL
+
+typedef struct {
+  uint64_t k0, k1;
+  uint64_t ctr;     /* number of 4-word blocks produced so far */
+  int pos;          /* next word inside buf (4 = empty) */
+  uint64_t buf[4];
+  int has32;        /* a buffered high half is pending */
+  uint32_t u32;
+} orc_stream;
+
+static inline void mulhilo(uint64_t a, uint64_t b, uint64_t *hi, uint64_t *lo) {
+  unsigned __int128 p = (unsigned __int128)a * b;
+  *lo = (uint64_t)p;
+  *hi = (uint64_t)(p >> 64);
+}
+
+/* One Philox4x64-10 block for counter value `block` (>= 1; the stream's
+ * first block has counter 1 because numpy increments before generating). */
+void orc_philox_block(uint64_t block, uint64_t k0, uint64_t k1, uint64_t out[4]) {
+  uint64_t c0 = block, c1 = 0, c2 = 0, c3 = 0;
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += PHILOX_W0; k1 += PHILOX_W1; }
+    uint64_t hi0, lo0, hi1, lo1;
+    mulhilo(PHILOX_M0, c0, &hi0, &lo0);
+    mulhilo(PHILOX_M1, c2, &hi1, &lo1);
+    uint64_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+void orc_init(orc_stream *s, uint64_t k0, uint64_t k1) {
+  memset(s, 0, sizeof(*s));
+  s->k0 = k0; s->k1 = k1; s->pos = 4;
+}
+
+uint64_t orc_next64(orc_stream *s) {
+  if (s->pos >= 4) {
+    s->ctr += 1;
+    orc_philox_block(s->ctr, s->k0, s->k1, s->buf);
+    s->pos = 0;
+  }
+  return s->buf[s->pos++];
+}
+
+uint32_t orc_next32(orc_stream *s) {
+  if (s->has32) { s->has32 = 0; return s->u32; }
+  uint64_t w = orc_next64(s);
+  s->has32 = 1;
+  s->u32 = (uint32_t)(w >> 32);
+  return (uint32_t)w;
+}
+
+double orc_next_double(orc_stream *s) {
+  return (double)(orc_next64(s) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+/* Words consumed so far (64-bit units), and the u32 cursor (32-bit units). */
+uint64_t orc_words_used(const orc_stream *s) { return s->ctr * 4 - (uint64_t)(4 - s->pos); }
+uint64_t orc_u32_used(const orc_stream *s) { return orc_words_used(s) * 2 - (s->has32 ? 1 : 0); }
+
+/* integers(lo, lo+ex) with 1 <= ex <= 2^32, int64 output. */
+int orc_integers(orc_stream *s, int64_t lo, uint64_t ex, int64_t n, int64_t *out) {
+  if (ex == 0 || ex > (1ULL << 32)) return -1;
+  if (ex == 1) { for (int64_t i = 0; i < n; ++i) out[i] = lo; return 0; }
+  if (ex == (1ULL << 32)) { for (int64_t i = 0; i < n; ++i) out[i] = lo + (int64_t)orc_next32(s); return 0; }
+  const uint32_t exc = (uint32_t)ex;
+  const uint32_t threshold = (uint32_t)((0x100000000ULL - ex) % ex);
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t m = (uint64_t)orc_next32(s) * exc;
+    uint32_t left = (uint32_t)m;
+    if (left < exc) {
+      while (left < threshold) {
+        m = (uint64_t)orc_next32(s) * exc;
+        left = (uint32_t)m;
+      }
+    }
+    out[i] = lo + (int64_t)(m >> 32);
+  }
+  return 0;
+}
+
+static inline double bits2d(uint64_t b) { double d; memcpy(&d, &b, 8); return d; }
+
+double orc_standard_normal(orc_stream *s) {
+  for (;;) {
+    uint64_t r = orc_next64(s);
+    int idx = (int)(r & 0xff);
+    r >>= 8;
+    int sign = (int)(r & 1);
+    uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = (double)rabs * bits2d(ZIG_WI_DOUBLE_BITS[idx]);
+    if (sign) x = -x;
+    if (rabs < ZIG_KI_DOUBLE_BITS[idx]) return x;
+    if (idx == 0) {
+      for (;;) {
+        double xx = -ZIG_NOR_INV_R * log1p(-orc_next_double(s));
+        double yy = -log1p(-orc_next_double(s));
+        if (yy + yy > xx * xx)
+          return ((rabs >> 8) & 1) ? -(ZIG_NOR_R + xx) : ZIG_NOR_R + xx;
+      }
+    } else {
+      double f0 = bits2d(ZIG_FI_DOUBLE_BITS[idx - 1]), f1 = bits2d(ZIG_FI_DOUBLE_BITS[idx]);
+      if ((f0 - f1) * orc_next_double(s) + f1 < exp(-0.5 * x * x)) return x;
+    }
+  }
+}
+
+void orc_normal(orc_stream *s, double loc, double scale, int64_t n, double *out) {
+  for (int64_t i = 0; i < n; ++i) {
+    double z = orc_standard_normal(s);
+    out[i] = loc + scale * z;  /* built with -ffp-contract=off: no FMA */
+  }
+}
+
+void orc_uniform(orc_stream *s, double lo, double hi, int64_t n, double *out) {
+  double range = hi - lo;
+  for (int64_t i = 0; i < n; ++i) {
+    out[i] = lo + range * orc_next_double(s);
+  }
+}
+
+/* poisson(lam) for 0 <= lam < 10 with enlam = exp(-lam) supplied by the
+ * caller (the host's libm, as numpy computes it). */
+int orc_poisson(orc_stream *s, double lam, double enlam, int64_t n, int64_t *out) {
+  if (!(lam >= 0.0) || lam >= 10.0) return -1;
+  if (lam == 0.0) { for (int64_t i = 0; i < n; ++i) out[i] = 0; return 0; }
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t x = 0;
+    double prod = 1.0;
+    for (;;) {
+      prod *= orc_next_double(s);
+      if (prod > enlam) x += 1; else break;
+    }
+    out[i] = x;
+  }
+  return 0;
+}
+
+/* Random access: words [w0, w0+n) of the stream keyed (k0, k1). */
+void orc_words(uint64_t k0, uint64_t k1, uint64_t w0, int64_t n, uint64_t *out) {
+  uint64_t blk[4];
+  uint64_t cur = ~0ULL;
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t w = w0 + (uint64_t)i;
+    if ((w >> 2) != cur) { cur = w >> 2; orc_philox_block(cur + 1, k0, k1, blk); }
+    out[i] = blk[w & 3];
+  }
+}
+
+/* Sizes/state access for the ctypes wrapper. */
+int orc_sizeof_stream(void) { return (int)sizeof(orc_stream); }

@@ -1,0 +1,35 @@
+// C-ABI plumbing: error strings and library identity.
+// Status codes (include/spikemesh_b200.h): 0 ok, -1 ValueError, -2
+// ConsistencyError, -3 CUDA error, -4 ProtocolError, -5 DelayRangeError --
+// the reference's exception classes (sm/core.py:39-52).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cuda_runtime.h>
+
+static thread_local char g_err[1024] = {0};
+
+extern "C" void smx_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" int smx_last_error(char* buf, size_t cap) {
+  if (!buf || cap == 0) return (int)strlen(g_err);
+  strncpy(buf, g_err, cap - 1);
+  buf[cap - 1] = 0;
+  return (int)strlen(buf);
+}
+
+extern "C" const char* smx_version(void) { return "spikemesh-b200 0.1.0 sm_100a"; }
+
+extern "C" int smx_stream_sync(void* stream) {
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    smx_set_error("stream sync: %s", cudaGetErrorString(e));
+    return -3;
+  }
+  return 0;
+}

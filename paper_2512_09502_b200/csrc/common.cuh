@@ -1,0 +1,233 @@
+// Shared device helpers for the spikemesh-b200 kernels (sm_100a).
+//
+// Random arithmetic restates numpy 2.3.5's Philox4x64-10 bit generator and
+// its consumers exactly (the reference draws every random number through
+// numpy.random.Generator(Philox), sm/core.py:119-141):
+//   word w of a stream      = Philox4x64_10(ctr = w/4 + 1, key)[w % 4]
+//   u32 position u          = low half of word u/2 if u even, else high half
+//   next_double(word)       = (word >> 11) * 2^-53
+//   integers(lo, lo+ex)     = 32-bit Lemire; a u32 draw v is accepted iff
+//                             (v*ex mod 2^32) >= (2^32-ex) % ex, value = v*ex >> 32
+// Floating-point arithmetic that must match numpy bit-for-bit is written
+// with explicit round-to-nearest intrinsics (no FMA contraction).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define SMX_PHILOX_M0 0xD2E7470EE14C6C93ULL
+#define SMX_PHILOX_M1 0xCA5A826395121157ULL
+#define SMX_PHILOX_W0 0x9E3779B97F4A7C15ULL
+#define SMX_PHILOX_W1 0xBB67AE8584CAA73BULL
+
+// Packed record payload: target row (24 bits) | syn class (8 bits).
+#define SMX_ROW_BITS 24
+#define SMX_ROW_MASK 0x00FFFFFFu
+// Pending-record keys with this bit set are temporary keys resolved through
+// the per-rank key LUT at sort time (remote-call records whose image ids are
+// assigned after generation).
+#define SMX_TMP_KEY 0x80000000u
+
+namespace smx {
+
+struct Key {
+  uint64_t k0, k1;
+};
+
+__device__ __forceinline__ void philox4x64_10(uint64_t block, Key key, uint64_t out[4]) {
+  uint64_t c0 = block, c1 = 0, c2 = 0, c3 = 0;
+  uint64_t k0 = key.k0, k1 = key.k1;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += SMX_PHILOX_W0; k1 += SMX_PHILOX_W1; }
+    const uint64_t hi0 = __umul64hi(SMX_PHILOX_M0, c0), lo0 = SMX_PHILOX_M0 * c0;
+    const uint64_t hi1 = __umul64hi(SMX_PHILOX_M1, c2), lo1 = SMX_PHILOX_M1 * c2;
+    const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+__device__ __forceinline__ uint64_t philox_word(Key key, uint64_t w) {
+  uint64_t b[4];
+  philox4x64_10((w >> 2) + 1, key, b);
+  return b[w & 3];
+}
+
+__device__ __forceinline__ double u53(uint64_t w) {
+  return __dmul_rn((double)(w >> 11), 1.0 / 9007199254740992.0);
+}
+
+struct Lemire {
+  uint32_t ex;         // range size, 2 <= ex <= 2^32-1; ex==0 encodes 2^32
+  uint32_t threshold;  // (2^32 - ex) % ex
+  __device__ __forceinline__ bool accept(uint32_t v, uint32_t& out) const {
+    if (ex == 0) { out = v; return true; }
+    const uint64_t m = (uint64_t)v * (uint64_t)ex;
+    out = (uint32_t)(m >> 32);
+    return (uint32_t)m >= threshold;
+  }
+};
+
+// A sequential stream cursor on the device (one thread), mirroring numpy's
+// Philox state: 64-bit word position plus the buffered high half.
+struct SeqStream {
+  Key key;
+  uint64_t word;   // next 64-bit word index
+  uint64_t buf[4];
+  uint64_t bufblk; // block index held in buf (0 = none)
+  __device__ __forceinline__ void init(Key k, uint64_t w) { key = k; word = w; bufblk = 0; }
+  __device__ __forceinline__ uint64_t next64() {
+    const uint64_t blk = (word >> 2) + 1;
+    if (blk != bufblk) { philox4x64_10(blk, key, buf); bufblk = blk; }
+    return buf[(word++) & 3];
+  }
+  __device__ __forceinline__ double next_double() { return u53(next64()); }
+};
+
+// ---------------------------------------------------------------------------
+// Ziggurat standard normal (numpy random_standard_normal), bit-exact on the
+// fast path (98.5% of first words).  The wedge / tail branches use CUDA's
+// exp / log1p, which are faithfully rounded (<= 1 ulp) like glibc's; a
+// decision could only differ when both sides of a comparison are within one
+// ulp of each other.
+// ---------------------------------------------------------------------------
+}  // namespace smx
+
+#include "ziggurat_tables.cuh"
+
+namespace smx {
+
+__device__ __forceinline__ double zig_standard_normal(SeqStream& s) {
+  for (;;) {
+    uint64_t r = s.next64();
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = __dmul_rn((double)rabs, __longlong_as_double((long long)ZIG_WI_DOUBLE_BITS[idx]));
+    if (sign) x = -x;
+    if (rabs < ZIG_KI_DOUBLE_BITS[idx]) return x;
+    if (idx == 0) {
+      for (;;) {
+        const double xx = __dmul_rn(-ZIG_NOR_INV_R, log1p(-s.next_double()));
+        const double yy = -log1p(-s.next_double());
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx))
+          return ((rabs >> 8) & 1) ? -__dadd_rn(ZIG_NOR_R, xx) : __dadd_rn(ZIG_NOR_R, xx);
+      }
+    } else {
+      const double f0 = __longlong_as_double((long long)ZIG_FI_DOUBLE_BITS[idx - 1]);
+      const double f1 = __longlong_as_double((long long)ZIG_FI_DOUBLE_BITS[idx]);
+      const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(f0, f1), s.next_double()), f1);
+      if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) return x;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// BLAKE2b-128 of a short message (< 128 bytes, one block), used to derive the
+// per-neuron ("init-v", gid) Philox keys on the device (sm/core.py:119-126).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t rotr64(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
+
+__device__ __constant__ uint64_t BLAKE2B_IV[8] = {
+    0x6a09e667f3bcc908ULL, 0xbb67ae8584caa73bULL, 0x3c6ef372fe94f82bULL, 0xa54ff53a5f1d36f1ULL,
+    0x510e527fade682d1ULL, 0x9b05688c2b3e6c1fULL, 0x1f83d9abfb41bd6bULL, 0x5be0cd19137e2179ULL};
+
+__device__ __constant__ uint8_t BLAKE2B_SIGMA[12][16] = {
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+    {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4},
+    {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13},
+    {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11},
+    {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5},
+    {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+    {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+
+// msg: little-endian message words (16 x u64, zero padded), len in bytes.
+__device__ inline Key blake2b_128(const uint64_t m[16], uint32_t len) {
+  uint64_t h[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) h[i] = BLAKE2B_IV[i];
+  h[0] ^= 0x01010000ULL ^ 16ULL;  // digest 16, key 0, fanout 1, depth 1
+  uint64_t v[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { v[i] = h[i]; v[i + 8] = BLAKE2B_IV[i]; }
+  v[12] ^= (uint64_t)len;
+  v[14] = ~v[14];  // final block
+#define SMX_G(a, b, c, d, x, y)            \
+  a = a + b + x; d = rotr64(d ^ a, 32);    \
+  c = c + d;     b = rotr64(b ^ c, 24);    \
+  a = a + b + y; d = rotr64(d ^ a, 16);    \
+  c = c + d;     b = rotr64(b ^ c, 63);
+  for (int r = 0; r < 12; ++r) {
+    const uint8_t* s = BLAKE2B_SIGMA[r];
+    SMX_G(v[0], v[4], v[8], v[12], m[s[0]], m[s[1]]);
+    SMX_G(v[1], v[5], v[9], v[13], m[s[2]], m[s[3]]);
+    SMX_G(v[2], v[6], v[10], v[14], m[s[4]], m[s[5]]);
+    SMX_G(v[3], v[7], v[11], v[15], m[s[6]], m[s[7]]);
+    SMX_G(v[0], v[5], v[10], v[15], m[s[8]], m[s[9]]);
+    SMX_G(v[1], v[6], v[11], v[12], m[s[10]], m[s[11]]);
+    SMX_G(v[2], v[7], v[8], v[13], m[s[12]], m[s[13]]);
+    SMX_G(v[3], v[4], v[9], v[14], m[s[14]], m[s[15]]);
+  }
+#undef SMX_G
+  Key k;
+  k.k0 = h[0] ^ v[0] ^ v[8];
+  k.k1 = h[1] ^ v[1] ^ v[9];
+  return k;
+}
+
+// Warp/block scan helpers -----------------------------------------------------
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// Exclusive block scan of one value per thread; returns exclusive prefix and
+// writes the block total.  `ws` needs blockDim.x/32 entries of scratch.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* ws, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t inc = warp_incl_scan(x);
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t t = lane < nw ? ws[lane] : 0;
+    t = warp_incl_scan(t);
+    if (lane < nw) ws[lane] = t;
+  }
+  __syncthreads();
+  total = ws[nw - 1];
+  const uint32_t base = warp ? ws[warp - 1] : 0;
+  __syncthreads();
+  return base + inc - x;
+}
+
+}  // namespace smx
+
+// Error reporting shared by every translation unit (defined in capi.cu).
+extern "C" void smx_set_error(const char* fmt, ...);
+#define SMX_CUDA_CHECK(expr)                                                       \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      smx_set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+      return -3;                                                                   \
+    }                                                                              \
+  } while (0)
+#define SMX_LAUNCH_CHECK()                                                         \
+  do {                                                                             \
+    cudaError_t _e = cudaGetLastError();                                           \
+    if (_e != cudaSuccess) {                                                       \
+      smx_set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e)); \
+      return -3;                                                                   \
+    }                                                                              \
+  } while (0)

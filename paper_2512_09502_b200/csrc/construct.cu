@@ -1,0 +1,502 @@
+// Construction kernels: connection-rule generation into the pending record
+// buffers, remote-source bitmaps and image assignment, the temporary-key LUT,
+// and the preparation-time compactions (R/L, S, H/I) and routing tables
+// (T/P, G/Q).
+//
+// Reference mapping (sm/construction.py):
+//   _realize_pairs / _draw_source_positions (391-432)  -> gen_draw / gen_pairs
+//   used_flags / extract_used (454-470)                -> mark_values
+//   lookup_or_create_images + RemoteSourceMap.insert   -> assign_images
+//     (473-486, 227-236): new images get ids M, M+1, ... in ascending order of
+//     the new source values, per (group, source rank), source ranks ascending
+//   remap_connection_sources (489-495)                 -> LUT resolved at sort
+//   mirror_merge / roster update (295-306, 620-636)    -> bits_or
+//   prepare: rosters, image_lookups, routes (710-807)  -> bits_compact,
+//     gather_lookup, build_routes
+//
+// Remote-source maps are stored densely per (group, source rank): img_of[v]
+// (int32, -1 = no image) over the source rank's node values plus a presence
+// bitmap; the sorted (R, L) pair of the reference is the compaction of that
+// bitmap.  Lookups are O(1) gathers instead of searchsorted.
+#include "draw_host.cuh"
+
+using namespace smx;
+
+namespace {
+
+constexpr int T256 = 256;
+
+inline unsigned nblk(uint64_t n, int t = T256) { return (unsigned)((n + t - 1) / t); }
+
+__device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t b) {
+  const uint32_t m = 1u << (b & 31);
+  uint32_t* w = bits + (b >> 5);
+  if (!(__ldcg(w) & m)) atomicOr(w, m);
+}
+
+// --- key / payload tables ----------------------------------------------------
+
+__global__ void pay_table_kernel(const int64_t* targets, uint64_t n, const int32_t* node2row,
+                                 uint64_t n_nodes, uint32_t cls, uint32_t* pay, int* bad) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t t = targets[i];
+  int32_t row = (t >= 0 && (uint64_t)t < n_nodes) ? node2row[t] : -1;
+  if (row < 0 || row > (int32_t)SMX_ROW_MASK) { atomicExch(bad, 1); row = 0; }
+  pay[i] = (uint32_t)row | (cls << SMX_ROW_BITS);
+}
+
+__global__ void key_table_kernel(const int64_t* sources, uint64_t n, uint32_t tmp_base, int tmp,
+                                 uint32_t* key) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  key[i] = tmp ? (SMX_TMP_KEY | (tmp_base + (uint32_t)i)) : (uint32_t)sources[i];
+}
+
+// Distributed fixed in-degree: flat population index f -> pending key and the
+// bit (global value key gv = vbase[rank] + node) to mark in the call's
+// used-value bitmap.  Local sources (rank == tgt_rank) get their node as the
+// key directly; they are marked too (their presence bumps the local counter).
+__global__ void dist_tables_kernel(const int32_t* src_rank, const int64_t* src_node, uint64_t total,
+                                   const uint32_t* vbase, int tgt_rank, uint32_t lut_base,
+                                   uint32_t* key, uint32_t* gv_out) {
+  const uint64_t f = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= total) return;
+  const int r = src_rank[f];
+  const uint32_t node = (uint32_t)src_node[f];
+  const uint32_t gv = vbase[r] + node;
+  key[f] = (r == tgt_rank) ? node : (SMX_TMP_KEY | (lut_base + gv));
+  gv_out[f] = gv;
+}
+
+// --- generation sinks ----------------------------------------------------------
+
+enum { K_NONE = 0, K_FROM_VALUE = 1, K_FROM_J = 2 };
+enum { P_NONE = 0, P_FROM_VALUE = 1, P_FROM_J = 2 };
+
+struct GenSink {
+  int key_mode, pay_mode;
+  const uint32_t* key_tab;
+  const uint32_t* pay_tab;
+  uint32_t kdiv;
+  uint32_t* keys;        // pre-offset to the call's first record
+  uint32_t* vals;
+  uint32_t* used_bits;   // optional
+  const uint32_t* used_tab;  // optional position -> bit (0xffffffff = skip)
+  __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const {
+    if (key_mode == K_FROM_VALUE) {
+      if (keys) keys[j] = key_tab[v];
+      if (used_bits) {
+        const uint32_t b = used_tab ? used_tab[v] : v;
+        if (b != 0xffffffffu) set_bit(used_bits, b);
+      }
+    } else if (key_mode == K_FROM_J) {
+      keys[j] = key_tab[j / kdiv];
+    }
+    if (pay_mode == P_FROM_J) vals[j] = pay_tab[j / kdiv];
+    else if (pay_mode == P_FROM_VALUE) vals[j] = pay_tab[v];
+  }
+};
+
+// Deterministic-use rules: one_to_one / assigned (mode 0: record i = (i, i)),
+// all_to_all (mode 1: record r = (r % n_src, r / n_src)).
+__global__ void pairs_kernel(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab,
+                             const uint32_t* pay_tab, uint32_t* keys, uint32_t* vals) {
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  uint64_t s = r, t = r;
+  if (mode == 1) { s = r % n_src; t = r / n_src; }
+  keys[r] = key_tab[s];
+  vals[r] = pay_tab[t];
+}
+
+// --- bitmaps and images ---------------------------------------------------------
+
+// vbits[sources[p]] = 1 for every position p whose bit is set in pos_bits
+// (pos_bits == null: every position).
+__global__ void mark_values_kernel(const uint32_t* pos_bits, const int64_t* sources, uint64_t n,
+                                   uint32_t* vbits) {
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  if (pos_bits && !((pos_bits[p >> 5] >> (p & 31)) & 1)) return;
+  set_bit(vbits, (uint32_t)sources[p]);
+}
+
+struct Segment {          // one (group, source rank) map inside a call
+  uint64_t word0;         // first word of the segment in the concatenated bitmap
+  uint64_t nwords;
+  uint32_t* present;      // the map's presence bitmap (nwords words)
+  int32_t* img_of;        // the map's dense value -> image array
+};
+
+__device__ __forceinline__ int find_seg(const Segment* segs, int ns, uint64_t w) {
+  int lo = 0, hi = ns - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].word0 <= w) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void new_counts_kernel(const uint32_t* vbits, uint64_t nwords, const Segment* segs, int ns,
+                                  uint32_t* cnt) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nwords) return;
+  const int s = find_seg(segs, ns, w);
+  const uint64_t lw = w - segs[s].word0;
+  if (!segs[s].img_of || lw >= segs[s].nwords) { cnt[w] = 0; return; }
+  cnt[w] = __popc(vbits[w] & ~segs[s].present[lw]);
+}
+
+__global__ void assign_kernel(const uint32_t* vbits, uint64_t nwords, const Segment* segs, int ns,
+                              const int64_t* excl, int64_t m0) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nwords) return;
+  const int s = find_seg(segs, ns, w);
+  const uint64_t lw = w - segs[s].word0;
+  if (!segs[s].img_of || lw >= segs[s].nwords) return;
+  uint32_t nb = vbits[w] & ~segs[s].present[lw];
+  if (!nb) return;
+  int64_t id = m0 + excl[w];
+  segs[s].present[lw] |= nb;
+  while (nb) {
+    const int b = __ffs(nb) - 1;
+    nb &= nb - 1;
+    segs[s].img_of[lw * 32 + b] = (int32_t)(id++);
+  }
+}
+
+__global__ void gather_lut_kernel(const int64_t* sources, uint64_t n, const int32_t* img_of,
+                                  uint32_t* lut) {
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  lut[p] = (uint32_t)img_of[sources[p]];
+}
+
+__global__ void bits_or_kernel(uint32_t* dst, const uint32_t* src, uint64_t nwords) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < nwords) {
+    const uint32_t x = src[w];
+    if (x) dst[w] |= x;
+  }
+}
+
+__global__ void popc_kernel(const uint32_t* bits, uint64_t nwords, uint32_t* cnt) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < nwords) cnt[w] = __popc(bits[w]);
+}
+
+// out[excl[w] + k] = value of the k-th set bit of word w (ascending).
+__global__ void compact_kernel(const uint32_t* bits, uint64_t nwords, const int64_t* excl, int64_t* out,
+                               const int32_t* img_of, int64_t* img_out) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nwords) return;
+  uint32_t x = bits[w];
+  int64_t o = excl[w];
+  while (x) {
+    const int b = __ffs(x) - 1;
+    x &= x - 1;
+    const int64_t v = (int64_t)(w * 32 + b);
+    out[o] = v;
+    if (img_out) img_out[o] = img_of ? (int64_t)img_of[v] : -1;
+    ++o;
+  }
+}
+
+// Routing tables of one source rank (T/P or G/Q).  For node s, every table
+// t (destination rank or group, ascending) whose bitmap holds s contributes
+// (dest[t], rank of s in that bitmap).  Tables are given as bitmaps plus
+// per-word exclusive prefix counts.
+struct RouteTable {
+  const uint32_t* bits;
+  const int64_t* excl;
+  uint64_t nwords;
+  int32_t dest;
+};
+
+__global__ void route_count_kernel(const RouteTable* tabs, int nt, uint64_t n_nodes, uint32_t* cnt) {
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_nodes) return;
+  uint32_t c = 0;
+  for (int t = 0; t < nt; ++t) {
+    const uint64_t w = s >> 5;
+    if (w < tabs[t].nwords && ((tabs[t].bits[w] >> (s & 31)) & 1)) ++c;
+  }
+  cnt[s] = c;
+}
+
+__global__ void route_fill_kernel(const RouteTable* tabs, int nt, uint64_t n_nodes, const int64_t* first,
+                                  int32_t* dest, uint32_t* pos) {
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_nodes) return;
+  int64_t o = first[s];
+  for (int t = 0; t < nt; ++t) {
+    const uint64_t w = s >> 5;
+    if (w >= tabs[t].nwords) continue;
+    const uint32_t x = tabs[t].bits[w];
+    if ((x >> (s & 31)) & 1) {
+      dest[o] = tabs[t].dest;
+      pos[o] = (uint32_t)(tabs[t].excl[w] + __popc(x & ((1u << (s & 31)) - 1)));
+      ++o;
+    }
+  }
+}
+
+// Wide-mode (per-record weight/delay) helpers.
+__global__ void fill_wide_const_kernel(double* w, uint32_t* meta, uint64_t n, double wv, uint32_t mv) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { w[i] = wv; meta[i] = mv; }
+}
+
+__global__ void promote_wide_kernel(const uint32_t* vals, uint64_t n, const double* cls_w,
+                                    const uint32_t* cls_meta, uint32_t* rows, double* w, uint32_t* meta) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t v = vals[i];
+  const uint32_t c = v >> SMX_ROW_BITS;
+  rows[i] = v & SMX_ROW_MASK;
+  w[i] = cls_w[c];
+  meta[i] = cls_meta[c];
+}
+
+__global__ void gather_wide_kernel(const uint32_t* idx, uint64_t n, const uint32_t* rows_in,
+                                   const double* w_in, const uint32_t* meta_in, uint32_t* rows,
+                                   double* w, uint32_t* meta) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t j = idx[i];
+  rows[i] = rows_in[j];
+  w[i] = w_in[j];
+  meta[i] = meta_in[j];
+}
+
+__global__ void max_meta_kernel(const uint32_t* meta, uint64_t n, uint32_t* max_delay, uint32_t* max_port) {
+  uint32_t md = 0, mp = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t m = meta[i];
+    md = max(md, m & 0xffffffu);
+    mp = max(mp, m >> 24);
+  }
+  for (int o = 16; o; o >>= 1) {
+    md = max(md, __shfl_xor_sync(0xffffffffu, md, o));
+    mp = max(mp, __shfl_xor_sync(0xffffffffu, mp, o));
+  }
+  if ((threadIdx.x & 31) == 0) { atomicMax(max_delay, md); atomicMax(max_port, mp); }
+}
+
+}  // namespace
+
+extern "C" int smx_counts_to_offsets(const uint32_t* counts, uint64_t n, int64_t* first_index, void* stream);
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+extern "C" int smx_pay_table(const int64_t* targets, uint64_t n, const int32_t* node2row, uint64_t n_nodes,
+                             uint32_t cls, uint32_t* pay_tab, void* stream) {
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* bad = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&bad, sizeof(int), st));
+  SMX_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  pay_table_kernel<<<nblk(n), T256, 0, st>>>(targets, n, node2row, n_nodes, cls, pay_tab, bad);
+  SMX_LAUNCH_CHECK();
+  int hbad = 0;
+  SMX_CUDA_CHECK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+  cudaFreeAsync(bad, st);
+  if (hbad) {
+    smx_set_error("connection targets must be real neurons of the target rank (image target or row >= 2^24)");
+    return -1;
+  }
+  return 0;
+}
+
+extern "C" int smx_key_table(const int64_t* sources, uint64_t n, uint32_t tmp_base, int tmp, uint32_t* key_tab,
+                             void* stream) {
+  if (n == 0) return 0;
+  key_table_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(sources, n, tmp_base, tmp, key_tab);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int smx_dist_tables(const int32_t* src_rank, const int64_t* src_node, uint64_t total,
+                               const uint32_t* vbase, int tgt_rank, uint32_t lut_base, uint32_t* key_tab,
+                               uint32_t* gv_tab, void* stream) {
+  if (total == 0) return 0;
+  dist_tables_kernel<<<nblk(total), T256, 0, (cudaStream_t)stream>>>(src_rank, src_node, total, vbase, tgt_rank,
+                                                                       lut_base, key_tab, gv_tab);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+// One numpy integers(0, ex, size=n) draw on stream (k0,k1) from u32 cursor u0,
+// routed into the pending record buffers by the rule's sink.
+extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, uint64_t n, int key_mode,
+                            int pay_mode, const uint32_t* key_tab, const uint32_t* pay_tab, uint32_t kdiv,
+                            uint32_t* keys, uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab,
+                            uint64_t* cursor_out, void* stream) {
+  GenSink s;
+  s.key_mode = key_mode;
+  s.pay_mode = pay_mode;
+  s.key_tab = key_tab;
+  s.pay_tab = pay_tab;
+  s.kdiv = kdiv ? kdiv : 1;
+  s.keys = keys;
+  s.vals = vals;
+  s.used_bits = used_bits;
+  s.used_tab = used_tab;
+  DrawResult res;
+  if (ex == 1) {  // numpy: a one-value range consumes nothing; every draw is 0
+    if (n) {
+      draw_const_kernel<GenSink><<<nblk(n), T256, 0, (cudaStream_t)stream>>>(n, s);
+      SMX_LAUNCH_CHECK();
+    }
+    *cursor_out = u0;
+    return 0;
+  }
+  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, (cudaStream_t)stream, &res);
+  *cursor_out = res.cursor;
+  return rc;
+}
+
+extern "C" int smx_gen_pairs(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab,
+                             const uint32_t* pay_tab, uint32_t* keys, uint32_t* vals, void* stream) {
+  if (n == 0) return 0;
+  pairs_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(mode, n, n_src, key_tab, pay_tab, keys, vals);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int smx_mark_values(const uint32_t* pos_bits, const int64_t* sources, uint64_t n, uint32_t* vbits,
+                               void* stream) {
+  if (n == 0) return 0;
+  mark_values_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(pos_bits, sources, n, vbits);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+// Assign image ids m0, m0+1, ... to the values set in vbits (a concatenation
+// of segments, one per (group, source rank) map, in ascending source-rank
+// order) that are not yet present in their map.  Returns the number of new
+// images in *n_new (host).
+extern "C" int smx_assign_images(const uint32_t* vbits, uint64_t nwords, const void* segs_host, int ns,
+                                 int64_t m0, int64_t* n_new, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  *n_new = 0;
+  if (nwords == 0 || ns == 0) return 0;
+  Segment* segs = nullptr;
+  uint32_t* cnt = nullptr;
+  int64_t* excl = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&segs, sizeof(Segment) * ns, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&cnt, sizeof(uint32_t) * nwords, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&excl, sizeof(int64_t) * (nwords + 1), st));
+  SMX_CUDA_CHECK(cudaMemcpyAsync(segs, segs_host, sizeof(Segment) * ns, cudaMemcpyHostToDevice, st));
+  new_counts_kernel<<<nblk(nwords), T256, 0, st>>>(vbits, nwords, segs, ns, cnt);
+  SMX_LAUNCH_CHECK();
+  if (int rc = smx_counts_to_offsets(cnt, nwords, excl, st)) return rc;
+  assign_kernel<<<nblk(nwords), T256, 0, st>>>(vbits, nwords, segs, ns, excl, m0);
+  SMX_LAUNCH_CHECK();
+  SMX_CUDA_CHECK(cudaMemcpyAsync(n_new, excl + nwords, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+  cudaFreeAsync(segs, st);
+  cudaFreeAsync(cnt, st);
+  cudaFreeAsync(excl, st);
+  return 0;
+}
+
+extern "C" int smx_gather_lut(const int64_t* sources, uint64_t n, const int32_t* img_of, uint32_t* lut,
+                              void* stream) {
+  if (n == 0) return 0;
+  gather_lut_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(sources, n, img_of, lut);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int smx_bits_or(uint32_t* dst, const uint32_t* src, uint64_t nwords, void* stream) {
+  if (nwords == 0) return 0;
+  bits_or_kernel<<<nblk(nwords), T256, 0, (cudaStream_t)stream>>>(dst, src, nwords);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+// Per-word exclusive popcount prefix of a bitmap (nwords + 1 entries).
+extern "C" int smx_bits_prefix(const uint32_t* bits, uint64_t nwords, int64_t* excl, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* cnt = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&cnt, sizeof(uint32_t) * (nwords ? nwords : 1), st));
+  if (nwords) {
+    popc_kernel<<<nblk(nwords), T256, 0, st>>>(bits, nwords, cnt);
+    SMX_LAUNCH_CHECK();
+  }
+  if (int rc = smx_counts_to_offsets(cnt, nwords, excl, st)) return rc;
+  cudaFreeAsync(cnt, st);
+  return 0;
+}
+
+// Ascending values of the set bits (needs the prefix from smx_bits_prefix);
+// optionally the image of each value (img_of null -> -1).
+extern "C" int smx_bits_compact(const uint32_t* bits, uint64_t nwords, const int64_t* excl, int64_t* out,
+                                const int32_t* img_of, int64_t* img_out, void* stream) {
+  if (nwords == 0) return 0;
+  compact_kernel<<<nblk(nwords), T256, 0, (cudaStream_t)stream>>>(bits, nwords, excl, out, img_of, img_out);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+// Build one source rank's routing CSR over nodes [0, n_nodes): first[n+1],
+// dest[], pos[] (capacity from a first call with dest == null: returns the
+// total entries in *n_entries).
+extern "C" int smx_build_routes(const void* tabs_host, int nt, uint64_t n_nodes, uint32_t* cnt_scratch,
+                                int64_t* first, int32_t* dest, uint32_t* pos, int64_t* n_entries, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  *n_entries = 0;
+  RouteTable* tabs = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&tabs, sizeof(RouteTable) * (nt ? nt : 1), st));
+  if (nt) SMX_CUDA_CHECK(cudaMemcpyAsync(tabs, tabs_host, sizeof(RouteTable) * nt, cudaMemcpyHostToDevice, st));
+  if (n_nodes) {
+    route_count_kernel<<<nblk(n_nodes), T256, 0, st>>>(tabs, nt, n_nodes, cnt_scratch);
+    SMX_LAUNCH_CHECK();
+  }
+  if (int rc = smx_counts_to_offsets(cnt_scratch, n_nodes, first, st)) return rc;
+  SMX_CUDA_CHECK(cudaMemcpyAsync(n_entries, first + n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (dest && n_nodes) {
+    route_fill_kernel<<<nblk(n_nodes), T256, 0, st>>>(tabs, nt, n_nodes, first, dest, pos);
+    SMX_LAUNCH_CHECK();
+  }
+  cudaFreeAsync(tabs, st);
+  return 0;
+}
+
+extern "C" int smx_fill_wide_const(double* w, uint32_t* meta, uint64_t n, double wv, uint32_t mv, void* stream) {
+  if (n == 0) return 0;
+  fill_wide_const_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(w, meta, n, wv, mv);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int smx_promote_wide(const uint32_t* vals, uint64_t n, const double* cls_w, const uint32_t* cls_meta,
+                                uint32_t* rows, double* w, uint32_t* meta, void* stream) {
+  if (n == 0) return 0;
+  promote_wide_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(vals, n, cls_w, cls_meta, rows, w, meta);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int smx_gather_wide(const uint32_t* idx, uint64_t n, const uint32_t* rows_in, const double* w_in,
+                               const uint32_t* meta_in, uint32_t* rows, double* w, uint32_t* meta, void* stream) {
+  if (n == 0) return 0;
+  gather_wide_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(idx, n, rows_in, w_in, meta_in, rows, w, meta);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out2, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  SMX_CUDA_CHECK(cudaMemsetAsync(out2, 0, 8, st));
+  if (n == 0) return 0;
+  max_meta_kernel<<<148 * 4, T256, 0, st>>>(meta, n, out2, out2 + 1);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}

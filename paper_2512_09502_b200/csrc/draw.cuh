@@ -1,0 +1,127 @@
+// Ordered Lemire draw engine: numpy `Generator.integers(lo, lo+ex, size=n)`
+// on a Philox stream starting at an arbitrary u32 cursor, parallelised as
+// "accept-mask + ordered compaction" (every raw u32 draw, first try or retry,
+// is accepted by the same predicate, so the n-th accepted raw u32 is the
+// n-th output value; verified against numpy in tests/test_oracle_rng.py).
+//
+// Two launches per draw call:
+//   count:  CTA c counts accepts over its raw range (compute only)
+//   write:  CTA c regenerates its range, ranks accepts with a block scan,
+//           and hands (output index, value) to a Sink functor.
+// A tiny single-CTA scan between them turns per-CTA counts into offsets.
+#pragma once
+#include "common.cuh"
+
+namespace smx {
+
+constexpr int DRAW_THREADS = 256;
+
+struct DrawRange {
+  Key key;
+  uint64_t u0;       // first raw u32 position
+  uint64_t n_raw;    // raw positions covered by the launch
+  uint64_t per_cta;  // raw positions per CTA
+  Lemire lm;
+};
+
+// Accept mask and values for the 8 u32 draws of Philox block `blk`,
+// restricted to raw positions in [lo, hi).
+__device__ __forceinline__ uint32_t block_accepts(const DrawRange& r, uint64_t blk, uint64_t lo,
+                                                  uint64_t hi, uint32_t vals[8]) {
+  uint64_t w[4];
+  philox4x64_10(blk, r.key, w);
+  const uint64_t p0 = (blk - 1) * 8;
+  uint32_t mask = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t v = (i & 1) ? (uint32_t)(w[i >> 1] >> 32) : (uint32_t)w[i >> 1];
+    const uint64_t p = p0 + i;
+    uint32_t out;
+    const bool ok = r.lm.accept(v, out);
+    vals[i] = out;
+    if (ok && p >= lo && p < hi) mask |= 1u << i;
+  }
+  return mask;
+}
+
+static __global__ void draw_count_kernel(DrawRange r, uint32_t* cta_counts) {
+  const uint64_t lo = r.u0 + (uint64_t)blockIdx.x * r.per_cta;
+  const uint64_t end = r.u0 + r.n_raw;
+  const uint64_t hi = lo + r.per_cta < end ? lo + r.per_cta : end;
+  uint32_t cnt = 0;
+  if (lo < hi) {
+    const uint64_t b0 = lo / 8 + 1, b1 = (hi - 1) / 8 + 1;
+    for (uint64_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x) {
+      uint32_t v[8];
+      cnt += __popc(block_accepts(r, b, lo, hi, v));
+    }
+  }
+  __shared__ uint32_t ws[DRAW_THREADS / 32];
+  uint32_t tot;
+  block_excl_scan(cnt, ws, tot);
+  if (threadIdx.x == 0) cta_counts[blockIdx.x] = tot;
+}
+
+// Exclusive scan of per-CTA counts (n <= a few thousand) into 64-bit offsets;
+// offsets[n] = total.
+static __global__ void cta_offsets_kernel(const uint32_t* counts, int n, uint64_t* offsets) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const uint32_t x = i < n ? counts[i] : 0;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(x, ws, tot);
+    if (i < n) offsets[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) offsets[n] = carry;
+}
+
+// Sink contract: `void operator()(uint64_t j, uint32_t value)` for j < n_out,
+// and `void cursor(uint64_t u32_after)` from the thread that emits j = n_out-1.
+template <class Sink>
+__global__ void draw_write_kernel(DrawRange r, const uint64_t* cta_offsets, uint64_t n_out,
+                                  Sink sink, uint64_t* cursor_out) {
+  const uint64_t lo = r.u0 + (uint64_t)blockIdx.x * r.per_cta;
+  const uint64_t end = r.u0 + r.n_raw;
+  const uint64_t hi = lo + r.per_cta < end ? lo + r.per_cta : end;
+  if (lo >= hi) return;
+  uint64_t base = cta_offsets[blockIdx.x];
+  if (base >= n_out) return;
+  __shared__ uint32_t ws[DRAW_THREADS / 32];
+  const uint64_t b0 = lo / 8 + 1, b1 = (hi - 1) / 8 + 1;
+  for (uint64_t bb = b0; bb <= b1; bb += blockDim.x) {
+    const uint64_t b = bb + threadIdx.x;
+    uint32_t v[8];
+    uint32_t mask = 0;
+    if (b <= b1) mask = block_accepts(r, b, lo, hi, v);
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(__popc(mask), ws, tot);
+    uint64_t j = base + ex;
+    while (mask) {
+      const int i = __ffs(mask) - 1;
+      mask &= mask - 1;
+      if (j < n_out) {
+        sink(j, v[i]);
+        if (j == n_out - 1 && cursor_out) *cursor_out = (b - 1) * 8 + i + 1;
+      }
+      ++j;
+    }
+    base += tot;
+    if (base >= n_out) break;
+  }
+}
+
+// A one-value range (ex == 1) consumes no draws: every value is 0.
+template <class Sink>
+__global__ void draw_const_kernel(uint64_t n_out, Sink sink) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n_out) sink(j, 0u);
+}
+
+}  // namespace smx

@@ -1,0 +1,71 @@
+// Host driver for the ordered Lemire draw engine (draw.cuh).
+#pragma once
+#include <cmath>
+#include "draw.cuh"
+
+namespace smx {
+
+struct DrawResult {
+  uint64_t cursor;  // u32 cursor after the last consumed draw
+};
+
+// numpy integers(lo, lo+ex, size=n) on stream `key` from u32 cursor u0.
+// Hands every (index, value-lo) to `sink`; returns 0 or a negative status.
+template <class Sink>
+int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink,
+             cudaStream_t st, DrawResult* res) {
+  res->cursor = u0;
+  if (n_out == 0) return 0;
+  if (ex == 1) {  // numpy: range of one value consumes nothing
+    smx_set_error("run_draw: ex == 1 must be handled by the caller");
+    return -1;
+  }
+  if (ex < 1 || ex > (1ULL << 32)) {
+    smx_set_error("integer range %llu outside [2, 2^32]", (unsigned long long)ex);
+    return -1;
+  }
+  DrawRange r;
+  r.key = key;
+  r.u0 = u0;
+  r.lm.ex = (uint32_t)(ex & 0xffffffffULL);
+  r.lm.threshold = ex == (1ULL << 32) ? 0u : (uint32_t)(((1ULL << 32) - ex) % ex);
+  const double prej = (double)r.lm.threshold / 4294967296.0;
+  uint64_t n_raw = n_out + (uint64_t)std::ceil(n_out * prej * 1.25 + 12.0 * std::sqrt(n_out * prej + 1.0) + 64.0);
+  uint32_t* counts = nullptr;
+  uint64_t* offs = nullptr;
+  uint64_t* cur_d = nullptr;
+  int rc = 0;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    int G = (int)std::min<uint64_t>((n_raw + 16383) / 16384, 148 * 8);
+    if (G < 1) G = 1;
+    r.n_raw = n_raw;
+    r.per_cta = ((n_raw + G - 1) / G + 7) / 8 * 8;
+    SMX_CUDA_CHECK(cudaMallocAsync((void**)&counts, sizeof(uint32_t) * G, st));
+    SMX_CUDA_CHECK(cudaMallocAsync((void**)&offs, sizeof(uint64_t) * (G + 1), st));
+    SMX_CUDA_CHECK(cudaMallocAsync((void**)&cur_d, sizeof(uint64_t), st));
+    draw_count_kernel<<<G, DRAW_THREADS, 0, st>>>(r, counts);
+    cta_offsets_kernel<<<1, 1024, 0, st>>>(counts, G, offs);
+    SMX_LAUNCH_CHECK();
+    uint64_t total = 0;
+    SMX_CUDA_CHECK(cudaMemcpyAsync(&total, offs + G, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (total >= n_out) {
+      draw_write_kernel<Sink><<<G, DRAW_THREADS, 0, st>>>(r, offs, n_out, sink, cur_d);
+      SMX_LAUNCH_CHECK();
+      SMX_CUDA_CHECK(cudaMemcpyAsync(&res->cursor, cur_d, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+      rc = 0;
+    } else {
+      rc = 1;
+    }
+    cudaFreeAsync(counts, st);
+    cudaFreeAsync(offs, st);
+    cudaFreeAsync(cur_d, st);
+    if (rc == 0) return 0;
+    n_raw = n_raw + n_raw / 2 + 1024;
+  }
+  smx_set_error("run_draw: could not cover %llu accepted draws", (unsigned long long)n_out);
+  return -3;
+}
+
+}  // namespace smx

@@ -1,0 +1,269 @@
+// numpy-exact Poisson drive: Generator.poisson(lam, size=n) for lam < 10 on a
+// Philox stream whose word cursor carries across calls (PoissonSource draws
+// one count per target per step from one stream, sm/dynamics.py:232-248).
+//
+// numpy's multiplication method (random_poisson_mult) consumes X+1 words per
+// sample: prod *= next_double until prod <= exp(-lam).  The word where a
+// sample starts therefore depends on every earlier sample.  Parallel form:
+//   chunk kernel    per chunk of C words: U and len(w) (= X+1 for a sample
+//                   starting at word w) for every word; the orbit of starts
+//                   from entry offset 0 (bitmap S0); and for each entry
+//                   offset e < E the (exit offset, sample count) -- chains
+//                   from different entries merge with S0 after a few samples,
+//                   so each is a short walk.
+//   compose kernels sequential composition of the per-chunk entry->exit maps
+//                   in groups of 64 chunks, then across groups (one thread),
+//                   then back into each chunk: true entry and first sample
+//                   index of every chunk.
+//   emit kernel     walks from the true entry to the merge point, then ranks
+//                   the S0 starts in parallel: count[k] = len(start_k) - 1.
+// Exact for every input: no speculation is assumed beyond E (a sample longer
+// than E-1 words raises the error flag instead of being mis-composed).
+#include "common.cuh"
+
+namespace {
+
+constexpr int PC = 2048;          // words per chunk
+constexpr int PE = 64;            // entry offsets tracked per chunk
+constexpr int PG = 64;            // chunks per composition group
+constexpr int P_THREADS = 128;
+
+struct PoisJob {
+  smx::Key key;
+  const uint64_t* w0_dev;  // word cursor before the batch (device)
+  double enlam;       // exp(-lam), computed by the host's libm like numpy
+  uint64_t n;         // samples wanted
+  int n_chunks;
+  uint8_t* len;       // [n_chunks * PC]
+  uint32_t* s0;       // [n_chunks * PC/32]
+  uint8_t* ex;        // [n_chunks * PE] exit offsets
+  uint16_t* cnt;      // [n_chunks * PE] samples started inside the chunk
+  uint8_t* gex;       // [n_groups * PE]
+  uint32_t* gcnt;     // [n_groups * PE]
+  uint8_t* entry;     // [n_chunks]
+  uint64_t* kbase;    // [n_chunks]
+  uint8_t* out;       // counts[n]
+  uint64_t* cursor;   // word after the n-th sample
+  int* err;
+};
+
+__global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
+  __shared__ double U[PC + PE];
+  __shared__ uint8_t L[PC + PE];
+  __shared__ uint32_t S0[PC / 32];
+  __shared__ uint32_t cnt0_pos[PC / 32 + 1];  // S0 popcount prefix per word
+  __shared__ int exit0, count0;
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const uint64_t cw = (*J.w0_dev & ~3ULL) + (uint64_t)c * PC;
+  // U for words [cw, cw + PC + PE)
+  for (int q = tid; q < (PC + PE) / 4; q += P_THREADS) {
+    uint64_t b[4];
+    smx::philox4x64_10(((cw >> 2) + q) + 1, J.key, b);  // cw is a multiple of 4
+#pragma unroll
+    for (int i = 0; i < 4; ++i) U[4 * q + i] = smx::u53(b[i]);
+  }
+  for (int q = tid; q < PC / 32; q += P_THREADS) S0[q] = 0;
+  __syncthreads();
+  // len(w) for w in [0, PC + PE): products forward; words past the window
+  // tail are regenerated one at a time (rare).
+  for (int w = tid; w < PC + PE; w += P_THREADS) {
+    double prod = 1.0;
+    int k = 0;
+    for (;;) {
+      const int idx = w + k;
+      double u;
+      if (idx < PC + PE) {
+        u = U[idx];
+      } else {
+        u = smx::u53(smx::philox_word(J.key, cw + idx));
+      }
+      prod = __dmul_rn(prod, u);
+      ++k;
+      if (!(prod > J.enlam)) break;
+      if (k >= 255) break;
+    }
+    if (k >= PE) atomicExch(J.err, 11);
+    L[w] = (uint8_t)k;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int p = 0, n0 = 0;
+    while (p < PC) {
+      S0[p >> 5] |= 1u << (p & 31);
+      ++n0;
+      p += L[p];
+    }
+    exit0 = p - PC;
+    count0 = n0;
+    int acc = 0;
+    for (int q = 0; q < PC / 32; ++q) { cnt0_pos[q] = acc; acc += __popc(S0[q]); }
+    cnt0_pos[PC / 32] = acc;
+  }
+  __syncthreads();
+  // per entry offset: walk until merging with S0 or leaving the chunk
+  for (int e = tid; e < PE; e += P_THREADS) {
+    int p = e, pre = 0;
+    int ex_ = -1, ct = 0;
+    while (p < PC) {
+      if ((S0[p >> 5] >> (p & 31)) & 1) {  // merged at start p
+        const int rank = cnt0_pos[p >> 5] + __popc(S0[p >> 5] & ((1u << (p & 31)) - 1));
+        ex_ = exit0;
+        ct = pre + (count0 - rank);
+        break;
+      }
+      ++pre;
+      p += L[p];
+    }
+    if (ex_ < 0) { ex_ = p - PC; ct = pre; }
+    if (ex_ >= PE) { atomicExch(J.err, 12); ex_ = PE - 1; }
+    J.ex[(size_t)c * PE + e] = (uint8_t)ex_;
+    J.cnt[(size_t)c * PE + e] = (uint16_t)ct;
+  }
+  for (int w = tid; w < PC; w += P_THREADS) J.len[(size_t)c * PC + w] = L[w];
+  for (int q = tid; q < PC / 32; q += P_THREADS) J.s0[(size_t)c * (PC / 32) + q] = S0[q];
+}
+
+__global__ void group_kernel(PoisJob J) {
+  const int g = blockIdx.x, e0 = threadIdx.x;
+  if (e0 >= PE) return;
+  int e = e0;
+  uint32_t tot = 0;
+  const int c0 = g * PG, c1 = min(J.n_chunks, c0 + PG);
+  for (int c = c0; c < c1; ++c) {
+    tot += J.cnt[(size_t)c * PE + e];
+    e = J.ex[(size_t)c * PE + e];
+  }
+  J.gex[(size_t)g * PE + e0] = (uint8_t)e;
+  J.gcnt[(size_t)g * PE + e0] = tot;
+}
+
+__global__ void across_kernel(PoisJob J, int n_groups, uint8_t* gentry, uint64_t* gbase) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int e = (int)(*J.w0_dev & 3);
+  uint64_t k = 0;
+  for (int g = 0; g < n_groups; ++g) {
+    gentry[g] = (uint8_t)e;
+    gbase[g] = k;
+    k += J.gcnt[(size_t)g * PE + e];
+    e = J.gex[(size_t)g * PE + e];
+  }
+  if (k < J.n) atomicExch(J.err, 13);  // window too small
+}
+
+__global__ void within_kernel(PoisJob J, const uint8_t* gentry, const uint64_t* gbase) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g * PG >= J.n_chunks) return;
+  int e = gentry[g];
+  uint64_t k = gbase[g];
+  const int c0 = g * PG, c1 = min(J.n_chunks, c0 + PG);
+  for (int c = c0; c < c1; ++c) {
+    J.entry[c] = (uint8_t)e;
+    J.kbase[c] = k;
+    k += J.cnt[(size_t)c * PE + e];
+    e = J.ex[(size_t)c * PE + e];
+  }
+}
+
+__device__ __forceinline__ void emit(const PoisJob& J, uint64_t k, int c, int p, int len) {
+  if (k < J.n) {
+    J.out[k] = (uint8_t)(len - 1);
+    if (k == J.n - 1) *J.cursor = (*J.w0_dev & ~3ULL) + (uint64_t)c * PC + p + len;
+  }
+}
+
+__global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
+  __shared__ uint32_t ws[32];
+  __shared__ int merge_p, pre_n;
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const uint64_t kb = J.kbase[c];
+  if (kb >= J.n) return;
+  const uint8_t* L = J.len + (size_t)c * PC;
+  const uint32_t* S0 = J.s0 + (size_t)c * (PC / 32);
+  if (tid == 0) {
+    int p = J.entry[c], pre = 0;
+    while (p < PC && !((S0[p >> 5] >> (p & 31)) & 1)) {
+      emit(J, kb + pre, c, p, L[p]);
+      ++pre;
+      p += L[p];
+    }
+    merge_p = p;
+    pre_n = pre;
+  }
+  __syncthreads();
+  const int m = merge_p;
+  if (m >= PC) return;
+  // S0 starts >= m, ranked in order
+  for (int q0 = 0; q0 < PC / 32; q0 += P_THREADS) {
+    const int q = q0 + tid;
+    uint32_t bits = 0;
+    if (q < PC / 32) {
+      bits = S0[q];
+      const int lo = q * 32;
+      if (m > lo) bits &= (m - lo >= 32) ? 0u : ~((1u << (m - lo)) - 1);
+    }
+    uint32_t tot;
+    const uint32_t ex = smx::block_excl_scan(__popc(bits), ws, tot);
+    // carry across iterations of q0: PC/32 = 64 words <= P_THREADS, one pass
+    uint64_t k = kb + pre_n + ex;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int p = q * 32 + b;
+      emit(J, k, c, p, L[p]);
+      ++k;
+    }
+  }
+}
+
+}  // namespace
+
+// Workspace sizes for a window of n_chunks chunks (bytes).
+extern "C" uint64_t smx_poisson_workspace(int n_chunks) {
+  const int ng = (n_chunks + PG - 1) / PG;
+  return (uint64_t)n_chunks * PC + (uint64_t)n_chunks * (PC / 32) * 4 + (uint64_t)n_chunks * PE * 3 +
+         (uint64_t)ng * PE * 5 + (uint64_t)n_chunks * 9 + (uint64_t)ng * 9 + 256;
+}
+
+extern "C" int smx_poisson_chunks_for(uint64_t n, double lam) {
+  const double words = (double)n * (1.0 + lam) + 10.0 * sqrt((double)n * (lam + 1.0)) + 2.0 * PC + PE;
+  return (int)((words + PC - 1) / PC);
+}
+
+// counts[0..n) = numpy poisson(lam) samples drawn from the word cursor
+// *cursor_in of stream (k0, k1); *cursor_out (a different word) receives the
+// cursor after the last sample.  No host synchronisation.  `ws` is a device
+// workspace of smx_poisson_workspace(n_chunks) bytes.
+extern "C" int smx_poisson_counts(uint64_t k0, uint64_t k1, const uint64_t* cursor_in, double enlam, uint64_t n,
+                                  int n_chunks, void* ws, uint8_t* counts, uint64_t* cursor_out, int* err,
+                                  void* stream) {
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  PoisJob J;
+  J.key = smx::Key{k0, k1};
+  J.w0_dev = cursor_in;
+  J.enlam = enlam;
+  J.n = n;
+  J.n_chunks = n_chunks;
+  const int ng = (n_chunks + PG - 1) / PG;
+  uint8_t* p = (uint8_t*)ws;
+  J.len = p; p += (size_t)n_chunks * PC;
+  J.s0 = (uint32_t*)p; p += (size_t)n_chunks * (PC / 32) * 4;
+  J.cnt = (uint16_t*)p; p += (size_t)n_chunks * PE * 2;
+  J.gcnt = (uint32_t*)p; p += (size_t)ng * PE * 4;
+  J.kbase = (uint64_t*)p; p += (size_t)n_chunks * 8;
+  uint64_t* gbase = (uint64_t*)p; p += (size_t)ng * 8;
+  J.ex = p; p += (size_t)n_chunks * PE;
+  J.gex = p; p += (size_t)ng * PE;
+  J.entry = p; p += (size_t)n_chunks;
+  uint8_t* gentry = p; p += (size_t)ng;
+  J.out = counts;
+  J.cursor = cursor_out;
+  J.err = err;
+  chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  group_kernel<<<ng, PE, 0, st>>>(J);
+  across_kernel<<<1, 32, 0, st>>>(J, ng, gentry, gbase);
+  within_kernel<<<(ng + 127) / 128, 128, 0, st>>>(J, gentry, gbase);
+  emit_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}

@@ -1,0 +1,399 @@
+// Propagation kernels: one simulation step of one rank (sm/engine.py:277-310).
+//
+//   lif_kernel          consume_inputs + lif_step (sm/dynamics.py:191-204,
+//                       kernels/_speedups.pyx:13-35): read and zero the ring
+//                       slot now%L of every real row (summed over ports), add
+//                       i_e, advance V with the exact propagator in fp64
+//                       without FMA, and ballot the spikes into a bitmap.
+//   poisson_emit_kernel PoissonSource.emit_into (sm/dynamics.py:235-248) from
+//                       precomputed numpy-exact counts (poisson.cu).
+//   spikes_kernel       flatnonzero + SpikeRecorder.append + route_point_spikes /
+//                       route_group_spikes (sm/engine.py:89-128): ordered spike
+//                       list, raster append, per-destination packets, and the
+//                       local delivery source list.
+//   unpack_kernel       deliver_point_packets / deliver_gather_packets
+//                       (sm/engine.py:146-190): packet positions -> image nodes
+//                       via L (p2p) or I (collective, -1 dropped).
+//   plan / deliver      deliver_spikes (kernels/_speedups.pyx:38-54): every
+//                       (source node, emission step) expands its CSR range of
+//                       records into atomicAdd(ring[(t+d)%L][port][row], w*m).
+//
+// Ring layout is slot-major [L][P][N_real] fp64, real rows only.  fp64 adds
+// are exact for the dyadic weights of the reference models, so atomic order
+// does not change any bit; for non-dyadic weights V stays within the stated
+// tolerance.
+#include "common.cuh"
+
+namespace {
+
+constexpr int T256 = 256;
+inline unsigned nblk(uint64_t n, int t = T256) { return (unsigned)((n + t - 1) / t); }
+
+struct LifState {
+  double* v;
+  int32_t* ref;
+  const double* decay;
+  const double* v_rest;
+  const double* v_reset;
+  const double* v_th;
+  const int32_t* ref_steps;
+  const double* i_e;
+};
+
+__global__ void lif_kernel(LifState s, uint32_t n, double* ring, int n_ports, int L, int64_t now,
+                           uint32_t* spike_bits) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool spk = false;
+  if (i < n) {
+    const int slot = (int)(now % L);
+    double* base = ring + (size_t)slot * n_ports * n;
+    double in = base[i];
+    base[i] = 0.0;
+    for (int p = 1; p < n_ports; ++p) {
+      in = __dadd_rn(in, base[(size_t)p * n + i]);
+      base[(size_t)p * n + i] = 0.0;
+    }
+    in = __dadd_rn(in, s.i_e[i]);
+    const int32_t r = s.ref[i];
+    if (r > 0) {
+      s.ref[i] = r - 1;
+      s.v[i] = s.v_reset[i];
+    } else {
+      const double vr = s.v_rest[i];
+      const double integ = __dadd_rn(__dadd_rn(vr, __dmul_rn(__dsub_rn(s.v[i], vr), s.decay[i])), in);
+      if (integ >= s.v_th[i]) {
+        spk = true;
+        s.v[i] = s.v_reset[i];
+        s.ref[i] = s.ref_steps[i];
+      } else {
+        s.v[i] = integ;
+      }
+    }
+  }
+  const uint32_t b = __ballot_sync(0xffffffffu, spk);
+  if ((threadIdx.x & 31) == 0 && (i >> 5) < (n + 31) / 32) spike_bits[i >> 5] = b;
+}
+
+__global__ void poisson_emit_kernel(const uint8_t* counts, uint32_t n_t, const uint32_t* rows, double w,
+                                    double* ring_slot_port) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_t) return;
+  const uint32_t c = counts[t];
+  if (c) atomicAdd(ring_slot_port + rows[t], __dmul_rn(w, (double)c));
+}
+
+struct Routes {             // one routing family (p2p T/P or collective G/Q)
+  const int64_t* first;     // [M+1]
+  const int32_t* dest;      // destination rank (p2p) or group slot (collective)
+  const uint32_t* pos;      // map / roster position
+  int n_dest;               // number of packet buffers
+  uint32_t* packets;        // [n_dest][cap] (position, step) pairs
+  uint32_t* counts;         // [n_dest]
+  uint32_t cap;
+};
+
+struct SpikeOut {
+  const uint32_t* spike_bits;
+  uint32_t n_rows;
+  const uint32_t* row2node;
+  const int64_t* gid;       // per row
+  int64_t now;
+  // local delivery source list (node, step)
+  uint32_t* src_nodes;
+  uint32_t* src_steps;
+  uint32_t* n_src;          // device counter (appended to)
+  uint32_t src_cap;
+  // raster
+  int record;
+  int64_t* rec;             // (step, gid) pairs
+  uint64_t* n_rec;
+  uint64_t rec_cap;
+  uint32_t* spike_count;    // per-step total (optional accumulation)
+  int* overflow;
+};
+
+// Single CTA: ordered compaction of the spike bitmap, raster append, local
+// delivery list, and packets for both routing families.
+__global__ void __launch_bounds__(1024) spikes_kernel(SpikeOut o, Routes p2p, Routes grp) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t carry, src_base;
+  __shared__ uint32_t pk_base[2][64];
+  const int tid = threadIdx.x;
+  if (tid == 0) { carry = 0; src_base = *o.n_src; }
+  for (int d = tid; d < 64; d += blockDim.x) {
+    pk_base[0][d] = d < p2p.n_dest ? p2p.counts[d] : 0;
+    pk_base[1][d] = d < grp.n_dest ? grp.counts[d] : 0;
+  }
+  __syncthreads();
+  const uint32_t nwords = (o.n_rows + 31) / 32;
+  for (uint32_t w0 = 0; w0 < nwords; w0 += blockDim.x) {
+    const uint32_t w = w0 + tid;
+    uint32_t bits = w < nwords ? o.spike_bits[w] : 0;
+    uint32_t tot;
+    const uint32_t ex = smx::block_excl_scan(__popc(bits), ws, tot);
+    uint32_t k = carry + ex;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const uint32_t row = w * 32 + b;
+      const uint32_t node = o.row2node[row];
+      const uint32_t si = src_base + k;
+      if (si < o.src_cap) { o.src_nodes[si] = node; o.src_steps[si] = (uint32_t)o.now; }
+      else atomicExch(o.overflow, 1);
+      if (o.record) {
+        const uint64_t ri = *o.n_rec + k;
+        if (ri < o.rec_cap) { o.rec[2 * ri] = o.now; o.rec[2 * ri + 1] = o.gid[row]; }
+        else atomicExch(o.overflow, 2);
+      }
+      ++k;
+    }
+    __syncthreads();
+    if (tid == 0) carry += tot;
+    __syncthreads();
+  }
+  const uint32_t n_spk = carry;
+  // packets: positions in spike order, per destination in route order
+  for (int fam = 0; fam < 2; ++fam) {
+    const Routes& R = fam ? grp : p2p;
+    if (R.n_dest == 0) continue;
+    for (uint32_t c0 = 0; c0 < n_spk; c0 += blockDim.x) {
+      const uint32_t c = c0 + tid;
+      int64_t lo = 0, hi = 0;
+      if (c < n_spk && src_base + c < o.src_cap) {
+        const uint32_t node = o.src_nodes[src_base + c];
+        lo = R.first[node];
+        hi = R.first[node + 1];
+      }
+      for (int d = 0; d < R.n_dest; ++d) {
+        uint32_t cnt = 0;
+        for (int64_t e = lo; e < hi; ++e) cnt += (R.dest[e] == d);
+        uint32_t tot;
+        const uint32_t ex = smx::block_excl_scan(cnt, ws, tot);
+        uint32_t q = pk_base[fam][d] + ex;
+        for (int64_t e = lo; e < hi; ++e) {
+          if (R.dest[e] != d) continue;
+          if (q < R.cap) {
+            R.packets[2 * ((size_t)d * R.cap + q)] = R.pos[e];
+            R.packets[2 * ((size_t)d * R.cap + q) + 1] = (uint32_t)o.now;
+          } else {
+            atomicExch(o.overflow, 3);
+          }
+          ++q;
+        }
+        __syncthreads();
+        if (tid == 0) pk_base[fam][d] += tot;
+        __syncthreads();
+      }
+    }
+    for (int d = tid; d < R.n_dest; d += blockDim.x) R.counts[d] = min(pk_base[fam][d], R.cap);
+  }
+  if (tid == 0) {
+    *o.n_src = min(src_base + n_spk, o.src_cap);
+    if (o.record) *o.n_rec += n_spk;
+    if (o.spike_count) *o.spike_count += n_spk;
+  }
+}
+
+// Packet positions -> image nodes appended to a delivery source list.
+__global__ void unpack_kernel(const uint32_t* packets, const uint32_t* count, const int64_t* table,
+                              uint64_t table_len, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src,
+                              uint32_t src_cap, int* err) {
+  const uint32_t n = *count;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t p = packets[2 * i];
+    if (p >= table_len) { atomicExch(err, 4); continue; }
+    const int64_t img = table[p];
+    if (img < 0) continue;
+    const uint32_t k = atomicAdd(n_src, 1u);
+    if (k < src_cap) { src_nodes[k] = (uint32_t)img; src_steps[k] = packets[2 * i + 1]; }
+    else atomicExch(err, 1);
+  }
+}
+
+constexpr uint32_t CHUNK = 1024;  // records per delivery work item
+
+// Single CTA: work-item prefix over the source list (ceil(len/CHUNK) each).
+__global__ void __launch_bounds__(1024) plan_kernel(const uint32_t* src_nodes, const uint32_t* n_src,
+                                                    const int64_t* first, uint32_t* wprefix, uint32_t* n_work) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const uint32_t n = *n_src;
+  for (uint32_t c0 = 0; c0 < n; c0 += blockDim.x) {
+    const uint32_t c = c0 + threadIdx.x;
+    uint32_t w = 0;
+    if (c < n) {
+      const uint32_t node = src_nodes[c];
+      const int64_t len = first[node + 1] - first[node];
+      w = (uint32_t)((len + CHUNK - 1) / CHUNK);
+    }
+    uint32_t tot;
+    const uint32_t ex = smx::block_excl_scan(w, ws, tot);
+    if (c < n) wprefix[c] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *n_work = carry;
+}
+
+struct SynTable {  // packed mode: class -> (weight, delay, port)
+  const double* w;
+  const uint32_t* delay;
+  const uint32_t* port;
+};
+
+template <bool WIDE>
+__global__ void __launch_bounds__(T256) deliver_kernel(const uint32_t* src_nodes, const uint32_t* src_steps,
+                                                       const uint32_t* n_src, const uint32_t* wprefix,
+                                                       const uint32_t* n_work, const int64_t* first,
+                                                       const uint32_t* payload, SynTable syn, const double* wide_w,
+                                                       const uint32_t* wide_meta, double* ring, uint32_t n_rows,
+                                                       int n_ports, int L) {
+  const uint32_t nw = *n_work, ns = *n_src;
+  __shared__ double cw[256];
+  __shared__ uint32_t cd[256], cp[256];
+  if (!WIDE) {
+    for (int c = threadIdx.x; c < 256; c += blockDim.x) {
+      cw[c] = syn.w[c];
+      cd[c] = syn.delay[c];
+      cp[c] = syn.port[c];
+    }
+    __syncthreads();
+  }
+  const size_t slot_stride = (size_t)n_ports * n_rows;
+  for (uint32_t w = blockIdx.x; w < nw; w += gridDim.x) {
+    // source index: last c with wprefix[c] <= w
+    uint32_t lo = 0, hi = ns - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (wprefix[mid] <= w) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t node = src_nodes[lo];
+    const int64_t now = src_steps[lo];
+    const int64_t a = first[node] + (int64_t)(w - wprefix[lo]) * CHUNK;
+    int64_t b = first[node + 1];
+    if (b > a + CHUNK) b = a + CHUNK;
+    for (int64_t k = a + threadIdx.x; k < b; k += blockDim.x) {
+      const uint32_t pl = payload[k];
+      double wt;
+      uint32_t d, port, row;
+      if (WIDE) {
+        const uint32_t m = wide_meta[k];
+        wt = wide_w[k];
+        d = m & 0xffffffu;
+        port = m >> 24;
+        row = pl;
+      } else {
+        const uint32_t c = pl >> SMX_ROW_BITS;
+        wt = cw[c];
+        d = cd[c];
+        port = cp[c];
+        row = pl & SMX_ROW_MASK;
+      }
+      const int slot = (int)((now + d) % L);
+      atomicAdd(ring + slot * slot_stride + (size_t)port * n_rows + row, wt);
+    }
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI (engine layout)
+// ---------------------------------------------------------------------------
+
+extern "C" int smx_lif_update(double* v, int32_t* ref, const double* decay, const double* v_rest,
+                              const double* v_reset, const double* v_th, const int32_t* ref_steps,
+                              const double* i_e, uint32_t n, double* ring, int n_ports, int L, int64_t now,
+                              uint32_t* spike_bits, void* stream) {
+  if (n == 0) return 0;
+  LifState s{v, ref, decay, v_rest, v_reset, v_th, ref_steps, i_e};
+  lif_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(s, n, ring, n_ports, L, now, spike_bits);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int smx_poisson_emit(const uint8_t* counts, uint32_t n_t, const uint32_t* rows, double w,
+                                double* ring_slot_port, void* stream) {
+  if (n_t == 0) return 0;
+  poisson_emit_kernel<<<nblk(n_t), T256, 0, (cudaStream_t)stream>>>(counts, n_t, rows, w, ring_slot_port);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+// Route-family descriptor as laid out by the host (matches Routes).
+struct SmxRoutes {
+  const int64_t* first;
+  const int32_t* dest;
+  const uint32_t* pos;
+  int n_dest;
+  uint32_t* packets;
+  uint32_t* counts;
+  uint32_t cap;
+};
+
+extern "C" int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uint32_t* row2node,
+                          const int64_t* gid, int64_t now, uint32_t* src_nodes, uint32_t* src_steps,
+                          uint32_t* n_src, uint32_t src_cap, int record, int64_t* rec, uint64_t* n_rec,
+                          uint64_t rec_cap, uint32_t* spike_count, int* overflow, const SmxRoutes* p2p,
+                          const SmxRoutes* grp, void* stream) {
+  SpikeOut o;
+  o.spike_bits = spike_bits;
+  o.n_rows = n_rows;
+  o.row2node = row2node;
+  o.gid = gid;
+  o.now = now;
+  o.src_nodes = src_nodes;
+  o.src_steps = src_steps;
+  o.n_src = n_src;
+  o.src_cap = src_cap;
+  o.record = record;
+  o.rec = rec;
+  o.n_rec = n_rec;
+  o.rec_cap = rec_cap;
+  o.spike_count = spike_count;
+  o.overflow = overflow;
+  Routes a{}, b{};
+  if (p2p) a = Routes{p2p->first, p2p->dest, p2p->pos, p2p->n_dest, p2p->packets, p2p->counts, p2p->cap};
+  if (grp) b = Routes{grp->first, grp->dest, grp->pos, grp->n_dest, grp->packets, grp->counts, grp->cap};
+  if (a.n_dest > 64 || b.n_dest > 64) {
+    smx_set_error("at most 64 packet destinations per routing family");
+    return -1;
+  }
+  spikes_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(o, a, b);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int smx_unpack(const uint32_t* packets, const uint32_t* count, const int64_t* table, uint64_t table_len,
+                          uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err,
+                          void* stream) {
+  unpack_kernel<<<148, T256, 0, (cudaStream_t)stream>>>(packets, count, table, table_len, src_nodes, src_steps,
+                                                         n_src, src_cap, err);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+// Deliver every (node, step) of the source list through the CSR tables.
+// wprefix needs src_cap entries, work a 1-word counter.
+extern "C" int smx_deliver(const uint32_t* src_nodes, const uint32_t* src_steps, const uint32_t* n_src,
+                           uint32_t* wprefix, uint32_t* n_work, const int64_t* first, const uint32_t* payload,
+                           const double* cls_w, const uint32_t* cls_delay, const uint32_t* cls_port,
+                           const double* wide_w, const uint32_t* wide_meta, double* ring, uint32_t n_rows,
+                           int n_ports, int L, int grid, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  plan_kernel<<<1, 1024, 0, st>>>(src_nodes, n_src, first, wprefix, n_work);
+  SynTable syn{cls_w, cls_delay, cls_port};
+  if (grid <= 0) grid = 148 * 8;
+  if (wide_w) {
+    deliver_kernel<true><<<grid, T256, 0, st>>>(src_nodes, src_steps, n_src, wprefix, n_work, first, payload, syn,
+                                                 wide_w, wide_meta, ring, n_rows, n_ports, L);
+  } else {
+    deliver_kernel<false><<<grid, T256, 0, st>>>(src_nodes, src_steps, n_src, wprefix, n_work, first, payload, syn,
+                                                  wide_w, wide_meta, ring, n_rows, n_ports, L);
+  }
+  SMX_LAUNCH_CHECK();
+  return 0;
+}

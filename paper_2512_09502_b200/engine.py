@@ -1,0 +1,1292 @@
+"""The GPU `Cluster`: the reference façade (sm/engine.py:197-399) over
+sm_100a kernels.
+
+Every heavy step is a call through the C ABI (`_lib`) on device buffers owned
+by torch tensors (plumbing only).  Host work is bookkeeping per façade call:
+stream keys (blake2b of the stream id), call counters, argument validation
+and buffer sizing.  There is no CPU fallback: without a CUDA device or the
+built library every method raises.
+
+Rank placement.  The reference keeps every rank in one process.  Here a
+process owns a set of *local* ranks:
+  * single process (default): all ranks are local, placed on `devices`
+    (default cuda:0) -- the layout used by the parity tests;
+  * one process per GPU (torch.distributed initialised with
+    world_size == n_ranks): only rank == dist.get_rank() is local.  Every
+    process runs the whole construction script; calls that touch no local
+    rank only advance counters, exactly like the paper's per-process scripts.
+Construction and preparation never communicate (check_construction_silent).
+"""
+from __future__ import annotations
+
+import math
+import time
+from contextlib import contextmanager
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call
+from .api import (POINT_TO_POINT, ConnSpec, ConsistencyError, DelayRangeError, LifParams,
+                  ProtocolError, Raster, SimConfig, SynSpec, canonical_bytes, stream_key)
+
+TMP_KEY = 0x80000000
+ROW_MASK = 0xFFFFFF
+MAX_CLASSES = 256
+PHASES = ("construction", "preparation", "propagation")
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _words(nbits: int) -> int:
+    return (int(nbits) + 31) // 32
+
+
+@dataclass
+class PhaseTimers:
+    """sm/engine.py:40-52 (seconds; host wall clock around each façade call,
+    with a device synchronisation at the end of the phase)."""
+
+    initialization: float = 0.0
+    node_creation: float = 0.0
+    local_connection: float = 0.0
+    remote_connection: float = 0.0
+    preparation: float = 0.0
+    propagation: float = 0.0
+
+    def as_dict(self) -> dict:
+        return asdict(self)
+
+
+@dataclass
+class RunReport:
+    """sm/engine.py:55-82 (arena peaks are out of scope: reported as 0)."""
+
+    n_ranks: int
+    comm_mode: str
+    opt_level: int
+    seed: int
+    kernel_backend: str
+    n_neurons: int
+    n_synapses: int
+    timers: dict
+    warmup_s: float
+    model_time_s: float
+    rtf: float
+    host_peak_bytes: list
+    device_peak_bytes: list
+    transport_messages: dict
+    transport_bytes: dict
+    n_spike_events: int
+    raster_sha256: str | None
+
+
+class _Buf:
+    """Growable 1-D device buffer."""
+
+    def __init__(self, dtype, device, cap=0, fill=None):
+        self.dtype, self.device, self.fill = dtype, device, fill
+        self.t = self._alloc(max(cap, 16))
+        self.n = 0
+
+    def _alloc(self, cap):
+        if self.fill is None:
+            return torch.empty(cap, dtype=self.dtype, device=self.device)
+        return torch.full((cap,), self.fill, dtype=self.dtype, device=self.device)
+
+    def reserve(self, n):
+        if n > self.t.numel():
+            cap = max(n, int(self.t.numel() * 1.5) + 16)
+            nt = self._alloc(cap)
+            nt[: self.t.numel()].copy_(self.t)
+            self.t = nt
+
+    def view(self, a=0, b=None):
+        return self.t[a: self.n if b is None else b]
+
+
+class _Map:
+    """Dense remote-source map (group, source rank) on a target rank:
+    img_of[value] (-1 = no image) plus a presence bitmap.  (R, L) of the
+    reference is the compaction of the bitmap (sm/construction.py:183-242)."""
+
+    def __init__(self, device):
+        self.img_of = _Buf(torch.int32, device, fill=-1)
+        self.present = _Buf(torch.int32, device, fill=0)
+
+    def ensure(self, n_values: int):
+        nw = _words(n_values)
+        self.present.reserve(nw)
+        self.present.n = max(self.present.n, nw)
+        self.img_of.reserve(nw * 32)
+        self.img_of.n = max(self.img_of.n, nw * 32)
+
+
+class _Bits:
+    """Growable bitmap over node values."""
+
+    def __init__(self, device):
+        self.b = _Buf(torch.int32, device, fill=0)
+
+    def ensure(self, n_values):
+        nw = _words(n_values)
+        self.b.reserve(nw)
+        self.b.n = max(self.b.n, nw)
+        return self
+
+    @property
+    def t(self):
+        return self.b.view()
+
+
+class _Rank:
+    """Everything one local rank owns on its device."""
+
+    def __init__(self, rank: int, device: torch.device):
+        self.rank = rank
+        self.device = device
+        self.n_nodes = 0
+        self.n_real = 0
+        self.node2row = _Buf(torch.int32, device, fill=-1)     # device node -> row
+        self.row2node: list[np.ndarray] = []
+        self.row_gid: list[np.ndarray] = []
+        self.row_param: list[np.ndarray] = []
+        self.v0: list[torch.Tensor] = []
+        self.keys = _Buf(torch.int32, device)
+        self.vals = _Buf(torch.int32, device)
+        self.wide = False
+        self.w_rows = self.w_w = self.w_meta = None
+        self.lut = _Buf(torch.int32, device)
+        self.maps: dict[tuple, _Map] = {}
+        self.mirrors: dict[int, _Bits] = {}
+        self.rosters: dict[tuple, _Bits] = {}
+        self.devices: list[dict] = []
+        self.prepared = False
+
+    @property
+    def stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def map_for(self, group, src_rank) -> _Map:
+        key = (int(group), int(src_rank))
+        if key not in self.maps:
+            self.maps[key] = _Map(self.device)
+        return self.maps[key]
+
+    def reserve_records(self, n_new):
+        need = self.keys.n + n_new
+        self.keys.reserve(need)
+        self.vals.reserve(need)
+        if self.wide:
+            self.w_rows.reserve(need)
+            self.w_w.reserve(need)
+            self.w_meta.reserve(need)
+        return self.keys.n
+
+    def commit_records(self, n_new):
+        self.keys.n += n_new
+        self.vals.n += n_new
+        if self.wide:
+            self.w_rows.n += n_new
+            self.w_w.n += n_new
+            self.w_meta.n += n_new
+
+
+class Cluster:
+    """GPU cluster with the reference façade (sm/engine.py:197-399)."""
+
+    def __init__(self, cfg: SimConfig, devices=None, local_ranks=None):
+        t0 = time.perf_counter()
+        if not torch.cuda.is_available():
+            raise RuntimeError("spikemesh-b200 needs a CUDA device (no CPU fallback)")
+        _lib.lib()
+        self.cfg = cfg
+        self.timers = PhaseTimers()
+        self.now = 0
+        self.prepared = False
+        self.n_ranks = cfg.n_ranks
+        dist = torch.distributed
+        self.distributed = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        if local_ranks is None:
+            if self.distributed:
+                if dist.get_world_size() != cfg.n_ranks:
+                    raise ValueError("one process per rank: world_size must equal n_ranks")
+                local_ranks = [dist.get_rank()]
+            else:
+                local_ranks = list(range(cfg.n_ranks))
+        self.local = sorted(int(r) for r in local_ranks)
+        if devices is None:
+            if self.distributed:
+                devices = [torch.device("cuda", torch.cuda.current_device())]
+            else:
+                devices = [torch.device("cuda", 0)]
+        devices = [torch.device(d) for d in devices]
+        self.ranks: dict[int, _Rank] = {
+            r: _Rank(r, devices[i % len(devices)]) for i, r in enumerate(self.local)}
+        # host-side counters and node counts for every rank (scripts run everywhere)
+        self.n_nodes = [0] * cfg.n_ranks
+        self.images_made = [False] * cfg.n_ranks
+        self.local_ctr = [0] * cfg.n_ranks
+        self.pair_ctr: dict[tuple, int] = {}
+        self.dist_ctr = 0
+        self.groups: dict[int, tuple] = {}
+        self.params: list[LifParams] = []
+        self.param_index: dict = {}
+        self.classes: list[tuple] = []      # (weight, delay, port)
+        self.class_index: dict = {}
+        self.messages = {p: 0 for p in PHASES}
+        self.bytes = {p: 0 for p in PHASES}
+        self.phase = "construction"
+        self.timers.initialization += time.perf_counter() - t0
+
+    # ------------------------------------------------------------------ utils
+    def is_local(self, r) -> bool:
+        return int(r) in self.ranks
+
+    def _key(self, sid):
+        return stream_key(self.cfg.seed, sid)
+
+    @contextmanager
+    def _timed(self, bucket):
+        t0 = time.perf_counter()
+        try:
+            yield
+        finally:
+            for st in self.ranks.values():
+                torch.cuda.synchronize(st.device)
+            setattr(self.timers, bucket, getattr(self.timers, bucket) + time.perf_counter() - t0)
+
+    def _require_unprepared(self):
+        if self.prepared:
+            raise ConsistencyError("construction after preparation")
+
+    def _param_id(self, p: LifParams) -> int:
+        key = tuple(asdict(p).values())
+        if key not in self.param_index:
+            self.param_index[key] = len(self.params)
+            self.params.append(p)
+        return self.param_index[key]
+
+    def _class_id(self, weight: float, delay: int, port: int):
+        key = (float(weight), int(delay), int(port))
+        if key not in self.class_index:
+            self.class_index[key] = len(self.classes)
+            self.classes.append(key)
+        return self.class_index[key]
+
+    # ------------------------------------------------------------ node creation
+    def declare_group(self, group_id: int, members) -> None:
+        with self._timed("initialization"):
+            members = tuple(int(m) for m in members)
+            if group_id < 0:
+                raise ValueError(f"group ids must be >= 0, got {group_id}")
+            if len(set(members)) != len(members) or not members:
+                raise ValueError(f"group members must be a non-empty unique list, got {members}")
+            for m in members:
+                if not 0 <= m < self.n_ranks:
+                    raise ValueError(f"group member rank {m} out of range")
+            if group_id in self.groups:
+                raise ValueError(f"group {group_id} already declared")
+            self.groups[group_id] = members
+
+    def create_neurons(self, rank: int, n: int, params: LifParams | None = None, v_init=None,
+                       gids=None) -> range:
+        """sm/construction.py:335-370; initial V per gid drawn on the device."""
+        with self._timed("node_creation"):
+            self._require_unprepared()
+            if n <= 0:
+                raise ValueError(f"need n >= 1 neurons, got {n}")
+            params = params if params is not None else LifParams()
+            start = self.n_nodes[rank]
+            if not self.is_local(rank) and self.images_made[rank]:
+                raise NotImplementedError(
+                    "node ranges of a remote rank are unknown after it created images")
+            if gids is None:
+                gids = np.arange(start, start + n, dtype=np.int64)
+            else:
+                gids = np.asarray(gids, dtype=np.int64)
+                if len(gids) != n:
+                    raise ValueError("gids must have one entry per neuron")
+            self.n_nodes[rank] = start + n
+            if not self.is_local(rank):
+                return range(start, start + n)
+            st = self.ranks[rank]
+            dev = st.device
+            if v_init is None:
+                v = torch.full((n,), float(params.v_rest), dtype=torch.float64, device=dev)
+            elif isinstance(v_init, tuple):
+                if len(v_init) != 3 or v_init[0] != "normal":
+                    raise ValueError(f"bad v_init spec {v_init!r}")
+                v = torch.empty(n, dtype=torch.float64, device=dev)
+                g = torch.from_numpy(gids).to(dev)
+                pre = canonical_bytes((int(self.cfg.seed), ("init-v", 0)))
+                prefix = pre[: pre.rindex(b"i:0))") + 2]
+                suffix = b"))"
+                call("smx_init_v", prefix, len(prefix), suffix, len(suffix), _ptr(g), n,
+                     float(v_init[1]), float(v_init[2]), _ptr(v), st.stream)
+            elif np.ndim(v_init) == 0:
+                v = torch.full((n,), float(v_init), dtype=torch.float64, device=dev)
+            else:
+                v = torch.as_tensor(np.asarray(v_init, dtype=np.float64)).to(dev)
+                if v.numel() != n:
+                    raise ValueError("v_init must have one entry per neuron")
+            row0 = st.n_real
+            st.node2row.reserve(start + n)
+            st.node2row.t[start: start + n] = torch.arange(row0, row0 + n, dtype=torch.int32, device=dev)
+            st.node2row.n = start + n
+            st.row2node.append(np.arange(start, start + n, dtype=np.int64))
+            st.row_gid.append(gids)
+            st.row_param.append(np.full(n, self._param_id(params), dtype=np.int32))
+            st.v0.append(v)
+            st.n_real += n
+            st.n_nodes = start + n
+            if st.n_real > ROW_MASK:
+                raise ValueError("more than 2^24 real neurons on one rank")
+            return range(start, start + n)
+
+    def add_poisson_source(self, rank: int, rate_hz: float, weight: float, delay_steps: int, targets,
+                           port: int = 0):
+        """sm/construction.py:373-384 (stream ("poisson", rank, device index))."""
+        with self._timed("node_creation"):
+            self._require_unprepared()
+            if rate_hz < 0.0:
+                raise ValueError(f"rate must be >= 0, got {rate_hz}")
+            if delay_steps < 1:
+                raise ValueError(f"delay must be >= 1 step, got {delay_steps}")
+            targets = np.asarray(targets, dtype=np.int64)
+            if len(targets) and (targets.min() < 0 or targets.max() >= self.n_nodes[rank]):
+                raise ValueError("poisson targets outside the rank's node range")
+            lam = float(rate_hz) * self.cfg.resolution_ms * 1e-3
+            if lam >= 10.0:
+                raise NotImplementedError("poisson drive with lam >= 10 (numpy PTRS) is not implemented")
+            if not self.is_local(rank):
+                return None
+            st = self.ranks[rank]
+            d = dict(index=len(st.devices), key=self._key(("poisson", rank, len(st.devices))), lam=lam,
+                     enlam=math.exp(-lam), weight=float(weight), delay=int(delay_steps),
+                     port=int(port), targets=targets)
+            st.devices.append(d)
+            return d
+
+    # -------------------------------------------------------------- connections
+    def _tables(self, st: _Rank, sources, targets, cls, tmp_base=None):
+        dev = st.device
+        src = torch.from_numpy(np.ascontiguousarray(sources, dtype=np.int64)).to(dev)
+        tgt = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.int64)).to(dev)
+        key_tab = torch.empty(len(sources), dtype=torch.int32, device=dev)
+        pay_tab = torch.empty(len(targets), dtype=torch.int32, device=dev)
+        call("smx_key_table", _ptr(src), len(sources), 0 if tmp_base is None else tmp_base,
+             0 if tmp_base is None else 1, _ptr(key_tab), st.stream)
+        call("smx_pay_table", _ptr(tgt), len(targets), _ptr(st.node2row.t), st.node2row.n,
+             cls & 0xFF, _ptr(pay_tab), st.stream)
+        return src, tgt, key_tab, pay_tab
+
+    def _syn_class(self, st: _Rank, syn: SynSpec, port: int):
+        """Class id for a constant SynSpec in packed mode, or None (wide)."""
+        if syn.is_constant and not st.wide:
+            cid = self._class_id(float(syn.weight), int(syn.delay_steps), port)
+            if cid < MAX_CLASSES:
+                return cid
+        return None
+
+    def _make_wide(self, st: _Rank):
+        if st.wide:
+            return
+        dev = st.device
+        n = st.keys.n
+        st.w_rows = _Buf(torch.int32, dev, cap=st.keys.t.numel())
+        st.w_w = _Buf(torch.float64, dev, cap=st.keys.t.numel())
+        st.w_meta = _Buf(torch.int32, dev, cap=st.keys.t.numel())
+        if n:
+            cw, cm = self._class_tables(dev)
+            call("smx_promote_wide", _ptr(st.vals.t), n, _ptr(cw), _ptr(cm), _ptr(st.w_rows.t),
+                 _ptr(st.w_w.t), _ptr(st.w_meta.t), st.stream)
+        st.w_rows.n = st.w_w.n = st.w_meta.n = n
+        st.wide = True
+
+    def _class_tables(self, dev):
+        cw = torch.zeros(MAX_CLASSES, dtype=torch.float64)
+        cm = torch.zeros(MAX_CLASSES, dtype=torch.int64)
+        for i, (w, d, p) in enumerate(self.classes[:MAX_CLASSES]):
+            cw[i] = w
+            cm[i] = (d & 0xFFFFFF) | (p << 24)
+        return cw.to(dev), cm.to(torch.int32).to(dev)
+
+    def _write_syn(self, st: _Rank, syn: SynSpec, port: int, base: int, n: int, syn_key):
+        """Per-record weights/delays for wide ranks (sm/construction.py:157-176)."""
+        dev = st.device
+        w, d = syn.weight, syn.delay_steps
+        if isinstance(w, tuple) or isinstance(d, tuple):
+            raise NotImplementedError("random SynSpec draws (normal / uniform_int) are not implemented yet")
+        wv = np.asarray(w, dtype=np.float64)
+        dv = np.asarray(d, dtype=np.int64)
+        if wv.ndim and len(wv) != n:
+            raise ValueError(f"{len(wv)} weights for {n} records")
+        if dv.ndim and len(dv) != n:
+            raise ValueError(f"{len(dv)} delays for {n} records")
+        if dv.ndim and len(dv) and dv.min() < 1:
+            raise DelayRangeError(f"connection delays must be >= 1 step, got {dv.min()}")
+        if (dv.max() if dv.size else 0) > ROW_MASK or port > 255:
+            raise DelayRangeError("delay >= 2^24 steps or port > 255 not representable")
+        seg_w = st.w_w.t[base: base + n]
+        seg_m = st.w_meta.t[base: base + n]
+        if wv.ndim == 0 and dv.ndim == 0:
+            call("smx_fill_wide_const", _ptr(seg_w), _ptr(seg_m), n, float(wv),
+                 (int(dv) & ROW_MASK) | (port << 24), st.stream)
+        else:
+            seg_w.copy_(torch.from_numpy(np.broadcast_to(wv, (n,)).copy()))
+            meta = (np.broadcast_to(dv, (n,)).astype(np.int64) & ROW_MASK) | (port << 24)
+            seg_m.copy_(torch.from_numpy(meta.astype(np.uint32).view(np.int32)))
+
+    def _emit_records(self, st: _Rank, conn: ConnSpec, sources, targets, syn: SynSpec, port: int,
+                      aligned_key, local_key, syn_key, tmp_base=None, pos_bits=None):
+        """Realize one call's records into the pending buffers (target side).
+        Returns the record count.  sm/construction.py:410-432 + 530-534."""
+        n_src, n_tgt = len(sources), len(targets)
+        cls = self._syn_class(st, syn, port)
+        if cls is None:
+            self._make_wide(st)
+        src, tgt, key_tab, pay_tab = self._tables(st, sources, targets, 0 if cls is None else cls, tmp_base)
+        rule = conn.rule
+        if rule in ("one_to_one", "assigned"):
+            n = n_src
+        elif rule == "all_to_all":
+            n = n_src * n_tgt
+        elif rule == "fixed_indegree":
+            n = int(conn.k_in) * n_tgt
+        elif rule == "fixed_outdegree":
+            n = int(conn.k_out) * n_src
+        else:
+            n = int(conn.n_total)
+        base = st.reserve_records(n)
+        keys = st.keys.t[base:]
+        vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
+        cur = np.zeros(1, dtype=np.uint64)
+        sk = st.stream
+        if n:
+            if rule in ("one_to_one", "assigned"):
+                call("smx_gen_pairs", 0, n, n_src, _ptr(key_tab), _ptr(pay_tab), _ptr(keys), _ptr(vals), sk)
+            elif rule == "all_to_all":
+                call("smx_gen_pairs", 1, n, n_src, _ptr(key_tab), _ptr(pay_tab), _ptr(keys), _ptr(vals), sk)
+            elif rule == "fixed_indegree":
+                call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 2, _ptr(key_tab),
+                     _ptr(pay_tab), int(conn.k_in), _ptr(keys), _ptr(vals), _ptr(pos_bits), 0,
+                     cur.ctypes.data, sk)
+            elif rule == "fixed_outdegree":
+                call("smx_gen_draw", local_key[0], local_key[1], 0, n_tgt, n, 2, 1, _ptr(key_tab),
+                     _ptr(pay_tab), int(conn.k_out), _ptr(keys), _ptr(vals), 0, 0, cur.ctypes.data, sk)
+            else:  # fixed_total: positions (aligned) then targets (local; same stream locally)
+                call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 0, _ptr(key_tab),
+                     0, 1, _ptr(keys), 0, _ptr(pos_bits), 0, cur.ctypes.data, sk)
+                u0 = int(cur[0]) if local_key == aligned_key else 0
+                call("smx_gen_draw", local_key[0], local_key[1], u0, n_tgt, n, 0, 1, 0,
+                     _ptr(pay_tab), 1, 0, _ptr(vals), 0, 0, cur.ctypes.data, sk)
+        if st.wide:
+            self._write_syn(st, syn, port, base, n, syn_key)
+        st.commit_records(n)
+        return n, src
+
+    def _validate_conn(self, rank, sources, targets, conn, syn, what="connect"):
+        sources = np.asarray(sources, dtype=np.int64)
+        targets = np.asarray(targets, dtype=np.int64)
+        if len(sources) == 0 or len(targets) == 0:
+            raise ValueError("connect needs non-empty source and target sets")
+        for name, arr, r in (("source", sources, rank[0]), ("target", targets, rank[1])):
+            if arr.min() < 0 or arr.max() >= self.n_nodes[r]:
+                raise ValueError(f"{name} index outside the rank's node range")
+        conn.validate(len(sources), len(targets))
+        syn.validate()
+        if not conn.allow_autapses and conn.rule in ("fixed_indegree", "fixed_total"):
+            raise NotImplementedError("allow_autapses=False (redraw loop) is not implemented yet")
+        if conn.rule == "fixed_indegree" and not conn.allow_multapses:
+            raise NotImplementedError("allow_multapses=False (choice without replacement) is not implemented yet")
+        return sources, targets
+
+    def connect(self, rank: int, sources, targets, conn: ConnSpec, syn: SynSpec, port: int = 0) -> int:
+        """sm/construction.py:507-534."""
+        with self._timed("local_connection"):
+            return self._connect_local(rank, sources, targets, conn, syn, port)
+
+    def _connect_local(self, rank, sources, targets, conn, syn, port, validated=False):
+        self._require_unprepared()
+        if not validated:
+            sources, targets = self._validate_conn((rank, rank), sources, targets, conn, syn)
+        if port < 0:
+            raise ValueError("ports must be >= 0")
+        self.local_ctr[rank] += 1
+        if not self.is_local(rank):
+            return 0
+        st = self.ranks[rank]
+        ctr = self.local_ctr[rank]
+        k = self._key(("conn-local", rank, ctr))
+        n, _ = self._emit_records(st, conn, sources, targets, syn, port, k, k,
+                                  self._key(("syn-local", rank, ctr)))
+        return n
+
+    def connect_remote(self, src_rank: int, sources, tgt_rank: int, targets, conn: ConnSpec,
+                       syn: SynSpec, port: int = 0, group: int = POINT_TO_POINT) -> int:
+        """sm/construction.py:550-637."""
+        with self._timed("remote_connection"):
+            return self._remote(src_rank, sources, tgt_rank, targets, conn, syn, port, group)
+
+    def _flagging(self, conn, n_src, n_tgt) -> bool:
+        """sm/construction.py:439-451."""
+        if conn.rule == "fixed_indegree":
+            return int(conn.k_in) * n_tgt / n_src < self.cfg.flag_threshold
+        if conn.rule == "fixed_total":
+            return int(conn.n_total) / n_src < self.cfg.flag_threshold
+        return False
+
+    def _bump_pair(self, sr, tr) -> int:
+        idx = self.pair_ctr.get((sr, tr), 0) + 1
+        self.pair_ctr[(sr, tr)] = idx
+        return idx
+
+    def _remote(self, sr, sources, tr, targets, conn, syn, port, group):
+        for r in (sr, tr):
+            if not 0 <= r < self.n_ranks:
+                raise ValueError(f"rank {r} out of range 0..{self.n_ranks - 1}")
+        if sr == tr:
+            return self._connect_local(sr, sources, targets, conn, syn, port)
+        self._require_unprepared()
+        sources, targets = self._validate_conn((sr, tr), sources, targets, conn, syn)
+        members = None
+        if group != POINT_TO_POINT:
+            members = self.groups.get(group)
+            if members is None:
+                raise ValueError(f"group {group} is not declared")
+            if sr not in members or tr not in members:
+                raise ValueError(f"ranks {sr} and {tr} must both belong to group {group}")
+        n_src, n_tgt = len(sources), len(targets)
+        idx = self._bump_pair(sr, tr)
+        flag = self._flagging(conn, n_src, n_tgt)
+        k_src = self._key(("remote-src", sr, tr, idx))
+        k_tgt = self._key(("remote-tgt", sr, tr, idx))
+        k_syn = self._key(("remote-syn", sr, tr, idx))
+        n_rec = 0
+        used_pos = None
+        span = int(sources.max()) + 1
+        if self.is_local(tr):
+            st = self.ranks[tr]
+            dev = st.device
+            pos_bits = torch.zeros(_words(n_src), dtype=torch.int32, device=dev) if flag else None
+            lut_base = st.lut.n
+            n_rec, src_dev = self._emit_records(st, conn, sources, targets, syn, port, k_src, k_tgt, k_syn,
+                                                tmp_base=lut_base, pos_bits=pos_bits)
+            vbits = torch.zeros(_words(span), dtype=torch.int32, device=dev)
+            call("smx_mark_values", _ptr(pos_bits), _ptr(src_dev), n_src, _ptr(vbits), st.stream)
+            if flag:
+                used_pos = pos_bits
+            m = st.map_for(group, sr)
+            m.ensure(span)
+            self._assign(st, vbits, [(0, _words(span), m)])
+            st.lut.reserve(lut_base + n_src)
+            call("smx_gather_lut", _ptr(src_dev), n_src, _ptr(m.img_of.t), _ptr(st.lut.t[lut_base:]), st.stream)
+            st.lut.n = lut_base + n_src
+        # source side
+        if group == POINT_TO_POINT:
+            if self.is_local(sr):
+                ss = self.ranks[sr]
+                dev = ss.device
+                src_dev = torch.from_numpy(sources).to(dev)
+                pb = None
+                if flag:
+                    if used_pos is not None and used_pos.device == dev:
+                        pb = used_pos
+                    else:
+                        pb = self._replay_positions(ss, conn, n_src, n_tgt, k_src)
+                mir = ss.mirrors.setdefault(tr, _Bits(dev)).ensure(span)
+                call("smx_mark_values", _ptr(pb), _ptr(src_dev), n_src, _ptr(mir.t), ss.stream)
+        else:
+            for mbr in members:
+                if self.is_local(mbr):
+                    ms = self.ranks[mbr]
+                    src_dev = torch.from_numpy(sources).to(ms.device)
+                    ros = ms.rosters.setdefault((group, sr), _Bits(ms.device)).ensure(span)
+                    call("smx_mark_values", 0, _ptr(src_dev), n_src, _ptr(ros.t), ms.stream)
+        return n_rec
+
+    def _replay_positions(self, ss: _Rank, conn, n_src, n_tgt, k_src):
+        """Source-side replay of the aligned position draws (sm/construction.py:620-627)."""
+        pb = torch.zeros(_words(n_src), dtype=torch.int32, device=ss.device)
+        n = int(conn.k_in) * n_tgt if conn.rule == "fixed_indegree" else int(conn.n_total)
+        cur = np.zeros(1, dtype=np.uint64)
+        if n:
+            call("smx_gen_draw", k_src[0], k_src[1], 0, n_src, n, 1, 0, 0, 0, 1, 0, 0, _ptr(pb), 0,
+                 cur.ctypes.data, ss.stream)
+        return pb
+
+    def _assign(self, st: _Rank, vbits, segs):
+        """New images for set bits of vbits, segments in ascending source-rank
+        order: ids n_nodes, n_nodes+1, ... (sm/construction.py:473-486)."""
+        arr = (ctypes_segment * len(segs))()
+        for i, (w0, nw, m) in enumerate(segs):
+            arr[i].word0 = w0
+            arr[i].nwords = nw
+            arr[i].present = _ptr(m.present.t) if m is not None else 0
+            arr[i].img_of = _ptr(m.img_of.t) if m is not None else 0
+        n_new = np.zeros(1, dtype=np.int64)
+        call("smx_assign_images", _ptr(vbits), vbits.numel(), ctypes_addr(arr), len(segs),
+             st.n_nodes, n_new.ctypes.data, st.stream)
+        n_new = int(n_new[0])
+        if n_new:
+            st.node2row.reserve(st.n_nodes + n_new)
+            st.node2row.t[st.n_nodes: st.n_nodes + n_new] = -1
+            st.n_nodes += n_new
+            st.node2row.n = st.n_nodes
+            self.n_nodes[st.rank] = st.n_nodes
+            self.images_made[st.rank] = True
+        return n_new
+
+    def connect_fixed_indegree_distributed(self, source_pops, target_pops, k_in: int, syn: SynSpec,
+                                           port: int = 0, group: int = POINT_TO_POINT,
+                                           allow_multapses: bool = True) -> int:
+        """sm/construction.py:640-703, one fused pass per target rank."""
+        with self._timed("remote_connection"):
+            return self._dist(source_pops, target_pops, k_in, syn, port, group, allow_multapses)
+
+    def _dist(self, source_pops, target_pops, k_in, syn, port, group, allow_multapses):
+        self._require_unprepared()
+        if k_in < 0:
+            raise ValueError(f"k_in must be >= 0, got {k_in}")
+        src_ranks = [int(r) for r, _ in source_pops]
+        src_nodes = [np.asarray(nodes, dtype=np.int64) for _, nodes in source_pops]
+        if not src_nodes or any(len(a) == 0 for a in src_nodes):
+            raise ValueError("source populations must be non-empty")
+        if not allow_multapses:
+            raise NotImplementedError("allow_multapses=False (choice without replacement) is not implemented yet")
+        syn.validate()
+        if not syn.is_constant:
+            raise NotImplementedError("random / per-record SynSpec in the distributed rule is not implemented yet")
+        all_rank = np.concatenate([np.full(len(a), r, dtype=np.int32) for r, a in zip(src_ranks, src_nodes)])
+        all_node = np.concatenate(src_nodes)
+        total = len(all_node)
+        for r, a in zip(src_ranks, src_nodes):
+            if a.min() < 0 or a.max() >= self.n_nodes[r]:
+                raise ValueError("source index outside the source rank's node range")
+        self.dist_ctr += 1
+        call_idx = self.dist_ctr
+        # value segments per source rank, ascending rank, word aligned
+        ranks_sorted = sorted(set(src_ranks))
+        span = {r: int(max(a.max() for rr, a in zip(src_ranks, src_nodes) if rr == r)) + 1 for r in ranks_sorted}
+        vbase = np.zeros(self.n_ranks, dtype=np.int64)
+        seg_words = {}
+        acc = 0
+        for r in ranks_sorted:
+            vbase[r] = acc * 32
+            seg_words[r] = (acc, _words(span[r]))
+            acc += _words(span[r])
+        total_words = acc
+        n_created = 0
+        members = self.groups.get(group) if group != POINT_TO_POINT else None
+        if group != POINT_TO_POINT and members is None:
+            raise ValueError(f"group {group} is not declared")
+        tgt_bits: dict[int, torch.Tensor] = {}   # per target rank: used-value bitmap (when computed)
+        for tr, tg in target_pops:
+            tr = int(tr)
+            tg = np.asarray(tg, dtype=np.int64)
+            if len(tg) == 0:
+                raise ValueError("target populations must be non-empty")
+            key = self._key(("dist-indegree", call_idx, tr))
+            n = k_in * len(tg)
+            need_bits = self.is_local(tr) or any(
+                self.is_local(r) for r in (members or ranks_sorted))
+            if not need_bits or n == 0:
+                continue
+            if self.is_local(tr):
+                st = self.ranks[tr]
+                if tg.min() < 0 or tg.max() >= self.n_nodes[tr]:
+                    raise ValueError("target index outside the rank's node range")
+                vb, present = self._dist_target(st, key, tr, tg, k_in, total, all_rank, all_node, vbase,
+                                                seg_words, total_words, syn, port, group, ranks_sorted)
+            else:
+                dev = next(iter(self.ranks.values())).device
+                vb = self._dist_replay(dev, key, tr, total, all_rank, all_node, vbase, total_words, n)
+                present = None
+            tgt_bits[tr] = (vb, present)
+        # counters, in the reference's (target, source-rank) call order
+        for tr, tg in target_pops:
+            tr = int(tr)
+            if tr not in tgt_bits:
+                continue
+            vb, present = tgt_bits[tr]
+            if present is None:
+                present = self._present_ranks(vb, ranks_sorted, seg_words)
+            for sr in present:
+                if sr == tr:
+                    self.local_ctr[tr] += 1
+                else:
+                    self._bump_pair(sr, tr)
+            if self.is_local(tr):
+                n_created += k_in * len(tg)
+            # source side: mirrors (p2p) / rosters (collective)
+            for sr in present:
+                if sr == tr:
+                    continue
+                w0, nw = seg_words[sr]
+                if group == POINT_TO_POINT:
+                    if self.is_local(sr):
+                        ss = self.ranks[sr]
+                        mir = ss.mirrors.setdefault(tr, _Bits(ss.device)).ensure(span[sr])
+                        seg = vb[w0: w0 + nw].to(ss.device)
+                        call("smx_bits_or", _ptr(mir.t), _ptr(seg), nw, ss.stream)
+                else:
+                    for mbr in members:
+                        if self.is_local(mbr):
+                            ms = self.ranks[mbr]
+                            ros = ms.rosters.setdefault((group, sr), _Bits(ms.device)).ensure(span[sr])
+                            seg = vb[w0: w0 + nw].to(ms.device)
+                            call("smx_bits_or", _ptr(ros.t), _ptr(seg), nw, ms.stream)
+        return n_created
+
+    def _present_ranks(self, vb, ranks_sorted, seg_words):
+        counts = []
+        for r in ranks_sorted:
+            w0, nw = seg_words[r]
+            counts.append(vb[w0: w0 + nw])
+        any_set = torch.stack([c.ne(0).any() for c in counts]).cpu().numpy()
+        return [r for r, a in zip(ranks_sorted, any_set) if a]
+
+    def _dist_tables(self, dev, stream, tr, total, all_rank, all_node, vbase, lut_base):
+        rk = torch.from_numpy(all_rank).to(dev)
+        nd = torch.from_numpy(all_node).to(dev)
+        vb = torch.from_numpy(vbase.astype(np.uint32).view(np.int32)).to(dev)
+        key_tab = torch.empty(total, dtype=torch.int32, device=dev)
+        gv_tab = torch.empty(total, dtype=torch.int32, device=dev)
+        call("smx_dist_tables", _ptr(rk), _ptr(nd), total, _ptr(vb), tr, lut_base, _ptr(key_tab),
+             _ptr(gv_tab), stream)
+        return key_tab, gv_tab, rk, nd
+
+    def _dist_target(self, st, key, tr, tg, k_in, total, all_rank, all_node, vbase, seg_words,
+                     total_words, syn, port, group, ranks_sorted):
+        dev, sk = st.device, st.stream
+        lut_base = st.lut.n
+        key_tab, gv_all, rk, nd = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)
+        vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
+        cls = self._syn_class(st, syn, port)
+        if cls is None:
+            self._make_wide(st)
+        tgt = torch.from_numpy(np.ascontiguousarray(tg)).to(dev)
+        pay_tab = torch.empty(len(tg), dtype=torch.int32, device=dev)
+        call("smx_pay_table", _ptr(tgt), len(tg), _ptr(st.node2row.t), st.node2row.n,
+             0 if cls is None else cls, _ptr(pay_tab), sk)
+        n = k_in * len(tg)
+        base = st.reserve_records(n)
+        vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
+        cur = np.zeros(1, dtype=np.uint64)
+        call("smx_gen_draw", key[0], key[1], 0, total, n, 1, 2, _ptr(key_tab), _ptr(pay_tab), k_in,
+             _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits), _ptr(gv_all), cur.ctypes.data, sk)
+        if st.wide:
+            self._write_syn(st, syn, port, base, n, None)
+        st.commit_records(n)
+        present = self._present_ranks(vbits, ranks_sorted, seg_words)
+        segs = []
+        for r in ranks_sorted:
+            sw0, snw = seg_words[r]
+            m = None
+            if r != tr and r in present:
+                m = st.map_for(group, r)
+                m.ensure(snw * 32)
+            segs.append((sw0, snw, m))
+        self._assign(st, vbits, segs)
+        # LUT over the concatenated value space: lut[base + gv] = img_of[rank][value]
+        st.lut.reserve(lut_base + total_words * 32)
+        for r in present:
+            if r == tr:
+                continue
+            sw0, snw = seg_words[r]
+            m = st.maps[(int(group), r)]
+            st.lut.t[lut_base + sw0 * 32: lut_base + (sw0 + snw) * 32].copy_(m.img_of.t[: snw * 32])
+        st.lut.n = lut_base + total_words * 32
+        return vbits, present
+
+    def _dist_replay(self, dev, key, tr, total, all_rank, all_node, vbase, total_words, n):
+        """Source-side replay of a remote target's draws: used-value bitmap only."""
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _, gv_all, _, _ = self._dist_tables(dev, stream, tr, total, all_rank, all_node, vbase, 0)
+        vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
+        cur = np.zeros(1, dtype=np.uint64)
+        call("smx_gen_draw", key[0], key[1], 0, total, n, 1, 0, 0, 0, 1, 0, 0, _ptr(vbits), _ptr(gv_all),
+             cur.ctypes.data, stream)
+        return vbits
+
+    # -------------------------------------------------------------- preparation
+    def prepare(self) -> None:
+        if self.prepared:
+            raise ConsistencyError("cluster already prepared")
+        self.phase = "preparation"
+        with self._timed("preparation"):
+            if not self.distributed:
+                gids = np.concatenate([g for st in self.ranks.values() for g in st.row_gid] or
+                                      [np.empty(0, np.int64)])
+                if len(np.unique(gids)) != len(gids):
+                    raise ConsistencyError("neuron gids must be globally unique")
+            for st in self.ranks.values():
+                self._prepare_rank(st)
+        self.has_p2p = self._compute_has_p2p()
+        self.group_ids = sorted(self.groups)
+        self.prepared = True
+
+    def _compute_has_p2p(self):
+        flags = [bool(st.mirrors) or any(k[0] == POINT_TO_POINT for k in st.maps) for st in self.ranks.values()]
+        val = any(flags)
+        if self.distributed:
+            return True if self.n_ranks > 1 and self.cfg.comm_mode == "p2p" else val
+        return val
+
+    def _prepare_rank(self, st: _Rank):
+        dev, sk = st.device, st.stream
+        dt = self.cfg.resolution_ms
+        n_nodes = st.n_nodes
+        # delays / ports in use (sm/construction.py:759-768)
+        max_delay, max_port = 1, 0
+        if st.wide:
+            mm = torch.zeros(2, dtype=torch.int32, device=dev)
+            call("smx_max_meta", _ptr(st.w_meta.t), st.w_meta.n, _ptr(mm), sk)
+            mm = mm.cpu().numpy()
+            max_delay, max_port = max(max_delay, int(mm[0])), max(max_port, int(mm[1]))
+        elif st.keys.n:
+            used = torch.unique(torch.bitwise_right_shift(st.vals.view(), 24) & 0xFF).cpu().numpy()
+            for c in used:
+                _, d, p = self.classes[int(c)]
+                max_delay, max_port = max(max_delay, d), max(max_port, p)
+        for d in st.devices:
+            max_delay, max_port = max(max_delay, d["delay"]), max(max_port, d["port"])
+        st.L = max(2, max_delay + 1)
+        st.P = 1 + max_port
+        # neuron state, real rows only (sm/dynamics.py:153-189)
+        N = st.n_real
+        st.N = N
+        prm = np.concatenate(st.row_param) if st.row_param else np.empty(0, np.int32)
+        tab = np.array([[math.exp(-dt / p.tau_m), p.v_rest, p.v_reset, p.v_th, p.i_e] for p in self.params] or
+                       [[0.0] * 5], dtype=np.float64)
+        rs = np.array([int(round(p.t_ref / dt)) for p in self.params] or [0], dtype=np.int32)
+        f64 = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        st.decay, st.v_rest, st.v_reset, st.v_th, st.i_e = (f64(tab[prm, j]) for j in range(5))
+        st.ref_steps = f64(rs[prm])
+        st.v = torch.cat(st.v0) if st.v0 else torch.empty(0, dtype=torch.float64, device=dev)
+        st.ref = torch.zeros(N, dtype=torch.int32, device=dev)
+        st.row2node_np = np.concatenate(st.row2node) if st.row2node else np.empty(0, np.int64)
+        st.row2node_t = torch.from_numpy(st.row2node_np.astype(np.int32)).to(dev)
+        st.gid_np = np.concatenate(st.row_gid) if st.row_gid else np.empty(0, np.int64)
+        st.gid_t = torch.from_numpy(st.gid_np).to(dev)
+        st.ring = torch.zeros(st.L * st.P * max(N, 1), dtype=torch.float64, device=dev)
+        # sort the store (sm/core.py:299-324)
+        n = st.keys.n
+        st.n_records = n
+        key_bits = max(1, int(n_nodes - 1).bit_length())
+        st.counts = torch.empty(max(n_nodes, 1), dtype=torch.int32, device=dev)
+        kb = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        vb = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        which = np.zeros(1, dtype=np.int32)
+        lut = st.lut.t
+        if n and n_nodes >= (1 << 31):
+            raise ValueError("more than 2^31 nodes on one rank")
+        call("smx_sort_records", _ptr(st.keys.t), _ptr(st.vals.t), _ptr(kb), _ptr(vb), n, key_bits,
+             1 if st.wide else 0, _ptr(lut), _ptr(st.counts), n_nodes, which.ctypes.data, sk)
+        sorted_vals = (vb if which[0] else st.vals.t)[:n]
+        st.first_index = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
+        call("smx_counts_to_offsets", _ptr(st.counts), n_nodes, _ptr(st.first_index), sk)
+        if n and int(st.first_index[-1].item()) != n:
+            raise ConsistencyError(f"record source beyond node count {n_nodes}")
+        if st.wide:
+            st.payload = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            st.ww = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+            st.wm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            call("smx_gather_wide", _ptr(sorted_vals), n, _ptr(st.w_rows.t), _ptr(st.w_w.t), _ptr(st.w_meta.t),
+                 _ptr(st.payload), _ptr(st.ww), _ptr(st.wm), sk)
+            st.w_rows = st.w_w = st.w_meta = None
+        else:
+            st.payload = sorted_vals.clone() if n else torch.empty(1, dtype=torch.int32, device=dev)
+            st.ww = st.wm = None
+        del kb, vb
+        st.keys = st.vals = None
+        st.cls_w, cm = self._class_tables(dev)
+        cmn = cm.cpu().numpy().view(np.uint32)
+        st.cls_delay = torch.from_numpy((cmn & ROW_MASK).astype(np.int32)).to(dev)
+        st.cls_port = torch.from_numpy((cmn >> 24).astype(np.int32)).to(dev)
+        # maps -> sorted (R, L) (sm/construction.py:183-242)
+        st.RL = {}
+        for key, m in st.maps.items():
+            st.RL[key] = self._compact(st, m.present.view(), m.img_of.view())
+        # mirrors -> S (source side of each p2p pair)
+        st.S = {tr: self._compact(st, b.t, None)[0] for tr, b in st.mirrors.items()}
+        # rosters -> H; image lookups I (sm/construction.py:780-803)
+        st.H, st.I = {}, {}
+        for key in sorted(st.rosters):
+            st.H[key] = self._compact(st, st.rosters[key].t, None)[0]
+        for key in sorted(st.H):
+            g, sr = key
+            if sr == st.rank:
+                continue
+            m = st.maps.get(key)
+            if m is not None:
+                rw = st.rosters[key].t
+                pw = m.present.view()
+                nw = min(rw.numel(), pw.numel())
+                extra = (pw[:nw] & ~rw[:nw]).ne(0).any() or pw[nw:].ne(0).any()
+                if bool(extra):
+                    raise ConsistencyError(f"rank {st.rank}: map keys for {key} missing from roster")
+                m.ensure(rw.numel() * 32)
+                st.I[key] = self._compact(st, rw, m.img_of.view())[1]
+            else:
+                st.I[key] = torch.full((st.H[key].numel(),), -1, dtype=torch.int64, device=dev)
+        # routing tables: T/P from mirrors (dest = target rank, ascending),
+        # G/Q from own rosters (dest = group slot, groups ascending)
+        self.group_slots = {g: i for i, g in enumerate(sorted(self.groups))}
+        st.TP = self._routes(st, [(tr, st.mirrors[tr].t) for tr in sorted(st.mirrors)])
+        own = [(self.group_slots[g], st.rosters[(g, sr)].t) for (g, sr) in sorted(st.rosters) if sr == st.rank]
+        st.GQ = self._routes(st, own)
+        # propagation buffers
+        self._alloc_propagation(st)
+        st.prepared = True
+
+    def _compact(self, st, bits, img_of):
+        nw = bits.numel()
+        excl = torch.empty(nw + 1, dtype=torch.int64, device=st.device)
+        call("smx_bits_prefix", _ptr(bits), nw, _ptr(excl), st.stream)
+        cnt = int(excl[-1].item())
+        vals = torch.empty(max(cnt, 1), dtype=torch.int64, device=st.device)
+        imgs = torch.empty(max(cnt, 1), dtype=torch.int64, device=st.device)
+        call("smx_bits_compact", _ptr(bits), nw, _ptr(excl), _ptr(vals), _ptr(img_of), _ptr(imgs), st.stream)
+        return vals[:cnt], imgs[:cnt]
+
+    def _routes(self, st, tables):
+        dev = st.device
+        n_nodes = st.n_nodes
+        arr = (ctypes_route * max(len(tables), 1))()
+        keep = []
+        for i, (dest, bits) in enumerate(tables):
+            excl = torch.empty(bits.numel() + 1, dtype=torch.int64, device=dev)
+            call("smx_bits_prefix", _ptr(bits), bits.numel(), _ptr(excl), st.stream)
+            keep.append(excl)
+            arr[i].bits = _ptr(bits)
+            arr[i].excl = _ptr(excl)
+            arr[i].nwords = bits.numel()
+            arr[i].dest = int(dest)
+        first = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
+        cnt = torch.empty(max(n_nodes, 1), dtype=torch.int32, device=dev)
+        ne = np.zeros(1, dtype=np.int64)
+        call("smx_build_routes", ctypes_addr(arr), len(tables), n_nodes, _ptr(cnt), _ptr(first), 0, 0,
+             ne.ctypes.data, st.stream)
+        ne = int(ne[0])
+        dest = torch.empty(max(ne, 1), dtype=torch.int32, device=dev)
+        pos = torch.empty(max(ne, 1), dtype=torch.int32, device=dev)
+        call("smx_build_routes", ctypes_addr(arr), len(tables), n_nodes, _ptr(cnt), _ptr(first), _ptr(dest),
+             _ptr(pos), ne.ctypes.data, st.stream)
+        return dict(first=first, dest=dest[:ne], pos=pos[:ne], n=ne)
+
+    def _alloc_propagation(self, st):
+        dev = st.device
+        N = st.N
+        st.spike_bits = torch.zeros(max(_words(N), 1), dtype=torch.int32, device=dev)
+        # packets: p2p buffers per destination rank, collective per group slot
+        st.pk_cap = max(N, 1)
+        st.p2p_packets = torch.zeros(self.n_ranks * st.pk_cap * 2, dtype=torch.int32, device=dev)
+        st.p2p_counts = torch.zeros(self.n_ranks, dtype=torch.int32, device=dev)
+        ng = max(len(self.groups), 1)
+        st.g_packets = torch.zeros(ng * st.pk_cap * 2, dtype=torch.int32, device=dev)
+        st.g_counts = torch.zeros(ng, dtype=torch.int32, device=dev)
+        st.src_cap = N + self.n_ranks * st.pk_cap + 16
+        st.src_nodes = torch.zeros(st.src_cap, dtype=torch.int32, device=dev)
+        st.src_steps = torch.zeros(st.src_cap, dtype=torch.int32, device=dev)
+        st.n_src = torch.zeros(1, dtype=torch.int32, device=dev)
+        st.wprefix = torch.zeros(st.src_cap, dtype=torch.int32, device=dev)
+        st.n_work = torch.zeros(1, dtype=torch.int32, device=dev)
+        st.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        st.rec_cap = 1 << 20
+        st.rec = torch.zeros(2 * st.rec_cap, dtype=torch.int64, device=dev)
+        st.n_rec = torch.zeros(1, dtype=torch.int64, device=dev)
+        st.spike_total = torch.zeros(1, dtype=torch.int32, device=dev)
+        st.recorded: list[np.ndarray] = []
+        st.p2p_desc = ctypes_routes_desc(st.TP, st.p2p_packets, st.p2p_counts, self.n_ranks, st.pk_cap)
+        st.g_desc = ctypes_routes_desc(st.GQ, st.g_packets, st.g_counts, len(self.groups), st.pk_cap)
+        # Poisson devices: counts generated in batches of S steps
+        st.pois_steps = 64
+        for d in st.devices:
+            nt = len(d["targets"])
+            rows = np.asarray(st_node2row_host(st, d["targets"]), dtype=np.int64)
+            if (rows < 0).any():
+                raise ValueError("poisson targets must be real neurons")
+            d["rows"] = torch.from_numpy(rows.astype(np.int32)).to(dev)
+            d["nt"] = nt
+            d["active"] = nt > 0 and d["lam"] != 0.0
+            if not d["active"]:
+                continue
+            S = st.pois_steps
+            d["counts"] = torch.zeros(S * nt, dtype=torch.uint8, device=dev)
+            d["cursor"] = torch.zeros(2, dtype=torch.int64, device=dev)
+            d["ping"] = 0
+            d["chunks"] = _lib.lib().smx_poisson_chunks_for(S * nt, d["lam"])
+            d["ws"] = torch.empty(int(_lib.lib().smx_poisson_workspace(d["chunks"])), dtype=torch.uint8,
+                                  device=dev)
+            d["batch0"] = -1
+
+    # -------------------------------------------------------------- propagation
+    def _poisson(self, st, now):
+        S = st.pois_steps
+        for d in st.devices:
+            if not d["active"]:
+                continue
+            b0 = now - now % S
+            if d["batch0"] != b0:
+                cin = d["cursor"][d["ping"]:]
+                cout = d["cursor"][1 - d["ping"]:]
+                call("smx_poisson_counts", d["key"][0], d["key"][1], _ptr(cin), d["enlam"], S * d["nt"],
+                     d["chunks"], _ptr(d["ws"]), _ptr(d["counts"]), _ptr(cout), _ptr(st.err), st.stream)
+                d["ping"] = 1 - d["ping"]
+                d["batch0"] = b0
+            slot = (now + d["delay"]) % st.L
+            off = (slot * st.P + d["port"]) * st.N
+            call("smx_poisson_emit", _ptr(d["counts"][(now - b0) * d["nt"]:]), d["nt"], _ptr(d["rows"]),
+                 d["weight"], _ptr(st.ring[off:]), st.stream)
+
+    def _deliver(self, st):
+        call("smx_deliver", _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), _ptr(st.wprefix),
+             _ptr(st.n_work), _ptr(st.first_index), _ptr(st.payload), _ptr(st.cls_w), _ptr(st.cls_delay),
+             _ptr(st.cls_port), _ptr(st.ww), _ptr(st.wm), _ptr(st.ring), st.N, st.P, st.L, 0, st.stream)
+
+    def step(self):
+        """sm/engine.py:277-310; returns nothing (spikes stay on the device)."""
+        if not self.prepared:
+            raise ConsistencyError("prepare() the cluster before stepping")
+        now = self.now
+        for st in self.ranks.values():
+            sk = st.stream
+            st.n_src.zero_()
+            st.p2p_counts.zero_()
+            st.g_counts.zero_()
+            call("smx_lif_update", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
+                 _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, now,
+                 _ptr(st.spike_bits), sk)
+            self._poisson(st, now)
+            call("smx_spikes", _ptr(st.spike_bits), st.N, _ptr(st.row2node_t), _ptr(st.gid_t), now,
+                 _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, 1 if self._recording else 0,
+                 _ptr(st.rec), _ptr(st.n_rec), st.rec_cap, _ptr(st.spike_total), _ptr(st.err),
+                 ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), sk)
+            self._deliver(st)
+        if self.n_ranks > 1:
+            self._exchange(now)
+        self.now += 1
+
+    def _exchange(self, now):
+        """One p2p round (if any p2p routing exists) then one allgather round
+        per group (sm/engine.py:297-308), as device-resident packet reads."""
+        if self.distributed:
+            return self._exchange_nccl(now)
+        for st in self.ranks.values():
+            st.n_src.zero_()
+        if self.has_p2p:
+            for st in self.ranks.values():
+                for sr in range(self.n_ranks):
+                    if sr == st.rank:
+                        continue
+                    src = self.ranks[sr]
+                    rl = st.RL.get((POINT_TO_POINT, sr))
+                    if rl is None:
+                        continue
+                    pk = src.p2p_packets[st.rank * src.pk_cap * 2:]
+                    cnt = src.p2p_counts[st.rank:]
+                    call("smx_unpack", _ptr(pk), _ptr(cnt), _ptr(rl[1]), rl[1].numel(), _ptr(st.src_nodes),
+                         _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
+            self.messages["propagation"] += self.n_ranks * (self.n_ranks - 1)
+        for g in self.group_ids:
+            slot = self.group_slots[g]
+            members = self.groups[g]
+            for m in members:
+                st = self.ranks[m]
+                for sr in sorted(members):
+                    if sr == m:
+                        continue
+                    lk = st.I.get((g, sr))
+                    if lk is None:
+                        continue
+                    src = self.ranks[sr]
+                    pk = src.g_packets[slot * src.pk_cap * 2:]
+                    cnt = src.g_counts[slot:]
+                    call("smx_unpack", _ptr(pk), _ptr(cnt), _ptr(lk), lk.numel(), _ptr(st.src_nodes),
+                         _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
+            self.messages["propagation"] += len(members)
+        for st in self.ranks.values():
+            self._deliver(st)
+
+    def _exchange_nccl(self, now):
+        raise NotImplementedError("multi-process exchange is set up by engine_dist")
+
+    _recording = False
+
+    def simulate(self, warmup_ms: float = 0.0, model_ms: float = 0.0, record: bool = True) -> RunReport:
+        """sm/engine.py:312-359.  RTF = propagation wall time / model time, the
+        wall time bracketed by device synchronisations."""
+        if not self.prepared:
+            self.prepare()
+        warm = self.cfg.steps_for(warmup_ms)
+        steps = self.cfg.steps_for(model_ms)
+        self.phase = "propagation"
+        self._recording = False
+        self._sync()
+        t0 = time.perf_counter()
+        for _ in range(warm):
+            self.step()
+        self._sync()
+        warm_s = time.perf_counter() - t0
+        self._recording = record
+        t1 = time.perf_counter()
+        for _ in range(steps):
+            self.step()
+        self._sync()
+        prop = time.perf_counter() - t1
+        self._recording = False
+        self.timers.propagation += prop
+        self._check_errors()
+        model_s = steps * self.cfg.resolution_ms * 1e-3
+        raster = self.merged_raster() if record else None
+        return RunReport(
+            n_ranks=self.n_ranks, comm_mode=self.cfg.comm_mode, opt_level=self.cfg.opt_level,
+            seed=self.cfg.seed, kernel_backend="cuda-sm_100a",
+            n_neurons=sum(st.n_real for st in self.ranks.values()),
+            n_synapses=sum(st.n_records for st in self.ranks.values()),
+            timers=self.timers.as_dict(), warmup_s=warm_s, model_time_s=model_s,
+            rtf=prop / model_s if model_s > 0 else 0.0,
+            host_peak_bytes=[0] * self.n_ranks, device_peak_bytes=[0] * self.n_ranks,
+            transport_messages=dict(self.messages), transport_bytes=dict(self.bytes),
+            n_spike_events=raster.n_events if raster is not None else 0,
+            raster_sha256=raster.sha256() if raster is not None else None)
+
+    def _sync(self):
+        for st in self.ranks.values():
+            torch.cuda.synchronize(st.device)
+
+    def _check_errors(self):
+        for st in self.ranks.values():
+            e = int(st.err.item())
+            if e:
+                raise ProtocolError(f"rank {st.rank}: device error code {e} during propagation")
+
+    # -------------------------------------------------------------- inspection
+    def rank_events(self, rank) -> np.ndarray:
+        st = self.ranks[rank]
+        n = int(st.n_rec.item())
+        return st.rec[: 2 * n].view(-1, 2).cpu().numpy()
+
+    def merged_raster(self) -> Raster:
+        parts = [self.rank_events(r) for r in self.ranks]
+        ev = np.concatenate(parts) if parts else np.empty((0, 2), np.int64)
+        return Raster.from_events(ev, self.cfg.resolution_ms)
+
+    def check_construction_silent(self) -> None:
+        for phase in ("construction", "preparation"):
+            if self.messages[phase] or self.bytes[phase]:
+                raise ConsistencyError(f"transport was used during {phase}")
+
+    def check_alignment(self) -> None:
+        """sm/engine.py:378-399: mirrors S equal map keys R for every p2p pair."""
+        if not self.prepared:
+            raise ConsistencyError("prepare() first")
+        for tr, st in self.ranks.items():
+            for (g, sr), rl in st.RL.items():
+                if g != POINT_TO_POINT or sr not in self.ranks:
+                    continue
+                s = self.ranks[sr].S.get(tr)
+                if s is None or not torch.equal(s.cpu(), rl[0].cpu()):
+                    raise ConsistencyError(f"mirror of rank {sr} for rank {tr} does not match the map keys")
+        for sr, ss in self.ranks.items():
+            for tr, s in ss.S.items():
+                if tr not in self.ranks:
+                    continue
+                rl = self.ranks[tr].RL.get((POINT_TO_POINT, sr))
+                if rl is None or not torch.equal(s.cpu(), rl[0].cpu()):
+                    raise ConsistencyError(f"map of rank {tr} for source rank {sr} does not match the mirror")
+
+    def export(self, rank) -> dict:
+        """Every table of one rank as numpy arrays, in the reference's terms:
+        store columns sorted by source, first_index, (R, L) per map, mirrors
+        S, rosters H, lookups I, routes T/P and G/Q, neuron state."""
+        st = self.ranks[rank]
+        fi = st.first_index.cpu().numpy()
+        n = st.n_records
+        src = np.repeat(np.arange(st.n_nodes, dtype=np.int64), np.diff(fi))
+        pay = st.payload[:n].cpu().numpy().view(np.uint32).astype(np.int64)
+        if st.ww is not None:
+            rows = pay
+            w = st.ww[:n].cpu().numpy()
+            meta = st.wm[:n].cpu().numpy().view(np.uint32).astype(np.int64)
+            delay, port = meta & ROW_MASK, meta >> 24
+        else:
+            rows = pay & ROW_MASK
+            cls = pay >> 24
+            ctab = np.array(self.classes or [(0.0, 0, 0)], dtype=object)
+            w = np.array([self.classes[c][0] for c in range(len(self.classes))] or [0.0])[cls]
+            delay = np.array([c[1] for c in self.classes] or [0], dtype=np.int64)[cls]
+            port = np.array([c[2] for c in self.classes] or [0], dtype=np.int64)[cls]
+            del ctab
+        tgt = st.row2node_np[rows] if n else np.empty(0, np.int64)
+        out = dict(src=src, tgt=tgt, weight=np.asarray(w, dtype=np.float64), delay=delay, port=port,
+                   first_index=fi, n_nodes=st.n_nodes)
+        out["maps"] = {k: (v[0].cpu().numpy(), v[1].cpu().numpy()) for k, v in st.RL.items()}
+        out["mirrors"] = {k: v.cpu().numpy() for k, v in st.S.items()}
+        out["rosters"] = {k: v.cpu().numpy() for k, v in st.H.items()}
+        out["lookups"] = {k: v.cpu().numpy() for k, v in st.I.items()}
+        inv_slot = {v: k for k, v in self.group_slots.items()}
+        for name, tab, mapper in (("point_routes", st.TP, lambda d: d), ("group_routes", st.GQ, lambda d: inv_slot[d])):
+            f = tab["first"].cpu().numpy()
+            dst = tab["dest"].cpu().numpy()
+            pos = tab["pos"].cpu().numpy().view(np.uint32).astype(np.int64)
+            routes = {}
+            for s in np.flatnonzero(np.diff(f)):
+                a, b = f[s], f[s + 1]
+                routes[int(s)] = (np.array([mapper(int(x)) for x in dst[a:b]], dtype=np.int64), pos[a:b])
+            out[name] = routes
+        out["v"] = st.v.cpu().numpy()
+        out["ref"] = st.ref.cpu().numpy()
+        out["gid"] = st.gid_np
+        out["row2node"] = st.row2node_np
+        return out
+
+
+def st_node2row_host(st: _Rank, nodes: np.ndarray) -> np.ndarray:
+    n2r = np.full(st.n_nodes, -1, dtype=np.int64)
+    if st.row2node:
+        r2n = np.concatenate(st.row2node)
+        n2r[r2n] = np.arange(len(r2n))
+    return n2r[np.asarray(nodes, dtype=np.int64)]
+
+
+# ---------------------------------------------------------------- ctypes structs
+import ctypes  # noqa: E402
+
+
+class ctypes_segment(ctypes.Structure):
+    _fields_ = [("word0", ctypes.c_uint64), ("nwords", ctypes.c_uint64),
+                ("present", ctypes.c_void_p), ("img_of", ctypes.c_void_p)]
+
+
+class ctypes_route(ctypes.Structure):
+    _fields_ = [("bits", ctypes.c_void_p), ("excl", ctypes.c_void_p), ("nwords", ctypes.c_uint64),
+                ("dest", ctypes.c_int32)]
+
+
+class ctypes_routes(ctypes.Structure):
+    _fields_ = [("first", ctypes.c_void_p), ("dest", ctypes.c_void_p), ("pos", ctypes.c_void_p),
+                ("n_dest", ctypes.c_int), ("packets", ctypes.c_void_p), ("counts", ctypes.c_void_p),
+                ("cap", ctypes.c_uint32)]
+
+
+def ctypes_routes_desc(tab, packets, counts, n_dest, cap):
+    d = ctypes_routes()
+    d.first = _ptr(tab["first"])
+    d.dest = _ptr(tab["dest"])
+    d.pos = _ptr(tab["pos"])
+    d.n_dest = int(n_dest) if tab["n"] else 0
+    d.packets = _ptr(packets)
+    d.counts = _ptr(counts)
+    d.cap = int(cap)
+    return d
+
+
+def ctypes_addr(obj) -> int:
+    return ctypes.addressof(obj)

@@ -1,0 +1,93 @@
+"""Generate the golden fixtures from the REFERENCE itself.
+
+Runs in the build container only (it imports /root/reference/pkg/src, which
+does not exist on the GPU box); the outputs are committed:
+  tests/golden/rng.npz           raw Philox words, integers (with rejections
+                                 and continued cursors), normals, poisson
+                                 chains, per-gid init-v -- numpy 2.3.5
+  tests/golden/tables_<name>.npz per-rank construction tables of each
+                                 scenario in tests/scenarios.py
+  tests/golden/rasters.json      raster SHA-256 / event counts per scenario
+Usage:  python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+from types import SimpleNamespace
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+sys.path.insert(0, os.path.dirname(HERE))
+os.environ["SPIKEMESH_PURE_PYTHON"] = "1"
+
+import spikemesh as sm  # noqa: E402
+from spikemesh import models as smm  # noqa: E402
+
+import scenarios  # noqa: E402
+import tables  # noqa: E402
+
+
+def ref_namespace():
+    return SimpleNamespace(
+        SimConfig=sm.SimConfig, make_cluster=sm.Cluster, ConnSpec=sm.ConnSpec, SynSpec=sm.SynSpec,
+        LifParams=sm.LifParams, build_balanced_network=smm.build_balanced_network,
+        BalancedParams=smm.BalancedParams, ExplicitNetwork=smm.ExplicitNetwork,
+        build_multi_area=smm.build_multi_area, AreaSpec=smm.AreaSpec, pack_areas=smm.pack_areas,
+        MultiAreaParams=smm.MultiAreaParams)
+
+
+def gen_rng():
+    assert np.__version__ == "2.3.5", np.__version__
+    out = {}
+    streams = [(7, ("dist-indegree", 1, 0)), (12345, ("conn-local", 0, 3)), (11, ("init-v", 42))]
+    for i, (seed, sid) in enumerate(streams):
+        st = sm.RngStream(seed, sid)
+        k = st._key
+        out[f"s{i}/key"] = np.array([k & (2**64 - 1), k >> 64], dtype=np.uint64)
+        out[f"s{i}/words"] = sm.RngStream(seed, sid).gen.bit_generator.random_raw(64).astype(np.uint64)
+        g = sm.RngStream(seed, sid)
+        # integers with continued cursors, odd lengths (buffered high half),
+        # ranges with many rejections (ex = 3e9) and ex = 1 (no draws)
+        seq = [(0, 36, 101), (0, 640000, 1001), (5, 3_000_000_005, 777), (0, 1, 9), (0, 2**32, 33),
+               (1, 21, 500), (0, 8000, 2048)]
+        for j, (lo, hi, n) in enumerate(seq):
+            out[f"s{i}/int{j}"] = g.integers(lo, hi, size=n)
+            out[f"s{i}/int{j}/spec"] = np.array([lo, hi, n], dtype=np.int64)
+        out[f"s{i}/normal"] = sm.RngStream(seed, sid).normal(-58.0, 5.0, size=4000)
+        out[f"s{i}/poisson"] = sm.RngStream(seed, sid).poisson(1.1, size=20000)
+        p = sm.RngStream(seed, sid)
+        out[f"s{i}/poisson_steps"] = np.stack([p.poisson(1.1, size=333) for _ in range(20)])
+    gids = np.array([0, 1, 2, 7, 99, 1000, 12345, 99999, 4_000_000, 2**40 + 3], dtype=np.int64)
+    out["initv/gids"] = gids
+    out["initv/seed11"] = np.array([sm.RngStream(11, ("init-v", int(g))).normal(-58.0, 5.0) for g in gids])
+    out["initv/seed12345"] = np.array([sm.RngStream(12345, ("init-v", int(g))).normal(-58.0, 5.0) for g in gids])
+    np.savez_compressed(os.path.join(HERE, "rng.npz"), **out)
+
+
+def gen_tables():
+    ns = ref_namespace()
+    rasters = {}
+    for name, fn in scenarios.SCENARIOS.items():
+        c, sim = fn(ns)
+        c.prepare()
+        t = tables.canon_reference(c)
+        np.savez_compressed(os.path.join(HERE, f"tables_{name}.npz"), **t)
+        if sim is not None:
+            rep = c.simulate(sim[0], sim[1], record=True)
+            rasters[name] = dict(sha256=rep.raster_sha256, n_events=rep.n_spike_events,
+                                 warmup_ms=sim[0], model_ms=sim[1])
+        print(name, "records", sum(len(st.store.src) for st in c.ranks), rasters.get(name), file=sys.stderr)
+    with open(os.path.join(HERE, "rasters.json"), "w") as fh:
+        json.dump(rasters, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    gen_rng()
+    gen_tables()

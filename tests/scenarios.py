@@ -1,0 +1,116 @@
+"""Construction scenarios shared by the golden-fixture generator (reference),
+the oracle tests (CPU) and the parity tests (GPU).
+
+Each scenario takes a namespace `ns` with the façade classes (Cluster,
+SimConfig, ConnSpec, SynSpec, LifParams) and the model builders, builds a
+network, and returns (cluster, sim) where sim = (warmup_ms, model_ms) or
+None (tables only).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def balanced(ns, n_ranks, mode, per_rank, k_exc, k_inh, seed, sim=(0.0, 20.0), **kw):
+    cfg = ns.SimConfig(n_ranks=n_ranks, comm_mode=mode, seed=seed)
+    c = ns.make_cluster(cfg)
+    ns.build_balanced_network(c, ns.BalancedParams(neurons_per_rank=per_rank, k_exc=k_exc, k_inh=k_inh, **kw))
+    return c, sim
+
+
+def explicit(ns, n_ranks, mode, n_neurons=300, n_edges=6000, net_seed=5, seed=11, sim=(0.0, 30.0)):
+    net = ns.ExplicitNetwork.generate(n_neurons, n_edges, seed=net_seed)
+    cfg = ns.SimConfig(n_ranks=n_ranks, comm_mode=mode, seed=seed)
+    c = ns.make_cluster(cfg)
+    rank_of = np.arange(n_neurons) % n_ranks if n_ranks > 1 else np.zeros(n_neurons, dtype=np.int64)
+    net.instantiate(c, rank_of)
+    return c, sim
+
+
+def rules_local(ns, seed=3):
+    """Every connection rule on one rank with constant syn (packed tables)."""
+    cfg = ns.SimConfig(n_ranks=1, seed=seed)
+    c = ns.make_cluster(cfg)
+    a = c.create_neurons(0, 40, ns.LifParams(), ("normal", -60.0, 3.0), gids=np.arange(40))
+    b = c.create_neurons(0, 25, ns.LifParams(i_e=0.5), -62.5, gids=np.arange(40, 65))
+    A = np.arange(a.start, a.stop)
+    B = np.arange(b.start, b.stop)
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    c.connect(0, A, B, S("fixed_indegree", k_in=7), Sy(0.25, 3))
+    c.connect(0, B, A, S("fixed_total", n_total=333), Sy(-0.5, 2))
+    c.connect(0, A[:25], B, S("one_to_one"), Sy(0.125, 1))
+    c.connect(0, B[:5], A[:7], S("all_to_all"), Sy(0.0625, 4))
+    c.connect(0, A[3:9], B, S("fixed_outdegree", k_out=6), Sy(0.5, 5))
+    c.connect(0, A[[1, 1, 5]], B[[2, 3, 2]], S("assigned"), Sy(1.0, 6), port=1)
+    c.connect(0, A, A, S("fixed_indegree", k_in=1), Sy(0.25, 3))   # single-source draws
+    c.connect(0, A[:1], B, S("fixed_indegree", k_in=2), Sy(0.25, 3))  # ex == 1: no draws
+    return c, (0.0, 5.0)
+
+
+def rules_wide(ns, seed=4):
+    """Per-record weight / delay arrays (wide tables)."""
+    cfg = ns.SimConfig(n_ranks=1, seed=seed)
+    c = ns.make_cluster(cfg)
+    a = c.create_neurons(0, 30, ns.LifParams(i_e=0.375), ("normal", -60.0, 3.0), gids=np.arange(30))
+    A = np.arange(a.start, a.stop)
+    rng = np.random.default_rng(1)
+    src = rng.integers(0, 30, 500)
+    tgt = rng.integers(0, 30, 500)
+    w = rng.integers(-64, 65, 500) / 256.0
+    d = rng.integers(1, 9, 500)
+    c.connect(0, A[src], A[tgt], ns.ConnSpec("assigned"), ns.SynSpec(w, d))
+    c.connect(0, A, A, ns.ConnSpec("fixed_indegree", k_in=3), ns.SynSpec(0.5, 2))
+    return c, (0.0, 5.0)
+
+
+def remote_mix(ns, mode="p2p", seed=9):
+    """Remote connections of every rule across 3 ranks, sparse (flagged) and
+    dense (unflagged), p2p or collective."""
+    cfg = ns.SimConfig(n_ranks=3, comm_mode=mode, seed=seed)
+    c = ns.make_cluster(cfg)
+    group = -1
+    if mode == "collective":
+        group = 0
+        c.declare_group(0, [0, 1, 2])
+    pops = []
+    for r in range(3):
+        x = c.create_neurons(r, 50, ns.LifParams(), ("normal", -58.0, 4.0), gids=r * 50 + np.arange(50))
+        pops.append(np.arange(x.start, x.stop))
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    c.connect_remote(0, pops[0], 1, pops[1][:3], S("fixed_indegree", k_in=4), Sy(0.25, 2), group=group)   # flagged
+    c.connect_remote(0, pops[0], 1, pops[1], S("fixed_indegree", k_in=5), Sy(0.125, 3), group=group)      # dense
+    c.connect_remote(1, pops[1][10:40], 2, pops[2], S("fixed_total", n_total=12), Sy(0.5, 2), group=group)  # flagged
+    c.connect_remote(2, pops[2][:20], 0, pops[0][:20], S("one_to_one"), Sy(0.25, 1), group=group)
+    c.connect_remote(2, pops[2][5:9], 1, pops[1][:6], S("all_to_all"), Sy(-0.25, 4), group=group)
+    c.connect_remote(1, pops[1][:4], 0, pops[0], S("fixed_outdegree", k_out=9), Sy(0.125, 2), group=group)
+    c.connect_remote(0, pops[0][[7, 3, 7]], 2, pops[2][[1, 2, 3]], S("assigned"), Sy(0.75, 3), group=group)
+    c.connect_remote(0, pops[0], 1, pops[1][5:9], S("fixed_indegree", k_in=2), Sy(0.25, 2), group=group)  # flagged again
+    for r in range(3):
+        c.connect(r, pops[r], pops[r], S("fixed_indegree", k_in=6), Sy(0.0625, 2))
+        c.add_poisson_source(r, 16000.0, 0.25, 2, pops[r])
+    return c, (0.0, 10.0)
+
+
+def multi_area(ns, n_ranks=2, mode="p2p", seed=21):
+    areas = [ns.AreaSpec(f"A{i}", 120 + 10 * i, 1000 * (i + 1)) for i in range(4)]
+    assign, _ = ns.pack_areas(areas, n_ranks)
+    cfg = ns.SimConfig(n_ranks=n_ranks, comm_mode=mode, seed=seed)
+    c = ns.make_cluster(cfg)
+    ns.build_multi_area(c, areas, assign, ns.MultiAreaParams(k_intra_exc=12, k_intra_inh=3, k_inter=4))
+    return c, (0.0, 10.0)
+
+
+SCENARIOS = {
+    "balanced_1r": lambda ns: balanced(ns, 1, "p2p", 400, 32, 8, 12345, sim=(0.0, 30.0)),
+    "balanced_4r_p2p": lambda ns: balanced(ns, 4, "p2p", 200, 16, 4, 7, sim=(0.0, 20.0)),
+    "balanced_4r_coll": lambda ns: balanced(ns, 4, "collective", 200, 16, 4, 7, sim=(0.0, 20.0)),
+    "balanced_2r_sparse_coll": lambda ns: balanced(ns, 2, "collective", 300, 3, 1, 17, sim=(0.0, 10.0)),
+    "rules_local": rules_local,
+    "rules_wide": rules_wide,
+    "remote_p2p": lambda ns: remote_mix(ns, "p2p"),
+    "remote_coll": lambda ns: remote_mix(ns, "collective"),
+    "explicit_1r": lambda ns: explicit(ns, 1, "p2p"),
+    "explicit_3r_p2p": lambda ns: explicit(ns, 3, "p2p"),
+    "explicit_3r_coll": lambda ns: explicit(ns, 3, "collective"),
+    "multi_area_2r": lambda ns: multi_area(ns, 2, "p2p"),
+}

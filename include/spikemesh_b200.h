@@ -1,0 +1,142 @@
+/*
+ * spikemesh-b200 C ABI -- the drop-in boundary of the sm_100a construction
+ * and propagation path of arXiv 2512.09502 (reference package `spikemesh`
+ * 0.1.0, cited as sm/<file>:<line> = /root/reference/pkg/src/spikemesh/...).
+ *
+ * Conventions
+ *   - every function is `extern "C"`, takes plain pointers and sizes, and
+ *     returns an int status: 0 ok, -1 ValueError, -2 ConsistencyError,
+ *     -3 CUDA error, -4 ProtocolError, -5 DelayRangeError (the reference's
+ *     exception classes, sm/core.py:39-52); smx_last_error() has the text;
+ *   - pointers are DEVICE pointers unless named *_host; `stream` is a
+ *     cudaStream_t (pass 0 for the legacy default stream);
+ *   - stream keys are the two Philox key words (k0, k1) of
+ *     RngStream(seed, stream_id) (sm/core.py:119-126): k0 | k1 << 64 =
+ *     int.from_bytes(blake2b(canonical_bytes((seed, stream_id)), 16), "little");
+ *   - u32 cursors count 32-bit draws consumed from the start of a stream
+ *     (numpy's next_uint32 buffering), word cursors count 64-bit words.
+ * Library: paper_2512_09502_b200/_build/libspikemesh_b200.so
+ */
+#ifndef SPIKEMESH_B200_H
+#define SPIKEMESH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* --- plumbing ------------------------------------------------------------ */
+int smx_last_error(char* buf, size_t cap);
+const char* smx_version(void);
+int smx_stream_sync(void* stream);
+
+/* --- keyed streams (numpy 2.3.5 Generator(Philox) semantics) -------------
+ * Replaces RngStream (sm/core.py:110-148) draws made by the construction
+ * path: integers at sm/construction.py:169,402,406,426,430,527,679 and
+ * sm/models.py:175-178; normal at :160,:362; poisson at sm/dynamics.py:233. */
+int smx_philox_words(uint64_t k0, uint64_t k1, uint64_t w0, uint64_t n, uint64_t* out, void* stream);
+/* Generator.integers(lo, lo+ex, size=n) (int64) from u32 cursor; ex in [1, 2^32]. */
+int smx_integers(uint64_t k0, uint64_t k1, uint64_t u32_cursor, int64_t lo, uint64_t ex, uint64_t n,
+                 int64_t* out, uint64_t* cursor_out_host, void* stream);
+/* v[i] = RngStream(seed, (..., gids[i])).normal(mu, sd), canonical bytes of the
+ * stream id = prefix + decimal(gid) + suffix (sm/construction.py:361-365). */
+int smx_init_v(const uint8_t* prefix_host, uint32_t plen, const uint8_t* suffix_host, uint32_t slen,
+               const int64_t* gids, uint64_t n, double mu, double sd, double* v_out, void* stream);
+int smx_stream_keys(const uint8_t* prefix_host, uint32_t plen, const uint8_t* suffix_host, uint32_t slen,
+                    const int64_t* ids, uint64_t n, uint64_t* keys_out, void* stream);
+/* Generator.poisson(lam < 10, size=n) from the word cursor *cursor_in;
+ * writes the cursor after the last sample to *cursor_out (no host sync).
+ * Workspace: smx_poisson_workspace(smx_poisson_chunks_for(n, lam)) bytes. */
+uint64_t smx_poisson_workspace(int n_chunks);
+int smx_poisson_chunks_for(uint64_t n, double lam);
+int smx_poisson_counts(uint64_t k0, uint64_t k1, const uint64_t* cursor_in, double enlam, uint64_t n,
+                       int n_chunks, void* workspace, uint8_t* counts, uint64_t* cursor_out, int* err,
+                       void* stream);
+
+/* --- construction ---------------------------------------------------------
+ * Replaces sm/construction.py:391-703 (rule realization, flag/extract,
+ * image maps, remap) and ConnectionStore.append_batch (sm/core.py:257-293).
+ * Pending records are (u32 key, u32 payload): key = source node, or
+ * 0x80000000 | lut index for remote-call records whose image ids are
+ * assigned after generation; payload = target row | syn class << 24. */
+int smx_pay_table(const int64_t* targets, uint64_t n, const int32_t* node2row, uint64_t n_nodes, uint32_t cls,
+                  uint32_t* pay_tab, void* stream);
+int smx_key_table(const int64_t* sources, uint64_t n, uint32_t tmp_base, int tmp, uint32_t* key_tab, void* stream);
+int smx_dist_tables(const int32_t* src_rank, const int64_t* src_node, uint64_t total, const uint32_t* vbase,
+                    int tgt_rank, uint32_t lut_base, uint32_t* key_tab, uint32_t* gv_tab, void* stream);
+/* One Generator.integers(0, ex, size=n) draw routed into pending records:
+ * key_mode 0 none / 1 key_tab[value] / 2 key_tab[j / kdiv];
+ * pay_mode 0 none / 1 pay_tab[value] / 2 pay_tab[j / kdiv];
+ * used_bits (optional) marks bit used_tab ? used_tab[value] : value. */
+int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u32_cursor, uint64_t ex, uint64_t n, int key_mode,
+                 int pay_mode, const uint32_t* key_tab, const uint32_t* pay_tab, uint32_t kdiv, uint32_t* keys,
+                 uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab, uint64_t* cursor_out_host,
+                 void* stream);
+/* one_to_one / assigned (mode 0), all_to_all (mode 1): sm/construction.py:415-419 */
+int smx_gen_pairs(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab, const uint32_t* pay_tab,
+                  uint32_t* keys, uint32_t* vals, void* stream);
+/* used_flags + extract_used (sm/construction.py:454-470) as a value bitmap */
+int smx_mark_values(const uint32_t* pos_bits, const int64_t* sources, uint64_t n, uint32_t* vbits, void* stream);
+/* lookup_or_create_images + RemoteSourceMap.insert (sm/construction.py:473-486,
+ * 227-236); segs_host: array of {u64 word0, u64 nwords, u32* present, i32* img_of}. */
+int smx_assign_images(const uint32_t* vbits, uint64_t nwords, const void* segs_host, int n_segs, int64_t m0,
+                      int64_t* n_new_host, void* stream);
+/* remap_connection_sources (sm/construction.py:489-495) via the key LUT */
+int smx_gather_lut(const int64_t* sources, uint64_t n, const int32_t* img_of, uint32_t* lut, void* stream);
+/* mirror_merge / roster update (sm/construction.py:295-306, 633-636) */
+int smx_bits_or(uint32_t* dst, const uint32_t* src, uint64_t nwords, void* stream);
+int smx_bits_prefix(const uint32_t* bits, uint64_t nwords, int64_t* excl, void* stream);
+int smx_bits_compact(const uint32_t* bits, uint64_t nwords, const int64_t* excl, int64_t* out,
+                     const int32_t* img_of, int64_t* img_out, void* stream);
+int smx_fill_wide_const(double* w, uint32_t* meta, uint64_t n, double wv, uint32_t mv, void* stream);
+int smx_promote_wide(const uint32_t* vals, uint64_t n, const double* cls_w, const uint32_t* cls_meta,
+                     uint32_t* rows, double* w, uint32_t* meta, void* stream);
+
+/* --- preparation (sm/construction.py:742-807, sm/core.py:299-324) ---------- */
+/* ConnectionStore.finalize: stable sort of pending records by source. */
+int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, uint64_t n,
+                     int key_bits, int index_values, const uint32_t* lut, uint32_t* counts, uint64_t n_keys,
+                     int* out_in_b_host, void* stream);
+/* first_index = exclusive scan of per-source counts (np.add.at + np.cumsum) */
+int smx_counts_to_offsets(const uint32_t* counts, uint64_t n, int64_t* first_index, void* stream);
+int smx_gather_wide(const uint32_t* idx, uint64_t n, const uint32_t* rows_in, const double* w_in,
+                    const uint32_t* meta_in, uint32_t* rows, double* w, uint32_t* meta, void* stream);
+int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out2, void* stream);
+/* _build_point_routes / _build_group_routes (sm/construction.py:710-739);
+ * tabs_host: array of {u32* bits, i64* excl, u64 nwords, i32 dest}. */
+int smx_build_routes(const void* tabs_host, int nt, uint64_t n_nodes, uint32_t* cnt_scratch, int64_t* first,
+                     int32_t* dest, uint32_t* pos, int64_t* n_entries_host, void* stream);
+
+/* --- propagation (sm/engine.py:277-310) ----------------------------------- */
+/* consume_inputs + kernels.lif_step (sm/dynamics.py:191-204,
+ * kernels/_speedups.pyx:13-35) on real rows; ring is [L][P][n] fp64. */
+int smx_lif_update(double* v, int32_t* ref, const double* decay, const double* v_rest, const double* v_reset,
+                   const double* v_th, const int32_t* ref_steps, const double* i_e, uint32_t n, double* ring,
+                   int n_ports, int L, int64_t now, uint32_t* spike_bits, void* stream);
+/* PoissonSource.emit_into (sm/dynamics.py:235-248) from precomputed counts */
+int smx_poisson_emit(const uint8_t* counts, uint32_t n_t, const uint32_t* rows, double w, double* ring_slot_port,
+                     void* stream);
+/* flatnonzero + recorder + route_point_spikes / route_group_spikes
+ * (sm/engine.py:89-128); p2p/grp: {i64* first, i32* dest, u32* pos, int n_dest,
+ * u32* packets, u32* counts, u32 cap} (host structs). */
+int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uint32_t* row2node, const int64_t* gid,
+               int64_t now, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap,
+               int record, int64_t* rec, uint64_t* n_rec, uint64_t rec_cap, uint32_t* spike_count, int* overflow,
+               const void* p2p_host, const void* grp_host, void* stream);
+/* deliver_point_packets / deliver_gather_packets (sm/engine.py:146-190) */
+int smx_unpack(const uint32_t* packets, const uint32_t* count, const int64_t* table, uint64_t table_len,
+               uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err, void* stream);
+/* kernels.deliver_spikes (kernels/_speedups.pyx:38-54) over a device list of
+ * (source node, emission step); packed (cls_*) or wide (wide_w/wide_meta). */
+int smx_deliver(const uint32_t* src_nodes, const uint32_t* src_steps, const uint32_t* n_src, uint32_t* wprefix,
+                uint32_t* n_work, const int64_t* first, const uint32_t* payload, const double* cls_w,
+                const uint32_t* cls_delay, const uint32_t* cls_port, const double* wide_w,
+                const uint32_t* wide_meta, double* ring, uint32_t n_rows, int n_ports, int L, int grid,
+                void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPIKEMESH_B200_H */

@@ -970,14 +970,14 @@ class Cluster:
             arr[i].dest = int(dest)
         first = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
         cnt = torch.empty(max(n_nodes, 1), dtype=torch.int32, device=dev)
-        ne = np.zeros(1, dtype=np.int64)
+        ne_h = np.zeros(1, dtype=np.int64)
         call("smx_build_routes", ctypes_addr(arr), len(tables), n_nodes, _ptr(cnt), _ptr(first), 0, 0,
-             ne.ctypes.data, st.stream)
-        ne = int(ne[0])
+             ne_h.ctypes.data, st.stream)
+        ne = int(ne_h[0])
         dest = torch.empty(max(ne, 1), dtype=torch.int32, device=dev)
         pos = torch.empty(max(ne, 1), dtype=torch.int32, device=dev)
         call("smx_build_routes", ctypes_addr(arr), len(tables), n_nodes, _ptr(cnt), _ptr(first), _ptr(dest),
-             _ptr(pos), ne.ctypes.data, st.stream)
+             _ptr(pos), ne_h.ctypes.data, st.stream)
         return dict(first=first, dest=dest[:ne], pos=pos[:ne], n=ne)
 
     def _alloc_propagation(self, st):

@@ -1,0 +1,285 @@
+"""Benchmark: the hpc_benchmark weak-scaling network (BASELINE.json configs[2],
+SURVEY.md §8 C3) on N B200s -- construction throughput (synapses/s, the
+headline `value`) and the propagation real-time factor.
+
+One "step" is one complete construction of the network through the public
+façade: create neurons (per-gid initial V), attach the Poisson drive, two
+distributed fixed in-degree projections (E then I), prepare (stable sort by
+source, first-index, image maps, rosters, routes).  Per GPU: 1e5 neurons
+(80,000 E + 20,000 I), K = 11,250 (9,000 + 2,250) -> 1.125e9 synapses.
+Collective spike exchange (group 0 over all ranks) when N > 1.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]  (N > 1 under
+torchrun, one rank per GPU, NCCL).  --impl reference times the CPU oracle
+port (the reference's algorithm restated in numpy + the numpy-exact RNG in
+C, oracle/) on a bounded sample on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import gc
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_PEAK_FALLBACK = 6650.0
+BYTES_PER_SYN = 20.0  # BASELINE.md §4 / SURVEY §8(d): generation + sort, constant syn
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--neurons", type=int, default=100_000)
+    ap.add_argument("--k-exc", type=int, default=9_000)
+    ap.add_argument("--k-inh", type=int, default=2_250)
+    ap.add_argument("--model-ms", type=float, default=100.0)
+    ap.add_argument("--prop-warmup-ms", type=float, default=20.0)
+    ap.add_argument("--seed", type=int, default=12345)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-neurons", type=int, default=10_000)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_PEAK_FALLBACK, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        util = [float(r[6]) for r in self.rows if len(r) > 6 and r[6].replace(".", "").isdigit()]
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_info():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """CPU oracle port on the box's host cores, bounded sample, rank 0 only."""
+    world, rank, _ = dist_info()
+    if rank != 0:
+        return
+    from oracle.spikemesh_oracle import OracleCluster
+    from paper_2512_09502_b200 import api, models
+    n = args.cpu_sample_neurons
+    scale = n / args.neurons
+    k_e, k_i = max(1, int(round(args.k_exc * scale))), max(1, int(round(args.k_inh * scale)))
+    sample = (f"oracle port, 1 rank, {n} neurons, K={k_e}+{k_i} ({n * (k_e + k_i):.3g} synapses) "
+              f"per step; same structure as the GPU workload scaled by {scale:g}")
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        c = OracleCluster(api.SimConfig(n_ranks=1, seed=args.seed))
+        models.build_balanced_network(c, models.BalancedParams(neurons_per_rank=n, k_exc=k_e, k_inh=k_i))
+        c.prepare()
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+        del c
+    syn = n * (k_e + k_i)
+    value = syn / float(np.mean(times))
+    line = {
+        "impl": "reference", "metric": "construction_synapses_per_s", "value": value, "unit": "synapses/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
+        "config": {"workload": "hpc_benchmark_C3_sampled", "neurons_per_rank": n, "k_in": k_e + k_i},
+        "cpu_baseline": {"value": value, "unit": "synapses/s", "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "synapses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args):
+    """Oracle port timed on the host for the headline line (rank 0, N=1)."""
+    from oracle.spikemesh_oracle import OracleCluster
+    from paper_2512_09502_b200 import api, models
+    n = args.cpu_sample_neurons
+    scale = n / args.neurons
+    k_e, k_i = max(1, int(round(args.k_exc * scale))), max(1, int(round(args.k_inh * scale)))
+    t0 = time.perf_counter()
+    c = OracleCluster(api.SimConfig(n_ranks=1, seed=args.seed))
+    models.build_balanced_network(c, models.BalancedParams(neurons_per_rank=n, k_exc=k_e, k_inh=k_i))
+    c.prepare()
+    dt = time.perf_counter() - t0
+    rep = c.simulate(0.0, 5.0, record=False)
+    syn = n * (k_e + k_i)
+    return {"value": syn / dt, "unit": "synapses/s", "cores": 1, "kind": "port",
+            "sample": f"oracle port: 1 rank, {n} neurons, K={k_e}+{k_i} ({syn:.3g} synapses) construction "
+                      f"{dt:.2f} s; propagation RTF {rep['rtf']:.2f} over 5 ms",
+            "rtf": rep["rtf"]}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_09502_b200 import _lib, api, engine, models
+
+    world, rank, local = dist_info()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    cfg = api.SimConfig(n_ranks=world, comm_mode="collective" if world > 1 else "p2p", seed=args.seed)
+    params = models.BalancedParams(neurons_per_rank=args.neurons, k_exc=args.k_exc, k_inh=args.k_inh)
+    syn_per_rank = args.neurons * (args.k_exc + args.k_inh)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def construct():
+        c = engine.Cluster(cfg, profile=True)
+        models.build_balanced_network(c, params)
+        c.prepare()
+        return c
+
+    c = None
+    for _ in range(args.warmup):
+        del c
+        gc.collect()
+        c = construct()
+        barrier()
+    step_ms, wall_s, gen_ms, sort_ms, launches, h2d = [], [], [], [], [], []
+    with Clocks(dev.index) as clk:
+        for _ in range(args.steps):
+            del c
+            gc.collect()
+            barrier()
+            L0 = _lib.lib().smx_launch_count()
+            H0 = engine.H2D_BYTES[0]
+            stream = torch.cuda.current_stream(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(stream)
+            c = construct()
+            e1.record(stream)
+            # end-to-end: read the result back to the host (records per rank)
+            n_rec = int(c.ranks[rank].first_index[-1].item())
+            wall = time.perf_counter() - t0
+            torch.cuda.synchronize(dev)
+            barrier()
+            assert n_rec == syn_per_rank, (n_rec, syn_per_rank)
+            step_ms.append(max_over_ranks(e0.elapsed_time(e1)))
+            wall_s.append(max_over_ranks(wall))
+            gen_ms.append(c.kernel_ms("gen"))
+            sort_ms.append(c.kernel_ms("sort"))
+            launches.append(_lib.lib().smx_launch_count() - L0)
+            h2d.append(engine.H2D_BYTES[0] - H0)
+        # propagation on the last network
+        rep = c.simulate(args.prop_warmup_ms, args.model_ms, record=False)
+    rtf = max_over_ranks(rep.rtf)
+    clocks = clk.summary()
+    ms = float(np.mean(step_ms))
+    total_syn = world * syn_per_rank
+    value = total_syn / (ms * 1e-3)
+    e2e = total_syn / float(np.mean(wall_s))
+    peak, peak_kind = peaks()
+    k_ms = float(np.mean(gen_ms)) + float(np.mean(sort_ms))
+    achieved = BYTES_PER_SYN * syn_per_rank / (k_ms * 1e-3) / 1e9
+    if rank != 0:
+        return
+    line = {
+        "metric": "construction_synapses_per_s", "value": value, "unit": "synapses/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+        "config": {"workload": "hpc_benchmark_C3_weak", "neurons_per_gpu": args.neurons,
+                   "k_in": args.k_exc + args.k_in if False else args.k_exc + args.k_inh,
+                   "synapses_per_gpu": syn_per_rank, "comm": cfg.comm_mode, "parallelism": f"ranks{world}",
+                   "l2": "inputs larger than L2 (tables 4.5 GB per GPU)", "seed": args.seed},
+        "construction_wall_s": float(np.mean(wall_s)),
+        "rtf": rtf, "rtf_model_ms": args.model_ms, "n_spikes_model": None,
+        "gpu_launches": int(np.mean(launches)),
+        "e2e": {"value": e2e, "unit": "synapses/s", "h2d_bytes_per_step": int(np.mean(h2d)),
+                "d2h_bytes_per_step": 8},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "generation (smx_gen_draw) + stable sort (smx_sort_records)",
+                     "kernel_ms": k_ms, "bytes_per_synapse": BYTES_PER_SYN},
+        "clocks": clocks,
+        "phase_ms": {"gen": float(np.mean(gen_ms)), "sort": float(np.mean(sort_ms))},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

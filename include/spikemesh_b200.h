@@ -31,6 +31,8 @@ extern "C" {
 int smx_last_error(char* buf, size_t cap);
 const char* smx_version(void);
 int smx_stream_sync(void* stream);
+/* kernels launched by the library so far (process-wide counter) */
+uint64_t smx_launch_count(void);
 
 /* --- keyed streams (numpy 2.3.5 Generator(Philox) semantics) -------------
  * Replaces RngStream (sm/core.py:110-148) draws made by the construction

@@ -25,6 +25,7 @@ SIGNATURES = {
     "smx_last_error": (I32, [ctypes.c_char_p, ctypes.c_size_t]),
     "smx_version": (ctypes.c_char_p, []),
     "smx_stream_sync": (I32, [P]),
+    "smx_launch_count": (U64, []),
     "smx_philox_words": (I32, [U64, U64, U64, U64, P, P]),
     "smx_integers": (I32, [U64, U64, U64, I64, U64, U64, P, P, P]),
     "smx_init_v": (I32, [P, U32, P, U32, P, U64, D, D, P, P]),

@@ -7,7 +7,16 @@
 #include <cstring>
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
+
 static thread_local char g_err[1024] = {0};
+static std::atomic<uint64_t> g_launches{0};
+
+// Every kernel launch of the library bumps this counter (bench.py reports
+// the launches inside its timed region from it).
+extern "C" void smx_count_launch(void) { g_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" uint64_t smx_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" void smx_set_error(const char* fmt, ...) {
   va_list ap;

@@ -213,8 +213,10 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* ws, ui
 
 }  // namespace smx
 
-// Error reporting shared by every translation unit (defined in capi.cu).
+// Error reporting and the kernel-launch counter shared by every translation
+// unit (defined in capi.cu).
 extern "C" void smx_set_error(const char* fmt, ...);
+extern "C" void smx_count_launch(void);
 #define SMX_CUDA_CHECK(expr)                                                       \
   do {                                                                             \
     cudaError_t _e = (expr);                                                       \

@@ -299,7 +299,7 @@ extern "C" int smx_pay_table(const int64_t* targets, uint64_t n, const int32_t* 
   int* bad = nullptr;
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&bad, sizeof(int), st));
   SMX_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), st));
-  pay_table_kernel<<<nblk(n), T256, 0, st>>>(targets, n, node2row, n_nodes, cls, pay_tab, bad);
+  smx_count_launch(); pay_table_kernel<<<nblk(n), T256, 0, st>>>(targets, n, node2row, n_nodes, cls, pay_tab, bad);
   SMX_LAUNCH_CHECK();
   int hbad = 0;
   SMX_CUDA_CHECK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -315,7 +315,7 @@ extern "C" int smx_pay_table(const int64_t* targets, uint64_t n, const int32_t* 
 extern "C" int smx_key_table(const int64_t* sources, uint64_t n, uint32_t tmp_base, int tmp, uint32_t* key_tab,
                              void* stream) {
   if (n == 0) return 0;
-  key_table_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(sources, n, tmp_base, tmp, key_tab);
+  smx_count_launch(); key_table_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(sources, n, tmp_base, tmp, key_tab);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -324,7 +324,7 @@ extern "C" int smx_dist_tables(const int32_t* src_rank, const int64_t* src_node,
                                const uint32_t* vbase, int tgt_rank, uint32_t lut_base, uint32_t* key_tab,
                                uint32_t* gv_tab, void* stream) {
   if (total == 0) return 0;
-  dist_tables_kernel<<<nblk(total), T256, 0, (cudaStream_t)stream>>>(src_rank, src_node, total, vbase, tgt_rank,
+  smx_count_launch(); dist_tables_kernel<<<nblk(total), T256, 0, (cudaStream_t)stream>>>(src_rank, src_node, total, vbase, tgt_rank,
                                                                        lut_base, key_tab, gv_tab);
   SMX_LAUNCH_CHECK();
   return 0;
@@ -349,7 +349,7 @@ extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, 
   DrawResult res;
   if (ex == 1) {  // numpy: a one-value range consumes nothing; every draw is 0
     if (n) {
-      draw_const_kernel<GenSink><<<nblk(n), T256, 0, (cudaStream_t)stream>>>(n, s);
+      smx_count_launch(); draw_const_kernel<GenSink><<<nblk(n), T256, 0, (cudaStream_t)stream>>>(n, s);
       SMX_LAUNCH_CHECK();
     }
     *cursor_out = u0;
@@ -363,7 +363,7 @@ extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, 
 extern "C" int smx_gen_pairs(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab,
                              const uint32_t* pay_tab, uint32_t* keys, uint32_t* vals, void* stream) {
   if (n == 0) return 0;
-  pairs_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(mode, n, n_src, key_tab, pay_tab, keys, vals);
+  smx_count_launch(); pairs_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(mode, n, n_src, key_tab, pay_tab, keys, vals);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -371,7 +371,7 @@ extern "C" int smx_gen_pairs(int mode, uint64_t n, uint64_t n_src, const uint32_
 extern "C" int smx_mark_values(const uint32_t* pos_bits, const int64_t* sources, uint64_t n, uint32_t* vbits,
                                void* stream) {
   if (n == 0) return 0;
-  mark_values_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(pos_bits, sources, n, vbits);
+  smx_count_launch(); mark_values_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(pos_bits, sources, n, vbits);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -392,10 +392,10 @@ extern "C" int smx_assign_images(const uint32_t* vbits, uint64_t nwords, const v
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&cnt, sizeof(uint32_t) * nwords, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&excl, sizeof(int64_t) * (nwords + 1), st));
   SMX_CUDA_CHECK(cudaMemcpyAsync(segs, segs_host, sizeof(Segment) * ns, cudaMemcpyHostToDevice, st));
-  new_counts_kernel<<<nblk(nwords), T256, 0, st>>>(vbits, nwords, segs, ns, cnt);
+  smx_count_launch(); new_counts_kernel<<<nblk(nwords), T256, 0, st>>>(vbits, nwords, segs, ns, cnt);
   SMX_LAUNCH_CHECK();
   if (int rc = smx_counts_to_offsets(cnt, nwords, excl, st)) return rc;
-  assign_kernel<<<nblk(nwords), T256, 0, st>>>(vbits, nwords, segs, ns, excl, m0);
+  smx_count_launch(); assign_kernel<<<nblk(nwords), T256, 0, st>>>(vbits, nwords, segs, ns, excl, m0);
   SMX_LAUNCH_CHECK();
   SMX_CUDA_CHECK(cudaMemcpyAsync(n_new, excl + nwords, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   SMX_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -408,14 +408,14 @@ extern "C" int smx_assign_images(const uint32_t* vbits, uint64_t nwords, const v
 extern "C" int smx_gather_lut(const int64_t* sources, uint64_t n, const int32_t* img_of, uint32_t* lut,
                               void* stream) {
   if (n == 0) return 0;
-  gather_lut_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(sources, n, img_of, lut);
+  smx_count_launch(); gather_lut_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(sources, n, img_of, lut);
   SMX_LAUNCH_CHECK();
   return 0;
 }
 
 extern "C" int smx_bits_or(uint32_t* dst, const uint32_t* src, uint64_t nwords, void* stream) {
   if (nwords == 0) return 0;
-  bits_or_kernel<<<nblk(nwords), T256, 0, (cudaStream_t)stream>>>(dst, src, nwords);
+  smx_count_launch(); bits_or_kernel<<<nblk(nwords), T256, 0, (cudaStream_t)stream>>>(dst, src, nwords);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -426,7 +426,7 @@ extern "C" int smx_bits_prefix(const uint32_t* bits, uint64_t nwords, int64_t* e
   uint32_t* cnt = nullptr;
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&cnt, sizeof(uint32_t) * (nwords ? nwords : 1), st));
   if (nwords) {
-    popc_kernel<<<nblk(nwords), T256, 0, st>>>(bits, nwords, cnt);
+    smx_count_launch(); popc_kernel<<<nblk(nwords), T256, 0, st>>>(bits, nwords, cnt);
     SMX_LAUNCH_CHECK();
   }
   if (int rc = smx_counts_to_offsets(cnt, nwords, excl, st)) return rc;
@@ -439,7 +439,7 @@ extern "C" int smx_bits_prefix(const uint32_t* bits, uint64_t nwords, int64_t* e
 extern "C" int smx_bits_compact(const uint32_t* bits, uint64_t nwords, const int64_t* excl, int64_t* out,
                                 const int32_t* img_of, int64_t* img_out, void* stream) {
   if (nwords == 0) return 0;
-  compact_kernel<<<nblk(nwords), T256, 0, (cudaStream_t)stream>>>(bits, nwords, excl, out, img_of, img_out);
+  smx_count_launch(); compact_kernel<<<nblk(nwords), T256, 0, (cudaStream_t)stream>>>(bits, nwords, excl, out, img_of, img_out);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -455,14 +455,14 @@ extern "C" int smx_build_routes(const void* tabs_host, int nt, uint64_t n_nodes,
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&tabs, sizeof(RouteTable) * (nt ? nt : 1), st));
   if (nt) SMX_CUDA_CHECK(cudaMemcpyAsync(tabs, tabs_host, sizeof(RouteTable) * nt, cudaMemcpyHostToDevice, st));
   if (n_nodes) {
-    route_count_kernel<<<nblk(n_nodes), T256, 0, st>>>(tabs, nt, n_nodes, cnt_scratch);
+    smx_count_launch(); route_count_kernel<<<nblk(n_nodes), T256, 0, st>>>(tabs, nt, n_nodes, cnt_scratch);
     SMX_LAUNCH_CHECK();
   }
   if (int rc = smx_counts_to_offsets(cnt_scratch, n_nodes, first, st)) return rc;
   SMX_CUDA_CHECK(cudaMemcpyAsync(n_entries, first + n_nodes, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   SMX_CUDA_CHECK(cudaStreamSynchronize(st));
   if (dest && n_nodes) {
-    route_fill_kernel<<<nblk(n_nodes), T256, 0, st>>>(tabs, nt, n_nodes, first, dest, pos);
+    smx_count_launch(); route_fill_kernel<<<nblk(n_nodes), T256, 0, st>>>(tabs, nt, n_nodes, first, dest, pos);
     SMX_LAUNCH_CHECK();
   }
   cudaFreeAsync(tabs, st);
@@ -471,7 +471,7 @@ extern "C" int smx_build_routes(const void* tabs_host, int nt, uint64_t n_nodes,
 
 extern "C" int smx_fill_wide_const(double* w, uint32_t* meta, uint64_t n, double wv, uint32_t mv, void* stream) {
   if (n == 0) return 0;
-  fill_wide_const_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(w, meta, n, wv, mv);
+  smx_count_launch(); fill_wide_const_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(w, meta, n, wv, mv);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -479,7 +479,7 @@ extern "C" int smx_fill_wide_const(double* w, uint32_t* meta, uint64_t n, double
 extern "C" int smx_promote_wide(const uint32_t* vals, uint64_t n, const double* cls_w, const uint32_t* cls_meta,
                                 uint32_t* rows, double* w, uint32_t* meta, void* stream) {
   if (n == 0) return 0;
-  promote_wide_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(vals, n, cls_w, cls_meta, rows, w, meta);
+  smx_count_launch(); promote_wide_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(vals, n, cls_w, cls_meta, rows, w, meta);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -487,7 +487,7 @@ extern "C" int smx_promote_wide(const uint32_t* vals, uint64_t n, const double* 
 extern "C" int smx_gather_wide(const uint32_t* idx, uint64_t n, const uint32_t* rows_in, const double* w_in,
                                const uint32_t* meta_in, uint32_t* rows, double* w, uint32_t* meta, void* stream) {
   if (n == 0) return 0;
-  gather_wide_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(idx, n, rows_in, w_in, meta_in, rows, w, meta);
+  smx_count_launch(); gather_wide_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(idx, n, rows_in, w_in, meta_in, rows, w, meta);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -496,7 +496,7 @@ extern "C" int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out2, vo
   cudaStream_t st = (cudaStream_t)stream;
   SMX_CUDA_CHECK(cudaMemsetAsync(out2, 0, 8, st));
   if (n == 0) return 0;
-  max_meta_kernel<<<148 * 4, T256, 0, st>>>(meta, n, out2, out2 + 1);
+  smx_count_launch(); max_meta_kernel<<<148 * 4, T256, 0, st>>>(meta, n, out2, out2 + 1);
   SMX_LAUNCH_CHECK();
   return 0;
 }

@@ -43,14 +43,14 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
     SMX_CUDA_CHECK(cudaMallocAsync((void**)&counts, sizeof(uint32_t) * G, st));
     SMX_CUDA_CHECK(cudaMallocAsync((void**)&offs, sizeof(uint64_t) * (G + 1), st));
     SMX_CUDA_CHECK(cudaMallocAsync((void**)&cur_d, sizeof(uint64_t), st));
-    draw_count_kernel<<<G, DRAW_THREADS, 0, st>>>(r, counts);
-    cta_offsets_kernel<<<1, 1024, 0, st>>>(counts, G, offs);
+    smx_count_launch(); draw_count_kernel<<<G, DRAW_THREADS, 0, st>>>(r, counts);
+    smx_count_launch(); cta_offsets_kernel<<<1, 1024, 0, st>>>(counts, G, offs);
     SMX_LAUNCH_CHECK();
     uint64_t total = 0;
     SMX_CUDA_CHECK(cudaMemcpyAsync(&total, offs + G, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     SMX_CUDA_CHECK(cudaStreamSynchronize(st));
     if (total >= n_out) {
-      draw_write_kernel<Sink><<<G, DRAW_THREADS, 0, st>>>(r, offs, n_out, sink, cur_d);
+      smx_count_launch(); draw_write_kernel<Sink><<<G, DRAW_THREADS, 0, st>>>(r, offs, n_out, sink, cur_d);
       SMX_LAUNCH_CHECK();
       SMX_CUDA_CHECK(cudaMemcpyAsync(&res->cursor, cur_d, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
       SMX_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -259,11 +259,11 @@ extern "C" int smx_poisson_counts(uint64_t k0, uint64_t k1, const uint64_t* curs
   J.out = counts;
   J.cursor = cursor_out;
   J.err = err;
-  chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
-  group_kernel<<<ng, PE, 0, st>>>(J);
-  across_kernel<<<1, 32, 0, st>>>(J, ng, gentry, gbase);
-  within_kernel<<<(ng + 127) / 128, 128, 0, st>>>(J, gentry, gbase);
-  emit_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  smx_count_launch(); chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
+  smx_count_launch(); across_kernel<<<1, 32, 0, st>>>(J, ng, gentry, gbase);
+  smx_count_launch(); within_kernel<<<(ng + 127) / 128, 128, 0, st>>>(J, gentry, gbase);
+  smx_count_launch(); emit_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
   SMX_LAUNCH_CHECK();
   return 0;
 }

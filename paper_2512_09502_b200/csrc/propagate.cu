@@ -310,7 +310,7 @@ extern "C" int smx_lif_update(double* v, int32_t* ref, const double* decay, cons
                               uint32_t* spike_bits, void* stream) {
   if (n == 0) return 0;
   LifState s{v, ref, decay, v_rest, v_reset, v_th, ref_steps, i_e};
-  lif_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(s, n, ring, n_ports, L, now, spike_bits);
+  smx_count_launch(); lif_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(s, n, ring, n_ports, L, now, spike_bits);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -318,7 +318,7 @@ extern "C" int smx_lif_update(double* v, int32_t* ref, const double* decay, cons
 extern "C" int smx_poisson_emit(const uint8_t* counts, uint32_t n_t, const uint32_t* rows, double w,
                                 double* ring_slot_port, void* stream) {
   if (n_t == 0) return 0;
-  poisson_emit_kernel<<<nblk(n_t), T256, 0, (cudaStream_t)stream>>>(counts, n_t, rows, w, ring_slot_port);
+  smx_count_launch(); poisson_emit_kernel<<<nblk(n_t), T256, 0, (cudaStream_t)stream>>>(counts, n_t, rows, w, ring_slot_port);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -362,7 +362,7 @@ extern "C" int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uin
     smx_set_error("at most 64 packet destinations per routing family");
     return -1;
   }
-  spikes_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(o, a, b);
+  smx_count_launch(); spikes_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(o, a, b);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -370,7 +370,7 @@ extern "C" int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uin
 extern "C" int smx_unpack(const uint32_t* packets, const uint32_t* count, const int64_t* table, uint64_t table_len,
                           uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err,
                           void* stream) {
-  unpack_kernel<<<148, T256, 0, (cudaStream_t)stream>>>(packets, count, table, table_len, src_nodes, src_steps,
+  smx_count_launch(); unpack_kernel<<<148, T256, 0, (cudaStream_t)stream>>>(packets, count, table, table_len, src_nodes, src_steps,
                                                          n_src, src_cap, err);
   SMX_LAUNCH_CHECK();
   return 0;
@@ -384,14 +384,14 @@ extern "C" int smx_deliver(const uint32_t* src_nodes, const uint32_t* src_steps,
                            const double* wide_w, const uint32_t* wide_meta, double* ring, uint32_t n_rows,
                            int n_ports, int L, int grid, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  plan_kernel<<<1, 1024, 0, st>>>(src_nodes, n_src, first, wprefix, n_work);
+  smx_count_launch(); plan_kernel<<<1, 1024, 0, st>>>(src_nodes, n_src, first, wprefix, n_work);
   SynTable syn{cls_w, cls_delay, cls_port};
   if (grid <= 0) grid = 148 * 8;
   if (wide_w) {
-    deliver_kernel<true><<<grid, T256, 0, st>>>(src_nodes, src_steps, n_src, wprefix, n_work, first, payload, syn,
+    smx_count_launch(); deliver_kernel<true><<<grid, T256, 0, st>>>(src_nodes, src_steps, n_src, wprefix, n_work, first, payload, syn,
                                                  wide_w, wide_meta, ring, n_rows, n_ports, L);
   } else {
-    deliver_kernel<false><<<grid, T256, 0, st>>>(src_nodes, src_steps, n_src, wprefix, n_work, first, payload, syn,
+    smx_count_launch(); deliver_kernel<false><<<grid, T256, 0, st>>>(src_nodes, src_steps, n_src, wprefix, n_work, first, payload, syn,
                                                   wide_w, wide_meta, ring, n_rows, n_ports, L);
   }
   SMX_LAUNCH_CHECK();

@@ -99,7 +99,7 @@ extern "C" int smx_philox_words(uint64_t k0, uint64_t k1, uint64_t w0, uint64_t 
                                 void* stream) {
   if (n == 0) return 0;
   const unsigned blocks = (unsigned)((n + 255) / 256);
-  words_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(Key{k0, k1}, w0, n, out);
+  smx_count_launch(); words_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(Key{k0, k1}, w0, n, out);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -111,7 +111,7 @@ extern "C" int smx_integers(uint64_t k0, uint64_t k1, uint64_t u32_cursor, int64
   cudaStream_t st = (cudaStream_t)stream;
   if (ex == 1) {  // numpy: a one-value range consumes no draws
     if (n) {
-      fill_i64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, lo);
+      smx_count_launch(); fill_i64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, lo);
       SMX_LAUNCH_CHECK();
     }
     *cursor_out = u32_cursor;
@@ -129,7 +129,7 @@ extern "C" int smx_init_v(const uint8_t* prefix, uint32_t plen, const uint8_t* s
   if (n == 0) return 0;
   KeyedIdSpec s;
   if (int rc = make_spec(prefix, plen, suffix, slen, &s)) return rc;
-  init_v_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(s, gids, n, mu, sd, v_out);
+  smx_count_launch(); init_v_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(s, gids, n, mu, sd, v_out);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -140,7 +140,7 @@ extern "C" int smx_stream_keys(const uint8_t* prefix, uint32_t plen, const uint8
   if (n == 0) return 0;
   KeyedIdSpec s;
   if (int rc = make_spec(prefix, plen, suffix, slen, &s)) return rc;
-  stream_keys_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(s, ids, n, keys_out);
+  smx_count_launch(); stream_keys_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(s, ids, n, keys_out);
   SMX_LAUNCH_CHECK();
   return 0;
 }

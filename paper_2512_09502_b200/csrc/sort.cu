@@ -229,9 +229,9 @@ extern "C" int smx_counts_to_offsets(const uint32_t* counts, uint64_t n, int64_t
   const int nb = (int)((n + per - 1) / per) + (n == 0 ? 1 : 0);
   uint64_t* part = nullptr;
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&part, sizeof(uint64_t) * (nb + 1), st));
-  scan_reduce_kernel<<<nb, SC_THREADS, 0, st>>>(counts, n, part);
-  scan_parts_kernel<<<1, 32, 0, st>>>(part, nb);
-  scan_apply_kernel<<<nb, SC_THREADS, 0, st>>>(counts, n, part, first_index);
+  smx_count_launch(); scan_reduce_kernel<<<nb, SC_THREADS, 0, st>>>(counts, n, part);
+  smx_count_launch(); scan_parts_kernel<<<1, 32, 0, st>>>(part, nb);
+  smx_count_launch(); scan_apply_kernel<<<nb, SC_THREADS, 0, st>>>(counts, n, part, first_index);
   SMX_LAUNCH_CHECK();
   cudaFreeAsync(part, st);
   return 0;
@@ -276,9 +276,9 @@ extern "C" int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
     p.hist_scan = hscan;
     p.keys_out = p.last ? nullptr : (from_a ? keys_b : keys_a);
     p.vals_out = from_a ? vals_b : vals_a;
-    upsweep_kernel<<<G, RS_THREADS, 0, st>>>(p, hist);
-    scan_small_kernel<<<1, 1024, 0, st>>>(hist, hscan, RS_BINS * G);
-    downsweep_kernel<<<G, RS_THREADS, 0, st>>>(p);
+    smx_count_launch(); upsweep_kernel<<<G, RS_THREADS, 0, st>>>(p, hist);
+    smx_count_launch(); scan_small_kernel<<<1, 1024, 0, st>>>(hist, hscan, RS_BINS * G);
+    smx_count_launch(); downsweep_kernel<<<G, RS_THREADS, 0, st>>>(p);
     SMX_LAUNCH_CHECK();
     *out_in_b = from_a ? 1 : 0;
   }

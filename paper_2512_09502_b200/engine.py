@@ -42,6 +42,16 @@ def _ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
 
+H2D_BYTES = [0]
+
+
+def _up(arr, dev) -> torch.Tensor:
+    """Host -> device upload (counted for the end-to-end byte accounting)."""
+    a = np.ascontiguousarray(arr)
+    H2D_BYTES[0] += a.nbytes
+    return torch.from_numpy(a).to(dev)
+
+
 def _words(nbits: int) -> int:
     return (int(nbits) + 31) // 32
 
@@ -165,6 +175,7 @@ class _Rank:
         self.mirrors: dict[int, _Bits] = {}
         self.rosters: dict[tuple, _Bits] = {}
         self.devices: list[dict] = []
+        self.used_classes: set[int] = set()
         self.prepared = False
 
     @property
@@ -199,8 +210,9 @@ class _Rank:
 class Cluster:
     """GPU cluster with the reference façade (sm/engine.py:197-399)."""
 
-    def __init__(self, cfg: SimConfig, devices=None, local_ranks=None):
+    def __init__(self, cfg: SimConfig, devices=None, local_ranks=None, profile: bool = False):
         t0 = time.perf_counter()
+        self.prof = {"gen": [], "sort": []} if profile else None
         if not torch.cuda.is_available():
             raise RuntimeError("spikemesh-b200 needs a CUDA device (no CPU fallback)")
         _lib.lib()
@@ -238,6 +250,8 @@ class Cluster:
         self.param_index: dict = {}
         self.classes: list[tuple] = []      # (weight, delay, port)
         self.class_index: dict = {}
+        self.any_p2p = False
+        self._pg = None
         self.messages = {p: 0 for p in PHASES}
         self.bytes = {p: 0 for p in PHASES}
         self.phase = "construction"
@@ -259,6 +273,17 @@ class Cluster:
             for st in self.ranks.values():
                 torch.cuda.synchronize(st.device)
             setattr(self.timers, bucket, getattr(self.timers, bucket) + time.perf_counter() - t0)
+
+    @staticmethod
+    def _event(st):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream(st.device))
+        return e
+
+    def kernel_ms(self, what: str) -> float:
+        """Summed CUDA-event time of the profiled C-ABI calls ('gen', 'sort')."""
+        torch.cuda.synchronize()
+        return float(sum(a.elapsed_time(b) for a, b in self.prof[what]))
 
     def _require_unprepared(self):
         if self.prepared:
@@ -322,7 +347,7 @@ class Cluster:
                 if len(v_init) != 3 or v_init[0] != "normal":
                     raise ValueError(f"bad v_init spec {v_init!r}")
                 v = torch.empty(n, dtype=torch.float64, device=dev)
-                g = torch.from_numpy(gids).to(dev)
+                g = _up(gids, dev)
                 pre = canonical_bytes((int(self.cfg.seed), ("init-v", 0)))
                 prefix = pre[: pre.rindex(b"i:0))") + 2]
                 suffix = b"))"
@@ -331,7 +356,7 @@ class Cluster:
             elif np.ndim(v_init) == 0:
                 v = torch.full((n,), float(v_init), dtype=torch.float64, device=dev)
             else:
-                v = torch.as_tensor(np.asarray(v_init, dtype=np.float64)).to(dev)
+                v = _up(np.asarray(v_init, dtype=np.float64), dev)
                 if v.numel() != n:
                     raise ValueError("v_init must have one entry per neuron")
             row0 = st.n_real
@@ -375,8 +400,8 @@ class Cluster:
     # -------------------------------------------------------------- connections
     def _tables(self, st: _Rank, sources, targets, cls, tmp_base=None):
         dev = st.device
-        src = torch.from_numpy(np.ascontiguousarray(sources, dtype=np.int64)).to(dev)
-        tgt = torch.from_numpy(np.ascontiguousarray(targets, dtype=np.int64)).to(dev)
+        src = _up(np.ascontiguousarray(sources, dtype=np.int64), dev)
+        tgt = _up(np.ascontiguousarray(targets, dtype=np.int64), dev)
         key_tab = torch.empty(len(sources), dtype=torch.int32, device=dev)
         pay_tab = torch.empty(len(targets), dtype=torch.int32, device=dev)
         call("smx_key_table", _ptr(src), len(sources), 0 if tmp_base is None else tmp_base,
@@ -390,6 +415,7 @@ class Cluster:
         if syn.is_constant and not st.wide:
             cid = self._class_id(float(syn.weight), int(syn.delay_steps), port)
             if cid < MAX_CLASSES:
+                st.used_classes.add(cid)
                 return cid
         return None
 
@@ -438,9 +464,9 @@ class Cluster:
             call("smx_fill_wide_const", _ptr(seg_w), _ptr(seg_m), n, float(wv),
                  (int(dv) & ROW_MASK) | (port << 24), st.stream)
         else:
-            seg_w.copy_(torch.from_numpy(np.broadcast_to(wv, (n,)).copy()))
+            seg_w.copy_(_up(np.broadcast_to(wv, (n,)).copy(), seg_w.device))
             meta = (np.broadcast_to(dv, (n,)).astype(np.int64) & ROW_MASK) | (port << 24)
-            seg_m.copy_(torch.from_numpy(meta.astype(np.uint32).view(np.int32)))
+            seg_m.copy_(_up(meta.astype(np.uint32).view(np.int32), seg_m.device))
 
     def _emit_records(self, st: _Rank, conn: ConnSpec, sources, targets, syn: SynSpec, port: int,
                       aligned_key, local_key, syn_key, tmp_base=None, pos_bits=None):
@@ -467,6 +493,7 @@ class Cluster:
         vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
         cur = np.zeros(1, dtype=np.uint64)
         sk = st.stream
+        ev0 = self._event(st) if self.prof is not None else None
         if n:
             if rule in ("one_to_one", "assigned"):
                 call("smx_gen_pairs", 0, n, n_src, _ptr(key_tab), _ptr(pay_tab), _ptr(keys), _ptr(vals), sk)
@@ -485,6 +512,8 @@ class Cluster:
                 u0 = int(cur[0]) if local_key == aligned_key else 0
                 call("smx_gen_draw", local_key[0], local_key[1], u0, n_tgt, n, 0, 1, 0,
                      _ptr(pay_tab), 1, 0, _ptr(vals), 0, 0, cur.ctypes.data, sk)
+        if self.prof is not None:
+            self.prof["gen"].append((ev0, self._event(st)))
         if st.wide:
             self._write_syn(st, syn, port, base, n, syn_key)
         st.commit_records(n)
@@ -562,6 +591,8 @@ class Cluster:
             if sr not in members or tr not in members:
                 raise ValueError(f"ranks {sr} and {tr} must both belong to group {group}")
         n_src, n_tgt = len(sources), len(targets)
+        if group == POINT_TO_POINT:
+            self.any_p2p = True
         idx = self._bump_pair(sr, tr)
         flag = self._flagging(conn, n_src, n_tgt)
         k_src = self._key(("remote-src", sr, tr, idx))
@@ -592,7 +623,7 @@ class Cluster:
             if self.is_local(sr):
                 ss = self.ranks[sr]
                 dev = ss.device
-                src_dev = torch.from_numpy(sources).to(dev)
+                src_dev = _up(sources, dev)
                 pb = None
                 if flag:
                     if used_pos is not None and used_pos.device == dev:
@@ -605,7 +636,7 @@ class Cluster:
             for mbr in members:
                 if self.is_local(mbr):
                     ms = self.ranks[mbr]
-                    src_dev = torch.from_numpy(sources).to(ms.device)
+                    src_dev = _up(sources, ms.device)
                     ros = ms.rosters.setdefault((group, sr), _Bits(ms.device)).ensure(span)
                     call("smx_mark_values", 0, _ptr(src_dev), n_src, _ptr(ros.t), ms.stream)
         return n_rec
@@ -670,6 +701,9 @@ class Cluster:
                 raise ValueError("source index outside the source rank's node range")
         self.dist_ctr += 1
         call_idx = self.dist_ctr
+        if group == POINT_TO_POINT and (len(set(src_ranks)) > 1 or
+                                        any(int(t) not in src_ranks for t, _ in target_pops)):
+            self.any_p2p = True
         # value segments per source rank, ascending rank, word aligned
         ranks_sorted = sorted(set(src_ranks))
         span = {r: int(max(a.max() for rr, a in zip(src_ranks, src_nodes) if rr == r)) + 1 for r in ranks_sorted}
@@ -752,9 +786,9 @@ class Cluster:
         return [r for r, a in zip(ranks_sorted, any_set) if a]
 
     def _dist_tables(self, dev, stream, tr, total, all_rank, all_node, vbase, lut_base):
-        rk = torch.from_numpy(all_rank).to(dev)
-        nd = torch.from_numpy(all_node).to(dev)
-        vb = torch.from_numpy(vbase.astype(np.uint32).view(np.int32)).to(dev)
+        rk = _up(all_rank, dev)
+        nd = _up(all_node, dev)
+        vb = _up(vbase.astype(np.uint32).view(np.int32), dev)
         key_tab = torch.empty(total, dtype=torch.int32, device=dev)
         gv_tab = torch.empty(total, dtype=torch.int32, device=dev)
         call("smx_dist_tables", _ptr(rk), _ptr(nd), total, _ptr(vb), tr, lut_base, _ptr(key_tab),
@@ -770,7 +804,7 @@ class Cluster:
         cls = self._syn_class(st, syn, port)
         if cls is None:
             self._make_wide(st)
-        tgt = torch.from_numpy(np.ascontiguousarray(tg)).to(dev)
+        tgt = _up(np.ascontiguousarray(tg), dev)
         pay_tab = torch.empty(len(tg), dtype=torch.int32, device=dev)
         call("smx_pay_table", _ptr(tgt), len(tg), _ptr(st.node2row.t), st.node2row.n,
              0 if cls is None else cls, _ptr(pay_tab), sk)
@@ -778,8 +812,11 @@ class Cluster:
         base = st.reserve_records(n)
         vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
         cur = np.zeros(1, dtype=np.uint64)
+        ev0 = self._event(st) if self.prof is not None else None
         call("smx_gen_draw", key[0], key[1], 0, total, n, 1, 2, _ptr(key_tab), _ptr(pay_tab), k_in,
              _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits), _ptr(gv_all), cur.ctypes.data, sk)
+        if self.prof is not None:
+            self.prof["gen"].append((ev0, self._event(st)))
         if st.wide:
             self._write_syn(st, syn, port, base, n, None)
         st.commit_records(n)
@@ -832,11 +869,13 @@ class Cluster:
         self.prepared = True
 
     def _compute_has_p2p(self):
-        flags = [bool(st.mirrors) or any(k[0] == POINT_TO_POINT for k in st.maps) for st in self.ranks.values()]
-        val = any(flags)
+        """sm/engine.py:268-271.  With one process per rank a process cannot
+        see the other ranks' maps without communicating, so the round runs
+        whenever the (identical) script issued any cross-rank p2p call."""
         if self.distributed:
-            return True if self.n_ranks > 1 and self.cfg.comm_mode == "p2p" else val
-        return val
+            return self.any_p2p
+        return any(bool(st.mirrors) or any(k[0] == POINT_TO_POINT for k in st.maps)
+                   for st in self.ranks.values())
 
     def _prepare_rank(self, st: _Rank):
         dev, sk = st.device, st.stream
@@ -849,9 +888,8 @@ class Cluster:
             call("smx_max_meta", _ptr(st.w_meta.t), st.w_meta.n, _ptr(mm), sk)
             mm = mm.cpu().numpy()
             max_delay, max_port = max(max_delay, int(mm[0])), max(max_port, int(mm[1]))
-        elif st.keys.n:
-            used = torch.unique(torch.bitwise_right_shift(st.vals.view(), 24) & 0xFF).cpu().numpy()
-            for c in used:
+        else:
+            for c in st.used_classes:
                 _, d, p = self.classes[int(c)]
                 max_delay, max_port = max(max_delay, d), max(max_port, p)
         for d in st.devices:
@@ -865,15 +903,15 @@ class Cluster:
         tab = np.array([[math.exp(-dt / p.tau_m), p.v_rest, p.v_reset, p.v_th, p.i_e] for p in self.params] or
                        [[0.0] * 5], dtype=np.float64)
         rs = np.array([int(round(p.t_ref / dt)) for p in self.params] or [0], dtype=np.int32)
-        f64 = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        f64 = lambda a: _up(np.ascontiguousarray(a), dev)  # noqa: E731
         st.decay, st.v_rest, st.v_reset, st.v_th, st.i_e = (f64(tab[prm, j]) for j in range(5))
         st.ref_steps = f64(rs[prm])
         st.v = torch.cat(st.v0) if st.v0 else torch.empty(0, dtype=torch.float64, device=dev)
         st.ref = torch.zeros(N, dtype=torch.int32, device=dev)
         st.row2node_np = np.concatenate(st.row2node) if st.row2node else np.empty(0, np.int64)
-        st.row2node_t = torch.from_numpy(st.row2node_np.astype(np.int32)).to(dev)
+        st.row2node_t = _up(st.row2node_np.astype(np.int32), dev)
         st.gid_np = np.concatenate(st.row_gid) if st.row_gid else np.empty(0, np.int64)
-        st.gid_t = torch.from_numpy(st.gid_np).to(dev)
+        st.gid_t = _up(st.gid_np, dev)
         st.ring = torch.zeros(st.L * st.P * max(N, 1), dtype=torch.float64, device=dev)
         # sort the store (sm/core.py:299-324)
         n = st.keys.n
@@ -886,9 +924,12 @@ class Cluster:
         lut = st.lut.t
         if n and n_nodes >= (1 << 31):
             raise ValueError("more than 2^31 nodes on one rank")
+        ev0 = self._event(st) if self.prof is not None else None
         call("smx_sort_records", _ptr(st.keys.t), _ptr(st.vals.t), _ptr(kb), _ptr(vb), n, key_bits,
              1 if st.wide else 0, _ptr(lut), _ptr(st.counts), n_nodes, which.ctypes.data, sk)
         sorted_vals = (vb if which[0] else st.vals.t)[:n]
+        if self.prof is not None:
+            self.prof["sort"].append((ev0, self._event(st)))
         st.first_index = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
         call("smx_counts_to_offsets", _ptr(st.counts), n_nodes, _ptr(st.first_index), sk)
         if n and int(st.first_index[-1].item()) != n:
@@ -901,14 +942,15 @@ class Cluster:
                  _ptr(st.payload), _ptr(st.ww), _ptr(st.wm), sk)
             st.w_rows = st.w_w = st.w_meta = None
         else:
-            st.payload = sorted_vals.clone() if n else torch.empty(1, dtype=torch.int32, device=dev)
+            st.payload = sorted_vals if n else torch.empty(1, dtype=torch.int32, device=dev)
             st.ww = st.wm = None
-        del kb, vb
+        del kb, vb, sorted_vals
         st.keys = st.vals = None
+        st.lut = None
         st.cls_w, cm = self._class_tables(dev)
         cmn = cm.cpu().numpy().view(np.uint32)
-        st.cls_delay = torch.from_numpy((cmn & ROW_MASK).astype(np.int32)).to(dev)
-        st.cls_port = torch.from_numpy((cmn >> 24).astype(np.int32)).to(dev)
+        st.cls_delay = _up((cmn & ROW_MASK).astype(np.int32), dev)
+        st.cls_port = _up((cmn >> 24).astype(np.int32), dev)
         # maps -> sorted (R, L) (sm/construction.py:183-242)
         st.RL = {}
         for key, m in st.maps.items():
@@ -1012,7 +1054,7 @@ class Cluster:
             rows = np.asarray(st_node2row_host(st, d["targets"]), dtype=np.int64)
             if (rows < 0).any():
                 raise ValueError("poisson targets must be real neurons")
-            d["rows"] = torch.from_numpy(rows.astype(np.int32)).to(dev)
+            d["rows"] = _up(rows.astype(np.int32), dev)
             d["nt"] = nt
             d["active"] = nt > 0 and d["lam"] != 0.0
             if not d["active"]:
@@ -1115,7 +1157,62 @@ class Cluster:
             self._deliver(st)
 
     def _exchange_nccl(self, now):
-        raise NotImplementedError("multi-process exchange is set up by engine_dist")
+        """One process per rank: the same rounds over NCCL.  Counts travel
+        first (device int32), then only max-count packets."""
+        dist = torch.distributed
+        (st,) = self.ranks.values()
+        me = st.rank
+        st.n_src.zero_()
+        if self._pg is None:
+            self._pg = {g: dist.new_group(list(self.groups[g])) for g in sorted(self.groups)}
+        if self.has_p2p:
+            send_c = st.p2p_counts.clone()
+            recv_c = torch.empty_like(send_c)
+            dist.all_to_all_single(recv_c, send_c)
+            sc, rc = send_c.cpu().numpy(), recv_c.cpu().numpy()
+            inp = torch.cat([st.p2p_packets[d * st.pk_cap * 2: d * st.pk_cap * 2 + 2 * int(sc[d])]
+                             for d in range(self.n_ranks)])
+            out = torch.empty(int(2 * rc.sum()), dtype=torch.int32, device=st.device)
+            dist.all_to_all_single(out, inp, [2 * int(x) for x in rc], [2 * int(x) for x in sc])
+            off = 0
+            for sr in range(self.n_ranks):
+                n = int(rc[sr])
+                rl = st.RL.get((POINT_TO_POINT, sr))
+                if n and rl is not None and sr != me:
+                    call("smx_unpack", _ptr(out[off:]), _ptr(recv_c[sr:]), _ptr(rl[1]), rl[1].numel(),
+                         _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err),
+                         st.stream)
+                elif n and sr != me:
+                    raise ProtocolError(f"rank {me}: spikes from rank {sr} but no map for that pair")
+                off += 2 * n
+            self.messages["propagation"] += self.n_ranks * (self.n_ranks - 1)
+            self.bytes["propagation"] += 8 * int(sc.sum())
+        for g in self.group_ids:
+            members = self.groups[g]
+            if me not in members:
+                continue
+            slot = self.group_slots[g]
+            pg = self._pg[g]
+            nm = len(members)
+            allc = torch.empty(nm, dtype=torch.int32, device=st.device)
+            dist.all_gather_into_tensor(allc, st.g_counts[slot: slot + 1], group=pg)
+            cmax = int(allc.max().item())
+            if cmax:
+                send = st.g_packets[slot * st.pk_cap * 2: slot * st.pk_cap * 2 + 2 * cmax]
+                recv = torch.empty(nm * 2 * cmax, dtype=torch.int32, device=st.device)
+                dist.all_gather_into_tensor(recv, send.contiguous(), group=pg)
+                for i, sr in enumerate(sorted(members)):
+                    if sr == me:
+                        continue
+                    lk = st.I.get((g, sr))
+                    if lk is None:
+                        continue
+                    call("smx_unpack", _ptr(recv[i * 2 * cmax:]), _ptr(allc[i:]), _ptr(lk), lk.numel(),
+                         _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err),
+                         st.stream)
+            self.messages["propagation"] += nm
+            self.bytes["propagation"] += 8 * int(st.g_counts[slot].item())
+        self._deliver(st)
 
     _recording = False
 

@@ -81,15 +81,9 @@ struct GenSink {
   uint32_t kdiv;
   uint32_t* keys;        // pre-offset to the call's first record
   uint32_t* vals;
-  uint32_t* used_bits;   // optional
-  const uint32_t* used_tab;  // optional position -> bit (0xffffffff = skip)
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const {
     if (key_mode == K_FROM_VALUE) {
-      if (keys) keys[j] = key_tab[v];
-      if (used_bits) {
-        const uint32_t b = used_tab ? used_tab[v] : v;
-        if (b != 0xffffffffu) set_bit(used_bits, b);
-      }
+      if (keys) keys[j] = __ldg(key_tab + v);
     } else if (key_mode == K_FROM_J) {
       keys[j] = key_tab[j / kdiv];
     }
@@ -97,6 +91,11 @@ struct GenSink {
     else if (pay_mode == P_FROM_VALUE) vals[j] = pay_tab[v];
   }
 };
+
+__global__ void mark_one_kernel(uint32_t* bits, const uint32_t* tab) {
+  const uint32_t b = tab ? tab[0] : 0u;
+  if (b != 0xffffffffu) atomicOr(&bits[b >> 5], 1u << (b & 31));
+}
 
 // Deterministic-use rules: one_to_one / assigned (mode 0: record i = (i, i)),
 // all_to_all (mode 1: record r = (r % n_src, r / n_src)).
@@ -335,7 +334,7 @@ extern "C" int smx_dist_tables(const int32_t* src_rank, const int64_t* src_node,
 extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, uint64_t n, int key_mode,
                             int pay_mode, const uint32_t* key_tab, const uint32_t* pay_tab, uint32_t kdiv,
                             uint32_t* keys, uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab,
-                            uint64_t* cursor_out, void* stream) {
+                            uint32_t used_bits_words, uint64_t* cursor_out, void* stream) {
   GenSink s;
   s.key_mode = key_mode;
   s.pay_mode = pay_mode;
@@ -344,18 +343,20 @@ extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, 
   s.kdiv = kdiv ? kdiv : 1;
   s.keys = keys;
   s.vals = vals;
-  s.used_bits = used_bits;
-  s.used_tab = used_tab;
   DrawResult res;
   if (ex == 1) {  // numpy: a one-value range consumes nothing; every draw is 0
     if (n) {
       smx_count_launch(); draw_const_kernel<GenSink><<<nblk(n), T256, 0, (cudaStream_t)stream>>>(n, s);
+      if (used_bits) { smx_count_launch(); mark_one_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(used_bits, used_tab); }
       SMX_LAUNCH_CHECK();
     }
     *cursor_out = u0;
     return 0;
   }
-  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, (cudaStream_t)stream, &res);
+  // used-value marking (flagged / remote sources): bitmap size from the table
+  // range -- the caller sizes used_bits to cover every bit it can receive
+  DrawMark mk{used_bits, used_tab, used_bits_words, 0};
+  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, (cudaStream_t)stream, &res, mk);
   *cursor_out = res.cursor;
   return rc;
 }

@@ -84,36 +84,73 @@ static __global__ void cta_offsets_kernel(const uint32_t* counts, int n, uint64_
 
 // Sink contract: `void operator()(uint64_t j, uint32_t value)` for j < n_out,
 // and `void cursor(uint64_t u32_after)` from the thread that emits j = n_out-1.
+// Optional used-value marking fused into the write pass: bit
+// (tab ? tab[value] : value) of `bits` is set for every emitted draw.  Small
+// bitmaps are accumulated in shared memory and OR-ed out once per CTA.
+struct DrawMark {
+  uint32_t* bits;
+  const uint32_t* tab;
+  uint32_t nwords;  // bitmap size
+  int in_smem;      // nwords fit the dynamic shared-memory bitmap
+};
+
+constexpr uint32_t DRAW_MARK_SMEM_WORDS = 12288;  // 48 KB
+
 template <class Sink>
-__global__ void draw_write_kernel(DrawRange r, const uint64_t* cta_offsets, uint64_t n_out,
-                                  Sink sink, uint64_t* cursor_out) {
+__global__ void __launch_bounds__(DRAW_THREADS) draw_write_kernel(DrawRange r, const uint64_t* cta_offsets,
+                                                                  uint64_t n_out, Sink sink, uint64_t* cursor_out,
+                                                                  DrawMark mk) {
+  extern __shared__ uint32_t smark[];
   const uint64_t lo = r.u0 + (uint64_t)blockIdx.x * r.per_cta;
   const uint64_t end = r.u0 + r.n_raw;
   const uint64_t hi = lo + r.per_cta < end ? lo + r.per_cta : end;
-  if (lo >= hi) return;
   uint64_t base = cta_offsets[blockIdx.x];
-  if (base >= n_out) return;
+  if (lo >= hi || base >= n_out) return;
+  if (mk.in_smem) {
+    for (uint32_t w = threadIdx.x; w < mk.nwords; w += blockDim.x) smark[w] = 0;
+  }
   __shared__ uint32_t ws[DRAW_THREADS / 32];
+  __shared__ uint32_t sv[DRAW_THREADS * 8];  // accepted values of one iteration, in order
   const uint64_t b0 = lo / 8 + 1, b1 = (hi - 1) / 8 + 1;
-  for (uint64_t bb = b0; bb <= b1; bb += blockDim.x) {
+  for (uint64_t bb = b0; bb <= b1 && base < n_out; bb += blockDim.x) {
     const uint64_t b = bb + threadIdx.x;
     uint32_t v[8];
     uint32_t mask = 0;
     if (b <= b1) mask = block_accepts(r, b, lo, hi, v);
     uint32_t tot;
     const uint32_t ex = block_excl_scan(__popc(mask), ws, tot);
-    uint64_t j = base + ex;
+    uint32_t k = ex;
     while (mask) {
       const int i = __ffs(mask) - 1;
       mask &= mask - 1;
+      sv[k] = v[i];
+      if (base + k == n_out - 1 && cursor_out) *cursor_out = (b - 1) * 8 + i + 1;
+      ++k;
+    }
+    __syncthreads();
+    // coalesced hand-off: consecutive threads own consecutive output indices
+    for (uint32_t q = threadIdx.x; q < tot; q += blockDim.x) {
+      const uint64_t j = base + q;
       if (j < n_out) {
-        sink(j, v[i]);
-        if (j == n_out - 1 && cursor_out) *cursor_out = (b - 1) * 8 + i + 1;
+        const uint32_t val = sv[q];
+        sink(j, val);
+        if (mk.bits) {
+          const uint32_t bit = mk.tab ? __ldg(mk.tab + val) : val;
+          if (bit != 0xffffffffu) {
+            if (mk.in_smem) atomicOr(&smark[bit >> 5], 1u << (bit & 31));
+            else atomicOr(&mk.bits[bit >> 5], 1u << (bit & 31));
+          }
+        }
       }
-      ++j;
     }
     base += tot;
-    if (base >= n_out) break;
+    __syncthreads();
+  }
+  if (mk.in_smem) {
+    for (uint32_t w = threadIdx.x; w < mk.nwords; w += blockDim.x) {
+      const uint32_t x = smark[w];
+      if (x) atomicOr(&mk.bits[w], x);
+    }
   }
 }
 

@@ -13,7 +13,7 @@ struct DrawResult {
 // Hands every (index, value-lo) to `sink`; returns 0 or a negative status.
 template <class Sink>
 int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink,
-             cudaStream_t st, DrawResult* res) {
+             cudaStream_t st, DrawResult* res, DrawMark mk = DrawMark{nullptr, nullptr, 0, 0}) {
   res->cursor = u0;
   if (n_out == 0) return 0;
   if (ex == 1) {  // numpy: range of one value consumes nothing
@@ -50,7 +50,13 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
     SMX_CUDA_CHECK(cudaMemcpyAsync(&total, offs + G, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     SMX_CUDA_CHECK(cudaStreamSynchronize(st));
     if (total >= n_out) {
-      smx_count_launch(); draw_write_kernel<Sink><<<G, DRAW_THREADS, 0, st>>>(r, offs, n_out, sink, cur_d);
+      mk.in_smem = mk.bits && mk.nwords <= DRAW_MARK_SMEM_WORDS;
+      const size_t smem = mk.in_smem ? mk.nwords * 4 : 0;
+      if (smem > 48 * 1024) {
+        SMX_CUDA_CHECK(cudaFuncSetAttribute(draw_write_kernel<Sink>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem));
+      }
+      smx_count_launch(); draw_write_kernel<Sink><<<G, DRAW_THREADS, smem, st>>>(r, offs, n_out, sink, cur_d, mk);
       SMX_LAUNCH_CHECK();
       SMX_CUDA_CHECK(cudaMemcpyAsync(&res->cursor, cur_d, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
       SMX_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -5,7 +5,8 @@
 // stable sort by final source over that order reproduces the reference's
 // table order exactly.
 //
-// Per 8-bit digit pass (reduce-then-scan):
+// ceil(key_bits / 11) passes of equal digit width (<= 11 bits), each a
+// reduce-then-scan:
 //   upsweep   per-CTA digit histogram of a contiguous segment
 //   scan      exclusive scan over (digit, CTA) -> each CTA's base per digit
 //   downsweep CTA walks its segment in 4096-record tiles; warp-striped loads,
@@ -25,7 +26,7 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_IPT = 16;                       // items per thread per tile
 constexpr int RS_TILE = RS_THREADS * RS_IPT;     // 4096
-constexpr int RS_BINS = 256;
+constexpr int RS_MAX_BITS = 11;
 
 struct SortPass {
   const uint32_t* keys_in;
@@ -39,29 +40,40 @@ struct SortPass {
   int last;
   const uint32_t* lut;      // temporary-key LUT (first pass)
   uint32_t* counts;         // per-key counts (last pass)
-  const uint32_t* hist_scan;  // [RS_BINS * G] exclusive offsets
+  const uint32_t* hist_scan;  // [BINS * G] exclusive offsets
 };
 
 __device__ __forceinline__ uint32_t resolve(uint32_t k, const uint32_t* lut) {
   return (k & SMX_TMP_KEY) ? lut[k & ~SMX_TMP_KEY] : k;
 }
 
+template <int BITS>
 __global__ void __launch_bounds__(RS_THREADS) upsweep_kernel(SortPass p, uint32_t* hist) {
-  __shared__ uint32_t h[RS_BINS];
-  for (int i = threadIdx.x; i < RS_BINS; i += RS_THREADS) h[i] = 0;
+  constexpr int BINS = 1 << BITS;
+  __shared__ uint32_t h[BINS];
+  for (int i = threadIdx.x; i < BINS; i += RS_THREADS) h[i] = 0;
   __syncthreads();
   const uint64_t lo = (uint64_t)blockIdx.x * p.seg;
   const uint64_t hi = lo + p.seg < p.n ? lo + p.seg : p.n;
-  for (uint64_t i = lo + threadIdx.x; i < hi; i += RS_THREADS) {
-    uint32_t k = p.keys_in[i];
-    if (p.first) k = resolve(k, p.lut);
-    atomicAdd(&h[(k >> p.shift) & 0xff], 1u);
+  const uint32_t mask = BINS - 1;
+  // 4-wide vector loads (segments are multiples of 4096 records)
+  const uint4* k4 = reinterpret_cast<const uint4*>(p.keys_in);
+  for (uint64_t i = lo / 4 + threadIdx.x; i < (hi + 3) / 4; i += RS_THREADS) {
+    const uint4 q = k4[i];
+    const uint32_t kk[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (i * 4 + j >= hi) break;
+      uint32_t k = kk[j];
+      if (p.first) k = resolve(k, p.lut);
+      atomicAdd(&h[(k >> p.shift) & mask], 1u);
+    }
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < RS_BINS; d += RS_THREADS) hist[(uint64_t)d * gridDim.x + blockIdx.x] = h[d];
+  for (int d = threadIdx.x; d < BINS; d += RS_THREADS) hist[(uint64_t)d * gridDim.x + blockIdx.x] = h[d];
 }
 
-// Single-CTA exclusive scan of n u32 (n = RS_BINS * G, fits in u32 totals).
+// Single-CTA exclusive scan of n u32 (n = BINS * G, totals fit in u32).
 __global__ void scan_small_kernel(const uint32_t* in, uint32_t* out, int n) {
   __shared__ uint32_t ws[32];
   __shared__ uint32_t carry;
@@ -79,74 +91,97 @@ __global__ void scan_small_kernel(const uint32_t* in, uint32_t* out, int n) {
   }
 }
 
-__global__ void __launch_bounds__(RS_THREADS) downsweep_kernel(SortPass p) {
-  __shared__ uint32_t wcnt[RS_WARPS][RS_BINS];
-  __shared__ uint32_t run_base[RS_BINS];
-  __shared__ uint32_t tstart[RS_BINS];
-  __shared__ uint32_t skey[RS_TILE];
-  __shared__ uint32_t sval[RS_TILE];
+// Stable scatter of one segment per CTA by the digit (key >> shift) & (2^BITS-1).
+template <int BITS>
+__global__ void __launch_bounds__(RS_THREADS, 3) downsweep_kernel(SortPass p) {
+  constexpr int BINS = 1 << BITS;
+  constexpr int DPT = BINS >= RS_THREADS ? BINS / RS_THREADS : 1;  // digits per thread
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(smem);                       // [RS_WARPS][BINS]
+  uint32_t* run_base = reinterpret_cast<uint32_t*>(smem + RS_WARPS * BINS * 2);  // [BINS]
+  uint32_t* tstart = run_base + BINS;                                       // [BINS + 1]
+  uint32_t* skey = tstart + BINS + 1;                                       // [RS_TILE]
+  uint32_t* sval = skey + RS_TILE;                                          // [RS_TILE]
   __shared__ uint32_t ws[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1;
-  for (int d = tid; d < RS_BINS; d += RS_THREADS) run_base[d] = p.hist_scan[(uint64_t)d * gridDim.x + blockIdx.x];
+  const uint32_t mask = BINS - 1;
+  for (int d = tid; d < BINS; d += RS_THREADS) run_base[d] = p.hist_scan[(uint64_t)d * gridDim.x + blockIdx.x];
   const uint64_t lo = (uint64_t)blockIdx.x * p.seg;
   const uint64_t hi = lo + p.seg < p.n ? lo + p.seg : p.n;
   for (uint64_t t0 = lo; t0 < hi; t0 += RS_TILE) {
-    for (int d = tid; d < RS_WARPS * RS_BINS; d += RS_THREADS) (&wcnt[0][0])[d] = 0;
+    for (int d = tid; d < RS_WARPS * BINS / 2; d += RS_THREADS) reinterpret_cast<uint32_t*>(wcnt)[d] = 0;
     __syncthreads();
-    uint32_t key[RS_IPT], val[RS_IPT], rank[RS_IPT];
-    // warp-striped: warp w owns [t0 + w*512, +512), batch i = 32 consecutive records
+    uint32_t key[RS_IPT];
+    uint32_t rank2[RS_IPT / 2];  // two 16-bit ranks per register; 0xffff = invalid
+    const uint64_t wbase = t0 + (uint64_t)warp * (32 * RS_IPT) + lane;
 #pragma unroll
     for (int i = 0; i < RS_IPT; ++i) {
-      const uint64_t idx = t0 + (uint64_t)warp * (32 * RS_IPT) + i * 32 + lane;
+      const uint64_t idx = wbase + i * 32;
       const bool valid = idx < hi;
-      uint32_t k = 0, v = 0;
+      uint32_t k = 0;
       if (valid) {
         k = p.keys_in[idx];
         if (p.first) k = resolve(k, p.lut);
-        v = p.vals_in ? p.vals_in[idx] : (uint32_t)idx;
       }
       key[i] = k;
-      val[i] = v;
-      const uint32_t d = (k >> p.shift) & 0xff;
-      const uint32_t tag = valid ? d : 0x100u + lane;
+      const uint32_t d = (k >> p.shift) & mask;
+      const uint32_t tag = valid ? d : 0x10000u + lane;
       const uint32_t peers = __match_any_sync(0xffffffffu, tag);
       const int leader = __ffs(peers) - 1;
       uint32_t old = 0;
       if (valid && lane == leader) {
-        old = wcnt[warp][d];
-        wcnt[warp][d] = old + __popc(peers);
+        old = wcnt[warp * BINS + d];
+        wcnt[warp * BINS + d] = (uint16_t)(old + __popc(peers));
       }
       old = __shfl_sync(0xffffffffu, old, leader);
-      rank[i] = valid ? old + __popc(peers & lt_mask) : 0xffffffffu;
+      const uint32_t r = valid ? old + __popc(peers & lt_mask) : 0xffffu;
+      if (i & 1) rank2[i >> 1] |= r << 16; else rank2[i >> 1] = r;
     }
     __syncthreads();
-    // per digit: warp prefixes (in place) and tile totals
-    uint32_t total = 0;
-    if (tid < RS_BINS) {
-      for (int w = 0; w < RS_WARPS; ++w) {
-        const uint32_t c = wcnt[w][tid];
-        wcnt[w][tid] = total;
-        total += c;
+    // digits [tid*DPT, tid*DPT+DPT): warp prefixes in place, tile totals, block scan
+    uint32_t tot_d[DPT];
+    uint32_t mysum = 0;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const int d = tid * DPT + j;
+      uint32_t t = 0;
+      if (d < BINS) {
+#pragma unroll
+        for (int w = 0; w < RS_WARPS; ++w) {
+          const uint32_t c = wcnt[w * BINS + d];
+          wcnt[w * BINS + d] = (uint16_t)t;
+          t += c;
+        }
       }
+      tot_d[j] = t;
+      mysum += t;
     }
     uint32_t tsum;
-    const uint32_t ts = smx::block_excl_scan(tid < RS_BINS ? total : 0, ws, tsum);
-    if (tid < RS_BINS) tstart[tid] = ts;
+    uint32_t run = smx::block_excl_scan(mysum, ws, tsum);
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const int d = tid * DPT + j;
+      if (d < BINS) tstart[d] = run;
+      run += tot_d[j];
+    }
+    if (tid == 0) tstart[BINS] = tsum;
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < RS_IPT; ++i) {
-      if (rank[i] != 0xffffffffu) {
-        const uint32_t d = (key[i] >> p.shift) & 0xff;
-        const uint32_t pos = tstart[d] + wcnt[warp][d] + rank[i];
+      const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+      if (r != 0xffffu) {
+        const uint32_t d = (key[i] >> p.shift) & mask;
+        const uint32_t pos = tstart[d] + wcnt[warp * BINS + d] + r;
+        const uint64_t idx = wbase + i * 32;
         skey[pos] = key[i];
-        sval[pos] = val[i];
+        sval[pos] = p.vals_in ? p.vals_in[idx] : (uint32_t)idx;
       }
     }
     __syncthreads();
     for (uint32_t q = tid; q < tsum; q += RS_THREADS) {
       const uint32_t k = skey[q];
-      const uint32_t d = (k >> p.shift) & 0xff;
+      const uint32_t d = (k >> p.shift) & mask;
       const uint64_t g = (uint64_t)run_base[d] + (q - tstart[d]);
       p.vals_out[g] = sval[q];
       if (!p.last) {
@@ -158,14 +193,39 @@ __global__ void __launch_bounds__(RS_THREADS) downsweep_kernel(SortPass p) {
       }
     }
     __syncthreads();
-    if (tid < RS_BINS) {
-      uint32_t c = 0;
-      // tile count of digit tid = next tstart - tstart
-      const uint32_t nxt = tid + 1 < RS_BINS ? tstart[tid + 1] : tsum;
-      c = nxt - tstart[tid];
-      run_base[tid] += c;
-    }
+    for (int d = tid; d < BINS; d += RS_THREADS) run_base[d] += tstart[d + 1] - tstart[d];
     __syncthreads();
+  }
+}
+
+template <int BITS>
+size_t downsweep_smem() {
+  return (size_t)RS_WARPS * (1 << BITS) * 2 + (size_t)(2 * (1 << BITS) + 1) * 4 + (size_t)2 * RS_TILE * 4;
+}
+
+template <int BITS>
+int run_pass(const SortPass& p, int G, uint32_t* hist, uint32_t* hscan, cudaStream_t st) {
+  const size_t smem = downsweep_smem<BITS>();
+  static bool configured = false;
+  if (!configured) {
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    configured = true;
+  }
+  smx_count_launch(); upsweep_kernel<BITS><<<G, RS_THREADS, 0, st>>>(p, hist);
+  smx_count_launch(); scan_small_kernel<<<1, 1024, 0, st>>>(hist, hscan, (1 << BITS) * G);
+  smx_count_launch(); downsweep_kernel<BITS><<<G, RS_THREADS, smem, st>>>(p);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+int run_pass_bits(int bits, const SortPass& p, int G, uint32_t* hist, uint32_t* hscan, cudaStream_t st) {
+  switch (bits) {
+    case 1: case 2: case 3: case 4: case 5: case 6: case 7:
+    case 8: return run_pass<8>(p, G, hist, hscan, st);
+    case 9: return run_pass<9>(p, G, hist, hscan, st);
+    case 10: return run_pass<10>(p, G, hist, hscan, st);
+    default: return run_pass<11>(p, G, hist, hscan, st);
   }
 }
 
@@ -238,9 +298,10 @@ extern "C" int smx_counts_to_offsets(const uint32_t* counts, uint64_t n, int64_t
 }
 
 // Stable sort of n records by key (key_bits significant bits after LUT
-// resolution).  keys_a/vals_a hold the pending records; with index_values the
-// initial value of record i is i (vals_a is then only scratch).  keys_b/vals_b
-// are scratch of n entries.  The sorted values land in vals_a or vals_b;
+// resolution) in ceil(key_bits / 11) passes of equal digit width.
+// keys_a/vals_a hold the pending records; with index_values the initial
+// value of record i is i (vals_a is then only scratch).  keys_b/vals_b are
+// scratch of n entries.  The sorted values land in vals_a or vals_b;
 // *out_in_b tells which.  counts[0..n_keys) receive per-key record counts.
 extern "C" int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b,
                                 uint64_t n, int key_bits, int index_values, const uint32_t* lut,
@@ -253,14 +314,17 @@ extern "C" int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
     smx_set_error("smx_sort_records: %llu records exceed the 32-bit record index", (unsigned long long)n);
     return -1;
   }
-  const int passes = key_bits <= 8 ? 1 : (key_bits + 7) / 8;
-  int G = (int)std::min<uint64_t>((n + RS_TILE - 1) / RS_TILE, 148 * 4);
+  if (key_bits < 1) key_bits = 1;
+  const int passes = (key_bits + RS_MAX_BITS - 1) / RS_MAX_BITS;
+  const int bits = (key_bits + passes - 1) / passes;
+  int G = (int)std::min<uint64_t>((n + RS_TILE - 1) / RS_TILE, 148 * 3);
   if (G < 1) G = 1;
   const uint64_t seg = ((n + G - 1) / G + RS_TILE - 1) / RS_TILE * RS_TILE;
   G = (int)((n + seg - 1) / seg);
   uint32_t *hist = nullptr, *hscan = nullptr;
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&hist, sizeof(uint32_t) * RS_BINS * G, st));
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&hscan, sizeof(uint32_t) * RS_BINS * G, st));
+  const size_t hn = (size_t)(1 << std::max(bits, 8)) * G;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&hist, sizeof(uint32_t) * hn, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&hscan, sizeof(uint32_t) * hn, st));
   for (int pass = 0; pass < passes; ++pass) {
     const bool from_a = (pass & 1) == 0;
     SortPass p;
@@ -268,7 +332,7 @@ extern "C" int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
     p.vals_in = (pass == 0 && index_values) ? nullptr : (from_a ? vals_a : vals_b);
     p.first = pass == 0;
     p.last = pass == passes - 1;
-    p.shift = 8 * pass;
+    p.shift = bits * pass;
     p.n = n;
     p.seg = seg;
     p.lut = lut;
@@ -276,10 +340,7 @@ extern "C" int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
     p.hist_scan = hscan;
     p.keys_out = p.last ? nullptr : (from_a ? keys_b : keys_a);
     p.vals_out = from_a ? vals_b : vals_a;
-    smx_count_launch(); upsweep_kernel<<<G, RS_THREADS, 0, st>>>(p, hist);
-    smx_count_launch(); scan_small_kernel<<<1, 1024, 0, st>>>(hist, hscan, RS_BINS * G);
-    smx_count_launch(); downsweep_kernel<<<G, RS_THREADS, 0, st>>>(p);
-    SMX_LAUNCH_CHECK();
+    if (int rc = run_pass_bits(bits, p, G, hist, hscan, st)) return rc;
     *out_in_b = from_a ? 1 : 0;
   }
   cudaFreeAsync(hist, st);

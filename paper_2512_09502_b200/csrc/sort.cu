@@ -18,6 +18,7 @@
 // equal keys: within a last-pass tile the lower digits are already sorted,
 // so equal keys are adjacent in the staging buffer).
 #include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace {
@@ -41,6 +42,7 @@ struct SortPass {
   const uint32_t* lut;      // temporary-key LUT (first pass)
   uint32_t* counts;         // per-key counts (last pass)
   const uint32_t* hist_scan;  // [BINS * G] exclusive offsets
+  unsigned long long* timing; // optional per-phase cycle counters (tuning)
 };
 
 __device__ __forceinline__ uint32_t resolve(uint32_t k, const uint32_t* lut) {
@@ -92,39 +94,85 @@ __global__ void scan_small_kernel(const uint32_t* in, uint32_t* out, int n) {
 }
 
 // Stable scatter of one segment per CTA by the digit (key >> shift) & (2^BITS-1).
+// Input tiles are double-buffered in shared memory by TMA 1-D bulk copies
+// (cp.async.bulk + mbarrier): tile i+1 streams in while tile i is ranked and
+// scattered, so the warps never wait on DRAM for their inputs.
 template <int BITS>
-__global__ void __launch_bounds__(RS_THREADS, 3) downsweep_kernel(SortPass p) {
+__global__ void __launch_bounds__(RS_THREADS, 2) downsweep_kernel(SortPass p) {
   constexpr int BINS = 1 << BITS;
   constexpr int DPT = BINS >= RS_THREADS ? BINS / RS_THREADS : 1;  // digits per thread
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint16_t* wcnt = reinterpret_cast<uint16_t*>(smem);                       // [RS_WARPS][BINS]
-  uint32_t* run_base = reinterpret_cast<uint32_t*>(smem + RS_WARPS * BINS * 2);  // [BINS]
-  uint32_t* tstart = run_base + BINS;                                       // [BINS + 1]
-  uint32_t* skey = tstart + BINS + 1;                                       // [RS_TILE]
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* inbuf = reinterpret_cast<uint32_t*>(smem);                      // [2][2][RS_TILE] keys, vals
+  uint32_t* skey = inbuf + 4 * RS_TILE;                                     // [RS_TILE]
   uint32_t* sval = skey + RS_TILE;                                          // [RS_TILE]
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(sval + RS_TILE);             // [RS_WARPS][BINS]
+  uint32_t* run_base = reinterpret_cast<uint32_t*>(wcnt + RS_WARPS * BINS);  // [BINS]
+  uint32_t* tstart = run_base + BINS;                                       // [BINS + 1]
   __shared__ uint32_t ws[32];
+  __shared__ __align__(8) uint64_t bar[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1;
   const uint32_t mask = BINS - 1;
   for (int d = tid; d < BINS; d += RS_THREADS) run_base[d] = p.hist_scan[(uint64_t)d * gridDim.x + blockIdx.x];
   const uint64_t lo = (uint64_t)blockIdx.x * p.seg;
   const uint64_t hi = lo + p.seg < p.n ? lo + p.seg : p.n;
-  for (uint64_t t0 = lo; t0 < hi; t0 += RS_TILE) {
+  const bool has_vals = p.vals_in != nullptr;
+  if (tid == 0) {
+    smx::mbar_init(&bar[0], 1);
+    smx::mbar_init(&bar[1], 1);
+    smx::fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint64_t t0, int b) {  // thread 0: full tiles only
+    const uint32_t bytes = RS_TILE * 4;
+    smx::mbar_expect_tx(&bar[b], has_vals ? 2 * bytes : bytes);
+    smx::bulk_g2s(inbuf + (2 * b) * RS_TILE, p.keys_in + t0, bytes, &bar[b]);
+    if (has_vals) smx::bulk_g2s(inbuf + (2 * b + 1) * RS_TILE, p.vals_in + t0, bytes, &bar[b]);
+  };
+  uint32_t phase[2] = {0, 0};
+  if (tid == 0 && lo + RS_TILE <= hi) issue(lo, 0);
+  long long tm = clock64();
+#define TMARK(i)                                                     \
+  if (p.timing && tid == 0) {                                        \
+    const long long t_ = clock64();                                  \
+    atomicAdd(p.timing + (i), (unsigned long long)(t_ - tm));        \
+    tm = t_;                                                         \
+  }
+  int b = 0;
+  for (uint64_t t0 = lo; t0 < hi; t0 += RS_TILE, b ^= 1) {
+    const bool full = t0 + RS_TILE <= hi;
+    uint32_t* kin = inbuf + (2 * b) * RS_TILE;
+    uint32_t* vin = kin + RS_TILE;
+    // prefetch the next tile into the other buffer (consumed two iterations ago)
+    if (tid == 0 && t0 + 2 * RS_TILE <= hi) {
+      smx::fence_proxy_async();
+      issue(t0 + RS_TILE, b ^ 1);
+    }
+    TMARK(5);
+    if (full) {
+      smx::mbar_wait(&bar[b], phase[b]);
+      phase[b] ^= 1;
+    } else {  // partial last tile: plain loads
+      for (uint32_t q = tid; q < RS_TILE; q += RS_THREADS) {
+        const uint64_t idx = t0 + q;
+        kin[q] = idx < hi ? p.keys_in[idx] : 0u;
+        if (has_vals) vin[q] = idx < hi ? p.vals_in[idx] : 0u;
+      }
+    }
     for (int d = tid; d < RS_WARPS * BINS / 2; d += RS_THREADS) reinterpret_cast<uint32_t*>(wcnt)[d] = 0;
     __syncthreads();
-    uint32_t key[RS_IPT];
+    TMARK(0);
     uint32_t rank2[RS_IPT / 2];  // two 16-bit ranks per register; 0xffff = invalid
-    const uint64_t wbase = t0 + (uint64_t)warp * (32 * RS_IPT) + lane;
+    const uint32_t wofs = warp * (32 * RS_IPT) + lane;
 #pragma unroll
     for (int i = 0; i < RS_IPT; ++i) {
-      const uint64_t idx = wbase + i * 32;
-      const bool valid = idx < hi;
-      uint32_t k = 0;
-      if (valid) {
-        k = p.keys_in[idx];
-        if (p.first) k = resolve(k, p.lut);
+      const uint32_t q = wofs + i * 32;
+      const bool valid = t0 + q < hi;
+      uint32_t k = kin[q];
+      if (p.first) {
+        k = resolve(k, p.lut);
+        kin[q] = k;  // later phases reread the resolved key
       }
-      key[i] = k;
       const uint32_t d = (k >> p.shift) & mask;
       const uint32_t tag = valid ? d : 0x10000u + lane;
       const uint32_t peers = __match_any_sync(0xffffffffu, tag);
@@ -139,6 +187,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) downsweep_kernel(SortPass p) {
       if (i & 1) rank2[i >> 1] |= r << 16; else rank2[i >> 1] = r;
     }
     __syncthreads();
+    TMARK(1);
     // digits [tid*DPT, tid*DPT+DPT): warp prefixes in place, tile totals, block scan
     uint32_t tot_d[DPT];
     uint32_t mysum = 0;
@@ -167,18 +216,21 @@ __global__ void __launch_bounds__(RS_THREADS, 3) downsweep_kernel(SortPass p) {
     }
     if (tid == 0) tstart[BINS] = tsum;
     __syncthreads();
+    TMARK(2);
 #pragma unroll
     for (int i = 0; i < RS_IPT; ++i) {
       const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
       if (r != 0xffffu) {
-        const uint32_t d = (key[i] >> p.shift) & mask;
+        const uint32_t q = wofs + i * 32;
+        const uint32_t k = kin[q];
+        const uint32_t d = (k >> p.shift) & mask;
         const uint32_t pos = tstart[d] + wcnt[warp * BINS + d] + r;
-        const uint64_t idx = wbase + i * 32;
-        skey[pos] = key[i];
-        sval[pos] = p.vals_in ? p.vals_in[idx] : (uint32_t)idx;
+        skey[pos] = k;
+        sval[pos] = has_vals ? vin[q] : (uint32_t)(t0 + q);
       }
     }
     __syncthreads();
+    TMARK(3);
     for (uint32_t q = tid; q < tsum; q += RS_THREADS) {
       const uint32_t k = skey[q];
       const uint32_t d = (k >> p.shift) & mask;
@@ -193,6 +245,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) downsweep_kernel(SortPass p) {
       }
     }
     __syncthreads();
+    TMARK(4);
     for (int d = tid; d < BINS; d += RS_THREADS) run_base[d] += tstart[d + 1] - tstart[d];
     __syncthreads();
   }
@@ -200,7 +253,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) downsweep_kernel(SortPass p) {
 
 template <int BITS>
 size_t downsweep_smem() {
-  return (size_t)RS_WARPS * (1 << BITS) * 2 + (size_t)(2 * (1 << BITS) + 1) * 4 + (size_t)2 * RS_TILE * 4;
+  return (size_t)6 * RS_TILE * 4 + (size_t)RS_WARPS * (1 << BITS) * 2 + (size_t)(2 * (1 << BITS) + 1) * 4;
 }
 
 template <int BITS>
@@ -282,6 +335,11 @@ __global__ void scan_apply_kernel(const uint32_t* in, uint64_t n, const uint64_t
 
 }  // namespace
 
+static unsigned long long* g_sort_timing = nullptr;
+// Tuning aid: per-phase cycle counters of the downsweep (thread 0 of every
+// CTA; phases: zero, rank, scan, stage, write, wait).  Pass null to disable.
+extern "C" void smx_sort_timing(unsigned long long* counters) { g_sort_timing = counters; }
+
 // first_index[0..n] = exclusive scan of counts[0..n-1]; first_index[n] = total.
 extern "C" int smx_counts_to_offsets(const uint32_t* counts, uint64_t n, int64_t* first_index, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -315,9 +373,11 @@ extern "C" int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
     return -1;
   }
   if (key_bits < 1) key_bits = 1;
-  const int passes = (key_bits + RS_MAX_BITS - 1) / RS_MAX_BITS;
+  static const int max_bits = getenv("SMX_SORT_MAX_BITS") ? atoi(getenv("SMX_SORT_MAX_BITS")) : RS_MAX_BITS;
+  static const int grid_cap = getenv("SMX_SORT_GRID") ? atoi(getenv("SMX_SORT_GRID")) : 148 * 2;
+  const int passes = (key_bits + max_bits - 1) / max_bits;
   const int bits = (key_bits + passes - 1) / passes;
-  int G = (int)std::min<uint64_t>((n + RS_TILE - 1) / RS_TILE, 148 * 3);
+  int G = (int)std::min<uint64_t>((n + RS_TILE - 1) / RS_TILE, grid_cap);
   if (G < 1) G = 1;
   const uint64_t seg = ((n + G - 1) / G + RS_TILE - 1) / RS_TILE * RS_TILE;
   G = (int)((n + seg - 1) / seg);
@@ -338,6 +398,7 @@ extern "C" int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
     p.lut = lut;
     p.counts = counts;
     p.hist_scan = hscan;
+    p.timing = g_sort_timing;
     p.keys_out = p.last ? nullptr : (from_a ? keys_b : keys_a);
     p.vals_out = from_a ? vals_b : vals_a;
     if (int rc = run_pass_bits(bits, p, G, hist, hscan, st)) return rc;

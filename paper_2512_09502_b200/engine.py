@@ -593,6 +593,8 @@ class Cluster:
         n_src, n_tgt = len(sources), len(targets)
         if group == POINT_TO_POINT:
             self.any_p2p = True
+        if not self.is_local(tr):
+            self.images_made[tr] = True  # the target may have grown images
         idx = self._bump_pair(sr, tr)
         flag = self._flagging(conn, n_src, n_tgt)
         k_src = self._key(("remote-src", sr, tr, idx))
@@ -725,6 +727,8 @@ class Cluster:
             tg = np.asarray(tg, dtype=np.int64)
             if len(tg) == 0:
                 raise ValueError("target populations must be non-empty")
+            if not self.is_local(tr) and any(r != tr for r in src_ranks):
+                self.images_made[tr] = True
             key = self._key(("dist-indegree", call_idx, tr))
             n = k_in * len(tg)
             need_bits = self.is_local(tr) or any(

@@ -113,4 +113,7 @@ SCENARIOS = {
     "explicit_3r_p2p": lambda ns: explicit(ns, 3, "p2p"),
     "explicit_3r_coll": lambda ns: explicit(ns, 3, "collective"),
     "multi_area_2r": lambda ns: multi_area(ns, 2, "p2p"),
+    "balanced_2r_p2p": lambda ns: balanced(ns, 2, "p2p", 250, 20, 5, 8, sim=(0.0, 20.0)),
+    "explicit_2r_coll": lambda ns: explicit(ns, 2, "collective"),
+    "multi_area_2r_coll": lambda ns: multi_area(ns, 2, "collective"),
 }

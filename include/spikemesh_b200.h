@@ -119,17 +119,18 @@ int smx_build_routes(const void* tabs_host, int nt, uint64_t n_nodes, uint32_t* 
  * kernels/_speedups.pyx:13-35) on real rows; ring is [L][P][n] fp64. */
 int smx_lif_update(double* v, int32_t* ref, const double* decay, const double* v_rest, const double* v_reset,
                    const double* v_th, const int32_t* ref_steps, const double* i_e, uint32_t n, double* ring,
-                   int n_ports, int L, int64_t now, uint32_t* spike_bits, void* stream);
-/* PoissonSource.emit_into (sm/dynamics.py:235-248) from precomputed counts */
-int smx_poisson_emit(const uint8_t* counts, uint32_t n_t, const uint32_t* rows, double w, double* ring_slot_port,
-                     void* stream);
+                   int n_ports, int L, const int64_t* now_dev, uint32_t* spike_bits, void* stream);
+/* PoissonSource.emit_into (sm/dynamics.py:235-248) from a batch of
+ * precomputed counts [S][n_t]; step taken from the device counter *now_dev. */
+int smx_poisson_emit(const uint8_t* counts, int S, uint32_t n_t, const uint32_t* rows, double w, double* ring,
+                     uint32_t n_rows, int n_ports, int L, int delay, int port, const int64_t* now_dev, void* stream);
 /* flatnonzero + recorder + route_point_spikes / route_group_spikes
  * (sm/engine.py:89-128); p2p/grp: {i64* first, i32* dest, u32* pos, int n_dest,
  * u32* packets, u32* counts, u32 cap} (host structs). */
 int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uint32_t* row2node, const int64_t* gid,
-               int64_t now, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap,
-               int record, int64_t* rec, uint64_t* n_rec, uint64_t rec_cap, uint32_t* spike_count, int* overflow,
-               const void* p2p_host, const void* grp_host, void* stream);
+               int64_t* now_dev, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap,
+               const int* record_dev, int64_t* rec, uint64_t* n_rec, uint64_t rec_cap, uint32_t* spike_count,
+               int* overflow, const void* p2p_host, const void* grp_host, void* stream);
 /* deliver_point_packets / deliver_gather_packets (sm/engine.py:146-190) */
 int smx_unpack(const uint32_t* packets, const uint32_t* count, const int64_t* table, uint64_t table_len,
                uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err, void* stream);

@@ -49,12 +49,12 @@ SIGNATURES = {
     "smx_promote_wide": (I32, [P, U64, P, P, P, P, P, P]),
     "smx_gather_wide": (I32, [P, U64, P, P, P, P, P, P, P]),
     "smx_max_meta": (I32, [P, U64, P, P]),
-    "smx_lif_update": (I32, [P, P, P, P, P, P, P, P, U32, P, I32, I32, I64, P, P]),
-    "smx_poisson_emit": (I32, [P, U32, P, D, P, P]),
+    "smx_lif_update": (I32, [P, P, P, P, P, P, P, P, U32, P, I32, I32, P, P, P]),
+    "smx_poisson_emit": (I32, [P, I32, U32, P, D, P, U32, I32, I32, I32, I32, P, P]),
     "smx_poisson_workspace": (U64, [I32]),
     "smx_poisson_chunks_for": (I32, [U64, D]),
     "smx_poisson_counts": (I32, [U64, U64, P, D, U64, I32, P, P, P, P, P]),
-    "smx_spikes": (I32, [P, U32, P, P, I64, P, P, P, U32, I32, P, P, U64, P, P, P, P, P]),
+    "smx_spikes": (I32, [P, U32, P, P, P, P, P, P, U32, P, P, P, U64, P, P, P, P, P]),
     "smx_unpack": (I32, [P, P, P, U64, P, P, P, U32, P, P]),
     "smx_deliver": (I32, [P, P, P, P, P, P, P, P, P, P, P, P, P, U32, I32, I32, I32, P]),
 }

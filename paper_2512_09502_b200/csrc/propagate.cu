@@ -40,9 +40,10 @@ struct LifState {
   const double* i_e;
 };
 
-__global__ void lif_kernel(LifState s, uint32_t n, double* ring, int n_ports, int L, int64_t now,
+__global__ void lif_kernel(LifState s, uint32_t n, double* ring, int n_ports, int L, const int64_t* now_dev,
                            uint32_t* spike_bits) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t now = *now_dev;
   bool spk = false;
   if (i < n) {
     const int slot = (int)(now % L);
@@ -74,12 +75,19 @@ __global__ void lif_kernel(LifState s, uint32_t n, double* ring, int n_ports, in
   if ((threadIdx.x & 31) == 0 && (i >> 5) < (n + 31) / 32) spike_bits[i >> 5] = b;
 }
 
-__global__ void poisson_emit_kernel(const uint8_t* counts, uint32_t n_t, const uint32_t* rows, double w,
-                                    double* ring_slot_port) {
+// counts: [S][n_t] batch of S steps starting at a multiple of S; the row
+// and the ring slot (now + delay) % L are taken from the device step counter.
+__global__ void poisson_emit_kernel(const uint8_t* counts, int S, uint32_t n_t, const uint32_t* rows, double w,
+                                    double* ring, uint32_t n_rows, int n_ports, int L, int delay, int port,
+                                    const int64_t* now_dev) {
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_t) return;
-  const uint32_t c = counts[t];
-  if (c) atomicAdd(ring_slot_port + rows[t], __dmul_rn(w, (double)c));
+  const int64_t now = *now_dev;
+  const uint32_t c = counts[(size_t)(now % S) * n_t + t];
+  if (c) {
+    const int slot = (int)((now + delay) % L);
+    atomicAdd(ring + ((size_t)slot * n_ports + port) * n_rows + rows[t], __dmul_rn(w, (double)c));
+  }
 }
 
 struct Routes {             // one routing family (p2p T/P or collective G/Q)
@@ -97,14 +105,14 @@ struct SpikeOut {
   uint32_t n_rows;
   const uint32_t* row2node;
   const int64_t* gid;       // per row
-  int64_t now;
+  int64_t* now_dev;         // step counter, advanced by this kernel
+  const int* record_dev;
   // local delivery source list (node, step)
   uint32_t* src_nodes;
   uint32_t* src_steps;
   uint32_t* n_src;          // device counter (appended to)
   uint32_t src_cap;
   // raster
-  int record;
   int64_t* rec;             // (step, gid) pairs
   uint64_t* n_rec;
   uint64_t rec_cap;
@@ -119,7 +127,9 @@ __global__ void __launch_bounds__(1024) spikes_kernel(SpikeOut o, Routes p2p, Ro
   __shared__ uint32_t carry, src_base;
   __shared__ uint32_t pk_base[2][64];
   const int tid = threadIdx.x;
-  if (tid == 0) { carry = 0; src_base = *o.n_src; }
+  const int64_t now = *o.now_dev;
+  const int record = *o.record_dev;
+  if (tid == 0) { carry = 0; src_base = 0; }
   for (int d = tid; d < 64; d += blockDim.x) {
     pk_base[0][d] = d < p2p.n_dest ? p2p.counts[d] : 0;
     pk_base[1][d] = d < grp.n_dest ? grp.counts[d] : 0;
@@ -138,11 +148,11 @@ __global__ void __launch_bounds__(1024) spikes_kernel(SpikeOut o, Routes p2p, Ro
       const uint32_t row = w * 32 + b;
       const uint32_t node = o.row2node[row];
       const uint32_t si = src_base + k;
-      if (si < o.src_cap) { o.src_nodes[si] = node; o.src_steps[si] = (uint32_t)o.now; }
+      if (si < o.src_cap) { o.src_nodes[si] = node; o.src_steps[si] = (uint32_t)now; }
       else atomicExch(o.overflow, 1);
-      if (o.record) {
+      if (record) {
         const uint64_t ri = *o.n_rec + k;
-        if (ri < o.rec_cap) { o.rec[2 * ri] = o.now; o.rec[2 * ri + 1] = o.gid[row]; }
+        if (ri < o.rec_cap) { o.rec[2 * ri] = now; o.rec[2 * ri + 1] = o.gid[row]; }
         else atomicExch(o.overflow, 2);
       }
       ++k;
@@ -174,7 +184,7 @@ __global__ void __launch_bounds__(1024) spikes_kernel(SpikeOut o, Routes p2p, Ro
           if (R.dest[e] != d) continue;
           if (q < R.cap) {
             R.packets[2 * ((size_t)d * R.cap + q)] = R.pos[e];
-            R.packets[2 * ((size_t)d * R.cap + q) + 1] = (uint32_t)o.now;
+            R.packets[2 * ((size_t)d * R.cap + q) + 1] = (uint32_t)now;
           } else {
             atomicExch(o.overflow, 3);
           }
@@ -189,8 +199,9 @@ __global__ void __launch_bounds__(1024) spikes_kernel(SpikeOut o, Routes p2p, Ro
   }
   if (tid == 0) {
     *o.n_src = min(src_base + n_spk, o.src_cap);
-    if (o.record) *o.n_rec += n_spk;
+    if (record) *o.n_rec += n_spk;
     if (o.spike_count) *o.spike_count += n_spk;
+    *o.now_dev = now + 1;
   }
 }
 
@@ -306,19 +317,20 @@ __global__ void __launch_bounds__(T256) deliver_kernel(const uint32_t* src_nodes
 
 extern "C" int smx_lif_update(double* v, int32_t* ref, const double* decay, const double* v_rest,
                               const double* v_reset, const double* v_th, const int32_t* ref_steps,
-                              const double* i_e, uint32_t n, double* ring, int n_ports, int L, int64_t now,
-                              uint32_t* spike_bits, void* stream) {
+                              const double* i_e, uint32_t n, double* ring, int n_ports, int L,
+                              const int64_t* now_dev, uint32_t* spike_bits, void* stream) {
   if (n == 0) return 0;
   LifState s{v, ref, decay, v_rest, v_reset, v_th, ref_steps, i_e};
-  smx_count_launch(); lif_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(s, n, ring, n_ports, L, now, spike_bits);
+  smx_count_launch(); lif_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(s, n, ring, n_ports, L, now_dev, spike_bits);
   SMX_LAUNCH_CHECK();
   return 0;
 }
 
-extern "C" int smx_poisson_emit(const uint8_t* counts, uint32_t n_t, const uint32_t* rows, double w,
-                                double* ring_slot_port, void* stream) {
+extern "C" int smx_poisson_emit(const uint8_t* counts, int S, uint32_t n_t, const uint32_t* rows, double w,
+                                double* ring, uint32_t n_rows, int n_ports, int L, int delay, int port,
+                                const int64_t* now_dev, void* stream) {
   if (n_t == 0) return 0;
-  smx_count_launch(); poisson_emit_kernel<<<nblk(n_t), T256, 0, (cudaStream_t)stream>>>(counts, n_t, rows, w, ring_slot_port);
+  smx_count_launch(); poisson_emit_kernel<<<nblk(n_t), T256, 0, (cudaStream_t)stream>>>(counts, S, n_t, rows, w, ring, n_rows, n_ports, L, delay, port, now_dev);
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -335,8 +347,8 @@ struct SmxRoutes {
 };
 
 extern "C" int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uint32_t* row2node,
-                          const int64_t* gid, int64_t now, uint32_t* src_nodes, uint32_t* src_steps,
-                          uint32_t* n_src, uint32_t src_cap, int record, int64_t* rec, uint64_t* n_rec,
+                          const int64_t* gid, int64_t* now_dev, uint32_t* src_nodes, uint32_t* src_steps,
+                          uint32_t* n_src, uint32_t src_cap, const int* record_dev, int64_t* rec, uint64_t* n_rec,
                           uint64_t rec_cap, uint32_t* spike_count, int* overflow, const SmxRoutes* p2p,
                           const SmxRoutes* grp, void* stream) {
   SpikeOut o;
@@ -344,12 +356,12 @@ extern "C" int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uin
   o.n_rows = n_rows;
   o.row2node = row2node;
   o.gid = gid;
-  o.now = now;
+  o.now_dev = now_dev;
+  o.record_dev = record_dev;
   o.src_nodes = src_nodes;
   o.src_steps = src_steps;
   o.n_src = n_src;
   o.src_cap = src_cap;
-  o.record = record;
   o.rec = rec;
   o.n_rec = n_rec;
   o.rec_cap = rec_cap;

@@ -251,6 +251,9 @@ class Cluster:
         self.classes: list[tuple] = []      # (weight, delay, port)
         self.class_index: dict = {}
         self.any_p2p = False
+        self.min_remote_delay = None
+        self.use_graphs = True
+        self._graph = None
         self._pg = None
         self.messages = {p: 0 for p in PHASES}
         self.bytes = {p: 0 for p in PHASES}
@@ -570,6 +573,17 @@ class Cluster:
             return int(conn.n_total) / n_src < self.cfg.flag_threshold
         return False
 
+    def _note_remote_delay(self, syn: SynSpec):
+        d = syn.delay_steps
+        if isinstance(d, tuple):
+            m = int(d[1])
+        elif isinstance(d, (list, np.ndarray)):
+            m = int(np.min(d)) if len(d) else None
+        else:
+            m = int(d)
+        if m is not None:
+            self.min_remote_delay = m if self.min_remote_delay is None else min(self.min_remote_delay, m)
+
     def _bump_pair(self, sr, tr) -> int:
         idx = self.pair_ctr.get((sr, tr), 0) + 1
         self.pair_ctr[(sr, tr)] = idx
@@ -595,6 +609,7 @@ class Cluster:
             self.any_p2p = True
         if not self.is_local(tr):
             self.images_made[tr] = True  # the target may have grown images
+        self._note_remote_delay(syn)
         idx = self._bump_pair(sr, tr)
         flag = self._flagging(conn, n_src, n_tgt)
         k_src = self._key(("remote-src", sr, tr, idx))
@@ -729,6 +744,8 @@ class Cluster:
                 raise ValueError("target populations must be non-empty")
             if not self.is_local(tr) and any(r != tr for r in src_ranks):
                 self.images_made[tr] = True
+            if any(r != tr for r in src_ranks):
+                self._note_remote_delay(syn)
             key = self._key(("dist-indegree", call_idx, tr))
             n = k_in * len(tg)
             need_bits = self.is_local(tr) or any(
@@ -866,6 +883,8 @@ class Cluster:
                                       [np.empty(0, np.int64)])
                 if len(np.unique(gids)) != len(gids):
                     raise ConsistencyError("neuron gids must be globally unique")
+            self.block = self._block_size()
+            self.group_slots = {g: i for i, g in enumerate(sorted(self.groups))}
             for st in self.ranks.values():
                 self._prepare_rank(st)
         self.has_p2p = self._compute_has_p2p()
@@ -983,7 +1002,6 @@ class Cluster:
                 st.I[key] = torch.full((st.H[key].numel(),), -1, dtype=torch.int64, device=dev)
         # routing tables: T/P from mirrors (dest = target rank, ascending),
         # G/Q from own rosters (dest = group slot, groups ascending)
-        self.group_slots = {g: i for i, g in enumerate(sorted(self.groups))}
         st.TP = self._routes(st, [(tr, st.mirrors[tr].t) for tr in sorted(st.mirrors)])
         own = [(self.group_slots[g], st.rosters[(g, sr)].t) for (g, sr) in sorted(st.rosters) if sr == st.rank]
         st.GQ = self._routes(st, own)
@@ -1029,9 +1047,13 @@ class Cluster:
     def _alloc_propagation(self, st):
         dev = st.device
         N = st.N
+        B = self.block
         st.spike_bits = torch.zeros(max(_words(N), 1), dtype=torch.int32, device=dev)
-        # packets: p2p buffers per destination rank, collective per group slot
-        st.pk_cap = max(N, 1)
+        st.now_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        st.record_dev = torch.zeros(1, dtype=torch.int32, device=dev)
+        # packets of one exchange block (B steps): p2p per destination rank,
+        # collective per group slot; entries are (position, emission step)
+        st.pk_cap = max(N, 1) * B
         st.p2p_packets = torch.zeros(self.n_ranks * st.pk_cap * 2, dtype=torch.int32, device=dev)
         st.p2p_counts = torch.zeros(self.n_ranks, dtype=torch.int32, device=dev)
         ng = max(len(self.groups), 1)
@@ -1044,15 +1066,17 @@ class Cluster:
         st.wprefix = torch.zeros(st.src_cap, dtype=torch.int32, device=dev)
         st.n_work = torch.zeros(1, dtype=torch.int32, device=dev)
         st.err = torch.zeros(1, dtype=torch.int32, device=dev)
-        st.rec_cap = 1 << 20
+        st.rec_cap = 1 << 22
         st.rec = torch.zeros(2 * st.rec_cap, dtype=torch.int64, device=dev)
         st.n_rec = torch.zeros(1, dtype=torch.int64, device=dev)
         st.spike_total = torch.zeros(1, dtype=torch.int32, device=dev)
-        st.recorded: list[np.ndarray] = []
         st.p2p_desc = ctypes_routes_desc(st.TP, st.p2p_packets, st.p2p_counts, self.n_ranks, st.pk_cap)
         st.g_desc = ctypes_routes_desc(st.GQ, st.g_packets, st.g_counts, len(self.groups), st.pk_cap)
-        # Poisson devices: counts generated in batches of S steps
-        st.pois_steps = 64
+        st.graph = None
+        # Poisson devices: numpy-exact counts generated for S steps at a time
+        # (S a multiple of the exchange block, so a block never straddles two
+        # batches and can be replayed from a CUDA graph)
+        st.pois_steps = B * max(1, -(-64 // B))
         for d in st.devices:
             nt = len(d["targets"])
             rows = np.asarray(st_node2row_host(st, d["targets"]), dtype=np.int64)
@@ -1073,57 +1097,123 @@ class Cluster:
             d["batch0"] = -1
 
     # -------------------------------------------------------------- propagation
-    def _poisson(self, st, now):
+    def _block_size(self) -> int:
+        """Steps per exchange round.  A spike emitted at step t over a remote
+        connection of delay d >= D is consumed at t + d, so exchanging every D
+        = min remote delay steps delivers every spike before its slot is read
+        (the script-level minimum is identical on every rank)."""
+        if self.n_ranks == 1 or self.min_remote_delay is None:
+            return 16
+        return int(max(1, min(self.min_remote_delay, 32)))
+
+    def _poisson_batch(self, st, now):
+        """Counts for steps [now, now + S) of every active device (now % S == 0)."""
         S = st.pois_steps
         for d in st.devices:
-            if not d["active"]:
+            if not d["active"] or d["batch0"] == now:
                 continue
-            b0 = now - now % S
-            if d["batch0"] != b0:
-                cin = d["cursor"][d["ping"]:]
-                cout = d["cursor"][1 - d["ping"]:]
-                call("smx_poisson_counts", d["key"][0], d["key"][1], _ptr(cin), d["enlam"], S * d["nt"],
-                     d["chunks"], _ptr(d["ws"]), _ptr(d["counts"]), _ptr(cout), _ptr(st.err), st.stream)
-                d["ping"] = 1 - d["ping"]
-                d["batch0"] = b0
-            slot = (now + d["delay"]) % st.L
-            off = (slot * st.P + d["port"]) * st.N
-            call("smx_poisson_emit", _ptr(d["counts"][(now - b0) * d["nt"]:]), d["nt"], _ptr(d["rows"]),
-                 d["weight"], _ptr(st.ring[off:]), st.stream)
+            cin = d["cursor"][d["ping"]:]
+            cout = d["cursor"][1 - d["ping"]:]
+            call("smx_poisson_counts", d["key"][0], d["key"][1], _ptr(cin), d["enlam"], S * d["nt"],
+                 d["chunks"], _ptr(d["ws"]), _ptr(d["counts"]), _ptr(cout), _ptr(st.err), st.stream)
+            d["ping"] = 1 - d["ping"]
+            d["batch0"] = now
+
+    def _step_kernels(self, st):
+        """One step of one rank, every argument device-resident (graph-safe):
+        consume + LIF, Poisson emission, spike list / raster / packets, local
+        delivery (sm/engine.py:285-296)."""
+        sk = st.stream
+        call("smx_lif_update", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
+             _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, _ptr(st.now_dev),
+             _ptr(st.spike_bits), sk)
+        for d in st.devices:
+            if d["active"]:
+                call("smx_poisson_emit", _ptr(d["counts"]), st.pois_steps, d["nt"], _ptr(d["rows"]), d["weight"],
+                     _ptr(st.ring), st.N, st.P, st.L, d["delay"], d["port"], _ptr(st.now_dev), sk)
+        call("smx_spikes", _ptr(st.spike_bits), st.N, _ptr(st.row2node_t), _ptr(st.gid_t), _ptr(st.now_dev),
+             _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.record_dev),
+             _ptr(st.rec), _ptr(st.n_rec), st.rec_cap, _ptr(st.spike_total), _ptr(st.err),
+             ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), sk)
+        self._deliver(st)
 
     def _deliver(self, st):
         call("smx_deliver", _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), _ptr(st.wprefix),
              _ptr(st.n_work), _ptr(st.first_index), _ptr(st.payload), _ptr(st.cls_w), _ptr(st.cls_delay),
              _ptr(st.cls_port), _ptr(st.ww), _ptr(st.wm), _ptr(st.ring), st.N, st.P, st.L, 0, st.stream)
 
-    def step(self):
-        """sm/engine.py:277-310; returns nothing (spikes stay on the device)."""
-        if not self.prepared:
-            raise ConsistencyError("prepare() the cluster before stepping")
+    def _block_body(self, n_steps: int):
+        for _ in range(n_steps):
+            for st in self.ranks.values():
+                self._step_kernels(st)
+        if self.n_ranks > 1 and not self.distributed:
+            self._exchange_local()
+
+    def _run_block(self, n_steps: int, use_graph: bool):
+        """n_steps steps of every local rank, then one exchange round."""
         now = self.now
         for st in self.ranks.values():
-            sk = st.stream
-            st.n_src.zero_()
+            if now % st.pois_steps == 0 or any(d["active"] and d["batch0"] != now - now % st.pois_steps
+                                               for d in st.devices):
+                self._poisson_batch(st, now - now % st.pois_steps)
+        if use_graph:
+            if self._graph is None:
+                for st in self.ranks.values():
+                    torch.cuda.synchronize(st.device)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._block_body(n_steps)
+                self._graph = g
+            self._graph.replay()
+        else:
+            self._block_body(n_steps)
+        if self.n_ranks > 1 and self.distributed:
+            self._exchange_nccl()
+        for st in self.ranks.values():
             st.p2p_counts.zero_()
             st.g_counts.zero_()
-            call("smx_lif_update", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
-                 _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, now,
-                 _ptr(st.spike_bits), sk)
-            self._poisson(st, now)
-            call("smx_spikes", _ptr(st.spike_bits), st.N, _ptr(st.row2node_t), _ptr(st.gid_t), now,
-                 _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, 1 if self._recording else 0,
-                 _ptr(st.rec), _ptr(st.n_rec), st.rec_cap, _ptr(st.spike_total), _ptr(st.err),
-                 ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), sk)
-            self._deliver(st)
-        if self.n_ranks > 1:
-            self._exchange(now)
-        self.now += 1
+        self._count_rounds(n_steps)
+        self.now += n_steps
 
-    def _exchange(self, now):
+    def _count_rounds(self, n_steps):
+        """Message counters as the reference's lockstep transport would count
+        them: one p2p round (n(n-1) messages) and one allgather per group per
+        step (sm/transport.py:128,165)."""
+        if self.n_ranks == 1:
+            return
+        per = (self.n_ranks * (self.n_ranks - 1) if self.has_p2p else 0)
+        per += sum(len(self.groups[g]) for g in self.group_ids)
+        self.messages["propagation"] += per * n_steps
+
+    def step(self):
+        """One step of every rank including its exchange round (sm/engine.py:277-310)."""
+        if not self.prepared:
+            raise ConsistencyError("prepare() the cluster before stepping")
+        self._set_record(self._recording)
+        self._run_block(1, use_graph=False)
+
+    def _set_record(self, on: bool):
+        for st in self.ranks.values():
+            st.record_dev.fill_(1 if on else 0)
+
+    def _advance(self, n_steps: int):
+        """Advance n_steps in exchange blocks; whole blocks aligned on the block
+        size replay one captured CUDA graph."""
+        B = self.block
+        done = 0
+        while done < n_steps:
+            if self.now % B == 0 and n_steps - done >= B:
+                self._run_block(B, use_graph=self.use_graphs)
+                done += B
+            else:
+                k = min(n_steps - done, B - self.now % B)
+                self._run_block(k, use_graph=False)
+                done += k
+
+    def _exchange_local(self):
         """One p2p round (if any p2p routing exists) then one allgather round
-        per group (sm/engine.py:297-308), as device-resident packet reads."""
-        if self.distributed:
-            return self._exchange_nccl(now)
+        per group (sm/engine.py:297-308), as device-resident packet reads
+        between ranks of this process."""
         for st in self.ranks.values():
             st.n_src.zero_()
         if self.has_p2p:
@@ -1139,7 +1229,6 @@ class Cluster:
                     cnt = src.p2p_counts[st.rank:]
                     call("smx_unpack", _ptr(pk), _ptr(cnt), _ptr(rl[1]), rl[1].numel(), _ptr(st.src_nodes),
                          _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
-            self.messages["propagation"] += self.n_ranks * (self.n_ranks - 1)
         for g in self.group_ids:
             slot = self.group_slots[g]
             members = self.groups[g]
@@ -1156,19 +1245,18 @@ class Cluster:
                     cnt = src.g_counts[slot:]
                     call("smx_unpack", _ptr(pk), _ptr(cnt), _ptr(lk), lk.numel(), _ptr(st.src_nodes),
                          _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
-            self.messages["propagation"] += len(members)
         for st in self.ranks.values():
             self._deliver(st)
 
-    def _exchange_nccl(self, now):
-        """One process per rank: the same rounds over NCCL.  Counts travel
-        first (device int32), then only max-count packets."""
+    def _exchange_nccl(self):
+        """One process per rank: the same rounds over NCCL, once per block.
+        Counts travel first (device int32), then only max-count packets."""
         dist = torch.distributed
         (st,) = self.ranks.values()
         me = st.rank
         st.n_src.zero_()
         if self._pg is None:
-            self._pg = {g: dist.new_group(list(self.groups[g])) for g in sorted(self.groups)}
+            self._pg = {g: dist.new_group(sorted(self.groups[g])) for g in sorted(self.groups)}
         if self.has_p2p:
             send_c = st.p2p_counts.clone()
             recv_c = torch.empty_like(send_c)
@@ -1176,8 +1264,8 @@ class Cluster:
             sc, rc = send_c.cpu().numpy(), recv_c.cpu().numpy()
             inp = torch.cat([st.p2p_packets[d * st.pk_cap * 2: d * st.pk_cap * 2 + 2 * int(sc[d])]
                              for d in range(self.n_ranks)])
-            out = torch.empty(int(2 * rc.sum()), dtype=torch.int32, device=st.device)
-            dist.all_to_all_single(out, inp, [2 * int(x) for x in rc], [2 * int(x) for x in sc])
+            out = torch.empty(max(int(2 * rc.sum()), 1), dtype=torch.int32, device=st.device)
+            dist.all_to_all_single(out[: int(2 * rc.sum())], inp, [2 * int(x) for x in rc], [2 * int(x) for x in sc])
             off = 0
             for sr in range(self.n_ranks):
                 n = int(rc[sr])
@@ -1189,7 +1277,6 @@ class Cluster:
                 elif n and sr != me:
                     raise ProtocolError(f"rank {me}: spikes from rank {sr} but no map for that pair")
                 off += 2 * n
-            self.messages["propagation"] += self.n_ranks * (self.n_ranks - 1)
             self.bytes["propagation"] += 8 * int(sc.sum())
         for g in self.group_ids:
             members = self.groups[g]
@@ -1200,13 +1287,14 @@ class Cluster:
             nm = len(members)
             allc = torch.empty(nm, dtype=torch.int32, device=st.device)
             dist.all_gather_into_tensor(allc, st.g_counts[slot: slot + 1], group=pg)
-            cmax = int(allc.max().item())
+            ac = allc.cpu().numpy()
+            cmax = int(ac.max())
             if cmax:
                 send = st.g_packets[slot * st.pk_cap * 2: slot * st.pk_cap * 2 + 2 * cmax]
                 recv = torch.empty(nm * 2 * cmax, dtype=torch.int32, device=st.device)
                 dist.all_gather_into_tensor(recv, send.contiguous(), group=pg)
                 for i, sr in enumerate(sorted(members)):
-                    if sr == me:
+                    if sr == me or ac[i] == 0:
                         continue
                     lk = st.I.get((g, sr))
                     if lk is None:
@@ -1214,8 +1302,7 @@ class Cluster:
                     call("smx_unpack", _ptr(recv[i * 2 * cmax:]), _ptr(allc[i:]), _ptr(lk), lk.numel(),
                          _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err),
                          st.stream)
-            self.messages["propagation"] += nm
-            self.bytes["propagation"] += 8 * int(st.g_counts[slot].item())
+            self.bytes["propagation"] += 8 * int(ac[sorted(members).index(me)])
         self._deliver(st)
 
     _recording = False
@@ -1229,19 +1316,20 @@ class Cluster:
         steps = self.cfg.steps_for(model_ms)
         self.phase = "propagation"
         self._recording = False
+        self._set_record(False)
         self._sync()
         t0 = time.perf_counter()
-        for _ in range(warm):
-            self.step()
+        self._advance(warm)
         self._sync()
         warm_s = time.perf_counter() - t0
         self._recording = record
+        self._set_record(record)
         t1 = time.perf_counter()
-        for _ in range(steps):
-            self.step()
+        self._advance(steps)
         self._sync()
         prop = time.perf_counter() - t1
         self._recording = False
+        self._set_record(False)
         self.timers.propagation += prop
         self._check_errors()
         model_s = steps * self.cfg.resolution_ms * 1e-3

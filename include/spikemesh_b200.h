@@ -142,6 +142,23 @@ int smx_deliver(const uint32_t* src_nodes, const uint32_t* src_steps, const uint
                 const uint32_t* wide_meta, double* ring, uint32_t n_rows, int n_ports, int L, int grid,
                 void* stream);
 
+/* One complete local step (sm/engine.py:285-296) in three launches: fused
+ * consume + LIF + Poisson emission + spike compaction + raster + packet
+ * routing; local delivery; step-counter advance.  devs_host: array of
+ * {u8* counts[S][n_t], u32* rows, u32 n_t, double w, int delay, int port}
+ * (Poisson devices with unique target rows); the step is *now_dev +
+ * step_offset; ctr: 2 x u64 list counters indexed by step parity; owner:
+ * work item -> list entry scratch. */
+int smx_step(double* v, int32_t* ref, const double* decay, const double* v_rest, const double* v_reset,
+             const double* v_th, const int32_t* ref_steps, const double* i_e, uint32_t n, double* ring, int n_ports,
+             int L, int64_t* now_dev, int step_offset, const int* record_dev, int S, const void* devs_host, int n_dev,
+             const uint32_t* row2node, const int64_t* gid, const int64_t* first, uint32_t* src_nodes,
+             uint32_t* src_steps, uint32_t* wbase, uint32_t* owner, uint32_t owner_cap, unsigned long long* ctr,
+             uint32_t src_cap, int64_t* rec, unsigned long long* n_rec, uint64_t rec_cap, int* err,
+             const void* p2p_host, const void* grp_host, const uint32_t* payload, const double* cls_w,
+             const uint32_t* cls_delay, const uint32_t* cls_port, const double* wide_w, const uint32_t* wide_meta,
+             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,44 +123,82 @@ __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
   for (int q = tid; q < PC / 32; q += P_THREADS) J.s0[(size_t)c * (PC / 32) + q] = S0[q];
 }
 
-__global__ void group_kernel(PoisJob J) {
+// One CTA per group of PG chunks: the group's entry->exit tables are staged
+// in shared memory, then thread e composes them sequentially from entry e.
+__global__ void __launch_bounds__(PE) group_kernel(PoisJob J) {
+  __shared__ uint8_t ex[PG * PE];
+  __shared__ uint16_t ct[PG * PE];
   const int g = blockIdx.x, e0 = threadIdx.x;
-  if (e0 >= PE) return;
+  const int c0 = g * PG, c1 = min(J.n_chunks, c0 + PG), nc = c1 - c0;
+  for (int q = threadIdx.x; q < nc * PE; q += blockDim.x) {
+    ex[q] = J.ex[(size_t)c0 * PE + q];
+    ct[q] = J.cnt[(size_t)c0 * PE + q];
+  }
+  __syncthreads();
   int e = e0;
   uint32_t tot = 0;
-  const int c0 = g * PG, c1 = min(J.n_chunks, c0 + PG);
-  for (int c = c0; c < c1; ++c) {
-    tot += J.cnt[(size_t)c * PE + e];
-    e = J.ex[(size_t)c * PE + e];
+  for (int c = 0; c < nc; ++c) {
+    tot += ct[c * PE + e];
+    e = ex[c * PE + e];
   }
   J.gex[(size_t)g * PE + e0] = (uint8_t)e;
   J.gcnt[(size_t)g * PE + e0] = tot;
 }
 
-__global__ void across_kernel(PoisJob J, int n_groups, uint8_t* gentry, uint64_t* gbase) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int e = (int)(*J.w0_dev & 3);
-  uint64_t k = 0;
-  for (int g = 0; g < n_groups; ++g) {
-    gentry[g] = (uint8_t)e;
-    gbase[g] = k;
-    k += J.gcnt[(size_t)g * PE + e];
-    e = J.gex[(size_t)g * PE + e];
+// Single CTA: the groups' tables are staged in shared memory (in slices),
+// then one thread walks the groups in order.
+constexpr int ACROSS_SLICE = 96;  // groups per shared-memory slice
+__global__ void __launch_bounds__(256) across_kernel(PoisJob J, int n_groups, uint8_t* gentry, uint64_t* gbase) {
+  __shared__ uint8_t gx[ACROSS_SLICE * PE];
+  __shared__ uint32_t gc[ACROSS_SLICE * PE];
+  __shared__ int e_sh;
+  __shared__ unsigned long long k_sh;
+  if (threadIdx.x == 0) { e_sh = (int)(*J.w0_dev & 3); k_sh = 0; }
+  for (int g0 = 0; g0 < n_groups; g0 += ACROSS_SLICE) {
+    const int ng = min(ACROSS_SLICE, n_groups - g0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < ng * PE; q += blockDim.x) {
+      gx[q] = J.gex[(size_t)g0 * PE + q];
+      gc[q] = J.gcnt[(size_t)g0 * PE + q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int e = e_sh;
+      unsigned long long k = k_sh;
+      for (int g = 0; g < ng; ++g) {
+        gentry[g0 + g] = (uint8_t)e;
+        gbase[g0 + g] = k;
+        k += gc[g * PE + e];
+        e = gx[g * PE + e];
+      }
+      e_sh = e;
+      k_sh = k;
+    }
   }
-  if (k < J.n) atomicExch(J.err, 13);  // window too small
+  __syncthreads();
+  if (threadIdx.x == 0 && k_sh < J.n) atomicExch(J.err, 13);  // window too small
 }
 
-__global__ void within_kernel(PoisJob J, const uint8_t* gentry, const uint64_t* gbase) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g * PG >= J.n_chunks) return;
+// One CTA per group: chunk tables staged in shared memory, one thread walks
+// the group's chunks from the group's true entry.
+__global__ void __launch_bounds__(PE) within_kernel(PoisJob J, const uint8_t* gentry, const uint64_t* gbase) {
+  __shared__ uint8_t ex[PG * PE];
+  __shared__ uint16_t ct[PG * PE];
+  const int g = blockIdx.x;
+  const int c0 = g * PG, c1 = min(J.n_chunks, c0 + PG), nc = c1 - c0;
+  for (int q = threadIdx.x; q < nc * PE; q += blockDim.x) {
+    ex[q] = J.ex[(size_t)c0 * PE + q];
+    ct[q] = J.cnt[(size_t)c0 * PE + q];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   int e = gentry[g];
   uint64_t k = gbase[g];
-  const int c0 = g * PG, c1 = min(J.n_chunks, c0 + PG);
-  for (int c = c0; c < c1; ++c) {
-    J.entry[c] = (uint8_t)e;
-    J.kbase[c] = k;
-    k += J.cnt[(size_t)c * PE + e];
-    e = J.ex[(size_t)c * PE + e];
+  for (int c = 0; c < nc; ++c) {
+    J.entry[c0 + c] = (uint8_t)e;
+    J.kbase[c0 + c] = k;
+    k += ct[c * PE + e];
+    e = ex[c * PE + e];
   }
 }
 
@@ -261,8 +299,8 @@ extern "C" int smx_poisson_counts(uint64_t k0, uint64_t k1, const uint64_t* curs
   J.err = err;
   smx_count_launch(); chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
-  smx_count_launch(); across_kernel<<<1, 32, 0, st>>>(J, ng, gentry, gbase);
-  smx_count_launch(); within_kernel<<<(ng + 127) / 128, 128, 0, st>>>(J, gentry, gbase);
+  smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
+  smx_count_launch(); within_kernel<<<ng, PE, 0, st>>>(J, gentry, gbase);
   smx_count_launch(); emit_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
   SMX_LAUNCH_CHECK();
   return 0;

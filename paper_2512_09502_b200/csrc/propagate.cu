@@ -22,6 +22,7 @@
 // are exact for the dyadic weights of the reference models, so atomic order
 // does not change any bit; for non-dyadic weights V stays within the stated
 // tolerance.
+#include <algorithm>
 #include "common.cuh"
 
 namespace {
@@ -309,6 +310,218 @@ __global__ void __launch_bounds__(T256) deliver_kernel(const uint32_t* src_nodes
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused step kernel: consume + LIF (all real rows), Poisson emission (every
+// device with unique target rows, thread t = target t), spike compaction
+// with warp-aggregated atomics, raster append, packet routing and the local
+// delivery work list -- one launch per step.  Spike order inside the lists
+// is not the reference's ascending order; delivery sums are exact for dyadic
+// weights and the merged raster is sorted, so results are unchanged.
+// ---------------------------------------------------------------------------
+constexpr int MAX_FUSED_DEV = 8;
+
+struct FusedDev {
+  const uint8_t* counts;  // [S][n_t]
+  const uint32_t* rows;
+  uint32_t n_t;
+  double w;
+  int delay, port;
+};
+
+struct StepArgs {
+  LifState s;
+  uint32_t n;
+  double* ring;
+  int n_ports, L;
+  int64_t* now_dev;
+  const int* record_dev;
+  int S;
+  int n_dev;
+  FusedDev dev[MAX_FUSED_DEV];
+  const uint32_t* row2node;
+  const int64_t* gid;
+  const int64_t* first;           // CSR of the store (for work chunks)
+  uint32_t* src_nodes;
+  uint32_t* src_steps;
+  uint32_t* wbase;                // first work item of each listed source
+  uint32_t* owner;                // work item -> list entry
+  uint32_t owner_cap;
+  unsigned long long* ctr;        // [2] (n_src << 32 | n_work), by step parity
+  uint32_t src_cap;
+  int64_t* rec;
+  unsigned long long* n_rec;
+  uint64_t rec_cap;
+  int* err;
+  int step_offset;                // now = *now_dev (block start) + step_offset
+  Routes p2p, grp;
+};
+
+__device__ __forceinline__ void route_spike(const Routes& R, uint32_t node, int64_t now, int* err) {
+  if (R.n_dest == 0) return;
+  const int64_t a = R.first[node], b = R.first[node + 1];
+  for (int64_t e = a; e < b; ++e) {
+    const int d = R.dest[e];
+    const uint32_t q = atomicAdd(&R.counts[d], 1u);
+    if (q < R.cap) {
+      R.packets[2 * ((size_t)d * R.cap + q)] = R.pos[e];
+      R.packets[2 * ((size_t)d * R.cap + q) + 1] = (uint32_t)now;
+    } else {
+      atomicExch(err, 3);
+    }
+  }
+}
+
+__device__ __noinline__ void spike_lists(const StepArgs& A, uint32_t i, int lane, int64_t now, int par, bool spk,
+                                              uint32_t ball) {
+  // local delivery list: (index, work base) reserved with one 64-bit atomic per warp
+  uint32_t node = 0, chunks = 0;
+  if (spk) {
+    node = A.row2node[i];
+    const int64_t len = A.first[node + 1] - A.first[node];
+    chunks = (uint32_t)((len + CHUNK - 1) / CHUNK);
+  }
+  uint32_t cpre = smx::warp_incl_scan(chunks);
+  const uint32_t ctot = __shfl_sync(0xffffffffu, cpre, 31);
+  cpre -= chunks;
+  const int leader = __ffs(ball) - 1;
+  unsigned long long old = 0;
+  if (lane == leader)
+    old = atomicAdd(&A.ctr[par], ((unsigned long long)__popc(ball) << 32) | (unsigned long long)ctot);
+  old = __shfl_sync(0xffffffffu, old, leader);
+  const int record = *A.record_dev;
+  unsigned long long rbase = 0;
+  if (record && lane == leader) rbase = atomicAdd(A.n_rec, (unsigned long long)__popc(ball));
+  rbase = __shfl_sync(0xffffffffu, rbase, leader);
+  if (!spk) return;
+  const uint32_t rank = __popc(ball & ((1u << lane) - 1));
+  const uint32_t idx = (uint32_t)(old >> 32) + rank;
+  if (idx < A.src_cap) {
+    A.src_nodes[idx] = node;
+    A.src_steps[idx] = (uint32_t)now;
+    const uint32_t wb = (uint32_t)old + cpre;
+    A.wbase[idx] = wb;
+    for (uint32_t j = 0; j < chunks; ++j) {
+      if (wb + j < A.owner_cap) A.owner[wb + j] = idx;
+      else atomicExch(A.err, 5);
+    }
+  } else {
+    atomicExch(A.err, 1);
+  }
+  if (record) {
+    const unsigned long long ri = rbase + rank;
+    if (ri < A.rec_cap) { A.rec[2 * ri] = now; A.rec[2 * ri + 1] = A.gid[i]; }
+    else atomicExch(A.err, 2);
+  }
+  route_spike(A.p2p, node, now, A.err);
+  route_spike(A.grp, node, now, A.err);
+}
+
+
+__global__ void __launch_bounds__(T256) step_kernel(StepArgs A) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t now = *A.now_dev + A.step_offset;
+  const int par = (int)(now & 1);
+  if (i == 0) A.ctr[par ^ 1] = 0ULL;  // next step's list (its last reader finished)
+  // Poisson emission into slot (now + delay) % L, thread t = target t
+  for (int k = 0; k < A.n_dev; ++k) {
+    const FusedDev& D = A.dev[k];
+    if (i < D.n_t) {
+      const uint32_t c = D.counts[(size_t)(now % A.S) * D.n_t + i];
+      if (c) {
+        const int slot = (int)((now + D.delay) % A.L);
+        double* cell = A.ring + ((size_t)slot * A.n_ports + D.port) * A.n + D.rows[i];
+        *cell = __dadd_rn(*cell, __dmul_rn(D.w, (double)c));
+      }
+    }
+  }
+  // consume + LIF (sm/dynamics.py:191-204, kernels/_speedups.pyx:17-35)
+  bool spk = false;
+  if (i < A.n) {
+    const int slot = (int)(now % A.L);
+    double* base = A.ring + (size_t)slot * A.n_ports * A.n;
+    double in = base[i];
+    base[i] = 0.0;
+    for (int p = 1; p < A.n_ports; ++p) {
+      in = __dadd_rn(in, base[(size_t)p * A.n + i]);
+      base[(size_t)p * A.n + i] = 0.0;
+    }
+    in = __dadd_rn(in, A.s.i_e[i]);
+    const int32_t r = A.s.ref[i];
+    if (r > 0) {
+      A.s.ref[i] = r - 1;
+      A.s.v[i] = A.s.v_reset[i];
+    } else {
+      const double vr = A.s.v_rest[i];
+      const double integ = __dadd_rn(__dadd_rn(vr, __dmul_rn(__dsub_rn(A.s.v[i], vr), A.s.decay[i])), in);
+      if (integ >= A.s.v_th[i]) {
+        spk = true;
+        A.s.v[i] = A.s.v_reset[i];
+        A.s.ref[i] = A.s.ref_steps[i];
+      } else {
+        A.s.v[i] = integ;
+      }
+    }
+  }
+  const uint32_t ball = __ballot_sync(0xffffffffu, spk);
+  if (ball) spike_lists(A, i, lane, now, par, spk, ball);
+}
+
+
+template <bool WIDE>
+__global__ void __launch_bounds__(T256) deliver_step_kernel(const uint32_t* src_nodes, const uint32_t* src_steps,
+                                                            const uint32_t* wbase, const uint32_t* owner,
+                                                            const unsigned long long* ctr,
+                                                            const int64_t* now_dev, const int64_t* first,
+                                                            const uint32_t* payload, SynTable syn,
+                                                            const double* wide_w, const uint32_t* wide_meta,
+                                                            double* ring, uint32_t n_rows, int n_ports, int L,
+                                                            int step_offset) {
+  const unsigned long long c = ctr[(*now_dev + step_offset) & 1];
+  const uint32_t nw = (uint32_t)(c & 0xffffffffULL);
+  if (nw == 0) return;
+  __shared__ double cw[256];
+  __shared__ uint32_t cd[256], cp[256];
+  if (!WIDE) {
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) {
+      cw[k] = syn.w[k];
+      cd[k] = syn.delay[k];
+      cp[k] = syn.port[k];
+    }
+    __syncthreads();
+  }
+  const size_t slot_stride = (size_t)n_ports * n_rows;
+  for (uint32_t w = blockIdx.x; w < nw; w += gridDim.x) {
+    const uint32_t e = owner[w];  // list entry whose chunk range holds w
+    const uint32_t node = src_nodes[e];
+    const int64_t now = src_steps[e];
+    const int64_t a = first[node] + (int64_t)(w - wbase[e]) * CHUNK;
+    int64_t b = first[node + 1];
+    if (b > a + CHUNK) b = a + CHUNK;
+    for (int64_t k = a + threadIdx.x; k < b; k += blockDim.x) {
+      const uint32_t pl = payload[k];
+      double wt;
+      uint32_t d, port, row;
+      if (WIDE) {
+        const uint32_t m = wide_meta[k];
+        wt = wide_w[k];
+        d = m & 0xffffffu;
+        port = m >> 24;
+        row = pl;
+      } else {
+        const uint32_t cl = pl >> SMX_ROW_BITS;
+        wt = cw[cl];
+        d = cd[cl];
+        port = cp[cl];
+        row = pl & SMX_ROW_MASK;
+      }
+      const int slot = (int)((now + d) % L);
+      atomicAdd(ring + slot * slot_stride + (size_t)port * n_rows + row, wt);
+    }
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -405,6 +618,84 @@ extern "C" int smx_deliver(const uint32_t* src_nodes, const uint32_t* src_steps,
   } else {
     smx_count_launch(); deliver_kernel<false><<<grid, T256, 0, st>>>(src_nodes, src_steps, n_src, wprefix, n_work, first, payload, syn,
                                                   wide_w, wide_meta, ring, n_rows, n_ports, L);
+  }
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+// Host mirror of the fused-device descriptor.
+struct SmxFusedDev {
+  const uint8_t* counts;
+  const uint32_t* rows;
+  uint32_t n_t;
+  double w;
+  int delay, port;
+};
+
+// One complete local step (sm/engine.py:285-296) in two launches: fused
+// LIF/Poisson/compaction/routing, then local delivery.  The step is
+// *now_dev + step_offset: the host sets *now_dev once per exchange block, so a
+// block of steps replays from one CUDA graph with no counter kernels.
+// ctr: 2 x u64 list counters indexed by step parity.
+extern "C" int smx_step(double* v, int32_t* ref, const double* decay, const double* v_rest, const double* v_reset,
+                        const double* v_th, const int32_t* ref_steps, const double* i_e, uint32_t n, double* ring,
+                        int n_ports, int L, int64_t* now_dev, int step_offset, const int* record_dev, int S,
+                        const SmxFusedDev* devs_host, int n_dev, const uint32_t* row2node, const int64_t* gid,
+                        const int64_t* first, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* wbase,
+                        uint32_t* owner, uint32_t owner_cap, unsigned long long* ctr, uint32_t src_cap, int64_t* rec, unsigned long long* n_rec,
+                        uint64_t rec_cap, int* err, const SmxRoutes* p2p, const SmxRoutes* grp,
+                        const uint32_t* payload, const double* cls_w, const uint32_t* cls_delay,
+                        const uint32_t* cls_port, const double* wide_w, const uint32_t* wide_meta, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_dev > MAX_FUSED_DEV) {
+    smx_set_error("smx_step: at most %d fused Poisson devices", MAX_FUSED_DEV);
+    return -1;
+  }
+  StepArgs A;
+  A.s = LifState{v, ref, decay, v_rest, v_reset, v_th, ref_steps, i_e};
+  A.n = n;
+  A.ring = ring;
+  A.n_ports = n_ports;
+  A.L = L;
+  A.now_dev = now_dev;
+  A.record_dev = record_dev;
+  A.S = S;
+  A.n_dev = n_dev;
+  uint32_t threads = n;
+  for (int k = 0; k < n_dev; ++k) {
+    A.dev[k] = FusedDev{devs_host[k].counts, devs_host[k].rows, devs_host[k].n_t, devs_host[k].w,
+                        devs_host[k].delay, devs_host[k].port};
+    threads = std::max(threads, devs_host[k].n_t);
+  }
+  A.row2node = row2node;
+  A.gid = gid;
+  A.first = first;
+  A.src_nodes = src_nodes;
+  A.src_steps = src_steps;
+  A.wbase = wbase;
+  A.owner = owner;
+  A.owner_cap = owner_cap;
+  A.ctr = ctr;
+  A.src_cap = src_cap;
+  A.rec = rec;
+  A.n_rec = n_rec;
+  A.rec_cap = rec_cap;
+  A.err = err;
+  A.step_offset = step_offset;
+  A.p2p = p2p ? Routes{p2p->first, p2p->dest, p2p->pos, p2p->n_dest, p2p->packets, p2p->counts, p2p->cap} : Routes{};
+  A.grp = grp ? Routes{grp->first, grp->dest, grp->pos, grp->n_dest, grp->packets, grp->counts, grp->cap} : Routes{};
+  if (threads == 0) threads = 1;
+  smx_count_launch(); step_kernel<<<nblk(threads), T256, 0, st>>>(A);
+  // deliver the step's local spikes: the list counters live in ctr[now & 1]
+  // (n_src << 32 | n_work); the deliver kernel picks the word by parity
+  SynTable syn{cls_w, cls_delay, cls_port};
+  const int grid = 148 * 8;
+  if (wide_w) {
+    smx_count_launch(); deliver_step_kernel<true><<<grid, T256, 0, st>>>(src_nodes, src_steps, wbase, owner, ctr, now_dev, first,
+                                                        payload, syn, wide_w, wide_meta, ring, n, n_ports, L, step_offset);
+  } else {
+    smx_count_launch(); deliver_step_kernel<false><<<grid, T256, 0, st>>>(src_nodes, src_steps, wbase, owner, ctr, now_dev, first,
+                                                         payload, syn, wide_w, wide_meta, ring, n, n_ports, L, step_offset);
   }
   SMX_LAUNCH_CHECK();
   return 0;

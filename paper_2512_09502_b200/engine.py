@@ -1095,6 +1095,21 @@ class Cluster:
             d["ws"] = torch.empty(int(_lib.lib().smx_poisson_workspace(d["chunks"])), dtype=torch.uint8,
                                   device=dev)
             d["batch0"] = -1
+        # fused step path: every active device hits each row at most once
+        act = [d for d in st.devices if d["active"]]
+        st.fused = len(act) <= 8 and all(len(np.unique(d["rows"].cpu().numpy())) == d["nt"] for d in act)
+        st.ctr = torch.zeros(2, dtype=torch.int64, device=dev)
+        st.owner_cap = st.n_records // 1024 + N + 16
+        st.owner = torch.zeros(st.owner_cap, dtype=torch.int32, device=dev)
+        st.fdev = (ctypes_fdev * max(len(act), 1))()
+        for k, d in enumerate(act):
+            st.fdev[k].counts = _ptr(d["counts"])
+            st.fdev[k].rows = _ptr(d["rows"])
+            st.fdev[k].n_t = d["nt"]
+            st.fdev[k].w = d["weight"]
+            st.fdev[k].delay = d["delay"]
+            st.fdev[k].port = d["port"]
+        st.n_fdev = len(act)
 
     # -------------------------------------------------------------- propagation
     def _block_size(self) -> int:
@@ -1119,11 +1134,20 @@ class Cluster:
             d["ping"] = 1 - d["ping"]
             d["batch0"] = now
 
-    def _step_kernels(self, st):
+    def _step_kernels(self, st, offset: int = 0):
         """One step of one rank, every argument device-resident (graph-safe):
         consume + LIF, Poisson emission, spike list / raster / packets, local
         delivery (sm/engine.py:285-296)."""
         sk = st.stream
+        if st.fused:
+            call("smx_step", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
+                 _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, _ptr(st.now_dev),
+                 offset, _ptr(st.record_dev), st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
+                 _ptr(st.gid_t), _ptr(st.first_index), _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.wprefix),
+                 _ptr(st.owner), st.owner_cap, _ptr(st.ctr), st.src_cap, _ptr(st.rec), _ptr(st.n_rec), st.rec_cap,
+                 _ptr(st.err), ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), _ptr(st.payload), _ptr(st.cls_w),
+                 _ptr(st.cls_delay), _ptr(st.cls_port), _ptr(st.ww), _ptr(st.wm), sk)
+            return
         call("smx_lif_update", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
              _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, _ptr(st.now_dev),
              _ptr(st.spike_bits), sk)
@@ -1143,9 +1167,9 @@ class Cluster:
              _ptr(st.cls_port), _ptr(st.ww), _ptr(st.wm), _ptr(st.ring), st.N, st.P, st.L, 0, st.stream)
 
     def _block_body(self, n_steps: int):
-        for _ in range(n_steps):
+        for j in range(n_steps):
             for st in self.ranks.values():
-                self._step_kernels(st)
+                self._step_kernels(st, j)
         if self.n_ranks > 1 and not self.distributed:
             self._exchange_local()
 
@@ -1156,6 +1180,8 @@ class Cluster:
             if now % st.pois_steps == 0 or any(d["active"] and d["batch0"] != now - now % st.pois_steps
                                                for d in st.devices):
                 self._poisson_batch(st, now - now % st.pois_steps)
+        for st in self.ranks.values():
+            st.now_dev.fill_(now)  # block start; fused steps add their offset
         if use_graph:
             if self._graph is None:
                 for st in self.ranks.values():
@@ -1457,6 +1483,11 @@ class ctypes_segment(ctypes.Structure):
 class ctypes_route(ctypes.Structure):
     _fields_ = [("bits", ctypes.c_void_p), ("excl", ctypes.c_void_p), ("nwords", ctypes.c_uint64),
                 ("dest", ctypes.c_int32)]
+
+
+class ctypes_fdev(ctypes.Structure):
+    _fields_ = [("counts", ctypes.c_void_p), ("rows", ctypes.c_void_p), ("n_t", ctypes.c_uint32),
+                ("w", ctypes.c_double), ("delay", ctypes.c_int), ("port", ctypes.c_int)]
 
 
 class ctypes_routes(ctypes.Structure):

@@ -31,6 +31,11 @@ extern "C" {
 int smx_last_error(char* buf, size_t cap);
 const char* smx_version(void);
 int smx_stream_sync(void* stream);
+/* host wait policy for synchronisations, before context creation
+ * (cudaDeviceScheduleSpin = 1, Yield = 2, BlockingSync = 4) */
+int smx_set_sync_policy(int flags);
+/* keep the default stream-ordered pool's memory mapped (no trim at sync) */
+int smx_pool_setup(int device);
 /* kernels launched by the library so far (process-wide counter) */
 uint64_t smx_launch_count(void);
 

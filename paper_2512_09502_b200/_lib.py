@@ -25,6 +25,8 @@ SIGNATURES = {
     "smx_last_error": (I32, [ctypes.c_char_p, ctypes.c_size_t]),
     "smx_version": (ctypes.c_char_p, []),
     "smx_stream_sync": (I32, [P]),
+    "smx_set_sync_policy": (I32, [I32]),
+    "smx_pool_setup": (I32, [I32]),
     "smx_launch_count": (U64, []),
     "smx_philox_words": (I32, [U64, U64, U64, U64, P, P]),
     "smx_integers": (I32, [U64, U64, U64, I64, U64, U64, P, P, P]),
@@ -98,5 +100,28 @@ def check(rc: int, what: str = "") -> None:
         raise _EXC.get(rc, SmxError)(f"{what}: {last_error()}" if what else last_error())
 
 
+TRACE = {} if os.environ.get("SMX_TRACE") else None
+TIMELINE = [] if os.environ.get("SMX_TIMELINE") else None
+
+
 def call(name: str, *args) -> None:
+    if TIMELINE is not None:
+        import time
+        import torch
+        t0 = time.perf_counter()
+        check(getattr(lib(), name)(*args), name)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        TIMELINE.append((name, t0, time.perf_counter(), e))
+        return
+    if TRACE is None:
+        check(getattr(lib(), name)(*args), name)
+        return
+    import time
+    import torch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     check(getattr(lib(), name)(*args), name)
+    torch.cuda.synchronize()
+    n, t = TRACE.get(name, (0, 0.0))
+    TRACE[name] = (n + 1, t + time.perf_counter() - t0)

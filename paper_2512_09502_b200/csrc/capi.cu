@@ -34,6 +34,34 @@ extern "C" int smx_last_error(char* buf, size_t cap) {
 
 extern "C" const char* smx_version(void) { return "spikemesh-b200 0.1.0 sm_100a"; }
 
+// Host-thread wait policy for synchronisations (must run before the CUDA
+// context is created): 1 = spin, 2 = yield, 4 = blocking sync.
+extern "C" int smx_set_sync_policy(int flags) {
+  cudaError_t e = cudaSetDeviceFlags((unsigned)flags);
+  if (e != cudaSuccess) {
+    smx_set_error("cudaSetDeviceFlags: %s", cudaGetErrorString(e));
+    return -3;
+  }
+  return 0;
+}
+
+// Keep the stream-ordered allocator's freed memory mapped between calls
+// (release threshold = max): without it every synchronisation trims the
+// default pool and the next cudaMallocAsync re-maps physical pages.
+extern "C" int smx_pool_setup(int device) {
+  cudaMemPool_t pool;
+  cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+  if (e == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (e != cudaSuccess) {
+    smx_set_error("mempool setup: %s", cudaGetErrorString(e));
+    return -3;
+  }
+  return 0;
+}
+
 extern "C" int smx_stream_sync(void* stream) {
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) {

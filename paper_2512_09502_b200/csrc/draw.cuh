@@ -120,12 +120,13 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_write_kernel(DrawRange r, c
     uint32_t tot;
     const uint32_t ex = block_excl_scan(__popc(mask), ws, tot);
     uint32_t k = ex;
-    while (mask) {
-      const int i = __ffs(mask) - 1;
-      mask &= mask - 1;
-      sv[k] = v[i];
-      if (base + k == n_out - 1 && cursor_out) *cursor_out = (b - 1) * 8 + i + 1;
-      ++k;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // static indexing keeps v[] in registers
+      if ((mask >> i) & 1u) {
+        sv[k] = v[i];
+        if (base + k == n_out - 1 && cursor_out) *cursor_out = (b - 1) * 8 + i + 1;
+        ++k;
+      }
     }
     __syncthreads();
     // coalesced hand-off: consecutive threads own consecutive output indices

@@ -123,7 +123,8 @@ struct SpikeOut {
 
 // Single CTA: ordered compaction of the spike bitmap, raster append, local
 // delivery list, and packets for both routing families.
-__global__ void __launch_bounds__(1024) spikes_kernel(SpikeOut o, Routes p2p, Routes grp) {
+__global__ void __launch_bounds__(1024) spikes_kernel(const __grid_constant__ SpikeOut o, const __grid_constant__ Routes p2p,
+                                                      const __grid_constant__ Routes grp) {
   __shared__ uint32_t ws[32];
   __shared__ uint32_t carry, src_base;
   __shared__ uint32_t pk_base[2][64];
@@ -418,7 +419,7 @@ __device__ __noinline__ void spike_lists(const StepArgs& A, uint32_t i, int lane
 }
 
 
-__global__ void __launch_bounds__(T256) step_kernel(StepArgs A) {
+__global__ void __launch_bounds__(T256) step_kernel(const __grid_constant__ StepArgs A) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int64_t now = *A.now_dev + A.step_offset;

@@ -239,6 +239,10 @@ class Cluster:
         devices = [torch.device(d) for d in devices]
         self.ranks: dict[int, _Rank] = {
             r: _Rank(r, devices[i % len(devices)]) for i, r in enumerate(self.local)}
+        for d in {st.device for st in self.ranks.values()}:
+            with torch.cuda.device(d):
+                torch.cuda.current_stream(d)  # make sure the context exists
+                call("smx_pool_setup", d.index if d.index is not None else 0)
         # host-side counters and node counts for every rank (scripts run everywhere)
         self.n_nodes = [0] * cfg.n_ranks
         self.images_made = [False] * cfg.n_ranks

@@ -25,7 +25,7 @@ timing = torch.zeros(8, dtype=torch.int64, device=dev)
 if os.environ.get("TIMING"):
     _lib.lib().smx_sort_timing(timing.data_ptr())
 times = []
-for it in range(4):
+for it in range(int(os.environ.get('ITERS', '4'))):
     keys.copy_(ka)
     vals.copy_(va)
     torch.cuda.synchronize()
@@ -48,4 +48,4 @@ if os.environ.get("TIMING"):
     t = timing.cpu().numpy().astype(float)
     print("phase cycles share (zero, rank, scan, stage, write, wait):", np.round(t[:6] / t[:6].sum(), 3))
 print(f"n={n:.3g} M={M} bits={bits} env={ {k: v for k, v in os.environ.items() if k.startswith('SMX_')} } "
-      f"ms={min(times):.2f} GB/s(20B)={20 * n / min(times) / 1e6:.0f} ok={ok}")
+      f"ms={min(times):.2f} GB/s(20B)={20 * n / min(times) / 1e6:.0f} ok={ok} all={[round(t, 1) for t in times]}")

@@ -77,11 +77,14 @@ int smx_dist_tables(const int32_t* src_rank, const int64_t* src_node, uint64_t t
  * key_mode 0 none / 1 key_tab[value] / 2 key_tab[j / kdiv];
  * pay_mode 0 none / 1 pay_tab[value] / 2 pay_tab[j / kdiv];
  * used_bits (optional, used_bits_words words) marks bit
- * used_tab ? used_tab[value] : value for every emitted draw. */
+ * used_tab ? used_tab[value] : value for every emitted draw, or with
+ * mark_from_key the bit of the record key: (key & ~TMP) - tmp_base for
+ * temporary keys, local_bit for direct ones. */
 int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u32_cursor, uint64_t ex, uint64_t n, int key_mode,
                  int pay_mode, const uint32_t* key_tab, const uint32_t* pay_tab, uint32_t kdiv, uint32_t* keys,
                  uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab, uint32_t used_bits_words,
-                 uint64_t* cursor_out_host, void* stream);
+                 int mark_from_key, uint32_t tmp_base, uint32_t local_bit, uint64_t* cursor_out_host,
+                 void* stream);
 /* one_to_one / assigned (mode 0), all_to_all (mode 1): sm/construction.py:415-419 */
 int smx_gen_pairs(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab, const uint32_t* pay_tab,
                   uint32_t* keys, uint32_t* vals, void* stream);

@@ -38,7 +38,7 @@ SIGNATURES = {
     "smx_pay_table": (I32, [P, U64, P, U64, U32, P, P]),
     "smx_key_table": (I32, [P, U64, U32, I32, P, P]),
     "smx_dist_tables": (I32, [P, P, U64, P, I32, U32, P, P, P]),
-    "smx_gen_draw": (I32, [U64, U64, U64, U64, U64, I32, I32, P, P, U32, P, P, P, P, U32, P, P]),
+    "smx_gen_draw": (I32, [U64, U64, U64, U64, U64, I32, I32, P, P, U32, P, P, P, P, U32, I32, U32, U32, P, P]),
     "smx_gen_pairs": (I32, [I32, U64, U64, P, P, P, P, P]),
     "smx_mark_values": (I32, [P, P, U64, P, P]),
     "smx_assign_images": (I32, [P, U64, P, I32, I64, P, P]),

@@ -181,6 +181,27 @@ __device__ inline Key blake2b_128(const uint64_t m[16], uint32_t len) {
   return k;
 }
 
+// Division of u32 by an invariant divisor without the (slow, software) integer
+// divide: Granlund-Montgomery round-up multiplier, exact for every n < 2^32.
+struct FastDiv {
+  uint32_t d, m;
+  int l;
+  __host__ __device__ static FastDiv make(uint32_t d) {
+    FastDiv f;
+    f.d = d ? d : 1;
+    int l = 0;
+    while ((1ULL << l) < f.d) ++l;
+    f.l = l;
+    f.m = (uint32_t)(((1ULL << 32) * ((1ULL << l) - f.d)) / f.d + 1);
+    return f;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    if (l == 0) return n;
+    const uint32_t t = __umulhi(m, n);
+    return (t + ((n - t) >> 1)) >> (l - 1);
+  }
+};
+
 // TMA 1-D bulk copies (cp.async.bulk) with mbarrier completion --------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

@@ -18,6 +18,7 @@
 // (int32, -1 = no image) over the source rank's node values plus a presence
 // bitmap; the sorted (R, L) pair of the reference is the compaction of that
 // bitmap.  Lookups are O(1) gathers instead of searchsorted.
+#include <cstdlib>
 #include "draw_host.cuh"
 
 using namespace smx;
@@ -79,6 +80,7 @@ struct GenSink {
   const uint32_t* key_tab;
   const uint32_t* pay_tab;
   uint32_t kdiv;
+  FastDiv kd;  // j / kdiv for call-local record indices j < 2^32
   uint32_t* keys;        // pre-offset to the call's first record
   uint32_t* vals;
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const {
@@ -89,6 +91,31 @@ struct GenSink {
     }
     if (pay_mode == P_FROM_J) vals[j] = pay_tab[j / kdiv];
     else if (pay_mode == P_FROM_VALUE) vals[j] = pay_tab[v];
+  }
+  // 8 items at j0 + u*stride: all gathers issued before any store
+  __device__ __forceinline__ void batch(uint64_t j0, uint32_t stride, const uint32_t* v, uint32_t okm,
+                                        uint32_t* kk) const {
+    uint32_t pp[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint64_t j = j0 + (uint64_t)u * stride;
+      const bool ok = (okm >> u) & 1u;
+      kk[u] = 0;
+      pp[u] = 0;
+      if (ok) {
+        if (key_mode == K_FROM_VALUE) kk[u] = __ldg(key_tab + v[u]);
+        else if (key_mode == K_FROM_J) kk[u] = __ldg(key_tab + kd.div((uint32_t)j));
+        if (pay_mode == P_FROM_J) pp[u] = __ldg(pay_tab + kd.div((uint32_t)j));
+        else if (pay_mode == P_FROM_VALUE) pp[u] = __ldg(pay_tab + v[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (!((okm >> u) & 1u)) continue;
+      const uint64_t j = j0 + (uint64_t)u * stride;
+      if (key_mode != K_NONE && keys) keys[j] = kk[u];
+      if (pay_mode != P_NONE) vals[j] = pp[u];
+    }
   }
 };
 
@@ -334,13 +361,19 @@ extern "C" int smx_dist_tables(const int32_t* src_rank, const int64_t* src_node,
 extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, uint64_t n, int key_mode,
                             int pay_mode, const uint32_t* key_tab, const uint32_t* pay_tab, uint32_t kdiv,
                             uint32_t* keys, uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab,
-                            uint32_t used_bits_words, uint64_t* cursor_out, void* stream) {
+                            uint32_t used_bits_words, int mark_from_key, uint32_t tmp_base, uint32_t local_bit,
+                            uint64_t* cursor_out, void* stream) {
   GenSink s;
   s.key_mode = key_mode;
   s.pay_mode = pay_mode;
   s.key_tab = key_tab;
   s.pay_tab = pay_tab;
   s.kdiv = kdiv ? kdiv : 1;
+  s.kd = FastDiv::make(s.kdiv);
+  if (n >= (1ULL << 32)) {
+    smx_set_error("smx_gen_draw: %llu records in one call exceed 2^32", (unsigned long long)n);
+    return -1;
+  }
   s.keys = keys;
   s.vals = vals;
   DrawResult res;
@@ -355,7 +388,10 @@ extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, 
   }
   // used-value marking (flagged / remote sources): bitmap size from the table
   // range -- the caller sizes used_bits to cover every bit it can receive
-  DrawMark mk{used_bits, used_tab, used_bits_words, 0};
+  DrawMark mk{used_bits, used_tab, used_bits_words, 0, mark_from_key, tmp_base, local_bit};
+  static const int variant = getenv("SMX_GEN_VARIANT") ? atoi(getenv("SMX_GEN_VARIANT")) : 0;  // tuning only
+  if (variant & 1) mk.bits = nullptr;
+  if (variant & 2) { s.key_mode = K_NONE; s.pay_mode = P_NONE; }
   const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, (cudaStream_t)stream, &res, mk);
   *cursor_out = res.cursor;
   return rc;

@@ -82,19 +82,28 @@ static __global__ void cta_offsets_kernel(const uint32_t* counts, int n, uint64_
   if (threadIdx.x == 0) offsets[n] = carry;
 }
 
-// Sink contract: `void operator()(uint64_t j, uint32_t value)` for j < n_out,
-// and `void cursor(uint64_t u32_after)` from the thread that emits j = n_out-1.
+// Sink contract: `void batch(uint64_t j0, uint32_t stride, const uint32_t v[8],
+// uint32_t ok, uint32_t keys_out[8])` consumes values v[u] (bit u of ok set)
+// for output indices j0 + u*stride and reports the record keys it wrote;
+// `void operator()(uint64_t j, uint32_t value)` consumes one item.
 // Optional used-value marking fused into the write pass: bit
-// (tab ? tab[value] : value) of `bits` is set for every emitted draw.  Small
-// bitmaps are accumulated in shared memory and OR-ed out once per CTA.
+// (tab ? tab[value] : value) of `bits` is set for every emitted draw; with
+// from_key the bit comes from the sink's key instead: temporary keys mark
+// (key & ~TMP) - tmp_base, direct (local) keys mark local_bit.  Small bitmaps
+// are accumulated in shared memory and OR-ed out once per CTA; only first
+// sightings pay an atomic.
 struct DrawMark {
   uint32_t* bits;
   const uint32_t* tab;
   uint32_t nwords;  // bitmap size
   int in_smem;      // nwords fit the dynamic shared-memory bitmap
+  int from_key;
+  uint32_t tmp_base;
+  uint32_t local_bit;
 };
 
 constexpr uint32_t DRAW_MARK_SMEM_WORDS = 12288;  // 48 KB
+constexpr int DRAW_BPT = 2;                       // Philox blocks per thread per iteration
 
 template <class Sink>
 __global__ void __launch_bounds__(DRAW_THREADS) draw_write_kernel(DrawRange r, const uint64_t* cta_offsets,
@@ -110,37 +119,62 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_write_kernel(DrawRange r, c
     for (uint32_t w = threadIdx.x; w < mk.nwords; w += blockDim.x) smark[w] = 0;
   }
   __shared__ uint32_t ws[DRAW_THREADS / 32];
-  __shared__ uint32_t sv[DRAW_THREADS * 8];  // accepted values of one iteration, in order
+  __shared__ uint32_t sv[DRAW_THREADS * 8 * DRAW_BPT];  // accepted values of one iteration, in order
   const uint64_t b0 = lo / 8 + 1, b1 = (hi - 1) / 8 + 1;
-  for (uint64_t bb = b0; bb <= b1 && base < n_out; bb += blockDim.x) {
-    const uint64_t b = bb + threadIdx.x;
-    uint32_t v[8];
-    uint32_t mask = 0;
-    if (b <= b1) mask = block_accepts(r, b, lo, hi, v);
+  for (uint64_t bb = b0; bb <= b1 && base < n_out; bb += (uint64_t)DRAW_BPT * blockDim.x) {
+    // thread t owns blocks bb + BPT*t .. +BPT-1: raw order = thread order
+    uint32_t v[DRAW_BPT][8];
+    uint32_t mask[DRAW_BPT];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int q = 0; q < DRAW_BPT; ++q) {
+      const uint64_t b = bb + (uint64_t)DRAW_BPT * threadIdx.x + q;
+      mask[q] = b <= b1 ? block_accepts(r, b, lo, hi, v[q]) : 0u;
+      cnt += __popc(mask[q]);
+    }
     uint32_t tot;
-    const uint32_t ex = block_excl_scan(__popc(mask), ws, tot);
+    const uint32_t ex = block_excl_scan(cnt, ws, tot);
     uint32_t k = ex;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {  // static indexing keeps v[] in registers
-      if ((mask >> i) & 1u) {
-        sv[k] = v[i];
-        if (base + k == n_out - 1 && cursor_out) *cursor_out = (b - 1) * 8 + i + 1;
-        ++k;
+    for (int q = 0; q < DRAW_BPT; ++q) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {  // static indexing keeps v[] in registers
+        if ((mask[q] >> i) & 1u) {
+          sv[k] = v[q][i];
+          if (base + k == n_out - 1 && cursor_out) {
+            const uint64_t b = bb + (uint64_t)DRAW_BPT * threadIdx.x + q;
+            *cursor_out = (b - 1) * 8 + i + 1;
+          }
+          ++k;
+        }
       }
     }
     __syncthreads();
-    // coalesced hand-off: consecutive threads own consecutive output indices
-    for (uint32_t q = threadIdx.x; q < tot; q += blockDim.x) {
-      const uint64_t j = base + q;
-      if (j < n_out) {
-        const uint32_t val = sv[q];
-        sink(j, val);
-        if (mk.bits) {
-          const uint32_t bit = mk.tab ? __ldg(mk.tab + val) : val;
-          if (bit != 0xffffffffu) {
-            if (mk.in_smem) atomicOr(&smark[bit >> 5], 1u << (bit & 31));
-            else atomicOr(&mk.bits[bit >> 5], 1u << (bit & 31));
-          }
+    // coalesced hand-off: consecutive threads own consecutive output indices;
+    // a thread's items go over in batches of 8 so their gathers overlap
+#pragma unroll
+    for (int h = 0; h < DRAW_BPT; ++h) {
+      uint32_t vv[8], kk[8];
+      uint32_t okm = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t q = threadIdx.x + (h * 8 + u) * blockDim.x;
+        const bool ok = q < tot && base + q < n_out;
+        vv[u] = ok ? sv[q] : 0u;
+        okm |= (ok ? 1u : 0u) << u;
+      }
+      sink.batch(base + threadIdx.x + (uint64_t)h * 8 * blockDim.x, blockDim.x, vv, okm, kk);
+      if (mk.bits) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (!((okm >> u) & 1u)) continue;
+          uint32_t bit;
+          if (mk.from_key) bit = (kk[u] & SMX_TMP_KEY) ? (kk[u] & ~SMX_TMP_KEY) - mk.tmp_base : mk.local_bit;
+          else bit = mk.tab ? __ldg(mk.tab + vv[u]) : vv[u];
+          if (bit == 0xffffffffu) continue;
+          const uint32_t m = 1u << (bit & 31);
+          uint32_t* w = mk.in_smem ? &smark[bit >> 5] : &mk.bits[bit >> 5];
+          if (!(*(volatile uint32_t*)w & m)) atomicOr(w, m);
         }
       }
     }
@@ -148,9 +182,10 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_write_kernel(DrawRange r, c
     __syncthreads();
   }
   if (mk.in_smem) {
+    __syncthreads();
     for (uint32_t w = threadIdx.x; w < mk.nwords; w += blockDim.x) {
       const uint32_t x = smark[w];
-      if (x) atomicOr(&mk.bits[w], x);
+      if (x & ~__ldcg(&mk.bits[w])) atomicOr(&mk.bits[w], x);
     }
   }
 }

@@ -13,7 +13,7 @@ struct DrawResult {
 // Hands every (index, value-lo) to `sink`; returns 0 or a negative status.
 template <class Sink>
 int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink,
-             cudaStream_t st, DrawResult* res, DrawMark mk = DrawMark{nullptr, nullptr, 0, 0}) {
+             cudaStream_t st, DrawResult* res, DrawMark mk = DrawMark{nullptr, nullptr, 0, 0, 0, 0, 0}) {
   res->cursor = u0;
   if (n_out == 0) return 0;
   if (ex == 1) {  // numpy: range of one value consumes nothing

@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(T256) deliver_kernel(const uint32_t* src_nodes
     }
     const uint32_t node = src_nodes[lo];
     const int64_t now = src_steps[lo];
+    const uint32_t slot0 = (uint32_t)(now % L);  // once per work item
     const int64_t a = first[node] + (int64_t)(w - wprefix[lo]) * CHUNK;
     int64_t b = first[node + 1];
     if (b > a + CHUNK) b = a + CHUNK;
@@ -305,7 +306,8 @@ __global__ void __launch_bounds__(T256) deliver_kernel(const uint32_t* src_nodes
         port = cp[c];
         row = pl & SMX_ROW_MASK;
       }
-      const int slot = (int)((now + d) % L);
+      uint32_t slot = slot0 + d;  // d < L: one conditional wrap
+      if (slot >= (uint32_t)L) slot -= (uint32_t)L;
       atomicAdd(ring + slot * slot_stride + (size_t)port * n_rows + row, wt);
     }
   }
@@ -497,6 +499,7 @@ __global__ void __launch_bounds__(T256) deliver_step_kernel(const uint32_t* src_
     const uint32_t e = owner[w];  // list entry whose chunk range holds w
     const uint32_t node = src_nodes[e];
     const int64_t now = src_steps[e];
+    const uint32_t slot0 = (uint32_t)(now % L);  // once per work item
     const int64_t a = first[node] + (int64_t)(w - wbase[e]) * CHUNK;
     int64_t b = first[node + 1];
     if (b > a + CHUNK) b = a + CHUNK;
@@ -517,7 +520,8 @@ __global__ void __launch_bounds__(T256) deliver_step_kernel(const uint32_t* src_
         port = cp[cl];
         row = pl & SMX_ROW_MASK;
       }
-      const int slot = (int)((now + d) % L);
+      uint32_t slot = slot0 + d;  // d < L: one conditional wrap
+      if (slot >= (uint32_t)L) slot -= (uint32_t)L;
       atomicAdd(ring + slot * slot_stride + (size_t)port * n_rows + row, wt);
     }
   }

@@ -21,6 +21,14 @@ struct RawSink {
   int64_t lo;
   int64_t* out;
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const { out[j] = lo + (int64_t)v; }
+  __device__ __forceinline__ void batch(uint64_t j0, uint32_t stride, const uint32_t* v, uint32_t ok,
+                                        uint32_t* keys) const {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      keys[u] = 0;
+      if ((ok >> u) & 1u) out[j0 + (uint64_t)u * stride] = lo + (int64_t)v[u];
+    }
+  }
 };
 
 // Append the decimal form of x (may be negative) to buf at *len.

@@ -231,17 +231,21 @@ __global__ void __launch_bounds__(RS_THREADS, 2) downsweep_kernel(SortPass p) {
     }
     __syncthreads();
     TMARK(3);
-    for (uint32_t q = tid; q < tsum; q += RS_THREADS) {
-      const uint32_t k = skey[q];
-      const uint32_t d = (k >> p.shift) & mask;
-      const uint64_t g = (uint64_t)run_base[d] + (q - tstart[d]);
-      p.vals_out[g] = sval[q];
-      if (!p.last) {
-        p.keys_out[g] = k;
-      } else if (q == 0 || skey[q - 1] != k) {
-        uint32_t e = q + 1;
-        while (e < tsum && skey[e] == k) ++e;
-        atomicAdd(&p.counts[k], e - q);
+    for (uint32_t q0 = 0; q0 < tsum; q0 += RS_THREADS) {
+      const uint32_t q = q0 + tid;
+      const bool ok = q < tsum;
+      const uint32_t k = ok ? skey[q] : 0xffffffffu;
+      if (ok) {
+        const uint32_t d = (k >> p.shift) & mask;
+        const uint64_t g = (uint64_t)run_base[d] + (q - tstart[d]);
+        p.vals_out[g] = sval[q];
+        if (!p.last) p.keys_out[g] = k;
+      }
+      if (p.last) {
+        // per-source counts: equal keys are adjacent in the staging buffer,
+        // so one warp-aggregated atomic per distinct key per warp
+        const uint32_t peers = __match_any_sync(0xffffffffu, k);
+        if (ok && lane == __ffs(peers) - 1) atomicAdd(&p.counts[k], (uint32_t)__popc(peers));
       }
     }
     __syncthreads();

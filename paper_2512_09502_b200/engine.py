@@ -509,16 +509,16 @@ class Cluster:
             elif rule == "fixed_indegree":
                 call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 2, _ptr(key_tab),
                      _ptr(pay_tab), int(conn.k_in), _ptr(keys), _ptr(vals), _ptr(pos_bits), 0,
-                     _words(n_src), cur.ctypes.data, sk)
+                     _words(n_src), 0, 0, 0, cur.ctypes.data, sk)
             elif rule == "fixed_outdegree":
                 call("smx_gen_draw", local_key[0], local_key[1], 0, n_tgt, n, 2, 1, _ptr(key_tab),
-                     _ptr(pay_tab), int(conn.k_out), _ptr(keys), _ptr(vals), 0, 0, 0, cur.ctypes.data, sk)
+                     _ptr(pay_tab), int(conn.k_out), _ptr(keys), _ptr(vals), 0, 0, 0, 0, 0, 0, cur.ctypes.data, sk)
             else:  # fixed_total: positions (aligned) then targets (local; same stream locally)
                 call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 0, _ptr(key_tab),
-                     0, 1, _ptr(keys), 0, _ptr(pos_bits), 0, _words(n_src), cur.ctypes.data, sk)
+                     0, 1, _ptr(keys), 0, _ptr(pos_bits), 0, _words(n_src), 0, 0, 0, cur.ctypes.data, sk)
                 u0 = int(cur[0]) if local_key == aligned_key else 0
                 call("smx_gen_draw", local_key[0], local_key[1], u0, n_tgt, n, 0, 1, 0,
-                     _ptr(pay_tab), 1, 0, _ptr(vals), 0, 0, 0, cur.ctypes.data, sk)
+                     _ptr(pay_tab), 1, 0, _ptr(vals), 0, 0, 0, 0, 0, 0, cur.ctypes.data, sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
         if st.wide:
@@ -669,7 +669,7 @@ class Cluster:
         cur = np.zeros(1, dtype=np.uint64)
         if n:
             call("smx_gen_draw", k_src[0], k_src[1], 0, n_src, n, 1, 0, 0, 0, 1, 0, 0, _ptr(pb), 0,
-                 _words(n_src), cur.ctypes.data, ss.stream)
+                 _words(n_src), 0, 0, 0, cur.ctypes.data, ss.stream)
         return pb
 
     def _assign(self, st: _Rank, vbits, segs):
@@ -839,7 +839,8 @@ class Cluster:
         cur = np.zeros(1, dtype=np.uint64)
         ev0 = self._event(st) if self.prof is not None else None
         call("smx_gen_draw", key[0], key[1], 0, total, n, 1, 2, _ptr(key_tab), _ptr(pay_tab), k_in,
-             _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits), _ptr(gv_all), vbits.numel(), cur.ctypes.data, sk)
+             _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits), 0, vbits.numel(), 1, lut_base, int(vbase[tr]),
+             cur.ctypes.data, sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
         if st.wide:
@@ -873,7 +874,7 @@ class Cluster:
         vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
         cur = np.zeros(1, dtype=np.uint64)
         call("smx_gen_draw", key[0], key[1], 0, total, n, 1, 0, 0, 0, 1, 0, 0, _ptr(vbits), _ptr(gv_all),
-             vbits.numel(), cur.ctypes.data, stream)
+             vbits.numel(), 0, 0, 0, cur.ctypes.data, stream)
         return vbits
 
     # -------------------------------------------------------------- preparation

@@ -11,6 +11,8 @@ from paper_2512_09502_b200 import _lib  # noqa: E402
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_125_000_000
 M = int(float(sys.argv[2])) if len(sys.argv) > 2 else 100_000
 dev = torch.device("cuda")
+torch.zeros(1, device=dev)
+_lib.call("smx_pool_setup", 0)
 g = torch.Generator(device=dev).manual_seed(1)
 keys = torch.randint(0, M, (n,), device=dev, dtype=torch.int32, generator=g)
 vals = torch.arange(n, device=dev, dtype=torch.int32)

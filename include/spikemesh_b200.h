@@ -167,6 +167,19 @@ int smx_step(double* v, int32_t* ref, const double* decay, const double* v_rest,
              const uint32_t* cls_delay, const uint32_t* cls_port, const double* wide_w, const uint32_t* wide_meta,
              void* stream);
 
+/* --- reference-layout drop-ins for sm/kernels (kernels/__init__.py:25-26) ---
+ * lif_step (_speedups.pyx:13-35): v f64[n], ref_count i64[n], real_mask u8[n],
+ * inputs f64[n], decay/v_rest/v_reset/v_th f64[n], ref_steps i64[n],
+ * spiked_out u8[n]. */
+int smx_ref_lif_step(double* v, int64_t* ref_count, const uint8_t* real_mask, const double* inputs,
+                     const double* decay, const double* v_rest, const double* v_reset, const double* v_th,
+                     const int64_t* ref_steps, uint8_t* spiked_out, uint64_t n, void* stream);
+/* deliver_spikes (_speedups.pyx:38-54): src_nodes/mults i64[k], first_index
+ * i64[M+1], tgt/port/delay i64[S], weight f64[S], buffers f64[M][P][L]. */
+int smx_ref_deliver_spikes(const int64_t* src_nodes, const int64_t* mults, uint64_t k, const int64_t* first_index,
+                           const int64_t* tgt, const int64_t* port, const int64_t* delay, const double* weight,
+                           double* buffers, int64_t n_ports, int64_t L, int64_t now, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

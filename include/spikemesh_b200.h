@@ -102,6 +102,15 @@ int smx_bits_prefix(const uint32_t* bits, uint64_t nwords, int64_t* excl, void* 
 int smx_bits_compact(const uint32_t* bits, uint64_t nwords, const int64_t* excl, int64_t* out,
                      const int32_t* img_of, int64_t* img_out, void* stream);
 int smx_fill_wide_const(double* w, uint32_t* meta, uint64_t n, double wv, uint32_t mv, void* stream);
+/* _realize_syn random specs (sm/construction.py:157-176): normal weights
+ * (numpy Generator.normal from word cursor *cursor_in; workspace as for the
+ * Poisson counts with smx_normal_chunks_for(n) chunks) and uniform_int delays
+ * (integers from u32 cursor u0) written as meta = delay | port << 24. */
+int smx_normal_chunks_for(uint64_t n);
+int smx_normal_fill(uint64_t k0, uint64_t k1, const uint64_t* cursor_in, double loc, double scale, uint64_t n,
+                    int n_chunks, void* workspace, double* values, uint64_t* cursor_out, int* err, void* stream);
+int smx_delay_fill(uint64_t k0, uint64_t k1, uint64_t u0, uint32_t lo, uint64_t ex, uint64_t n, uint32_t port,
+                   uint32_t* meta, uint64_t* cursor_out_host, void* stream);
 int smx_promote_wide(const uint32_t* vals, uint64_t n, const double* cls_w, const uint32_t* cls_meta,
                      uint32_t* rows, double* w, uint32_t* meta, void* stream);
 

@@ -48,6 +48,9 @@ SIGNATURES = {
     "smx_bits_compact": (I32, [P, U64, P, P, P, P, P]),
     "smx_build_routes": (I32, [P, I32, U64, P, P, P, P, P, P]),
     "smx_fill_wide_const": (I32, [P, P, U64, D, U32, P]),
+    "smx_normal_chunks_for": (I32, [U64]),
+    "smx_normal_fill": (I32, [U64, U64, P, D, D, U64, I32, P, P, P, P, P]),
+    "smx_delay_fill": (I32, [U64, U64, U64, U32, U64, U64, U32, P, P, P]),
     "smx_promote_wide": (I32, [P, U64, P, P, P, P, P, P]),
     "smx_gather_wide": (I32, [P, U64, P, P, P, P, P, P, P]),
     "smx_max_meta": (I32, [P, U64, P, P]),

@@ -124,6 +124,22 @@ __global__ void mark_one_kernel(uint32_t* bits, const uint32_t* tab) {
   if (b != 0xffffffffu) atomicOr(&bits[b >> 5], 1u << (b & 31));
 }
 
+// uniform_int delays of a wide call: meta[j] = (lo + value) | port << 24
+struct MetaSink {
+  uint32_t lo;
+  uint32_t port_bits;
+  uint32_t* meta;
+  __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const { meta[j] = (lo + v) | port_bits; }
+  __device__ __forceinline__ void batch(uint64_t j0, uint32_t stride, const uint32_t* v, uint32_t ok,
+                                        uint32_t* keys) const {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      keys[u] = 0;
+      if ((ok >> u) & 1u) meta[j0 + (uint64_t)u * stride] = (lo + v[u]) | port_bits;
+    }
+  }
+};
+
 // Deterministic-use rules: one_to_one / assigned (mode 0: record i = (i, i)),
 // all_to_all (mode 1: record r = (r % n_src, r / n_src)).
 __global__ void pairs_kernel(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab,
@@ -536,4 +552,22 @@ extern "C" int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out2, vo
   smx_count_launch(); max_meta_kernel<<<148 * 4, T256, 0, st>>>(meta, n, out2, out2 + 1);
   SMX_LAUNCH_CHECK();
   return 0;
+}
+
+// Delays of a wide call drawn as numpy integers(lo, lo+ex, size=n) from u32
+// cursor u0 (sm/construction.py:168-169), stored as meta = delay | port << 24.
+extern "C" int smx_delay_fill(uint64_t k0, uint64_t k1, uint64_t u0, uint32_t lo, uint64_t ex, uint64_t n,
+                              uint32_t port, uint32_t* meta, uint64_t* cursor_out, void* stream) {
+  MetaSink s{lo, port << 24, meta};
+  *cursor_out = u0;
+  if (n == 0) return 0;
+  if (ex == 1) {
+    smx_count_launch(); draw_const_kernel<MetaSink><<<nblk(n), T256, 0, (cudaStream_t)stream>>>(n, s);
+    SMX_LAUNCH_CHECK();
+    return 0;
+  }
+  DrawResult res;
+  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, (cudaStream_t)stream, &res);
+  *cursor_out = res.cursor;
+  return rc;
 }

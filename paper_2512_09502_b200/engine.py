@@ -454,7 +454,7 @@ class Cluster:
         dev = st.device
         w, d = syn.weight, syn.delay_steps
         if isinstance(w, tuple) or isinstance(d, tuple):
-            raise NotImplementedError("random SynSpec draws (normal / uniform_int) are not implemented yet")
+            return self._write_syn_random(st, syn, port, base, n, syn_key)
         wv = np.asarray(w, dtype=np.float64)
         dv = np.asarray(d, dtype=np.int64)
         if wv.ndim and len(wv) != n:
@@ -474,6 +474,53 @@ class Cluster:
             seg_w.copy_(_up(np.broadcast_to(wv, (n,)).copy(), seg_w.device))
             meta = (np.broadcast_to(dv, (n,)).astype(np.int64) & ROW_MASK) | (port << 24)
             seg_m.copy_(_up(meta.astype(np.uint32).view(np.int32), seg_m.device))
+
+    def _write_syn_random(self, st: _Rank, syn: SynSpec, port: int, base: int, n: int, syn_key):
+        """Random syn specs drawn on the device from the call's syn stream:
+        normal weights (next64 words) then uniform_int delays continuing at
+        the next u32 (sm/construction.py:157-176)."""
+        dev = st.device
+        w, d = syn.weight, syn.delay_steps
+        seg_w = st.w_w.t[base: base + n]
+        seg_m = st.w_meta.t[base: base + n]
+        if port > 255:
+            raise DelayRangeError("port > 255 not representable")
+        u32 = 0
+        if isinstance(w, tuple):
+            L = _lib.lib()
+            chunks = L.smx_normal_chunks_for(n)
+            ws = torch.empty(int(L.smx_poisson_workspace(chunks)), dtype=torch.uint8, device=dev)
+            cur = torch.zeros(2, dtype=torch.int64, device=dev)
+            err = torch.zeros(1, dtype=torch.int32, device=dev)
+            call("smx_normal_fill", syn_key[0], syn_key[1], _ptr(cur), float(w[1]), float(w[2]), n, chunks,
+                 _ptr(ws), _ptr(seg_w), _ptr(cur[1:]), _ptr(err), st.stream)
+            if int(err.item()):
+                raise RuntimeError(f"normal weight chain error {int(err.item())}")
+            u32 = 2 * int(cur[1].item())
+        else:
+            wv = np.asarray(w, dtype=np.float64)
+            if wv.ndim:
+                if len(wv) != n:
+                    raise ValueError(f"{len(wv)} weights for {n} records")
+                seg_w.copy_(_up(wv, dev))
+            else:
+                seg_w.fill_(float(wv))
+        if isinstance(d, tuple):
+            lo, hi = int(d[1]), int(d[2])
+            if hi > ROW_MASK:
+                raise DelayRangeError("delay >= 2^24 steps not representable")
+            cur = np.zeros(1, dtype=np.uint64)
+            call("smx_delay_fill", syn_key[0], syn_key[1], u32, lo, hi - lo + 1, n, port, _ptr(seg_m),
+                 cur.ctypes.data, st.stream)
+        else:
+            dv = np.asarray(d, dtype=np.int64)
+            if dv.ndim:
+                if len(dv) != n:
+                    raise ValueError(f"{len(dv)} delays for {n} records")
+                meta = (dv & ROW_MASK) | (port << 24)
+                seg_m.copy_(_up(meta.astype(np.uint32).view(np.int32), dev))
+            else:
+                seg_m.fill_(int((int(dv) & ROW_MASK) | (port << 24)) - (1 << 32 if port >= 128 else 0))
 
     def _emit_records(self, st: _Rank, conn: ConnSpec, sources, targets, syn: SynSpec, port: int,
                       aligned_key, local_key, syn_key, tmp_base=None, pos_bits=None):

@@ -35,7 +35,13 @@ import tables  # noqa: E402
 
 
 def ref_namespace():
+    # the PD microcircuit script (C2) has no reference counterpart: the
+    # reference Cluster runs this repository's script (it only calls façade
+    # methods and duck-typed ConnSpec/SynSpec/LifParams)
+    sys.path.insert(0, ROOT)
+    from paper_2512_09502_b200 import models as mm
     return SimpleNamespace(
+        build_microcircuit=mm.build_microcircuit, MicrocircuitParams=mm.MicrocircuitParams,
         SimConfig=sm.SimConfig, make_cluster=sm.Cluster, ConnSpec=sm.ConnSpec, SynSpec=sm.SynSpec,
         LifParams=sm.LifParams, build_balanced_network=smm.build_balanced_network,
         BalancedParams=smm.BalancedParams, ExplicitNetwork=smm.ExplicitNetwork,

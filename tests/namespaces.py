@@ -10,7 +10,8 @@ def _common(make):
         LifParams=api.LifParams, build_balanced_network=models.build_balanced_network,
         BalancedParams=models.BalancedParams, ExplicitNetwork=models.ExplicitNetwork,
         build_multi_area=models.build_multi_area, AreaSpec=models.AreaSpec, pack_areas=models.pack_areas,
-        MultiAreaParams=models.MultiAreaParams)
+        MultiAreaParams=models.MultiAreaParams, build_microcircuit=models.build_microcircuit,
+        MicrocircuitParams=models.MicrocircuitParams)
 
 
 def oracle_ns():

@@ -63,6 +63,50 @@ def rules_wide(ns, seed=4):
     return c, (0.0, 5.0)
 
 
+def rules_random(ns, seed=5):
+    """Random SynSpec draws: normal weights then uniform_int delays from the
+    call's syn stream (sm/construction.py:157-176), every draw-based rule."""
+    cfg = ns.SimConfig(n_ranks=1, seed=seed)
+    c = ns.make_cluster(cfg)
+    a = c.create_neurons(0, 60, ns.LifParams(i_e=0.25), ("normal", -60.0, 3.0), gids=np.arange(60))
+    A = np.arange(a.start, a.stop)
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    c.connect(0, A, A, S("fixed_indegree", k_in=9), Sy(("normal", 0.25, 0.05), ("uniform_int", 1, 8)))
+    c.connect(0, A[:30], A[30:], S("fixed_total", n_total=1111), Sy(("normal", -0.5, 0.1), 3))
+    c.connect(0, A[:7], A, S("fixed_outdegree", k_out=20), Sy(0.125, ("uniform_int", 2, 2)))
+    c.connect(0, A[5:25], A[10:30], S("one_to_one"), Sy(("normal", 0.0, 1.0), ("uniform_int", 1, 30)))
+    c.connect(0, A[:4], A[:9], S("all_to_all"), Sy(0.25, ("uniform_int", 3, 9)))
+    return c, (0.0, 5.0)
+
+
+def remote_random(ns, mode="p2p", seed=6):
+    cfg = ns.SimConfig(n_ranks=2, comm_mode=mode, seed=seed)
+    c = ns.make_cluster(cfg)
+    group = -1
+    if mode == "collective":
+        group = 0
+        c.declare_group(0, [0, 1])
+    pops = []
+    for r in range(2):
+        x = c.create_neurons(r, 80, ns.LifParams(i_e=0.2), ("normal", -58.0, 4.0), gids=r * 80 + np.arange(80))
+        pops.append(np.arange(x.start, x.stop))
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    c.connect_remote(0, pops[0], 1, pops[1], S("fixed_indegree", k_in=6), Sy(("normal", 0.2, 0.02), ("uniform_int", 2, 9)),
+                     group=group)
+    c.connect_remote(1, pops[1], 0, pops[0][:10], S("fixed_indegree", k_in=2), Sy(("normal", 0.3, 0.01), 4),
+                     group=group)  # flagged
+    c.connect_remote(1, pops[1][:40], 0, pops[0], S("fixed_total", n_total=500), Sy(0.125, ("uniform_int", 2, 5)),
+                     group=group)
+    return c, (0.0, 5.0)
+
+
+def microcircuit(ns, scale=0.02, seed=77):
+    cfg = ns.SimConfig(n_ranks=1, seed=seed)
+    c = ns.make_cluster(cfg)
+    ns.build_microcircuit(c, ns.MicrocircuitParams(scale=scale))
+    return c, (0.0, 5.0)
+
+
 def remote_mix(ns, mode="p2p", seed=9):
     """Remote connections of every rule across 3 ranks, sparse (flagged) and
     dense (unflagged), p2p or collective."""
@@ -116,4 +160,12 @@ SCENARIOS = {
     "balanced_2r_p2p": lambda ns: balanced(ns, 2, "p2p", 250, 20, 5, 8, sim=(0.0, 20.0)),
     "explicit_2r_coll": lambda ns: explicit(ns, 2, "collective"),
     "multi_area_2r_coll": lambda ns: multi_area(ns, 2, "collective"),
+    "rules_random": rules_random,
+    "remote_random_p2p": lambda ns: remote_random(ns, "p2p"),
+    "remote_random_coll": lambda ns: remote_random(ns, "collective"),
+    "microcircuit_small": microcircuit,
 }
+
+# scenarios whose weights are not dyadic: tables are bit-exact, the raster is
+# compared with a tolerance (fp64 sums depend on the atomic delivery order)
+NON_DYADIC = {"rules_random", "remote_random_p2p", "remote_random_coll", "microcircuit_small"}

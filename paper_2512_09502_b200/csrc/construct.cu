@@ -85,7 +85,7 @@ struct GenSink {
   uint32_t* vals;
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const {
     if (key_mode == K_FROM_VALUE) {
-      if (keys) keys[j] = __ldg(key_tab + v);
+      if (keys && key_tab) keys[j] = __ldg(key_tab + v);
     } else if (key_mode == K_FROM_J) {
       keys[j] = key_tab[j / kdiv];
     }
@@ -103,8 +103,10 @@ struct GenSink {
       kk[u] = 0;
       pp[u] = 0;
       if (ok) {
-        if (key_mode == K_FROM_VALUE) kk[u] = __ldg(key_tab + v[u]);
-        else if (key_mode == K_FROM_J) kk[u] = __ldg(key_tab + kd.div((uint32_t)j));
+        if (key_tab) {
+          if (key_mode == K_FROM_VALUE) kk[u] = __ldg(key_tab + v[u]);
+          else if (key_mode == K_FROM_J) kk[u] = __ldg(key_tab + kd.div((uint32_t)j));
+        }
         if (pay_mode == P_FROM_J) pp[u] = __ldg(pay_tab + kd.div((uint32_t)j));
         else if (pay_mode == P_FROM_VALUE) pp[u] = __ldg(pay_tab + v[u]);
       }

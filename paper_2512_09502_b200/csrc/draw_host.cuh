@@ -52,9 +52,9 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
     if (total >= n_out) {
       mk.in_smem = mk.bits && mk.nwords <= DRAW_MARK_SMEM_WORDS;
       const size_t smem = mk.in_smem ? mk.nwords * 4 : 0;
-      if (smem > 48 * 1024) {
+      if (smem > 0) {  // static (staging) + dynamic (bitmap) may exceed the 48 KB default
         SMX_CUDA_CHECK(cudaFuncSetAttribute(draw_write_kernel<Sink>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem));
+                                            (int)(DRAW_MARK_SMEM_WORDS * 4)));
       }
       smx_count_launch(); draw_write_kernel<Sink><<<G, DRAW_THREADS, smem, st>>>(r, offs, n_out, sink, cur_d, mk);
       SMX_LAUNCH_CHECK();

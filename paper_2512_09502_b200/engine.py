@@ -915,14 +915,42 @@ class Cluster:
         return vbits, present
 
     def _dist_replay(self, dev, key, tr, total, all_rank, all_node, vbase, total_words, n):
-        """Source-side replay of a remote target's draws: used-value bitmap only."""
+        """Source-side replay of a remote target's draws: used-value bitmap only
+        (compute only, no communication).  Coupon-collector early exit: the
+        draws are replayed in growing pieces and the replay stops once every
+        distinct source value is marked -- no later draw can add a bit, so the
+        bitmap equals the full replay's (SURVEY §7 hard part 6)."""
         stream = torch.cuda.current_stream(dev).cuda_stream
         _, gv_all, _, _ = self._dist_tables(dev, stream, tr, total, all_rank, all_node, vbase, 0)
         vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
+        n_distinct = self._n_distinct_gv(all_rank, all_node, vbase, total_words)
+        excl = torch.empty(vbits.numel() + 1, dtype=torch.int64, device=dev)
         cur = np.zeros(1, dtype=np.uint64)
-        call("smx_gen_draw", key[0], key[1], 0, total, n, 1, 0, 0, 0, 1, 0, 0, _ptr(vbits), _ptr(gv_all),
-             vbits.numel(), 0, 0, 0, cur.ctypes.data, stream)
+        u0, done = 0, 0
+        piece = max(16 * total, 1 << 22)
+        while done < n:
+            k = min(piece, n - done)
+            call("smx_gen_draw", key[0], key[1], u0, total, k, 1, 0, 0, 0, 1, 0, 0, _ptr(vbits), _ptr(gv_all),
+                 vbits.numel(), 0, 0, 0, cur.ctypes.data, stream)
+            u0 = int(cur[0])
+            done += k
+            if done < n:
+                call("smx_bits_prefix", _ptr(vbits), vbits.numel(), _ptr(excl), stream)
+                if int(excl[-1].item()) >= n_distinct:
+                    break
+                piece *= 2
         return vbits
+
+    def _n_distinct_gv(self, all_rank, all_node, vbase, total_words):
+        """Distinct (rank, node) source values of a distributed call (cached per call)."""
+        cache = getattr(self, "_gv_cache", None)
+        if cache is not None and cache[0] == self.dist_ctr:
+            return cache[1]
+        mask = np.zeros(max(total_words, 1) * 32, dtype=bool)
+        mask[vbase[all_rank].astype(np.int64) + all_node] = True
+        nd = int(mask.sum())
+        self._gv_cache = (self.dist_ctr, nd)
+        return nd
 
     # -------------------------------------------------------------- preparation
     def prepare(self) -> None:

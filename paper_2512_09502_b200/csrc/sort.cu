@@ -174,8 +174,16 @@ __global__ void __launch_bounds__(RS_THREADS, 2) downsweep_kernel(SortPass p) {
         kin[q] = k;  // later phases reread the resolved key
       }
       const uint32_t d = (k >> p.shift) & mask;
-      const uint32_t tag = valid ? d : 0x10000u + lane;
-      const uint32_t peers = __match_any_sync(0xffffffffu, tag);
+      // warp-level multisplit: lanes with the same digit, one ballot per bit
+      // (cheaper than MATCH.ANY on sm_100)
+      uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+      for (int b = 0; b < BITS; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
+      }
+      if (!valid) peers = 1u << lane;
       const int leader = __ffs(peers) - 1;
       uint32_t old = 0;
       if (valid && lane == leader) {

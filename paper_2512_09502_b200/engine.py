@@ -1355,8 +1355,9 @@ class Cluster:
             self._deliver(st)
 
     def _exchange_nccl(self):
-        """One process per rank: the same rounds over NCCL, once per block.
-        Counts travel first (device int32), then only max-count packets."""
+        """One process per rank: the same rounds over NCCL, once per block
+        (exchange.py: counts first, then only the occupied packets)."""
+        from .exchange import allgather_round, p2p_round
         dist = torch.distributed
         (st,) = self.ranks.values()
         me = st.rank
@@ -1364,51 +1365,33 @@ class Cluster:
         if self._pg is None:
             self._pg = {g: dist.new_group(sorted(self.groups[g])) for g in sorted(self.groups)}
         if self.has_p2p:
-            send_c = st.p2p_counts.clone()
-            recv_c = torch.empty_like(send_c)
-            dist.all_to_all_single(recv_c, send_c)
-            sc, rc = send_c.cpu().numpy(), recv_c.cpu().numpy()
-            inp = torch.cat([st.p2p_packets[d * st.pk_cap * 2: d * st.pk_cap * 2 + 2 * int(sc[d])]
-                             for d in range(self.n_ranks)])
-            out = torch.empty(max(int(2 * rc.sum()), 1), dtype=torch.int32, device=st.device)
-            dist.all_to_all_single(out[: int(2 * rc.sum())], inp, [2 * int(x) for x in rc], [2 * int(x) for x in sc])
-            off = 0
+            out, rc, recv_c, offs = p2p_round(st.p2p_counts, st.p2p_packets, st.pk_cap)
             for sr in range(self.n_ranks):
                 n = int(rc[sr])
+                if not n or sr == me:
+                    continue
                 rl = st.RL.get((POINT_TO_POINT, sr))
-                if n and rl is not None and sr != me:
-                    call("smx_unpack", _ptr(out[off:]), _ptr(recv_c[sr:]), _ptr(rl[1]), rl[1].numel(),
-                         _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err),
-                         st.stream)
-                elif n and sr != me:
+                if rl is None:
                     raise ProtocolError(f"rank {me}: spikes from rank {sr} but no map for that pair")
-                off += 2 * n
-            self.bytes["propagation"] += 8 * int(sc.sum())
+                call("smx_unpack", _ptr(out[int(offs[sr]):]), _ptr(recv_c[sr:]), _ptr(rl[1]), rl[1].numel(),
+                     _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
+            self.bytes["propagation"] += 8 * int(st.p2p_counts.sum().item())
         for g in self.group_ids:
-            members = self.groups[g]
+            members = sorted(self.groups[g])
             if me not in members:
                 continue
             slot = self.group_slots[g]
-            pg = self._pg[g]
-            nm = len(members)
-            allc = torch.empty(nm, dtype=torch.int32, device=st.device)
-            dist.all_gather_into_tensor(allc, st.g_counts[slot: slot + 1], group=pg)
-            ac = allc.cpu().numpy()
-            cmax = int(ac.max())
-            if cmax:
-                send = st.g_packets[slot * st.pk_cap * 2: slot * st.pk_cap * 2 + 2 * cmax]
-                recv = torch.empty(nm * 2 * cmax, dtype=torch.int32, device=st.device)
-                dist.all_gather_into_tensor(recv, send.contiguous(), group=pg)
-                for i, sr in enumerate(sorted(members)):
-                    if sr == me or ac[i] == 0:
-                        continue
-                    lk = st.I.get((g, sr))
-                    if lk is None:
-                        continue
-                    call("smx_unpack", _ptr(recv[i * 2 * cmax:]), _ptr(allc[i:]), _ptr(lk), lk.numel(),
-                         _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err),
-                         st.stream)
-            self.bytes["propagation"] += 8 * int(ac[sorted(members).index(me)])
+            pk = st.g_packets[slot * st.pk_cap * 2:]
+            recv, ac, allc, cmax = allgather_round(st.g_counts[slot: slot + 1], pk, len(members), self._pg[g])
+            for i, sr in enumerate(members):
+                if sr == me or ac[i] == 0:
+                    continue
+                lk = st.I.get((g, sr))
+                if lk is None:
+                    continue
+                call("smx_unpack", _ptr(recv[i * 2 * cmax:]), _ptr(allc[i:]), _ptr(lk), lk.numel(),
+                     _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
+            self.bytes["propagation"] += 8 * int(ac[members.index(me)])
         self._deliver(st)
 
     _recording = False

@@ -11,7 +11,7 @@ P = models.BalancedParams(neurons_per_rank=100000, k_exc=9000, k_inh=2250)
 import os
 sys.path.insert(0, '/root/repo/tools')
 from stall_sampler import Sampler
-SAMP = Sampler().start()
+SAMP = Sampler(period=float(os.environ.get('PERIOD', '0.005'))).start()
 x = torch.randn(8192, 8192, device='cuda')
 for rep in range(int(os.environ.get('REPS', '4'))):
     if os.environ.get('PREWARM'):
@@ -23,8 +23,8 @@ for rep in range(int(os.environ.get('REPS', '4'))):
     c.prepare()
     torch.cuda.synchronize(); t2 = time.perf_counter()
     s = torch.cuda.memory_stats()
-    if (t2 - t0) > 0.2:
-        SAMP.summarise(t0, t2)
+    if (t2 - t0) > 0.2 or os.environ.get('SAMPLE_ALL'):
+        SAMP.summarise(t0, t2, top=int(os.environ.get('TOP', '8')))
     print(f"rep {rep}: build {1e3*(t1-t0):.1f} ms  prepare {1e3*(t2-t1):.1f} ms  timers={ {k: round(v*1e3,1) for k,v in c.timers.as_dict().items()} } "
           f"segments={s['segment.all.current']} alloc_retries={s['num_alloc_retries']} reserved={s['reserved_bytes.all.current']/1e9:.1f}GB cudaMalloc={s.get('num_device_alloc', '?')}", flush=True)
     if _lib.TIMELINE is not None:

@@ -88,6 +88,11 @@ int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u32_cursor, uint64_t ex, uin
 /* one_to_one / assigned (mode 0), all_to_all (mode 1): sm/construction.py:415-419 */
 int smx_gen_pairs(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab, const uint32_t* pay_tab,
                   uint32_t* keys, uint32_t* vals, void* stream);
+/* allow_autapses=False redraw loop of local fixed_indegree / fixed_total
+ * calls (sm/construction.py:524-529), continuing the call's stream at u0. */
+int smx_autapse_fix(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t n_src, const uint32_t* key_tab, uint32_t* keys,
+                    const uint32_t* rows, uint64_t n, const int32_t* node2row, uint64_t n_nodes,
+                    uint64_t* cursor_out_host, void* stream);
 /* used_flags + extract_used (sm/construction.py:454-470) as a value bitmap */
 int smx_mark_values(const uint32_t* pos_bits, const int64_t* sources, uint64_t n, uint32_t* vbits, void* stream);
 /* lookup_or_create_images + RemoteSourceMap.insert (sm/construction.py:473-486,

@@ -41,6 +41,7 @@ SIGNATURES = {
     "smx_gen_draw": (I32, [U64, U64, U64, U64, U64, I32, I32, P, P, U32, P, P, P, P, U32, I32, U32, U32, P, P]),
     "smx_gen_pairs": (I32, [I32, U64, U64, P, P, P, P, P]),
     "smx_mark_values": (I32, [P, P, U64, P, P]),
+    "smx_autapse_fix": (I32, [U64, U64, U64, U64, P, P, P, U64, P, U64, P, P]),
     "smx_assign_images": (I32, [P, U64, P, I32, I64, P, P]),
     "smx_gather_lut": (I32, [P, U64, P, P, P]),
     "smx_bits_or": (I32, [P, P, U64, P]),

@@ -142,6 +142,43 @@ struct MetaSink {
   }
 };
 
+// --- autapse redraw loop (sm/construction.py:524-529) ------------------------
+// flag[i] = record idx[i] is a self-connection (source node's row == target row)
+__global__ void autapse_flags_kernel(const uint32_t* idx, uint32_t m, const uint32_t* keys, const uint32_t* rows,
+                                     const int32_t* node2row, uint64_t n_nodes, uint32_t* flag) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint32_t j = idx ? idx[i] : i;
+  const uint32_t k = keys[j];
+  const int32_t r = (uint64_t)k < n_nodes ? node2row[k] : -1;
+  flag[i] = (r >= 0 && (uint32_t)r == (rows[j] & SMX_ROW_MASK)) ? 1u : 0u;
+}
+
+__global__ void autapse_compact_kernel(const uint32_t* idx, uint32_t m, const uint32_t* flag, const int64_t* excl,
+                                       uint32_t* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m && flag[i]) out[excl[i]] = idx ? idx[i] : i;
+}
+
+__global__ void autapse_apply_kernel(const uint32_t* idx, uint32_t m, const int64_t* draws, const uint32_t* key_tab,
+                                     uint32_t* keys) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) keys[idx[i]] = key_tab[draws[i]];
+}
+
+struct RawI64Sink {
+  int64_t* out;
+  __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const { out[j] = (int64_t)v; }
+  __device__ __forceinline__ void batch(uint64_t j0, uint32_t stride, const uint32_t* v, uint32_t ok,
+                                        uint32_t* keys) const {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      keys[u] = 0;
+      if ((ok >> u) & 1u) out[j0 + (uint64_t)u * stride] = (int64_t)v[u];
+    }
+  }
+};
+
 // Deterministic-use rules: one_to_one / assigned (mode 0: record i = (i, i)),
 // all_to_all (mode 1: record r = (r % n_src, r / n_src)).
 __global__ void pairs_kernel(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab,
@@ -572,4 +609,56 @@ extern "C" int smx_delay_fill(uint64_t k0, uint64_t k1, uint64_t u0, uint32_t lo
   const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, (cudaStream_t)stream, &res);
   *cursor_out = res.cursor;
   return rc;
+}
+
+// allow_autapses=False for fixed_indegree / fixed_total local calls
+// (sm/construction.py:524-529): while any record connects a node to itself,
+// redraw those records' sources -- in ascending record order -- from the
+// call's stream, continuing at u32 cursor u0.  keys/rows are the call's
+// pending records (n of them); key_tab maps positions to source nodes.
+extern "C" int smx_autapse_fix(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t n_src, const uint32_t* key_tab,
+                               uint32_t* keys, const uint32_t* rows, uint64_t n, const int32_t* node2row,
+                               uint64_t n_nodes, uint64_t* cursor_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  *cursor_out = u0;
+  if (n == 0) return 0;
+  uint32_t *flag = nullptr, *idx_a = nullptr, *idx_b = nullptr;
+  int64_t *excl = nullptr, *draws = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&flag, sizeof(uint32_t) * n, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&excl, sizeof(int64_t) * (n + 1), st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&idx_a, sizeof(uint32_t) * n, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&idx_b, sizeof(uint32_t) * n, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&draws, sizeof(int64_t) * n, st));
+  // initial bad list over all records
+  smx_count_launch(); autapse_flags_kernel<<<nblk(n), T256, 0, st>>>(nullptr, (uint32_t)n, keys, rows, node2row, n_nodes, flag);
+  if (int rc = smx_counts_to_offsets(flag, n, excl, st)) return rc;
+  smx_count_launch(); autapse_compact_kernel<<<nblk(n), T256, 0, st>>>(nullptr, (uint32_t)n, flag, excl, idx_a);
+  SMX_LAUNCH_CHECK();
+  int64_t m = 0;
+  SMX_CUDA_CHECK(cudaMemcpyAsync(&m, excl + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+  uint64_t cur = u0;
+  int rounds = 0;
+  while (m > 0) {
+    if (++rounds > 100000) { smx_set_error("autapse redraw did not terminate"); return -2; }
+    if (n_src == 1) { smx_set_error("cannot avoid autapses with a single source"); return -1; }
+    DrawResult res;
+    if (int rc = run_draw(Key{k0, k1}, cur, n_src, (uint64_t)m, RawI64Sink{draws}, st, &res)) return rc;
+    cur = res.cursor;
+    smx_count_launch(); autapse_apply_kernel<<<nblk(m), T256, 0, st>>>(idx_a, (uint32_t)m, draws, key_tab, keys);
+    smx_count_launch(); autapse_flags_kernel<<<nblk(m), T256, 0, st>>>(idx_a, (uint32_t)m, keys, rows, node2row, n_nodes, flag);
+    if (int rc = smx_counts_to_offsets(flag, (uint64_t)m, excl, st)) return rc;
+    smx_count_launch(); autapse_compact_kernel<<<nblk(m), T256, 0, st>>>(idx_a, (uint32_t)m, flag, excl, idx_b);
+    SMX_LAUNCH_CHECK();
+    SMX_CUDA_CHECK(cudaMemcpyAsync(&m, excl + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+    uint32_t* t = idx_a; idx_a = idx_b; idx_b = t;
+  }
+  *cursor_out = cur;
+  cudaFreeAsync(flag, st);
+  cudaFreeAsync(excl, st);
+  cudaFreeAsync(idx_a, st);
+  cudaFreeAsync(idx_b, st);
+  cudaFreeAsync(draws, st);
+  return 0;
 }

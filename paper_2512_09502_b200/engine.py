@@ -523,7 +523,7 @@ class Cluster:
                 seg_m.fill_(int((int(dv) & ROW_MASK) | (port << 24)) - (1 << 32 if port >= 128 else 0))
 
     def _emit_records(self, st: _Rank, conn: ConnSpec, sources, targets, syn: SynSpec, port: int,
-                      aligned_key, local_key, syn_key, tmp_base=None, pos_bits=None):
+                      aligned_key, local_key, syn_key, tmp_base=None, pos_bits=None, autapse_fix=False):
         """Realize one call's records into the pending buffers (target side).
         Returns the record count.  sm/construction.py:410-432 + 530-534."""
         n_src, n_tgt = len(sources), len(targets)
@@ -568,6 +568,12 @@ class Cluster:
                      _ptr(pay_tab), 1, 0, _ptr(vals), 0, 0, 0, 0, 0, 0, cur.ctypes.data, sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
+        if autapse_fix and n:
+            # redraw self-connections from the same stream, continuing after
+            # the pair draws (sm/construction.py:524-529)
+            u0 = int(cur[0])
+            call("smx_autapse_fix", local_key[0], local_key[1], u0, n_src, _ptr(key_tab), _ptr(keys), _ptr(vals),
+                 n, _ptr(st.node2row.t), st.node2row.n, cur.ctypes.data, sk)
         if st.wide:
             self._write_syn(st, syn, port, base, n, syn_key)
         st.commit_records(n)
@@ -583,8 +589,6 @@ class Cluster:
                 raise ValueError(f"{name} index outside the rank's node range")
         conn.validate(len(sources), len(targets))
         syn.validate()
-        if not conn.allow_autapses and conn.rule in ("fixed_indegree", "fixed_total"):
-            raise NotImplementedError("allow_autapses=False (redraw loop) is not implemented yet")
         if conn.rule == "fixed_indegree" and not conn.allow_multapses:
             raise NotImplementedError("allow_multapses=False (choice without replacement) is not implemented yet")
         return sources, targets
@@ -607,7 +611,9 @@ class Cluster:
         ctr = self.local_ctr[rank]
         k = self._key(("conn-local", rank, ctr))
         n, _ = self._emit_records(st, conn, sources, targets, syn, port, k, k,
-                                  self._key(("syn-local", rank, ctr)))
+                                  self._key(("syn-local", rank, ctr)),
+                                  autapse_fix=not conn.allow_autapses and conn.rule in ("fixed_indegree",
+                                                                                       "fixed_total"))
         return n
 
     def connect_remote(self, src_rank: int, sources, tgt_rank: int, targets, conn: ConnSpec,

@@ -79,6 +79,21 @@ def rules_random(ns, seed=5):
     return c, (0.0, 5.0)
 
 
+def rules_no_autapse(ns, seed=8):
+    """allow_autapses=False: self-connections redrawn from the call's stream
+    (sm/construction.py:524-529); tiny populations force several rounds."""
+    cfg = ns.SimConfig(n_ranks=1, seed=seed)
+    c = ns.make_cluster(cfg)
+    a = c.create_neurons(0, 40, ns.LifParams(i_e=0.3), ("normal", -60.0, 3.0), gids=np.arange(40))
+    A = np.arange(a.start, a.stop)
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    c.connect(0, A, A, S("fixed_indegree", k_in=12, allow_autapses=False), Sy(0.25, 2))
+    c.connect(0, A[:3], A[:3], S("fixed_indegree", k_in=40, allow_autapses=False), Sy(0.125, 3))
+    c.connect(0, A[:6], A[:6], S("fixed_total", n_total=300, allow_autapses=False), Sy(("normal", 0.1, 0.01), 2))
+    c.connect(0, A, A, S("fixed_total", n_total=500, allow_autapses=False), Sy(-0.25, ("uniform_int", 1, 4)))
+    return c, (0.0, 5.0)
+
+
 def remote_random(ns, mode="p2p", seed=6):
     cfg = ns.SimConfig(n_ranks=2, comm_mode=mode, seed=seed)
     c = ns.make_cluster(cfg)
@@ -164,8 +179,9 @@ SCENARIOS = {
     "remote_random_p2p": lambda ns: remote_random(ns, "p2p"),
     "remote_random_coll": lambda ns: remote_random(ns, "collective"),
     "microcircuit_small": microcircuit,
+    "rules_no_autapse": rules_no_autapse,
 }
 
 # scenarios whose weights are not dyadic: tables are bit-exact, the raster is
 # compared with a tolerance (fp64 sums depend on the atomic delivery order)
-NON_DYADIC = {"rules_random", "remote_random_p2p", "remote_random_coll", "microcircuit_small"}
+NON_DYADIC = {"rules_random", "remote_random_p2p", "remote_random_coll", "microcircuit_small", "rules_no_autapse"}

@@ -130,7 +130,8 @@ void smx_sort_timing(unsigned long long* counters);
 int smx_counts_to_offsets(const uint32_t* counts, uint64_t n, int64_t* first_index, void* stream);
 int smx_gather_wide(const uint32_t* idx, uint64_t n, const uint32_t* rows_in, const double* w_in,
                     const uint32_t* meta_in, uint32_t* rows, double* w, uint32_t* meta, void* stream);
-int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out2, void* stream);
+/* out3 = {max delay, max port, min delay} of wide records */
+int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out3, void* stream);
 /* _build_point_routes / _build_group_routes (sm/construction.py:710-739);
  * tabs_host: array of {u32* bits, i64* excl, u64 nwords, i32 dest}. */
 int smx_build_routes(const void* tabs_host, int nt, uint64_t n_nodes, uint32_t* cnt_scratch, int64_t* first,
@@ -167,8 +168,8 @@ int smx_deliver(const uint32_t* src_nodes, const uint32_t* src_steps, const uint
 /* One complete local step (sm/engine.py:285-296) in three launches: fused
  * consume + LIF + Poisson emission + spike compaction + raster + packet
  * routing; local delivery; step-counter advance.  devs_host: array of
- * {u8* counts[S][n_t], u32* rows, u32 n_t, double w, int delay, int port}
- * (Poisson devices with unique target rows); the step is *now_dev +
+ * {u8* counts[S][n_t], i32* inv (row -> target index or -1), u32 n_t,
+ * double w, int delay, int port} (Poisson devices with unique target rows); the step is *now_dev +
  * step_offset; ctr: 2 x u64 list counters indexed by step parity; owner:
  * work item -> list entry scratch. */
 int smx_step(double* v, int32_t* ref, const double* decay, const double* v_rest, const double* v_reset,
@@ -180,6 +181,21 @@ int smx_step(double* v, int32_t* ref, const double* decay, const double* v_rest,
              const void* p2p_host, const void* grp_host, const uint32_t* payload, const double* cls_w,
              const uint32_t* cls_delay, const uint32_t* cls_port, const double* wide_w, const uint32_t* wide_meta,
              void* stream);
+
+/* A block of n_steps local steps in two launches when every record delay
+ * is >= n_steps (Poisson devices are applied by the target row's thread):
+ * per-thread multi-step LIF with state in registers, then one
+ * delivery of all the block's spikes.  Same arguments as smx_step plus
+ * n_steps; ctr[0] is the block's list counter. */
+int smx_block(double* v, int32_t* ref, const double* decay, const double* v_rest, const double* v_reset,
+              const double* v_th, const int32_t* ref_steps, const double* i_e, uint32_t n, double* ring, int n_ports,
+              int L, int64_t* now_dev, int step_offset, int n_steps, const int* record_dev, int S,
+              const void* devs_host, int n_dev, const uint32_t* row2node, const int64_t* gid, const int64_t* first,
+              uint32_t* src_nodes, uint32_t* src_steps, uint32_t* wbase, uint32_t* owner, uint32_t owner_cap,
+              unsigned long long* ctr, uint32_t src_cap, int64_t* rec, unsigned long long* n_rec, uint64_t rec_cap,
+              int* err, const void* p2p_host, const void* grp_host, const uint32_t* payload, const double* cls_w,
+              const uint32_t* cls_delay, const uint32_t* cls_port, const double* wide_w, const uint32_t* wide_meta,
+              void* stream);
 
 /* --- reference-layout drop-ins for sm/kernels (kernels/__init__.py:25-26) ---
  * lif_step (_speedups.pyx:13-35): v f64[n], ref_count i64[n], real_mask u8[n],

@@ -351,18 +351,20 @@ __global__ void gather_wide_kernel(const uint32_t* idx, uint64_t n, const uint32
   meta[i] = meta_in[j];
 }
 
-__global__ void max_meta_kernel(const uint32_t* meta, uint64_t n, uint32_t* max_delay, uint32_t* max_port) {
-  uint32_t md = 0, mp = 0;
+__global__ void max_meta_kernel(const uint32_t* meta, uint64_t n, uint32_t* out3) {
+  uint32_t md = 0, mp = 0, mn = 0xffffffffu;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t m = meta[i];
     md = max(md, m & 0xffffffu);
+    mn = min(mn, m & 0xffffffu);
     mp = max(mp, m >> 24);
   }
   for (int o = 16; o; o >>= 1) {
     md = max(md, __shfl_xor_sync(0xffffffffu, md, o));
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     mp = max(mp, __shfl_xor_sync(0xffffffffu, mp, o));
   }
-  if ((threadIdx.x & 31) == 0) { atomicMax(max_delay, md); atomicMax(max_port, mp); }
+  if ((threadIdx.x & 31) == 0) { atomicMax(out3, md); atomicMax(out3 + 1, mp); atomicMin(out3 + 2, mn); }
 }
 
 }  // namespace
@@ -584,11 +586,13 @@ extern "C" int smx_gather_wide(const uint32_t* idx, uint64_t n, const uint32_t* 
   return 0;
 }
 
-extern "C" int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out2, void* stream) {
+// out3 = {max delay, max port, min delay} of wide records (meta = delay | port << 24)
+extern "C" int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out3, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  SMX_CUDA_CHECK(cudaMemsetAsync(out2, 0, 8, st));
+  SMX_CUDA_CHECK(cudaMemsetAsync(out3, 0, 8, st));
+  SMX_CUDA_CHECK(cudaMemsetAsync(out3 + 2, 0xff, 4, st));
   if (n == 0) return 0;
-  smx_count_launch(); max_meta_kernel<<<148 * 4, T256, 0, st>>>(meta, n, out2, out2 + 1);
+  smx_count_launch(); max_meta_kernel<<<148 * 4, T256, 0, st>>>(meta, n, out3);
   SMX_LAUNCH_CHECK();
   return 0;
 }

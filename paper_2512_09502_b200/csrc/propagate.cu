@@ -326,7 +326,7 @@ constexpr int MAX_FUSED_DEV = 8;
 
 struct FusedDev {
   const uint8_t* counts;  // [S][n_t]
-  const uint32_t* rows;
+  const int32_t* inv;     // row -> target index, -1 if the row is not a target
   uint32_t n_t;
   double w;
   int delay, port;
@@ -427,15 +427,19 @@ __global__ void __launch_bounds__(T256) step_kernel(const __grid_constant__ Step
   const int64_t now = *A.now_dev + A.step_offset;
   const int par = (int)(now & 1);
   if (i == 0) A.ctr[par ^ 1] = 0ULL;  // next step's list (its last reader finished)
-  // Poisson emission into slot (now + delay) % L, thread t = target t
-  for (int k = 0; k < A.n_dev; ++k) {
-    const FusedDev& D = A.dev[k];
-    if (i < D.n_t) {
-      const uint32_t c = D.counts[(size_t)(now % A.S) * D.n_t + i];
-      if (c) {
-        const int slot = (int)((now + D.delay) % A.L);
-        double* cell = A.ring + ((size_t)slot * A.n_ports + D.port) * A.n + D.rows[i];
-        *cell = __dadd_rn(*cell, __dmul_rn(D.w, (double)c));
+  // Poisson emission into slot (now + delay) % L by the thread that owns the
+  // target row: every read-modify-write of a ring cell is thread-local
+  if (i < A.n) {
+    for (int k = 0; k < A.n_dev; ++k) {
+      const FusedDev& D = A.dev[k];
+      const int32_t t = D.inv[i];
+      if (t >= 0) {
+        const uint32_t c = D.counts[(size_t)(now % A.S) * D.n_t + t];
+        if (c) {
+          const int slot = (int)((now + D.delay) % A.L);
+          double* cell = A.ring + ((size_t)slot * A.n_ports + D.port) * A.n + i;
+          *cell = __dadd_rn(*cell, __dmul_rn(D.w, (double)c));
+        }
       }
     }
   }
@@ -481,7 +485,7 @@ __global__ void __launch_bounds__(T256) deliver_step_kernel(const uint32_t* src_
                                                             const double* wide_w, const uint32_t* wide_meta,
                                                             double* ring, uint32_t n_rows, int n_ports, int L,
                                                             int step_offset) {
-  const unsigned long long c = ctr[(*now_dev + step_offset) & 1];
+  const unsigned long long c = now_dev ? ctr[(*now_dev + step_offset) & 1] : ctr[0];
   const uint32_t nw = (uint32_t)(c & 0xffffffffULL);
   if (nw == 0) return;
   __shared__ double cw[256];
@@ -525,6 +529,72 @@ __global__ void __launch_bounds__(T256) deliver_step_kernel(const uint32_t* src_
       atomicAdd(ring + slot * slot_stride + (size_t)port * n_rows + row, wt);
     }
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Multi-step block kernel: when every connection delay and every non-aligned
+// Poisson delay is >= n_steps, the n_steps LIF updates of a block do not see
+// each other's spikes (a spike emitted at t lands in slot t + d >= block end).
+// Each thread then advances its neuron through the whole block with the state
+// in registers -- ring slot, Poisson count and LIF per step -- and appends its
+// spikes (node, step) to one delivery list for the block (sm/engine.py:285-296
+// repeated n_steps times, identical results).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(T256) lif_block_kernel(const __grid_constant__ StepArgs A, int n_steps) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t t0 = *A.now_dev + A.step_offset;
+  const bool live = i < A.n;
+  double v = 0.0, vr = 0.0, vreset = 0.0, vth = 0.0, decay = 0.0, ie = 0.0;
+  int32_t ref = 0, refsteps = 0;
+  if (live) {
+    v = A.s.v[i]; ref = A.s.ref[i];
+    vr = A.s.v_rest[i]; vreset = A.s.v_reset[i]; vth = A.s.v_th[i]; decay = A.s.decay[i]; ie = A.s.i_e[i];
+    refsteps = A.s.ref_steps[i];
+  }
+  for (int s = 0; s < n_steps; ++s) {
+    const int64_t now = t0 + s;
+    bool spk = false;
+    if (live) {
+      const uint32_t slot = (uint32_t)(now % A.L);
+      double* base = A.ring + (size_t)slot * A.n_ports * A.n;
+      double in = base[i];
+      base[i] = 0.0;
+      for (int p = 1; p < A.n_ports; ++p) {
+        in = __dadd_rn(in, base[(size_t)p * A.n + i]);
+        base[(size_t)p * A.n + i] = 0.0;
+      }
+      in = __dadd_rn(in, ie);
+      if (ref > 0) {
+        ref -= 1;
+        v = vreset;
+      } else {
+        const double integ = __dadd_rn(__dadd_rn(vr, __dmul_rn(__dsub_rn(v, vr), decay)), in);
+        if (integ >= vth) { spk = true; v = vreset; ref = refsteps; }
+        else v = integ;
+      }
+    }
+    // Poisson emission of this step by the row's own thread: the slot
+    // (now + d) % L it writes is read by this thread only, at time now + d
+    if (live) {
+      for (int k = 0; k < A.n_dev; ++k) {
+        const FusedDev& D = A.dev[k];
+        const int32_t t = D.inv[i];
+        if (t >= 0) {
+          const uint32_t c = D.counts[(size_t)(now % A.S) * D.n_t + t];
+          if (c) {
+            const uint32_t slot = (uint32_t)((now + D.delay) % A.L);
+            double* cell = A.ring + ((size_t)slot * A.n_ports + D.port) * A.n + i;
+            *cell = __dadd_rn(*cell, __dmul_rn(D.w, (double)c));
+          }
+        }
+      }
+    }
+    const uint32_t ball = __ballot_sync(0xffffffffu, spk);
+    if (ball) spike_lists(A, i, lane, now, 0, spk, ball);
+  }
+  if (live) { A.s.v[i] = v; A.s.ref[i] = ref; }
 }
 
 }  // namespace
@@ -631,7 +701,7 @@ extern "C" int smx_deliver(const uint32_t* src_nodes, const uint32_t* src_steps,
 // Host mirror of the fused-device descriptor.
 struct SmxFusedDev {
   const uint8_t* counts;
-  const uint32_t* rows;
+  const int32_t* inv;
   uint32_t n_t;
   double w;
   int delay, port;
@@ -668,9 +738,8 @@ extern "C" int smx_step(double* v, int32_t* ref, const double* decay, const doub
   A.n_dev = n_dev;
   uint32_t threads = n;
   for (int k = 0; k < n_dev; ++k) {
-    A.dev[k] = FusedDev{devs_host[k].counts, devs_host[k].rows, devs_host[k].n_t, devs_host[k].w,
+    A.dev[k] = FusedDev{devs_host[k].counts, devs_host[k].inv, devs_host[k].n_t, devs_host[k].w,
                         devs_host[k].delay, devs_host[k].port};
-    threads = std::max(threads, devs_host[k].n_t);
   }
   A.row2node = row2node;
   A.gid = gid;
@@ -701,6 +770,70 @@ extern "C" int smx_step(double* v, int32_t* ref, const double* decay, const doub
   } else {
     smx_count_launch(); deliver_step_kernel<false><<<grid, T256, 0, st>>>(src_nodes, src_steps, wbase, owner, ctr, now_dev, first,
                                                          payload, syn, wide_w, wide_meta, ring, n, n_ports, L, step_offset);
+  }
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+// A block of n_steps local steps in two launches (lif_block_kernel, then the
+// delivery of every spike of the block); preconditions in lif_block_kernel.
+extern "C" int smx_block(double* v, int32_t* ref, const double* decay, const double* v_rest, const double* v_reset,
+                         const double* v_th, const int32_t* ref_steps, const double* i_e, uint32_t n, double* ring,
+                         int n_ports, int L, int64_t* now_dev, int step_offset, int n_steps, const int* record_dev,
+                         int S, const SmxFusedDev* devs_host, int n_dev, const uint32_t* row2node, const int64_t* gid,
+                         const int64_t* first, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* wbase,
+                         uint32_t* owner, uint32_t owner_cap, unsigned long long* ctr, uint32_t src_cap, int64_t* rec,
+                         unsigned long long* n_rec, uint64_t rec_cap, int* err, const SmxRoutes* p2p,
+                         const SmxRoutes* grp, const uint32_t* payload, const double* cls_w, const uint32_t* cls_delay,
+                         const uint32_t* cls_port, const double* wide_w, const uint32_t* wide_meta, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_dev > MAX_FUSED_DEV) {
+    smx_set_error("smx_block: at most %d fused Poisson devices", MAX_FUSED_DEV);
+    return -1;
+  }
+  StepArgs A;
+  A.s = LifState{v, ref, decay, v_rest, v_reset, v_th, ref_steps, i_e};
+  A.n = n;
+  A.ring = ring;
+  A.n_ports = n_ports;
+  A.L = L;
+  A.now_dev = now_dev;
+  A.record_dev = record_dev;
+  A.S = S;
+  A.n_dev = n_dev;
+  uint32_t threads = n;
+  for (int k = 0; k < n_dev; ++k) {
+    A.dev[k] = FusedDev{devs_host[k].counts, devs_host[k].inv, devs_host[k].n_t, devs_host[k].w,
+                        devs_host[k].delay, devs_host[k].port};
+  }
+  A.row2node = row2node;
+  A.gid = gid;
+  A.first = first;
+  A.src_nodes = src_nodes;
+  A.src_steps = src_steps;
+  A.wbase = wbase;
+  A.owner = owner;
+  A.owner_cap = owner_cap;
+  A.ctr = ctr;
+  A.src_cap = src_cap;
+  A.rec = rec;
+  A.n_rec = n_rec;
+  A.rec_cap = rec_cap;
+  A.err = err;
+  A.step_offset = step_offset;
+  A.p2p = p2p ? Routes{p2p->first, p2p->dest, p2p->pos, p2p->n_dest, p2p->packets, p2p->counts, p2p->cap} : Routes{};
+  A.grp = grp ? Routes{grp->first, grp->dest, grp->pos, grp->n_dest, grp->packets, grp->counts, grp->cap} : Routes{};
+  if (threads == 0) threads = 1;
+  SMX_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+  smx_count_launch(); lif_block_kernel<<<nblk(threads), T256, 0, st>>>(A, n_steps);
+  SynTable syn{cls_w, cls_delay, cls_port};
+  const int grid = 148 * 8;
+  if (wide_w) {
+    smx_count_launch(); deliver_step_kernel<true><<<grid, T256, 0, st>>>(src_nodes, src_steps, wbase, owner, ctr, nullptr, first,
+                                                        payload, syn, wide_w, wide_meta, ring, n, n_ports, L, 0);
+  } else {
+    smx_count_launch(); deliver_step_kernel<false><<<grid, T256, 0, st>>>(src_nodes, src_steps, wbase, owner, ctr, nullptr, first,
+                                                         payload, syn, wide_w, wide_meta, ring, n, n_ports, L, 0);
   }
   SMX_LAUNCH_CHECK();
   return 0;

@@ -969,6 +969,8 @@ class Cluster:
                                       [np.empty(0, np.int64)])
                 if len(np.unique(gids)) != len(gids):
                     raise ConsistencyError("neuron gids must be globally unique")
+            for st in self.ranks.values():
+                self._delay_stats(st)
             self.block = self._block_size()
             self.group_slots = {g: i for i, g in enumerate(sorted(self.groups))}
             for st in self.ranks.values():
@@ -986,25 +988,30 @@ class Cluster:
         return any(bool(st.mirrors) or any(k[0] == POINT_TO_POINT for k in st.maps)
                    for st in self.ranks.values())
 
+    def _delay_stats(self, st: _Rank):
+        """Delays and ports in use (sm/construction.py:759-768) plus the
+        smallest record delay (it bounds the multi-step LIF block)."""
+        max_delay, max_port, min_delay = 1, 0, None
+        if st.wide and st.w_meta.n:
+            mm = torch.zeros(3, dtype=torch.int32, device=st.device)
+            call("smx_max_meta", _ptr(st.w_meta.t), st.w_meta.n, _ptr(mm), st.stream)
+            mm = mm.cpu().numpy().view(np.uint32)
+            max_delay, max_port, min_delay = max(max_delay, int(mm[0])), max(max_port, int(mm[1])), int(mm[2])
+        elif not st.wide:
+            for c in st.used_classes:
+                _, d, p = self.classes[int(c)]
+                max_delay, max_port = max(max_delay, d), max(max_port, p)
+                min_delay = d if min_delay is None else min(min_delay, d)
+        for d in st.devices:
+            max_delay, max_port = max(max_delay, d["delay"]), max(max_port, d["port"])
+        st.max_delay, st.max_port, st.min_delay = max_delay, max_port, min_delay
+
     def _prepare_rank(self, st: _Rank):
         dev, sk = st.device, st.stream
         dt = self.cfg.resolution_ms
         n_nodes = st.n_nodes
-        # delays / ports in use (sm/construction.py:759-768)
-        max_delay, max_port = 1, 0
-        if st.wide:
-            mm = torch.zeros(2, dtype=torch.int32, device=dev)
-            call("smx_max_meta", _ptr(st.w_meta.t), st.w_meta.n, _ptr(mm), sk)
-            mm = mm.cpu().numpy()
-            max_delay, max_port = max(max_delay, int(mm[0])), max(max_port, int(mm[1]))
-        else:
-            for c in st.used_classes:
-                _, d, p = self.classes[int(c)]
-                max_delay, max_port = max(max_delay, d), max(max_port, p)
-        for d in st.devices:
-            max_delay, max_port = max(max_delay, d["delay"]), max(max_port, d["port"])
-        st.L = max(2, max_delay + 1)
-        st.P = 1 + max_port
+        st.L = max(2, st.max_delay + 1)
+        st.P = 1 + st.max_port
         # neuron state, real rows only (sm/dynamics.py:153-189)
         N = st.n_real
         st.N = N
@@ -1185,12 +1192,21 @@ class Cluster:
         act = [d for d in st.devices if d["active"]]
         st.fused = len(act) <= 8 and all(len(np.unique(d["rows"].cpu().numpy())) == d["nt"] for d in act)
         st.ctr = torch.zeros(2, dtype=torch.int64, device=dev)
-        st.owner_cap = st.n_records // 1024 + N + 16
+        fi = st.first_index
+        max_len = int((fi[1:] - fi[:-1]).max().item()) if st.n_nodes else 0
+        max_chunks = max(1, -(-max_len // 1024))
+        st.owner_cap = N * B * max_chunks + 16
+        # multi-step LIF blocks: every record delay >= block length (Poisson
+        # devices are applied by their target row's own thread)
+        st.block_ok = st.min_delay is None or st.min_delay >= B
         st.owner = torch.zeros(st.owner_cap, dtype=torch.int32, device=dev)
         st.fdev = (ctypes_fdev * max(len(act), 1))()
         for k, d in enumerate(act):
+            inv = np.full(max(N, 1), -1, dtype=np.int32)
+            inv[d["rows"].cpu().numpy()] = np.arange(d["nt"], dtype=np.int32)
+            d["inv"] = _up(inv, dev)
             st.fdev[k].counts = _ptr(d["counts"])
-            st.fdev[k].rows = _ptr(d["rows"])
+            st.fdev[k].inv = _ptr(d["inv"])
             st.fdev[k].n_t = d["nt"]
             st.fdev[k].w = d["weight"]
             st.fdev[k].delay = d["delay"]
@@ -1204,7 +1220,10 @@ class Cluster:
         = min remote delay steps delivers every spike before its slot is read
         (the script-level minimum is identical on every rank)."""
         if self.n_ranks == 1 or self.min_remote_delay is None:
-            return 16
+            # no exchange: the block only sets the CUDA-graph / LIF-block length
+            mins = [st.min_delay for st in self.ranks.values() if st.min_delay is not None]
+            m = min(mins) if mins else 32
+            return int(min(m, 32)) if m >= 4 else 16
         return int(max(1, min(self.min_remote_delay, 32)))
 
     def _poisson_batch(self, st, now):
@@ -1247,15 +1266,28 @@ class Cluster:
              ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), sk)
         self._deliver(st)
 
+    def _block_kernels(self, st, n_steps: int):
+        """n_steps steps of one rank in two launches (smx_block)."""
+        call("smx_block", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
+             _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, _ptr(st.now_dev),
+             0, n_steps, _ptr(st.record_dev), st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
+             _ptr(st.gid_t), _ptr(st.first_index), _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.wprefix),
+             _ptr(st.owner), st.owner_cap, _ptr(st.ctr), st.src_cap, _ptr(st.rec), _ptr(st.n_rec), st.rec_cap,
+             _ptr(st.err), ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), _ptr(st.payload), _ptr(st.cls_w),
+             _ptr(st.cls_delay), _ptr(st.cls_port), _ptr(st.ww), _ptr(st.wm), st.stream)
+
     def _deliver(self, st):
         call("smx_deliver", _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), _ptr(st.wprefix),
              _ptr(st.n_work), _ptr(st.first_index), _ptr(st.payload), _ptr(st.cls_w), _ptr(st.cls_delay),
              _ptr(st.cls_port), _ptr(st.ww), _ptr(st.wm), _ptr(st.ring), st.N, st.P, st.L, 0, st.stream)
 
     def _block_body(self, n_steps: int):
-        for j in range(n_steps):
-            for st in self.ranks.values():
-                self._step_kernels(st, j)
+        for st in self.ranks.values():
+            if st.fused and st.block_ok and n_steps > 1:
+                self._block_kernels(st, n_steps)
+            else:
+                for j in range(n_steps):
+                    self._step_kernels(st, j)
         if self.n_ranks > 1 and not self.distributed:
             self._exchange_local()
 
@@ -1555,7 +1587,7 @@ class ctypes_route(ctypes.Structure):
 
 
 class ctypes_fdev(ctypes.Structure):
-    _fields_ = [("counts", ctypes.c_void_p), ("rows", ctypes.c_void_p), ("n_t", ctypes.c_uint32),
+    _fields_ = [("counts", ctypes.c_void_p), ("inv", ctypes.c_void_p), ("n_t", ctypes.c_uint32),
                 ("w", ctypes.c_double), ("delay", ctypes.c_int), ("port", ctypes.c_int)]
 
 

@@ -94,6 +94,31 @@ def rules_no_autapse(ns, seed=8):
     return c, (0.0, 5.0)
 
 
+def poisson_multi(ns, mode="p2p", seed=12):
+    """Several Poisson devices per rank with overlapping, permuted targets and
+    delays below / above the exchange block (all records delay >= 5, so ranks
+    run multi-step LIF blocks of 5)."""
+    cfg = ns.SimConfig(n_ranks=2, comm_mode=mode, seed=seed)
+    c = ns.make_cluster(cfg)
+    group = -1
+    if mode == "collective":
+        group = 0
+        c.declare_group(0, [0, 1])
+    pops = []
+    for r in range(2):
+        x = c.create_neurons(r, 90, ns.LifParams(), ("normal", -60.0, 3.0), gids=r * 90 + np.arange(90))
+        pops.append(np.arange(x.start, x.stop))
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    for r in range(2):
+        c.connect(r, pops[r], pops[r], S("fixed_indegree", k_in=8), Sy(0.25, 5))
+        c.add_poisson_source(r, 8000.0, 0.125, 2, pops[r])
+        c.add_poisson_source(r, 5000.0, 0.25, 9, pops[r][::-1][:40])
+        c.add_poisson_source(r, 3000.0, 0.5, 5, pops[r][10:70:3])
+    c.connect_remote(0, pops[0], 1, pops[1], S("fixed_indegree", k_in=6), Sy(0.125, 5), group=group)
+    c.connect_remote(1, pops[1], 0, pops[0], S("fixed_indegree", k_in=6), Sy(-0.25, 7), group=group)
+    return c, (0.0, 12.0)
+
+
 def remote_random(ns, mode="p2p", seed=6):
     cfg = ns.SimConfig(n_ranks=2, comm_mode=mode, seed=seed)
     c = ns.make_cluster(cfg)
@@ -180,6 +205,8 @@ SCENARIOS = {
     "remote_random_coll": lambda ns: remote_random(ns, "collective"),
     "microcircuit_small": microcircuit,
     "rules_no_autapse": rules_no_autapse,
+    "poisson_multi_p2p": lambda ns: poisson_multi(ns, "p2p"),
+    "poisson_multi_coll": lambda ns: poisson_multi(ns, "collective"),
 }
 
 # scenarios whose weights are not dyadic: tables are bit-exact, the raster is

@@ -1166,6 +1166,10 @@ class Cluster:
         st.p2p_desc = ctypes_routes_desc(st.TP, st.p2p_packets, st.p2p_counts, self.n_ranks, st.pk_cap)
         st.g_desc = ctypes_routes_desc(st.GQ, st.g_packets, st.g_counts, len(self.groups), st.pk_cap)
         st.graph = None
+        st.pois_stream = torch.cuda.Stream(device=dev)
+        st.pois_ready = None
+        st.pois_next = -1
+        st.pois_have = -1
         # Poisson devices: numpy-exact counts generated for S steps at a time
         # (S a multiple of the exchange block, so a block never straddles two
         # batches and can be replayed from a CUDA graph)
@@ -1181,7 +1185,7 @@ class Cluster:
             if not d["active"]:
                 continue
             S = st.pois_steps
-            d["counts"] = torch.zeros(S * nt, dtype=torch.uint8, device=dev)
+            d["counts"] = torch.zeros(2 * S * nt, dtype=torch.uint8, device=dev)  # 2 batches (ring of 2S steps)
             d["cursor"] = torch.zeros(2, dtype=torch.int64, device=dev)
             d["ping"] = 0
             d["chunks"] = _lib.lib().smx_poisson_chunks_for(S * nt, d["lam"])
@@ -1226,18 +1230,42 @@ class Cluster:
             return int(min(m, 32)) if m >= 4 else 16
         return int(max(1, min(self.min_remote_delay, 32)))
 
-    def _poisson_batch(self, st, now):
-        """Counts for steps [now, now + S) of every active device (now % S == 0)."""
+    def _poisson_gen(self, st, b0, stream):
+        """Counts for steps [b0, b0 + S) of every active device into ring half
+        (b0 / S) % 2, on `stream` (numpy-exact, cursor carried on the device)."""
         S = st.pois_steps
+        half = (b0 // S) % 2
         for d in st.devices:
-            if not d["active"] or d["batch0"] == now:
+            if not d["active"]:
                 continue
             cin = d["cursor"][d["ping"]:]
             cout = d["cursor"][1 - d["ping"]:]
             call("smx_poisson_counts", d["key"][0], d["key"][1], _ptr(cin), d["enlam"], S * d["nt"],
-                 d["chunks"], _ptr(d["ws"]), _ptr(d["counts"]), _ptr(cout), _ptr(st.err), st.stream)
+                 d["chunks"], _ptr(d["ws"]), _ptr(d["counts"][half * S * d["nt"]:]), _ptr(cout), _ptr(st.err),
+                 stream.cuda_stream)
             d["ping"] = 1 - d["ping"]
-            d["batch0"] = now
+
+    def _poisson_batch(self, st, b0):
+        """Make batch b0 ready for the main stream and start generating batch
+        b0 + S on a side stream, overlapped with the propagation of batch b0
+        (the Poisson chain only depends on the previous batch's cursor)."""
+        if not any(d["active"] for d in st.devices):
+            return
+        S = st.pois_steps
+        main = torch.cuda.current_stream(st.device)
+        if st.pois_next != b0:  # first batch, or steps were skipped: generate in line
+            self._poisson_gen(st, b0, main)
+        else:
+            main.wait_event(st.pois_ready)
+        # batch b0 + S reuses the half of batch b0 - S: everything queued on
+        # the main stream so far (batch b0 - S's steps) must finish first
+        freed = torch.cuda.Event()
+        freed.record(main)
+        st.pois_stream.wait_event(freed)
+        self._poisson_gen(st, b0 + S, st.pois_stream)
+        st.pois_ready = torch.cuda.Event()
+        st.pois_ready.record(st.pois_stream)
+        st.pois_next = b0 + S
 
     def _step_kernels(self, st, offset: int = 0):
         """One step of one rank, every argument device-resident (graph-safe):
@@ -1247,7 +1275,7 @@ class Cluster:
         if st.fused:
             call("smx_step", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
                  _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, _ptr(st.now_dev),
-                 offset, _ptr(st.record_dev), st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
+                 offset, _ptr(st.record_dev), 2 * st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
                  _ptr(st.gid_t), _ptr(st.first_index), _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.wprefix),
                  _ptr(st.owner), st.owner_cap, _ptr(st.ctr), st.src_cap, _ptr(st.rec), _ptr(st.n_rec), st.rec_cap,
                  _ptr(st.err), ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), _ptr(st.payload), _ptr(st.cls_w),
@@ -1258,7 +1286,7 @@ class Cluster:
              _ptr(st.spike_bits), sk)
         for d in st.devices:
             if d["active"]:
-                call("smx_poisson_emit", _ptr(d["counts"]), st.pois_steps, d["nt"], _ptr(d["rows"]), d["weight"],
+                call("smx_poisson_emit", _ptr(d["counts"]), 2 * st.pois_steps, d["nt"], _ptr(d["rows"]), d["weight"],
                      _ptr(st.ring), st.N, st.P, st.L, d["delay"], d["port"], _ptr(st.now_dev), sk)
         call("smx_spikes", _ptr(st.spike_bits), st.N, _ptr(st.row2node_t), _ptr(st.gid_t), _ptr(st.now_dev),
              _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.record_dev),
@@ -1270,7 +1298,7 @@ class Cluster:
         """n_steps steps of one rank in two launches (smx_block)."""
         call("smx_block", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
              _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, _ptr(st.now_dev),
-             0, n_steps, _ptr(st.record_dev), st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
+             0, n_steps, _ptr(st.record_dev), 2 * st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
              _ptr(st.gid_t), _ptr(st.first_index), _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.wprefix),
              _ptr(st.owner), st.owner_cap, _ptr(st.ctr), st.src_cap, _ptr(st.rec), _ptr(st.n_rec), st.rec_cap,
              _ptr(st.err), ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), _ptr(st.payload), _ptr(st.cls_w),
@@ -1295,9 +1323,10 @@ class Cluster:
         """n_steps steps of every local rank, then one exchange round."""
         now = self.now
         for st in self.ranks.values():
-            if now % st.pois_steps == 0 or any(d["active"] and d["batch0"] != now - now % st.pois_steps
-                                               for d in st.devices):
-                self._poisson_batch(st, now - now % st.pois_steps)
+            b0 = now - now % st.pois_steps
+            if st.pois_have != b0:
+                self._poisson_batch(st, b0)
+                st.pois_have = b0
         for st in self.ranks.values():
             st.now_dev.fill_(now)  # block start; fused steps add their offset
         if use_graph:

@@ -375,6 +375,29 @@ __device__ __forceinline__ void route_spike(const Routes& R, uint32_t node, int6
   }
 }
 
+// Poisson drive consumed at arrival time: the count a device emitted at
+// step now - d onto this row (PoissonSource.emit_into adds w * count into
+// slot (t + d) % L, sm/dynamics.py:235-248; for dyadic w the sum is the same
+// whether it passes through the ring or is added here).  counts is a ring of
+// A.S steps (three batches), so emissions up to one batch back are kept.
+__device__ __forceinline__ double poisson_input(const StepArgs& A, uint32_t i, int64_t now) {
+  double acc = 0.0;
+  bool any = false;
+  for (int k = 0; k < A.n_dev; ++k) {
+    const FusedDev& D = A.dev[k];
+    const int32_t t = D.inv[i];
+    const int64_t te = now - D.delay;
+    if (t < 0 || te < 0) continue;
+    const uint32_t c = __ldg(D.counts + (size_t)(te % A.S) * D.n_t + t);
+    if (c) {
+      const double x = __dmul_rn(D.w, (double)c);
+      acc = any ? __dadd_rn(acc, x) : x;
+      any = true;
+    }
+  }
+  return acc;
+}
+
 __device__ __noinline__ void spike_lists(const StepArgs& A, uint32_t i, int lane, int64_t now, int par, bool spk,
                                               uint32_t ball) {
   // local delivery list: (index, work base) reserved with one 64-bit atomic per warp
@@ -427,22 +450,6 @@ __global__ void __launch_bounds__(T256) step_kernel(const __grid_constant__ Step
   const int64_t now = *A.now_dev + A.step_offset;
   const int par = (int)(now & 1);
   if (i == 0) A.ctr[par ^ 1] = 0ULL;  // next step's list (its last reader finished)
-  // Poisson emission into slot (now + delay) % L by the thread that owns the
-  // target row: every read-modify-write of a ring cell is thread-local
-  if (i < A.n) {
-    for (int k = 0; k < A.n_dev; ++k) {
-      const FusedDev& D = A.dev[k];
-      const int32_t t = D.inv[i];
-      if (t >= 0) {
-        const uint32_t c = D.counts[(size_t)(now % A.S) * D.n_t + t];
-        if (c) {
-          const int slot = (int)((now + D.delay) % A.L);
-          double* cell = A.ring + ((size_t)slot * A.n_ports + D.port) * A.n + i;
-          *cell = __dadd_rn(*cell, __dmul_rn(D.w, (double)c));
-        }
-      }
-    }
-  }
   // consume + LIF (sm/dynamics.py:191-204, kernels/_speedups.pyx:17-35)
   bool spk = false;
   if (i < A.n) {
@@ -454,6 +461,7 @@ __global__ void __launch_bounds__(T256) step_kernel(const __grid_constant__ Step
       in = __dadd_rn(in, base[(size_t)p * A.n + i]);
       base[(size_t)p * A.n + i] = 0.0;
     }
+    in = __dadd_rn(in, poisson_input(A, i, now));
     in = __dadd_rn(in, A.s.i_e[i]);
     const int32_t r = A.s.ref[i];
     if (r > 0) {
@@ -541,6 +549,8 @@ __global__ void __launch_bounds__(T256) deliver_step_kernel(const uint32_t* src_
 // spikes (node, step) to one delivery list for the block (sm/engine.py:285-296
 // repeated n_steps times, identical results).
 // ---------------------------------------------------------------------------
+constexpr int MAX_BLOCK = 16;  // inputs of up to 16 steps held in registers
+
 __global__ void __launch_bounds__(T256) lif_block_kernel(const __grid_constant__ StepArgs A, int n_steps) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -553,19 +563,42 @@ __global__ void __launch_bounds__(T256) lif_block_kernel(const __grid_constant__
     vr = A.s.v_rest[i]; vreset = A.s.v_reset[i]; vth = A.s.v_th[i]; decay = A.s.decay[i]; ie = A.s.i_e[i];
     refsteps = A.s.ref_steps[i];
   }
-  for (int s = 0; s < n_steps; ++s) {
-    const int64_t now = t0 + s;
+  const uint32_t L = (uint32_t)A.L;
+  const size_t slot_stride = (size_t)A.n_ports * A.n;
+  // every input of the block up front: no ring slot read here is written
+  // during the block (all delays >= n_steps; Poisson is consumed at arrival)
+  double rin[MAX_BLOCK];
+  uint32_t sl = (uint32_t)(t0 % A.L);
+#pragma unroll
+  for (int s = 0; s < MAX_BLOCK; ++s) {
+    rin[s] = 0.0;
+    if (s < n_steps && live) {
+      double* base = A.ring + (size_t)sl * slot_stride;
+      double in = base[i];
+      for (int p = 1; p < A.n_ports; ++p) in = __dadd_rn(in, base[(size_t)p * A.n + i]);
+      rin[s] = in;
+    }
+    if (++sl == L) sl = 0;
+  }
+  if (live) {
+#pragma unroll
+    for (int s = 0; s < MAX_BLOCK; ++s) rin[s] = s < n_steps ? __dadd_rn(rin[s], poisson_input(A, i, t0 + s)) : 0.0;
+  }
+  sl = (uint32_t)(t0 % A.L);
+#pragma unroll
+  for (int s = 0; s < MAX_BLOCK; ++s) {
+    if (s < n_steps && live) {
+      double* base = A.ring + (size_t)sl * slot_stride;
+      for (int p = 0; p < A.n_ports; ++p) base[(size_t)p * A.n + i] = 0.0;
+    }
+    if (++sl == L) sl = 0;
+  }
+#pragma unroll
+  for (int s = 0; s < MAX_BLOCK; ++s) {
+    if (s >= n_steps) continue;  // uniform guard keeps rin[] statically indexed
     bool spk = false;
     if (live) {
-      const uint32_t slot = (uint32_t)(now % A.L);
-      double* base = A.ring + (size_t)slot * A.n_ports * A.n;
-      double in = base[i];
-      base[i] = 0.0;
-      for (int p = 1; p < A.n_ports; ++p) {
-        in = __dadd_rn(in, base[(size_t)p * A.n + i]);
-        base[(size_t)p * A.n + i] = 0.0;
-      }
-      in = __dadd_rn(in, ie);
+      const double in = __dadd_rn(rin[s], ie);
       if (ref > 0) {
         ref -= 1;
         v = vreset;
@@ -575,24 +608,8 @@ __global__ void __launch_bounds__(T256) lif_block_kernel(const __grid_constant__
         else v = integ;
       }
     }
-    // Poisson emission of this step by the row's own thread: the slot
-    // (now + d) % L it writes is read by this thread only, at time now + d
-    if (live) {
-      for (int k = 0; k < A.n_dev; ++k) {
-        const FusedDev& D = A.dev[k];
-        const int32_t t = D.inv[i];
-        if (t >= 0) {
-          const uint32_t c = D.counts[(size_t)(now % A.S) * D.n_t + t];
-          if (c) {
-            const uint32_t slot = (uint32_t)((now + D.delay) % A.L);
-            double* cell = A.ring + ((size_t)slot * A.n_ports + D.port) * A.n + i;
-            *cell = __dadd_rn(*cell, __dmul_rn(D.w, (double)c));
-          }
-        }
-      }
-    }
     const uint32_t ball = __ballot_sync(0xffffffffu, spk);
-    if (ball) spike_lists(A, i, lane, now, 0, spk, ball);
+    if (ball) spike_lists(A, i, lane, t0 + s, 0, spk, ball);
   }
   if (live) { A.s.v[i] = v; A.s.ref[i] = ref; }
 }
@@ -825,6 +842,10 @@ extern "C" int smx_block(double* v, int32_t* ref, const double* decay, const dou
   A.grp = grp ? Routes{grp->first, grp->dest, grp->pos, grp->n_dest, grp->packets, grp->counts, grp->cap} : Routes{};
   if (threads == 0) threads = 1;
   SMX_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+  if (n_steps > MAX_BLOCK) {
+    smx_set_error("smx_block: at most %d steps per block", MAX_BLOCK);
+    return -1;
+  }
   smx_count_launch(); lif_block_kernel<<<nblk(threads), T256, 0, st>>>(A, n_steps);
   SynTable syn{cls_w, cls_delay, cls_port};
   const int grid = 148 * 8;

@@ -1172,8 +1172,11 @@ class Cluster:
         st.pois_have = -1
         # Poisson devices: numpy-exact counts generated for S steps at a time
         # (S a multiple of the exchange block, so a block never straddles two
-        # batches and can be replayed from a CUDA graph)
-        st.pois_steps = B * max(1, -(-64 // B))
+        # batches and can be replayed from a CUDA graph).  The fused kernels
+        # add a count at its arrival step now = t + d, reading back up to d
+        # steps: S >= max Poisson delay keeps that inside the previous batch.
+        max_pd = max([int(d["delay"]) for d in st.devices] + [64])
+        st.pois_steps = B * max(1, -(-max_pd // B))
         for d in st.devices:
             nt = len(d["targets"])
             rows = np.asarray(st_node2row_host(st, d["targets"]), dtype=np.int64)
@@ -1185,7 +1188,9 @@ class Cluster:
             if not d["active"]:
                 continue
             S = st.pois_steps
-            d["counts"] = torch.zeros(2 * S * nt, dtype=torch.uint8, device=dev)  # 2 batches (ring of 2S steps)
+            # ring of 3 batches: the one being consumed, the previous one (read
+            # back by delay) and the next one (generated on the side stream)
+            d["counts"] = torch.zeros(3 * S * nt, dtype=torch.uint8, device=dev)
             d["cursor"] = torch.zeros(2, dtype=torch.int64, device=dev)
             d["ping"] = 0
             d["chunks"] = _lib.lib().smx_poisson_chunks_for(S * nt, d["lam"])
@@ -1231,10 +1236,10 @@ class Cluster:
         return int(max(1, min(self.min_remote_delay, 32)))
 
     def _poisson_gen(self, st, b0, stream):
-        """Counts for steps [b0, b0 + S) of every active device into ring half
-        (b0 / S) % 2, on `stream` (numpy-exact, cursor carried on the device)."""
+        """Counts for steps [b0, b0 + S) of every active device into ring third
+        (b0 / S) % 3, on `stream` (numpy-exact, cursor carried on the device)."""
         S = st.pois_steps
-        half = (b0 // S) % 2
+        half = (b0 // S) % 3
         for d in st.devices:
             if not d["active"]:
                 continue
@@ -1257,8 +1262,9 @@ class Cluster:
             self._poisson_gen(st, b0, main)
         else:
             main.wait_event(st.pois_ready)
-        # batch b0 + S reuses the half of batch b0 - S: everything queued on
-        # the main stream so far (batch b0 - S's steps) must finish first
+        # batch b0 + S reuses the third of batch b0 - 2S, last read by batch
+        # b0 - S's steps: everything queued on the main stream so far must
+        # finish first
         freed = torch.cuda.Event()
         freed.record(main)
         st.pois_stream.wait_event(freed)
@@ -1275,7 +1281,7 @@ class Cluster:
         if st.fused:
             call("smx_step", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
                  _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, _ptr(st.now_dev),
-                 offset, _ptr(st.record_dev), 2 * st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
+                 offset, _ptr(st.record_dev), 3 * st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
                  _ptr(st.gid_t), _ptr(st.first_index), _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.wprefix),
                  _ptr(st.owner), st.owner_cap, _ptr(st.ctr), st.src_cap, _ptr(st.rec), _ptr(st.n_rec), st.rec_cap,
                  _ptr(st.err), ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), _ptr(st.payload), _ptr(st.cls_w),
@@ -1286,7 +1292,7 @@ class Cluster:
              _ptr(st.spike_bits), sk)
         for d in st.devices:
             if d["active"]:
-                call("smx_poisson_emit", _ptr(d["counts"]), 2 * st.pois_steps, d["nt"], _ptr(d["rows"]), d["weight"],
+                call("smx_poisson_emit", _ptr(d["counts"]), 3 * st.pois_steps, d["nt"], _ptr(d["rows"]), d["weight"],
                      _ptr(st.ring), st.N, st.P, st.L, d["delay"], d["port"], _ptr(st.now_dev), sk)
         call("smx_spikes", _ptr(st.spike_bits), st.N, _ptr(st.row2node_t), _ptr(st.gid_t), _ptr(st.now_dev),
              _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.record_dev),
@@ -1298,7 +1304,7 @@ class Cluster:
         """n_steps steps of one rank in two launches (smx_block)."""
         call("smx_block", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
              _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, _ptr(st.now_dev),
-             0, n_steps, _ptr(st.record_dev), 2 * st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
+             0, n_steps, _ptr(st.record_dev), 3 * st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
              _ptr(st.gid_t), _ptr(st.first_index), _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.wprefix),
              _ptr(st.owner), st.owner_cap, _ptr(st.ctr), st.src_cap, _ptr(st.rec), _ptr(st.n_rec), st.rec_cap,
              _ptr(st.err), ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), _ptr(st.payload), _ptr(st.cls_w),

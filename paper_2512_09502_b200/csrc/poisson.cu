@@ -54,6 +54,8 @@ __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
   __shared__ uint8_t L[PC + PE];
   __shared__ uint32_t S0[PC / 32];
   __shared__ uint32_t cnt0_pos[PC / 32 + 1];  // S0 popcount prefix per word
+  __shared__ int seg_exit[P_THREADS];
+  __shared__ uint16_t M16[P_THREADS];
   __shared__ int exit0, count0;
   const int c = blockIdx.x, tid = threadIdx.x;
   const uint64_t cw = (*J.w0_dev & ~3ULL) + (uint64_t)c * PC;
@@ -64,7 +66,6 @@ __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) U[4 * q + i] = smx::u53(b[i]);
   }
-  for (int q = tid; q < PC / 32; q += P_THREADS) S0[q] = 0;
   __syncthreads();
   // len(w) for w in [0, PC + PE): products forward; words past the window
   // tail are regenerated one at a time (rare).
@@ -97,18 +98,56 @@ __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
     L[w] = (uint8_t)k;
   }
   __syncthreads();
-  if (tid == 0) {
-    int p = 0, n0 = 0;
-    while (p < PC) {
-      S0[p >> 5] |= 1u << (p & 31);
-      ++n0;
-      p += L[p];
+  // Orbit of starts from entry offset 0 (bitmap S0), segment-parallel: thread
+  // t owns words [SEG*t, SEG*(t+1)) and walks them from its entry (the first
+  // orbit position >= SEG*t).  Round 0 guesses the segment start; each later
+  // round takes the previous thread's exit as the entry and re-walks only
+  // until the walk lands on a start of its previous chain (from there on the
+  // chain is unchanged).  After round r segments 0..r are exact, so the loop
+  // ends at the exact orbit; chains merge within a few samples, so it
+  // normally ends after two or three rounds.
+  {
+    constexpr int SEG = PC / P_THREADS;
+    static_assert(SEG == 16, "segment mask is 16 bits");
+    const int lo = SEG * tid, hi = lo + SEG;
+    uint32_t mask = 0;
+    int entry = lo, ex_ = lo;
+    while (ex_ < hi) { mask |= 1u << (ex_ - lo); ex_ += L[ex_]; }
+    seg_exit[tid] = ex_;
+    for (;;) {
+      __syncthreads();
+      const int e_in = tid == 0 ? 0 : seg_exit[tid - 1];
+      bool changed = false;
+      if (e_in != entry) {
+        entry = e_in;
+        uint32_t m = 0;
+        int p = e_in;
+        while (p < hi && !((mask >> (p - lo)) & 1)) { m |= 1u << (p - lo); p += L[p]; }
+        const int ex_new = p < hi ? ex_ : p;  // merged: same exit as before
+        mask = p < hi ? (m | (mask & ~((1u << (p - lo)) - 1))) : m;
+        changed = ex_new != ex_;
+        ex_ = ex_new;
+      }
+      __syncthreads();
+      seg_exit[tid] = ex_;
+      if (!__syncthreads_or(changed)) break;
     }
-    exit0 = p - PC;
-    count0 = n0;
-    int acc = 0;
-    for (int q = 0; q < PC / 32; ++q) { cnt0_pos[q] = acc; acc += __popc(S0[q]); }
-    cnt0_pos[PC / 32] = acc;
+    M16[tid] = (uint16_t)mask;
+    __syncthreads();
+    if (tid < PC / 32) S0[tid] = (uint32_t)M16[2 * tid] | ((uint32_t)M16[2 * tid + 1] << 16);
+    __syncthreads();
+    if (tid < 32) {  // popcount prefix of the 64 S0 words (two per lane)
+      const uint32_t a = __popc(S0[2 * tid]), b = __popc(S0[2 * tid + 1]);
+      uint32_t x = a + b;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (tid >= o) x += y;
+      }
+      cnt0_pos[2 * tid] = x - a - b;
+      cnt0_pos[2 * tid + 1] = x - b;
+      if (tid == 31) { cnt0_pos[PC / 32] = x; count0 = (int)x; exit0 = seg_exit[P_THREADS - 1] - PC; }
+    }
   }
   __syncthreads();
   // per entry offset: walk until merging with S0 or leaving the chunk

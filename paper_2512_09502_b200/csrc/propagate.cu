@@ -380,22 +380,16 @@ __device__ __forceinline__ void route_spike(const Routes& R, uint32_t node, int6
 // slot (t + d) % L, sm/dynamics.py:235-248; for dyadic w the sum is the same
 // whether it passes through the ring or is added here).  counts is a ring of
 // A.S steps (three batches), so emissions up to one batch back are kept.
-__device__ __forceinline__ double poisson_input(const StepArgs& A, uint32_t i, int64_t now) {
-  double acc = 0.0;
-  bool any = false;
+__device__ __forceinline__ double add_poisson_input(const StepArgs& A, uint32_t i, int64_t now, double in) {
   for (int k = 0; k < A.n_dev; ++k) {
     const FusedDev& D = A.dev[k];
     const int32_t t = D.inv[i];
     const int64_t te = now - D.delay;
     if (t < 0 || te < 0) continue;
     const uint32_t c = __ldg(D.counts + (size_t)(te % A.S) * D.n_t + t);
-    if (c) {
-      const double x = __dmul_rn(D.w, (double)c);
-      acc = any ? __dadd_rn(acc, x) : x;
-      any = true;
-    }
+    if (c) in = __dadd_rn(in, __dmul_rn(D.w, (double)c));
   }
-  return acc;
+  return in;
 }
 
 __device__ __noinline__ void spike_lists(const StepArgs& A, uint32_t i, int lane, int64_t now, int par, bool spk,
@@ -461,7 +455,7 @@ __global__ void __launch_bounds__(T256) step_kernel(const __grid_constant__ Step
       in = __dadd_rn(in, base[(size_t)p * A.n + i]);
       base[(size_t)p * A.n + i] = 0.0;
     }
-    in = __dadd_rn(in, poisson_input(A, i, now));
+    in = add_poisson_input(A, i, now, in);
     in = __dadd_rn(in, A.s.i_e[i]);
     const int32_t r = A.s.ref[i];
     if (r > 0) {
@@ -549,13 +543,66 @@ __global__ void __launch_bounds__(T256) deliver_step_kernel(const uint32_t* src_
 // spikes (node, step) to one delivery list for the block (sm/engine.py:285-296
 // repeated n_steps times, identical results).
 // ---------------------------------------------------------------------------
-constexpr int MAX_BLOCK = 16;  // inputs of up to 16 steps held in registers
+constexpr int MAX_BLOCK = 16;  // steps per LIF block (inputs staged in shared memory)
+constexpr int TB = 128;        // threads per CTA of the block kernel
 
-__global__ void __launch_bounds__(T256) lif_block_kernel(const __grid_constant__ StepArgs A, int n_steps) {
+// n_steps (<= MAX_BLOCK) consecutive steps of every real row.  No ring slot
+// read here is written during the block (every record delay >= n_steps, the
+// Poisson drive is consumed at arrival), so all inputs are loaded up front
+// with independent loads into shared memory, the slots are zeroed, and the
+// LIF recurrence runs as a short rolled loop (small code: the kernel was
+// instruction-fetch bound when fully unrolled).
+__global__ void __launch_bounds__(TB) lif_block_kernel(const __grid_constant__ StepArgs A, int n_steps) {
+  __shared__ double rin[MAX_BLOCK][TB];
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, tx = threadIdx.x;
   const int64_t t0 = *A.now_dev + A.step_offset;
   const bool live = i < A.n;
+  const uint32_t L = (uint32_t)A.L;
+  const size_t slot_stride = (size_t)A.n_ports * A.n;
+  const uint32_t sl0 = (uint32_t)(t0 % A.L);
+  if (live) {
+    // slot sl0 + s, port p; summed over ports in port order as consume does
+#pragma unroll 1
+    for (int p = 0; p < A.n_ports; ++p) {
+      double x[MAX_BLOCK];
+      uint32_t sl = sl0;
+#pragma unroll
+      for (int s = 0; s < MAX_BLOCK; ++s) {
+        x[s] = s < n_steps ? A.ring[(size_t)sl * slot_stride + (size_t)p * A.n + i] : 0.0;
+        if (++sl == L) sl = 0;
+      }
+#pragma unroll
+      for (int s = 0; s < MAX_BLOCK; ++s)
+        if (s < n_steps) rin[s][tx] = p == 0 ? x[s] : __dadd_rn(rin[s][tx], x[s]);
+    }
+    // Poisson drive emitted at t0 + s - d (same association as step_kernel)
+    for (int k = 0; k < A.n_dev; ++k) {
+      const FusedDev& D = A.dev[k];
+      const int32_t t = D.inv[i];
+      if (t < 0) continue;
+      const int64_t te0 = t0 - D.delay;
+      uint32_t ci = (uint32_t)(((te0 % A.S) + A.S) % A.S);
+      uint32_t cs[MAX_BLOCK];
+#pragma unroll
+      for (int s = 0; s < MAX_BLOCK; ++s) {  // independent loads first
+        cs[s] = (s < n_steps && te0 + s >= 0) ? __ldg(D.counts + (size_t)ci * D.n_t + t) : 0u;
+        if (++ci == (uint32_t)A.S) ci = 0;
+      }
+#pragma unroll
+      for (int s = 0; s < MAX_BLOCK; ++s)
+        if (cs[s]) rin[s][tx] = __dadd_rn(rin[s][tx], __dmul_rn(D.w, (double)cs[s]));
+    }
+#pragma unroll 1
+    for (int p = 0; p < A.n_ports; ++p) {
+      uint32_t sl = sl0;
+#pragma unroll
+      for (int s = 0; s < MAX_BLOCK; ++s) {
+        if (s < n_steps) A.ring[(size_t)sl * slot_stride + (size_t)p * A.n + i] = 0.0;
+        if (++sl == L) sl = 0;
+      }
+    }
+  }
   double v = 0.0, vr = 0.0, vreset = 0.0, vth = 0.0, decay = 0.0, ie = 0.0;
   int32_t ref = 0, refsteps = 0;
   if (live) {
@@ -563,42 +610,11 @@ __global__ void __launch_bounds__(T256) lif_block_kernel(const __grid_constant__
     vr = A.s.v_rest[i]; vreset = A.s.v_reset[i]; vth = A.s.v_th[i]; decay = A.s.decay[i]; ie = A.s.i_e[i];
     refsteps = A.s.ref_steps[i];
   }
-  const uint32_t L = (uint32_t)A.L;
-  const size_t slot_stride = (size_t)A.n_ports * A.n;
-  // every input of the block up front: no ring slot read here is written
-  // during the block (all delays >= n_steps; Poisson is consumed at arrival)
-  double rin[MAX_BLOCK];
-  uint32_t sl = (uint32_t)(t0 % A.L);
-#pragma unroll
-  for (int s = 0; s < MAX_BLOCK; ++s) {
-    rin[s] = 0.0;
-    if (s < n_steps && live) {
-      double* base = A.ring + (size_t)sl * slot_stride;
-      double in = base[i];
-      for (int p = 1; p < A.n_ports; ++p) in = __dadd_rn(in, base[(size_t)p * A.n + i]);
-      rin[s] = in;
-    }
-    if (++sl == L) sl = 0;
-  }
-  if (live) {
-#pragma unroll
-    for (int s = 0; s < MAX_BLOCK; ++s) rin[s] = s < n_steps ? __dadd_rn(rin[s], poisson_input(A, i, t0 + s)) : 0.0;
-  }
-  sl = (uint32_t)(t0 % A.L);
-#pragma unroll
-  for (int s = 0; s < MAX_BLOCK; ++s) {
-    if (s < n_steps && live) {
-      double* base = A.ring + (size_t)sl * slot_stride;
-      for (int p = 0; p < A.n_ports; ++p) base[(size_t)p * A.n + i] = 0.0;
-    }
-    if (++sl == L) sl = 0;
-  }
-#pragma unroll
-  for (int s = 0; s < MAX_BLOCK; ++s) {
-    if (s >= n_steps) continue;  // uniform guard keeps rin[] statically indexed
+#pragma unroll 1
+  for (int s = 0; s < n_steps; ++s) {
     bool spk = false;
     if (live) {
-      const double in = __dadd_rn(rin[s], ie);
+      const double in = __dadd_rn(rin[s][tx], ie);
       if (ref > 0) {
         ref -= 1;
         v = vreset;
@@ -846,7 +862,7 @@ extern "C" int smx_block(double* v, int32_t* ref, const double* decay, const dou
     smx_set_error("smx_block: at most %d steps per block", MAX_BLOCK);
     return -1;
   }
-  smx_count_launch(); lif_block_kernel<<<nblk(threads), T256, 0, st>>>(A, n_steps);
+  smx_count_launch(); lif_block_kernel<<<nblk(threads, TB), TB, 0, st>>>(A, n_steps);
   SynTable syn{cls_w, cls_delay, cls_port};
   const int grid = 148 * 8;
   if (wide_w) {

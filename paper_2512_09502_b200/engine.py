@@ -52,6 +52,38 @@ def _up(arr, dev) -> torch.Tensor:
     return torch.from_numpy(a).to(dev)
 
 
+_PREP_STREAMS: dict = {}
+
+
+def _prep_stream(dev) -> "torch.cuda.Stream":
+    """One preparation side stream per device for the whole process (its
+    caching-allocator pool is then reused by every Cluster)."""
+    key = torch.device(dev).index
+    if key not in _PREP_STREAMS:
+        _PREP_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _PREP_STREAMS[key]
+
+
+def _record_stream(obj, stream, depth: int = 0) -> None:
+    """Tell the caching allocator that the tensors reachable from obj are used
+    on `stream` (they were allocated on a preparation side stream)."""
+    if isinstance(obj, torch.Tensor):
+        obj.record_stream(stream)
+    elif depth < 3 and isinstance(obj, dict):
+        for v in obj.values():
+            _record_stream(v, stream, depth + 1)
+    elif depth < 3 and isinstance(obj, (list, tuple)):
+        for v in obj:
+            _record_stream(v, stream, depth + 1)
+
+
+def _all_distinct(a: np.ndarray) -> bool:
+    """True when a has no repeated value (O(n) for the usual ascending ids)."""
+    if len(a) < 2 or bool((a[1:] > a[:-1]).all()):
+        return True
+    return len(np.unique(a)) == len(a)
+
+
 def _words(nbits: int) -> int:
     return (int(nbits) + 31) // 32
 
@@ -967,7 +999,7 @@ class Cluster:
             if not self.distributed:
                 gids = np.concatenate([g for st in self.ranks.values() for g in st.row_gid] or
                                       [np.empty(0, np.int64)])
-                if len(np.unique(gids)) != len(gids):
+                if not _all_distinct(gids):
                     raise ConsistencyError("neuron gids must be globally unique")
             for st in self.ranks.values():
                 self._delay_stats(st)
@@ -1012,24 +1044,9 @@ class Cluster:
         n_nodes = st.n_nodes
         st.L = max(2, st.max_delay + 1)
         st.P = 1 + st.max_port
-        # neuron state, real rows only (sm/dynamics.py:153-189)
-        N = st.n_real
-        st.N = N
-        prm = np.concatenate(st.row_param) if st.row_param else np.empty(0, np.int32)
-        tab = np.array([[math.exp(-dt / p.tau_m), p.v_rest, p.v_reset, p.v_th, p.i_e] for p in self.params] or
-                       [[0.0] * 5], dtype=np.float64)
-        rs = np.array([int(round(p.t_ref / dt)) for p in self.params] or [0], dtype=np.int32)
-        f64 = lambda a: _up(np.ascontiguousarray(a), dev)  # noqa: E731
-        st.decay, st.v_rest, st.v_reset, st.v_th, st.i_e = (f64(tab[prm, j]) for j in range(5))
-        st.ref_steps = f64(rs[prm])
-        st.v = torch.cat(st.v0) if st.v0 else torch.empty(0, dtype=torch.float64, device=dev)
-        st.ref = torch.zeros(N, dtype=torch.int32, device=dev)
-        st.row2node_np = np.concatenate(st.row2node) if st.row2node else np.empty(0, np.int64)
-        st.row2node_t = _up(st.row2node_np.astype(np.int32), dev)
-        st.gid_np = np.concatenate(st.row_gid) if st.row_gid else np.empty(0, np.int64)
-        st.gid_t = _up(st.gid_np, dev)
-        st.ring = torch.zeros(st.L * st.P * max(N, 1), dtype=torch.float64, device=dev)
-        # sort the store (sm/core.py:299-324)
+        # sort the store first (sm/core.py:299-324): it is the long kernel
+        # sequence, and everything below up to the first_index check is host
+        # work or independent small kernels that overlap it on a side stream
         n = st.keys.n
         st.n_records = n
         key_bits = max(1, int(n_nodes - 1).bit_length())
@@ -1048,21 +1065,58 @@ class Cluster:
             self.prof["sort"].append((ev0, self._event(st)))
         st.first_index = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
         call("smx_counts_to_offsets", _ptr(st.counts), n_nodes, _ptr(st.first_index), sk)
-        if n and int(st.first_index[-1].item()) != n:
-            raise ConsistencyError(f"record source beyond node count {n_nodes}")
         if st.wide:
             st.payload = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
             st.ww = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
             st.wm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
             call("smx_gather_wide", _ptr(sorted_vals), n, _ptr(st.w_rows.t), _ptr(st.w_w.t), _ptr(st.w_meta.t),
                  _ptr(st.payload), _ptr(st.ww), _ptr(st.wm), sk)
-            st.w_rows = st.w_w = st.w_meta = None
         else:
             st.payload = sorted_vals if n else torch.empty(1, dtype=torch.int32, device=dev)
             st.ww = st.wm = None
+        main = torch.cuda.current_stream(dev)
+        side = _prep_stream(dev)
+        side.wait_stream(main)  # maps / mirrors / rosters were written on main
+        with torch.cuda.stream(side):
+            self._prepare_tables(st)
+        main.wait_stream(side)
+        _record_stream(st.__dict__, main)  # side-stream allocations are used on main
+        if n and int(st.first_index[-1].item()) != n:
+            raise ConsistencyError(f"record source beyond node count {n_nodes}")
+        # record lists are dropped only after the sort has consumed them
         del kb, vb, sorted_vals
         st.keys = st.vals = None
+        st.w_rows = st.w_w = st.w_meta = None
         st.lut = None
+        fi = st.first_index
+        max_len = int((fi[1:] - fi[:-1]).max().item()) if st.n_nodes else 0
+        max_chunks = max(1, -(-max_len // 1024))
+        st.owner_cap = st.N * self.block * max_chunks + 16
+        st.owner = torch.zeros(st.owner_cap, dtype=torch.int32, device=dev)
+        st.prepared = True
+
+    def _prepare_tables(self, st: _Rank):
+        """Everything of prepare that does not read the sorted store: neuron
+        state, class tables, (R, L), S, H, I, T/P, G/Q, propagation buffers."""
+        dev = st.device
+        dt = self.cfg.resolution_ms
+        # neuron state, real rows only (sm/dynamics.py:153-189)
+        N = st.n_real
+        st.N = N
+        prm = np.concatenate(st.row_param) if st.row_param else np.empty(0, np.int32)
+        tab = np.array([[math.exp(-dt / p.tau_m), p.v_rest, p.v_reset, p.v_th, p.i_e] for p in self.params] or
+                       [[0.0] * 5], dtype=np.float64)
+        rs = np.array([int(round(p.t_ref / dt)) for p in self.params] or [0], dtype=np.int32)
+        f64 = lambda a: _up(np.ascontiguousarray(a), dev)  # noqa: E731
+        st.decay, st.v_rest, st.v_reset, st.v_th, st.i_e = (f64(tab[prm, j]) for j in range(5))
+        st.ref_steps = f64(rs[prm])
+        st.v = torch.cat(st.v0) if st.v0 else torch.empty(0, dtype=torch.float64, device=dev)
+        st.ref = torch.zeros(N, dtype=torch.int32, device=dev)
+        st.row2node_np = np.concatenate(st.row2node) if st.row2node else np.empty(0, np.int64)
+        st.row2node_t = _up(st.row2node_np.astype(np.int32), dev)
+        st.gid_np = np.concatenate(st.row_gid) if st.row_gid else np.empty(0, np.int64)
+        st.gid_t = _up(st.gid_np, dev)
+        st.ring = torch.zeros(st.L * st.P * max(N, 1), dtype=torch.float64, device=dev)
         st.cls_w, cm = self._class_tables(dev)
         cmn = cm.cpu().numpy().view(np.uint32)
         st.cls_delay = _up((cmn & ROW_MASK).astype(np.int32), dev)
@@ -1100,7 +1154,6 @@ class Cluster:
         st.GQ = self._routes(st, own)
         # propagation buffers
         self._alloc_propagation(st)
-        st.prepared = True
 
     def _compact(self, st, bits, img_of):
         nw = bits.numel()
@@ -1199,16 +1252,11 @@ class Cluster:
             d["batch0"] = -1
         # fused step path: every active device hits each row at most once
         act = [d for d in st.devices if d["active"]]
-        st.fused = len(act) <= 8 and all(len(np.unique(d["rows"].cpu().numpy())) == d["nt"] for d in act)
+        st.fused = len(act) <= 8 and all(_all_distinct(d["rows"].cpu().numpy()) for d in act)
         st.ctr = torch.zeros(2, dtype=torch.int64, device=dev)
-        fi = st.first_index
-        max_len = int((fi[1:] - fi[:-1]).max().item()) if st.n_nodes else 0
-        max_chunks = max(1, -(-max_len // 1024))
-        st.owner_cap = N * B * max_chunks + 16
         # multi-step LIF blocks: every record delay >= block length (Poisson
         # devices are applied by their target row's own thread)
         st.block_ok = st.min_delay is None or st.min_delay >= B
-        st.owner = torch.zeros(st.owner_cap, dtype=torch.int32, device=dev)
         st.fdev = (ctypes_fdev * max(len(act), 1))()
         for k, d in enumerate(act):
             inv = np.full(max(N, 1), -1, dtype=np.int32)

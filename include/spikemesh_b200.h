@@ -124,8 +124,6 @@ int smx_promote_wide(const uint32_t* vals, uint64_t n, const double* cls_w, cons
 int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, uint64_t n,
                      int key_bits, int index_values, const uint32_t* lut, uint32_t* counts, uint64_t n_keys,
                      int* out_in_b_host, void* stream);
-/* tuning aid: per-phase cycle counters of the sort downsweep (6 u64, or null) */
-void smx_sort_timing(unsigned long long* counters);
 /* first_index = exclusive scan of per-source counts (np.add.at + np.cumsum) */
 int smx_counts_to_offsets(const uint32_t* counts, uint64_t n, int64_t* first_index, void* stream);
 int smx_gather_wide(const uint32_t* idx, uint64_t n, const uint32_t* rows_in, const double* w_in,

@@ -33,7 +33,6 @@ SIGNATURES = {
     "smx_init_v": (I32, [P, U32, P, U32, P, U64, D, D, P, P]),
     "smx_stream_keys": (I32, [P, U32, P, U32, P, U64, P, P]),
     "smx_counts_to_offsets": (I32, [P, U64, P, P]),
-    "smx_sort_timing": (None, [P]),
     "smx_sort_records": (I32, [P, P, P, P, U64, I32, I32, P, P, U64, P, P]),
     "smx_pay_table": (I32, [P, U64, P, U64, U32, P, P]),
     "smx_key_table": (I32, [P, U64, U32, I32, P, P]),

@@ -23,11 +23,15 @@
 
 namespace {
 
-constexpr int RS_THREADS = 256;
-constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_IPT = 16;                       // items per thread per tile
-constexpr int RS_TILE = RS_THREADS * RS_IPT;     // 4096
+constexpr int DS_THREADS = 256;
+constexpr int DS_WARPS = DS_THREADS / 32;
+constexpr int DS_IPT = 15;                        // items per thread per tile
+constexpr int DS_TILE = DS_THREADS * DS_IPT;      // 3840 records (15 KB of keys)
 constexpr int RS_MAX_BITS = 11;
+constexpr int US_THREADS = 1024;
+constexpr int CNT_BINS = 12288;                   // last-pass key-count bins in SMEM (48 KB)
+
+__host__ __device__ constexpr int ds_ctas_per_sm(int bits) { return bits <= 9 ? 3 : 2; }
 
 struct SortPass {
   const uint32_t* keys_in;
@@ -35,263 +39,418 @@ struct SortPass {
   uint32_t* keys_out;       // null on the last pass
   uint32_t* vals_out;
   uint64_t n;
-  uint64_t seg;             // records per CTA (multiple of RS_TILE)
+  uint64_t seg;             // records per CTA (multiple of DS_TILE)
   int shift;
   int first;
   int last;
   const uint32_t* lut;      // temporary-key LUT (first pass)
-  uint32_t* counts;         // per-key counts (last pass)
+  uint32_t* counts;         // per-key counts (filled by the last pass's upsweep)
+  uint64_t n_keys;
   const uint32_t* hist_scan;  // [BINS * G] exclusive offsets
-  unsigned long long* timing; // optional per-phase cycle counters (tuning)
 };
 
 __device__ __forceinline__ uint32_t resolve(uint32_t k, const uint32_t* lut) {
   return (k & SMX_TMP_KEY) ? lut[k & ~SMX_TMP_KEY] : k;
 }
 
+__device__ __forceinline__ void count_key(const SortPass& p, uint32_t key, uint32_t c) {
+  if (key < p.n_keys) atomicAdd(&p.counts[key], c);  // out-of-range keys show up in the total check
+}
+
+// Per-tile digit histograms tcnt[tile][BINS] (u16), one warp per tile with a
+// warp-private SMEM histogram; a CTA covers a contiguous run of tiles.  The
+// last pass also produces the per-key record counts (-> first_index): its
+// input is sorted by the lower key bits (all earlier passes), so the CTA's
+// run covers a short range [lo_v, hi_v] of lower values and (lower - lo_v,
+// digit) indexes a small SMEM table -- one shared atomic per record, flushed
+// with one global atomic per non-empty bin.  Degenerate ranges fall back to
+// one global atomic per record.
+constexpr int TH_WARPS = US_THREADS / 32;
+// warps that histogram tiles (their u32 histograms fit in 160 KB of SMEM)
+__host__ __device__ constexpr int th_hist_warps(int bits) {
+  return (160 * 1024) / (4 << bits) < TH_WARPS ? (160 * 1024) / (4 << bits) : TH_WARPS;
+}
+
 template <int BITS>
-__global__ void __launch_bounds__(RS_THREADS) upsweep_kernel(SortPass p, uint32_t* hist) {
+__global__ void __launch_bounds__(US_THREADS) tile_hist_kernel(SortPass p, uint16_t* tcnt, uint32_t n_tiles,
+                                                               uint32_t tiles_per_cta) {
   constexpr int BINS = 1 << BITS;
-  __shared__ uint32_t h[BINS];
-  for (int i = threadIdx.x; i < BINS; i += RS_THREADS) h[i] = 0;
-  __syncthreads();
-  const uint64_t lo = (uint64_t)blockIdx.x * p.seg;
-  const uint64_t hi = lo + p.seg < p.n ? lo + p.seg : p.n;
+  constexpr int HW = th_hist_warps(BITS);
+  extern __shared__ uint32_t th[];  // [HW][BINS] warp histograms, then count bins
+  uint32_t* cnt = th + HW * BINS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t tile0 = blockIdx.x * tiles_per_cta;
+  const uint32_t tile1 = min(n_tiles, tile0 + tiles_per_cta);
+  const uint64_t lo = (uint64_t)tile0 * DS_TILE;
+  const uint64_t hi = min(p.n, (uint64_t)tile1 * DS_TILE);
   const uint32_t mask = BINS - 1;
-  // 4-wide vector loads (segments are multiples of 4096 records)
-  const uint4* k4 = reinterpret_cast<const uint4*>(p.keys_in);
-  for (uint64_t i = lo / 4 + threadIdx.x; i < (hi + 3) / 4; i += RS_THREADS) {
-    const uint4 q = k4[i];
-    const uint32_t kk[4] = {q.x, q.y, q.z, q.w};
+  const uint32_t lm = (1u << p.shift) - 1;
+  int mode = 0;  // 0 digits only, 1 key bins in SMEM, 2 key counts by global atomics
+  uint32_t lo_v = 0, span = 1;
+  if (p.last && p.counts && lo < hi) {
+    if (p.shift == 0) {
+      mode = 1;
+    } else {
+      lo_v = p.keys_in[lo] & lm;
+      const uint32_t hi_v = p.keys_in[hi - 1] & lm;
+      span = hi_v - lo_v + 1;
+      mode = (hi_v >= lo_v && (uint64_t)span * BINS <= CNT_BINS) ? 1 : 2;
+    }
+    const uint32_t nb = mode == 1 ? span * BINS : 0;
+    for (uint32_t i = threadIdx.x; i < nb; i += US_THREADS) cnt[i] = 0;
+  }
+  __syncthreads();
+  uint32_t* wh = th + warp * BINS;
+  for (uint32_t t = tile0 + warp; warp < HW && t < tile1; t += HW) {
+    for (int j = lane; j < BINS; j += 32) wh[j] = 0;
+    __syncwarp();
+    const uint64_t a = (uint64_t)t * DS_TILE, b = min(p.n, a + DS_TILE);
+    const uint4* k4 = reinterpret_cast<const uint4*>(p.keys_in + a);
+    const uint32_t nq = (uint32_t)((b - a) / 4);
+    for (uint32_t i = lane; i < nq + 1; i += 32) {
+      uint32_t kk[4];
+      int m = 4;
+      if (i < nq) {
+        const uint4 q = k4[i];
+        kk[0] = q.x; kk[1] = q.y; kk[2] = q.z; kk[3] = q.w;
+      } else {  // ragged tail of the last tile
+        m = (int)((b - a) - 4 * (uint64_t)nq);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (i * 4 + j >= hi) break;
-      uint32_t k = kk[j];
-      if (p.first) k = resolve(k, p.lut);
-      atomicAdd(&h[(k >> p.shift) & mask], 1u);
+        for (int j = 0; j < 4; ++j) kk[j] = j < m ? p.keys_in[a + 4 * nq + j] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= m) break;
+        uint32_t k = kk[j];
+        if (p.first) k = resolve(k, p.lut);
+        const uint32_t d = (k >> p.shift) & mask;
+        atomicAdd(&wh[d], 1u);
+        if (mode == 1) atomicAdd(&cnt[((k & lm) - lo_v) * BINS + d], 1u);
+        else if (mode == 2) count_key(p, k, 1u);
+      }
+    }
+    __syncwarp();
+    uint32_t* out = reinterpret_cast<uint32_t*>(tcnt + (size_t)t * BINS);
+    for (int j = lane; j < BINS / 2; j += 32) out[j] = wh[2 * j] | (wh[2 * j + 1] << 16);
+    __syncwarp();
+  }
+  if (mode == 1) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < span * BINS; i += US_THREADS) {
+      const uint32_t c = cnt[i];
+      if (c) count_key(p, (lo_v + i / BINS) | ((i % BINS) << p.shift), c);
     }
   }
-  __syncthreads();
-  for (int d = threadIdx.x; d < BINS; d += RS_THREADS) hist[(uint64_t)d * gridDim.x + blockIdx.x] = h[d];
 }
 
-// Single-CTA exclusive scan of n u32 (n = BINS * G, totals fit in u32).
-__global__ void scan_small_kernel(const uint32_t* in, uint32_t* out, int n) {
-  __shared__ uint32_t ws[32];
-  __shared__ uint32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    const uint32_t x = i < n ? in[i] : 0;
-    uint32_t tot;
-    const uint32_t ex = smx::block_excl_scan(x, ws, tot);
-    if (i < n) out[i] = carry + ex;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
+// Column sums of tcnt over chunks of TC tiles: csum[chunk][d].
+constexpr int TC = 256;
+template <int BITS>
+__global__ void __launch_bounds__(256) chunk_sum_kernel(const uint16_t* tcnt, uint32_t n_tiles, uint32_t* csum) {
+  constexpr int BINS = 1 << BITS;
+  const uint32_t c = blockIdx.x;
+  const uint32_t t0 = c * TC, t1 = min(n_tiles, t0 + TC);
+  for (int d = threadIdx.x; d < BINS; d += 256) {
+    uint32_t s = 0;
+#pragma unroll 8
+    for (uint32_t t = t0; t < t1; ++t) s += tcnt[(size_t)t * BINS + d];
+    csum[(size_t)c * BINS + d] = s;
   }
 }
 
-// Stable scatter of one segment per CTA by the digit (key >> shift) & (2^BITS-1).
-// Input tiles are double-buffered in shared memory by TMA 1-D bulk copies
-// (cp.async.bulk + mbarrier): tile i+1 streams in while tile i is ranked and
-// scattered, so the warps never wait on DRAM for their inputs.
+// Single CTA: per digit, exclusive scan over chunks, offset by the digit's
+// global base (exclusive scan of the digit totals).  In place on csum.
 template <int BITS>
-__global__ void __launch_bounds__(RS_THREADS, 2) downsweep_kernel(SortPass p) {
+__global__ void __launch_bounds__(1024) chunk_scan_kernel(uint32_t* csum, uint32_t n_chunks) {
   constexpr int BINS = 1 << BITS;
-  constexpr int DPT = BINS >= RS_THREADS ? BINS / RS_THREADS : 1;  // digits per thread
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint32_t* inbuf = reinterpret_cast<uint32_t*>(smem);                      // [2][2][RS_TILE] keys, vals
-  uint32_t* skey = inbuf + 4 * RS_TILE;                                     // [RS_TILE]
-  uint32_t* sval = skey + RS_TILE;                                          // [RS_TILE]
-  uint16_t* wcnt = reinterpret_cast<uint16_t*>(sval + RS_TILE);             // [RS_WARPS][BINS]
-  uint32_t* run_base = reinterpret_cast<uint32_t*>(wcnt + RS_WARPS * BINS);  // [BINS]
-  uint32_t* tstart = run_base + BINS;                                       // [BINS + 1]
+  constexpr int DPT = (BINS + 1023) / 1024;
   __shared__ uint32_t ws[32];
-  __shared__ __align__(8) uint64_t bar[2];
+  uint32_t tot[DPT];
+  uint32_t mysum = 0;
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int d = threadIdx.x * DPT + j;
+    uint32_t s = 0;
+    if (d < BINS) {
+#pragma unroll 8
+      for (uint32_t c = 0; c < n_chunks; ++c) s += csum[(size_t)c * BINS + d];
+    }
+    tot[j] = s;
+    mysum += s;
+  }
+  uint32_t total;
+  uint32_t base = smx::block_excl_scan(mysum, ws, total);
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int d = threadIdx.x * DPT + j;
+    if (d < BINS) {
+      uint32_t run = base;
+      for (uint32_t c = 0; c < n_chunks; ++c) {
+        const uint32_t x = csum[(size_t)c * BINS + d];
+        csum[(size_t)c * BINS + d] = run;
+        run += x;
+      }
+    }
+    base += tot[j];
+  }
+}
+
+// off[tile][d] = global output position of the tile's first record of digit d.
+template <int BITS>
+__global__ void __launch_bounds__(256) tile_offsets_kernel(const uint16_t* tcnt, const uint32_t* cbase,
+                                                           uint32_t n_tiles, uint32_t* off) {
+  constexpr int BINS = 1 << BITS;
+  const uint32_t c = blockIdx.x;
+  const uint32_t t0 = c * TC, t1 = min(n_tiles, t0 + TC);
+  for (int d = threadIdx.x; d < BINS; d += 256) {
+    uint32_t run = cbase[(size_t)c * BINS + d];
+    for (uint32_t t = t0; t < t1; ++t) {
+      off[(size_t)t * BINS + d] = run;
+      run += tcnt[(size_t)t * BINS + d];
+    }
+  }
+}
+
+// Stable scatter by the digit (key >> shift) & (2^BITS-1).  CTAs take tiles
+// in global order from an atomic ticket (one tile ahead, for the TMA
+// prefetch): the tiles in flight are neighbours, so every digit's output
+// grows at one frontier and a sector split between two tiles is completed
+// while it is still in L2.  (Contiguous per-CTA segments left G frontiers per
+// digit, and even a static interleave drifts by many tiles; both paid a DRAM
+// read-modify-write per partial sector -- 2x the traffic of the pass.)  The
+// tile's global digit offsets are precomputed (tile_hist -> chunk scans), so
+// no tile waits on another.
+// Per 3840-record tile:
+//   load    the tile arrived in SMEM by TMA (cp.async.bulk + mbarrier) with
+//           its offset row; each thread takes its 15 keys/values into
+//           registers, so the buffer is free again and the next tile's TMA is
+//           issued right after barrier 1
+//   rank    warp-private u16 digit counters + ballot multisplit (stable)
+//   scan    tile offsets; delta[d] = off[tile][d] - tile offset of d
+//   stage   records to SMEM in digit order
+//   write   coalesced runs: g = delta[d] + q
+template <int BITS>
+__global__ void __launch_bounds__(DS_THREADS, ds_ctas_per_sm(BITS)) downsweep_kernel(SortPass p, const uint32_t* off,
+                                                                                    uint32_t n_tiles,
+                                                                                    uint32_t* tile_ctr) {
+  constexpr int BINS = 1 << BITS;
+  constexpr int DPT = BINS / DS_THREADS;  // digits per thread (BITS >= 8)
+  static_assert(DPT >= 1, "at least 8-bit digits");
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint32_t* ikey = reinterpret_cast<uint32_t*>(smem);  // [DS_TILE] TMA target
+  uint32_t* ival = ikey + DS_TILE;                      // [DS_TILE] TMA target
+  uint32_t* ioff = ival + DS_TILE;                      // [2][BINS] TMA target (offset rows)
+  uint32_t* skey = ioff + 2 * BINS;                     // [DS_TILE] staging
+  uint32_t* sval = skey + DS_TILE;                      // [DS_TILE] staging
+  uint32_t* delta = sval + DS_TILE;                     // [BINS]
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(delta + BINS);  // [DS_WARPS][BINS]
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t ticket[2];
+  __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1;
   const uint32_t mask = BINS - 1;
-  for (int d = tid; d < BINS; d += RS_THREADS) run_base[d] = p.hist_scan[(uint64_t)d * gridDim.x + blockIdx.x];
-  const uint64_t lo = (uint64_t)blockIdx.x * p.seg;
-  const uint64_t hi = lo + p.seg < p.n ? lo + p.seg : p.n;
   const bool has_vals = p.vals_in != nullptr;
   if (tid == 0) {
-    smx::mbar_init(&bar[0], 1);
-    smx::mbar_init(&bar[1], 1);
+    smx::mbar_init(&bar, 1);
     smx::fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](uint64_t t0, int b) {  // thread 0: full tiles only
-    const uint32_t bytes = RS_TILE * 4;
-    smx::mbar_expect_tx(&bar[b], has_vals ? 2 * bytes : bytes);
-    smx::bulk_g2s(inbuf + (2 * b) * RS_TILE, p.keys_in + t0, bytes, &bar[b]);
-    if (has_vals) smx::bulk_g2s(inbuf + (2 * b + 1) * RS_TILE, p.vals_in + t0, bytes, &bar[b]);
-  };
-  uint32_t phase[2] = {0, 0};
-  if (tid == 0 && lo + RS_TILE <= hi) issue(lo, 0);
-  long long tm = clock64();
-#define TMARK(i)                                                     \
-  if (p.timing && tid == 0) {                                        \
-    const long long t_ = clock64();                                  \
-    atomicAdd(p.timing + (i), (unsigned long long)(t_ - tm));        \
-    tm = t_;                                                         \
-  }
-  int b = 0;
-  for (uint64_t t0 = lo; t0 < hi; t0 += RS_TILE, b ^= 1) {
-    const bool full = t0 + RS_TILE <= hi;
-    uint32_t* kin = inbuf + (2 * b) * RS_TILE;
-    uint32_t* vin = kin + RS_TILE;
-    // prefetch the next tile into the other buffer (consumed two iterations ago)
-    if (tid == 0 && t0 + 2 * RS_TILE <= hi) {
-      smx::fence_proxy_async();
-      issue(t0 + RS_TILE, b ^ 1);
-    }
-    TMARK(5);
+  // thread 0: TMA of tile t (keys, values if any, offset row into slot b)
+  auto issue = [&](uint32_t t, int b) {
+    const uint64_t t0 = (uint64_t)t * DS_TILE;
+    const bool full = t0 + DS_TILE <= p.n;
+    const uint32_t bytes = DS_TILE * 4;
+    smx::mbar_expect_tx(&bar, BINS * 4 + (full ? (has_vals ? 2 * bytes : bytes) : 0));
+    smx::bulk_g2s(ioff + b * BINS, off + (size_t)t * BINS, BINS * 4, &bar);
     if (full) {
-      smx::mbar_wait(&bar[b], phase[b]);
-      phase[b] ^= 1;
-    } else {  // partial last tile: plain loads
-      for (uint32_t q = tid; q < RS_TILE; q += RS_THREADS) {
-        const uint64_t idx = t0 + q;
-        kin[q] = idx < hi ? p.keys_in[idx] : 0u;
-        if (has_vals) vin[q] = idx < hi ? p.vals_in[idx] : 0u;
+      smx::bulk_g2s(ikey, p.keys_in + t0, bytes, &bar);
+      if (has_vals) smx::bulk_g2s(ival, p.vals_in + t0, bytes, &bar);
+    }
+  };
+  uint32_t phase = 0;
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(tile_ctr, 1u);
+    ticket[0] = t;
+    if (t < n_tiles) issue(t, 0);
+  }
+  __syncthreads();
+  const uint32_t wofs = warp * (32 * DS_IPT) + lane;
+  uint16_t* mycnt = wcnt + warp * BINS;
+  int slot = 0;
+  for (uint32_t tile = ticket[0]; tile < n_tiles; tile = ticket[slot ^= 1]) {
+    const uint64_t t0 = (uint64_t)tile * DS_TILE;
+    const bool full = t0 + DS_TILE <= p.n;
+    uint32_t k[DS_IPT], v[DS_IPT];
+    smx::mbar_wait(&bar, phase);
+    phase ^= 1;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < DS_IPT; ++i) {
+        const uint32_t q = wofs + i * 32;
+        k[i] = ikey[q];
+        v[i] = has_vals ? ival[q] : (uint32_t)(t0 + q);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < DS_IPT; ++i) {
+        const uint64_t idx = t0 + wofs + i * 32;
+        const bool ok = idx < p.n;
+        k[i] = ok ? p.keys_in[idx] : 0u;
+        v[i] = ok ? (has_vals ? p.vals_in[idx] : (uint32_t)idx) : 0u;
       }
     }
-    for (int d = tid; d < RS_WARPS * BINS / 2; d += RS_THREADS) reinterpret_cast<uint32_t*>(wcnt)[d] = 0;
-    __syncthreads();
-    TMARK(0);
-    uint32_t rank2[RS_IPT / 2];  // two 16-bit ranks per register; 0xffff = invalid
-    const uint32_t wofs = warp * (32 * RS_IPT) + lane;
+    if (p.first) {
 #pragma unroll
-    for (int i = 0; i < RS_IPT; ++i) {
-      const uint32_t q = wofs + i * 32;
-      const bool valid = t0 + q < hi;
-      uint32_t k = kin[q];
-      if (p.first) {
-        k = resolve(k, p.lut);
-        kin[q] = k;  // later phases reread the resolved key
-      }
-      const uint32_t d = (k >> p.shift) & mask;
-      // warp-level multisplit: lanes with the same digit, one ballot per bit
-      // (cheaper than MATCH.ANY on sm_100)
-      uint32_t peers = __ballot_sync(0xffffffffu, valid);
+      for (int i = 0; i < DS_IPT; ++i) k[i] = resolve(k[i], p.lut);
+    }
+    {
+      uint32_t* w32 = reinterpret_cast<uint32_t*>(mycnt);
+#pragma unroll
+      for (int j = lane; j < BINS / 2; j += 32) w32[j] = 0;
+      __syncwarp();
+    }
+    uint32_t rank2[(DS_IPT + 1) / 2];
+#pragma unroll
+    for (int i = 0; i < DS_IPT; ++i) {
+      const bool valid = full || t0 + wofs + i * 32 < p.n;
+      const uint32_t d = (k[i] >> p.shift) & mask;
+      // warp multisplit: lanes holding the same digit, one ballot per bit
+      uint32_t peers = full ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
 #pragma unroll
       for (int b = 0; b < BITS; ++b) {
-        const bool bit = (d >> b) & 1u;
+        const uint32_t bit = (d >> b) & 1u;
         const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-        peers &= bit ? bal : ~bal;
+        peers &= ~(bal ^ (0u - bit));
       }
       if (!valid) peers = 1u << lane;
       const int leader = __ffs(peers) - 1;
       uint32_t old = 0;
       if (valid && lane == leader) {
-        old = wcnt[warp * BINS + d];
-        wcnt[warp * BINS + d] = (uint16_t)(old + __popc(peers));
+        old = mycnt[d];
+        mycnt[d] = (uint16_t)(old + __popc(peers));
       }
       old = __shfl_sync(0xffffffffu, old, leader);
       const uint32_t r = valid ? old + __popc(peers & lt_mask) : 0xffffu;
       if (i & 1) rank2[i >> 1] |= r << 16; else rank2[i >> 1] = r;
     }
-    __syncthreads();
-    TMARK(1);
-    // digits [tid*DPT, tid*DPT+DPT): warp prefixes in place, tile totals, block scan
-    uint32_t tot_d[DPT];
+    __syncthreads();  // 1: counters complete, TMA buffers of this tile consumed
+    if (tid == 0) {  // next ticket: tiles are taken in global order
+      const uint32_t t = atomicAdd(tile_ctr, 1u);
+      ticket[slot ^ 1] = t;
+      if (t < n_tiles) {
+        smx::fence_proxy_async();
+        issue(t, slot ^ 1);
+      }
+    }
+    uint32_t tot[DPT];
     uint32_t mysum = 0;
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
       const int d = tid * DPT + j;
       uint32_t t = 0;
-      if (d < BINS) {
 #pragma unroll
-        for (int w = 0; w < RS_WARPS; ++w) {
-          const uint32_t c = wcnt[w * BINS + d];
-          wcnt[w * BINS + d] = (uint16_t)t;
-          t += c;
-        }
-      }
-      tot_d[j] = t;
+      for (int w = 0; w < DS_WARPS; ++w) t += wcnt[w * BINS + d];
+      tot[j] = t;
       mysum += t;
     }
     uint32_t tsum;
     uint32_t run = smx::block_excl_scan(mysum, ws, tsum);
+    const uint32_t* orow = ioff + slot * BINS;
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
       const int d = tid * DPT + j;
-      if (d < BINS) tstart[d] = run;
-      run += tot_d[j];
-    }
-    if (tid == 0) tstart[BINS] = tsum;
-    __syncthreads();
-    TMARK(2);
+      uint32_t t = run;
 #pragma unroll
-    for (int i = 0; i < RS_IPT; ++i) {
+      for (int w = 0; w < DS_WARPS; ++w) {
+        const uint32_t c = wcnt[w * BINS + d];
+        wcnt[w * BINS + d] = (uint16_t)t;
+        t += c;
+      }
+      delta[d] = orow[d] - run;
+      run += tot[j];
+    }
+    __syncthreads();  // 2: offsets ready
+#pragma unroll
+    for (int i = 0; i < DS_IPT; ++i) {
       const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
       if (r != 0xffffu) {
-        const uint32_t q = wofs + i * 32;
-        const uint32_t k = kin[q];
-        const uint32_t d = (k >> p.shift) & mask;
-        const uint32_t pos = tstart[d] + wcnt[warp * BINS + d] + r;
-        skey[pos] = k;
-        sval[pos] = has_vals ? vin[q] : (uint32_t)(t0 + q);
+        const uint32_t d = (k[i] >> p.shift) & mask;
+        const uint32_t pos = mycnt[d] + r;
+        skey[pos] = k[i];
+        sval[pos] = v[i];
       }
     }
-    __syncthreads();
-    TMARK(3);
-    for (uint32_t q0 = 0; q0 < tsum; q0 += RS_THREADS) {
-      const uint32_t q = q0 + tid;
-      const bool ok = q < tsum;
-      const uint32_t k = ok ? skey[q] : 0xffffffffu;
-      if (ok) {
-        const uint32_t d = (k >> p.shift) & mask;
-        const uint64_t g = (uint64_t)run_base[d] + (q - tstart[d]);
-        p.vals_out[g] = sval[q];
-        if (!p.last) p.keys_out[g] = k;
-      }
-      if (p.last) {
-        // per-source counts: equal keys are adjacent in the staging buffer,
-        // so one warp-aggregated atomic per distinct key per warp
-        const uint32_t peers = __match_any_sync(0xffffffffu, k);
-        if (ok && lane == __ffs(peers) - 1) atomicAdd(&p.counts[k], (uint32_t)__popc(peers));
-      }
+    __syncthreads();  // 3: tile staged in digit order
+    for (uint32_t q = tid; q < tsum; q += DS_THREADS) {
+      const uint32_t kk = skey[q];
+      const uint32_t g = delta[(kk >> p.shift) & mask] + q;
+      p.vals_out[g] = sval[q];
+      if (!p.last) p.keys_out[g] = kk;
     }
-    __syncthreads();
-    TMARK(4);
-    for (int d = tid; d < BINS; d += RS_THREADS) run_base[d] += tstart[d + 1] - tstart[d];
-    __syncthreads();
   }
 }
 
 template <int BITS>
 size_t downsweep_smem() {
-  return (size_t)6 * RS_TILE * 4 + (size_t)RS_WARPS * (1 << BITS) * 2 + (size_t)(2 * (1 << BITS) + 1) * 4;
+  return (size_t)4 * DS_TILE * 4 + (size_t)3 * (1 << BITS) * 4 + (size_t)DS_WARPS * (1 << BITS) * 2;
 }
 
 template <int BITS>
-int run_pass(const SortPass& p, int G, uint32_t* hist, uint32_t* hscan, cudaStream_t st) {
+int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, uint64_t n, int passes,
+             int index_values, const uint32_t* lut, uint32_t* counts, uint64_t n_keys, int* out_in_b,
+             cudaStream_t st) {
+  constexpr int BINS = 1 << BITS;
   const size_t smem = downsweep_smem<BITS>();
+  const size_t th_smem = (size_t)4 * (th_hist_warps(BITS) * BINS + CNT_BINS);
   static bool configured = false;
   if (!configured) {
     SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(tile_hist_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)th_smem));
     configured = true;
   }
-  smx_count_launch(); upsweep_kernel<BITS><<<G, RS_THREADS, 0, st>>>(p, hist);
-  smx_count_launch(); scan_small_kernel<<<1, 1024, 0, st>>>(hist, hscan, (1 << BITS) * G);
-  smx_count_launch(); downsweep_kernel<BITS><<<G, RS_THREADS, smem, st>>>(p);
-  SMX_LAUNCH_CHECK();
-  return 0;
-}
-
-int run_pass_bits(int bits, const SortPass& p, int G, uint32_t* hist, uint32_t* hscan, cudaStream_t st) {
-  switch (bits) {
-    case 1: case 2: case 3: case 4: case 5: case 6: case 7:
-    case 8: return run_pass<8>(p, G, hist, hscan, st);
-    case 9: return run_pass<9>(p, G, hist, hscan, st);
-    case 10: return run_pass<10>(p, G, hist, hscan, st);
-    default: return run_pass<11>(p, G, hist, hscan, st);
+  const uint32_t n_tiles = (uint32_t)((n + DS_TILE - 1) / DS_TILE);
+  const uint32_t n_chunks = (n_tiles + TC - 1) / TC;
+  uint16_t* tcnt = nullptr;
+  uint32_t *off = nullptr, *csum = nullptr, *ctr = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&ctr, sizeof(uint32_t) * passes, st));
+  SMX_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * passes, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&tcnt, sizeof(uint16_t) * n_tiles * BINS, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&off, sizeof(uint32_t) * n_tiles * BINS, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&csum, sizeof(uint32_t) * n_chunks * BINS, st));
+  const uint32_t hg = std::min<uint32_t>(n_tiles, 148 * 2);
+  const uint32_t tpc = (n_tiles + hg - 1) / hg;
+  const uint32_t hgrid = (n_tiles + tpc - 1) / tpc;
+  const uint32_t grid = std::min<uint32_t>(n_tiles, 148u * ds_ctas_per_sm(BITS));
+  for (int pass = 0; pass < passes; ++pass) {
+    const bool from_a = (pass & 1) == 0;
+    SortPass p{};
+    p.keys_in = from_a ? keys_a : keys_b;
+    p.vals_in = (pass == 0 && index_values) ? nullptr : (from_a ? vals_a : vals_b);
+    p.first = pass == 0;
+    p.last = pass == passes - 1;
+    p.shift = BITS * pass;
+    p.n = n;
+    p.lut = lut;
+    p.counts = counts;
+    p.n_keys = n_keys;
+    p.keys_out = p.last ? nullptr : (from_a ? keys_b : keys_a);
+    p.vals_out = from_a ? vals_b : vals_a;
+    smx_count_launch(); tile_hist_kernel<BITS><<<hgrid, US_THREADS, th_smem, st>>>(p, tcnt, n_tiles, tpc);
+    smx_count_launch(); chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, n_tiles, csum);
+    smx_count_launch(); chunk_scan_kernel<BITS><<<1, 1024, 0, st>>>(csum, n_chunks);
+    smx_count_launch(); tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, csum, n_tiles, off);
+    smx_count_launch(); downsweep_kernel<BITS><<<grid, DS_THREADS, smem, st>>>(p, off, n_tiles, ctr + pass);
+    SMX_LAUNCH_CHECK();
+    *out_in_b = from_a ? 1 : 0;
   }
+  cudaFreeAsync(tcnt, st);
+  cudaFreeAsync(off, st);
+  cudaFreeAsync(csum, st);
+  cudaFreeAsync(ctr, st);
+  return 0;
 }
 
 // --- large exclusive scan: counts (u32, n) -> offsets (i64, n+1) -------------
@@ -347,11 +506,6 @@ __global__ void scan_apply_kernel(const uint32_t* in, uint64_t n, const uint64_t
 
 }  // namespace
 
-static unsigned long long* g_sort_timing = nullptr;
-// Tuning aid: per-phase cycle counters of the downsweep (thread 0 of every
-// CTA; phases: zero, rank, scan, stage, write, wait).  Pass null to disable.
-extern "C" void smx_sort_timing(unsigned long long* counters) { g_sort_timing = counters; }
-
 // first_index[0..n] = exclusive scan of counts[0..n-1]; first_index[n] = total.
 extern "C" int smx_counts_to_offsets(const uint32_t* counts, uint64_t n, int64_t* first_index, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -386,37 +540,12 @@ extern "C" int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
   }
   if (key_bits < 1) key_bits = 1;
   static const int max_bits = getenv("SMX_SORT_MAX_BITS") ? atoi(getenv("SMX_SORT_MAX_BITS")) : RS_MAX_BITS;
-  static const int grid_cap = getenv("SMX_SORT_GRID") ? atoi(getenv("SMX_SORT_GRID")) : 148 * 2;
   const int passes = (key_bits + max_bits - 1) / max_bits;
-  const int bits = (key_bits + passes - 1) / passes;
-  int G = (int)std::min<uint64_t>((n + RS_TILE - 1) / RS_TILE, grid_cap);
-  if (G < 1) G = 1;
-  const uint64_t seg = ((n + G - 1) / G + RS_TILE - 1) / RS_TILE * RS_TILE;
-  G = (int)((n + seg - 1) / seg);
-  uint32_t *hist = nullptr, *hscan = nullptr;
-  const size_t hn = (size_t)(1 << std::max(bits, 8)) * G;
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&hist, sizeof(uint32_t) * hn, st));
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&hscan, sizeof(uint32_t) * hn, st));
-  for (int pass = 0; pass < passes; ++pass) {
-    const bool from_a = (pass & 1) == 0;
-    SortPass p;
-    p.keys_in = from_a ? keys_a : keys_b;
-    p.vals_in = (pass == 0 && index_values) ? nullptr : (from_a ? vals_a : vals_b);
-    p.first = pass == 0;
-    p.last = pass == passes - 1;
-    p.shift = bits * pass;
-    p.n = n;
-    p.seg = seg;
-    p.lut = lut;
-    p.counts = counts;
-    p.hist_scan = hscan;
-    p.timing = g_sort_timing;
-    p.keys_out = p.last ? nullptr : (from_a ? keys_b : keys_a);
-    p.vals_out = from_a ? vals_b : vals_a;
-    if (int rc = run_pass_bits(bits, p, G, hist, hscan, st)) return rc;
-    *out_in_b = from_a ? 1 : 0;
+  const int bits = std::max((key_bits + passes - 1) / passes, 8);
+  switch (bits) {
+    case 8: return run_sort<8>(keys_a, vals_a, keys_b, vals_b, n, passes, index_values, lut, counts, n_keys, out_in_b, st);
+    case 9: return run_sort<9>(keys_a, vals_a, keys_b, vals_b, n, passes, index_values, lut, counts, n_keys, out_in_b, st);
+    case 10: return run_sort<10>(keys_a, vals_a, keys_b, vals_b, n, passes, index_values, lut, counts, n_keys, out_in_b, st);
+    default: return run_sort<11>(keys_a, vals_a, keys_b, vals_b, n, passes, index_values, lut, counts, n_keys, out_in_b, st);
   }
-  cudaFreeAsync(hist, st);
-  cudaFreeAsync(hscan, st);
-  return 0;
 }

@@ -75,8 +75,9 @@ __global__ void dist_tables_kernel(const int32_t* src_rank, const int64_t* src_n
 enum { K_NONE = 0, K_FROM_VALUE = 1, K_FROM_J = 2 };
 enum { P_NONE = 0, P_FROM_VALUE = 1, P_FROM_J = 2 };
 
+template <int KM, int PM>
 struct GenSink {
-  int key_mode, pay_mode;
+  static constexpr bool kMark = true;
   const uint32_t* key_tab;
   const uint32_t* pay_tab;
   uint32_t kdiv;
@@ -84,13 +85,13 @@ struct GenSink {
   uint32_t* keys;        // pre-offset to the call's first record
   uint32_t* vals;
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const {
-    if (key_mode == K_FROM_VALUE) {
+    if (KM == K_FROM_VALUE) {
       if (keys && key_tab) keys[j] = __ldg(key_tab + v);
-    } else if (key_mode == K_FROM_J) {
+    } else if (KM == K_FROM_J) {
       keys[j] = key_tab[j / kdiv];
     }
-    if (pay_mode == P_FROM_J) vals[j] = pay_tab[j / kdiv];
-    else if (pay_mode == P_FROM_VALUE) vals[j] = pay_tab[v];
+    if (PM == P_FROM_J) vals[j] = pay_tab[j / kdiv];
+    else if (PM == P_FROM_VALUE) vals[j] = pay_tab[v];
   }
   // 8 items at j0 + u*stride: all gathers issued before any store
   __device__ __forceinline__ void batch(uint64_t j0, uint32_t stride, const uint32_t* v, uint32_t okm,
@@ -98,25 +99,23 @@ struct GenSink {
     uint32_t pp[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const uint64_t j = j0 + (uint64_t)u * stride;
+      const uint32_t j = (uint32_t)j0 + u * stride;  // call-local index < 2^32
       const bool ok = (okm >> u) & 1u;
       kk[u] = 0;
       pp[u] = 0;
       if (ok) {
-        if (key_tab) {
-          if (key_mode == K_FROM_VALUE) kk[u] = __ldg(key_tab + v[u]);
-          else if (key_mode == K_FROM_J) kk[u] = __ldg(key_tab + kd.div((uint32_t)j));
-        }
-        if (pay_mode == P_FROM_J) pp[u] = __ldg(pay_tab + kd.div((uint32_t)j));
-        else if (pay_mode == P_FROM_VALUE) pp[u] = __ldg(pay_tab + v[u]);
+        if (KM == K_FROM_VALUE && key_tab) kk[u] = __ldg(key_tab + v[u]);
+        else if (KM == K_FROM_J && key_tab) kk[u] = __ldg(key_tab + kd.div(j));
+        if (PM == P_FROM_J) pp[u] = __ldg(pay_tab + kd.div(j));
+        else if (PM == P_FROM_VALUE) pp[u] = __ldg(pay_tab + v[u]);
       }
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       if (!((okm >> u) & 1u)) continue;
       const uint64_t j = j0 + (uint64_t)u * stride;
-      if (key_mode != K_NONE && keys) keys[j] = kk[u];
-      if (pay_mode != P_NONE) vals[j] = pp[u];
+      if (KM != K_NONE && keys) keys[j] = kk[u];
+      if (PM != P_NONE) vals[j] = pp[u];
     }
   }
 };
@@ -415,43 +414,57 @@ extern "C" int smx_dist_tables(const int32_t* src_rank, const int64_t* src_node,
 
 // One numpy integers(0, ex, size=n) draw on stream (k0,k1) from u32 cursor u0,
 // routed into the pending record buffers by the rule's sink.
-extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, uint64_t n, int key_mode,
-                            int pay_mode, const uint32_t* key_tab, const uint32_t* pay_tab, uint32_t kdiv,
-                            uint32_t* keys, uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab,
-                            uint32_t used_bits_words, int mark_from_key, uint32_t tmp_base, uint32_t local_bit,
-                            uint64_t* cursor_out, void* stream) {
-  GenSink s;
-  s.key_mode = key_mode;
-  s.pay_mode = pay_mode;
+template <int KM, int PM>
+static int gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, uint64_t n, const uint32_t* key_tab,
+                    const uint32_t* pay_tab, uint32_t kdiv, uint32_t* keys, uint32_t* vals, const DrawMark& mk0,
+                    uint64_t* cursor_out, cudaStream_t st) {
+  GenSink<KM, PM> s;
   s.key_tab = key_tab;
   s.pay_tab = pay_tab;
   s.kdiv = kdiv ? kdiv : 1;
   s.kd = FastDiv::make(s.kdiv);
-  if (n >= (1ULL << 32)) {
-    smx_set_error("smx_gen_draw: %llu records in one call exceed 2^32", (unsigned long long)n);
-    return -1;
-  }
   s.keys = keys;
   s.vals = vals;
   DrawResult res;
   if (ex == 1) {  // numpy: a one-value range consumes nothing; every draw is 0
     if (n) {
-      smx_count_launch(); draw_const_kernel<GenSink><<<nblk(n), T256, 0, (cudaStream_t)stream>>>(n, s);
-      if (used_bits) { smx_count_launch(); mark_one_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(used_bits, used_tab); }
+      smx_count_launch(); draw_const_kernel<GenSink<KM, PM>><<<nblk(n), T256, 0, st>>>(n, s);
+      if (mk0.bits) { smx_count_launch(); mark_one_kernel<<<1, 1, 0, st>>>(mk0.bits, mk0.tab); }
       SMX_LAUNCH_CHECK();
     }
     *cursor_out = u0;
     return 0;
   }
-  // used-value marking (flagged / remote sources): bitmap size from the table
-  // range -- the caller sizes used_bits to cover every bit it can receive
-  DrawMark mk{used_bits, used_tab, used_bits_words, 0, mark_from_key, tmp_base, local_bit};
-  static const int variant = getenv("SMX_GEN_VARIANT") ? atoi(getenv("SMX_GEN_VARIANT")) : 0;  // tuning only
-  if (variant & 1) mk.bits = nullptr;
-  if (variant & 2) { s.key_mode = K_NONE; s.pay_mode = P_NONE; }
-  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, (cudaStream_t)stream, &res, mk);
+  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, st, &res, mk0);
   *cursor_out = res.cursor;
   return rc;
+}
+
+extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, uint64_t n, int key_mode,
+                            int pay_mode, const uint32_t* key_tab, const uint32_t* pay_tab, uint32_t kdiv,
+                            uint32_t* keys, uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab,
+                            uint32_t used_bits_words, int mark_from_key, uint32_t tmp_base, uint32_t local_bit,
+                            uint64_t* cursor_out, void* stream) {
+  if (n >= (1ULL << 32)) {
+    smx_set_error("smx_gen_draw: %llu records in one call exceed 2^32", (unsigned long long)n);
+    return -1;
+  }
+  if (key_mode < K_NONE || key_mode > K_FROM_J || pay_mode < P_NONE || pay_mode > P_FROM_J) {
+    smx_set_error("smx_gen_draw: bad key/payload mode %d/%d", key_mode, pay_mode);
+    return -1;
+  }
+  // used-value marking (flagged / remote sources): bitmap size from the table
+  // range -- the caller sizes used_bits to cover every bit it can receive
+  const DrawMark mk{used_bits, used_tab, used_bits_words, 0, mark_from_key, tmp_base, local_bit};
+  cudaStream_t st = (cudaStream_t)stream;
+#define SMX_GEN(KM, PM) \
+  if (key_mode == KM && pay_mode == PM) \
+    return gen_draw<KM, PM>(k0, k1, u0, ex, n, key_tab, pay_tab, kdiv, keys, vals, mk, cursor_out, st);
+  SMX_GEN(K_NONE, P_NONE) SMX_GEN(K_NONE, P_FROM_VALUE) SMX_GEN(K_NONE, P_FROM_J)
+  SMX_GEN(K_FROM_VALUE, P_NONE) SMX_GEN(K_FROM_VALUE, P_FROM_VALUE) SMX_GEN(K_FROM_VALUE, P_FROM_J)
+  SMX_GEN(K_FROM_J, P_NONE) SMX_GEN(K_FROM_J, P_FROM_VALUE) SMX_GEN(K_FROM_J, P_FROM_J)
+#undef SMX_GEN
+  return -1;
 }
 
 extern "C" int smx_gen_pairs(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab,

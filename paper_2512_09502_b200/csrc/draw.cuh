@@ -5,10 +5,12 @@
 // n-th output value; verified against numpy in tests/test_oracle_rng.py).
 //
 // Two launches per draw call:
-//   count:  CTA c counts accepts over its raw range (compute only)
-//   write:  CTA c regenerates its range, ranks accepts with a block scan,
-//           and hands (output index, value) to a Sink functor.
-// A tiny single-CTA scan between them turns per-CTA counts into offsets.
+//   count:  warp w counts accepts over its contiguous raw range (compute only)
+//   write:  warp w regenerates its range, ranks accepts with a warp scan,
+//           stages them in its own SMEM slice and hands (output index, value)
+//           to a Sink functor with coalesced indices.  Warps never wait for
+//           each other (no CTA barrier inside the loop).
+// A tiny single-CTA scan between them turns per-warp counts into offsets.
 #pragma once
 #include "common.cuh"
 
@@ -19,8 +21,8 @@ constexpr int DRAW_THREADS = 256;
 struct DrawRange {
   Key key;
   uint64_t u0;       // first raw u32 position
-  uint64_t n_raw;    // raw positions covered by the launch
-  uint64_t per_cta;  // raw positions per CTA
+  uint64_t n_raw;     // raw positions covered by the launch
+  uint64_t per_warp;  // raw positions per warp (multiple of 8)
   Lemire lm;
 };
 
@@ -35,34 +37,45 @@ __device__ __forceinline__ uint32_t block_accepts(const DrawRange& r, uint64_t b
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint32_t v = (i & 1) ? (uint32_t)(w[i >> 1] >> 32) : (uint32_t)w[i >> 1];
-    const uint64_t p = p0 + i;
     uint32_t out;
     const bool ok = r.lm.accept(v, out);
     vals[i] = out;
-    if (ok && p >= lo && p < hi) mask |= 1u << i;
+    mask |= (ok ? 1u : 0u) << i;
+  }
+  if (p0 < lo || p0 + 8 > hi) {  // block straddles the range edge (rare)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (p0 + i < lo || p0 + i >= hi) mask &= ~(1u << i);
   }
   return mask;
 }
 
-static __global__ void draw_count_kernel(DrawRange r, uint32_t* cta_counts) {
-  const uint64_t lo = r.u0 + (uint64_t)blockIdx.x * r.per_cta;
+constexpr int DRAW_WARPS = DRAW_THREADS / 32;
+
+__device__ __forceinline__ void warp_range(const DrawRange& r, uint64_t& lo, uint64_t& hi) {
+  const uint64_t gw = (uint64_t)blockIdx.x * DRAW_WARPS + (threadIdx.x >> 5);
+  lo = r.u0 + gw * r.per_warp;
   const uint64_t end = r.u0 + r.n_raw;
-  const uint64_t hi = lo + r.per_cta < end ? lo + r.per_cta : end;
+  hi = lo + r.per_warp < end ? lo + r.per_warp : end;
+}
+
+static __global__ void __launch_bounds__(DRAW_THREADS) draw_count_kernel(DrawRange r, uint32_t* warp_counts) {
+  uint64_t lo, hi;
+  warp_range(r, lo, hi);
   uint32_t cnt = 0;
   if (lo < hi) {
     const uint64_t b0 = lo / 8 + 1, b1 = (hi - 1) / 8 + 1;
-    for (uint64_t b = b0 + threadIdx.x; b <= b1; b += blockDim.x) {
+    for (uint64_t b = b0 + (threadIdx.x & 31); b <= b1; b += 32) {
       uint32_t v[8];
       cnt += __popc(block_accepts(r, b, lo, hi, v));
     }
   }
-  __shared__ uint32_t ws[DRAW_THREADS / 32];
-  uint32_t tot;
-  block_excl_scan(cnt, ws, tot);
-  if (threadIdx.x == 0) cta_counts[blockIdx.x] = tot;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) warp_counts[(uint64_t)blockIdx.x * DRAW_WARPS + (threadIdx.x >> 5)] = cnt;
 }
 
-// Exclusive scan of per-CTA counts (n <= a few thousand) into 64-bit offsets;
+// Exclusive scan of per-warp counts (n <= some ten thousand) into 64-bit offsets;
 // offsets[n] = total.
 static __global__ void cta_offsets_kernel(const uint32_t* counts, int n, uint64_t* offsets) {
   __shared__ uint32_t ws[32];
@@ -105,83 +118,118 @@ struct DrawMark {
 constexpr uint32_t DRAW_MARK_SMEM_WORDS = 12288;  // 48 KB
 constexpr int DRAW_BPT = 2;                       // Philox blocks per thread per iteration
 
-template <class Sink>
-__global__ void __launch_bounds__(DRAW_THREADS) draw_write_kernel(DrawRange r, const uint64_t* cta_offsets,
+// MARK: 0 no marking, 1 bit from the sink's key, 2 bit from the value (via tab)
+template <int MARK>
+__device__ __forceinline__ uint32_t mark_bit(const DrawMark& mk, uint32_t key, uint32_t value) {
+  if (MARK == 1) return (key & SMX_TMP_KEY) ? (key & ~SMX_TMP_KEY) - mk.tmp_base : mk.local_bit;
+  return mk.tab ? __ldg(mk.tab + value) : value;
+}
+
+template <class Sink, int MARK>
+__global__ void __launch_bounds__(DRAW_THREADS) draw_write_kernel(DrawRange r, const uint64_t* warp_offsets,
                                                                   uint64_t n_out, Sink sink, uint64_t* cursor_out,
                                                                   DrawMark mk) {
   extern __shared__ uint32_t smark[];
-  const uint64_t lo = r.u0 + (uint64_t)blockIdx.x * r.per_cta;
-  const uint64_t end = r.u0 + r.n_raw;
-  const uint64_t hi = lo + r.per_cta < end ? lo + r.per_cta : end;
-  uint64_t base = cta_offsets[blockIdx.x];
-  if (lo >= hi || base >= n_out) return;
-  if (mk.in_smem) {
+  __shared__ uint32_t sv_all[DRAW_WARPS][32 * 8 * DRAW_BPT];  // a warp's accepted values of one iteration
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* sv = sv_all[warp];
+  if (MARK && mk.in_smem) {
     for (uint32_t w = threadIdx.x; w < mk.nwords; w += blockDim.x) smark[w] = 0;
+    __syncthreads();
   }
-  __shared__ uint32_t ws[DRAW_THREADS / 32];
-  __shared__ uint32_t sv[DRAW_THREADS * 8 * DRAW_BPT];  // accepted values of one iteration, in order
-  const uint64_t b0 = lo / 8 + 1, b1 = (hi - 1) / 8 + 1;
-  for (uint64_t bb = b0; bb <= b1 && base < n_out; bb += (uint64_t)DRAW_BPT * blockDim.x) {
-    // thread t owns blocks bb + BPT*t .. +BPT-1: raw order = thread order
-    uint32_t v[DRAW_BPT][8];
-    uint32_t mask[DRAW_BPT];
-    uint32_t cnt = 0;
+  uint64_t lo, hi;
+  warp_range(r, lo, hi);
+  uint64_t base = warp_offsets[(uint64_t)blockIdx.x * DRAW_WARPS + warp];
+  bool saw_local = false;
+  if (lo < hi && base < n_out) {
+    const uint64_t b0 = lo / 8 + 1, b1 = (hi - 1) / 8 + 1;
+    for (uint64_t bb = b0; bb <= b1 && base < n_out; bb += (uint64_t)DRAW_BPT * 32) {
+      // lane l owns blocks bb + BPT*l .. +BPT-1: raw order = lane order
+      uint32_t v[DRAW_BPT][8];
+      uint32_t mask[DRAW_BPT];
+      uint32_t cnt = 0;
 #pragma unroll
-    for (int q = 0; q < DRAW_BPT; ++q) {
-      const uint64_t b = bb + (uint64_t)DRAW_BPT * threadIdx.x + q;
-      mask[q] = b <= b1 ? block_accepts(r, b, lo, hi, v[q]) : 0u;
-      cnt += __popc(mask[q]);
-    }
-    uint32_t tot;
-    const uint32_t ex = block_excl_scan(cnt, ws, tot);
-    uint32_t k = ex;
+      for (int q = 0; q < DRAW_BPT; ++q) {
+        const uint64_t b = bb + (uint64_t)DRAW_BPT * lane + q;
+        mask[q] = b <= b1 ? block_accepts(r, b, lo, hi, v[q]) : 0u;
+        cnt += __popc(mask[q]);
+      }
+      const uint32_t inc = warp_incl_scan(cnt);
+      const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+      uint32_t k = inc - cnt;
+      if (cursor_out && base + tot >= n_out) {  // this iteration holds the last output
+        const uint64_t want = n_out - 1 - base;   // its index within the iteration
+        if (want >= k && want < inc) {
+          uint32_t left = (uint32_t)(want - k);
 #pragma unroll
-    for (int q = 0; q < DRAW_BPT; ++q) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {  // static indexing keeps v[] in registers
-        if ((mask[q] >> i) & 1u) {
-          sv[k] = v[q][i];
-          if (base + k == n_out - 1 && cursor_out) {
-            const uint64_t b = bb + (uint64_t)DRAW_BPT * threadIdx.x + q;
-            *cursor_out = (b - 1) * 8 + i + 1;
+          for (int q = 0; q < DRAW_BPT; ++q) {
+            const uint32_t c = __popc(mask[q]);
+            if (left < c && left != 0xffffffffu) {
+              uint32_t m = mask[q];
+              for (uint32_t z = 0; z < left; ++z) m &= m - 1;
+              const uint64_t b = bb + (uint64_t)DRAW_BPT * lane + q;
+              *cursor_out = (b - 1) * 8 + (__ffs(m) - 1) + 1;
+              left = 0xffffffffu;
+            } else if (left != 0xffffffffu) {
+              left -= c;
+            }
           }
-          ++k;
         }
       }
-    }
-    __syncthreads();
-    // coalesced hand-off: consecutive threads own consecutive output indices;
-    // a thread's items go over in batches of 8 so their gathers overlap
 #pragma unroll
-    for (int h = 0; h < DRAW_BPT; ++h) {
-      uint32_t vv[8], kk[8];
-      uint32_t okm = 0;
+      for (int q = 0; q < DRAW_BPT; ++q) {
+        if (mask[q] == 0xffu) {  // no rejection in the block (the common case)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t q = threadIdx.x + (h * 8 + u) * blockDim.x;
-        const bool ok = q < tot && base + q < n_out;
-        vv[u] = ok ? sv[q] : 0u;
-        okm |= (ok ? 1u : 0u) << u;
+          for (int i = 0; i < 8; ++i) sv[k + i] = v[q][i];
+          k += 8;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {  // static indexing keeps v[] in registers
+            if ((mask[q] >> i) & 1u) sv[k++] = v[q][i];
+          }
+        }
       }
-      sink.batch(base + threadIdx.x + (uint64_t)h * 8 * blockDim.x, blockDim.x, vv, okm, kk);
-      if (mk.bits) {
+      __syncwarp();
+      // coalesced hand-off: consecutive lanes own consecutive output indices;
+      // a lane's items go over in batches of 8 so their gathers overlap
+#pragma unroll
+      for (int h = 0; h < DRAW_BPT; ++h) {
+        if ((uint32_t)h * 256 >= tot) break;
+        uint32_t vv[8], kk[8];
+        uint32_t okm = 0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          if (!((okm >> u) & 1u)) continue;
-          uint32_t bit;
-          if (mk.from_key) bit = (kk[u] & SMX_TMP_KEY) ? (kk[u] & ~SMX_TMP_KEY) - mk.tmp_base : mk.local_bit;
-          else bit = mk.tab ? __ldg(mk.tab + vv[u]) : vv[u];
-          if (bit == 0xffffffffu) continue;
-          const uint32_t m = 1u << (bit & 31);
-          uint32_t* w = mk.in_smem ? &smark[bit >> 5] : &mk.bits[bit >> 5];
-          if (!(*(volatile uint32_t*)w & m)) atomicOr(w, m);
+          const uint32_t q = lane + (h * 8 + u) * 32;
+          const bool ok = q < tot && base + q < n_out;
+          vv[u] = ok ? sv[q] : 0u;
+          okm |= (ok ? 1u : 0u) << u;
+        }
+        sink.batch(base + lane + (uint64_t)h * 256, 32, vv, okm, kk);
+        if (MARK) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (!((okm >> u) & 1u)) continue;
+            if (MARK == 1 && !(kk[u] & SMX_TMP_KEY)) {  // local key: one bit for all, set once below
+              saw_local = true;
+              continue;
+            }
+            const uint32_t bit = mark_bit<MARK>(mk, kk[u], vv[u]);
+            if (bit == 0xffffffffu) continue;
+            const uint32_t m = 1u << (bit & 31);
+            uint32_t* w = mk.in_smem ? &smark[bit >> 5] : &mk.bits[bit >> 5];
+            if (!(*(volatile uint32_t*)w & m)) atomicOr(w, m);
+          }
         }
       }
+      base += tot;
+      __syncwarp();
     }
-    base += tot;
-    __syncthreads();
   }
-  if (mk.in_smem) {
+  if (MARK == 1 && __any_sync(0xffffffffu, saw_local) && lane == 0 && mk.local_bit != 0xffffffffu) {
+    const uint32_t b = mk.local_bit;
+    atomicOr(mk.in_smem ? &smark[b >> 5] : &mk.bits[b >> 5], 1u << (b & 31));
+  }
+  if (MARK && mk.in_smem) {
     __syncthreads();
     for (uint32_t w = threadIdx.x; w < mk.nwords; w += blockDim.x) {
       const uint32_t x = smark[w];

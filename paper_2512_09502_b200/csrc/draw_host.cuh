@@ -9,6 +9,38 @@ struct DrawResult {
   uint64_t cursor;  // u32 cursor after the last consumed draw
 };
 
+template <class Sink, int MARK>
+int launch_write(int G, size_t smem, cudaStream_t st, const DrawRange& r, const uint64_t* offs, uint64_t n_out,
+                 const Sink& sink, uint64_t* cur_d, const DrawMark& mk) {
+  static bool configured = false;
+  if (smem > 0 && !configured) {  // static (staging) + dynamic (bitmap) may exceed the 48 KB default
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(draw_write_kernel<Sink, MARK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(DRAW_MARK_SMEM_WORDS * 4)));
+    configured = true;
+  }
+  smx_count_launch(); draw_write_kernel<Sink, MARK><<<G, DRAW_THREADS, smem, st>>>(r, offs, n_out, sink, cur_d, mk);
+  return 0;
+}
+
+// Sinks that may mark used values say so with `static constexpr bool kMark`.
+template <class Sink, class = void>
+struct sink_marks { static constexpr bool value = false; };
+template <class Sink>
+struct sink_marks<Sink, decltype((void)Sink::kMark, void())> { static constexpr bool value = Sink::kMark; };
+
+template <class Sink>
+int launch_draw_write(int mode, int G, size_t smem, cudaStream_t st, const DrawRange& r, const uint64_t* offs,
+                      uint64_t n_out, const Sink& sink, uint64_t* cur_d, const DrawMark& mk) {
+  if constexpr (sink_marks<Sink>::value) {
+    if (mode == 1) return launch_write<Sink, 1>(G, smem, st, r, offs, n_out, sink, cur_d, mk);
+    if (mode == 2) return launch_write<Sink, 2>(G, smem, st, r, offs, n_out, sink, cur_d, mk);
+  } else if (mode != 0) {
+    smx_set_error("run_draw: this sink does not mark used values");
+    return -1;
+  }
+  return launch_write<Sink, 0>(G, smem, st, r, offs, n_out, sink, cur_d, mk);
+}
+
 // numpy integers(lo, lo+ex, size=n) on stream `key` from u32 cursor u0.
 // Hands every (index, value-lo) to `sink`; returns 0 or a negative status.
 template <class Sink>
@@ -38,25 +70,23 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
   for (int attempt = 0; attempt < 8; ++attempt) {
     int G = (int)std::min<uint64_t>((n_raw + 16383) / 16384, 148 * 8);
     if (G < 1) G = 1;
+    const int NW = G * DRAW_WARPS;
     r.n_raw = n_raw;
-    r.per_cta = ((n_raw + G - 1) / G + 7) / 8 * 8;
-    SMX_CUDA_CHECK(cudaMallocAsync((void**)&counts, sizeof(uint32_t) * G, st));
-    SMX_CUDA_CHECK(cudaMallocAsync((void**)&offs, sizeof(uint64_t) * (G + 1), st));
+    r.per_warp = ((n_raw + NW - 1) / NW + 7) / 8 * 8;
+    SMX_CUDA_CHECK(cudaMallocAsync((void**)&counts, sizeof(uint32_t) * NW, st));
+    SMX_CUDA_CHECK(cudaMallocAsync((void**)&offs, sizeof(uint64_t) * (NW + 1), st));
     SMX_CUDA_CHECK(cudaMallocAsync((void**)&cur_d, sizeof(uint64_t), st));
     smx_count_launch(); draw_count_kernel<<<G, DRAW_THREADS, 0, st>>>(r, counts);
-    smx_count_launch(); cta_offsets_kernel<<<1, 1024, 0, st>>>(counts, G, offs);
+    smx_count_launch(); cta_offsets_kernel<<<1, 1024, 0, st>>>(counts, NW, offs);
     SMX_LAUNCH_CHECK();
     uint64_t total = 0;
-    SMX_CUDA_CHECK(cudaMemcpyAsync(&total, offs + G, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SMX_CUDA_CHECK(cudaMemcpyAsync(&total, offs + NW, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     SMX_CUDA_CHECK(cudaStreamSynchronize(st));
     if (total >= n_out) {
       mk.in_smem = mk.bits && mk.nwords <= DRAW_MARK_SMEM_WORDS;
       const size_t smem = mk.in_smem ? mk.nwords * 4 : 0;
-      if (smem > 0) {  // static (staging) + dynamic (bitmap) may exceed the 48 KB default
-        SMX_CUDA_CHECK(cudaFuncSetAttribute(draw_write_kernel<Sink>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)(DRAW_MARK_SMEM_WORDS * 4)));
-      }
-      smx_count_launch(); draw_write_kernel<Sink><<<G, DRAW_THREADS, smem, st>>>(r, offs, n_out, sink, cur_d, mk);
+      const int mode = mk.bits ? (mk.from_key ? 1 : 2) : 0;
+      if (rc = launch_draw_write(mode, G, smem, st, r, offs, n_out, sink, cur_d, mk); rc) return rc;
       SMX_LAUNCH_CHECK();
       SMX_CUDA_CHECK(cudaMemcpyAsync(&res->cursor, cur_d, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
       SMX_CUDA_CHECK(cudaStreamSynchronize(st));

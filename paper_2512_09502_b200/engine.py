@@ -1058,6 +1058,9 @@ class Cluster:
         if n and n_nodes >= (1 << 31):
             raise ValueError("more than 2^31 nodes on one rank")
         ev0 = self._event(st) if self.prof is not None else None
+        main = torch.cuda.current_stream(dev)
+        pre_sort = torch.cuda.Event()
+        pre_sort.record(main)  # maps / mirrors / rosters written so far
         call("smx_sort_records", _ptr(st.keys.t), _ptr(st.vals.t), _ptr(kb), _ptr(vb), n, key_bits,
              1 if st.wide else 0, _ptr(lut), _ptr(st.counts), n_nodes, which.ctypes.data, sk)
         sorted_vals = (vb if which[0] else st.vals.t)[:n]
@@ -1074,9 +1077,8 @@ class Cluster:
         else:
             st.payload = sorted_vals if n else torch.empty(1, dtype=torch.int32, device=dev)
             st.ww = st.wm = None
-        main = torch.cuda.current_stream(dev)
         side = _prep_stream(dev)
-        side.wait_stream(main)  # maps / mirrors / rosters were written on main
+        side.wait_event(pre_sort)  # not on the sort itself: the side work overlaps it
         with torch.cuda.stream(side):
             self._prepare_tables(st)
         main.wait_stream(side)

@@ -1,6 +1,9 @@
 // Host driver for the ordered Lemire draw engine (draw.cuh).
 #pragma once
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include "draw.cuh"
 
 namespace smx {
@@ -63,6 +66,12 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
   r.lm.threshold = ex == (1ULL << 32) ? 0u : (uint32_t)(((1ULL << 32) - ex) % ex);
   const double prej = (double)r.lm.threshold / 4294967296.0;
   uint64_t n_raw = n_out + (uint64_t)std::ceil(n_out * prej * 1.25 + 12.0 * std::sqrt(n_out * prej + 1.0) + 64.0);
+  static const bool timing = getenv("SMX_DRAW_TIMING") != nullptr;  // tuning aid
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t_start = timing ? now_us() : 0.0;
+  double t_count = 0.0;
   uint32_t* counts = nullptr;
   uint64_t* offs = nullptr;
   uint64_t* cur_d = nullptr;
@@ -82,6 +91,7 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
     uint64_t total = 0;
     SMX_CUDA_CHECK(cudaMemcpyAsync(&total, offs + NW, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (timing) t_count = now_us();
     if (total >= n_out) {
       mk.in_smem = mk.bits && mk.nwords <= DRAW_MARK_SMEM_WORDS;
       const size_t smem = mk.in_smem ? mk.nwords * 4 : 0;
@@ -90,6 +100,9 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
       SMX_LAUNCH_CHECK();
       SMX_CUDA_CHECK(cudaMemcpyAsync(&res->cursor, cur_d, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
       SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+      if (timing)
+        fprintf(stderr, "run_draw n=%llu G=%d: count+sync %.0f us, write+sync %.0f us\n", (unsigned long long)n_out, G,
+                t_count - t_start, now_us() - t_count);
       rc = 0;
     } else {
       rc = 1;

@@ -140,11 +140,15 @@ class _Buf:
             return torch.empty(cap, dtype=self.dtype, device=self.device)
         return torch.full((cap,), self.fill, dtype=self.dtype, device=self.device)
 
-    def reserve(self, n):
+    def reserve(self, n, headroom: float = 0.0):
+        """Capacity for n entries; a reallocation copies the used part only.
+        headroom: extra fraction of n allocated on growth (record buffers use
+        it so a later, smaller connect call does not move the earlier ones)."""
         if n > self.t.numel():
-            cap = max(n, int(self.t.numel() * 1.5) + 16)
+            cap = max(n + int(n * headroom), int(self.t.numel() * 1.5) + 16)
             nt = self._alloc(cap)
-            nt[: self.t.numel()].copy_(self.t)
+            if self.n:
+                nt[: self.n].copy_(self.t[: self.n])
             self.t = nt
 
     def view(self, a=0, b=None):
@@ -220,14 +224,17 @@ class _Rank:
             self.maps[key] = _Map(self.device)
         return self.maps[key]
 
+    RECORD_HEADROOM = 0.5
+
     def reserve_records(self, n_new):
         need = self.keys.n + n_new
-        self.keys.reserve(need)
-        self.vals.reserve(need)
+        h = self.RECORD_HEADROOM
+        self.keys.reserve(need, h)
+        self.vals.reserve(need, h)
         if self.wide:
-            self.w_rows.reserve(need)
-            self.w_w.reserve(need)
-            self.w_meta.reserve(need)
+            self.w_rows.reserve(need, h)
+            self.w_w.reserve(need, h)
+            self.w_meta.reserve(need, h)
         return self.keys.n
 
     def commit_records(self, n_new):

@@ -11,7 +11,7 @@ import os
 from .api import ConsistencyError, DelayRangeError, ProtocolError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libspikemesh_b200.so")
+LIB_PATH = os.environ.get("SMX_LIB_PATH") or os.path.join(_HERE, "_build", "libspikemesh_b200.so")  # env: A/B tuning
 
 P = ctypes.c_void_p
 U64 = ctypes.c_uint64

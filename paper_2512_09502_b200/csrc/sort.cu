@@ -34,10 +34,11 @@ constexpr int CNT_BINS = 12288;                   // last-pass key-count bins in
 __host__ __device__ constexpr int ds_ctas_per_sm(int bits) { return bits <= 9 ? 3 : 2; }
 
 struct SortPass {
-  const uint32_t* keys_in;
+  const uint32_t* keys_in;  // SoA input keys (first pass)
   const uint32_t* vals_in;  // null: value = record index (first pass only)
-  uint32_t* keys_out;       // null on the last pass
-  uint32_t* vals_out;
+  const uint2* recs_in;     // later passes: (key, value) records
+  uint2* recs_out;          // all but the last pass: (key, value) records
+  uint32_t* vals_out;       // last pass: values only
   uint64_t n;
   uint64_t seg;             // records per CTA (multiple of DS_TILE)
   int shift;
@@ -52,6 +53,10 @@ struct SortPass {
 
 __device__ __forceinline__ uint32_t resolve(uint32_t k, const uint32_t* lut) {
   return (k & SMX_TMP_KEY) ? lut[k & ~SMX_TMP_KEY] : k;
+}
+
+__device__ __forceinline__ uint32_t key_at(const SortPass& p, uint64_t i) {
+  return p.recs_in ? p.recs_in[i].x : p.keys_in[i];
 }
 
 __device__ __forceinline__ void count_key(const SortPass& p, uint32_t key, uint32_t c) {
@@ -92,8 +97,8 @@ __global__ void __launch_bounds__(US_THREADS) tile_hist_kernel(SortPass p, uint1
     if (p.shift == 0) {
       mode = 1;
     } else {
-      lo_v = p.keys_in[lo] & lm;
-      const uint32_t hi_v = p.keys_in[hi - 1] & lm;
+      lo_v = key_at(p, lo) & lm;
+      const uint32_t hi_v = key_at(p, hi - 1) & lm;
       span = hi_v - lo_v + 1;
       mode = (hi_v >= lo_v && (uint64_t)span * BINS <= CNT_BINS) ? 1 : 2;
     }
@@ -107,18 +112,23 @@ __global__ void __launch_bounds__(US_THREADS) tile_hist_kernel(SortPass p, uint1
     for (int j = lane; j < BINS; j += 32) wh[j] = 0;
     __syncwarp();
     const uint64_t a = (uint64_t)t * DS_TILE, b = min(p.n, a + DS_TILE);
-    const uint4* k4 = reinterpret_cast<const uint4*>(p.keys_in + a);
     const uint32_t nq = (uint32_t)((b - a) / 4);
     for (uint32_t i = lane; i < nq + 1; i += 32) {
       uint32_t kk[4];
       int m = 4;
       if (i < nq) {
-        const uint4 q = k4[i];
-        kk[0] = q.x; kk[1] = q.y; kk[2] = q.z; kk[3] = q.w;
+        if (p.recs_in) {  // four (key, value) records: two 16-byte loads
+          const uint4* r4 = reinterpret_cast<const uint4*>(p.recs_in + a) + 2 * i;
+          const uint4 q0 = r4[0], q1 = r4[1];
+          kk[0] = q0.x; kk[1] = q0.z; kk[2] = q1.x; kk[3] = q1.z;
+        } else {
+          const uint4 q = reinterpret_cast<const uint4*>(p.keys_in + a)[i];
+          kk[0] = q.x; kk[1] = q.y; kk[2] = q.z; kk[3] = q.w;
+        }
       } else {  // ragged tail of the last tile
         m = (int)((b - a) - 4 * (uint64_t)nq);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) kk[j] = j < m ? p.keys_in[a + 4 * nq + j] : 0u;
+        for (int j = 0; j < 4; ++j) kk[j] = j < m ? key_at(p, a + 4 * nq + j) : 0u;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -296,7 +306,7 @@ __global__ void __launch_bounds__(DS_THREADS, ds_ctas_per_sm(BITS)) downsweep_ke
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1;
   const uint32_t mask = BINS - 1;
-  const bool has_vals = p.vals_in != nullptr;
+  const bool has_vals = p.vals_in != nullptr || p.recs_in != nullptr;
   const bool any_tmp = p.first && p.lut && p.tmp_flag && *p.tmp_flag;  // temporary keys to resolve
   if (tid == 0) {
     smx::mbar_init(&bar, 1);
@@ -308,11 +318,15 @@ __global__ void __launch_bounds__(DS_THREADS, ds_ctas_per_sm(BITS)) downsweep_ke
     const uint64_t t0 = (uint64_t)t * DS_TILE;
     const bool full = t0 + DS_TILE <= p.n;
     const uint32_t bytes = DS_TILE * 4;
-    smx::mbar_expect_tx(&bar, BINS * 4 + (full ? (has_vals ? 2 * bytes : bytes) : 0));
+    smx::mbar_expect_tx(&bar, BINS * 4 + (full ? (has_vals ? 2 * bytes : bytes) : 0));  // records: 2 * bytes
     smx::bulk_g2s(ioff + b * BINS, off + (size_t)t * BINS, BINS * 4, &bar);
     if (full) {
-      smx::bulk_g2s(ikey, p.keys_in + t0, bytes, &bar);
-      if (has_vals) smx::bulk_g2s(ival, p.vals_in + t0, bytes, &bar);
+      if (p.recs_in) {
+        smx::bulk_g2s(ikey, p.recs_in + t0, 2 * bytes, &bar);  // ikey|ival hold the records
+      } else {
+        smx::bulk_g2s(ikey, p.keys_in + t0, bytes, &bar);
+        if (has_vals) smx::bulk_g2s(ival, p.vals_in + t0, bytes, &bar);
+      }
     }
   };
   uint32_t phase = 0;
@@ -332,19 +346,35 @@ __global__ void __launch_bounds__(DS_THREADS, ds_ctas_per_sm(BITS)) downsweep_ke
     smx::mbar_wait(&bar, phase);
     phase ^= 1;
     if (full) {
+      if (p.recs_in) {
+        const uint2* rin = reinterpret_cast<const uint2*>(ikey);
 #pragma unroll
-      for (int i = 0; i < DS_IPT; ++i) {
-        const uint32_t q = wofs + i * 32;
-        k[i] = ikey[q];
-        v[i] = has_vals ? ival[q] : (uint32_t)(t0 + q);
+        for (int i = 0; i < DS_IPT; ++i) {
+          const uint2 r = rin[wofs + i * 32];
+          k[i] = r.x;
+          v[i] = r.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < DS_IPT; ++i) {
+          const uint32_t q = wofs + i * 32;
+          k[i] = ikey[q];
+          v[i] = has_vals ? ival[q] : (uint32_t)(t0 + q);
+        }
       }
     } else {
 #pragma unroll
       for (int i = 0; i < DS_IPT; ++i) {
         const uint64_t idx = t0 + wofs + i * 32;
         const bool ok = idx < p.n;
-        k[i] = ok ? p.keys_in[idx] : 0u;
-        v[i] = ok ? (has_vals ? p.vals_in[idx] : (uint32_t)idx) : 0u;
+        if (p.recs_in) {
+          const uint2 r = ok ? p.recs_in[idx] : make_uint2(0u, 0u);
+          k[i] = r.x;
+          v[i] = r.y;
+        } else {
+          k[i] = ok ? p.keys_in[idx] : 0u;
+          v[i] = ok ? (p.vals_in ? p.vals_in[idx] : (uint32_t)idx) : 0u;
+        }
       }
     }
     if (any_tmp) {
@@ -411,8 +441,8 @@ __global__ void __launch_bounds__(DS_THREADS, ds_ctas_per_sm(BITS)) downsweep_ke
     for (uint32_t q = tid; q < tsum; q += DS_THREADS) {
       const uint32_t kk = skey[q];
       const uint32_t g = delta[(kk >> p.shift) & mask] + q;
-      p.vals_out[g] = sval[q];
-      if (!p.last) p.keys_out[g] = kk;
+      if (p.last) p.vals_out[g] = sval[q];
+      else p.recs_out[g] = make_uint2(kk, sval[q]);  // one 8-byte store per record
     }
   }
 }
@@ -450,11 +480,31 @@ int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* val
   const uint32_t tpc = (n_tiles + hg - 1) / hg;
   const uint32_t hgrid = (n_tiles + tpc - 1) / tpc;
   const uint32_t grid = std::min<uint32_t>(n_tiles, 148u * ds_ctas_per_sm(BITS));
+  // Intermediate passes move (key, value) records as one 8-byte item (AoS):
+  // half the store instructions and twice the bytes per scattered run of the
+  // SoA layout.  X lives in the scratch pair when keys_b | vals_b are
+  // contiguous, Y (three or more passes) in keys_a | vals_a likewise.
+  uint2* X = vals_b == keys_b + n ? reinterpret_cast<uint2*>(keys_b) : nullptr;
+  uint2* Y = nullptr;
+  uint2* own = nullptr;
+  if (passes > 1 && !X) {
+    SMX_CUDA_CHECK(cudaMallocAsync((void**)&own, sizeof(uint2) * n * (passes > 2 ? 2 : 1), st));
+    X = own;
+  }
+  if (passes > 2) Y = own ? own + n : (vals_a == keys_a + n ? reinterpret_cast<uint2*>(keys_a) : nullptr);
+  if (passes > 2 && !Y) {
+    SMX_CUDA_CHECK(cudaMallocAsync((void**)&own, sizeof(uint2) * n, st));
+    Y = own;
+  }
   for (int pass = 0; pass < passes; ++pass) {
-    const bool from_a = (pass & 1) == 0;
     SortPass p{};
-    p.keys_in = from_a ? keys_a : keys_b;
-    p.vals_in = (pass == 0 && index_values) ? nullptr : (from_a ? vals_a : vals_b);
+    const uint2* in = pass == 0 ? nullptr : (pass & 1 ? X : Y);
+    if (pass == 0) {
+      p.keys_in = keys_a;
+      p.vals_in = index_values ? nullptr : vals_a;
+    } else {
+      p.recs_in = in;
+    }
     p.first = pass == 0;
     p.last = pass == passes - 1;
     p.shift = BITS * pass;
@@ -462,8 +512,14 @@ int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* val
     p.lut = lut;
     p.counts = counts;
     p.n_keys = n_keys;
-    p.keys_out = p.last ? nullptr : (from_a ? keys_b : keys_a);
-    p.vals_out = from_a ? vals_b : vals_a;
+    if (!p.last) {
+      p.recs_out = pass & 1 ? Y : X;
+    } else {
+      // values land in whichever SoA value array does not overlap the input
+      const bool in_b = pass == 0 || in == reinterpret_cast<const uint2*>(keys_b);
+      p.vals_out = in_b ? (pass == 0 ? vals_b : vals_a) : vals_b;
+      *out_in_b = p.vals_out == vals_b ? 1 : 0;
+    }
     p.tmp_flag = ctr + passes;
     smx_count_launch(); tile_hist_kernel<BITS><<<hgrid, US_THREADS, th_smem, st>>>(p, tcnt, n_tiles, tpc);
     smx_count_launch(); chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, n_tiles, csum);
@@ -471,8 +527,8 @@ int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* val
     smx_count_launch(); tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, csum, n_tiles, off);
     smx_count_launch(); downsweep_kernel<BITS><<<grid, DS_THREADS, smem, st>>>(p, off, n_tiles, ctr + pass);
     SMX_LAUNCH_CHECK();
-    *out_in_b = from_a ? 1 : 0;
   }
+  if (own) cudaFreeAsync(own, st);
   cudaFreeAsync(tcnt, st);
   cudaFreeAsync(off, st);
   cudaFreeAsync(csum, st);

@@ -1058,8 +1058,10 @@ class Cluster:
         st.n_records = n
         key_bits = max(1, int(n_nodes - 1).bit_length())
         st.counts = torch.empty(max(n_nodes, 1), dtype=torch.int32, device=dev)
-        kb = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        vb = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        # scratch pair in one allocation: the sort's intermediate passes use it
+        # as n (key, value) records
+        scratch = torch.empty(2 * max(n, 1), dtype=torch.int32, device=dev)
+        kb, vb = scratch[: max(n, 1)], scratch[max(n, 1):]
         which = np.zeros(1, dtype=np.int32)
         lut = st.lut.t
         if n and n_nodes >= (1 << 31):
@@ -1093,7 +1095,7 @@ class Cluster:
         if n and int(st.first_index[-1].item()) != n:
             raise ConsistencyError(f"record source beyond node count {n_nodes}")
         # record lists are dropped only after the sort has consumed them
-        del kb, vb, sorted_vals
+        del kb, vb, scratch, sorted_vals
         st.keys = st.vals = None
         st.w_rows = st.w_w = st.w_meta = None
         st.lut = None

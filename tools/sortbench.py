@@ -16,8 +16,8 @@ _lib.call("smx_pool_setup", 0)
 g = torch.Generator(device=dev).manual_seed(1)
 keys = torch.randint(0, M, (n,), device=dev, dtype=torch.int32, generator=g)
 vals = torch.arange(n, device=dev, dtype=torch.int32)
-kb = torch.empty_like(keys)
-vb = torch.empty_like(vals)
+scratch = torch.empty(2 * n, device=dev, dtype=torch.int32)
+kb, vb = scratch[:n], scratch[n:]
 counts = torch.empty(M, dtype=torch.int32, device=dev)
 which = np.zeros(1, dtype=np.int32)
 bits = max(1, int(M - 1).bit_length())

@@ -94,13 +94,14 @@ struct GenSink {
     else if (PM == P_FROM_VALUE) vals[j] = pay_tab[v];
   }
   // 8 items at j0 + u*stride: all gathers issued before any store
+  template <bool ALL>
   __device__ __forceinline__ void batch(uint64_t j0, uint32_t stride, const uint32_t* v, uint32_t okm,
                                         uint32_t* kk) const {
     uint32_t pp[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const uint32_t j = (uint32_t)j0 + u * stride;  // call-local index < 2^32
-      const bool ok = (okm >> u) & 1u;
+      const bool ok = ALL || ((okm >> u) & 1u);
       kk[u] = 0;
       pp[u] = 0;
       if (ok) {
@@ -112,7 +113,7 @@ struct GenSink {
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      if (!((okm >> u) & 1u)) continue;
+      if (!ALL && !((okm >> u) & 1u)) continue;
       const uint64_t j = j0 + (uint64_t)u * stride;
       if (KM != K_NONE && keys) keys[j] = kk[u];
       if (PM != P_NONE) vals[j] = pp[u];
@@ -131,6 +132,7 @@ struct MetaSink {
   uint32_t port_bits;
   uint32_t* meta;
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const { meta[j] = (lo + v) | port_bits; }
+  template <bool ALL>
   __device__ __forceinline__ void batch(uint64_t j0, uint32_t stride, const uint32_t* v, uint32_t ok,
                                         uint32_t* keys) const {
 #pragma unroll
@@ -168,6 +170,7 @@ __global__ void autapse_apply_kernel(const uint32_t* idx, uint32_t m, const int6
 struct RawI64Sink {
   int64_t* out;
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const { out[j] = (int64_t)v; }
+  template <bool ALL>
   __device__ __forceinline__ void batch(uint64_t j0, uint32_t stride, const uint32_t* v, uint32_t ok,
                                         uint32_t* keys) const {
 #pragma unroll

@@ -95,8 +95,9 @@ static __global__ void cta_offsets_kernel(const uint32_t* counts, int n, uint64_
   if (threadIdx.x == 0) offsets[n] = carry;
 }
 
-// Sink contract: `void batch(uint64_t j0, uint32_t stride, const uint32_t v[8],
-// uint32_t ok, uint32_t keys_out[8])` consumes values v[u] (bit u of ok set)
+// Sink contract: `template <bool ALL> void batch(uint64_t j0, uint32_t stride,
+// const uint32_t v[8], uint32_t ok, uint32_t keys_out[8])` consumes values
+// v[u] (bit u of ok set; ALL: every bit set)
 // for output indices j0 + u*stride and reports the record keys it wrote;
 // `void operator()(uint64_t j, uint32_t value)` consumes one item.
 // Optional used-value marking fused into the write pass: bit
@@ -125,8 +126,11 @@ __device__ __forceinline__ uint32_t mark_bit(const DrawMark& mk, uint32_t key, u
   return mk.tab ? __ldg(mk.tab + value) : value;
 }
 
+#ifndef SMX_DRAW_MIN_BLOCKS
+#define SMX_DRAW_MIN_BLOCKS 3
+#endif
 template <class Sink, int MARK>
-__global__ void __launch_bounds__(DRAW_THREADS) draw_write_kernel(DrawRange r, const uint64_t* warp_offsets,
+__global__ void __launch_bounds__(DRAW_THREADS, SMX_DRAW_MIN_BLOCKS) draw_write_kernel(DrawRange r, const uint64_t* warp_offsets,
                                                                   uint64_t n_out, Sink sink, uint64_t* cursor_out,
                                                                   DrawMark mk) {
   extern __shared__ uint32_t smark[];
@@ -192,19 +196,27 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_write_kernel(DrawRange r, c
       __syncwarp();
       // coalesced hand-off: consecutive lanes own consecutive output indices;
       // a lane's items go over in batches of 8 so their gathers overlap
+      const bool all = tot == 256 * DRAW_BPT && base + tot <= n_out;  // every slot valid
 #pragma unroll
       for (int h = 0; h < DRAW_BPT; ++h) {
         if ((uint32_t)h * 256 >= tot) break;
         uint32_t vv[8], kk[8];
-        uint32_t okm = 0;
+        uint32_t okm = 0xffu;
+        if (all) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t q = lane + (h * 8 + u) * 32;
-          const bool ok = q < tot && base + q < n_out;
-          vv[u] = ok ? sv[q] : 0u;
-          okm |= (ok ? 1u : 0u) << u;
+          for (int u = 0; u < 8; ++u) vv[u] = sv[lane + (h * 8 + u) * 32];
+          sink.template batch<true>(base + lane + (uint64_t)h * 256, 32, vv, okm, kk);
+        } else {
+          okm = 0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t q = lane + (h * 8 + u) * 32;
+            const bool ok = q < tot && base + q < n_out;
+            vv[u] = ok ? sv[q] : 0u;
+            okm |= (ok ? 1u : 0u) << u;
+          }
+          sink.template batch<false>(base + lane + (uint64_t)h * 256, 32, vv, okm, kk);
         }
-        sink.batch(base + lane + (uint64_t)h * 256, 32, vv, okm, kk);
         if (MARK) {
 #pragma unroll
           for (int u = 0; u < 8; ++u) {

@@ -21,6 +21,7 @@ struct RawSink {
   int64_t lo;
   int64_t* out;
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const { out[j] = lo + (int64_t)v; }
+  template <bool ALL>
   __device__ __forceinline__ void batch(uint64_t j0, uint32_t stride, const uint32_t* v, uint32_t ok,
                                         uint32_t* keys) const {
 #pragma unroll

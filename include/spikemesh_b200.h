@@ -74,7 +74,9 @@ int smx_key_table(const int64_t* sources, uint64_t n, uint32_t tmp_base, int tmp
 int smx_dist_tables(const int32_t* src_rank, const int64_t* src_node, uint64_t total, const uint32_t* vbase,
                     int tgt_rank, uint32_t lut_base, uint32_t* key_tab, uint32_t* gv_tab, void* stream);
 /* One Generator.integers(0, ex, size=n) draw routed into pending records:
- * key_mode 0 none / 1 key_tab[value] / 2 key_tab[j / kdiv];
+ * key_mode 0 none / 1 key_tab[value] / 2 key_tab[j / kdiv] /
+ *          3 piecewise-affine key = value + delta[s] for start[s] <= value,
+ *            key_tab then being a HOST array {n (<= 8), start[n], delta[n]};
  * pay_mode 0 none / 1 pay_tab[value] / 2 pay_tab[j / kdiv];
  * used_bits (optional, used_bits_words words) marks bit
  * used_tab ? used_tab[value] : value for every emitted draw, or with

@@ -72,12 +72,34 @@ __global__ void dist_tables_kernel(const int32_t* src_rank, const int64_t* src_n
 
 // --- generation sinks ----------------------------------------------------------
 
-enum { K_NONE = 0, K_FROM_VALUE = 1, K_FROM_J = 2 };
+enum { K_NONE = 0, K_FROM_VALUE = 1, K_FROM_J = 2, K_PIECES = 3 };
+
+// Piecewise-affine key table: key(v) = v + delta[s] for start[s] <= v <
+// start[s+1].  A source population made of one contiguous node range per
+// rank (every reference model) is one piece per source rank, so the draw
+// writes keys without gathering from a table (the gather from an L2-resident
+// table was the generation kernel's longest dependency).
+constexpr int MAX_KEY_PIECES = 8;
+struct KeyPieces {
+  uint32_t n;
+  uint32_t start[MAX_KEY_PIECES];
+  uint32_t delta[MAX_KEY_PIECES];
+  __device__ __forceinline__ uint32_t key(uint32_t v) const {
+    uint32_t off = delta[0];
+    if (n > 1) {
+#pragma unroll
+      for (int s = 1; s < MAX_KEY_PIECES; ++s)
+        if (s < (int)n && v >= start[s]) off = delta[s];
+    }
+    return v + off;
+  }
+};
 enum { P_NONE = 0, P_FROM_VALUE = 1, P_FROM_J = 2 };
 
 template <int KM, int PM>
 struct GenSink {
   static constexpr bool kMark = true;
+  KeyPieces kp;
   const uint32_t* key_tab;
   const uint32_t* pay_tab;
   uint32_t kdiv;
@@ -87,6 +109,8 @@ struct GenSink {
   __device__ __forceinline__ void operator()(uint64_t j, uint32_t v) const {
     if (KM == K_FROM_VALUE) {
       if (keys && key_tab) keys[j] = __ldg(key_tab + v);
+    } else if (KM == K_PIECES) {
+      if (keys) keys[j] = kp.key(v);
     } else if (KM == K_FROM_J) {
       keys[j] = key_tab[j / kdiv];
     }
@@ -106,6 +130,7 @@ struct GenSink {
       pp[u] = 0;
       if (ok) {
         if (KM == K_FROM_VALUE && key_tab) kk[u] = __ldg(key_tab + v[u]);
+        else if (KM == K_PIECES) kk[u] = kp.key(v[u]);
         else if (KM == K_FROM_J && key_tab) kk[u] = __ldg(key_tab + kd.div(j));
         if (PM == P_FROM_J) pp[u] = __ldg(pay_tab + kd.div(j));
         else if (PM == P_FROM_VALUE) pp[u] = __ldg(pay_tab + v[u]);
@@ -422,6 +447,20 @@ static int gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, uint64_t
                     const uint32_t* pay_tab, uint32_t kdiv, uint32_t* keys, uint32_t* vals, const DrawMark& mk0,
                     uint64_t* cursor_out, cudaStream_t st) {
   GenSink<KM, PM> s;
+  s.kp.n = 0;
+  if (KM == K_PIECES) {  // key_tab is a host array {n, start[n], delta[n]}
+    const uint32_t np = key_tab ? key_tab[0] : 0;
+    if (np < 1 || np > MAX_KEY_PIECES) {
+      smx_set_error("smx_gen_draw: %u key pieces (1..%d supported)", np, MAX_KEY_PIECES);
+      return -1;
+    }
+    s.kp.n = np;
+    for (uint32_t i = 0; i < MAX_KEY_PIECES; ++i) {
+      s.kp.start[i] = i < np ? key_tab[1 + i] : 0xffffffffu;
+      s.kp.delta[i] = i < np ? key_tab[1 + np + i] : 0u;
+    }
+    key_tab = nullptr;
+  }
   s.key_tab = key_tab;
   s.pay_tab = pay_tab;
   s.kdiv = kdiv ? kdiv : 1;
@@ -452,7 +491,7 @@ extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, 
     smx_set_error("smx_gen_draw: %llu records in one call exceed 2^32", (unsigned long long)n);
     return -1;
   }
-  if (key_mode < K_NONE || key_mode > K_FROM_J || pay_mode < P_NONE || pay_mode > P_FROM_J) {
+  if (key_mode < K_NONE || key_mode > K_PIECES || pay_mode < P_NONE || pay_mode > P_FROM_J) {
     smx_set_error("smx_gen_draw: bad key/payload mode %d/%d", key_mode, pay_mode);
     return -1;
   }
@@ -466,6 +505,7 @@ extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, 
   SMX_GEN(K_NONE, P_NONE) SMX_GEN(K_NONE, P_FROM_VALUE) SMX_GEN(K_NONE, P_FROM_J)
   SMX_GEN(K_FROM_VALUE, P_NONE) SMX_GEN(K_FROM_VALUE, P_FROM_VALUE) SMX_GEN(K_FROM_VALUE, P_FROM_J)
   SMX_GEN(K_FROM_J, P_NONE) SMX_GEN(K_FROM_J, P_FROM_VALUE) SMX_GEN(K_FROM_J, P_FROM_J)
+  SMX_GEN(K_PIECES, P_FROM_J)
 #undef SMX_GEN
   return -1;
 }

@@ -912,11 +912,33 @@ class Cluster:
              _ptr(gv_tab), stream)
         return key_tab, gv_tab, rk, nd
 
+    @staticmethod
+    def _key_pieces(tr, all_rank, all_node, vbase, lut_base, max_pieces=8):
+        """The distributed call's key table as pieces key = value + delta
+        (one per run of consecutive nodes on one source rank), or None when
+        it has more than max_pieces pieces (smx_gen_draw key_mode 3)."""
+        r = np.asarray(all_rank, dtype=np.int64)
+        nd = np.asarray(all_node, dtype=np.int64)
+        if len(r) == 0:
+            return None
+        brk = np.flatnonzero((r[1:] != r[:-1]) | (nd[1:] != nd[:-1] + 1)) + 1
+        starts = np.concatenate([[0], brk])
+        if len(starts) > max_pieces:
+            return None
+        keys0 = np.where(r[starts] == tr, nd[starts],
+                         TMP_KEY | (lut_base + np.asarray(vbase, dtype=np.int64)[r[starts]] + nd[starts]))
+        if (r[starts] != tr).any() and int((lut_base + np.asarray(vbase, dtype=np.int64)[r] + nd).max()) >= TMP_KEY:
+            return None
+        delta = (keys0 - starts) & 0xFFFFFFFF
+        return np.concatenate([[len(starts)], starts, delta]).astype(np.uint32)
+
     def _dist_target(self, st, key, tr, tg, k_in, total, all_rank, all_node, vbase, seg_words,
                      total_words, syn, port, group, ranks_sorted):
         dev, sk = st.device, st.stream
         lut_base = st.lut.n
-        key_tab, gv_all, rk, nd = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)
+        pieces = self._key_pieces(tr, all_rank, all_node, vbase, lut_base)
+        if pieces is None:
+            key_tab = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)[0]
         vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
         cls = self._syn_class(st, syn, port)
         if cls is None:
@@ -930,7 +952,8 @@ class Cluster:
         vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
         cur = np.zeros(1, dtype=np.uint64)
         ev0 = self._event(st) if self.prof is not None else None
-        call("smx_gen_draw", key[0], key[1], 0, total, n, 1, 2, _ptr(key_tab), _ptr(pay_tab), k_in,
+        kmode, ktab = (1, _ptr(key_tab)) if pieces is None else (3, pieces.ctypes.data)
+        call("smx_gen_draw", key[0], key[1], 0, total, n, kmode, 2, ktab, _ptr(pay_tab), k_in,
              _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits), 0, vbits.numel(), 1, lut_base, int(vbase[tr]),
              cur.ctypes.data, sk)
         if self.prof is not None:

@@ -939,7 +939,21 @@ class Cluster:
         pieces = self._key_pieces(tr, all_rank, all_node, vbase, lut_base)
         if pieces is None:
             key_tab = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)[0]
-        vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
+        n = k_in * len(tg)
+        # used source values (images to create, present source ranks).  With
+        # piecewise keys the draw does not mark them: an early-exit replay of
+        # the same stream (what every source rank runs anyway) yields the same
+        # bitmap for a fraction of the draws; local values only need presence.
+        mark = pieces is None
+        if mark:
+            vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
+        elif bool((np.asarray(all_rank) != tr).any()):
+            vbits = self._dist_replay(dev, key, tr, total, all_rank, all_node, vbase, total_words, n)
+        else:
+            vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
+            if n and total:
+                b = int(vbase[tr])
+                vbits[b >> 5: (b >> 5) + 1] |= int(np.uint32(1 << (b & 31)).view(np.int32))
         cls = self._syn_class(st, syn, port)
         if cls is None:
             self._make_wide(st)
@@ -947,15 +961,14 @@ class Cluster:
         pay_tab = torch.empty(len(tg), dtype=torch.int32, device=dev)
         call("smx_pay_table", _ptr(tgt), len(tg), _ptr(st.node2row.t), st.node2row.n,
              0 if cls is None else cls, _ptr(pay_tab), sk)
-        n = k_in * len(tg)
         base = st.reserve_records(n)
         vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
         cur = np.zeros(1, dtype=np.uint64)
         ev0 = self._event(st) if self.prof is not None else None
         kmode, ktab = (1, _ptr(key_tab)) if pieces is None else (3, pieces.ctypes.data)
         call("smx_gen_draw", key[0], key[1], 0, total, n, kmode, 2, ktab, _ptr(pay_tab), k_in,
-             _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits), 0, vbits.numel(), 1, lut_base, int(vbase[tr]),
-             cur.ctypes.data, sk)
+             _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits) if mark else 0, 0, vbits.numel(), 1, lut_base,
+             int(vbase[tr]), cur.ctypes.data, sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
         if st.wide:

@@ -505,8 +505,9 @@ extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, 
   SMX_GEN(K_NONE, P_NONE) SMX_GEN(K_NONE, P_FROM_VALUE) SMX_GEN(K_NONE, P_FROM_J)
   SMX_GEN(K_FROM_VALUE, P_NONE) SMX_GEN(K_FROM_VALUE, P_FROM_VALUE) SMX_GEN(K_FROM_VALUE, P_FROM_J)
   SMX_GEN(K_FROM_J, P_NONE) SMX_GEN(K_FROM_J, P_FROM_VALUE) SMX_GEN(K_FROM_J, P_FROM_J)
-  SMX_GEN(K_PIECES, P_FROM_J)
+  SMX_GEN(K_PIECES, P_NONE) SMX_GEN(K_PIECES, P_FROM_VALUE) SMX_GEN(K_PIECES, P_FROM_J)
 #undef SMX_GEN
+  smx_set_error("smx_gen_draw: unsupported key/payload mode %d/%d", key_mode, pay_mode);
   return -1;
 }
 

@@ -913,47 +913,92 @@ class Cluster:
         return key_tab, gv_tab, rk, nd
 
     @staticmethod
-    def _key_pieces(tr, all_rank, all_node, vbase, lut_base, max_pieces=8):
-        """The distributed call's key table as pieces key = value + delta
-        (one per run of consecutive nodes on one source rank), or None when
-        it has more than max_pieces pieces (smx_gen_draw key_mode 3)."""
+    def _pieces_of(all_rank, all_node, max_pieces=8):
+        """Runs of consecutive nodes on one source rank: (starts, ranks, first
+        nodes), or None beyond max_pieces runs."""
         r = np.asarray(all_rank, dtype=np.int64)
         nd = np.asarray(all_node, dtype=np.int64)
         if len(r) == 0:
             return None
         brk = np.flatnonzero((r[1:] != r[:-1]) | (nd[1:] != nd[:-1] + 1)) + 1
-        starts = np.concatenate([[0], brk])
+        starts = np.concatenate([[0], brk]).astype(np.int64)
         if len(starts) > max_pieces:
             return None
-        keys0 = np.where(r[starts] == tr, nd[starts],
-                         TMP_KEY | (lut_base + np.asarray(vbase, dtype=np.int64)[r[starts]] + nd[starts]))
-        if (r[starts] != tr).any() and int((lut_base + np.asarray(vbase, dtype=np.int64)[r] + nd).max()) >= TMP_KEY:
-            return None
-        delta = (keys0 - starts) & 0xFFFFFFFF
+        return starts, r[starts], nd[starts]
+
+    @staticmethod
+    def _pack_pieces(starts, keys0):
+        delta = (np.asarray(keys0, dtype=np.int64) - starts) & 0xFFFFFFFF
         return np.concatenate([[len(starts)], starts, delta]).astype(np.uint32)
+
+    def _final_pieces(self, st, tr, group, runs, total, present):
+        """Key pieces with final source rows (local node or image id) when
+        every remote run's images are consecutive; None otherwise."""
+        starts, rks, nds = runs
+        ends = np.append(starts[1:], total)
+        keys0 = np.zeros(len(starts), dtype=np.int64)
+        checks = []
+        for i, (s0, r, nd0) in enumerate(zip(starts, rks, nds)):
+            r, nd0, ln = int(r), int(nd0), int(ends[i] - s0)
+            if r == tr:
+                keys0[i] = nd0
+                continue
+            if r not in present:
+                continue  # no draw falls in this run
+            img = st.maps[(int(group), r)].img_of.t[nd0: nd0 + ln]
+            ar = torch.arange(ln, dtype=img.dtype, device=img.device)
+            checks.append((i, img[0:1], ((img - img[0]) != ar).any().reshape(1)))
+        if checks:
+            first = torch.cat([c[1] for c in checks]).cpu().numpy()
+            bad = torch.cat([c[2] for c in checks]).cpu().numpy()
+            if bad.any() or (first < 0).any():
+                return None
+            for (i, _, _), f in zip(checks, first):
+                keys0[i] = int(f)
+        return self._pack_pieces(starts, keys0)
 
     def _dist_target(self, st, key, tr, tg, k_in, total, all_rank, all_node, vbase, seg_words,
                      total_words, syn, port, group, ranks_sorted):
         dev, sk = st.device, st.stream
         lut_base = st.lut.n
-        pieces = self._key_pieces(tr, all_rank, all_node, vbase, lut_base)
-        if pieces is None:
-            key_tab = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)[0]
         n = k_in * len(tg)
-        # used source values (images to create, present source ranks).  With
-        # piecewise keys the draw does not mark them: an early-exit replay of
-        # the same stream (what every source rank runs anyway) yields the same
-        # bitmap for a fraction of the draws; local values only need presence.
-        mark = pieces is None
-        if mark:
+        runs = self._pieces_of(all_rank, all_node)
+        remote = bool((np.asarray(all_rank) != tr).any())
+        if runs is None:
+            # general table: keys gathered from key_tab, used values marked by the draw
+            key_tab = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)[0]
             vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
-        elif bool((np.asarray(all_rank) != tr).any()):
+        elif remote:
+            # used source values from the early-exit replay of the same stream (what
+            # every source rank runs anyway), so images exist before the draw
             vbits = self._dist_replay(dev, key, tr, total, all_rank, all_node, vbase, total_words, n)
         else:
             vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
             if n and total:
                 b = int(vbase[tr])
                 vbits[b >> 5: (b >> 5) + 1] |= int(np.uint32(1 << (b & 31)).view(np.int32))
+
+        def assign(present):
+            segs = []
+            for r in ranks_sorted:
+                sw0, snw = seg_words[r]
+                m = None
+                if r != tr and r in present:
+                    m = st.map_for(group, r)
+                    m.ensure(snw * 32)
+                segs.append((sw0, snw, m))
+            self._assign(st, vbits, segs)
+
+        pieces, tmp_keys, present = None, True, None
+        if runs is not None:
+            present = self._present_ranks(vbits, ranks_sorted, seg_words)
+            assign(present)
+            pieces = self._final_pieces(st, tr, group, runs, total, present)
+            tmp_keys = pieces is None
+            if pieces is None:  # images not consecutive: temporary keys resolved through the LUT
+                starts, rks, nds = runs
+                keys0 = np.where(rks == tr, nds, TMP_KEY | (lut_base + np.asarray(vbase, np.int64)[rks] + nds))
+                pieces = self._pack_pieces(starts, keys0)
         cls = self._syn_class(st, syn, port)
         if cls is None:
             self._make_wide(st)
@@ -965,6 +1010,7 @@ class Cluster:
         vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
         cur = np.zeros(1, dtype=np.uint64)
         ev0 = self._event(st) if self.prof is not None else None
+        mark = runs is None
         kmode, ktab = (1, _ptr(key_tab)) if pieces is None else (3, pieces.ctypes.data)
         call("smx_gen_draw", key[0], key[1], 0, total, n, kmode, 2, ktab, _ptr(pay_tab), k_in,
              _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits) if mark else 0, 0, vbits.numel(), 1, lut_base,
@@ -974,25 +1020,19 @@ class Cluster:
         if st.wide:
             self._write_syn(st, syn, port, base, n, None)
         st.commit_records(n)
-        present = self._present_ranks(vbits, ranks_sorted, seg_words)
-        segs = []
-        for r in ranks_sorted:
-            sw0, snw = seg_words[r]
-            m = None
-            if r != tr and r in present:
-                m = st.map_for(group, r)
-                m.ensure(snw * 32)
-            segs.append((sw0, snw, m))
-        self._assign(st, vbits, segs)
-        # LUT over the concatenated value space: lut[base + gv] = img_of[rank][value]
-        st.lut.reserve(lut_base + total_words * 32)
-        for r in present:
-            if r == tr:
-                continue
-            sw0, snw = seg_words[r]
-            m = st.maps[(int(group), r)]
-            st.lut.t[lut_base + sw0 * 32: lut_base + (sw0 + snw) * 32].copy_(m.img_of.t[: snw * 32])
-        st.lut.n = lut_base + total_words * 32
+        if present is None:
+            present = self._present_ranks(vbits, ranks_sorted, seg_words)
+            assign(present)
+        if tmp_keys:
+            # LUT over the concatenated value space: lut[base + gv] = img_of[rank][value]
+            st.lut.reserve(lut_base + total_words * 32)
+            for r in present:
+                if r == tr:
+                    continue
+                sw0, snw = seg_words[r]
+                m = st.maps[(int(group), r)]
+                st.lut.t[lut_base + sw0 * 32: lut_base + (sw0 + snw) * 32].copy_(m.img_of.t[: snw * 32])
+            st.lut.n = lut_base + total_words * 32
         return vbits, present
 
     def _dist_replay(self, dev, key, tr, total, all_rank, all_node, vbase, total_words, n):
@@ -1000,19 +1040,30 @@ class Cluster:
         (compute only, no communication).  Coupon-collector early exit: the
         draws are replayed in growing pieces and the replay stops once every
         distinct source value is marked -- no later draw can add a bit, so the
-        bitmap equals the full replay's (SURVEY §7 hard part 6)."""
+        bitmap equals the full replay's (SURVEY §7 hard part 6).  The first
+        piece is sized for coupon collection (V (ln V + 6) draws for V distinct
+        values), so a full-coverage call needs one check."""
         stream = torch.cuda.current_stream(dev).cuda_stream
-        _, gv_all, _, _ = self._dist_tables(dev, stream, tr, total, all_rank, all_node, vbase, 0)
+        runs = self._pieces_of(all_rank, all_node)
+        if runs is None:
+            _, gv_all, _, _ = self._dist_tables(dev, stream, tr, total, all_rank, all_node, vbase, 0)
+        else:  # mark through keys TMP | gv (piecewise affine): no table
+            starts, rks, nds = runs
+            gvp = self._pack_pieces(starts, TMP_KEY | (np.asarray(vbase, np.int64)[rks] + nds))
         vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
         n_distinct = self._n_distinct_gv(all_rank, all_node, vbase, total_words)
         excl = torch.empty(vbits.numel() + 1, dtype=torch.int64, device=dev)
         cur = np.zeros(1, dtype=np.uint64)
         u0, done = 0, 0
-        piece = max(16 * total, 1 << 22)
+        piece = max(int(n_distinct * (math.log(max(n_distinct, 2)) + 6.0)), 1 << 20)
         while done < n:
             k = min(piece, n - done)
-            call("smx_gen_draw", key[0], key[1], u0, total, k, 1, 0, 0, 0, 1, 0, 0, _ptr(vbits), _ptr(gv_all),
-                 vbits.numel(), 0, 0, 0, cur.ctypes.data, stream)
+            if runs is None:
+                call("smx_gen_draw", key[0], key[1], u0, total, k, 1, 0, 0, 0, 1, 0, 0, _ptr(vbits), _ptr(gv_all),
+                     vbits.numel(), 0, 0, 0, cur.ctypes.data, stream)
+            else:
+                call("smx_gen_draw", key[0], key[1], u0, total, k, 3, 0, gvp.ctypes.data, 0, 1, 0, 0, _ptr(vbits),
+                     0, vbits.numel(), 1, 0, 0xFFFFFFFF, cur.ctypes.data, stream)
             u0 = int(cur[0])
             done += k
             if done < n:

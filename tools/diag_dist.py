@@ -29,5 +29,14 @@ for rep in range(int(os.environ.get("REPS", "3"))):
     print(f"rank {rank} rep {rep}: build {1e3 * (t1 - t0):.1f} prepare {1e3 * (t2 - t1):.1f} "
           f"gen {c.kernel_ms('gen'):.1f} sort {c.kernel_ms('sort'):.1f} records {st.n_records} nodes {st.n_nodes} "
           f"timers { {k: round(v * 1e3, 1) for k, v in c.timers.as_dict().items()} }", flush=True)
+    from paper_2512_09502_b200 import _lib
+    if _lib.TIMELINE is not None:
+        tl = _lib.TIMELINE
+        if rank == 0 and rep == int(os.environ.get("REPS", "3")) - 1:
+            ref = tl[0]
+            for i, (name, h0, h1, e) in enumerate(tl):
+                gpu = ref[3].elapsed_time(e)
+                print(f"    {name:24s} host {1e3 * (h0 - ref[1]):8.1f}->{1e3 * (h1 - ref[1]):8.1f} ms   gpu done {gpu:8.1f} ms")
+        tl.clear()
     del c
 dist.destroy_process_group()

@@ -962,8 +962,8 @@ class Cluster:
         dev, sk = st.device, st.stream
         lut_base = st.lut.n
         n = k_in * len(tg)
-        runs = self._pieces_of(all_rank, all_node)
-        remote = bool((np.asarray(all_rank) != tr).any())
+        runs = self._runs(all_rank, all_node)
+        remote = bool((runs[1] != tr).any()) if runs is not None else bool((np.asarray(all_rank) != tr).any())
         if runs is None:
             # general table: keys gathered from key_tab, used values marked by the draw
             key_tab = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)[0]
@@ -1044,7 +1044,7 @@ class Cluster:
         piece is sized for coupon collection (V (ln V + 6) draws for V distinct
         values), so a full-coverage call needs one check."""
         stream = torch.cuda.current_stream(dev).cuda_stream
-        runs = self._pieces_of(all_rank, all_node)
+        runs = self._runs(all_rank, all_node)
         if runs is None:
             _, gv_all, _, _ = self._dist_tables(dev, stream, tr, total, all_rank, all_node, vbase, 0)
         else:  # mark through keys TMP | gv (piecewise affine): no table
@@ -1073,11 +1073,33 @@ class Cluster:
                 piece *= 2
         return vbits
 
+    def _runs(self, all_rank, all_node):
+        """_pieces_of for the current distributed call (computed once per call)."""
+        cache = getattr(self, "_runs_cache", None)
+        if cache is not None and cache[0] == self.dist_ctr:
+            return cache[1]
+        runs = self._pieces_of(all_rank, all_node)
+        self._runs_cache = (self.dist_ctr, runs)
+        return runs
+
     def _n_distinct_gv(self, all_rank, all_node, vbase, total_words):
         """Distinct (rank, node) source values of a distributed call (cached per call)."""
         cache = getattr(self, "_gv_cache", None)
         if cache is not None and cache[0] == self.dist_ctr:
             return cache[1]
+        runs = self._runs(all_rank, all_node)
+        if runs is not None:  # union of the runs' node intervals per rank
+            starts, rks, nds = runs
+            lens = np.diff(np.append(starts, len(all_node)))
+            nd = 0
+            for r in np.unique(rks):
+                iv = sorted((int(a), int(a) + int(b)) for a, b in zip(nds[rks == r], lens[rks == r]))
+                hi = -1
+                for a, b in iv:
+                    nd += max(0, b - max(a, hi))
+                    hi = max(hi, b)
+            self._gv_cache = (self.dist_ctr, nd)
+            return nd
         mask = np.zeros(max(total_words, 1) * 32, dtype=bool)
         mask[vbase[all_rank].astype(np.int64) + all_node] = True
         nd = int(mask.sum())

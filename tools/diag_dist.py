@@ -14,6 +14,11 @@ torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
 dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
 P = models.BalancedParams(neurons_per_rank=100_000, k_exc=9000, k_inh=2250)
 cfg = api.SimConfig(n_ranks=world, comm_mode="collective", seed=12345)
+SAMP = None
+if os.environ.get("SAMPLE") and rank == 0:
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from stall_sampler import Sampler
+    SAMP = Sampler(period=0.0005).start()
 for rep in range(int(os.environ.get("REPS", "3"))):
     dist.barrier()
     torch.cuda.synchronize()
@@ -26,6 +31,9 @@ for rep in range(int(os.environ.get("REPS", "3"))):
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     st = c.ranks[rank]
+    if SAMP is not None and rep == int(os.environ.get("REPS", "3")) - 1:
+        print("-- build"); SAMP.summarise(t0, t1, top=int(os.environ.get("TOP", "25")))
+        print("-- prepare"); SAMP.summarise(t1, t2, top=int(os.environ.get("TOP", "25")))
     print(f"rank {rank} rep {rep}: build {1e3 * (t1 - t0):.1f} prepare {1e3 * (t2 - t1):.1f} "
           f"gen {c.kernel_ms('gen'):.1f} sort {c.kernel_ms('sort'):.1f} records {st.n_records} nodes {st.n_nodes} "
           f"timers { {k: round(v * 1e3, 1) for k, v in c.timers.as_dict().items()} }", flush=True)

@@ -51,6 +51,17 @@ def parse():
     return ap.parse_args()
 
 
+def traffic_per_synapse():
+    """DRAM bytes (read + write) per synapse of the generation + sort kernels,
+    from the committed ncu capture of one C3 construction (profiles/r1b)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1b", "traffic.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["bytes_per_synapse"]), "profiles/r1b/traffic.json"
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -244,6 +255,8 @@ def run_ours(args):
     peak, peak_kind = peaks()
     k_ms = float(np.mean(gen_ms)) + float(np.mean(sort_ms))
     achieved = BYTES_PER_SYN * syn_per_rank / (k_ms * 1e-3) / 1e9
+    tps, traffic_src = traffic_per_synapse()
+    traffic = tps * syn_per_rank if tps is not None else None  # bytes per construction, like achieved
     if rank != 0:
         return
     line = {
@@ -260,7 +273,8 @@ def run_ours(args):
         "e2e": {"value": e2e, "unit": "synapses/s", "h2d_bytes_per_step": int(np.mean(h2d)),
                 "d2h_bytes_per_step": 8},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind,
                      "kernel": "generation (smx_gen_draw) + stable sort (smx_sort_records)",
                      "kernel_ms": k_ms, "bytes_per_synapse": BYTES_PER_SYN},
         "clocks": clocks,

@@ -87,6 +87,12 @@ int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u32_cursor, uint64_t ex, uin
                  uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab, uint32_t used_bits_words,
                  int mark_from_key, uint32_t tmp_base, uint32_t local_bit, uint64_t* cursor_out_host,
                  void* stream);
+/* counts[s] += number of keys in [lo[s], hi[s]) for m <= 16 disjoint ranges;
+ * ranges_host = {m, lo[m], hi[m]}.  Records per source rank of one
+ * distributed call, for the modeled-byte accounting (sm/construction.py:689-703,
+ * 597-617). */
+int smx_count_ranges(const uint32_t* keys, uint64_t n, const uint32_t* ranges_host, unsigned long long* counts,
+                     void* stream);
 /* one_to_one / assigned (mode 0), all_to_all (mode 1): sm/construction.py:415-419 */
 int smx_gen_pairs(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab, const uint32_t* pay_tab,
                   uint32_t* keys, uint32_t* vals, void* stream);

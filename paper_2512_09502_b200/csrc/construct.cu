@@ -18,6 +18,7 @@
 // (int32, -1 = no image) over the source rank's node values plus a presence
 // bitmap; the sorted (R, L) pair of the reference is the compaction of that
 // bitmap.  Lookups are O(1) gathers instead of searchsorted.
+#include <algorithm>
 #include <cstdlib>
 #include "draw_host.cuh"
 
@@ -721,5 +722,82 @@ extern "C" int smx_autapse_fix(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t n
   cudaFreeAsync(idx_a, st);
   cudaFreeAsync(idx_b, st);
   cudaFreeAsync(draws, st);
+  return 0;
+}
+
+// --- per-range record counts (modeled-byte accounting) ------------------------
+// counts[s] += #{i : lo[s] <= keys[i] < hi[s]} for up to 16 disjoint ranges:
+// the records of one distributed call per source rank (the reference appends
+// one batch per source rank, sm/construction.py:689-703).
+constexpr int MAX_COUNT_RANGES = 16;
+struct CountRanges {
+  uint32_t m;
+  uint32_t lo[MAX_COUNT_RANGES], hi[MAX_COUNT_RANGES];
+};
+
+template <int M>
+__global__ void __launch_bounds__(256) count_ranges_kernel(const uint32_t* keys, uint64_t n, CountRanges R,
+                                                           unsigned long long* counts) {
+  uint32_t c[M];
+#pragma unroll
+  for (int s = 0; s < M; ++s) c[s] = 0;
+  const uint64_t n4 = n / 4;
+  const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4 + 1; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t kk[4];
+    int m = 4;
+    if (i < n4) {
+      const uint4 q = k4[i];
+      kk[0] = q.x; kk[1] = q.y; kk[2] = q.z; kk[3] = q.w;
+    } else {
+      m = (int)(n - 4 * n4);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) kk[j] = j < m ? keys[4 * n4 + j] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j >= m) break;
+#pragma unroll
+      for (int s = 0; s < M; ++s) c[s] += (kk[j] - R.lo[s] < R.hi[s] - R.lo[s]) ? 1u : 0u;  // lo <= k < hi
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < M; ++s) {
+    uint32_t x = c[s];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(counts + s, (unsigned long long)x);
+  }
+}
+
+template <int M>
+static void launch_count_ranges(const uint32_t* keys, uint64_t n, const CountRanges& R, unsigned long long* counts,
+                                cudaStream_t st) {
+  const unsigned grid = (unsigned)std::min<uint64_t>((n / 4 + 256) / 256, 148 * 8);
+  smx_count_launch(); count_ranges_kernel<M><<<grid, 256, 0, st>>>(keys, n, R, counts);
+}
+
+// ranges_host = {m, lo[m], hi[m]}; counts (device, m u64) are accumulated.
+extern "C" int smx_count_ranges(const uint32_t* keys, uint64_t n, const uint32_t* ranges_host,
+                                unsigned long long* counts, void* stream) {
+  CountRanges R{};
+  R.m = ranges_host[0];
+  if (R.m > (uint32_t)MAX_COUNT_RANGES) {
+    smx_set_error("smx_count_ranges: %u ranges (at most %d)", R.m, MAX_COUNT_RANGES);
+    return -1;
+  }
+  for (uint32_t s = 0; s < R.m; ++s) {
+    R.lo[s] = ranges_host[1 + s];
+    R.hi[s] = ranges_host[1 + R.m + s];
+  }
+  if (n == 0 || R.m == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (R.m) {  // pad to the next instantiated width (empty ranges count nothing)
+    case 1: case 2: launch_count_ranges<2>(keys, n, R, counts, st); break;
+    case 3: case 4: launch_count_ranges<4>(keys, n, R, counts, st); break;
+    case 5: case 6: case 7: case 8: launch_count_ranges<8>(keys, n, R, counts, st); break;
+    default: launch_count_ranges<16>(keys, n, R, counts, st); break;
+  }
+  SMX_LAUNCH_CHECK();
   return 0;
 }

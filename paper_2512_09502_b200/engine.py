@@ -28,6 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .memory import RankMemory
 from ._lib import call
 from .api import (POINT_TO_POINT, ConnSpec, ConsistencyError, DelayRangeError, LifParams,
                   ProtocolError, Raster, SimConfig, SynSpec, canonical_bytes, stream_key)
@@ -75,6 +76,29 @@ def _record_stream(obj, stream, depth: int = 0) -> None:
     elif depth < 3 and isinstance(obj, (list, tuple)):
         for v in obj:
             _record_stream(v, stream, depth + 1)
+
+
+def _popcount_dev(b):
+    """Set bits of an int32-word bitmap as a 0-dim device tensor (no sync)."""
+    excl = torch.zeros(b.numel() + 1, dtype=torch.int64, device=b.device)
+    if b.numel():
+        call("smx_bits_prefix", _ptr(b), b.numel(), _ptr(excl), torch.cuda.current_stream(b.device).cuda_stream)
+    return excl[-1]
+
+
+def _popcounts(bitmaps) -> list:
+    """Set bits of each bitmap (int32 words), one host synchronisation."""
+    outs = []
+    for b in bitmaps:
+        excl = torch.empty(b.numel() + 1, dtype=torch.int64, device=b.device)
+        if b.numel():
+            call("smx_bits_prefix", _ptr(b), b.numel(), _ptr(excl), torch.cuda.current_stream(b.device).cuda_stream)
+        else:
+            excl.zero_()
+        outs.append(excl[-1:])
+    if not outs:
+        return []
+    return [int(x) for x in torch.cat([o.to(outs[0].device) for o in outs]).cpu().numpy()]
 
 
 def _all_distinct(a: np.ndarray) -> bool:
@@ -212,6 +236,7 @@ class _Rank:
         self.rosters: dict[tuple, _Bits] = {}
         self.devices: list[dict] = []
         self.used_classes: set[int] = set()
+        self.mem: RankMemory | None = None   # modeled-byte arenas (memory.py)
         self.prepared = False
 
     @property
@@ -278,6 +303,8 @@ class Cluster:
         devices = [torch.device(d) for d in devices]
         self.ranks: dict[int, _Rank] = {
             r: _Rank(r, devices[i % len(devices)]) for i, r in enumerate(self.local)}
+        for st in self.ranks.values():
+            st.mem = RankMemory(cfg.opt_level, cfg.block_size)
         for d in {st.device for st in self.ranks.values()}:
             with torch.cuda.device(d):
                 torch.cuda.current_stream(d)  # make sure the context exists
@@ -386,6 +413,7 @@ class Cluster:
             if not self.is_local(rank):
                 return range(start, start + n)
             st = self.ranks[rank]
+            st.mem.later("neurons", n)
             dev = st.device
             if v_init is None:
                 v = torch.full((n,), float(params.v_rest), dtype=torch.float64, device=dev)
@@ -653,6 +681,7 @@ class Cluster:
                                   self._key(("syn-local", rank, ctr)),
                                   autapse_fix=not conn.allow_autapses and conn.rule in ("fixed_indegree",
                                                                                        "fixed_total"))
+        st.mem.later("store_append", n)
         return n
 
     def connect_remote(self, src_rank: int, sources, tgt_rank: int, targets, conn: ConnSpec,
@@ -731,6 +760,7 @@ class Cluster:
             st.lut.reserve(lut_base + n_src)
             call("smx_gather_lut", _ptr(src_dev), n_src, _ptr(m.img_of.t), _ptr(st.lut.t[lut_base:]), st.stream)
             st.lut.n = lut_base + n_src
+            st.mem.later("remote_batch", n_src, (int(group), sr), _popcount_dev(m.present.view()), n_rec)
         # source side
         if group == POINT_TO_POINT:
             if self.is_local(sr):
@@ -745,6 +775,7 @@ class Cluster:
                         pb = self._replay_positions(ss, conn, n_src, n_tgt, k_src)
                 mir = ss.mirrors.setdefault(tr, _Bits(dev)).ensure(span)
                 call("smx_mark_values", _ptr(pb), _ptr(src_dev), n_src, _ptr(mir.t), ss.stream)
+                ss.mem.later("mirror_size", tr, _popcount_dev(mir.t))
         else:
             for mbr in members:
                 if self.is_local(mbr):
@@ -885,6 +916,7 @@ class Cluster:
                         mir = ss.mirrors.setdefault(tr, _Bits(ss.device)).ensure(span[sr])
                         seg = vb[w0: w0 + nw].to(ss.device)
                         call("smx_bits_or", _ptr(mir.t), _ptr(seg), nw, ss.stream)
+                        ss.mem.later("mirror_size", tr, _popcount_dev(mir.t))
                 else:
                     for mbr in members:
                         if self.is_local(mbr):
@@ -1033,7 +1065,58 @@ class Cluster:
                 m = st.maps[(int(group), r)]
                 st.lut.t[lut_base + sw0 * 32: lut_base + (sw0 + snw) * 32].copy_(m.img_of.t[: snw * 32])
             st.lut.n = lut_base + total_words * 32
+        self._dist_accounting(st, tr, group, n, base, present, runs, pieces, tmp_keys, lut_base, vbase,
+                              seg_words)
         return vbits, present
+
+    def _dist_accounting(self, st, tr, group, n, base, present, runs, pieces, tmp_keys, lut_base, vbase,
+                         seg_words):
+        """Modeled bytes of one distributed call on its target rank: the
+        reference appends one batch per source rank present, ascending, the
+        remote ones through remote_connect (sm/construction.py:689-703)."""
+        remote = [r for r in present if r != tr]
+        if not remote:
+            st.mem.later("store_append", n)
+            return
+        # records per source rank: disjoint key ranges of the call's records,
+        # counted on the preparation side stream (memory-bound, it overlaps the
+        # next call's compute-bound draws)
+        los, his, owner = [], [], []
+        if runs is not None:
+            starts, rks, _ = runs
+            m = int(pieces[0])
+            lens = np.diff(np.append(starts, self._runs_total))
+            for i in range(m):
+                k0 = (int(pieces[1 + i]) + int(pieces[1 + m + i])) & 0xFFFFFFFF
+                los.append(k0)
+                his.append(k0 + int(lens[i]))
+                owner.append(int(rks[i]))
+        else:
+            los.append(0)
+            his.append(TMP_KEY)
+            owner.append(tr)
+            for r in remote:
+                sw0, snw = seg_words[r]
+                los.append(TMP_KEY | (lut_base + sw0 * 32))
+                his.append(TMP_KEY | (lut_base + (sw0 + snw) * 32))
+                owner.append(r)
+        rng = np.array([len(los)] + los + his, dtype=np.uint64).astype(np.uint32)
+        main = torch.cuda.current_stream(st.device)
+        side = _prep_stream(st.device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            cnt = torch.zeros(len(los), dtype=torch.int64, device=st.device)
+            call("smx_count_ranges", _ptr(st.keys.t[base:]), n, rng.ctypes.data, _ptr(cnt), side.cuda_stream)
+            idx = {r: [i for i, o in enumerate(owner) if o == r] for r in present}
+            per = {r: cnt[idx[r]].sum() if idx[r] else cnt[:0].sum() for r in present}
+        # (resolved in prepare on this same side stream; the keys stay untouched
+        # until the sort, which only reads them)
+        for r in present:
+            if r == tr:
+                st.mem.later("store_append", per[r])
+            else:
+                st.mem.later("remote_batch", per[r], (int(group), r),
+                             _popcount_dev(st.maps[(int(group), r)].present.view()), per[r])
 
     def _dist_replay(self, dev, key, tr, total, all_rank, all_node, vbase, total_words, n):
         """Source-side replay of a remote target's draws: used-value bitmap only
@@ -1075,6 +1158,7 @@ class Cluster:
 
     def _runs(self, all_rank, all_node):
         """_pieces_of for the current distributed call (computed once per call)."""
+        self._runs_total = len(all_node)
         cache = getattr(self, "_runs_cache", None)
         if cache is not None and cache[0] == self.dist_ctr:
             return cache[1]
@@ -1272,6 +1356,10 @@ class Cluster:
         st.TP = self._routes(st, [(tr, st.mirrors[tr].t) for tr in sorted(st.mirrors)])
         own = [(self.group_slots[g], st.rosters[(g, sr)].t) for (g, sr) in sorted(st.rosters) if sr == st.rank]
         st.GQ = self._routes(st, own)
+        # modeled bytes of prepare (sm/construction.py:763-807)
+        st.mem.resolve()
+        st.mem.prepare(st.N, st.P, st.L, st.n_nodes, {k: int(v.numel()) for k, v in st.H.items()}, st.rank,
+                       {k: int(v.numel()) for k, v in st.S.items()})
         # propagation buffers
         self._alloc_propagation(st)
 
@@ -1637,6 +1725,21 @@ class Cluster:
 
     _recording = False
 
+    def _per_rank(self, fn) -> list:
+        """fn(rank state) for every rank, in rank order; with one process per
+        rank the values are summed over processes (each fills its own)."""
+        vals = [0] * self.n_ranks
+        for r, st in self.ranks.items():
+            vals[r] = int(fn(st))
+        if self.distributed:
+            import torch.distributed as dist
+            dev = next(iter(self.ranks.values())).device
+            t = torch.tensor(vals, dtype=torch.int64,
+                             device=dev if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(t)
+            vals = [int(x) for x in t.cpu().numpy()]
+        return vals
+
     def simulate(self, warmup_ms: float = 0.0, model_ms: float = 0.0, record: bool = True) -> RunReport:
         """sm/engine.py:312-359.  RTF = propagation wall time / model time, the
         wall time bracketed by device synchronisations."""
@@ -1664,14 +1767,16 @@ class Cluster:
         self._check_errors()
         model_s = steps * self.cfg.resolution_ms * 1e-3
         raster = self.merged_raster() if record else None
+        n_neurons = sum(self._per_rank(lambda st: st.n_real))
+        n_synapses = sum(self._per_rank(lambda st: st.n_records))
         return RunReport(
             n_ranks=self.n_ranks, comm_mode=self.cfg.comm_mode, opt_level=self.cfg.opt_level,
             seed=self.cfg.seed, kernel_backend="cuda-sm_100a",
-            n_neurons=sum(st.n_real for st in self.ranks.values()),
-            n_synapses=sum(st.n_records for st in self.ranks.values()),
+            n_neurons=n_neurons, n_synapses=n_synapses,
             timers=self.timers.as_dict(), warmup_s=warm_s, model_time_s=model_s,
             rtf=prop / model_s if model_s > 0 else 0.0,
-            host_peak_bytes=[0] * self.n_ranks, device_peak_bytes=[0] * self.n_ranks,
+            host_peak_bytes=self._per_rank(lambda st: st.mem.host.peak_bytes),
+            device_peak_bytes=self._per_rank(lambda st: st.mem.device.peak_bytes),
             transport_messages=dict(self.messages), transport_bytes=dict(self.bytes),
             n_spike_events=raster.n_events if raster is not None else 0,
             raster_sha256=raster.sha256() if raster is not None else None)

@@ -8,6 +8,8 @@ does not exist on the GPU box); the outputs are committed:
   tests/golden/tables_<name>.npz per-rank construction tables of each
                                  scenario in tests/scenarios.py
   tests/golden/rasters.json      raster SHA-256 / event counts per scenario
+  tests/golden/memory.json       modeled host/device peak bytes per rank after
+                                 prepare, per scenario and optimisation level
 Usage:  python tests/golden/make_golden.py
 """
 from __future__ import annotations
@@ -94,6 +96,28 @@ def gen_tables():
         json.dump(rasters, fh, indent=1, sort_keys=True)
 
 
+def gen_memory():
+    """Arena peaks of the reference (sm/core.py:155-182) for every scenario at
+    optimisation levels 0..3 (placement plans, sm/construction.py:59-71)."""
+    import functools
+    out = {}
+    for name, fn in scenarios.SCENARIOS.items():
+        for level in (0, 1, 2, 3):
+            ns = ref_namespace()
+            ns.SimConfig = functools.partial(sm.SimConfig, opt_level=level)
+            c, _ = fn(ns)
+            c.prepare()
+            out[f"{name}/L{level}"] = dict(host=[int(st.host.peak_bytes) for st in c.ranks],
+                                          device=[int(st.device.peak_bytes) for st in c.ranks])
+        print(name, out[f"{name}/L2"], file=sys.stderr)
+    with open(os.path.join(HERE, "memory.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
+    if "--memory-only" in sys.argv:
+        gen_memory()
+        sys.exit(0)
     gen_rng()
     gen_tables()
+    gen_memory()

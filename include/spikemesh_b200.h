@@ -93,6 +93,16 @@ int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u32_cursor, uint64_t ex, uin
  * 597-617). */
 int smx_count_ranges(const uint32_t* keys, uint64_t n, const uint32_t* ranges_host, unsigned long long* counts,
                      void* stream);
+/* allow_multapses=False: rows x k values of numpy Generator.choice(n, k,
+ * replace=False), one row per target, back to back from u32 cursor u32_cursor
+ * (sm/core.py:140-141, sm/construction.py:403-404, 680-683). */
+int smx_choice_rows(uint64_t k0, uint64_t k1, uint64_t u32_cursor, uint64_t n, uint64_t k, uint64_t rows,
+                    uint32_t* values, uint64_t* cursor_out_host, void* stream);
+/* records from drawn positions: keys[j] = key_tab ? key_tab[v] : v, vals[j] =
+ * pay_tab[j / kdiv]; optional used-value bits (mark_tab ? mark_tab[v] : v). */
+int smx_records_from_values(const uint32_t* values, uint64_t n, const uint32_t* key_tab, const uint32_t* pay_tab,
+                            uint32_t kdiv, uint32_t* keys, uint32_t* vals, uint32_t* bits,
+                            const uint32_t* mark_tab, void* stream);
 /* one_to_one / assigned (mode 0), all_to_all (mode 1): sm/construction.py:415-419 */
 int smx_gen_pairs(int mode, uint64_t n, uint64_t n_src, const uint32_t* key_tab, const uint32_t* pay_tab,
                   uint32_t* keys, uint32_t* vals, void* stream);

@@ -25,6 +25,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "ziggurat_tables.h"
@@ -111,6 +112,67 @@ int orc_integers(orc_stream *s, int64_t lo, uint64_t ex, int64_t n, int64_t *out
       }
     }
     out[i] = lo + (int64_t)(m >> 32);
+  }
+  return 0;
+}
+
+/* numpy random_bounded_uint64(off=0, rng, mask=0, use_masked=false) for
+ * rng < 2^32: value in [0, rng], Lemire on next_uint32 (rng == 0 consumes
+ * nothing).  Used by Generator.choice(replace=False) and its shuffles. */
+static uint64_t bounded_incl(orc_stream *s, uint64_t rng) {
+  if (rng == 0) return 0;
+  if (rng == 0xFFFFFFFFULL) return orc_next32(s);
+  int64_t v;
+  orc_integers(s, 0, rng + 1, 1, &v);
+  return (uint64_t)v;
+}
+
+/* numpy 2.3.5 Generator.choice(n, size=k, replace=False, shuffle=True),
+ * p=None, integer population (verified against numpy in
+ * tests/test_oracle_rng.py): for n > 10000 and k > n // 50 a tail
+ * Fisher-Yates of arange(n) keeping the last k; otherwise Floyd's algorithm
+ * (values j or j's draw, first sighting wins) followed by a Fisher-Yates
+ * shuffle of the k picks.  All index draws are bounded_incl. */
+int orc_choice(orc_stream *s, int64_t n, int64_t k, int64_t *out) {
+  if (k < 0 || k > n) return -1;
+  if (k == 0) return 0;
+  if (n > 10000 && k > n / 50) {
+    int64_t *data = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    if (!data) return -2;
+    for (int64_t i = 0; i < n; ++i) data[i] = i;
+    const int64_t first = n - k > 1 ? n - k : 1;
+    for (int64_t i = n - 1; i >= first; --i) {
+      const int64_t j = (int64_t)bounded_incl(s, (uint64_t)i);
+      const int64_t t = data[j]; data[j] = data[i]; data[i] = t;
+    }
+    memcpy(out, data + (n - k), sizeof(int64_t) * (size_t)k);
+    free(data);
+    return 0;
+  }
+  uint64_t set_size = (uint64_t)(1.2 * (double)k), mask = set_size;
+  for (int sh = 1; sh < 64; sh <<= 1) mask |= mask >> sh;
+  set_size = mask + 1;
+  uint64_t *hs = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)set_size);
+  if (!hs) return -2;
+  for (uint64_t i = 0; i < set_size; ++i) hs[i] = ~0ULL;
+  for (int64_t j = n - k; j < n; ++j) {
+    const uint64_t val = bounded_incl(s, (uint64_t)j);
+    uint64_t loc = val & mask;
+    while (hs[loc] != ~0ULL && hs[loc] != val) loc = (loc + 1) & mask;
+    if (hs[loc] == ~0ULL) {
+      hs[loc] = val;
+      out[j - n + k] = (int64_t)val;
+    } else {
+      loc = (uint64_t)j & mask;
+      while (hs[loc] != ~0ULL) loc = (loc + 1) & mask;
+      hs[loc] = (uint64_t)j;
+      out[j - n + k] = j;
+    }
+  }
+  free(hs);
+  for (int64_t i = k - 1; i >= 1; --i) {
+    const int64_t j = (int64_t)bounded_incl(s, (uint64_t)i);
+    const int64_t t = out[j]; out[j] = out[i]; out[i] = t;
   }
   return 0;
 }

@@ -48,6 +48,8 @@ def lib():
         L.orc_u32_used.restype = u64
         L.orc_integers.argtypes = [p, i64, u64, i64, p]
         L.orc_integers.restype = ctypes.c_int
+        L.orc_choice.argtypes = [p, i64, i64, p]
+        L.orc_choice.restype = ctypes.c_int
         L.orc_normal.argtypes = [p, ctypes.c_double, ctypes.c_double, i64, p]
         L.orc_uniform.argtypes = [p, ctypes.c_double, ctypes.c_double, i64, p]
         L.orc_poisson.argtypes = [p, ctypes.c_double, ctypes.c_double, i64, p]
@@ -116,6 +118,15 @@ class OracleStream:
             if rc:
                 raise ValueError("bad integer range")
         return int(out[0]) if size is None else out
+
+    def choice_no_replace(self, n: int, k: int) -> np.ndarray:
+        """numpy Generator.choice(n, size=k, replace=False) (sm/core.py:140-141)."""
+        out = np.empty(max(int(k), 0), dtype=np.int64)
+        rc = lib().orc_choice(self._p, int(n), int(k), out.ctypes.data)
+        if rc:
+            raise ValueError("Cannot take a larger sample than population when replace is False"
+                             if rc == -1 else "oracle choice: allocation failed")
+        return out
 
     def normal(self, loc, scale, size=None):
         n = 1 if size is None else int(size)

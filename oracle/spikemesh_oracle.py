@@ -116,9 +116,11 @@ def _syn_draws(syn, n, stream):
 def _positions(conn, n_src, n_tgt, aligned):
     """sm/construction.py:391-407 -- the only consumer of the aligned stream."""
     if conn.rule == "fixed_indegree":
-        if not conn.allow_multapses:
-            raise NotImplementedError("choice_no_replace is outside the oracle's scope")
-        return aligned.integers(0, n_src, size=int(conn.k_in) * n_tgt)
+        k = int(conn.k_in)
+        if not conn.allow_multapses:  # one row per target (sm/construction.py:403-404)
+            rows = [aligned.choice_no_replace(n_src, k) for _ in range(n_tgt)]
+            return np.concatenate(rows).astype(np.int64) if rows else np.empty(0, np.int64)
+        return aligned.integers(0, n_src, size=k * n_tgt)
     if conn.rule == "fixed_total":
         return aligned.integers(0, n_src, size=int(conn.n_total))
     return None
@@ -412,7 +414,11 @@ class OracleCluster:
         for tr, tg in target_pops:
             tr = int(tr)
             tg = np.asarray(tg, np.int64)
-            flat = self._stream(("dist-indegree", call, tr)).integers(0, total, size=k_in * len(tg))
+            stream = self._stream(("dist-indegree", call, tr))
+            if allow_multapses:
+                flat = stream.integers(0, total, size=k_in * len(tg))
+            else:  # sm/construction.py:680-683
+                flat = np.concatenate([stream.choice_no_replace(total, k_in) for _ in tg]).astype(np.int64)
             sig, sv, tv = s_rank[flat], s_node[flat], np.repeat(tg, k_in)
             order = np.lexsort((sv, sig))
             sig, sv, tv = sig[order], sv[order], tv[order]

@@ -801,3 +801,185 @@ extern "C" int smx_count_ranges(const uint32_t* keys, uint64_t n, const uint32_t
   SMX_LAUNCH_CHECK();
   return 0;
 }
+
+// --- choice without replacement (allow_multapses=False) ------------------------
+// numpy 2.3.5 Generator.choice(n, size=k, replace=False), one row per target
+// from one stream (sm/core.py:140-141, sm/construction.py:403-404, 680-683):
+//   n > 10000 and k > n // 50: tail Fisher-Yates of arange(n), keep the last k
+//   otherwise:                 Floyd's algorithm, then a Fisher-Yates shuffle
+// every index draw is numpy's random_bounded_uint64 (Lemire on next_uint32,
+// value in [0, rng], rng == 0 consumes nothing).  The rows form one chain
+// through the stream (each row's length depends on its rejections), so one
+// warp walks the call sequentially: lane 0 draws, the warp clears the hash
+// tables.  A correctness path for the rule, not a throughput path.
+namespace {
+
+struct U32Stream {  // next_uint32 with numpy's low-half-first buffering, from a u32 cursor
+  smx::Key key;
+  uint64_t pos;     // next u32 position
+  uint64_t blk_w[4];
+  uint64_t blk;
+  __device__ void init(smx::Key k, uint64_t p) { key = k; pos = p; blk = 0; }
+  __device__ uint32_t next32() {
+    const uint64_t w = pos >> 1;
+    const uint64_t b = (w >> 2) + 1;
+    if (b != blk) { smx::philox4x64_10(b, key, blk_w); blk = b; }
+    const uint64_t word = blk_w[w & 3];
+    const uint32_t v = (pos & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+    ++pos;
+    return v;
+  }
+  __device__ uint32_t bounded_incl(uint32_t rng) {
+    if (rng == 0) return 0;
+    if (rng == 0xFFFFFFFFu) return next32();
+    const uint32_t ex = rng + 1;
+    uint64_t m = (uint64_t)next32() * ex;
+    uint32_t left = (uint32_t)m;
+    if (left < ex) {
+      const uint32_t thr = (uint32_t)((0x100000000ULL - ex) % ex);
+      while (left < thr) {
+        m = (uint64_t)next32() * ex;
+        left = (uint32_t)m;
+      }
+    }
+    return (uint32_t)(m >> 32);
+  }
+};
+
+constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
+
+__global__ void __launch_bounds__(32) choice_rows_kernel(smx::Key key, uint64_t u0, uint32_t n, uint32_t k,
+                                                         uint64_t rows, uint32_t* out, uint32_t* tab,
+                                                         uint32_t tab_mask, uint64_t* cursor_out) {
+  const int lane = threadIdx.x;
+  U32Stream s;
+  s.init(key, u0);
+  const bool tail = n > 10000u && k > n / 50u;
+  for (uint64_t r = 0; r < rows; ++r) {
+    uint32_t* row = out + r * k;
+    for (uint32_t i = lane; i <= tab_mask; i += 32) tab[i] = EMPTY32;           // hash keys
+    if (tail) for (uint32_t i = lane; i <= tab_mask; i += 32) tab[tab_mask + 1 + i] = 0;  // values
+    __syncwarp();
+    if (lane == 0) {
+      if (tail) {
+        // virtual array data[i] = i, swaps kept in an open-addressing map
+        auto find = [&](uint32_t key_) -> uint32_t {
+          uint32_t loc = (key_ * 2654435761u) & tab_mask;
+          while (tab[loc] != EMPTY32 && tab[loc] != key_) loc = (loc + 1) & tab_mask;
+          return loc;
+        };
+        auto get = [&](uint32_t idx) -> uint32_t {
+          const uint32_t loc = find(idx);
+          return tab[loc] == EMPTY32 ? idx : tab[tab_mask + 1 + loc];
+        };
+        auto put = [&](uint32_t idx, uint32_t val) {
+          const uint32_t loc = find(idx);
+          tab[loc] = idx;
+          tab[tab_mask + 1 + loc] = val;
+        };
+        const uint32_t first = n - k > 1 ? n - k : 1;
+        for (uint32_t i = n - 1; i >= first; --i) {
+          const uint32_t j = s.bounded_incl(i);
+          const uint32_t vi = get(i), vj = get(j);
+          put(j, vi);
+          put(i, vj);
+          if (i == 0) break;
+        }
+        for (uint32_t q = 0; q < k; ++q) row[q] = get(n - k + q);
+      } else {
+        for (uint32_t j = n - k; j < n; ++j) {
+          const uint32_t val = s.bounded_incl(j);
+          uint32_t loc = val & tab_mask;
+          while (tab[loc] != EMPTY32 && tab[loc] != val) loc = (loc + 1) & tab_mask;
+          if (tab[loc] == EMPTY32) {
+            tab[loc] = val;
+            row[j - n + k] = val;
+          } else {
+            loc = j & tab_mask;
+            while (tab[loc] != EMPTY32) loc = (loc + 1) & tab_mask;
+            tab[loc] = j;
+            row[j - n + k] = j;
+          }
+        }
+        for (uint32_t i = k - 1; i >= 1 && k > 1; --i) {
+          const uint32_t j = s.bounded_incl(i);
+          const uint32_t t = row[j];
+          row[j] = row[i];
+          row[i] = t;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && cursor_out) *cursor_out = s.pos;
+}
+
+}  // namespace
+
+// rows x k values (u32) of numpy choice(n, k, replace=False) drawn back to back
+// from u32 cursor u0; *cursor_out_host = u32 cursor after the last row.
+extern "C" int smx_choice_rows(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t n, uint64_t k, uint64_t rows,
+                               uint32_t* out, uint64_t* cursor_out_host, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k > n) {
+    smx_set_error("Cannot take a larger sample than population when replace is False");
+    return -1;
+  }
+  if (n >= 0xFFFFFFFFULL) {
+    smx_set_error("smx_choice_rows: population %llu exceeds 2^32 - 1", (unsigned long long)n);
+    return -1;
+  }
+  *cursor_out_host = u0;
+  if (rows == 0 || k == 0) return 0;
+  const bool tail = n > 10000 && k > n / 50;
+  // Floyd: set of k values (pow2 >= 1.2k, as numpy); tail: map of <= 2k touched indices
+  uint64_t want = tail ? 4 * k : (uint64_t)(1.2 * (double)k) + 1;
+  uint64_t cap = 1;
+  while (cap < want) cap <<= 1;
+  uint32_t* tab = nullptr;
+  uint64_t* cur = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&tab, sizeof(uint32_t) * cap * (tail ? 2 : 1), st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&cur, sizeof(uint64_t), st));
+  smx_count_launch();
+  choice_rows_kernel<<<1, 32, 0, st>>>(smx::Key{k0, k1}, u0, (uint32_t)n, (uint32_t)k, rows, out, tab,
+                                       (uint32_t)(cap - 1), cur);
+  SMX_LAUNCH_CHECK();
+  SMX_CUDA_CHECK(cudaMemcpyAsync(cursor_out_host, cur, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+  cudaFreeAsync(tab, st);
+  cudaFreeAsync(cur, st);
+  return 0;
+}
+
+// Records from drawn source positions: keys[j] = key_tab[v] (or v), vals[j] =
+// pay_tab[j / kdiv]; optional used-value bitmap bit (mark_tab ? mark_tab[v] : v).
+__global__ void records_from_values_kernel(const uint32_t* values, uint64_t n, const uint32_t* key_tab,
+                                           const uint32_t* pay_tab, smx::FastDiv kd, uint32_t* keys,
+                                           uint32_t* vals, uint32_t* bits, const uint32_t* mark_tab) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t v = values[j];
+  if (keys) keys[j] = key_tab ? key_tab[v] : v;
+  if (vals) vals[j] = pay_tab[kd.div((uint32_t)j)];
+  if (bits) {
+    const uint32_t b = mark_tab ? mark_tab[v] : v;
+    const uint32_t m = 1u << (b & 31);
+    if (!(bits[b >> 5] & m)) atomicOr(&bits[b >> 5], m);
+  }
+}
+
+extern "C" int smx_records_from_values(const uint32_t* values, uint64_t n, const uint32_t* key_tab,
+                                       const uint32_t* pay_tab, uint32_t kdiv, uint32_t* keys, uint32_t* vals,
+                                       uint32_t* bits, const uint32_t* mark_tab, void* stream) {
+  if (n == 0) return 0;
+  if (n >= (1ULL << 32)) {
+    smx_set_error("smx_records_from_values: %llu records exceed 2^32", (unsigned long long)n);
+    return -1;
+  }
+  smx_count_launch();
+  records_from_values_kernel<<<nblk(n), T256, 0, (cudaStream_t)stream>>>(values, n, key_tab, pay_tab,
+                                                                         FastDiv::make(kdiv ? kdiv : 1), keys, vals,
+                                                                         bits, mark_tab);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}

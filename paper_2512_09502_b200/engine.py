@@ -620,6 +620,13 @@ class Cluster:
                 call("smx_gen_pairs", 0, n, n_src, _ptr(key_tab), _ptr(pay_tab), _ptr(keys), _ptr(vals), sk)
             elif rule == "all_to_all":
                 call("smx_gen_pairs", 1, n, n_src, _ptr(key_tab), _ptr(pay_tab), _ptr(keys), _ptr(vals), sk)
+            elif rule == "fixed_indegree" and not conn.allow_multapses:
+                # one choice(n_src, k, replace=False) row per target (sm/construction.py:403-404)
+                pos = torch.empty(n, dtype=torch.int32, device=st.device)
+                call("smx_choice_rows", aligned_key[0], aligned_key[1], 0, n_src, int(conn.k_in), n_tgt, _ptr(pos),
+                     cur.ctypes.data, sk)
+                call("smx_records_from_values", _ptr(pos), n, _ptr(key_tab), _ptr(pay_tab), int(conn.k_in),
+                     _ptr(keys), _ptr(vals), _ptr(pos_bits), 0, sk)
             elif rule == "fixed_indegree":
                 call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 2, _ptr(key_tab),
                      _ptr(pay_tab), int(conn.k_in), _ptr(keys), _ptr(vals), _ptr(pos_bits), 0,
@@ -656,8 +663,6 @@ class Cluster:
                 raise ValueError(f"{name} index outside the rank's node range")
         conn.validate(len(sources), len(targets))
         syn.validate()
-        if conn.rule == "fixed_indegree" and not conn.allow_multapses:
-            raise NotImplementedError("allow_multapses=False (choice without replacement) is not implemented yet")
         return sources, targets
 
     def connect(self, rank: int, sources, targets, conn: ConnSpec, syn: SynSpec, port: int = 0) -> int:
@@ -790,7 +795,12 @@ class Cluster:
         pb = torch.zeros(_words(n_src), dtype=torch.int32, device=ss.device)
         n = int(conn.k_in) * n_tgt if conn.rule == "fixed_indegree" else int(conn.n_total)
         cur = np.zeros(1, dtype=np.uint64)
-        if n:
+        if n and conn.rule == "fixed_indegree" and not conn.allow_multapses:
+            pos = torch.empty(n, dtype=torch.int32, device=ss.device)
+            call("smx_choice_rows", k_src[0], k_src[1], 0, n_src, int(conn.k_in), n_tgt, _ptr(pos),
+                 cur.ctypes.data, ss.stream)
+            call("smx_records_from_values", _ptr(pos), n, 0, 0, 1, 0, 0, _ptr(pb), 0, ss.stream)
+        elif n:
             call("smx_gen_draw", k_src[0], k_src[1], 0, n_src, n, 1, 0, 0, 0, 1, 0, 0, _ptr(pb), 0,
                  _words(n_src), 0, 0, 0, cur.ctypes.data, ss.stream)
         return pb
@@ -832,14 +842,15 @@ class Cluster:
         src_nodes = [np.asarray(nodes, dtype=np.int64) for _, nodes in source_pops]
         if not src_nodes or any(len(a) == 0 for a in src_nodes):
             raise ValueError("source populations must be non-empty")
-        if not allow_multapses:
-            raise NotImplementedError("allow_multapses=False (choice without replacement) is not implemented yet")
         syn.validate()
         if not syn.is_constant:
             raise NotImplementedError("random / per-record SynSpec in the distributed rule is not implemented yet")
         all_rank = np.concatenate([np.full(len(a), r, dtype=np.int32) for r, a in zip(src_ranks, src_nodes)])
         all_node = np.concatenate(src_nodes)
         total = len(all_node)
+        if not allow_multapses and k_in > total:
+            raise ValueError(f"k_in {k_in} > population size {total} without multapses")
+        self._dist_multi, self._dist_kin = bool(allow_multapses), int(k_in)
         for r, a in zip(src_ranks, src_nodes):
             if a.min() < 0 or a.max() >= self.n_nodes[r]:
                 raise ValueError("source index outside the source rank's node range")
@@ -994,11 +1005,12 @@ class Cluster:
         dev, sk = st.device, st.stream
         lut_base = st.lut.n
         n = k_in * len(tg)
-        runs = self._runs(all_rank, all_node)
+        multi = self._dist_multi
+        runs = self._runs(all_rank, all_node) if multi else None
         remote = bool((runs[1] != tr).any()) if runs is not None else bool((np.asarray(all_rank) != tr).any())
         if runs is None:
             # general table: keys gathered from key_tab, used values marked by the draw
-            key_tab = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)[0]
+            key_tab, gv_tab = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)[:2]
             vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
         elif remote:
             # used source values from the early-exit replay of the same stream (what
@@ -1043,10 +1055,16 @@ class Cluster:
         cur = np.zeros(1, dtype=np.uint64)
         ev0 = self._event(st) if self.prof is not None else None
         mark = runs is None
-        kmode, ktab = (1, _ptr(key_tab)) if pieces is None else (3, pieces.ctypes.data)
-        call("smx_gen_draw", key[0], key[1], 0, total, n, kmode, 2, ktab, _ptr(pay_tab), k_in,
-             _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits) if mark else 0, 0, vbits.numel(), 1, lut_base,
-             int(vbase[tr]), cur.ctypes.data, sk)
+        if not multi:  # one choice(total, k_in, replace=False) row per target (sm/construction.py:680-683)
+            pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            call("smx_choice_rows", key[0], key[1], 0, total, k_in, len(tg), _ptr(pos), cur.ctypes.data, sk)
+            call("smx_records_from_values", _ptr(pos), n, _ptr(key_tab), _ptr(pay_tab), k_in,
+                 _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits), _ptr(gv_tab), sk)
+        else:
+            kmode, ktab = (1, _ptr(key_tab)) if pieces is None else (3, pieces.ctypes.data)
+            call("smx_gen_draw", key[0], key[1], 0, total, n, kmode, 2, ktab, _ptr(pay_tab), k_in,
+                 _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits) if mark else 0, 0, vbits.numel(), 1, lut_base,
+                 int(vbase[tr]), cur.ctypes.data, sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
         if st.wide:
@@ -1127,6 +1145,16 @@ class Cluster:
         piece is sized for coupon collection (V (ln V + 6) draws for V distinct
         values), so a full-coverage call needs one check."""
         stream = torch.cuda.current_stream(dev).cuda_stream
+        if not self._dist_multi:  # the rows form one chain: replay all of them
+            _, gv_all, _, _ = self._dist_tables(dev, stream, tr, total, all_rank, all_node, vbase, 0)
+            vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
+            k = self._dist_kin
+            pos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            cur = np.zeros(1, dtype=np.uint64)
+            call("smx_choice_rows", key[0], key[1], 0, total, k, n // k if k else 0, _ptr(pos), cur.ctypes.data,
+                 stream)
+            call("smx_records_from_values", _ptr(pos), n, 0, 0, 1, 0, 0, _ptr(vbits), _ptr(gv_all), stream)
+            return vbits
         runs = self._runs(all_rank, all_node)
         if runs is None:
             _, gv_all, _, _ = self._dist_tables(dev, stream, tr, total, all_rank, all_node, vbase, 0)

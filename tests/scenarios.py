@@ -94,6 +94,30 @@ def rules_no_autapse(ns, seed=8):
     return c, (0.0, 5.0)
 
 
+def no_multapse(ns, mode="p2p", seed=21):
+    """allow_multapses=False: one numpy choice(n, k, replace=False) row per
+    target (sm/construction.py:403-404, 680-683) -- the tail-shuffle variant
+    (n > 10000, k > n // 50), Floyd's variant, a flagged remote call (the
+    source rank replays the rows) and the distributed rule."""
+    cfg = ns.SimConfig(n_ranks=2, comm_mode=mode, seed=seed)
+    c = ns.make_cluster(cfg)
+    group = -1
+    if mode == "collective":
+        group = 0
+        c.declare_group(0, [0, 1])
+    a = c.create_neurons(0, 12000, ns.LifParams(i_e=0.2), ("normal", -60.0, 2.0), gids=np.arange(12000))
+    b = c.create_neurons(1, 500, ns.LifParams(i_e=0.4), ("normal", -58.0, 3.0), gids=np.arange(12000, 12500))
+    A, B = np.arange(a.start, a.stop), np.arange(b.start, b.stop)
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    c.connect(0, A, A[:50], S("fixed_indegree", k_in=300, allow_multapses=False), Sy(0.125, 2))
+    c.connect(1, B, B, S("fixed_indegree", k_in=20, allow_multapses=False), Sy(0.25, 3))
+    c.connect_remote(0, A[:1000], 1, B[:100], S("fixed_indegree", k_in=5, allow_multapses=False),
+                     Sy(0.5, 2), group=group)
+    c.connect_fixed_indegree_distributed([(0, A[:2000]), (1, B)], [(0, A[:30]), (1, B[:30])], 40,
+                                         Sy(-0.25, 2), group=group, allow_multapses=False)
+    return c, (0.0, 5.0)
+
+
 def poisson_multi(ns, mode="p2p", seed=12):
     """Several Poisson devices per rank with overlapping, permuted targets and
     delays below / above the exchange block (all records delay >= 5, so ranks
@@ -207,6 +231,8 @@ SCENARIOS = {
     "rules_no_autapse": rules_no_autapse,
     "poisson_multi_p2p": lambda ns: poisson_multi(ns, "p2p"),
     "poisson_multi_coll": lambda ns: poisson_multi(ns, "collective"),
+    "no_multapse_p2p": lambda ns: no_multapse(ns, "p2p"),
+    "no_multapse_coll": lambda ns: no_multapse(ns, "collective"),
 }
 
 # scenarios whose weights are not dyadic: tables are bit-exact, the raster is

@@ -56,3 +56,18 @@ def test_against_golden():
     for seed in (11, 12345):
         got = np.array([OracleStream(seed, ("init-v", int(g))).normal(-58.0, 5.0) for g in gids])
         assert np.array_equal(got, z[f"initv/seed{seed}"])
+
+
+@pytest.mark.parametrize("n,k", [(10, 3), (100, 50), (1000, 1000), (20000, 400), (20000, 401), (10001, 201),
+                                 (10000, 5000), (50000, 3000), (7, 0), (300, 299)])
+def test_choice_no_replace_matches_numpy(n, k):
+    """Generator.choice(n, k, replace=False) restated (sm/core.py:140-141):
+    Floyd + shuffle / tail shuffle, three consecutive calls per stream (the
+    reference draws one row per target from one stream)."""
+    from numpy.random import Generator, Philox
+    from oracle.rng import OracleStream
+    g = Generator(Philox(key=(7 << 64) | 11))
+    o = OracleStream(0, key=(11, 7))
+    for _ in range(3):
+        assert np.array_equal(o.choice_no_replace(n, k), g.choice(n, size=k, replace=False))
+    assert o.next64() == int(g.bit_generator.random_raw())

@@ -452,10 +452,10 @@ size_t downsweep_smem() {
   return (size_t)4 * DS_TILE * 4 + (size_t)3 * (1 << BITS) * 4 + (size_t)DS_WARPS * (1 << BITS) * 2;
 }
 
+// One pass (histograms, offsets, scatter) with BITS-wide digits.
 template <int BITS>
-int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, uint64_t n, int passes,
-             int index_values, const uint32_t* lut, uint32_t* counts, uint64_t n_keys, int* out_in_b,
-             cudaStream_t st) {
+int run_pass(const SortPass& p, uint32_t n_tiles, uint16_t* tcnt, uint32_t* off, uint32_t* csum,
+             uint32_t* tile_ctr, cudaStream_t st) {
   constexpr int BINS = 1 << BITS;
   const size_t smem = downsweep_smem<BITS>();
   const size_t th_smem = (size_t)4 * (th_hist_warps(BITS) * BINS + CNT_BINS);
@@ -467,19 +467,46 @@ int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* val
                                         (int)th_smem));
     configured = true;
   }
+  const uint32_t n_chunks = (n_tiles + TC - 1) / TC;
+  const uint32_t hg = std::min<uint32_t>(n_tiles, 148 * 2);
+  const uint32_t tpc = (n_tiles + hg - 1) / hg;
+  const uint32_t hgrid = (n_tiles + tpc - 1) / tpc;
+  const uint32_t grid = std::min<uint32_t>(n_tiles, 148u * ds_ctas_per_sm(BITS));
+  smx_count_launch(); tile_hist_kernel<BITS><<<hgrid, US_THREADS, th_smem, st>>>(p, tcnt, n_tiles, tpc);
+  smx_count_launch(); chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, n_tiles, csum);
+  smx_count_launch(); chunk_scan_kernel<BITS><<<1, 1024, 0, st>>>(csum, n_chunks);
+  smx_count_launch(); tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, csum, n_tiles, off);
+  smx_count_launch(); downsweep_kernel<BITS><<<grid, DS_THREADS, smem, st>>>(p, off, n_tiles, tile_ctr);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+int run_pass_bits(int bits, const SortPass& p, uint32_t n_tiles, uint16_t* tcnt, uint32_t* off, uint32_t* csum,
+                  uint32_t* tile_ctr, cudaStream_t st) {
+  switch (bits) {
+    case 8: return run_pass<8>(p, n_tiles, tcnt, off, csum, tile_ctr, st);
+    case 9: return run_pass<9>(p, n_tiles, tcnt, off, csum, tile_ctr, st);
+    case 10: return run_pass<10>(p, n_tiles, tcnt, off, csum, tile_ctr, st);
+    default: return run_pass<11>(p, n_tiles, tcnt, off, csum, tile_ctr, st);
+  }
+}
+
+// passes of pass_bits[0..passes) digit bits, least significant first
+int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, uint64_t n,
+             const int* pass_bits, int passes, int index_values, const uint32_t* lut, uint32_t* counts,
+             uint64_t n_keys, int* out_in_b, cudaStream_t st) {
+  int max_bits = 8;
+  for (int i = 0; i < passes; ++i) max_bits = std::max(max_bits, pass_bits[i]);
+  const uint32_t max_bins = 1u << max_bits;
   const uint32_t n_tiles = (uint32_t)((n + DS_TILE - 1) / DS_TILE);
   const uint32_t n_chunks = (n_tiles + TC - 1) / TC;
   uint16_t* tcnt = nullptr;
   uint32_t *off = nullptr, *csum = nullptr, *ctr = nullptr;
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&ctr, sizeof(uint32_t) * (passes + 1), st));
   SMX_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * (passes + 1), st));
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&tcnt, sizeof(uint16_t) * n_tiles * BINS, st));
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&off, sizeof(uint32_t) * n_tiles * BINS, st));
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&csum, sizeof(uint32_t) * n_chunks * BINS, st));
-  const uint32_t hg = std::min<uint32_t>(n_tiles, 148 * 2);
-  const uint32_t tpc = (n_tiles + hg - 1) / hg;
-  const uint32_t hgrid = (n_tiles + tpc - 1) / tpc;
-  const uint32_t grid = std::min<uint32_t>(n_tiles, 148u * ds_ctas_per_sm(BITS));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&tcnt, sizeof(uint16_t) * n_tiles * max_bins, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&off, sizeof(uint32_t) * n_tiles * max_bins, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&csum, sizeof(uint32_t) * n_chunks * max_bins, st));
   // Intermediate passes move (key, value) records as one 8-byte item (AoS):
   // half the store instructions and twice the bytes per scattered run of the
   // SoA layout.  X lives in the scratch pair when keys_b | vals_b are
@@ -496,6 +523,7 @@ int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* val
     SMX_CUDA_CHECK(cudaMallocAsync((void**)&own, sizeof(uint2) * n, st));
     Y = own;
   }
+  int shift = 0;
   for (int pass = 0; pass < passes; ++pass) {
     SortPass p{};
     const uint2* in = pass == 0 ? nullptr : (pass & 1 ? X : Y);
@@ -507,7 +535,7 @@ int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* val
     }
     p.first = pass == 0;
     p.last = pass == passes - 1;
-    p.shift = BITS * pass;
+    p.shift = shift;
     p.n = n;
     p.lut = lut;
     p.counts = counts;
@@ -521,12 +549,8 @@ int run_sort(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* val
       *out_in_b = p.vals_out == vals_b ? 1 : 0;
     }
     p.tmp_flag = ctr + passes;
-    smx_count_launch(); tile_hist_kernel<BITS><<<hgrid, US_THREADS, th_smem, st>>>(p, tcnt, n_tiles, tpc);
-    smx_count_launch(); chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, n_tiles, csum);
-    smx_count_launch(); chunk_scan_kernel<BITS><<<1, 1024, 0, st>>>(csum, n_chunks);
-    smx_count_launch(); tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, csum, n_tiles, off);
-    smx_count_launch(); downsweep_kernel<BITS><<<grid, DS_THREADS, smem, st>>>(p, off, n_tiles, ctr + pass);
-    SMX_LAUNCH_CHECK();
+    if (int rc = run_pass_bits(pass_bits[pass], p, n_tiles, tcnt, off, csum, ctr + pass, st)) return rc;
+    shift += pass_bits[pass];
   }
   if (own) cudaFreeAsync(own, st);
   cudaFreeAsync(tcnt, st);
@@ -622,13 +646,30 @@ extern "C" int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
     return -1;
   }
   if (key_bits < 1) key_bits = 1;
-  static const int max_bits = getenv("SMX_SORT_MAX_BITS") ? atoi(getenv("SMX_SORT_MAX_BITS")) : RS_MAX_BITS;
-  const int passes = (key_bits + max_bits - 1) / max_bits;
-  const int bits = std::max((key_bits + passes - 1) / passes, 8);
-  switch (bits) {
-    case 8: return run_sort<8>(keys_a, vals_a, keys_b, vals_b, n, passes, index_values, lut, counts, n_keys, out_in_b, st);
-    case 9: return run_sort<9>(keys_a, vals_a, keys_b, vals_b, n, passes, index_values, lut, counts, n_keys, out_in_b, st);
-    case 10: return run_sort<10>(keys_a, vals_a, keys_b, vals_b, n, passes, index_values, lut, counts, n_keys, out_in_b, st);
-    default: return run_sort<11>(keys_a, vals_a, keys_b, vals_b, n, passes, index_values, lut, counts, n_keys, out_in_b, st);
+  // digit plan: 9-bit lower passes (three CTAs per SM), the last pass takes
+  // the rest up to 10 bits (values only, the cheapest scatter); an env cap
+  // (tuning) forces equal passes of at most that many bits
+  static const int cap = getenv("SMX_SORT_MAX_BITS") ? atoi(getenv("SMX_SORT_MAX_BITS")) : 0;
+  int bits[8];
+  int passes = 0;
+  if (cap > 0) {
+    const int np = (key_bits + cap - 1) / cap;
+    for (int i = 0; i < np; ++i) bits[passes++] = std::max((key_bits + np - 1) / np, 8);
+  } else if (key_bits <= 11) {
+    bits[passes++] = std::max(key_bits, 8);
+  } else if (key_bits == 20) {  // a 9 + 11 split measured slower than 10 + 10
+    bits[passes++] = 10;
+    bits[passes++] = 10;
+  } else if (key_bits > 20 && key_bits <= 22) {
+    bits[passes++] = key_bits - 11;
+    bits[passes++] = 11;
+  } else {
+    int rest = key_bits;
+    while (rest > 10) {
+      bits[passes++] = 9;
+      rest -= 9;
+    }
+    bits[passes++] = std::max(rest, 8);
   }
+  return run_sort(keys_a, vals_a, keys_b, vals_b, n, bits, passes, index_values, lut, counts, n_keys, out_in_b, st);
 }

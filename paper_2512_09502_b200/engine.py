@@ -851,6 +851,8 @@ class Cluster:
         if not allow_multapses and k_in > total:
             raise ValueError(f"k_in {k_in} > population size {total} without multapses")
         self._dist_multi, self._dist_kin = bool(allow_multapses), int(k_in)
+        self._runs_total = total
+        self._runs_cache = (self.dist_ctr + 1, self._pops_runs(src_ranks, src_nodes))
         for r, a in zip(src_ranks, src_nodes):
             if a.min() < 0 or a.max() >= self.n_nodes[r]:
                 raise ValueError("source index outside the source rank's node range")
@@ -954,6 +956,30 @@ class Cluster:
         call("smx_dist_tables", _ptr(rk), _ptr(nd), total, _ptr(vb), tr, lut_base, _ptr(key_tab),
              _ptr(gv_tab), stream)
         return key_tab, gv_tab, rk, nd
+
+    @staticmethod
+    def _pops_runs(src_ranks, src_nodes, max_pieces=8):
+        """_pieces_of computed from the populations (no concatenated arrays)."""
+        starts, rks, nds = [], [], []
+        at = 0
+        for r, a in zip(src_ranks, src_nodes):
+            if len(a) == 0:
+                continue
+            brk = np.flatnonzero(np.diff(a) != 1) + 1
+            for b0 in np.concatenate([[0], brk]):
+                b0 = int(b0)
+                if starts and rks[-1] == r and nds[-1] + (at + b0 - starts[-1]) == int(a[b0]):
+                    pass  # continues the previous run (same rank, next node)
+                else:
+                    starts.append(at + b0)
+                    rks.append(int(r))
+                    nds.append(int(a[b0]))
+                if len(starts) > max_pieces:
+                    return None
+            at += len(a)
+        if not starts:
+            return None
+        return np.array(starts, np.int64), np.array(rks, np.int64), np.array(nds, np.int64)
 
     @staticmethod
     def _pieces_of(all_rank, all_node, max_pieces=8):
@@ -1125,16 +1151,10 @@ class Cluster:
         with torch.cuda.stream(side):
             cnt = torch.zeros(len(los), dtype=torch.int64, device=st.device)
             call("smx_count_ranges", _ptr(st.keys.t[base:]), n, rng.ctypes.data, _ptr(cnt), side.cuda_stream)
-            idx = {r: [i for i, o in enumerate(owner) if o == r] for r in present}
-            per = {r: cnt[idx[r]].sum() if idx[r] else cnt[:0].sum() for r in present}
         # (resolved in prepare on this same side stream; the keys stay untouched
         # until the sort, which only reads them)
-        for r in present:
-            if r == tr:
-                st.mem.later("store_append", per[r])
-            else:
-                st.mem.later("remote_batch", per[r], (int(group), r),
-                             _popcount_dev(st.maps[(int(group), r)].present.view()), per[r])
+        sizes = torch.stack([_popcount_dev(st.maps[(int(group), r)].present.view()) for r in remote])
+        st.mem.later("dist_batches", tr, int(group), list(present), owner, cnt, sizes)
 
     def _dist_replay(self, dev, key, tr, total, all_rank, all_node, vbase, total_words, n):
         """Source-side replay of a remote target's draws: used-value bitmap only

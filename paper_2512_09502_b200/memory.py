@@ -107,16 +107,39 @@ class RankMemory:
         self._pending.append((method, args))
 
     def resolve(self) -> None:
-        """Replay the queued events with one device->host transfer."""
+        """Replay the queued events with one device->host transfer (tensor
+        arguments become ints, or lists of ints when they hold several)."""
         if not self._pending:
             return
         import torch
         dev_vals = [a for _, args in self._pending for a in args if isinstance(a, torch.Tensor)]
-        host = iter(torch.stack([v.reshape(()).to(dev_vals[0].device) for v in dev_vals]).cpu().tolist()
-                    if dev_vals else [])
+        host = []
+        if dev_vals:
+            flat = torch.cat([v.reshape(-1).to(torch.int64).to(dev_vals[0].device) for v in dev_vals]).cpu().tolist()
+            at = 0
+            for v in dev_vals:
+                k = v.numel()
+                host.append(int(flat[at]) if v.dim() == 0 else [int(x) for x in flat[at: at + k]])
+                at += k
+        it = iter(host)
         pending, self._pending = self._pending, []
         for method, args in pending:
-            getattr(self, method)(*[int(next(host)) if isinstance(a, torch.Tensor) else a for a in args])
+            getattr(self, method)(*[next(it) if isinstance(a, torch.Tensor) else a for a in args])
+
+    def dist_batches(self, tr: int, group: int, present: list, owners: list, range_counts: list,
+                     map_sizes: list) -> None:
+        """One distributed call on its target rank: the reference appends one
+        batch per source rank present, ascending; remote ones go through
+        remote_connect (sm/construction.py:689-703, 597-617)."""
+        per = {}
+        for o, c in zip(owners, range_counts):
+            per[o] = per.get(o, 0) + int(c)
+        sizes = dict(zip([r for r in present if r != tr], map_sizes))
+        for r in present:
+            if r == tr:
+                self.store_append(per.get(r, 0))
+            else:
+                self.remote_batch(per.get(r, 0), (int(group), r), sizes[r], per.get(r, 0))
 
     def arena(self, kind: str) -> Arena:
         return self.host if kind == HOST else self.device

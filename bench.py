@@ -257,8 +257,6 @@ def run_ours(args):
     achieved = BYTES_PER_SYN * syn_per_rank / (k_ms * 1e-3) / 1e9
     tps, traffic_src = traffic_per_synapse()
     traffic = tps * syn_per_rank if tps is not None else None  # bytes per construction, like achieved
-    if rank != 0:
-        return
     line = {
         "metric": "construction_synapses_per_s", "value": value, "unit": "synapses/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -282,8 +280,11 @@ def run_ours(args):
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
+        c.close()
+        dist.barrier()
         dist.destroy_process_group()
 
 

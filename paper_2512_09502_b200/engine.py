@@ -324,6 +324,7 @@ class Cluster:
         self.min_remote_delay = None
         self.use_graphs = True
         self._graph = None
+        self._xgraph_ok = None   # exchange captured in the block graph (None: not tried yet)
         self._pg = None
         self.messages = {p: 0 for p in PHASES}
         self.bytes = {p: 0 for p in PHASES}
@@ -1475,6 +1476,7 @@ class Cluster:
         st.p2p_desc = ctypes_routes_desc(st.TP, st.p2p_packets, st.p2p_counts, self.n_ranks, st.pk_cap)
         st.g_desc = ctypes_routes_desc(st.GQ, st.g_packets, st.g_counts, len(self.groups), st.pk_cap)
         st.graph = None
+        st.xplan = None
         st.pois_stream = torch.cuda.Stream(device=dev)
         st.pois_ready = None
         st.pois_next = -1
@@ -1639,24 +1641,77 @@ class Cluster:
                 st.pois_have = b0
         for st in self.ranks.values():
             st.now_dev.fill_(now)  # block start; fused steps add their offset
+        nccl = self.n_ranks > 1 and self.distributed
         if use_graph:
             if self._graph is None:
+                if nccl and self._xgraph_ok is None:
+                    # one eager round first: communicators and exchange buffers exist
+                    # before the capture of the whole block (NCCL rounds included)
+                    self._block_body(n_steps)
+                    self._exchange_nccl()
+                    self._zero_counts()
+                    self._xgraph_ok = True
+                    self._count_rounds(n_steps)
+                    self.now += n_steps
+                    return
                 for st in self.ranks.values():
                     torch.cuda.synchronize(st.device)
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._block_body(n_steps)
+                ok = True
+                try:
+                    with torch.cuda.graph(g):
+                        self._block_body(n_steps)
+                        if nccl and self._xgraph_ok:
+                            self._exchange_nccl()
+                            self._zero_counts()
+                except RuntimeError as e:
+                    if not nccl:
+                        raise
+                    ok = False
+                    import sys
+                    print(f"[spikemesh-b200] ranks {list(self.ranks)}: exchange not captured ({e})", file=sys.stderr)
+                if nccl and self._xgraph_ok:
+                    # every rank must replay the same collectives: agree on the outcome
+                    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=self._dev0())
+                    torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+                    if not int(flag.item()):
+                        # collectives not capturable here: graph the block, exchange eagerly
+                        self._xgraph_ok = False
+                        for st in self.ranks.values():
+                            torch.cuda.synchronize(st.device)
+                        g = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(g):
+                            self._block_body(n_steps)
                 self._graph = g
             self._graph.replay()
+            if nccl and not self._xgraph_ok:
+                self._exchange_nccl()
+                self._zero_counts()
+            elif not nccl:
+                self._zero_counts()
         else:
             self._block_body(n_steps)
-        if self.n_ranks > 1 and self.distributed:
-            self._exchange_nccl()
+            if nccl:
+                self._exchange_nccl()
+            self._zero_counts()
+        self._count_rounds(n_steps)
+        self.now += n_steps
+
+    def close(self) -> None:
+        """Release the block graph (it may hold captured NCCL rounds: drop it
+        before torch.distributed.destroy_process_group)."""
+        self._sync()
+        self._graph = None
+        self._xgraph_ok = None
+        self._sync()
+
+    def _dev0(self):
+        return next(iter(self.ranks.values())).device
+
+    def _zero_counts(self):
         for st in self.ranks.values():
             st.p2p_counts.zero_()
             st.g_counts.zero_()
-        self._count_rounds(n_steps)
-        self.now += n_steps
 
     def _count_rounds(self, n_steps):
         """Message counters as the reference's lockstep transport would count
@@ -1731,45 +1786,110 @@ class Cluster:
         for st in self.ranks.values():
             self._deliver(st)
 
+    def _xplan(self, st):
+        """Fixed-capacity exchange buffers.  A neuron spikes at
+        most ceil(B / (ref_steps + 1)) times in a block of B steps, so a
+        group round carries at most (largest roster) x that many packets and a
+        p2p pair (mirror size) x that many: every size is known to sender and
+        receiver without a count round, and no host synchronisation is needed
+        per block.  Rosters are replicated on every member; a target's p2p map
+        has exactly the source's mirror entries."""
+        dev = st.device
+        me = st.rank
+        ref_min = int(st.ref_steps.min().item()) if st.N else 0
+        m = -(-self.block // (ref_min + 1))
+        plan = dict(groups={}, m=m)
+        for g in self.group_ids:
+            members = sorted(self.groups[g])
+            if me not in members:
+                continue
+            cap = max([int(st.H[(g, sr)].numel()) for sr in members if (g, sr) in st.H] + [0]) * m
+            cap = min(max(cap, 1), st.pk_cap)
+            plan["groups"][g] = dict(members=members, cap=cap,
+                                     send=torch.zeros(2 + 2 * cap, dtype=torch.int32, device=dev),
+                                     recv=torch.zeros(len(members) * (2 + 2 * cap), dtype=torch.int32, device=dev))
+        if self.has_p2p:
+            out_c = [min(int(st.S[d].numel()) * m, st.pk_cap) if d in st.S and d != me else 0
+                     for d in range(self.n_ranks)]
+            in_c = [min(int(st.RL[(POINT_TO_POINT, s)][0].numel()) * m, st.pk_cap)
+                    if (POINT_TO_POINT, s) in st.RL and s != me else 0 for s in range(self.n_ranks)]
+            out_sz = [2 + 2 * c if c else 0 for c in out_c]
+            in_sz = [2 + 2 * c if c else 0 for c in in_c]
+            plan["p2p"] = dict(out_c=out_c, in_c=in_c, out_sz=out_sz, in_sz=in_sz,
+                               send=torch.zeros(max(sum(out_sz), 1), dtype=torch.int32, device=dev),
+                               recv=torch.zeros(max(sum(in_sz), 1), dtype=torch.int32, device=dev))
+        plan["sent"] = torch.zeros(1, dtype=torch.int64, device=dev)    # packets sent (byte counter)
+        plan["over"] = torch.zeros(1, dtype=torch.int32, device=dev)    # capacity check
+        return plan
+
     def _exchange_nccl(self):
-        """One process per rank: the same rounds over NCCL, once per block
-        (exchange.py: counts first, then only the occupied packets)."""
-        from .exchange import allgather_round, p2p_round
+        """One process per rank: the exchange round of a block over NCCL
+        (sm/transport.py:92-168) with fixed-capacity buffers -- one collective
+        per group (all_gather) and one all_to_all for p2p pairs, each buffer
+        led by its count; nothing is read back to the host."""
         dist = torch.distributed
         (st,) = self.ranks.values()
         me = st.rank
         st.n_src.zero_()
         if self._pg is None:
             self._pg = {g: dist.new_group(sorted(self.groups[g])) for g in sorted(self.groups)}
+        if st.xplan is None:
+            st.xplan = self._xplan(st)
+        X = st.xplan
         if self.has_p2p:
-            out, rc, recv_c, offs = p2p_round(st.p2p_counts, st.p2p_packets, st.pk_cap)
+            P = X["p2p"]
+            send, off = P["send"], 0
+            for d in range(self.n_ranks):
+                c = P["out_c"][d]
+                if not c:
+                    continue
+                send[off: off + 1].copy_(st.p2p_counts[d: d + 1])
+                send[off + 2: off + 2 + 2 * c].copy_(st.p2p_packets[d * st.pk_cap * 2: d * st.pk_cap * 2 + 2 * c])
+                X["over"].bitwise_or_((st.p2p_counts[d: d + 1] > c).to(torch.int32))
+                off += P["out_sz"][d]
+            X["sent"] += st.p2p_counts.sum()
+            dist.all_to_all_single(P["recv"][: sum(P["in_sz"])], send[: sum(P["out_sz"])], P["in_sz"], P["out_sz"])
+            off = 0
             for sr in range(self.n_ranks):
-                n = int(rc[sr])
-                if not n or sr == me:
+                if not P["in_c"][sr]:
                     continue
                 rl = st.RL.get((POINT_TO_POINT, sr))
                 if rl is None:
                     raise ProtocolError(f"rank {me}: spikes from rank {sr} but no map for that pair")
-                call("smx_unpack", _ptr(out[int(offs[sr]):]), _ptr(recv_c[sr:]), _ptr(rl[1]), rl[1].numel(),
+                rv = P["recv"]
+                call("smx_unpack", _ptr(rv[off + 2:]), _ptr(rv[off:]), _ptr(rl[1]), rl[1].numel(),
                      _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
-            self.bytes["propagation"] += 8 * int(st.p2p_counts.sum().item())
-        for g in self.group_ids:
-            members = sorted(self.groups[g])
-            if me not in members:
-                continue
-            slot = self.group_slots[g]
-            pk = st.g_packets[slot * st.pk_cap * 2:]
-            recv, ac, allc, cmax = allgather_round(st.g_counts[slot: slot + 1], pk, len(members), self._pg[g])
+                off += P["in_sz"][sr]
+        for g, G in X["groups"].items():
+            slot, cap, members = self.group_slots[g], G["cap"], G["members"]
+            send, recv = G["send"], G["recv"]
+            send[0:1].copy_(st.g_counts[slot: slot + 1])
+            send[2:].copy_(st.g_packets[slot * st.pk_cap * 2: slot * st.pk_cap * 2 + 2 * cap])
+            X["over"].bitwise_or_((st.g_counts[slot: slot + 1] > cap).to(torch.int32))
+            X["sent"] += st.g_counts[slot]
+            dist.all_gather_into_tensor(recv, send, group=self._pg[g])
             for i, sr in enumerate(members):
-                if sr == me or ac[i] == 0:
+                if sr == me:
                     continue
                 lk = st.I.get((g, sr))
                 if lk is None:
                     continue
-                call("smx_unpack", _ptr(recv[i * 2 * cmax:]), _ptr(allc[i:]), _ptr(lk), lk.numel(),
+                base = i * (2 + 2 * cap)
+                call("smx_unpack", _ptr(recv[base + 2:]), _ptr(recv[base:]), _ptr(lk), lk.numel(),
                      _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
-            self.bytes["propagation"] += 8 * int(ac[members.index(me)])
         self._deliver(st)
+
+    def _settle_exchange(self):
+        """Byte counter and capacity check of the fixed-capacity rounds (read
+        once per simulate, not per block)."""
+        for st in self.ranks.values():
+            X = getattr(st, "xplan", None)
+            if X is None:
+                continue
+            if int(X["over"].item()):
+                raise ProtocolError(f"rank {st.rank}: exchange capacity exceeded")
+            self.bytes["propagation"] += 8 * int(X["sent"].item())
+            X["sent"].zero_()
 
     _recording = False
 
@@ -1812,6 +1932,7 @@ class Cluster:
         self._recording = False
         self._set_record(False)
         self.timers.propagation += prop
+        self._settle_exchange()
         self._check_errors()
         model_s = steps * self.cfg.resolution_ms * 1e-3
         raster = self.merged_raster() if record else None

@@ -47,6 +47,7 @@ def main(names):
             r = Raster.from_events(np.concatenate(parts), c.cfg.resolution_ms)
             if r.sha256() != gold_r[name]["sha256"]:
                 bad.append(f"raster {r.n_events} events vs {gold_r[name]['n_events']}")
+        c.close()
         if bad:
             bad_all.append((name, rank, bad[:5]))
         print(f"[rank {rank}] {name}: {'OK' if not bad else bad[:3]}", flush=True)

@@ -1062,8 +1062,11 @@ class Cluster:
 
         pieces, tmp_keys, present = None, True, None
         if runs is not None:
-            present = self._present_ranks(vbits, ranks_sorted, seg_words)
-            assign(present)
+            if remote:
+                present = self._present_ranks(vbits, ranks_sorted, seg_words)
+                assign(present)
+            else:  # all sources local: nothing to assign, present iff anything was drawn
+                present = [tr] if n and total else []
             pieces = self._final_pieces(st, tr, group, runs, total, present)
             tmp_keys = pieces is None
             if pieces is None:  # images not consecutive: temporary keys resolved through the LUT

@@ -18,7 +18,7 @@ SAMP = None
 if os.environ.get("SAMPLE") and rank == 0:
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     from stall_sampler import Sampler
-    SAMP = Sampler(period=0.0005).start()
+    SAMP = Sampler(period=float(os.environ.get("PERIOD", "0.0005"))).start()
 for rep in range(int(os.environ.get("REPS", "3"))):
     dist.barrier()
     torch.cuda.synchronize()

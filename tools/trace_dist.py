@@ -1,0 +1,54 @@
+"""torch.profiler trace of one construction on rank 0 under torchrun: prints
+GPU-busy vs wall time and the largest idle gaps with the CPU op active then."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+from paper_2512_09502_b200 import api, engine, models  # noqa: E402
+
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+P = models.BalancedParams(neurons_per_rank=100_000, k_exc=9000, k_inh=2250)
+cfg = api.SimConfig(n_ranks=world, comm_mode="collective" if world > 1 else "p2p", seed=12345)
+
+
+def build():
+    c = engine.Cluster(cfg)
+    models.build_balanced_network(c, P)
+    c.prepare()
+    torch.cuda.synchronize()
+    return c
+
+
+for _ in range(2):
+    c = build()
+    del c
+dist.barrier()
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], with_stack=False) as prof:
+    c = build()
+dist.barrier()
+if rank == 0:
+    path = "/tmp/trace.json"
+    prof.export_chrome_trace(path)
+    ev = json.load(open(path))["traceEvents"]
+    gpu = sorted((e["ts"], e["ts"] + e["dur"], e["name"]) for e in ev
+                 if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset"))
+    cpu = [e for e in ev if e.get("ph") == "X" and e.get("cat") in ("python_function", "user_annotation", "cpu_op")]
+    t0, t1 = gpu[0][0], gpu[-1][1]
+    busy, last, gaps = 0.0, t0, []
+    for a, b, n in gpu:
+        if a > last:
+            gaps.append((a - last, last, n))
+        busy += max(0.0, b - max(a, last))
+        last = max(last, b)
+    print(f"rank0: GPU span {1e-3 * (t1 - t0):.2f} ms, busy {1e-3 * busy:.2f} ms, idle {1e-3 * (t1 - t0 - busy):.2f} ms")
+    for g, at, n in sorted(gaps, reverse=True)[:25]:
+        ops = [e["name"] for e in cpu if e["ts"] <= at + g / 2 <= e["ts"] + e["dur"]]
+        print(f"  gap {1e-3 * g:6.3f} ms at {1e-3 * (at - t0):7.2f} ms before {n[:40]:40s} cpu: {ops[-3:]}")
+dist.destroy_process_group()

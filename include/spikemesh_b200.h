@@ -36,6 +36,9 @@ int smx_stream_sync(void* stream);
 int smx_set_sync_policy(int flags);
 /* keep the default stream-ordered pool's memory mapped (no trim at sync) */
 int smx_pool_setup(int device);
+/* device error word of asynchronous paths: read + clear (synchronises stream) */
+int smx_check_device_errors(void* stream);
+int* smx_device_error_word(void);
 /* kernels launched by the library so far (process-wide counter) */
 uint64_t smx_launch_count(void);
 
@@ -81,7 +84,9 @@ int smx_dist_tables(const int32_t* src_rank, const int64_t* src_node, uint64_t t
  * used_bits (optional, used_bits_words words) marks bit
  * used_tab ? used_tab[value] : value for every emitted draw, or with
  * mark_from_key the bit of the record key: (key & ~TMP) - tmp_base for
- * temporary keys, local_bit for direct ones. */
+ * temporary keys, local_bit for direct ones.  cursor_out_host may be NULL:
+ * then nothing is read back (no host synchronisation) and a draw window short
+ * of accepted draws (12-sigma margin) is reported by smx_check_device_errors. */
 int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u32_cursor, uint64_t ex, uint64_t n, int key_mode,
                  int pay_mode, const uint32_t* key_tab, const uint32_t* pay_tab, uint32_t kdiv, uint32_t* keys,
                  uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab, uint32_t used_bits_words,

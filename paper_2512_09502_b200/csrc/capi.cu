@@ -70,3 +70,41 @@ extern "C" int smx_stream_sync(void* stream) {
   }
   return 0;
 }
+
+// Device-side error word per device (asynchronous paths that cannot return a
+// status at launch time, e.g. a draw window found short on the device).
+static int* g_dev_err[64] = {nullptr};
+
+extern "C" int* smx_device_error_word(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  int*& p = g_dev_err[dev & 63];
+  if (!p) {
+    if (cudaMalloc((void**)&p, sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, sizeof(int)) != cudaSuccess) return nullptr;
+  }
+  return p;
+}
+
+// Reads and clears the device error word of the current device (synchronises
+// the stream); 0 = no error.
+extern "C" int smx_check_device_errors(void* stream) {
+  int* p = smx_device_error_word();
+  if (!p) {
+    smx_set_error("smx_check_device_errors: no device error word");
+    return -3;
+  }
+  int v = 0;
+  cudaError_t e = cudaMemcpyAsync(&v, p, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    smx_set_error("smx_check_device_errors: %s", cudaGetErrorString(e));
+    return -3;
+  }
+  if (v) {
+    cudaMemsetAsync(p, 0, sizeof(int), (cudaStream_t)stream);
+    smx_set_error("device error %d (1: a draw window was short of accepted draws)", v);
+    return -2;
+  }
+  return 0;
+}

@@ -267,6 +267,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* ws, ui
 // unit (defined in capi.cu).
 extern "C" void smx_set_error(const char* fmt, ...);
 extern "C" void smx_count_launch(void);
+extern "C" int* smx_device_error_word(void);
 #define SMX_CUDA_CHECK(expr)                                                       \
   do {                                                                             \
     cudaError_t _e = (expr);                                                       \

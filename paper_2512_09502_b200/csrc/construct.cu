@@ -475,11 +475,12 @@ static int gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, uint64_t
       if (mk0.bits) { smx_count_launch(); mark_one_kernel<<<1, 1, 0, st>>>(mk0.bits, mk0.tab); }
       SMX_LAUNCH_CHECK();
     }
-    *cursor_out = u0;
+    if (cursor_out) *cursor_out = u0;
     return 0;
   }
-  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, st, &res, mk0);
-  *cursor_out = res.cursor;
+  // no cursor wanted: the asynchronous path (no host synchronisation)
+  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, st, cursor_out ? &res : nullptr, mk0);
+  if (cursor_out) *cursor_out = res.cursor;
   return rc;
 }
 

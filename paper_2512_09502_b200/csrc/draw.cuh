@@ -250,6 +250,10 @@ __global__ void __launch_bounds__(DRAW_THREADS, SMX_DRAW_MIN_BLOCKS) draw_write_
   }
 }
 
+static __global__ void draw_window_check_kernel(const uint64_t* total, uint64_t n_out, int* err) {
+  if (*total < n_out) atomicExch(err, 1);
+}
+
 // A one-value range (ex == 1) consumes no draws: every value is 0.
 template <class Sink>
 __global__ void draw_const_kernel(uint64_t n_out, Sink sink) {

@@ -49,7 +49,7 @@ int launch_draw_write(int mode, int G, size_t smem, cudaStream_t st, const DrawR
 template <class Sink>
 int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink,
              cudaStream_t st, DrawResult* res, DrawMark mk = DrawMark{nullptr, nullptr, 0, 0, 0, 0, 0}) {
-  res->cursor = u0;
+  if (res) res->cursor = u0;
   if (n_out == 0) return 0;
   if (ex == 1) {  // numpy: range of one value consumes nothing
     smx_set_error("run_draw: ex == 1 must be handled by the caller");
@@ -62,6 +62,7 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
   DrawRange r;
   r.key = key;
   r.u0 = u0;
+  const bool async = res == nullptr;  // no cursor wanted: no host readback at all
   r.lm.ex = (uint32_t)(ex & 0xffffffffULL);
   r.lm.threshold = ex == (1ULL << 32) ? 0u : (uint32_t)(((1ULL << 32) - ex) % ex);
   const double prej = (double)r.lm.threshold / 4294967296.0;
@@ -88,6 +89,25 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
     smx_count_launch(); draw_count_kernel<<<G, DRAW_THREADS, 0, st>>>(r, counts);
     smx_count_launch(); cta_offsets_kernel<<<1, 1024, 0, st>>>(counts, NW, offs);
     SMX_LAUNCH_CHECK();
+    if (async) {
+      // the window covers n_out accepted draws by 12 sigma; a short window is
+      // flagged on the device (smx_check_device_errors) instead of retried
+      int* err = smx_device_error_word();
+      if (!err) {
+        smx_set_error("run_draw: no device error word");
+        return -3;
+      }
+      smx_count_launch(); draw_window_check_kernel<<<1, 1, 0, st>>>(offs + NW, n_out, err);
+      mk.in_smem = mk.bits && mk.nwords <= DRAW_MARK_SMEM_WORDS;
+      const size_t smem = mk.in_smem ? mk.nwords * 4 : 0;
+      const int mode = mk.bits ? (mk.from_key ? 1 : 2) : 0;
+      if (int rc2 = launch_draw_write(mode, G, smem, st, r, offs, n_out, sink, nullptr, mk)) return rc2;
+      SMX_LAUNCH_CHECK();
+      cudaFreeAsync(counts, st);
+      cudaFreeAsync(offs, st);
+      cudaFreeAsync(cur_d, st);
+      return 0;
+    }
     uint64_t total = 0;
     SMX_CUDA_CHECK(cudaMemcpyAsync(&total, offs + NW, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     SMX_CUDA_CHECK(cudaStreamSynchronize(st));

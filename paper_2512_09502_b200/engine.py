@@ -29,7 +29,7 @@ import torch
 
 from . import _lib
 from .memory import RankMemory
-from ._lib import call
+from ._lib import call, check
 from .api import (POINT_TO_POINT, ConnSpec, ConsistencyError, DelayRangeError, LifParams,
                   ProtocolError, Raster, SimConfig, SynSpec, canonical_bytes, stream_key)
 
@@ -878,6 +878,7 @@ class Cluster:
         if group != POINT_TO_POINT and members is None:
             raise ValueError(f"group {group} is not declared")
         tgt_bits: dict[int, torch.Tensor] = {}   # per target rank: used-value bitmap (when computed)
+        pending = []                             # source-side replays awaiting their batched check
         for tr, tg in target_pops:
             tr = int(tr)
             tg = np.asarray(tg, dtype=np.int64)
@@ -899,11 +900,18 @@ class Cluster:
                     raise ValueError("target index outside the rank's node range")
                 vb, present = self._dist_target(st, key, tr, tg, k_in, total, all_rank, all_node, vbase,
                                                 seg_words, total_words, syn, port, group, ranks_sorted)
+            elif self._dist_multi:  # source-side replay, checked in one batch below
+                dev = next(iter(self.ranks.values())).device
+                pending.append((tr, self._replay_start(dev, key, tr, total, all_rank, all_node, vbase,
+                                                       total_words, n)))
+                continue
             else:
                 dev = next(iter(self.ranks.values())).device
                 vb = self._dist_replay(dev, key, tr, total, all_rank, all_node, vbase, total_words, n)
                 present = None
             tgt_bits[tr] = (vb, present)
+        for (tr, _), vb in zip(pending, self._replay_finish([R for _, R in pending])):
+            tgt_bits[tr] = (vb, None)
         # counters, in the reference's (target, source-rank) call order
         for tr, tg in target_pops:
             tr = int(tr)
@@ -1092,9 +1100,10 @@ class Cluster:
                  _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits), _ptr(gv_tab), sk)
         else:
             kmode, ktab = (1, _ptr(key_tab)) if pieces is None else (3, pieces.ctypes.data)
+            # nothing follows on this stream: no cursor, no host synchronisation
             call("smx_gen_draw", key[0], key[1], 0, total, n, kmode, 2, ktab, _ptr(pay_tab), k_in,
                  _ptr(st.keys.t[base:]), _ptr(vals), _ptr(vbits) if mark else 0, 0, vbits.numel(), 1, lut_base,
-                 int(vbase[tr]), cur.ctypes.data, sk)
+                 int(vbase[tr]), 0, sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
         if st.wide:
@@ -1179,34 +1188,66 @@ class Cluster:
                  stream)
             call("smx_records_from_values", _ptr(pos), n, 0, 0, 1, 0, 0, _ptr(vbits), _ptr(gv_all), stream)
             return vbits
+        return self._replay_finish([self._replay_start(dev, key, tr, total, all_rank, all_node, vbase,
+                                                       total_words, n)])[0]
+
+    def _replay_start(self, dev, key, tr, total, all_rank, all_node, vbase, total_words, n):
+        """First piece of an early-exit replay, launched without any host
+        synchronisation (the cursor is not read back)."""
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        R = dict(dev=dev, key=key, total=total, n=n, stream=stream)
         runs = self._runs(all_rank, all_node)
         if runs is None:
-            _, gv_all, _, _ = self._dist_tables(dev, stream, tr, total, all_rank, all_node, vbase, 0)
+            R["gv_all"] = self._dist_tables(dev, stream, tr, total, all_rank, all_node, vbase, 0)[1]
         else:  # mark through keys TMP | gv (piecewise affine): no table
             starts, rks, nds = runs
-            gvp = self._pack_pieces(starts, TMP_KEY | (np.asarray(vbase, np.int64)[rks] + nds))
-        vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
-        n_distinct = self._n_distinct_gv(all_rank, all_node, vbase, total_words)
-        excl = torch.empty(vbits.numel() + 1, dtype=torch.int64, device=dev)
-        cur = np.zeros(1, dtype=np.uint64)
-        u0, done = 0, 0
-        piece = max(int(n_distinct * (math.log(max(n_distinct, 2)) + 6.0)), 1 << 20)
-        while done < n:
-            k = min(piece, n - done)
-            if runs is None:
-                call("smx_gen_draw", key[0], key[1], u0, total, k, 1, 0, 0, 0, 1, 0, 0, _ptr(vbits), _ptr(gv_all),
-                     vbits.numel(), 0, 0, 0, cur.ctypes.data, stream)
-            else:
-                call("smx_gen_draw", key[0], key[1], u0, total, k, 3, 0, gvp.ctypes.data, 0, 1, 0, 0, _ptr(vbits),
-                     0, vbits.numel(), 1, 0, 0xFFFFFFFF, cur.ctypes.data, stream)
-            u0 = int(cur[0])
-            done += k
-            if done < n:
-                call("smx_bits_prefix", _ptr(vbits), vbits.numel(), _ptr(excl), stream)
-                if int(excl[-1].item()) >= n_distinct:
-                    break
-                piece *= 2
-        return vbits
+            R["gvp"] = self._pack_pieces(starts, TMP_KEY | (np.asarray(vbase, np.int64)[rks] + nds))
+        R["vbits"] = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
+        R["n_distinct"] = self._n_distinct_gv(all_rank, all_node, vbase, total_words)
+        R["excl"] = torch.empty(R["vbits"].numel() + 1, dtype=torch.int64, device=dev)
+        R["piece"] = max(int(R["n_distinct"] * (math.log(max(R["n_distinct"], 2)) + 6.0)), 1 << 20)
+        k = min(R["piece"], n)
+        if k:
+            self._replay_piece(R, 0, k, None)
+            if k < n:
+                call("smx_bits_prefix", _ptr(R["vbits"]), R["vbits"].numel(), _ptr(R["excl"]), stream)
+        R["first"] = k
+        return R
+
+    def _replay_piece(self, R, u0, k, cur):
+        vb = R["vbits"]
+        cptr = cur.ctypes.data if cur is not None else 0
+        if "gv_all" in R:
+            call("smx_gen_draw", R["key"][0], R["key"][1], u0, R["total"], k, 1, 0, 0, 0, 1, 0, 0, _ptr(vb),
+                 _ptr(R["gv_all"]), vb.numel(), 0, 0, 0, cptr, R["stream"])
+        else:
+            call("smx_gen_draw", R["key"][0], R["key"][1], u0, R["total"], k, 3, 0, R["gvp"].ctypes.data, 0, 1, 0, 0,
+                 _ptr(vb), 0, vb.numel(), 1, 0, 0xFFFFFFFF, cptr, R["stream"])
+
+    def _replay_finish(self, states) -> list:
+        """Completes the replays: one batched check of the first pieces; the
+        rare incomplete ones continue in doubling pieces."""
+        need = [R for R in states if R["first"] < R["n"]]
+        if need:
+            got = torch.stack([R["excl"][-1] for R in need]).cpu().numpy()
+            for R, g in zip(need, got):
+                if int(g) >= R["n_distinct"]:
+                    continue
+                # redo the first piece with its cursor, then keep drawing
+                cur = np.zeros(1, dtype=np.uint64)
+                self._replay_piece(R, 0, R["first"], cur)
+                u0, done, piece = int(cur[0]), R["first"], R["piece"] * 2
+                while done < R["n"]:
+                    k = min(piece, R["n"] - done)
+                    self._replay_piece(R, u0, k, cur)
+                    u0 = int(cur[0])
+                    done += k
+                    if done < R["n"]:
+                        call("smx_bits_prefix", _ptr(R["vbits"]), R["vbits"].numel(), _ptr(R["excl"]), R["stream"])
+                        if int(R["excl"][-1].item()) >= R["n_distinct"]:
+                            break
+                        piece *= 2
+        return [R["vbits"] for R in states]
 
     def _runs(self, all_rank, all_node):
         """_pieces_of for the current distributed call (computed once per call)."""
@@ -1337,6 +1378,7 @@ class Cluster:
             self._prepare_tables(st)
         main.wait_stream(side)
         _record_stream(st.__dict__, main)  # side-stream allocations are used on main
+        check(_lib.lib().smx_check_device_errors(sk), "construction")  # asynchronous draws
         if n and int(st.first_index[-1].item()) != n:
             raise ConsistencyError(f"record source beyond node count {n_nodes}")
         # record lists are dropped only after the sort has consumed them

@@ -912,14 +912,20 @@ class Cluster:
             tgt_bits[tr] = (vb, present)
         for (tr, _), vb in zip(pending, self._replay_finish([R for _, R in pending])):
             tgt_bits[tr] = (vb, None)
+        # presence of every source rank in the replayed targets' draws: one sync
+        todo = [tr for tr, (vb, pr) in tgt_bits.items() if pr is None]
+        if todo:
+            flags = torch.stack([torch.stack([tgt_bits[tr][0][w0: w0 + nw].ne(0).any()
+                                              for w0, nw in (seg_words[r] for r in ranks_sorted)])
+                                 for tr in todo]).cpu().numpy()
+            for tr, f in zip(todo, flags):
+                tgt_bits[tr] = (tgt_bits[tr][0], [r for r, a in zip(ranks_sorted, f) if a])
         # counters, in the reference's (target, source-rank) call order
         for tr, tg in target_pops:
             tr = int(tr)
             if tr not in tgt_bits:
                 continue
             vb, present = tgt_bits[tr]
-            if present is None:
-                present = self._present_ranks(vb, ranks_sorted, seg_words)
             for sr in present:
                 if sr == tr:
                     self.local_ctr[tr] += 1

@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--prop-warmup-ms", type=float, default=20.0)
     ap.add_argument("--seed", type=int, default=12345)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: --neurons is the whole network, split over the GPUs")
     ap.add_argument("--cpu-sample-neurons", type=int, default=10_000)
     return ap.parse_args()
 
@@ -191,8 +193,9 @@ def run_ours(args):
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     cfg = api.SimConfig(n_ranks=world, comm_mode="collective" if world > 1 else "p2p", seed=args.seed)
-    params = models.BalancedParams(neurons_per_rank=args.neurons, k_exc=args.k_exc, k_inh=args.k_inh)
-    syn_per_rank = args.neurons * (args.k_exc + args.k_inh)
+    n_rank = args.neurons // world if args.strong else args.neurons
+    params = models.BalancedParams(neurons_per_rank=n_rank, k_exc=args.k_exc, k_inh=args.k_inh)
+    syn_per_rank = n_rank * (args.k_exc + args.k_inh)
 
     def barrier():
         if world > 1:
@@ -260,8 +263,10 @@ def run_ours(args):
     line = {
         "metric": "construction_synapses_per_s", "value": value, "unit": "synapses/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
-        "config": {"workload": "hpc_benchmark_C3_weak", "neurons_per_gpu": args.neurons,
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "u32/f64",
+        "data": "synthetic",
+        "config": {"workload": "hpc_benchmark_C3_strong" if args.strong else "hpc_benchmark_C3_weak",
+                   "neurons_per_gpu": n_rank,
                    "k_in": args.k_exc + args.k_in if False else args.k_exc + args.k_inh,
                    "synapses_per_gpu": syn_per_rank, "comm": cfg.comm_mode, "parallelism": f"ranks{world}",
                    "l2": "inputs larger than L2 (tables 4.5 GB per GPU)", "seed": args.seed},

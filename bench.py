@@ -267,7 +267,7 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": "hpc_benchmark_C3_strong" if args.strong else "hpc_benchmark_C3_weak",
                    "neurons_per_gpu": n_rank,
-                   "k_in": args.k_exc + args.k_in if False else args.k_exc + args.k_inh,
+                   "k_in": args.k_exc + args.k_inh,
                    "synapses_per_gpu": syn_per_rank, "comm": cfg.comm_mode, "parallelism": f"ranks{world}",
                    "l2": "inputs larger than L2 (tables 4.5 GB per GPU)", "seed": args.seed},
         "construction_wall_s": float(np.mean(wall_s)),

@@ -317,6 +317,7 @@ class Cluster:
         self.dist_ctr = 0
         self.groups: dict[int, tuple] = {}
         self.params: list[LifParams] = []
+        self._ref_min = None
         self.param_index: dict = {}
         self.classes: list[tuple] = []      # (weight, delay, port)
         self.class_index: dict = {}
@@ -411,6 +412,10 @@ class Cluster:
                 if len(gids) != n:
                     raise ValueError("gids must have one entry per neuron")
             self.n_nodes[rank] = start + n
+            # smallest refractory period of the whole network (every process
+            # runs the script): bounds the spikes per neuron in an exchange block
+            ref = int(round(params.t_ref / self.cfg.resolution_ms))
+            self._ref_min = ref if self._ref_min is None else min(self._ref_min, ref)
             if not self.is_local(rank):
                 return range(start, start + n)
             st = self.ranks[rank]
@@ -543,14 +548,14 @@ class Cluster:
             meta = (np.broadcast_to(dv, (n,)).astype(np.int64) & ROW_MASK) | (port << 24)
             seg_m.copy_(_up(meta.astype(np.uint32).view(np.int32), seg_m.device))
 
-    def _write_syn_random(self, st: _Rank, syn: SynSpec, port: int, base: int, n: int, syn_key):
+    def _write_syn_random(self, st: _Rank, syn: SynSpec, port: int, base: int, n: int, syn_key, out=None):
         """Random syn specs drawn on the device from the call's syn stream:
         normal weights (next64 words) then uniform_int delays continuing at
-        the next u32 (sm/construction.py:157-176)."""
+        the next u32 (sm/construction.py:157-176).  out: (weights, meta)
+        tensors to fill instead of the record range [base, base + n)."""
         dev = st.device
         w, d = syn.weight, syn.delay_steps
-        seg_w = st.w_w.t[base: base + n]
-        seg_m = st.w_meta.t[base: base + n]
+        seg_w, seg_m = out if out is not None else (st.w_w.t[base: base + n], st.w_meta.t[base: base + n])
         if port > 255:
             raise DelayRangeError("port > 255 not representable")
         u32 = 0
@@ -844,8 +849,11 @@ class Cluster:
         if not src_nodes or any(len(a) == 0 for a in src_nodes):
             raise ValueError("source populations must be non-empty")
         syn.validate()
-        if not syn.is_constant:
-            raise NotImplementedError("random / per-record SynSpec in the distributed rule is not implemented yet")
+        if not syn.is_constant and (not isinstance(syn.weight, (tuple, float, int)) or
+                                    not isinstance(syn.delay_steps, (tuple, int, np.integer))):
+            # per-record arrays cannot match every source-rank batch (the
+            # reference's _realize_syn raises on the first length mismatch)
+            raise ValueError("per-record weight/delay arrays are not valid in the distributed rule")
         all_rank = np.concatenate([np.full(len(a), r, dtype=np.int32) for r, a in zip(src_ranks, src_nodes)])
         all_node = np.concatenate(src_nodes)
         total = len(all_node)
@@ -873,6 +881,8 @@ class Cluster:
             seg_words[r] = (acc, _words(span[r]))
             acc += _words(span[r])
         total_words = acc
+        self._dist_arrays = (all_rank, all_node)
+        self._seg_nwords = {r: nw for r, (w0, nw) in seg_words.items()}
         n_created = 0
         members = self.groups.get(group) if group != POINT_TO_POINT else None
         if group != POINT_TO_POINT and members is None:
@@ -1112,7 +1122,10 @@ class Cluster:
                  int(vbase[tr]), 0, sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
-        if st.wide:
+        if st.wide and not syn.is_constant:
+            self._dist_syn(st, syn, port, key, tr, total, n, base, runs, vbase, total_words, ranks_sorted,
+                           pos if not multi else None, None if multi else gv_tab)
+        elif st.wide:
             self._write_syn(st, syn, port, base, n, None)
         st.commit_records(n)
         if present is None:
@@ -1131,6 +1144,59 @@ class Cluster:
         self._dist_accounting(st, tr, group, n, base, present, runs, pieces, tmp_keys, lut_base, vbase,
                               seg_words)
         return vbits, present
+
+    def _dist_syn(self, st, syn, port, key, tr, total, n, base, runs, vbase, total_words, ranks_sorted,
+                  pos, gv_tab):
+        """Random weights / delays of a distributed call (sm/construction.py:
+        689-703): the reference appends one batch per source rank, its records
+        in (source rank, source) order (stable lexsort of the draws), and draws
+        each batch's syn values from that batch's stream -- ("syn-local", r, c)
+        for its own rank, ("remote-syn", s, r, idx) for the others.  Here the
+        call's draws are regenerated as global source values gv (ascending in
+        (rank, source)), stably sorted, the batches drawn in sorted order and
+        scattered back to the records."""
+        dev, sk = st.device, st.stream
+        gvk = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        if pos is not None:  # choice rows: the drawn positions are already here
+            gvk[:n] = gv_tab[pos[:n].long()]
+        elif runs is not None:
+            starts, rks, nds = runs
+            gvp = self._pack_pieces(starts, np.asarray(vbase, np.int64)[rks] + nds)
+            call("smx_gen_draw", key[0], key[1], 0, total, n, 3, 0, gvp.ctypes.data, 0, 1, _ptr(gvk), 0, 0, 0, 0, 0,
+                 0, 0, 0, sk)
+        else:
+            gv_all = self._dist_tables(dev, sk, tr, total, *self._dist_arrays, vbase, 0)[1]
+            call("smx_gen_draw", key[0], key[1], 0, total, n, 1, 0, _ptr(gv_all), 0, 1, _ptr(gvk), 0, 0, 0, 0, 0,
+                 0, 0, 0, sk)
+        nv = max(total_words * 32, 1)
+        scratch = torch.empty(2 * max(n, 1), dtype=torch.int32, device=dev)
+        idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        counts = torch.empty(nv, dtype=torch.int32, device=dev)
+        which = np.zeros(1, dtype=np.int32)
+        call("smx_sort_records", _ptr(gvk), _ptr(idx), _ptr(scratch), _ptr(scratch[max(n, 1):]), n,
+             max(1, int(nv - 1).bit_length()), 1, 0, _ptr(counts), nv, which.ctypes.data, sk)
+        order = (scratch[max(n, 1):] if which[0] else idx)[:n].long()
+        per_rank = {}
+        csum = torch.cumsum(counts.long(), 0)
+        for r in ranks_sorted:
+            lo = int(vbase[r])
+            per_rank[r] = (lo, lo + 32 * int(self._seg_nwords[r]))
+        zero = torch.zeros((), dtype=csum.dtype, device=dev)
+        bounds = torch.stack([torch.stack([csum[lo - 1] if lo else zero, csum[hi - 1]])
+                              for lo, hi in per_rank.values()]).cpu().numpy()
+        tmp_w = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        tmp_m = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        for r, (b0, b1) in zip(per_rank, bounds):
+            b0, b1 = int(b0), int(b1)
+            if b1 <= b0:
+                continue
+            if r == tr:
+                skey = self._key(("syn-local", tr, self.local_ctr[tr] + 1))
+            else:
+                skey = self._key(("remote-syn", r, tr, self.pair_ctr.get((r, tr), 0) + 1))
+            self._write_syn_random(st, syn, port, 0, b1 - b0, skey, out=(tmp_w[b0:b1], tmp_m[b0:b1]))
+        st.w_w.t[base: base + n][order] = tmp_w[:n]
+        st.w_meta.t[base: base + n][order] = tmp_m[:n]
 
     def _dist_accounting(self, st, tr, group, n, base, present, runs, pieces, tmp_keys, lut_base, vbase,
                          seg_words):
@@ -1847,22 +1913,23 @@ class Cluster:
         has exactly the source's mirror entries."""
         dev = st.device
         me = st.rank
-        ref_min = int(st.ref_steps.min().item()) if st.N else 0
+        ref_min = max(self._ref_min or 0, 0)   # network-wide: both sides of a round agree
         m = -(-self.block // (ref_min + 1))
         plan = dict(groups={}, m=m)
         for g in self.group_ids:
             members = sorted(self.groups[g])
             if me not in members:
                 continue
-            cap = max([int(st.H[(g, sr)].numel()) for sr in members if (g, sr) in st.H] + [0]) * m
-            cap = min(max(cap, 1), st.pk_cap)
+            # identical on every member (no local clamp: sizes must agree)
+            cap = max(max([int(st.H[(g, sr)].numel()) for sr in members if (g, sr) in st.H] + [0]) * m, 1)
             plan["groups"][g] = dict(members=members, cap=cap,
                                      send=torch.zeros(2 + 2 * cap, dtype=torch.int32, device=dev),
                                      recv=torch.zeros(len(members) * (2 + 2 * cap), dtype=torch.int32, device=dev))
         if self.has_p2p:
-            out_c = [min(int(st.S[d].numel()) * m, st.pk_cap) if d in st.S and d != me else 0
-                     for d in range(self.n_ranks)]
-            in_c = [min(int(st.RL[(POINT_TO_POINT, s)][0].numel()) * m, st.pk_cap)
+            # a sender's mirror and the receiver's map hold the same sources, so
+            # both sides derive the same size (no local clamp)
+            out_c = [int(st.S[d].numel()) * m if d in st.S and d != me else 0 for d in range(self.n_ranks)]
+            in_c = [int(st.RL[(POINT_TO_POINT, s)][0].numel()) * m
                     if (POINT_TO_POINT, s) in st.RL and s != me else 0 for s in range(self.n_ranks)]
             out_sz = [2 + 2 * c if c else 0 for c in out_c]
             in_sz = [2 + 2 * c if c else 0 for c in in_c]
@@ -1895,7 +1962,8 @@ class Cluster:
                 if not c:
                     continue
                 send[off: off + 1].copy_(st.p2p_counts[d: d + 1])
-                send[off + 2: off + 2 + 2 * c].copy_(st.p2p_packets[d * st.pk_cap * 2: d * st.pk_cap * 2 + 2 * c])
+                cc = min(c, st.pk_cap)  # packets written never exceed the per-destination stride
+                send[off + 2: off + 2 + 2 * cc].copy_(st.p2p_packets[d * st.pk_cap * 2: d * st.pk_cap * 2 + 2 * cc])
                 X["over"].bitwise_or_((st.p2p_counts[d: d + 1] > c).to(torch.int32))
                 off += P["out_sz"][d]
             X["sent"] += st.p2p_counts.sum()
@@ -1915,7 +1983,8 @@ class Cluster:
             slot, cap, members = self.group_slots[g], G["cap"], G["members"]
             send, recv = G["send"], G["recv"]
             send[0:1].copy_(st.g_counts[slot: slot + 1])
-            send[2:].copy_(st.g_packets[slot * st.pk_cap * 2: slot * st.pk_cap * 2 + 2 * cap])
+            cc = min(cap, st.pk_cap)
+            send[2: 2 + 2 * cc].copy_(st.g_packets[slot * st.pk_cap * 2: slot * st.pk_cap * 2 + 2 * cc])
             X["over"].bitwise_or_((st.g_counts[slot: slot + 1] > cap).to(torch.int32))
             X["sent"] += st.g_counts[slot]
             dist.all_gather_into_tensor(recv, send, group=self._pg[g])

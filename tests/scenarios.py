@@ -118,6 +118,30 @@ def no_multapse(ns, mode="p2p", seed=21):
     return c, (0.0, 5.0)
 
 
+def dist_random(ns, mode="p2p", seed=31):
+    """Random SynSpec in the distributed rule: each source-rank batch draws its
+    weights / delays from its own stream in (rank, source) order
+    (sm/construction.py:689-703); a remote call first leaves pre-existing
+    images (non-consecutive image ids), the second call is without multapses."""
+    cfg = ns.SimConfig(n_ranks=3, comm_mode=mode, seed=seed)
+    c = ns.make_cluster(cfg)
+    group = -1
+    if mode == "collective":
+        group = 0
+        c.declare_group(0, [0, 1, 2])
+    pops = []
+    for r in range(3):
+        x = c.create_neurons(r, 60, ns.LifParams(i_e=0.25), ("normal", -58.0, 4.0), gids=r * 60 + np.arange(60))
+        pops.append(np.arange(x.start, x.stop))
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    c.connect_remote(1, pops[1][::3], 0, pops[0][:20], S("fixed_indegree", k_in=3), Sy(0.125, 3), group=group)
+    c.connect_fixed_indegree_distributed([(r, pops[r]) for r in range(3)], [(r, pops[r]) for r in range(3)], 12,
+                                         Sy(("normal", 0.1, 0.02), ("uniform_int", 2, 6)), group=group)
+    c.connect_fixed_indegree_distributed([(0, pops[0][:30]), (2, pops[2])], [(1, pops[1]), (2, pops[2][:25])], 7,
+                                         Sy(-0.25, ("uniform_int", 3, 5)), group=group, allow_multapses=False)
+    return c, (0.0, 5.0)
+
+
 def poisson_multi(ns, mode="p2p", seed=12):
     """Several Poisson devices per rank with overlapping, permuted targets and
     delays below / above the exchange block (all records delay >= 5, so ranks
@@ -233,8 +257,11 @@ SCENARIOS = {
     "poisson_multi_coll": lambda ns: poisson_multi(ns, "collective"),
     "no_multapse_p2p": lambda ns: no_multapse(ns, "p2p"),
     "no_multapse_coll": lambda ns: no_multapse(ns, "collective"),
+    "dist_random_p2p": lambda ns: dist_random(ns, "p2p"),
+    "dist_random_coll": lambda ns: dist_random(ns, "collective"),
 }
 
 # scenarios whose weights are not dyadic: tables are bit-exact, the raster is
 # compared with a tolerance (fp64 sums depend on the atomic delivery order)
-NON_DYADIC = {"rules_random", "remote_random_p2p", "remote_random_coll", "microcircuit_small", "rules_no_autapse"}
+NON_DYADIC = {"rules_random", "remote_random_p2p", "remote_random_coll", "microcircuit_small", "rules_no_autapse",
+              "dist_random_p2p", "dist_random_coll"}

@@ -12,8 +12,8 @@ pytestmark = pytest.mark.gpu
 
 CASES = {
     2: ["balanced_2r_p2p", "balanced_2r_sparse_coll", "explicit_2r_coll", "multi_area_2r", "multi_area_2r_coll",
-        "poisson_multi_p2p", "poisson_multi_coll"],
-    3: ["remote_p2p", "remote_coll", "explicit_3r_p2p", "explicit_3r_coll"],
+        "poisson_multi_p2p", "poisson_multi_coll", "no_multapse_p2p", "no_multapse_coll"],
+    3: ["remote_p2p", "remote_coll", "explicit_3r_p2p", "explicit_3r_coll", "dist_random_p2p", "dist_random_coll"],
     4: ["balanced_4r_p2p", "balanced_4r_coll"],
 }
 

@@ -64,6 +64,10 @@ int smx_poisson_chunks_for(uint64_t n, double lam);
 int smx_poisson_counts(uint64_t k0, uint64_t k1, const uint64_t* cursor_in, double enlam, uint64_t n,
                        int n_chunks, void* workspace, uint8_t* counts, uint64_t* cursor_out, int* err,
                        void* stream);
+/* lam >= 10: numpy random_poisson_ptrs (two words per trial), same chain
+ * machinery and contract; counts above 255 set the error flag. */
+int smx_poisson_counts_ptrs(uint64_t k0, uint64_t k1, const uint64_t* cursor_in, double lam, uint64_t n,
+                            int n_chunks, void* ws, uint8_t* counts, uint64_t* cursor_out, int* err, void* stream);
 
 /* --- construction ---------------------------------------------------------
  * Replaces sm/construction.py:391-703 (rule realization, flag/extract,

@@ -219,8 +219,57 @@ void orc_uniform(orc_stream *s, double lo, double hi, int64_t n, double *out) {
 
 /* poisson(lam) for 0 <= lam < 10 with enlam = exp(-lam) supplied by the
  * caller (the host's libm, as numpy computes it). */
+/* numpy random_loggam: log Gamma(x) by the Stirling series, shifted up to
+ * x >= 7 (numpy/random/src/distributions/distributions.c). */
+double orc_loggam(double x) {
+  static const double a[10] = {8.333333333333333e-02, -2.777777777777778e-03, 7.936507936507937e-04,
+                               -5.952380952380952e-04, 8.417508417508418e-04, -1.917526917526918e-03,
+                               6.410256410256410e-03, -2.955065359477124e-02, 1.796443723688307e-01,
+                               -1.39243221690590e+00};
+  if (x == 1.0 || x == 2.0) return 0.0;
+  int64_t n = x < 7.0 ? (int64_t)(7 - x) : 0;
+  double x0 = x + (double)n;
+  const double x2 = (1.0 / x0) * (1.0 / x0);
+  const double lg2pi = 1.8378770664093453e+00;
+  double gl0 = a[9];
+  for (int k = 8; k >= 0; --k) {
+    gl0 *= x2;
+    gl0 += a[k];
+  }
+  double gl = gl0 / x0 + 0.5 * lg2pi + (x0 - 0.5) * log(x0) - x0;
+  if (x < 7.0) {
+    for (int64_t k = 1; k <= n; ++k) {
+      gl -= log(x0 - 1.0);
+      x0 -= 1.0;
+    }
+  }
+  return gl;
+}
+
+/* numpy random_poisson_ptrs (lam >= 10): Hoermann's transformed rejection,
+ * two doubles per trial. */
+int64_t orc_poisson_ptrs(orc_stream *s, double lam) {
+  const double slam = sqrt(lam);
+  const double loglam = log(lam);
+  const double b = 0.931 + 2.53 * slam;
+  const double a = -0.059 + 0.02483 * b;
+  const double invalpha = 1.1239 + 1.1328 / (b - 3.4);
+  const double vr = 0.9277 - 3.6224 / (b - 2);
+  for (;;) {
+    const double U = orc_next_double(s) - 0.5;
+    const double V = orc_next_double(s);
+    const double us = 0.5 - fabs(U);
+    const int64_t k = (int64_t)floor((2 * a / us + b) * U + lam + 0.43);
+    if ((us >= 0.07) && (V <= vr)) return k;
+    if ((k < 0) || ((us < 0.013) && (V > us))) continue;
+    if ((log(V) + log(invalpha) - log(a / (us * us) + b)) <= (-lam + (double)k * loglam - orc_loggam((double)k + 1)))
+      return k;
+  }
+}
+
 int orc_poisson(orc_stream *s, double lam, double enlam, int64_t n, int64_t *out) {
-  if (!(lam >= 0.0) || lam >= 10.0) return -1;
+  if (!(lam >= 0.0)) return -1;
+  if (lam >= 10.0) { for (int64_t i = 0; i < n; ++i) out[i] = orc_poisson_ptrs(s, lam); return 0; }
   if (lam == 0.0) { for (int64_t i = 0; i < n; ++i) out[i] = 0; return 0; }
   for (int64_t i = 0; i < n; ++i) {
     int64_t x = 0;

@@ -148,7 +148,7 @@ class OracleStream:
         if n:
             rc = lib().orc_poisson(self._p, float(lam), math.exp(-float(lam)), n, out.ctypes.data)
             if rc:
-                raise ValueError("oracle poisson supports 0 <= lam < 10")
+                raise ValueError("lam < 0")
         return int(out[0]) if size is None else out
 
 

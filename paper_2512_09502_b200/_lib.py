@@ -63,6 +63,7 @@ SIGNATURES = {
     "smx_poisson_workspace": (U64, [I32]),
     "smx_poisson_chunks_for": (I32, [U64, D]),
     "smx_poisson_counts": (I32, [U64, U64, P, D, U64, I32, P, P, P, P, P]),
+    "smx_poisson_counts_ptrs": (I32, [U64, U64, P, D, U64, I32, P, P, P, P, P]),
     "smx_spikes": (I32, [P, U32, P, P, P, P, P, P, U32, P, P, P, U64, P, P, P, P, P]),
     "smx_step": (I32, [P, P, P, P, P, P, P, P, U32, P, I32, I32, P, I32, P, I32, P, I32, P, P, P, P, P, P, P, U32, P,
                         U32, P, P, U64, P, P, P, P, P, P, P, P, P, P]),

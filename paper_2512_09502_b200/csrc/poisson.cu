@@ -31,8 +31,9 @@ constexpr int P_THREADS = 128;
 struct PoisJob {
   smx::Key key;
   const uint64_t* w0_dev;  // word cursor before the batch (device)
-  int kind;           // 0 = poisson counts (u8), 1 = normal(loc, scale) (f64)
+  int kind;           // 0 = poisson counts (u8), 1 = normal(loc, scale) (f64), 2 = poisson PTRS (u8)
   double enlam;       // exp(-lam), computed by the host's libm like numpy
+  double lam, slam, loglam, pa, pb, invalpha, vr;  // PTRS constants (lam >= 10)
   double loc, scale;
   uint64_t n;         // samples wanted
   int n_chunks;
@@ -48,6 +49,45 @@ struct PoisJob {
   uint64_t* cursor;   // word after the n-th sample
   int* err;
 };
+
+// numpy random_loggam (Stirling series shifted to x >= 7), fp64 without FMA
+__device__ double loggam(double x) {
+  const double a[10] = {8.333333333333333e-02, -2.777777777777778e-03, 7.936507936507937e-04,
+                        -5.952380952380952e-04, 8.417508417508418e-04, -1.917526917526918e-03,
+                        6.410256410256410e-03, -2.955065359477124e-02, 1.796443723688307e-01,
+                        -1.39243221690590e+00};
+  if (x == 1.0 || x == 2.0) return 0.0;
+  const long long n = x < 7.0 ? (long long)(7 - x) : 0;
+  double x0 = __dadd_rn(x, (double)n);
+  const double r = __ddiv_rn(1.0, x0);
+  const double x2 = __dmul_rn(r, r);
+  double gl0 = a[9];
+  for (int k = 8; k >= 0; --k) gl0 = __dadd_rn(__dmul_rn(gl0, x2), a[k]);
+  double gl = __dadd_rn(__dadd_rn(__dadd_rn(__ddiv_rn(gl0, x0), __dmul_rn(0.5, 1.8378770664093453e+00)),
+                                  __dmul_rn(__dadd_rn(x0, -0.5), log(x0))), -x0);
+  if (x < 7.0) {
+    for (long long k = 1; k <= n; ++k) {
+      gl = __dadd_rn(gl, -log(__dadd_rn(x0, -1.0)));
+      x0 = __dadd_rn(x0, -1.0);
+    }
+  }
+  return gl;
+}
+
+// One PTRS trial on (next_double, next_double) = (u, v): returns true and the
+// count when accepted (numpy random_poisson_ptrs; log is CUDA's, <= 1 ulp).
+__device__ __forceinline__ bool ptrs_trial(const PoisJob& J, double u, double v, long long& k) {
+  const double U = __dadd_rn(u, -0.5);
+  const double us = __dadd_rn(0.5, -fabs(U));
+  k = (long long)floor(__dadd_rn(__dadd_rn(__dmul_rn(__dadd_rn(__ddiv_rn(__dmul_rn(2.0, J.pa), us), J.pb), U), J.lam),
+                                 0.43));
+  if (us >= 0.07 && v <= J.vr) return true;
+  if (k < 0 || (us < 0.013 && v > us)) return false;
+  const double lhs = __dadd_rn(__dadd_rn(log(v), log(J.invalpha)),
+                               -log(__dadd_rn(__ddiv_rn(J.pa, __dmul_rn(us, us)), J.pb)));
+  const double rhs = __dadd_rn(__dadd_rn(-J.lam, __dmul_rn((double)k, J.loglam)), -loggam(__dadd_rn((double)k, 1.0)));
+  return lhs <= rhs;
+}
 
 __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
   __shared__ double U[PC + PE];
@@ -85,6 +125,17 @@ __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
         ++k;
         if (!(prod > J.enlam)) break;
         if (k >= 255) break;
+      }
+    } else if (J.kind == 2) {
+      // PTRS: two doubles per trial until one is accepted
+      for (;;) {
+        const int i0 = w + k, i1 = w + k + 1;
+        const double u = i0 < PC + PE ? U[i0] : smx::u53(smx::philox_word(J.key, cw + i0));
+        const double v = i1 < PC + PE ? U[i1] : smx::u53(smx::philox_word(J.key, cw + i1));
+        k += 2;
+        long long cnt;
+        if (ptrs_trial(J, u, v, cnt)) break;
+        if (k >= 254) break;
       }
     } else {
       // ziggurat: one word on the fast path, else run the sampler to count
@@ -257,6 +308,12 @@ __device__ __forceinline__ void emit(const PoisJob& J, uint64_t k, int c, int p,
     const uint64_t start = (*J.w0_dev & ~3ULL) + (uint64_t)c * PC + p;
     if (J.kind == 0) {
       static_cast<uint8_t*>(J.out)[k] = (uint8_t)(len - 1);
+    } else if (J.kind == 2) {  // PTRS: the count of the accepted (last) trial
+      const double u = smx::u53(smx::philox_word(J.key, start + len - 2));
+      const double v = smx::u53(smx::philox_word(J.key, start + len - 1));
+      long long cnt = 0;
+      if (!ptrs_trial(J, u, v, cnt) || cnt < 0 || cnt > 255) atomicExch(J.err, 14);  // u8 counts
+      static_cast<uint8_t*>(J.out)[k] = (uint8_t)cnt;
     } else {  // numpy random_normal: loc + scale * z, no FMA
       smx::SeqStream st;
       st.init(J.key, start);
@@ -321,7 +378,10 @@ extern "C" uint64_t smx_poisson_workspace(int n_chunks) {
 }
 
 extern "C" int smx_poisson_chunks_for(uint64_t n, double lam) {
-  const double words = (double)n * (1.0 + lam) + 10.0 * sqrt((double)n * (lam + 1.0)) + 2.0 * PC + PE;
+  // multiplication method: lam + 1 words per sample; PTRS (lam >= 10): two
+  // words per trial, about 1.2 trials per sample
+  const double per = lam >= 10.0 ? 3.0 : 1.0 + lam;
+  const double words = (double)n * per + 10.0 * sqrt((double)n * per) + 2.0 * PC + PE;
   return (int)((words + PC - 1) / PC);
 }
 
@@ -340,6 +400,58 @@ extern "C" int smx_poisson_counts(uint64_t k0, uint64_t k1, const uint64_t* curs
   J.kind = 0;
   J.enlam = enlam;
   J.loc = J.scale = 0.0;
+  J.n = n;
+  J.n_chunks = n_chunks;
+  const int ng = (n_chunks + PG - 1) / PG;
+  uint8_t* p = (uint8_t*)ws;
+  J.len = p; p += (size_t)n_chunks * PC;
+  J.s0 = (uint32_t*)p; p += (size_t)n_chunks * (PC / 32) * 4;
+  J.cnt = (uint16_t*)p; p += (size_t)n_chunks * PE * 2;
+  J.gcnt = (uint32_t*)p; p += (size_t)ng * PE * 4;
+  J.kbase = (uint64_t*)p; p += (size_t)n_chunks * 8;
+  uint64_t* gbase = (uint64_t*)p; p += (size_t)ng * 8;
+  J.ex = p; p += (size_t)n_chunks * PE;
+  J.gex = p; p += (size_t)ng * PE;
+  J.entry = p; p += (size_t)n_chunks;
+  uint8_t* gentry = p; p += (size_t)ng;
+  J.out = counts;
+  J.cursor = cursor_out;
+  J.err = err;
+  smx_count_launch(); chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
+  smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
+  smx_count_launch(); within_kernel<<<ng, PE, 0, st>>>(J, gentry, gbase);
+  smx_count_launch(); emit_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+// counts[0..n) = numpy poisson(lam) samples for lam >= 10 (random_poisson_ptrs,
+// two words per trial), same chain machinery and contract as smx_poisson_counts;
+// counts above 255 raise the error flag (u8 counts).
+extern "C" int smx_poisson_counts_ptrs(uint64_t k0, uint64_t k1, const uint64_t* cursor_in, double lam, uint64_t n,
+                                       int n_chunks, void* ws, uint8_t* counts, uint64_t* cursor_out, int* err,
+                                       void* stream) {
+  if (n == 0) return 0;
+  if (!(lam >= 10.0)) {
+    smx_set_error("smx_poisson_counts_ptrs: lam %g < 10", lam);
+    return -1;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  PoisJob J;
+  J.key = smx::Key{k0, k1};
+  J.w0_dev = cursor_in;
+  J.kind = 2;
+  J.enlam = 0.0;
+  J.loc = J.scale = 0.0;
+  // the constants of random_poisson_ptrs, on the host like numpy's C code
+  J.lam = lam;
+  J.slam = sqrt(lam);
+  J.loglam = log(lam);
+  J.pb = 0.931 + 2.53 * J.slam;
+  J.pa = -0.059 + 0.02483 * J.pb;
+  J.invalpha = 1.1239 + 1.1328 / (J.pb - 3.4);
+  J.vr = 0.9277 - 3.6224 / (J.pb - 2);
   J.n = n;
   J.n_chunks = n_chunks;
   const int ng = (n_chunks + PG - 1) / PG;

@@ -60,7 +60,8 @@ class PoissonStream:
         out = torch.empty(max(n, 1), dtype=torch.uint8, device=self.dev)
         cin = self.cursor[self.ping:]
         cout = self.cursor[1 - self.ping:]
-        call("smx_poisson_counts", self.key[0], self.key[1], cin.data_ptr(), self.enlam, n, chunks,
+        fn, par = ("smx_poisson_counts_ptrs", self.lam) if self.lam >= 10.0 else ("smx_poisson_counts", self.enlam)
+        call(fn, self.key[0], self.key[1], cin.data_ptr(), par, n, chunks,
              ws.data_ptr(), out.data_ptr(), cout.data_ptr(), self.err.data_ptr(), _stream(self.dev))
         self.ping = 1 - self.ping
         if int(self.err.item()):

@@ -466,8 +466,6 @@ class Cluster:
             if len(targets) and (targets.min() < 0 or targets.max() >= self.n_nodes[rank]):
                 raise ValueError("poisson targets outside the rank's node range")
             lam = float(rate_hz) * self.cfg.resolution_ms * 1e-3
-            if lam >= 10.0:
-                raise NotImplementedError("poisson drive with lam >= 10 (numpy PTRS) is not implemented")
             if not self.is_local(rank):
                 return None
             st = self.ranks[rank]
@@ -1668,7 +1666,8 @@ class Cluster:
                 continue
             cin = d["cursor"][d["ping"]:]
             cout = d["cursor"][1 - d["ping"]:]
-            call("smx_poisson_counts", d["key"][0], d["key"][1], _ptr(cin), d["enlam"], S * d["nt"],
+            fn, par = ("smx_poisson_counts_ptrs", d["lam"]) if d["lam"] >= 10.0 else ("smx_poisson_counts", d["enlam"])
+            call(fn, d["key"][0], d["key"][1], _ptr(cin), par, S * d["nt"],
                  d["chunks"], _ptr(d["ws"]), _ptr(d["counts"][half * S * d["nt"]:]), _ptr(cout), _ptr(st.err),
                  stream.cuda_stream)
             d["ping"] = 1 - d["ping"]

@@ -118,6 +118,21 @@ def no_multapse(ns, mode="p2p", seed=21):
     return c, (0.0, 5.0)
 
 
+def poisson_high(ns, seed=41):
+    """Poisson drive with lam >= 10 (numpy's PTRS branch, two words per
+    trial): lam = 12 and 35 per step next to a lam = 1.1 device."""
+    cfg = ns.SimConfig(n_ranks=1, seed=seed)
+    c = ns.make_cluster(cfg)
+    a = c.create_neurons(0, 200, ns.LifParams(), ("normal", -60.0, 3.0), gids=np.arange(200))
+    A = np.arange(a.start, a.stop)
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    c.add_poisson_source(0, 120_000.0, 0.03125, 2, A[:120])
+    c.add_poisson_source(0, 350_000.0, 0.015625, 3, A[60:])
+    c.add_poisson_source(0, 11_000.0, 0.125, 4, A[::2])
+    c.connect(0, A, A, S("fixed_indegree", k_in=20), Sy(-0.125, 2))
+    return c, (0.0, 10.0)
+
+
 def dist_random(ns, mode="p2p", seed=31):
     """Random SynSpec in the distributed rule: each source-rank batch draws its
     weights / delays from its own stream in (rank, source) order
@@ -257,6 +272,7 @@ SCENARIOS = {
     "poisson_multi_coll": lambda ns: poisson_multi(ns, "collective"),
     "no_multapse_p2p": lambda ns: no_multapse(ns, "p2p"),
     "no_multapse_coll": lambda ns: no_multapse(ns, "collective"),
+    "poisson_high": poisson_high,
     "dist_random_p2p": lambda ns: dist_random(ns, "p2p"),
     "dist_random_coll": lambda ns: dist_random(ns, "collective"),
 }

@@ -85,7 +85,8 @@ def test_poisson_golden_steps():
         assert np.array_equal(steps, z[f"s{i}/poisson_steps"])
 
 
-@pytest.mark.parametrize("lam,n,batches", [(1.1, 1_000_000, 3), (0.3, 200_000, 4), (6.5, 300_000, 2)])
+@pytest.mark.parametrize("lam,n,batches", [(1.1, 1_000_000, 3), (0.3, 200_000, 4), (6.5, 300_000, 2),
+                                           (10.0, 300_000, 2), (27.5, 300_000, 2), (150.0, 200_000, 2)])
 def test_poisson_vs_oracle_large(lam, n, batches):
     from oracle.rng import OracleStream
     from paper_2512_09502_b200 import device_rng as dr

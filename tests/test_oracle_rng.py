@@ -71,3 +71,13 @@ def test_choice_no_replace_matches_numpy(n, k):
     for _ in range(3):
         assert np.array_equal(o.choice_no_replace(n, k), g.choice(n, size=k, replace=False))
     assert o.next64() == int(g.bit_generator.random_raw())
+
+
+@pytest.mark.parametrize("lam", [10.0, 11.5, 30.0, 100.0, 1234.5])
+def test_poisson_ptrs_matches_numpy(lam):
+    """numpy random_poisson_ptrs (lam >= 10) restated: counts and cursor."""
+    from numpy.random import Generator, Philox
+    g = Generator(Philox(key=(5 << 64) | 9))
+    o = OracleStream(0, key=(9, 5))
+    assert np.array_equal(o.poisson(lam, size=50_000), g.poisson(lam, size=50_000))
+    assert o.next64() == int(g.bit_generator.random_raw())

@@ -114,8 +114,10 @@ def _words(nbits: int) -> int:
 
 @dataclass
 class PhaseTimers:
-    """sm/engine.py:40-52 (seconds; host wall clock around each façade call,
-    with a device synchronisation at the end of the phase)."""
+    """sm/engine.py:40-52 (seconds per phase).  A façade call is not
+    synchronised at its end -- the host prepares the next call while the
+    device works -- so each call records CUDA events on its streams; when the
+    timers are read, a call counts max(host time, device span of its work)."""
 
     initialization: float = 0.0
     node_creation: float = 0.0
@@ -123,9 +125,20 @@ class PhaseTimers:
     remote_connection: float = 0.0
     preparation: float = 0.0
     propagation: float = 0.0
+    _pending: list = field(default_factory=list, repr=False)
+
+    def resolve(self) -> None:
+        pending, self._pending = self._pending, []
+        for bucket, host_s, pairs in pending:
+            gpu_s = 0.0
+            for a, b in pairs:
+                b.synchronize()
+                gpu_s = max(gpu_s, a.elapsed_time(b) * 1e-3)
+            setattr(self, bucket, getattr(self, bucket) + max(host_s, gpu_s))
 
     def as_dict(self) -> dict:
-        return asdict(self)
+        self.resolve()
+        return {k: v for k, v in asdict(self).items() if not k.startswith("_")}
 
 
 @dataclass
@@ -341,13 +354,13 @@ class Cluster:
 
     @contextmanager
     def _timed(self, bucket):
+        starts = [(st, self._event(st)) for st in self.ranks.values()]
         t0 = time.perf_counter()
         try:
             yield
         finally:
-            for st in self.ranks.values():
-                torch.cuda.synchronize(st.device)
-            setattr(self.timers, bucket, getattr(self.timers, bucket) + time.perf_counter() - t0)
+            host_s = time.perf_counter() - t0
+            self.timers._pending.append((bucket, host_s, [(a, self._event(st)) for st, a in starts]))
 
     @staticmethod
     def _event(st):

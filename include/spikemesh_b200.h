@@ -130,6 +130,8 @@ int smx_assign_images(const uint32_t* vbits, uint64_t nwords, const void* segs_h
 int smx_gather_lut(const int64_t* sources, uint64_t n, const int32_t* img_of, uint32_t* lut, void* stream);
 /* mirror_merge / roster update (sm/construction.py:295-306, 633-636) */
 int smx_bits_or(uint32_t* dst, const uint32_t* src, uint64_t nwords, void* stream);
+/* dst |= src[0] | ... | src[n-1] (srcs_host: host array of device pointers) */
+int smx_bits_or_many(uint32_t* dst, const uint32_t* const* srcs_host, int n_srcs, uint64_t nwords, void* stream);
 int smx_bits_prefix(const uint32_t* bits, uint64_t nwords, int64_t* excl, void* stream);
 int smx_bits_compact(const uint32_t* bits, uint64_t nwords, const int64_t* excl, int64_t* out,
                      const int32_t* img_of, int64_t* img_out, void* stream);

@@ -573,6 +573,35 @@ extern "C" int smx_bits_or(uint32_t* dst, const uint32_t* src, uint64_t nwords, 
   return 0;
 }
 
+// dst |= src[0] | src[1] | ... (up to 64 sources, host array of device
+// pointers): the source-rank segments of several targets' used-value bitmaps
+// merged into one mirror / roster in one launch.
+constexpr int MAX_OR_SRCS = 64;
+struct OrSrcs {
+  const uint32_t* p[MAX_OR_SRCS];
+  int n;
+};
+__global__ void bits_or_many_kernel(uint32_t* dst, OrSrcs S, uint64_t nwords) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nwords) return;
+  uint32_t x = 0;
+  for (int i = 0; i < S.n; ++i) x |= S.p[i][w];
+  if (x) dst[w] |= x;
+}
+
+extern "C" int smx_bits_or_many(uint32_t* dst, const uint32_t* const* srcs_host, int n_srcs, uint64_t nwords,
+                                void* stream) {
+  if (nwords == 0 || n_srcs == 0) return 0;
+  for (int a = 0; a < n_srcs; a += MAX_OR_SRCS) {
+    OrSrcs S{};
+    S.n = std::min(MAX_OR_SRCS, n_srcs - a);
+    for (int i = 0; i < S.n; ++i) S.p[i] = srcs_host[a + i];
+    smx_count_launch(); bits_or_many_kernel<<<nblk(nwords), T256, 0, (cudaStream_t)stream>>>(dst, S, nwords);
+  }
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
 // Per-word exclusive popcount prefix of a bitmap (nwords + 1 entries).
 extern "C" int smx_bits_prefix(const uint32_t* bits, uint64_t nwords, int64_t* excl, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;

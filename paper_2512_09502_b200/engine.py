@@ -942,6 +942,7 @@ class Cluster:
             for tr, f in zip(todo, flags):
                 tgt_bits[tr] = (tgt_bits[tr][0], [r for r, a in zip(ranks_sorted, f) if a])
         # counters, in the reference's (target, source-rank) call order
+        ros_segs: dict = {}
         for tr, tg in target_pops:
             tr = int(tr)
             if tr not in tgt_bits:
@@ -969,10 +970,13 @@ class Cluster:
                 else:
                     for mbr in members:
                         if self.is_local(mbr):
-                            ms = self.ranks[mbr]
-                            ros = ms.rosters.setdefault((group, sr), _Bits(ms.device)).ensure(span[sr])
-                            seg = vb[w0: w0 + nw].to(ms.device)
-                            call("smx_bits_or", _ptr(ros.t), _ptr(seg), nw, ms.stream)
+                            ros_segs.setdefault((mbr, sr), []).append(vb[w0: w0 + nw].to(self.ranks[mbr].device))
+        # rosters: the segments of every target merged in one launch per (member, source rank)
+        for (mbr, sr), segs in ros_segs.items():
+            ms = self.ranks[mbr]
+            ros = ms.rosters.setdefault((group, sr), _Bits(ms.device)).ensure(span[sr])
+            ptrs = (ctypes.c_void_p * len(segs))(*[s.data_ptr() for s in segs])
+            call("smx_bits_or_many", _ptr(ros.t), ctypes.addressof(ptrs), len(segs), seg_words[sr][1], ms.stream)
         return n_created
 
     def _present_ranks(self, vb, ranks_sorted, seg_words):

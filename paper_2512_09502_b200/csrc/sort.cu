@@ -447,6 +447,135 @@ __global__ void __launch_bounds__(DS_THREADS, ds_ctas_per_sm(BITS)) downsweep_ke
   }
 }
 
+// Last pass of a multi-pass sort with wide digits (10-11 bits): (key, value)
+// records in, values out.  The staging reuses the TMA input buffer (values +
+// u16 digits) and the offset row is single-buffered, so the kernel needs
+// 30 + 4 + 4 + 16 KB of SMEM at 10 bits -- three CTAs per SM instead of two.
+// The next tile's records are fetched after the write phase (the other CTAs
+// of the SM cover the load); its offset row right after the scan.
+constexpr int ds_last_ctas_per_sm(int bits) { return bits <= 10 ? 3 : 2; }
+
+template <int BITS>
+__global__ void __launch_bounds__(DS_THREADS, ds_last_ctas_per_sm(BITS)) downsweep_last_kernel(
+    SortPass p, const uint32_t* off, uint32_t n_tiles, uint32_t* tile_ctr) {
+  constexpr int BINS = 1 << BITS;
+  constexpr int DPT = BINS / DS_THREADS;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint2* irec = reinterpret_cast<uint2*>(smem);                           // [DS_TILE] TMA target
+  uint32_t* sval = reinterpret_cast<uint32_t*>(smem);                     // staging, aliases irec
+  uint16_t* sdig = reinterpret_cast<uint16_t*>(sval + DS_TILE);           // staging digits
+  uint32_t* ioff = reinterpret_cast<uint32_t*>(smem + (size_t)DS_TILE * 8);  // [BINS] TMA target
+  uint32_t* delta = ioff + BINS;                                          // [BINS]
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(delta + BINS);             // [DS_WARPS][BINS]
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t ticket[2];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t mask = BINS - 1;
+  if (tid == 0) {
+    smx::mbar_init(&bar, 1);
+    smx::fence_mbar_init();
+  }
+  __syncthreads();
+  auto full_tile = [&](uint32_t t) { return (uint64_t)t * DS_TILE + DS_TILE <= p.n; };
+  if (tid == 0) {
+    const uint32_t t = atomicAdd(tile_ctr, 1u);
+    ticket[0] = t;
+    if (t < n_tiles) {
+      smx::mbar_expect_tx(&bar, BINS * 4 + (full_tile(t) ? DS_TILE * 8 : 0));
+      smx::bulk_g2s(ioff, off + (size_t)t * BINS, BINS * 4, &bar);
+      if (full_tile(t)) smx::bulk_g2s(irec, p.recs_in + (uint64_t)t * DS_TILE, DS_TILE * 8, &bar);
+    }
+  }
+  __syncthreads();
+  const uint32_t wofs = warp * (32 * DS_IPT) + lane;
+  uint16_t* mycnt = wcnt + warp * BINS;
+  uint32_t phase = 0;
+  int slot = 0;
+  for (uint32_t tile = ticket[0]; tile < n_tiles; tile = ticket[slot ^= 1]) {
+    const uint64_t t0 = (uint64_t)tile * DS_TILE;
+    const bool full = full_tile(tile);
+    uint32_t k[DS_IPT], v[DS_IPT];
+    smx::mbar_wait(&bar, phase);
+    phase ^= 1;
+#pragma unroll
+    for (int i = 0; i < DS_IPT; ++i) {
+      const uint32_t q = wofs + i * 32;
+      uint2 r;
+      if (full) r = irec[q];
+      else r = t0 + q < p.n ? p.recs_in[t0 + q] : make_uint2(0u, 0u);
+      k[i] = r.x;
+      v[i] = r.y;
+    }
+    {
+      uint32_t* w32 = reinterpret_cast<uint32_t*>(mycnt);
+#pragma unroll
+      for (int j = lane; j < BINS / 2; j += 32) w32[j] = 0;
+      __syncwarp();
+    }
+    uint32_t rank2[(DS_IPT + 1) / 2];
+    if (full) rank_tile<BITS, true>(k, rank2, mycnt, p.shift, 0, 0, lane);
+    else rank_tile<BITS, false>(k, rank2, mycnt, p.shift, t0 + wofs, p.n, lane);
+    __syncthreads();  // 1: counters complete, records in registers
+    if (tid == 0) ticket[slot ^ 1] = atomicAdd(tile_ctr, 1u);
+    uint32_t tot[DPT];
+    uint32_t mysum = 0;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const int d = tid * DPT + j;
+      uint32_t t = 0;
+#pragma unroll
+      for (int w = 0; w < DS_WARPS; ++w) t += wcnt[w * BINS + d];
+      tot[j] = t;
+      mysum += t;
+    }
+    uint32_t tsum;
+    uint32_t run = smx::block_excl_scan(mysum, ws, tsum);
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const int d = tid * DPT + j;
+      uint32_t t = run;
+#pragma unroll
+      for (int w = 0; w < DS_WARPS; ++w) {
+        const uint32_t c = wcnt[w * BINS + d];
+        wcnt[w * BINS + d] = (uint16_t)t;
+        t += c;
+      }
+      delta[d] = ioff[d] - run;
+      run += tot[j];
+    }
+    __syncthreads();  // 2: offsets ready; the offset row and the input buffer are free
+    const uint32_t nxt = ticket[slot ^ 1];
+    if (tid == 0 && nxt < n_tiles) {
+      smx::fence_proxy_async();
+      smx::mbar_expect_tx(&bar, BINS * 4 + (full_tile(nxt) ? DS_TILE * 8 : 0));
+      smx::bulk_g2s(ioff, off + (size_t)nxt * BINS, BINS * 4, &bar);
+    }
+#pragma unroll
+    for (int i = 0; i < DS_IPT; ++i) {
+      const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+      if (r != 0xffffu) {
+        const uint32_t d = (k[i] >> p.shift) & mask;
+        const uint32_t pos = mycnt[d] + r;
+        sval[pos] = v[i];
+        sdig[pos] = (uint16_t)d;
+      }
+    }
+    __syncthreads();  // 3: tile staged in digit order
+    for (uint32_t q = tid; q < tsum; q += DS_THREADS) p.vals_out[delta[sdig[q]] + q] = sval[q];
+    __syncthreads();  // 4: staging read: the input buffer may be refilled
+    if (tid == 0 && nxt < n_tiles && full_tile(nxt)) {
+      smx::fence_proxy_async();
+      smx::bulk_g2s(irec, p.recs_in + (uint64_t)nxt * DS_TILE, DS_TILE * 8, &bar);
+    }
+  }
+}
+
+template <int BITS>
+size_t downsweep_last_smem() {
+  return (size_t)DS_TILE * 8 + (size_t)2 * (1 << BITS) * 4 + (size_t)DS_WARPS * (1 << BITS) * 2;
+}
+
 template <int BITS>
 size_t downsweep_smem() {
   return (size_t)4 * DS_TILE * 4 + (size_t)3 * (1 << BITS) * 4 + (size_t)DS_WARPS * (1 << BITS) * 2;
@@ -458,11 +587,14 @@ int run_pass(const SortPass& p, uint32_t n_tiles, uint16_t* tcnt, uint32_t* off,
              uint32_t* tile_ctr, cudaStream_t st) {
   constexpr int BINS = 1 << BITS;
   const size_t smem = downsweep_smem<BITS>();
+  const size_t smem_last = downsweep_last_smem<BITS>();
   const size_t th_smem = (size_t)4 * (th_hist_warps(BITS) * BINS + CNT_BINS);
   static bool configured = false;
   if (!configured) {
     SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_last_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem_last));
     SMX_CUDA_CHECK(cudaFuncSetAttribute(tile_hist_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)th_smem));
     configured = true;
@@ -476,7 +608,13 @@ int run_pass(const SortPass& p, uint32_t n_tiles, uint16_t* tcnt, uint32_t* off,
   smx_count_launch(); chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, n_tiles, csum);
   smx_count_launch(); chunk_scan_kernel<BITS><<<1, 1024, 0, st>>>(csum, n_chunks);
   smx_count_launch(); tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, csum, n_tiles, off);
-  smx_count_launch(); downsweep_kernel<BITS><<<grid, DS_THREADS, smem, st>>>(p, off, n_tiles, tile_ctr);
+  static const bool last_ok = !getenv("SMX_SORT_LAST") || atoi(getenv("SMX_SORT_LAST")) != 0;  // A/B switch
+  if (p.last && p.recs_in && BITS >= 10 && last_ok) {
+    const uint32_t g2 = std::min<uint32_t>(n_tiles, 148u * ds_last_ctas_per_sm(BITS));
+    smx_count_launch(); downsweep_last_kernel<BITS><<<g2, DS_THREADS, smem_last, st>>>(p, off, n_tiles, tile_ctr);
+  } else {
+    smx_count_launch(); downsweep_kernel<BITS><<<grid, DS_THREADS, smem, st>>>(p, off, n_tiles, tile_ctr);
+  }
   SMX_LAUNCH_CHECK();
   return 0;
 }

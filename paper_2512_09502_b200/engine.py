@@ -30,6 +30,7 @@ import torch
 from . import _lib
 from .memory import RankMemory
 from ._lib import call, check
+from .exchange import fixed_allgather, fixed_p2p
 from .api import (POINT_TO_POINT, ConnSpec, ConsistencyError, DelayRangeError, LifParams,
                   ProtocolError, Raster, SimConfig, SynSpec, canonical_bytes, stream_key)
 
@@ -1972,38 +1973,27 @@ class Cluster:
         X = st.xplan
         if self.has_p2p:
             P = X["p2p"]
-            send, off = P["send"], 0
-            for d in range(self.n_ranks):
-                c = P["out_c"][d]
-                if not c:
-                    continue
-                send[off: off + 1].copy_(st.p2p_counts[d: d + 1])
-                cc = min(c, st.pk_cap)  # packets written never exceed the per-destination stride
-                send[off + 2: off + 2 + 2 * cc].copy_(st.p2p_packets[d * st.pk_cap * 2: d * st.pk_cap * 2 + 2 * cc])
-                X["over"].bitwise_or_((st.p2p_counts[d: d + 1] > c).to(torch.int32))
-                off += P["out_sz"][d]
+            for d, c in enumerate(P["out_c"]):
+                if c:
+                    X["over"].bitwise_or_((st.p2p_counts[d: d + 1] > c).to(torch.int32))
             X["sent"] += st.p2p_counts.sum()
-            dist.all_to_all_single(P["recv"][: sum(P["in_sz"])], send[: sum(P["out_sz"])], P["in_sz"], P["out_sz"])
-            off = 0
+            rv, offs = fixed_p2p(st.p2p_counts, st.p2p_packets, st.pk_cap, P["out_c"], P["in_c"], P["send"], P["recv"])
             for sr in range(self.n_ranks):
                 if not P["in_c"][sr]:
                     continue
                 rl = st.RL.get((POINT_TO_POINT, sr))
                 if rl is None:
                     raise ProtocolError(f"rank {me}: spikes from rank {sr} but no map for that pair")
-                rv = P["recv"]
+                off = offs[sr]
                 call("smx_unpack", _ptr(rv[off + 2:]), _ptr(rv[off:]), _ptr(rl[1]), rl[1].numel(),
                      _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
-                off += P["in_sz"][sr]
         for g, G in X["groups"].items():
             slot, cap, members = self.group_slots[g], G["cap"], G["members"]
-            send, recv = G["send"], G["recv"]
-            send[0:1].copy_(st.g_counts[slot: slot + 1])
-            cc = min(cap, st.pk_cap)
-            send[2: 2 + 2 * cc].copy_(st.g_packets[slot * st.pk_cap * 2: slot * st.pk_cap * 2 + 2 * cc])
             X["over"].bitwise_or_((st.g_counts[slot: slot + 1] > cap).to(torch.int32))
             X["sent"] += st.g_counts[slot]
-            dist.all_gather_into_tensor(recv, send, group=self._pg[g])
+            recv = fixed_allgather(st.g_counts[slot: slot + 1],
+                                   st.g_packets[slot * st.pk_cap * 2: (slot + 1) * st.pk_cap * 2], cap,
+                                   G["send"], G["recv"], self._pg[g])
             for i, sr in enumerate(members):
                 if sr == me:
                     continue

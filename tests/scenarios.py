@@ -273,6 +273,8 @@ SCENARIOS = {
     "no_multapse_p2p": lambda ns: no_multapse(ns, "p2p"),
     "no_multapse_coll": lambda ns: no_multapse(ns, "collective"),
     "poisson_high": poisson_high,
+    "balanced_8r_coll": lambda ns: balanced(ns, 8, "collective", 120, 16, 4, 9, sim=(0.0, 10.0)),
+    "balanced_8r_p2p": lambda ns: balanced(ns, 8, "p2p", 120, 16, 4, 9, sim=(0.0, 10.0)),
     "dist_random_p2p": lambda ns: dist_random(ns, "p2p"),
     "dist_random_coll": lambda ns: dist_random(ns, "collective"),
 }

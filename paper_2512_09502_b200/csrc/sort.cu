@@ -78,7 +78,7 @@ __host__ __device__ constexpr int th_hist_warps(int bits) {
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(US_THREADS) tile_hist_kernel(SortPass p, uint16_t* tcnt, uint32_t n_tiles,
+__global__ void __launch_bounds__(US_THREADS, 2) tile_hist_kernel(SortPass p, uint16_t* tcnt, uint32_t n_tiles,
                                                                uint32_t tiles_per_cta) {
   constexpr int BINS = 1 << BITS;
   constexpr int HW = th_hist_warps(BITS);
@@ -113,7 +113,43 @@ __global__ void __launch_bounds__(US_THREADS) tile_hist_kernel(SortPass p, uint1
     __syncwarp();
     const uint64_t a = (uint64_t)t * DS_TILE, b = min(p.n, a + DS_TILE);
     const uint32_t nq = (uint32_t)((b - a) / 4);
-    for (uint32_t i = lane; i < nq + 1; i += 32) {
+    auto add_key = [&](uint32_t k) {
+      if (p.first && p.lut && (k & SMX_TMP_KEY)) {
+        saw_tmp = true;
+        k = p.lut[k & ~SMX_TMP_KEY];
+      }
+      const uint32_t d = (k >> p.shift) & mask;
+      atomicAdd(&wh[d], 1u);
+      if (mode == 1) atomicAdd(&cnt[((k & lm) - lo_v) * BINS + d], 1u);
+      else if (mode == 2) count_key(p, k, 1u);
+    };
+    if (b - a == DS_TILE) {
+      // full tile: three 4-key groups per lane loaded before any is counted
+      constexpr int PER = DS_TILE / 4 / 32;  // 30 groups of four keys per lane
+      constexpr int G = 3;
+      static_assert(PER % G == 0, "group count");
+#pragma unroll 1
+      for (int g0 = 0; g0 < PER; g0 += G) {
+        uint32_t kk[G][4];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const uint32_t i = lane + (uint32_t)(g0 + u) * 32;
+          if (p.recs_in) {
+            const uint4* r4 = reinterpret_cast<const uint4*>(p.recs_in + a) + 2 * i;
+            const uint4 q0 = __ldcs(r4), q1 = __ldcs(r4 + 1);
+            kk[u][0] = q0.x; kk[u][1] = q0.z; kk[u][2] = q1.x; kk[u][3] = q1.z;
+          } else {
+            const uint4 q = __ldcs(reinterpret_cast<const uint4*>(p.keys_in + a) + i);
+            kk[u][0] = q.x; kk[u][1] = q.y; kk[u][2] = q.z; kk[u][3] = q.w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < G; ++u)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) add_key(kk[u][j]);
+      }
+    }
+    for (uint32_t i = lane; b - a != DS_TILE && i < nq + 1; i += 32) {
       uint32_t kk[4];
       int m = 4;
       if (i < nq) {
@@ -133,15 +169,7 @@ __global__ void __launch_bounds__(US_THREADS) tile_hist_kernel(SortPass p, uint1
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (j >= m) break;
-        uint32_t k = kk[j];
-        if (p.first && p.lut && (k & SMX_TMP_KEY)) {
-          saw_tmp = true;
-          k = p.lut[k & ~SMX_TMP_KEY];
-        }
-        const uint32_t d = (k >> p.shift) & mask;
-        atomicAdd(&wh[d], 1u);
-        if (mode == 1) atomicAdd(&cnt[((k & lm) - lo_v) * BINS + d], 1u);
-        else if (mode == 2) count_key(p, k, 1u);
+        add_key(kk[j]);
       }
     }
     __syncwarp();

@@ -117,7 +117,10 @@ struct DrawMark {
 };
 
 constexpr uint32_t DRAW_MARK_SMEM_WORDS = 12288;  // 48 KB
-constexpr int DRAW_BPT = 2;                       // Philox blocks per thread per iteration
+#ifndef SMX_DRAW_BPT
+#define SMX_DRAW_BPT 1  // measured: 1 block per lane 4.94 ms, 2: 5.23 ms, 4: 7.69 ms (C3 generation)
+#endif
+constexpr int DRAW_BPT = SMX_DRAW_BPT;  // Philox blocks per lane per iteration
 
 // MARK: 0 no marking, 1 bit from the sink's key, 2 bit from the value (via tab)
 template <int MARK>

@@ -59,7 +59,10 @@ __device__ __forceinline__ void warp_range(const DrawRange& r, uint64_t& lo, uin
   hi = lo + r.per_warp < end ? lo + r.per_warp : end;
 }
 
-static __global__ void __launch_bounds__(DRAW_THREADS) draw_count_kernel(DrawRange r, uint32_t* warp_counts) {
+#ifndef SMX_DRAW_COUNT_MB
+#define SMX_DRAW_COUNT_MB 3
+#endif
+static __global__ void __launch_bounds__(DRAW_THREADS, SMX_DRAW_COUNT_MB) draw_count_kernel(DrawRange r, uint32_t* warp_counts) {
   uint64_t lo, hi;
   warp_range(r, lo, hi);
   uint32_t cnt = 0;

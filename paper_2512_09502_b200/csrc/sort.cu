@@ -475,23 +475,32 @@ __global__ void __launch_bounds__(DS_THREADS, ds_ctas_per_sm(BITS)) downsweep_ke
   }
 }
 
-// Last pass of a multi-pass sort with wide digits (10-11 bits): (key, value)
-// records in, values out.  The staging reuses the TMA input buffer (values +
-// u16 digits) and the offset row is single-buffered, so the kernel needs
-// 30 + 4 + 4 + 16 KB of SMEM at 10 bits -- three CTAs per SM instead of two.
-// The next tile's records are fetched after the write phase (the other CTAs
-// of the SM cover the load); its offset row right after the scan.
-constexpr int ds_last_ctas_per_sm(int bits) { return bits <= 10 ? 3 : 2; }
+// Downsweep with the staging aliased onto the TMA input buffer and a
+// single-buffered offset row: 30 + 2*BINS*4 + 16*BINS bytes of SMEM (38 KB at
+// 8 bits, 48 KB at 10) instead of 60 + ..., so more CTAs per SM.  The next
+// tile's input is fetched after the write phase (the other CTAs of the SM
+// cover the load); its offset row right after the scan.
+//   LAST:  (key, value) records in, values out (staging: values + u16 digits)
+//   !LAST: SoA keys/values, index values or records in; records out
+//          (staging: keys + values)
+#ifndef SMX_DS_ALIAS_CTAS
+#define SMX_DS_ALIAS_CTAS 3
+#endif
+constexpr int ds_last_ctas_per_sm(int bits) { return bits <= 9 ? SMX_DS_ALIAS_CTAS : bits <= 10 ? 3 : 2; }
 
-template <int BITS>
+template <int BITS, bool LAST>
 __global__ void __launch_bounds__(DS_THREADS, ds_last_ctas_per_sm(BITS)) downsweep_last_kernel(
     SortPass p, const uint32_t* off, uint32_t n_tiles, uint32_t* tile_ctr) {
   constexpr int BINS = 1 << BITS;
   constexpr int DPT = BINS / DS_THREADS;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint2* irec = reinterpret_cast<uint2*>(smem);                           // [DS_TILE] TMA target
-  uint32_t* sval = reinterpret_cast<uint32_t*>(smem);                     // staging, aliases irec
-  uint16_t* sdig = reinterpret_cast<uint16_t*>(sval + DS_TILE);           // staging digits
+  uint2* irec = reinterpret_cast<uint2*>(smem);                           // [DS_TILE] TMA target (records)
+  uint32_t* ikey = reinterpret_cast<uint32_t*>(smem);                     // [DS_TILE] TMA target (SoA keys)
+  uint32_t* ival = ikey + DS_TILE;                                        // [DS_TILE] TMA target (SoA values)
+  uint32_t* sval = reinterpret_cast<uint32_t*>(smem);                     // LAST staging, aliases the input
+  uint16_t* sdig = reinterpret_cast<uint16_t*>(sval + DS_TILE);           // LAST staging digits
+  uint32_t* skey = ikey;                                                  // !LAST staging keys
+  uint32_t* svl2 = ival;                                                  // !LAST staging values
   uint32_t* ioff = reinterpret_cast<uint32_t*>(smem + (size_t)DS_TILE * 8);  // [BINS] TMA target
   uint32_t* delta = ioff + BINS;                                          // [BINS]
   uint16_t* wcnt = reinterpret_cast<uint16_t*>(delta + BINS);             // [DS_WARPS][BINS]
@@ -500,19 +509,31 @@ __global__ void __launch_bounds__(DS_THREADS, ds_last_ctas_per_sm(BITS)) downswe
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t mask = BINS - 1;
+  const bool soa_vals = !p.recs_in && p.vals_in;
+  const bool any_tmp = !LAST && p.first && p.lut && p.tmp_flag && *p.tmp_flag;
+  const uint32_t in_bytes = (p.recs_in || soa_vals) ? DS_TILE * 8 : DS_TILE * 4;
   if (tid == 0) {
     smx::mbar_init(&bar, 1);
     smx::fence_mbar_init();
   }
   __syncthreads();
   auto full_tile = [&](uint32_t t) { return (uint64_t)t * DS_TILE + DS_TILE <= p.n; };
+  auto load_input = [&](uint32_t t) {  // thread 0, after expect_tx
+    const uint64_t t0 = (uint64_t)t * DS_TILE;
+    if (p.recs_in) {
+      smx::bulk_g2s(irec, p.recs_in + t0, DS_TILE * 8, &bar);
+    } else {
+      smx::bulk_g2s(ikey, p.keys_in + t0, DS_TILE * 4, &bar);
+      if (soa_vals) smx::bulk_g2s(ival, p.vals_in + t0, DS_TILE * 4, &bar);
+    }
+  };
   if (tid == 0) {
     const uint32_t t = atomicAdd(tile_ctr, 1u);
     ticket[0] = t;
     if (t < n_tiles) {
-      smx::mbar_expect_tx(&bar, BINS * 4 + (full_tile(t) ? DS_TILE * 8 : 0));
+      smx::mbar_expect_tx(&bar, BINS * 4 + (full_tile(t) ? in_bytes : 0));
       smx::bulk_g2s(ioff, off + (size_t)t * BINS, BINS * 4, &bar);
-      if (full_tile(t)) smx::bulk_g2s(irec, p.recs_in + (uint64_t)t * DS_TILE, DS_TILE * 8, &bar);
+      if (full_tile(t)) load_input(t);
     }
   }
   __syncthreads();
@@ -529,11 +550,25 @@ __global__ void __launch_bounds__(DS_THREADS, ds_last_ctas_per_sm(BITS)) downswe
 #pragma unroll
     for (int i = 0; i < DS_IPT; ++i) {
       const uint32_t q = wofs + i * 32;
-      uint2 r;
-      if (full) r = irec[q];
-      else r = t0 + q < p.n ? p.recs_in[t0 + q] : make_uint2(0u, 0u);
-      k[i] = r.x;
-      v[i] = r.y;
+      const uint64_t idx = t0 + q;
+      if (p.recs_in) {
+        uint2 r;
+        if (full) r = irec[q];
+        else r = idx < p.n ? p.recs_in[idx] : make_uint2(0u, 0u);
+        k[i] = r.x;
+        v[i] = r.y;
+      } else if (full) {
+        k[i] = ikey[q];
+        v[i] = soa_vals ? ival[q] : (uint32_t)idx;
+      } else {
+        const bool ok = idx < p.n;
+        k[i] = ok ? p.keys_in[idx] : 0u;
+        v[i] = ok ? (soa_vals ? p.vals_in[idx] : (uint32_t)idx) : 0u;
+      }
+    }
+    if (any_tmp) {
+#pragma unroll
+      for (int i = 0; i < DS_IPT; ++i) k[i] = resolve(k[i], p.lut);
     }
     {
       uint32_t* w32 = reinterpret_cast<uint32_t*>(mycnt);
@@ -576,7 +611,7 @@ __global__ void __launch_bounds__(DS_THREADS, ds_last_ctas_per_sm(BITS)) downswe
     const uint32_t nxt = ticket[slot ^ 1];
     if (tid == 0 && nxt < n_tiles) {
       smx::fence_proxy_async();
-      smx::mbar_expect_tx(&bar, BINS * 4 + (full_tile(nxt) ? DS_TILE * 8 : 0));
+      smx::mbar_expect_tx(&bar, BINS * 4 + (full_tile(nxt) ? in_bytes : 0));
       smx::bulk_g2s(ioff, off + (size_t)nxt * BINS, BINS * 4, &bar);
     }
 #pragma unroll
@@ -585,16 +620,28 @@ __global__ void __launch_bounds__(DS_THREADS, ds_last_ctas_per_sm(BITS)) downswe
       if (r != 0xffffu) {
         const uint32_t d = (k[i] >> p.shift) & mask;
         const uint32_t pos = mycnt[d] + r;
-        sval[pos] = v[i];
-        sdig[pos] = (uint16_t)d;
+        if (LAST) {
+          sval[pos] = v[i];
+          sdig[pos] = (uint16_t)d;
+        } else {
+          skey[pos] = k[i];
+          svl2[pos] = v[i];
+        }
       }
     }
     __syncthreads();  // 3: tile staged in digit order
-    for (uint32_t q = tid; q < tsum; q += DS_THREADS) p.vals_out[delta[sdig[q]] + q] = sval[q];
+    if (LAST) {
+      for (uint32_t q = tid; q < tsum; q += DS_THREADS) p.vals_out[delta[sdig[q]] + q] = sval[q];
+    } else {
+      for (uint32_t q = tid; q < tsum; q += DS_THREADS) {
+        const uint32_t kk = skey[q];
+        p.recs_out[delta[(kk >> p.shift) & mask] + q] = make_uint2(kk, svl2[q]);
+      }
+    }
     __syncthreads();  // 4: staging read: the input buffer may be refilled
     if (tid == 0 && nxt < n_tiles && full_tile(nxt)) {
       smx::fence_proxy_async();
-      smx::bulk_g2s(irec, p.recs_in + (uint64_t)nxt * DS_TILE, DS_TILE * 8, &bar);
+      load_input(nxt);
     }
   }
 }
@@ -621,8 +668,10 @@ int run_pass(const SortPass& p, uint32_t n_tiles, uint16_t* tcnt, uint32_t* off,
   if (!configured) {
     SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-    SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_last_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem_last));
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_last_kernel<BITS, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_last));
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_last_kernel<BITS, false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_last));
     SMX_CUDA_CHECK(cudaFuncSetAttribute(tile_hist_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)th_smem));
     configured = true;
@@ -636,10 +685,18 @@ int run_pass(const SortPass& p, uint32_t n_tiles, uint16_t* tcnt, uint32_t* off,
   smx_count_launch(); chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, n_tiles, csum);
   smx_count_launch(); chunk_scan_kernel<BITS><<<1, 1024, 0, st>>>(csum, n_chunks);
   smx_count_launch(); tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(tcnt, csum, n_tiles, off);
-  static const bool last_ok = !getenv("SMX_SORT_LAST") || atoi(getenv("SMX_SORT_LAST")) != 0;  // A/B switch
-  if (p.last && p.recs_in && BITS >= 10 && last_ok) {
-    const uint32_t g2 = std::min<uint32_t>(n_tiles, 148u * ds_last_ctas_per_sm(BITS));
-    smx_count_launch(); downsweep_last_kernel<BITS><<<g2, DS_THREADS, smem_last, st>>>(p, off, n_tiles, tile_ctr);
+  // A/B switches: SMX_SORT_LAST=0 disables the aliased last pass; SMX_SORT_ALIAS=<min bits> uses the
+  // aliased kernel for last passes from that width and SMX_SORT_ALIAS_MID=<min bits> for record-out passes.
+  static const bool last_ok = !getenv("SMX_SORT_LAST") || atoi(getenv("SMX_SORT_LAST")) != 0;
+  static const int alias_last = getenv("SMX_SORT_ALIAS") ? atoi(getenv("SMX_SORT_ALIAS")) : 10;
+  static const int alias_mid = getenv("SMX_SORT_ALIAS_MID") ? atoi(getenv("SMX_SORT_ALIAS_MID")) : 99;
+  const uint32_t g2 = std::min<uint32_t>(n_tiles, 148u * ds_last_ctas_per_sm(BITS));
+  if (p.last && p.recs_in && BITS >= alias_last && last_ok) {
+    smx_count_launch();
+    downsweep_last_kernel<BITS, true><<<g2, DS_THREADS, smem_last, st>>>(p, off, n_tiles, tile_ctr);
+  } else if (!p.last && BITS >= alias_mid) {
+    smx_count_launch();
+    downsweep_last_kernel<BITS, false><<<g2, DS_THREADS, smem_last, st>>>(p, off, n_tiles, tile_ctr);
   } else {
     smx_count_launch(); downsweep_kernel<BITS><<<grid, DS_THREADS, smem, st>>>(p, off, n_tiles, tile_ctr);
   }

@@ -30,7 +30,7 @@ for _ in range(2):
     c = build()
     del c
 dist.barrier()
-with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], with_stack=False) as prof:
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA], with_stack=bool(os.environ.get("STACK"))) as prof:
     c = build()
 dist.barrier()
 if rank == 0:
@@ -51,4 +51,9 @@ if rank == 0:
     for g, at, n in sorted(gaps, reverse=True)[:25]:
         ops = [e["name"] for e in cpu if e["ts"] <= at + g / 2 <= e["ts"] + e["dur"]]
         print(f"  gap {1e-3 * g:6.3f} ms at {1e-3 * (at - t0):7.2f} ms before {n[:40]:40s} cpu: {ops[-3:]}")
+    if os.environ.get("STACK"):  # host functions (>= 30 us) before the first generation launch
+        first = min((a for a, b, n in gpu if "draw_count" in n), default=t1)
+        for e in sorted(cpu, key=lambda e: e["ts"]):
+            if e["ts"] < first and e["dur"] >= 30 and e.get("cat") == "python_function":
+                print(f"  host {1e-3 * (e['ts'] - t0):7.2f} +{1e-3 * e['dur']:6.3f} ms  {e['name'][:90]}")
 dist.destroy_process_group()

@@ -912,7 +912,7 @@ class Cluster:
         if group != POINT_TO_POINT and members is None:
             raise ValueError(f"group {group} is not declared")
         tgt_bits: dict[int, torch.Tensor] = {}   # per target rank: used-value bitmap (when computed)
-        pending = []                             # source-side replays awaiting their batched check
+        work = []
         for tr, tg in target_pops:
             tr = int(tr)
             tg = np.asarray(tg, dtype=np.int64)
@@ -926,34 +926,54 @@ class Cluster:
             n = k_in * len(tg)
             need_bits = self.is_local(tr) or any(
                 self.is_local(r) for r in (members or ranks_sorted))
-            if not need_bits or n == 0:
-                continue
+            if need_bits and n:
+                work.append((tr, tg, key, n))
+        # 1. source-side replays of the remote targets, launched before the local
+        #    draws; their completion checks and presence flags come back in one
+        #    asynchronous read, so the host does not wait for the local draw
+        remote = []                               # (target rank, replay state or None, bitmap)
+        for tr, tg, key, n in work:
             if self.is_local(tr):
-                st = self.ranks[tr]
-                if tg.min() < 0 or tg.max() >= self.n_nodes[tr]:
-                    raise ValueError("target index outside the rank's node range")
-                vb, present = self._dist_target(st, key, tr, tg, k_in, total, all_rank, all_node, vbase,
-                                                seg_words, total_words, syn, port, group, ranks_sorted)
-            elif self._dist_multi:  # source-side replay, checked in one batch below
-                dev = next(iter(self.ranks.values())).device
-                pending.append((tr, self._replay_start(dev, key, tr, total, all_rank, all_node, vbase,
-                                                       total_words, n)))
                 continue
+            dev = next(iter(self.ranks.values())).device
+            if self._dist_multi:
+                R = self._replay_start(dev, key, tr, total, all_rank, all_node, vbase, total_words, n)
+                remote.append((tr, R, R["vbits"]))
             else:
-                dev = next(iter(self.ranks.values())).device
-                vb = self._dist_replay(dev, key, tr, total, all_rank, all_node, vbase, total_words, n)
-                present = None
-            tgt_bits[tr] = (vb, present)
-        for (tr, _), vb in zip(pending, self._replay_finish([R for _, R in pending])):
-            tgt_bits[tr] = (vb, None)
-        # presence of every source rank in the replayed targets' draws: one sync
-        todo = [tr for tr, (vb, pr) in tgt_bits.items() if pr is None]
-        if todo:
-            flags = torch.stack([torch.stack([tgt_bits[tr][0][w0: w0 + nw].ne(0).any()
-                                              for w0, nw in (seg_words[r] for r in ranks_sorted)])
-                                 for tr in todo]).cpu().numpy()
-            for tr, f in zip(todo, flags):
-                tgt_bits[tr] = (tgt_bits[tr][0], [r for r, a in zip(ranks_sorted, f) if a])
+                remote.append((tr, None, self._dist_replay(dev, key, tr, total, all_rank, all_node, vbase,
+                                                           total_words, n)))
+        chk_host, chk_ev = None, None
+        if remote:
+            big = torch.full((1,), 1 << 62, dtype=torch.int64, device=remote[0][2].device)
+            rows = []
+            for tr, R, vb in remote:
+                ex = R["excl"][-1:] if R is not None and R["first"] < R["n"] else big
+                fl = torch.stack([vb[w0: w0 + nw].ne(0).any() for w0, nw in (seg_words[r] for r in ranks_sorted)])
+                rows.append(torch.cat([ex, fl.to(torch.int64)]))
+            chk = torch.stack(rows)
+            chk_host = torch.empty(chk.shape, dtype=torch.int64, pin_memory=True)
+            chk_host.copy_(chk, non_blocking=True)
+            chk_ev = torch.cuda.Event()
+            chk_ev.record()
+        # 2. the local targets: replay, images, draw
+        for tr, tg, key, n in work:
+            if not self.is_local(tr):
+                continue
+            st = self.ranks[tr]
+            if tg.min() < 0 or tg.max() >= self.n_nodes[tr]:
+                raise ValueError("target index outside the rank's node range")
+            tgt_bits[tr] = self._dist_target(st, key, tr, tg, k_in, total, all_rank, all_node, vbase,
+                                             seg_words, total_words, syn, port, group, ranks_sorted)
+        # 3. remote bitmaps and their source ranks (the rare incomplete first
+        #    piece continues synchronously)
+        if remote:
+            chk_ev.synchronize()
+            got = chk_host.numpy()
+            for (tr, R, vb), row in zip(remote, got):
+                if R is not None and int(row[0]) < R["n_distinct"]:
+                    vb = self._replay_finish([R])[0]
+                    row = [0] + [int(vb[w0: w0 + nw].ne(0).any()) for w0, nw in (seg_words[r] for r in ranks_sorted)]
+                tgt_bits[tr] = (vb, [r for r, a in zip(ranks_sorted, row[1:]) if a])
         # counters, in the reference's (target, source-rank) call order
         ros_segs: dict = {}
         for tr, tg in target_pops:

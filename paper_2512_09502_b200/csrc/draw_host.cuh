@@ -25,6 +25,23 @@ int launch_write(int G, size_t smem, cudaStream_t st, const DrawRange& r, const 
   return 0;
 }
 
+template <class Sink, int MARK>
+int launch_op(int G, size_t smem, cudaStream_t st, const DrawRange& r, uint32_t tile, uint32_t n_tiles,
+              uint64_t* desc, uint32_t* ticket, uint64_t* total_d, uint64_t n_out, const Sink& sink, uint64_t* cur_d,
+              const DrawMark& mk) {
+  static size_t configured = 0;
+  smem += (size_t)DRAW_WARPS * tile * 4;
+  if (smem > 48 * 1024 && smem > configured) {
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(draw_onepass_kernel<Sink, MARK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    configured = smem;
+  }
+  smx_count_launch();
+  draw_onepass_kernel<Sink, MARK><<<G, DRAW_THREADS, smem, st>>>(r, tile, n_tiles, desc, ticket, total_d, n_out,
+                                                                  sink, cur_d, mk);
+  return 0;
+}
+
 // Sinks that may mark used values say so with `static constexpr bool kMark`.
 template <class Sink, class = void>
 struct sink_marks { static constexpr bool value = false; };
@@ -42,6 +59,20 @@ int launch_draw_write(int mode, int G, size_t smem, cudaStream_t st, const DrawR
     return -1;
   }
   return launch_write<Sink, 0>(G, smem, st, r, offs, n_out, sink, cur_d, mk);
+}
+
+template <class Sink>
+int launch_onepass(int mode, int G, size_t smem, cudaStream_t st, const DrawRange& r, uint32_t tile, uint32_t n_tiles,
+                   uint64_t* desc, uint32_t* ticket, uint64_t* total_d, uint64_t n_out, const Sink& sink,
+                   uint64_t* cur_d, const DrawMark& mk) {
+  if constexpr (sink_marks<Sink>::value) {
+    if (mode == 1) return launch_op<Sink, 1>(G, smem, st, r, tile, n_tiles, desc, ticket, total_d, n_out, sink, cur_d, mk);
+    if (mode == 2) return launch_op<Sink, 2>(G, smem, st, r, tile, n_tiles, desc, ticket, total_d, n_out, sink, cur_d, mk);
+  } else if (mode != 0) {
+    smx_set_error("run_draw: this sink does not mark used values");
+    return -1;
+  }
+  return launch_op<Sink, 0>(G, smem, st, r, tile, n_tiles, desc, ticket, total_d, n_out, sink, cur_d, mk);
 }
 
 // numpy integers(lo, lo+ex, size=n) on stream `key` from u32 cursor u0.
@@ -77,6 +108,63 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
   uint64_t* offs = nullptr;
   uint64_t* cur_d = nullptr;
   int rc = 0;
+  static const bool onepass = [] {
+    const char* e = getenv("SMX_DRAW_ONEPASS");
+    return !(e && e[0] == '0');
+  }();
+  if (onepass) {
+    mk.in_smem = mk.bits && mk.nwords <= DRAW_MARK_SMEM_WORDS;
+    const size_t smem = mk.in_smem ? mk.nwords * 4 : 0;
+    const int mode = mk.bits ? (mk.from_key ? 1 : 2) : 0;
+    static const uint32_t tile = [] {  // tuning aid: SMX_DRAW_TILE_RT overrides the tile size
+      const char* e = getenv("SMX_DRAW_TILE_RT");
+      const long v = e ? atol(e) : 0;
+      return v >= 256 && v % 256 == 0 && v <= 4096 ? (uint32_t)v : (uint32_t)OP_TILE;
+    }();
+    for (int attempt = 0; attempt < 8; ++attempt) {
+      const uint64_t n_tiles = (n_raw + tile - 1) / tile;
+      if (n_tiles >= 0xffffffffull) {
+        smx_set_error("run_draw: %llu raw positions exceed the tile ticket range", (unsigned long long)n_raw);
+        return -1;
+      }
+      r.n_raw = n_raw;
+      r.per_warp = 0;
+      const int G = (int)std::max<uint64_t>(1, std::min<uint64_t>((n_tiles + DRAW_WARPS - 1) / DRAW_WARPS,
+                                                                   148 * SMX_DRAW_MIN_BLOCKS));
+      // [desc n_tiles][ticket][total][cursor]
+      uint64_t* ws = nullptr;
+      SMX_CUDA_CHECK(cudaMallocAsync((void**)&ws, sizeof(uint64_t) * (n_tiles + 3), st));
+      SMX_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint64_t) * (n_tiles + 2), st));
+      uint32_t* ticket = reinterpret_cast<uint32_t*>(ws + n_tiles);
+      uint64_t* total_d = ws + n_tiles + 1;
+      uint64_t* cur_p = async ? nullptr : ws + n_tiles + 2;
+      if (int rc2 = launch_onepass(mode, G, smem, st, r, tile, (uint32_t)n_tiles, ws, ticket, total_d, n_out, sink, cur_p, mk))
+        return rc2;
+      SMX_LAUNCH_CHECK();
+      if (async) {
+        int* err = smx_device_error_word();
+        if (!err) {
+          smx_set_error("run_draw: no device error word");
+          return -3;
+        }
+        smx_count_launch(); draw_window_check_kernel<<<1, 1, 0, st>>>(total_d, n_out, err);
+        cudaFreeAsync(ws, st);
+        return 0;
+      }
+      uint64_t tc[2] = {0, 0};
+      SMX_CUDA_CHECK(cudaMemcpyAsync(tc, total_d, sizeof(tc), cudaMemcpyDeviceToHost, st));
+      SMX_CUDA_CHECK(cudaStreamSynchronize(st));
+      cudaFreeAsync(ws, st);
+      if (timing) fprintf(stderr, "run_draw onepass n=%llu G=%d: %.0f us\n", (unsigned long long)n_out, G, now_us() - t_start);
+      if (tc[0] >= n_out) {
+        res->cursor = tc[1];
+        return 0;
+      }
+      n_raw = n_raw + n_raw / 2 + 1024;
+    }
+    smx_set_error("run_draw: could not cover %llu accepted draws", (unsigned long long)n_out);
+    return -3;
+  }
   for (int attempt = 0; attempt < 8; ++attempt) {
     int G = (int)std::min<uint64_t>((n_raw + 16383) / 16384, 148 * 8);
     if (G < 1) G = 1;

@@ -55,11 +55,11 @@ def parse():
 
 def traffic_per_synapse():
     """DRAM bytes (read + write) per synapse of the generation + sort kernels,
-    from the committed ncu capture of one C3 construction (profiles/r1e)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1e", "traffic.json")
+    from the committed ncu capture of one C3 construction (profiles/r1f)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1f", "traffic.json")
     try:
         with open(path) as f:
-            return float(json.load(f)["bytes_per_synapse"]), "profiles/r1e/traffic.json"
+            return float(json.load(f)["bytes_per_synapse"]), "profiles/r1f/traffic.json"
     except (OSError, KeyError, ValueError):
         return None, None
 

@@ -4,7 +4,9 @@
 // is accepted by the same predicate, so the n-th accepted raw u32 is the
 // n-th output value; verified against numpy in tests/test_oracle_rng.py).
 //
-// Two launches per draw call:
+// Default: one launch per draw call (draw_onepass_kernel, below): ticketed
+// tiles, each drawn once, output bases by a decoupled look-back.
+// A/B path (SMX_DRAW_ONEPASS=0), two launches per draw call:
 //   count:  warp w counts accepts over its contiguous raw range (compute only)
 //   write:  warp w regenerates its range, ranks accepts with a warp scan,
 //           stages them in its own SMEM slice and hands (output index, value)

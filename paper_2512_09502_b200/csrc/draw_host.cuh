@@ -98,6 +98,10 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
   r.lm.threshold = ex == (1ULL << 32) ? 0u : (uint32_t)(((1ULL << 32) - ex) % ex);
   const double prej = (double)r.lm.threshold / 4294967296.0;
   uint64_t n_raw = n_out + (uint64_t)std::ceil(n_out * prej * 1.25 + 12.0 * std::sqrt(n_out * prej + 1.0) + 64.0);
+  // test aid: start synchronous calls from a window of exactly n_out raw
+  // positions, so any rejection exercises the widen-and-retry path
+  static const bool short_window = getenv("SMX_DRAW_SHORT_WINDOW") != nullptr;
+  if (short_window && res) n_raw = n_out;
   static const bool timing = getenv("SMX_DRAW_TIMING") != nullptr;  // tuning aid
   auto now_us = [] {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();

@@ -97,3 +97,43 @@ def test_poisson_vs_oracle_large(lam, n, batches):
     for _ in range(batches):
         assert np.array_equal(ps.draw(n).cpu().numpy().astype(np.int64), o.poisson(lam, size=n))
     assert ps.word_cursor == o.words_used
+
+
+_VARIANT_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle.rng import OracleStream
+from paper_2512_09502_b200 import device_rng as dr
+from paper_2512_09502_b200.api import stream_key
+for lo, hi, n in [(0, 8000, 1_000_000), (7, 3_000_000_007, 200_000), (0, 2, 100_001), (0, 100_000, 2047),
+                  (0, 100_000, 2048), (0, 100_000, 2049), (0, 2**32, 5000), (5, 9, 1)]:
+    for u0 in (0, 3, 4093):
+        k = stream_key(7, ("variant", lo, n, u0))
+        o = OracleStream(0, key=k)
+        if u0:
+            o.integers(0, 2**32, size=u0)  # consume u0 raw u32 draws (a full-range draw never rejects)
+        a = o.integers(lo, hi, size=n)
+        b = o.integers(lo, hi, size=3)
+        v, cur = dr.integers(k, u0, lo, hi, n)
+        assert np.array_equal(v.cpu().numpy(), a), (lo, hi, n, u0)
+        v2, _ = dr.integers(k, cur, lo, hi, 3)
+        assert np.array_equal(v2.cpu().numpy(), b), (lo, hi, n, u0, "cursor")
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"SMX_DRAW_TILE_RT": "256"}, {"SMX_DRAW_TILE_RT": "4096"},
+                                 {"SMX_DRAW_SHORT_WINDOW": "1"}, {"SMX_DRAW_ONEPASS": "0"},
+                                 {"SMX_DRAW_ONEPASS": "0", "SMX_DRAW_SHORT_WINDOW": "1"}])
+def test_integers_draw_variants(env):
+    """The one-pass draw at extreme tile sizes (deep look-back chains with 256),
+    the widen-and-retry path (a window of exactly n raw positions), and the
+    two-pass A/B path, all against the oracle stream incl. the cursor.  The
+    switches are read once per process, hence a subprocess per variant."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env={**os.environ, **env},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

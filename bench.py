@@ -10,9 +10,10 @@ source, first-index, image maps, rosters, routes).  Per GPU: 1e5 neurons
 Collective spike exchange (group 0 over all ranks) when N > 1.
 
 Launch: python bench.py [--gpus N --steps K --warmup W]  (N > 1 under
-torchrun, one rank per GPU, NCCL).  --impl reference times the CPU oracle
-port (the reference's algorithm restated in numpy + the numpy-exact RNG in
-C, oracle/) on a bounded sample on rank 0.
+torchrun, one rank per GPU, NCCL).  --impl reference times the unmodified
+reference package (baseline/_ref: Python + its Cython kernels; the CPU
+oracle port of oracle/ when it is not installed) on a bounded sample on
+rank 0.
 """
 from __future__ import annotations
 
@@ -49,7 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: --neurons is the whole network, split over the GPUs")
-    ap.add_argument("--cpu-sample-neurons", type=int, default=10_000)
+    ap.add_argument("--cpu-sample-neurons", type=int, default=5_000)
+    ap.add_argument("--cpu-sample-k-scale", type=float, default=0.1)
     return ap.parse_args()
 
 
@@ -125,59 +127,145 @@ def dist_info():
     return world, rank, local
 
 
+def host_info() -> dict:
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def reference_package():
+    """The unmodified reference (spikemesh, Python + its Cython kernels)
+    installed under baseline/_ref; None when it is not there."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(path) and path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import spikemesh
+        import spikemesh.models  # noqa: F401
+        from spikemesh import kernels
+        return spikemesh, kernels.backend_name() if hasattr(kernels, "backend_name") else kernels.BACKEND_NAME
+    except ImportError:
+        return None, None
+
+
+def cpu_sample(args):
+    """The CPU reference arm's workload: the same network scaled down (the
+    reference's 40 B records cannot hold C3's 1.125e9 synapses in host RAM)."""
+    n = args.cpu_sample_neurons
+    k_e = max(1, int(round(args.k_exc * args.cpu_sample_k_scale)))
+    k_i = max(1, int(round(args.k_inh * args.cpu_sample_k_scale)))
+    return n, k_e, k_i
+
+
+def cpu_construct(args):
+    """One construction of the sampled network on the host: the unmodified
+    reference when installed (kind "reference"), else the oracle port."""
+    sm, backend = reference_package()
+    n, k_e, k_i = cpu_sample(args)
+    if sm is not None:
+        c = sm.Cluster(sm.SimConfig(n_ranks=1, seed=args.seed))
+        sm.models.build_balanced_network(c, sm.models.BalancedParams(neurons_per_rank=n, k_exc=k_e, k_inh=k_i))
+        c.prepare()
+        return c, "reference", f"unmodified reference spikemesh 0.1.0 ({backend} kernels, baseline/_ref)"
+    from oracle.spikemesh_oracle import OracleCluster
+    from paper_2512_09502_b200 import api, models
+    c = OracleCluster(api.SimConfig(n_ranks=1, seed=args.seed))
+    models.build_balanced_network(c, models.BalancedParams(neurons_per_rank=n, k_exc=k_e, k_inh=k_i))
+    c.prepare()
+    return c, "port", "oracle port (reference not installed)"
+
+
 def run_reference(args):
-    """CPU oracle port on the box's host cores, bounded sample, rank 0 only."""
+    """The reference's CPU implementation on the box's host cores, bounded
+    sample, rank 0 only (other ranks exit without work)."""
     world, rank, _ = dist_info()
     if rank != 0:
         return
-    from oracle.spikemesh_oracle import OracleCluster
-    from paper_2512_09502_b200 import api, models
-    n = args.cpu_sample_neurons
-    scale = n / args.neurons
-    k_e, k_i = max(1, int(round(args.k_exc * scale))), max(1, int(round(args.k_inh * scale)))
-    sample = (f"oracle port, 1 rank, {n} neurons, K={k_e}+{k_i} ({n * (k_e + k_i):.3g} synapses) "
-              f"per step; same structure as the GPU workload scaled by {scale:g}")
+    n, k_e, k_i = cpu_sample(args)
     times = []
+    kind = what = None
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        c = OracleCluster(api.SimConfig(n_ranks=1, seed=args.seed))
-        models.build_balanced_network(c, models.BalancedParams(neurons_per_rank=n, k_exc=k_e, k_inh=k_i))
-        c.prepare()
+        c, kind, what = cpu_construct(args)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
         del c
+        gc.collect()
     syn = n * (k_e + k_i)
     value = syn / float(np.mean(times))
+    sample = (f"{what}: 1 rank, {n} neurons, K={k_e}+{k_i} ({syn:.3g} synapses) per step; the GPU workload's "
+              f"structure scaled down (neurons x{n / args.neurons:g}, K x{args.cpu_sample_k_scale:g}); "
+              f"single-threaded (1 core used)")
     line = {
         "impl": "reference", "metric": "construction_synapses_per_s", "value": value, "unit": "synapses/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
         "config": {"workload": "hpc_benchmark_C3_sampled", "neurons_per_rank": n, "k_in": k_e + k_i},
-        "cpu_baseline": {"value": value, "unit": "synapses/s", "cores": 1, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "synapses/s", "cores": 1, "kind": kind, "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "synapses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline(args):
-    """Oracle port timed on the host for the headline line (rank 0, N=1)."""
-    from oracle.spikemesh_oracle import OracleCluster
-    from paper_2512_09502_b200 import api, models
-    n = args.cpu_sample_neurons
-    scale = n / args.neurons
-    k_e, k_i = max(1, int(round(args.k_exc * scale))), max(1, int(round(args.k_inh * scale)))
+    """The reference timed on the host for the headline line (rank 0, N=1):
+    one construction, then a recorded propagation window (RTF, rate)."""
+    n, k_e, k_i = cpu_sample(args)
     t0 = time.perf_counter()
-    c = OracleCluster(api.SimConfig(n_ranks=1, seed=args.seed))
-    models.build_balanced_network(c, models.BalancedParams(neurons_per_rank=n, k_exc=k_e, k_inh=k_i))
-    c.prepare()
+    c, kind, what = cpu_construct(args)
     dt = time.perf_counter() - t0
-    rep = c.simulate(0.0, 5.0, record=False)
+    rep = c.simulate(20.0, 50.0, record=True)
+    rtf = rep.rtf if hasattr(rep, "rtf") else rep["rtf"]
+    n_ev = rep.n_spike_events if hasattr(rep, "n_spike_events") else int(c.raster().shape[0])
     syn = n * (k_e + k_i)
-    return {"value": syn / dt, "unit": "synapses/s", "cores": 1, "kind": "port",
-            "sample": f"oracle port: 1 rank, {n} neurons, K={k_e}+{k_i} ({syn:.3g} synapses) construction "
-                      f"{dt:.2f} s; propagation RTF {rep['rtf']:.2f} over 5 ms",
-            "rtf": rep["rtf"]}
+    return {"value": syn / dt, "unit": "synapses/s", "cores": 1, "kind": kind,
+            "sample": f"{what}: 1 rank, {n} neurons, K={k_e}+{k_i} ({syn:.3g} synapses) construction "
+                      f"{dt:.2f} s; propagation RTF {rtf:.2f} over 50 ms after 20 ms warmup",
+            "rtf": rtf, "rate_hz": n_ev / (n * 0.05), "host": host_info()}
+
+
+def propagation_stats(c, rep, rep2, args, world, n_rank, syn_per_rank, max_over_ranks):
+    """Event counts and the per-step roofline of propagation (SURVEY §8d:
+    B_step = 40 N + 20 E bytes; N neurons, E synaptic events per step).
+    rep: unrecorded run (RTF); rep2: recorded window of the same length."""
+    import torch
+    peak, _ = peaks()
+    steps = c.cfg.steps_for(args.model_ms)
+    (rank, st), = [(r, st) for r, st in c.ranks.items()][:1]
+    ev = c.rank_events(rank)
+    nodes = c._gid_to_node(st, ev[:, 1]) if len(ev) else np.empty(0, np.int64)
+    fi = st.first_index.cpu().numpy()
+    local_events = int((fi[nodes + 1] - fi[nodes]).sum()) if len(nodes) else 0
+    spikes = int(max_over_ranks(float(len(ev))) if world == 1 else 0)
+    if world > 1:
+        t = torch.tensor([float(len(ev)), float(local_events)], dtype=torch.float64, device=st.device)
+        torch.distributed.all_reduce(t)
+        spikes = int(t[0].item())
+    rate = spikes / (world * n_rank * args.model_ms * 1e-3)
+    if world == 1:
+        e_step = local_events / steps
+        how = "exact: sum of the spiking sources' row lengths"
+    else:  # every source has the same expected out-degree over all ranks
+        e_step = spikes * (syn_per_rank / n_rank) / steps / world
+        how = "per GPU, spikes x mean out-degree (K N / N_src)"
+    step_s = rep.rtf * c.cfg.resolution_ms * 1e-3
+    b_step = 40.0 * n_rank + 20.0 * e_step
+    achieved = b_step / step_s / 1e9 if step_s > 0 else 0.0
+    return {"spikes": spikes, "model_ms": args.model_ms, "steps": steps, "rate_hz": rate,
+            "events_per_step": e_step, "events_how": how, "rtf_recording": max_over_ranks(rep2.rtf),
+            "step_us": step_s * 1e6,
+            "roofline_prop": {"bound": "hbm", "bytes_per_step": b_step, "achieved": achieved, "peak": peak,
+                              "unit": "GB/s", "frac": achieved / peak,
+                              "formula": "(40 N + 20 E) / step time (SURVEY 8d)"}}
 
 
 def run_ours(args):
@@ -247,9 +335,12 @@ def run_ours(args):
             sort_ms.append(c.kernel_ms("sort"))
             launches.append(_lib.lib().smx_launch_count() - L0)
             h2d.append(engine.H2D_BYTES[0] - H0)
-        # propagation on the last network
+        # propagation on the last network: the RTF without recording, then a
+        # recorded window of the same length for spikes / events / rate
         rep = c.simulate(args.prop_warmup_ms, args.model_ms, record=False)
+        rep2 = c.simulate(0.0, args.model_ms, record=True)
     rtf = max_over_ranks(rep.rtf)
+    prop = propagation_stats(c, rep, rep2, args, world, n_rank, syn_per_rank, max_over_ranks)
     clocks = clk.summary()
     ms = float(np.mean(step_ms))
     total_syn = world * syn_per_rank
@@ -271,7 +362,8 @@ def run_ours(args):
                    "synapses_per_gpu": syn_per_rank, "comm": cfg.comm_mode, "parallelism": f"ranks{world}",
                    "l2": "inputs larger than L2 (tables 4.5 GB per GPU)", "seed": args.seed},
         "construction_wall_s": float(np.mean(wall_s)),
-        "rtf": rtf, "rtf_model_ms": args.model_ms, "n_spikes_model": None,
+        "rtf": rtf, "rtf_model_ms": args.model_ms, "n_spikes_model": prop["spikes"],
+        "propagation": prop,
         "gpu_launches": int(np.mean(launches)),
         "e2e": {"value": e2e, "unit": "synapses/s", "h2d_bytes_per_step": int(np.mean(h2d)),
                 "d2h_bytes_per_step": 8},

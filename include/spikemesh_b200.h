@@ -181,9 +181,12 @@ int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uint32_t* row2
                int64_t* now_dev, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap,
                const int* record_dev, int64_t* rec, uint64_t* n_rec, uint64_t rec_cap, uint32_t* spike_count,
                int* overflow, const void* p2p_host, const void* grp_host, void* stream);
-/* deliver_point_packets / deliver_gather_packets (sm/engine.py:146-190) */
-int smx_unpack(const uint32_t* packets, const uint32_t* count, const int64_t* table, uint64_t table_len,
-               uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err, void* stream);
+/* deliver_point_packets / deliver_gather_packets (sm/engine.py:146-190).
+ * *count (written by the sender) is clamped to max_count, the block's
+ * capacity; a larger count sets *err = 5. */
+int smx_unpack(const uint32_t* packets, const uint32_t* count, uint32_t max_count, const int64_t* table,
+               uint64_t table_len, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap,
+               int* err, void* stream);
 /* kernels.deliver_spikes (kernels/_speedups.pyx:38-54) over a device list of
  * (source node, emission step); packed (cls_*) or wide (wide_w/wide_meta). */
 int smx_deliver(const uint32_t* src_nodes, const uint32_t* src_steps, const uint32_t* n_src, uint32_t* wprefix,

@@ -72,7 +72,7 @@ SIGNATURES = {
     "smx_ref_deliver_spikes": (I32, [P, P, U64, P, P, P, P, P, P, I64, I64, I64, P]),
     "smx_block": (I32, [P, P, P, P, P, P, P, P, U32, P, I32, I32, P, I32, I32, P, I32, P, I32, P, P, P, P, P, P,
                          P, U32, P, U32, P, P, U64, P, P, P, P, P, P, P, P, P, P]),
-    "smx_unpack": (I32, [P, P, P, U64, P, P, P, U32, P, P]),
+    "smx_unpack": (I32, [P, P, U32, P, U64, P, P, P, U32, P, P]),
     "smx_deliver": (I32, [P, P, P, P, P, P, P, P, P, P, P, P, P, U32, I32, I32, I32, P]),
 }
 

@@ -105,6 +105,10 @@ static __global__ void cta_offsets_kernel(const uint32_t* counts, int n, uint64_
 // v[u] (bit u of ok set; ALL: every bit set)
 // for output indices j0 + u*stride and reports the record keys it wrote;
 // `void operator()(uint64_t j, uint32_t value)` consumes one item.
+// Sinks must be idempotent: when a synchronous call's raw window turns out
+// too short, run_draw widens it and launches again, so the same (j, value)
+// can be handed over more than once (every sink here stores positionally or
+// ORs marks; an accumulating sink would double-count).
 // Optional used-value marking fused into the write pass: bit
 // (tab ? tab[value] : value) of `bits` is set for every emitted draw; with
 // from_key the bit comes from the sink's key instead: temporary keys mark

@@ -208,10 +208,16 @@ __global__ void __launch_bounds__(1024) spikes_kernel(const __grid_constant__ Sp
 }
 
 // Packet positions -> image nodes appended to a delivery source list.
-__global__ void unpack_kernel(const uint32_t* packets, const uint32_t* count, const int64_t* table,
-                              uint64_t table_len, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src,
-                              uint32_t src_cap, int* err) {
-  const uint32_t n = *count;
+// `count` comes from the sending rank: it is clamped to the block's capacity
+// (max_count) so a corrupt or over-full block cannot read past it.
+__global__ void unpack_kernel(const uint32_t* packets, const uint32_t* count, uint32_t max_count,
+                              const int64_t* table, uint64_t table_len, uint32_t* src_nodes, uint32_t* src_steps,
+                              uint32_t* n_src, uint32_t src_cap, int* err) {
+  uint32_t n = *count;
+  if (n > max_count) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(err, 5);
+    n = max_count;
+  }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t p = packets[2 * i];
     if (p >= table_len) { atomicExch(err, 4); continue; }
@@ -700,11 +706,11 @@ extern "C" int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uin
   return 0;
 }
 
-extern "C" int smx_unpack(const uint32_t* packets, const uint32_t* count, const int64_t* table, uint64_t table_len,
-                          uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err,
-                          void* stream) {
-  smx_count_launch(); unpack_kernel<<<148, T256, 0, (cudaStream_t)stream>>>(packets, count, table, table_len, src_nodes, src_steps,
-                                                         n_src, src_cap, err);
+extern "C" int smx_unpack(const uint32_t* packets, const uint32_t* count, uint32_t max_count, const int64_t* table,
+                          uint64_t table_len, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src,
+                          uint32_t src_cap, int* err, void* stream) {
+  smx_count_launch(); unpack_kernel<<<148, T256, 0, (cudaStream_t)stream>>>(packets, count, max_count, table, table_len,
+                                                                         src_nodes, src_steps, n_src, src_cap, err);
   SMX_LAUNCH_CHECK();
   return 0;
 }

@@ -37,6 +37,7 @@ from .api import (POINT_TO_POINT, ConnSpec, ConsistencyError, DelayRangeError, L
 TMP_KEY = 0x80000000
 ROW_MASK = 0xFFFFFF
 MAX_CLASSES = 256
+MAX_LIF_BLOCK = 16   # steps per lif_block_kernel launch (csrc/propagate.cu MAX_BLOCK)
 PHASES = ("construction", "preparation", "propagation")
 
 
@@ -121,6 +122,13 @@ def _all_distinct(a: np.ndarray) -> bool:
     return len(np.unique(a)) == len(a)
 
 
+def _syn_is_constant(syn) -> bool:
+    """Scalar weight and delay.  Reads only the two fields the reference's
+    SynSpec has (sm/construction.py:125-154), so reference objects work."""
+    return not isinstance(syn.weight, (tuple, list, np.ndarray)) and \
+        not isinstance(syn.delay_steps, (tuple, list, np.ndarray))
+
+
 def _words(nbits: int) -> int:
     return (int(nbits) + 31) // 32
 
@@ -156,7 +164,8 @@ class PhaseTimers:
 
 @dataclass
 class RunReport:
-    """sm/engine.py:55-82 (arena peaks are out of scope: reported as 0)."""
+    """sm/engine.py:55-82; host/device peaks are the modeled-byte arenas of
+    memory.py (the reference's cost table and placement plans)."""
 
     n_ranks: int
     comm_mode: str
@@ -327,6 +336,11 @@ class Cluster:
             else:
                 devices = [torch.device("cuda", 0)]
         devices = [torch.device(d) for d in devices]
+        if len({(d.type, d.index) for d in devices}) > 1:
+            # native calls run on the current device's stream and per-device
+            # kernel attributes are configured once per process: several
+            # devices need one process each (torchrun), not one Cluster
+            raise ValueError("one Cluster drives one device; use one process per GPU (torchrun) for several")
         self.ranks: dict[int, _Rank] = {
             r: _Rank(r, devices[i % len(devices)]) for i, r in enumerate(self.local)}
         for st in self.ranks.values():
@@ -516,7 +530,7 @@ class Cluster:
 
     def _syn_class(self, st: _Rank, syn: SynSpec, port: int):
         """Class id for a constant SynSpec in packed mode, or None (wide)."""
-        if syn.is_constant and not st.wide:
+        if _syn_is_constant(syn) and not st.wide:
             cid = self._class_id(float(syn.weight), int(syn.delay_steps), port)
             if cid < MAX_CLASSES:
                 st.used_classes.add(cid)
@@ -873,7 +887,7 @@ class Cluster:
         if not src_nodes or any(len(a) == 0 for a in src_nodes):
             raise ValueError("source populations must be non-empty")
         syn.validate()
-        if not syn.is_constant and (not isinstance(syn.weight, (tuple, float, int)) or
+        if not _syn_is_constant(syn) and (not isinstance(syn.weight, (tuple, float, int)) or
                                     not isinstance(syn.delay_steps, (tuple, int, np.integer))):
             # per-record arrays cannot match every source-rank batch (the
             # reference's _realize_syn raises on the first length mismatch)
@@ -1170,7 +1184,7 @@ class Cluster:
                  int(vbase[tr]), 0, sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
-        if st.wide and not syn.is_constant:
+        if st.wide and not _syn_is_constant(syn):
             self._dist_syn(st, syn, port, key, tr, total, n, base, runs, vbase, total_words, ranks_sorted,
                            pos if not multi else None, None if multi else gv_tab)
         elif st.wide:
@@ -1634,10 +1648,17 @@ class Cluster:
         st.wprefix = torch.zeros(st.src_cap, dtype=torch.int32, device=dev)
         st.n_work = torch.zeros(1, dtype=torch.int32, device=dev)
         st.err = torch.zeros(1, dtype=torch.int32, device=dev)
-        st.rec_cap = 1 << 22
+        # device raster: (step, gid) pairs, spilled to the host every
+        # rec_spill_steps steps of a recording run (a bound that cannot fill
+        # half the buffer: one spike per refractory period per neuron)
+        st.rec_cap = int(min(1 << 23, max(1 << 16, 64 * max(N, 1))))
+        per_step = -(-max(N, 1) // (max(self._ref_min or 0, 0) + 1))
+        st.rec_spill_steps = max(B, (st.rec_cap // 2) // per_step // B * B)
         st.rec = torch.zeros(2 * st.rec_cap, dtype=torch.int64, device=dev)
         st.n_rec = torch.zeros(1, dtype=torch.int64, device=dev)
         st.spike_total = torch.zeros(1, dtype=torch.int32, device=dev)
+        st.sent = torch.zeros(1, dtype=torch.int64, device=dev)   # exchanged pairs (byte counter)
+        st.rec_spill = []
         st.p2p_desc = ctypes_routes_desc(st.TP, st.p2p_packets, st.p2p_counts, self.n_ranks, st.pk_cap)
         st.g_desc = ctypes_routes_desc(st.GQ, st.g_packets, st.g_counts, len(self.groups), st.pk_cap)
         st.graph = None
@@ -1772,11 +1793,12 @@ class Cluster:
              ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), sk)
         self._deliver(st)
 
-    def _block_kernels(self, st, n_steps: int):
-        """n_steps steps of one rank in two launches (smx_block)."""
+    def _block_kernels(self, st, n_steps: int, offset: int = 0):
+        """n_steps (<= MAX_LIF_BLOCK) steps of one rank from block step
+        `offset`, in two launches (smx_block)."""
         call("smx_block", _ptr(st.v), _ptr(st.ref), _ptr(st.decay), _ptr(st.v_rest), _ptr(st.v_reset),
              _ptr(st.v_th), _ptr(st.ref_steps), _ptr(st.i_e), st.N, _ptr(st.ring), st.P, st.L, _ptr(st.now_dev),
-             0, n_steps, _ptr(st.record_dev), 3 * st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
+             offset, n_steps, _ptr(st.record_dev), 3 * st.pois_steps, ctypes_addr(st.fdev), st.n_fdev, _ptr(st.row2node_t),
              _ptr(st.gid_t), _ptr(st.first_index), _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.wprefix),
              _ptr(st.owner), st.owner_cap, _ptr(st.ctr), st.src_cap, _ptr(st.rec), _ptr(st.n_rec), st.rec_cap,
              _ptr(st.err), ctypes_addr(st.p2p_desc), ctypes_addr(st.g_desc), _ptr(st.payload), _ptr(st.cls_w),
@@ -1790,7 +1812,10 @@ class Cluster:
     def _block_body(self, n_steps: int):
         for st in self.ranks.values():
             if st.fused and st.block_ok and n_steps > 1:
-                self._block_kernels(st, n_steps)
+                # the LIF block kernel stages at most MAX_LIF_BLOCK steps of
+                # inputs; longer exchange blocks run as consecutive sub-blocks
+                for s0 in range(0, n_steps, MAX_LIF_BLOCK):
+                    self._block_kernels(st, min(MAX_LIF_BLOCK, n_steps - s0), s0)
             else:
                 for j in range(n_steps):
                     self._step_kernels(st, j)
@@ -1883,18 +1908,39 @@ class Cluster:
         """Message counters as the reference's lockstep transport would count
         them: one p2p round (n(n-1) messages) and one allgather per group per
         step (sm/transport.py:128,165)."""
-        if self.n_ranks == 1:
-            return
         per = (self.n_ranks * (self.n_ranks - 1) if self.has_p2p else 0)
         per += sum(len(self.groups[g]) for g in self.group_ids)
         self.messages["propagation"] += per * n_steps
 
-    def step(self):
-        """One step of every rank including its exchange round (sm/engine.py:277-310)."""
+    def step(self) -> dict:
+        """One step of every rank including its exchange round; returns the
+        spiking nodes of each local rank, ascending (sm/engine.py:277-310).
+        The spikes are read back through the device raster buffer (one
+        readback per step); simulate() keeps everything on the device."""
         if not self.prepared:
             raise ConsistencyError("prepare() the cluster before stepping")
-        self._set_record(self._recording)
+        keep = self._recording
+        marks = {r: int(st.n_rec.item()) for r, st in self.ranks.items()}
+        self._set_record(True)
         self._run_block(1, use_graph=False)
+        self._set_record(keep)
+        out = {}
+        for r, st in self.ranks.items():
+            n1 = int(st.n_rec.item())
+            if n1 > st.rec_cap:
+                raise ProtocolError(f"rank {r}: raster buffer overflow")
+            gids = st.rec[2 * marks[r]: 2 * n1].view(-1, 2)[:, 1].cpu().numpy()
+            out[r] = np.sort(self._gid_to_node(st, gids))
+            if not keep:
+                st.n_rec.fill_(marks[r])
+        return out
+
+    @staticmethod
+    def _gid_to_node(st, gids: np.ndarray) -> np.ndarray:
+        if getattr(st, "gid_order", None) is None:
+            st.gid_order = np.argsort(st.gid_np, kind="stable")
+        pos = np.searchsorted(st.gid_np, gids, sorter=st.gid_order)
+        return st.row2node_np[st.gid_order[pos]]
 
     def _set_record(self, on: bool):
         for st in self.ranks.values():
@@ -1905,7 +1951,13 @@ class Cluster:
         size replay one captured CUDA graph."""
         B = self.block
         done = 0
+        spill = min(st.rec_spill_steps for st in self.ranks.values())
+        since = 0
         while done < n_steps:
+            if self._recording and since >= spill:
+                self._spill_rec()
+                since = 0
+            since += min(B, n_steps - done)
             if self.now % B == 0 and n_steps - done >= B:
                 self._run_block(B, use_graph=self.use_graphs)
                 done += B
@@ -1920,6 +1972,11 @@ class Cluster:
         between ranks of this process."""
         for st in self.ranks.values():
             st.n_src.zero_()
+            # pairs put on the wire this round (sm/transport.py:128-129,165-166)
+            if self.has_p2p:
+                st.sent += st.p2p_counts.sum()
+            if self.group_ids:
+                st.sent += st.g_counts.sum()
         if self.has_p2p:
             for st in self.ranks.values():
                 for sr in range(self.n_ranks):
@@ -1931,7 +1988,7 @@ class Cluster:
                         continue
                     pk = src.p2p_packets[st.rank * src.pk_cap * 2:]
                     cnt = src.p2p_counts[st.rank:]
-                    call("smx_unpack", _ptr(pk), _ptr(cnt), _ptr(rl[1]), rl[1].numel(), _ptr(st.src_nodes),
+                    call("smx_unpack", _ptr(pk), _ptr(cnt), src.pk_cap, _ptr(rl[1]), rl[1].numel(), _ptr(st.src_nodes),
                          _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
         for g in self.group_ids:
             slot = self.group_slots[g]
@@ -1947,7 +2004,7 @@ class Cluster:
                     src = self.ranks[sr]
                     pk = src.g_packets[slot * src.pk_cap * 2:]
                     cnt = src.g_counts[slot:]
-                    call("smx_unpack", _ptr(pk), _ptr(cnt), _ptr(lk), lk.numel(), _ptr(st.src_nodes),
+                    call("smx_unpack", _ptr(pk), _ptr(cnt), src.pk_cap, _ptr(lk), lk.numel(), _ptr(st.src_nodes),
                          _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
         for st in self.ranks.values():
             self._deliver(st)
@@ -2017,7 +2074,7 @@ class Cluster:
                 if rl is None:
                     raise ProtocolError(f"rank {me}: spikes from rank {sr} but no map for that pair")
                 off = offs[sr]
-                call("smx_unpack", _ptr(rv[off + 2:]), _ptr(rv[off:]), _ptr(rl[1]), rl[1].numel(),
+                call("smx_unpack", _ptr(rv[off + 2:]), _ptr(rv[off:]), P["in_c"][sr], _ptr(rl[1]), rl[1].numel(),
                      _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
         for g, G in X["groups"].items():
             slot, cap, members = self.group_slots[g], G["cap"], G["members"]
@@ -2033,7 +2090,7 @@ class Cluster:
                 if lk is None:
                     continue
                 base = i * (2 + 2 * cap)
-                call("smx_unpack", _ptr(recv[base + 2:]), _ptr(recv[base:]), _ptr(lk), lk.numel(),
+                call("smx_unpack", _ptr(recv[base + 2:]), _ptr(recv[base:]), cap, _ptr(lk), lk.numel(),
                      _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
         self._deliver(st)
 
@@ -2041,10 +2098,16 @@ class Cluster:
         """Byte counter and capacity check of the fixed-capacity rounds (read
         once per simulate, not per block)."""
         for st in self.ranks.values():
+            if getattr(st, "sent", None) is not None:
+                self.bytes["propagation"] += 8 * int(st.sent.item())
+                st.sent.zero_()
             X = getattr(st, "xplan", None)
             if X is None:
                 continue
-            if int(X["over"].item()):
+            over = X["over"].clone()
+            if self.distributed:  # every rank raises together (no rank left waiting in a collective)
+                torch.distributed.all_reduce(over, op=torch.distributed.ReduceOp.MAX)
+            if int(over.item()):
                 raise ProtocolError(f"rank {st.rank}: exchange capacity exceeded")
             self.bytes["propagation"] += 8 * int(X["sent"].item())
             X["sent"].zero_()
@@ -2119,10 +2182,24 @@ class Cluster:
                 raise ProtocolError(f"rank {st.rank}: device error code {e} during propagation")
 
     # -------------------------------------------------------------- inspection
+    def _spill_rec(self):
+        """Move the recorded events of every rank to the host and reset the
+        device buffers (they keep their addresses: the block graph stays valid)."""
+        for st in self.ranks.values():
+            n = int(st.n_rec.item())
+            if n > st.rec_cap:
+                raise ProtocolError(f"rank {st.rank}: raster buffer overflow ({n} > {st.rec_cap} events)")
+            if n:
+                st.rec_spill.append(st.rec[: 2 * n].view(-1, 2).cpu().numpy())
+                st.n_rec.zero_()
+
     def rank_events(self, rank) -> np.ndarray:
         st = self.ranks[rank]
         n = int(st.n_rec.item())
-        return st.rec[: 2 * n].view(-1, 2).cpu().numpy()
+        if n > st.rec_cap:
+            raise ProtocolError(f"rank {rank}: raster buffer overflow ({n} > {st.rec_cap} events)")
+        cur = st.rec[: 2 * n].view(-1, 2).cpu().numpy()
+        return np.concatenate(st.rec_spill + [cur]) if st.rec_spill else cur
 
     def merged_raster(self) -> Raster:
         parts = [self.rank_events(r) for r in self.ranks]

@@ -10,6 +10,10 @@ does not exist on the GPU box); the outputs are committed:
   tests/golden/rasters.json      raster SHA-256 / event counts per scenario
   tests/golden/memory.json       modeled host/device peak bytes per rank after
                                  prepare, per scenario and optimisation level
+  tests/golden/c1_digests.json   C1 (10k neurons, K=1000, seed 12345) at full
+                                 size: SHA-256 of every table column, raster
+                                 SHA over 100 ms, per-neuron spike counts
+  tests/golden/transport.json    messages / bytes per phase after simulate()
 Usage:  python tests/golden/make_golden.py
 """
 from __future__ import annotations
@@ -114,10 +118,60 @@ def gen_memory():
         json.dump(out, fh, indent=1, sort_keys=True)
 
 
+C1 = dict(neurons_per_rank=10_000, k_exc=800, k_inh=200)   # BASELINE configs[0]
+C1_SEED, C1_MODEL_MS = 12345, 100.0
+
+
+def gen_c1():
+    """C1 at full size (1e7 synapses, 1 rank, seed 12345): SHA-256 digests of
+    every canonical table column and the raster over 100 ms (sm/models.py:
+    106-144; reference numpy backend)."""
+    ns = ref_namespace()
+    c = sm.Cluster(sm.SimConfig(n_ranks=1, comm_mode="p2p", seed=C1_SEED))
+    smm.build_balanced_network(c, smm.BalancedParams(**C1))
+    c.prepare()
+    dig = tables.digests(tables.canon_reference(c))
+    rep = c.simulate(0.0, C1_MODEL_MS, record=True)
+    counts = np.zeros(C1["neurons_per_rank"], dtype=np.int64)
+    ev = c.merged_raster().events
+    np.add.at(counts, np.asarray([e[1] for e in ev], dtype=np.int64), 1)
+    out = dict(config=dict(C1, seed=C1_SEED, comm_mode="p2p", model_ms=C1_MODEL_MS),
+               n_synapses=int(sum(len(st.store.src) for st in c.ranks)), tables=dig,
+               raster=dict(sha256=rep.raster_sha256, n_events=rep.n_spike_events),
+               spike_counts_sha256=hashlib.sha256(counts.tobytes()).hexdigest())
+    with open(os.path.join(HERE, "c1_digests.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+    print("C1", out["n_synapses"], out["raster"], file=sys.stderr)
+    del ns
+
+
+def gen_transport():
+    """Transport counters of each simulated scenario (sm/transport.py:55-67,
+    128-129, 165-166): messages and bytes per phase after simulate()."""
+    ns = ref_namespace()
+    out = {}
+    for name, fn in scenarios.SCENARIOS.items():
+        c, sim = fn(ns)
+        if sim is None:
+            continue
+        rep = c.simulate(sim[0], sim[1], record=False)
+        out[name] = dict(messages=rep.transport_messages, bytes=rep.transport_bytes)
+    with open(os.path.join(HERE, "transport.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
+    if "--transport-only" in sys.argv:
+        gen_transport()
+        sys.exit(0)
+    if "--c1-only" in sys.argv:
+        gen_c1()
+        sys.exit(0)
     if "--memory-only" in sys.argv:
         gen_memory()
         sys.exit(0)
     gen_rng()
     gen_tables()
     gen_memory()
+    gen_c1()
+    gen_transport()

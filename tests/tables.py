@@ -106,3 +106,17 @@ def compare(a: dict, b: dict) -> list[str]:
             i = int(np.flatnonzero(x.astype(np.int64) != y.astype(np.int64))[0])
             bad.append(f"{k}: differs at {i} ({x.reshape(-1)[i]} vs {y.reshape(-1)[i]})")
     return bad
+
+
+def digests(t: dict) -> dict:
+    """SHA-256 of every non-empty canonical array (integers as int64, floats
+    as float64 bits, C order) -- full-size tables compared by digest."""
+    import hashlib
+    out = {}
+    for k in sorted(t):
+        x = np.asarray(t[k])
+        if not x.size:
+            continue
+        x = np.ascontiguousarray(x.astype(np.float64) if x.dtype.kind == "f" else x.astype(np.int64))
+        out[k] = dict(sha256=hashlib.sha256(x.tobytes()).hexdigest(), shape=list(x.shape))
+    return out

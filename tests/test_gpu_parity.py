@@ -33,8 +33,9 @@ def test_raster(name):
     rep = c.simulate(sim[0], sim[1], record=True)
     want = RASTERS[name]["n_events"]
     if name in scenarios.NON_DYADIC:
-        # non-dyadic weights: fp64 input sums depend on atomic order (1 ulp);
-        # spike counts agree over short runs up to rare threshold ties
+        # non-dyadic weights over the full span: last-ulp differences of the
+        # input sums can flip a rare threshold tie late in the run; exact
+        # per-neuron counts over a short run: test_non_dyadic_short_run
         assert abs(rep.n_spike_events - want) <= max(2, 0.01 * want)
     else:
         assert rep.n_spike_events == want
@@ -42,22 +43,29 @@ def test_raster(name):
 
 
 @pytest.mark.parametrize("name", sorted(scenarios.NON_DYADIC))
-def test_v_tolerance_non_dyadic(name):
-    """V within 1e-9 (relative) of the oracle for >= 99% of neurons after a
-    short run with per-synapse normal weights (north star: fp32 tolerance)."""
+def test_non_dyadic_short_run(name):
+    """Per-synapse normal weights: the fp64 input sums depend on the order of
+    the delivery atomics (last-ulp differences).  Over a short run (3 ms)
+    every neuron's spike count equals the oracle's (the reference's
+    sequential order) exactly, and EVERY neuron's V agrees within
+    V_TOL = 1e-9 mV (the north star's fp32 tolerance would be ~4e-6 mV at
+    -65 mV)."""
     from namespaces import gpu_ns, oracle_ns
+    V_TOL = 1e-9
     g, sim = scenarios.SCENARIOS[name](gpu_ns())
     o, _ = scenarios.SCENARIOS[name](oracle_ns())
-    g.simulate(0.0, 3.0, record=False)
-    o.simulate(0.0, 3.0, record=False)
-    close = total = 0
+    g.simulate(0.0, 3.0, record=True)
+    o.simulate(0.0, 3.0, record=True)
+    ge, oe = g.merged_raster().events, o.raster()
+    gids_g, cnt_g = np.unique(ge[:, 1], return_counts=True)
+    gids_o, cnt_o = np.unique(oe[:, 1], return_counts=True)
+    assert np.array_equal(gids_g, gids_o) and np.array_equal(cnt_g, cnt_o)
     for r in sorted(g.ranks):
         e = g.export(r)
         st = o.ranks[r]
         ov = st.v[np.flatnonzero(st.mask)]
-        close += int(np.sum(np.abs(e["v"] - ov) <= 1e-9 * np.abs(ov)))
-        total += len(ov)
-    assert close >= 0.99 * total, (close, total)
+        assert len(ov) == len(e["v"])
+        assert float(np.max(np.abs(e["v"] - ov), initial=0.0)) <= V_TOL
 
 
 def test_v_after_run_matches_oracle():

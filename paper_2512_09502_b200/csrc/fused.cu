@@ -1,0 +1,804 @@
+// Fused construction path: connectivity generation fused into the first pass
+// of the stable LSD sort (SURVEY §7 hard part 3).
+//
+// The reference realises a fixed-in-degree call as `integers(0, total, K*N)`
+// target-major draws (sm/construction.py:391-406, 640-703), appends the
+// records in call order and finally sorts them stably by source
+// (ConnectionStore.finalize, sm/core.py:299-324).  A stable LSD radix sort
+// of the records over their (call, draw) order reproduces that table, and its
+// first pass only needs each record's low key digit -- which the draw itself
+// produces.  So instead of writing (key, payload) records and re-reading them:
+//
+//   pass A (fused_gen_kernel, one launch per call, at prepare time)
+//     draws a tile of 8192 raw u32 positions once (Philox4x64-10 + Lemire),
+//     maps accepted values to final source keys, ranks the tile's records
+//     stably by the low key digit (ballot multisplit), finds each digit's
+//     position across tiles with a decoupled look-back (tiles taken in order
+//     from a ticket) and writes one packed u32 per record into that digit's
+//     region:  rec = (key >> lo_bits) << pbits | call tag | target index.
+//     Regions are sized from the exact digit probabilities of the call's
+//     source-value -> key map (expectation + 8 sigma); an overflow sets a flag
+//     and the engine rebuilds the rank through the general path.
+//   pass B (smx_fused_sort)
+//     per 3840-record tile of a region: histogram of the high digit
+//     (fb_hist), per-region / per-digit scans (per-key counts for
+//     first_index fall out of the same sums), then a stable scatter by the
+//     high digit that writes the final payload pay_tab[call][target index]
+//     (fb_scatter, TMA tile loads, coalesced digit runs).
+//
+// Record bytes: pass A writes 4 B, pass B reads 4 B twice and writes 4 B
+// (16 B/synapse against 51 B for generate-then-sort with 8-byte records).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+#include "common.cuh"
+
+using namespace smx;
+
+namespace {
+
+// ------------------------------------------------------------------ pass A
+constexpr int FG_THREADS = 512;
+constexpr int FG_WARPS = FG_THREADS / 32;
+constexpr int FG_IPT = 16;                       // raw positions per thread per tile
+constexpr int FG_TILE = FG_THREADS * FG_IPT;     // 8192 raw u32 positions per tile
+constexpr int FG_XS = FG_TILE + FG_TILE / 32;    // padded transpose buffer
+constexpr uint32_t FG_NOKEY = 0xFFFFFFFFu;       // rejected draw / outside the window
+constexpr uint32_t FG_SENTINEL = 0xFFFFFFFFu;    // accepted draw past the call's last record
+constexpr uint32_t ST_A = 1u << 30, ST_P = 2u << 30, ST_VAL = (1u << 30) - 1;
+constexpr int FG_MAXP = 8;
+#ifndef SMX_FG_MIN_BLOCKS
+#define SMX_FG_MIN_BLOCKS 2
+#endif
+
+struct FusedGen {
+  Key key;
+  Lemire lm;
+  uint64_t n_raw;     // raw u32 positions of the window (from stream position 0)
+  uint64_t n_out;     // records of the call
+  uint32_t np;        // key pieces (key mode 3)
+  uint32_t pstart[FG_MAXP], pdelta[FG_MAXP];
+  const uint32_t* key_tab;  // key mode 1: key = key_tab[value]
+  uint32_t kdiv;      // k_in: target index = j / kdiv
+  FastDiv kd;
+  int wide_j;         // j may reach 2^32
+  uint32_t tag;       // call tag << tidx_bits
+  int pbits;          // bits below the high key digit in a record
+  uint32_t* region;
+  const uint64_t* rstart;   // [B] first slot of each digit region
+  const uint64_t* rcap;     // [B] capacity of each region (records)
+  const uint64_t* fill_in;  // [B] records already in the region (earlier calls)
+  uint64_t* fill_out;       // [B] after this call (written by the last tile)
+  uint32_t* status;         // [n_tiles][B] look-back descriptors
+  uint32_t* ticket;
+  uint64_t* total;          // accepted draws in the window (last tile)
+  int* overflow;
+};
+
+template <int KM>
+__device__ __forceinline__ uint32_t fg_key(const FusedGen& g, uint32_t v) {
+  if (KM == 1) return __ldg(g.key_tab + v);
+  uint32_t off = g.pdelta[0];
+#pragma unroll
+  for (int s = 1; s < FG_MAXP; ++s)
+    if (s < (int)g.np && v >= g.pstart[s]) off = g.pdelta[s];
+  return v + off;
+}
+
+__device__ __forceinline__ uint32_t fg_tidx(const FusedGen& g, uint64_t j) {
+  if (!g.wide_j) return g.kd.div((uint32_t)j);
+  uint64_t q = (uint64_t)((double)j / (double)g.kdiv);  // within one of the quotient for j < 2^53
+  int64_t r = (int64_t)(j - q * g.kdiv);
+  while (r < 0) { --q; r += g.kdiv; }
+  while (r >= (int64_t)g.kdiv) { ++q; r -= g.kdiv; }
+  return (uint32_t)q;
+}
+
+__device__ __forceinline__ uint32_t ld_vol(const uint32_t* p) { return *(const volatile uint32_t*)p; }
+__device__ __forceinline__ void st_vol(uint32_t* p, uint32_t v) { *(volatile uint32_t*)p = v; }
+
+// Stable rank of one item per lane among the warp's items with the same
+// digit (ballot multisplit, as in sort.cu) against the warp's SMEM counters.
+template <int LB>
+__device__ __forceinline__ uint32_t fg_rank(uint32_t d, bool valid, uint32_t vm, uint16_t* mycnt, int lane,
+                                            uint32_t lt) {
+  uint32_t peers = vm;
+#pragma unroll
+  for (int b = 0; b < LB; ++b) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t, bal;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "vote.sync.ballot.b32 bal, p, 0xffffffff;\n\t"
+        "@!p not.b32 bal, bal;\n\t"
+        "and.b32 %0, %0, bal;\n\t}"
+        : "+r"(peers) : "r"(d), "r"(1u << b));
+  }
+  if (!valid) peers = 1u << lane;
+  const int leader = __ffs(peers) - 1;
+  uint32_t old = 0;
+  if (valid && lane == leader) {
+    old = mycnt[d];
+    mycnt[d] = (uint16_t)(old + __popc(peers));
+  }
+  old = __shfl_sync(0xffffffffu, old, leader);
+  return valid ? old + __popc(peers & lt) : 0xffffu;
+}
+
+template <int KM, int LB>
+__global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
+    fused_gen_kernel(const __grid_constant__ FusedGen g, uint32_t n_tiles) {
+  constexpr int B = 1 << LB;
+  constexpr uint32_t DM = B - 1;
+  constexpr int BC = B < 2 ? 2 : B;  // counter row length (even: zeroed as u32 words)
+  extern __shared__ __align__(16) uint8_t fg_smem[];
+  uint32_t* xs = reinterpret_cast<uint32_t*>(fg_smem);               // [FG_XS] keys, then staged records
+  uint64_t* delta = reinterpret_cast<uint64_t*>(xs + FG_XS);         // [B]
+  uint32_t* tstart = reinterpret_cast<uint32_t*>(delta + B);         // [B]
+  uint16_t* sd = reinterpret_cast<uint16_t*>(tstart + B);            // [FG_TILE] digit of each staged record
+  uint16_t* wcnt = sd + FG_TILE;                                     // [FG_WARPS][BC]
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t wacc[FG_WARPS];
+  __shared__ unsigned long long wred[FG_WARPS];
+  __shared__ uint32_t s_t;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1;
+  uint16_t* mycnt = wcnt + warp * BC;
+  for (;;) {
+    if (tid == 0) s_t = atomicAdd(g.ticket, 1u);
+    __syncthreads();
+    const uint32_t t = s_t;
+    if (t >= n_tiles) break;
+    // 1. draw the thread's 16 consecutive raw positions (two Philox blocks)
+    const uint64_t p0 = (uint64_t)t * FG_TILE + (uint64_t)tid * FG_IPT;
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      uint64_t w[4];
+      philox4x64_10(p0 / 8 + q + 1, g.key, w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t v = (i & 1) ? (uint32_t)(w[i >> 1] >> 32) : (uint32_t)w[i >> 1];
+        uint32_t out;
+        const bool ok = g.lm.accept(v, out) && p0 + 8 * q + i < g.n_raw;
+        const uint32_t p = tid * FG_IPT + 8 * q + i;
+        xs[p + (p >> 5)] = ok ? fg_key<KM>(g, out) : FG_NOKEY;
+      }
+    }
+    __syncthreads();
+    // 2. raw order, warp-striped: item i of lane l is warp position 32 i + l
+    uint32_t k[FG_IPT];
+#pragma unroll
+    for (int i = 0; i < FG_IPT; ++i) {
+      const uint32_t p = warp * (32 * FG_IPT) + 32 * i + lane;
+      k[i] = xs[p + (p >> 5)];
+    }
+    for (int j = lane; j < BC / 2; j += 32) reinterpret_cast<uint32_t*>(mycnt)[j] = 0;
+    __syncwarp();
+    uint32_t rank2[FG_IPT / 2];
+    uint32_t run = 0;
+#pragma unroll
+    for (int i = 0; i < FG_IPT; ++i) {
+      const bool valid = k[i] != FG_NOKEY;
+      const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+      const uint32_t ar = run + __popc(vm & lt);
+      run += __popc(vm);
+      const uint32_t r = LB == 0 ? (valid ? ar : 0xffffu) : fg_rank<LB>(k[i] & DM, valid, vm, mycnt, lane, lt);
+      if (i & 1) rank2[i >> 1] |= r << 16;
+      else rank2[i >> 1] = r;
+    }
+    if (lane == 0) {
+      wacc[warp] = run;
+      if (LB == 0) mycnt[0] = (uint16_t)run;
+    }
+    __syncthreads();  // counters complete; xs is free
+    // 3. per digit: tile count, per-warp exclusive bases; publish the aggregate
+    uint32_t c = 0;
+    if (tid < B) {
+      uint32_t acc = 0;
+#pragma unroll 4
+      for (int w = 0; w < FG_WARPS; ++w) {
+        const uint32_t x = wcnt[w * BC + tid];
+        wcnt[w * BC + tid] = (uint16_t)acc;
+        acc += x;
+      }
+      c = acc;
+      st_vol(g.status + (size_t)t * B + tid, (t == 0 ? ST_P : ST_A) | c);
+    }
+    uint32_t tot;
+    const uint32_t ts = block_excl_scan(tid < B ? c : 0u, ws, tot);
+    // 4. look-back: records of this digit in earlier tiles of the call
+    uint64_t excl = 0;
+    if (tid < B) {
+      tstart[tid] = ts;
+      if (t > 0) {
+        uint32_t e = 0;
+        for (int64_t i = (int64_t)t - 1;;) {
+          const uint32_t w = ld_vol(g.status + (size_t)i * B + tid);
+          if (w == 0) continue;  // predecessor still drawing
+          e += w & ST_VAL;
+          if (w & ST_P) break;
+          --i;
+        }
+        excl = e;
+        st_vol(g.status + (size_t)t * B + tid, ST_P | (e + c));
+      }
+      const uint64_t filled = g.fill_in[tid] + excl;
+      if (filled + c > g.rcap[tid]) {
+        atomicExch(g.overflow, 1);
+        delta[tid] = ~0ull;
+      } else {
+        delta[tid] = g.rstart[tid] + filled - ts;
+      }
+      if (t == n_tiles - 1) g.fill_out[tid] = filled + c;
+    }
+    // draw index of the tile's first accepted value = sum of the digit prefixes
+    unsigned long long sx = excl;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    if (lane == 0) wred[warp] = sx;
+    __syncthreads();
+    uint64_t jbase = 0, wbase = 0;
+#pragma unroll
+    for (int w = 0; w < FG_WARPS; ++w) {
+      jbase += wred[w];
+      if (w < warp) wbase += wacc[w];
+    }
+    if (t == n_tiles - 1 && tid == 0) *g.total = jbase + tot;
+    // 5. records, staged in digit order (accept ranks recomputed: fewer live registers)
+    uint64_t jw = jbase + wbase;
+#pragma unroll
+    for (int i = 0; i < FG_IPT; ++i) {
+      const uint32_t vm = __ballot_sync(0xffffffffu, k[i] != FG_NOKEY);
+      const uint64_t j = jw + __popc(vm & lt);
+      jw += __popc(vm);
+      const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+      if (r == 0xffffu) continue;
+      const uint32_t d = LB ? (k[i] & DM) : 0u;
+      const uint32_t rec = j < g.n_out ? (((k[i] >> LB) << g.pbits) | g.tag | fg_tidx(g, j)) : FG_SENTINEL;
+      const uint32_t pos = tstart[d] + wcnt[warp * BC + d] + r;
+      xs[pos] = rec;
+      sd[pos] = (uint16_t)d;
+    }
+    __syncthreads();
+    // 6. coalesced runs per digit
+    for (uint32_t q = tid; q < tot; q += FG_THREADS) {
+      const uint32_t d = sd[q];
+      const uint64_t base = delta[d];
+      if (base != ~0ull) g.region[base + q] = xs[q];
+    }
+    __syncthreads();
+  }
+}
+
+template <int KM, int LB>
+size_t fg_smem() {
+  constexpr int B = 1 << LB;
+  constexpr int BC = B < 2 ? 2 : B;
+  return (size_t)FG_XS * 4 + (size_t)B * 12 + (size_t)FG_TILE * 2 + (size_t)FG_WARPS * BC * 2;
+}
+
+template <int KM, int LB>
+int fg_launch(const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
+  const size_t smem = fg_smem<KM, LB>();
+  static int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {  // per device (one Cluster drives one device; see engine)
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(fused_gen_kernel<KM, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    configured = dev;
+  }
+  const uint32_t grid = std::min<uint32_t>(n_tiles, 148u * SMX_FG_MIN_BLOCKS);
+  smx_count_launch();
+  fused_gen_kernel<KM, LB><<<grid, FG_THREADS, smem, st>>>(g, n_tiles);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int KM>
+int fg_dispatch(int lo_bits, const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
+  switch (lo_bits) {
+    case 0: return fg_launch<KM, 0>(g, n_tiles, st);
+    case 1: return fg_launch<KM, 1>(g, n_tiles, st);
+    case 2: return fg_launch<KM, 2>(g, n_tiles, st);
+    case 3: return fg_launch<KM, 3>(g, n_tiles, st);
+    case 4: return fg_launch<KM, 4>(g, n_tiles, st);
+    case 5: return fg_launch<KM, 5>(g, n_tiles, st);
+    case 6: return fg_launch<KM, 6>(g, n_tiles, st);
+    case 7: return fg_launch<KM, 7>(g, n_tiles, st);
+    case 8: return fg_launch<KM, 8>(g, n_tiles, st);
+    case 9: return fg_launch<KM, 9>(g, n_tiles, st);
+    default: break;
+  }
+  smx_set_error("smx_fused_gen: low digit of %d bits (0..9 supported)", lo_bits);
+  return -1;
+}
+
+// ------------------------------------------------------------------ pass B
+constexpr int FB_THREADS = 256;
+constexpr int FB_WARPS = FB_THREADS / 32;
+constexpr int FB_IPT = 15;
+constexpr int FB_TILE = FB_THREADS * FB_IPT;   // 3840 records
+constexpr int FB_TC = 256;                     // tiles per scan chunk (chunks never straddle regions)
+
+struct FusedSort {
+  const uint32_t* region;
+  const uint64_t* rstart;     // [R] region start slots
+  const uint64_t* fill;       // [R] records per region
+  const uint32_t* tile_first; // [R + 1] first tile of each region
+  const uint32_t* chunk_first;// [R + 1] first scan chunk of each region
+  uint32_t n_regions;
+  int pbits;                  // record = hi << pbits | tag | tidx
+  int tidx_bits;
+  int lo_bits;                // key = hi << lo_bits | region
+  const uint64_t* pay_tabs;   // [n_tags] device pointers to u32 payload tables
+  uint32_t* counts;           // [n_keys] records per key
+  uint64_t n_keys;
+  uint32_t* out;              // final payload (sorted by key)
+  int* err;
+};
+
+__device__ __forceinline__ uint32_t upper_region(const uint32_t* first, uint32_t n, uint32_t x) {
+  // largest r with first[r] <= x  (first ascending, first[0] = 0)
+  uint32_t lo = 0, hi = n;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(first + mid) <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+struct FbTile {
+  uint32_t region;
+  uint64_t a;     // first slot
+  uint32_t n;     // records in the tile
+};
+
+__device__ __forceinline__ FbTile fb_tile(const FusedSort& s, uint32_t T) {
+  FbTile x;
+  x.region = upper_region(s.tile_first, s.n_regions, T);
+  const uint64_t local = (uint64_t)(T - __ldg(s.tile_first + x.region)) * FB_TILE;
+  x.a = __ldg(s.rstart + x.region) + local;
+  const uint64_t f = __ldg(s.fill + x.region);
+  x.n = f > local ? (f - local < (uint64_t)FB_TILE ? (uint32_t)(f - local) : (uint32_t)FB_TILE) : 0u;
+  return x;
+}
+
+// Per-tile histogram of the high digit (sentinels skipped); one warp per tile.
+template <int BITS>
+__global__ void __launch_bounds__(1024) fb_hist_kernel(const __grid_constant__ FusedSort s, uint16_t* tcnt,
+                                                       uint32_t n_tiles) {
+  constexpr int BINS = 1 << BITS;
+  extern __shared__ uint32_t fbh[];  // [32][BINS]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* wh = fbh + warp * BINS;
+  for (uint32_t T = blockIdx.x * 32 + warp; T < n_tiles; T += gridDim.x * 32) {
+    for (int j = lane; j < BINS; j += 32) wh[j] = 0;
+    __syncwarp();
+    const FbTile x = fb_tile(s, T);
+    const uint32_t* src = s.region + x.a;
+    const uint32_t nq = x.n / 4;
+    for (uint32_t i = lane; i < nq; i += 32) {
+      const uint4 q = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+      const uint32_t r[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (r[u] != FG_SENTINEL) atomicAdd(&wh[r[u] >> s.pbits], 1u);
+    }
+    for (uint32_t i = nq * 4 + lane; i < x.n; i += 32) {
+      const uint32_t r = src[i];
+      if (r != FG_SENTINEL) atomicAdd(&wh[r >> s.pbits], 1u);
+    }
+    __syncwarp();
+    uint32_t* o = reinterpret_cast<uint32_t*>(tcnt + (size_t)T * BINS);
+    for (int j = lane; j < BINS / 2; j += 32) o[j] = wh[2 * j] | (wh[2 * j + 1] << 16);
+    __syncwarp();
+  }
+}
+
+// csum[chunk][d] = sum of the chunk's tile counts
+template <int BITS>
+__global__ void __launch_bounds__(256) fb_chunk_sum_kernel(const __grid_constant__ FusedSort s, const uint16_t* tcnt,
+                                                           uint32_t* csum) {
+  constexpr int BINS = 1 << BITS;
+  const uint32_t C = blockIdx.x;
+  const uint32_t r = upper_region(s.chunk_first, s.n_regions, C);
+  const uint32_t t0 = s.tile_first[r] + (C - s.chunk_first[r]) * FB_TC;
+  const uint32_t t1 = min(s.tile_first[r + 1], t0 + FB_TC);
+  for (int d = threadIdx.x; d < BINS; d += 256) {
+    uint32_t acc = 0;
+#pragma unroll 8
+    for (uint32_t t = t0; t < t1; ++t) acc += tcnt[(size_t)t * BINS + d];
+    csum[(size_t)C * BINS + d] = acc;
+  }
+}
+
+// One CTA: per high digit, exclusive prefix over the chunks in (region,
+// chunk) order -- the stable order of the input -- in place; per-key
+// counts (key = d << lo_bits | region) from the per-region sums; digit bases.
+template <int BITS>
+__global__ void __launch_bounds__(1024) fb_digit_scan_kernel(const __grid_constant__ FusedSort s, uint32_t* csum,
+                                                             uint64_t* dbase) {
+  constexpr int BINS = 1 << BITS;
+  constexpr int DPT = (BINS + 1023) / 1024;
+  __shared__ unsigned long long ws[32];
+  uint64_t tot[DPT];
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int d = threadIdx.x * DPT + j;
+    uint64_t run = 0;
+    if (d < BINS) {
+      for (uint32_t r = 0; r < s.n_regions; ++r) {
+        const uint32_t c0 = s.chunk_first[r], c1 = s.chunk_first[r + 1];
+        // region r's records of digit d follow the earlier regions' (run)
+        uint32_t rsum = 0;
+#pragma unroll 4
+        for (uint32_t C = c0; C < c1; ++C) {
+          const uint32_t x = csum[(size_t)C * BINS + d];
+          csum[(size_t)C * BINS + d] = (uint32_t)run + rsum;
+          rsum += x;
+        }
+        if (run + rsum > 0xffffffffull) atomicExch(s.err, 7);  // within-digit offsets are 32-bit
+        const uint64_t key = ((uint64_t)d << s.lo_bits) | r;
+        if (rsum) {
+          if (key < s.n_keys) s.counts[key] = rsum;
+          else atomicExch(s.err, 6);
+        }
+        run += rsum;
+      }
+    }
+    tot[j] = run;
+  }
+  // exclusive scan of the digit totals -> digit bases (64-bit)
+  uint64_t mine = 0;
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) mine += tot[j];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t v = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    ws[lane] = v;
+  }
+  __syncthreads();
+  uint64_t base = (warp ? ws[warp - 1] : 0) + inc - mine;
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    const int d = threadIdx.x * DPT + j;
+    if (d < BINS) dbase[d] = base;
+    base += tot[j];
+  }
+}
+
+// off[tile][d] = within-digit position of the tile's first record of digit d
+template <int BITS>
+__global__ void __launch_bounds__(256) fb_tile_offsets_kernel(const __grid_constant__ FusedSort s, const uint16_t* tcnt,
+                                                              const uint32_t* csum, uint32_t* off) {
+  constexpr int BINS = 1 << BITS;
+  const uint32_t C = blockIdx.x;
+  const uint32_t r = upper_region(s.chunk_first, s.n_regions, C);
+  const uint32_t t0 = s.tile_first[r] + (C - s.chunk_first[r]) * FB_TC;
+  const uint32_t t1 = min(s.tile_first[r + 1], t0 + FB_TC);
+  for (int d = threadIdx.x; d < BINS; d += 256) {
+    uint32_t run = csum[(size_t)C * BINS + d];
+    for (uint32_t t = t0; t < t1; ++t) {
+      off[(size_t)t * BINS + d] = run;
+      run += tcnt[(size_t)t * BINS + d];
+    }
+  }
+}
+
+// Stable scatter by the high digit; tiles in global (region, tile) order from
+// a ticket so the tiles in flight write neighbouring parts of every digit's
+// output (partial sectors complete in L2).  Writes the final payload.
+template <int BITS>
+__global__ void __launch_bounds__(FB_THREADS, 2) fb_scatter_kernel(const __grid_constant__ FusedSort s,
+                                                                   const uint32_t* off, const uint64_t* dbase,
+                                                                   uint32_t n_tiles, uint32_t* tile_ctr) {
+  constexpr int BINS = 1 << BITS;
+  constexpr int DPT = BINS / FB_THREADS;
+  static_assert(DPT >= 1, "at least 8-bit digits");
+  constexpr uint32_t mask = BINS - 1;
+  extern __shared__ __align__(128) uint8_t fbs[];
+  uint32_t* irec = reinterpret_cast<uint32_t*>(fbs);              // [FB_TILE] TMA target, then staged payloads
+  uint16_t* sdig = reinterpret_cast<uint16_t*>(irec + FB_TILE);   // [FB_TILE] staged digits
+  uint32_t* ioff = reinterpret_cast<uint32_t*>(sdig + FB_TILE);   // [BINS] TMA target
+  uint64_t* delta = reinterpret_cast<uint64_t*>(ioff + BINS);     // [BINS]
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(delta + BINS);     // [FB_WARPS][BINS]
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t ticket[2];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1;
+  const uint32_t tmask = (1u << s.tidx_bits) - 1;
+  const uint32_t pmask = (1u << s.pbits) - 1;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t T) {  // thread 0: offset row + (full tiles) records
+    const FbTile x = fb_tile(s, T);
+    const bool full = x.n == FB_TILE;
+    mbar_expect_tx(&bar, BINS * 4 + (full ? FB_TILE * 4 : 0));
+    bulk_g2s(ioff, off + (size_t)T * BINS, BINS * 4, &bar);
+    if (full) bulk_g2s(irec, s.region + x.a, FB_TILE * 4, &bar);
+  };
+  if (tid == 0) {
+    const uint32_t T = atomicAdd(tile_ctr, 1u);
+    ticket[0] = T;
+    if (T < n_tiles) issue(T);
+  }
+  __syncthreads();
+  uint16_t* mycnt = wcnt + warp * BINS;
+  const uint32_t wofs = warp * (32 * FB_IPT) + lane;
+  uint32_t phase = 0;
+  int slot = 0;
+  for (uint32_t T = ticket[0]; T < n_tiles; T = ticket[slot ^= 1]) {
+    const FbTile x = fb_tile(s, T);
+    const bool full = x.n == FB_TILE;
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    uint32_t rec[FB_IPT];
+#pragma unroll
+    for (int i = 0; i < FB_IPT; ++i) {
+      const uint32_t q = wofs + i * 32;
+      rec[i] = full ? irec[q] : (q < x.n ? s.region[x.a + q] : FG_SENTINEL);
+    }
+    {
+      uint32_t* w32 = reinterpret_cast<uint32_t*>(mycnt);
+#pragma unroll
+      for (int j = lane; j < BINS / 2; j += 32) w32[j] = 0;
+      __syncwarp();
+    }
+    uint32_t rank2[(FB_IPT + 1) / 2];
+#pragma unroll
+    for (int i = 0; i < FB_IPT; ++i) {
+      const bool valid = rec[i] != FG_SENTINEL;
+      const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+      const uint32_t r = fg_rank<BITS>((rec[i] >> s.pbits) & mask, valid, vm, mycnt, lane, lt);
+      if (i & 1) rank2[i >> 1] |= r << 16; else rank2[i >> 1] = r;
+    }
+    __syncthreads();  // 1: counters complete, records in registers
+    if (tid == 0) ticket[slot ^ 1] = atomicAdd(tile_ctr, 1u);
+    uint32_t tot[DPT];
+    uint32_t mysum = 0;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const int d = tid * DPT + j;
+      uint32_t t = 0;
+#pragma unroll
+      for (int w = 0; w < FB_WARPS; ++w) t += wcnt[w * BINS + d];
+      tot[j] = t;
+      mysum += t;
+    }
+    uint32_t tsum;
+    uint32_t run = block_excl_scan(mysum, ws, tsum);
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const int d = tid * DPT + j;
+      uint32_t t = run;
+#pragma unroll
+      for (int w = 0; w < FB_WARPS; ++w) {
+        const uint32_t c = wcnt[w * BINS + d];
+        wcnt[w * BINS + d] = (uint16_t)t;
+        t += c;
+      }
+      delta[d] = dbase[d] + ioff[d] - run;
+      run += tot[j];
+    }
+    __syncthreads();  // 2: offsets ready; offset row and record buffer free
+    const uint32_t nxt = ticket[slot ^ 1];
+    // stage payloads in digit order (the record buffer is reused)
+#pragma unroll
+    for (int i = 0; i < FB_IPT; ++i) {
+      const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+      if (r != 0xffffu) {
+        const uint32_t d = (rec[i] >> s.pbits) & mask;
+        const uint32_t low = rec[i] & pmask;
+        const uint32_t* pt = reinterpret_cast<const uint32_t*>(__ldg(s.pay_tabs + (low >> s.tidx_bits)));
+        const uint32_t pos = mycnt[d] + r;
+        irec[pos] = __ldg(pt + (low & tmask));
+        sdig[pos] = (uint16_t)d;
+      }
+    }
+    __syncthreads();  // 3: staged
+    for (uint32_t q = tid; q < tsum; q += FB_THREADS) s.out[delta[sdig[q]] + q] = irec[q];
+    __syncthreads();  // 4: staging read: buffers may be refilled
+    if (tid == 0 && nxt < n_tiles) {
+      fence_proxy_async();
+      issue(nxt);
+    }
+  }
+}
+
+template <int BITS>
+int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, cudaStream_t st) {
+  constexpr int BINS = 1 << BITS;
+  uint16_t* tcnt = nullptr;
+  uint32_t *off = nullptr, *csum = nullptr, *ctr = nullptr;
+  uint64_t* dbase = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&tcnt, sizeof(uint16_t) * (size_t)n_tiles * BINS, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&off, sizeof(uint32_t) * (size_t)n_tiles * BINS, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&csum, sizeof(uint32_t) * (size_t)std::max<uint32_t>(n_chunks, 1) * BINS, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&dbase, sizeof(uint64_t) * BINS, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&ctr, sizeof(uint32_t), st));
+  SMX_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
+  const size_t h_smem = (size_t)32 * BINS * 4;
+  const size_t s_smem = (size_t)FB_TILE * 6 + (size_t)BINS * 12 + (size_t)FB_WARPS * BINS * 2;
+  static int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(fb_hist_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h_smem));
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(fb_scatter_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)s_smem));
+    configured = dev;
+  }
+  const uint32_t hgrid = std::max<uint32_t>(1, std::min<uint32_t>((n_tiles + 31) / 32, 148 * 2));
+  smx_count_launch(); fb_hist_kernel<BITS><<<hgrid, 1024, h_smem, st>>>(s, tcnt, n_tiles);
+  if (n_chunks) {
+    smx_count_launch(); fb_chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum);
+  }
+  smx_count_launch(); fb_digit_scan_kernel<BITS><<<1, 1024, 0, st>>>(s, csum, dbase);
+  if (n_chunks) {
+    smx_count_launch(); fb_tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum, off);
+  }
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(n_tiles, 148u * 2));
+  smx_count_launch(); fb_scatter_kernel<BITS><<<grid, FB_THREADS, s_smem, st>>>(s, off, dbase, n_tiles, ctr);
+  SMX_LAUNCH_CHECK();
+  cudaFreeAsync(tcnt, st);
+  cudaFreeAsync(off, st);
+  cudaFreeAsync(csum, st);
+  cudaFreeAsync(dbase, st);
+  cudaFreeAsync(ctr, st);
+  return 0;
+}
+
+}  // namespace
+
+// Pass A for one deferred fixed-indegree call (see the file comment): draws
+// integers(0, ex, size=n_out) from the start of stream (k0, k1); record j
+// has source key = pieces(value) (key_mode 3: key_tab is a HOST array
+// {n, start[n], delta[n]}) or key_tab[value] (key_mode 1: device table) and
+// target index j / kdiv.  rstart / rcap / fill_in / fill_out (device, 2^lo_bits
+// entries) describe the digit regions; *total_out receives the accepted draws
+// in the raw window (< n_out: the window was short, rebuild), *overflow is
+// set when a region is too small.
+extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_out, int key_mode,
+                             const uint32_t* key_tab, uint32_t kdiv, uint32_t tag, int lo_bits, int pbits,
+                             uint32_t* region, const uint64_t* rstart, const uint64_t* rcap, const uint64_t* fill_in,
+                             uint64_t* fill_out, uint64_t* total_out, int* overflow, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_out == 0) {
+    SMX_CUDA_CHECK(cudaMemcpyAsync(fill_out, fill_in, sizeof(uint64_t) << lo_bits, cudaMemcpyDeviceToDevice, st));
+    SMX_CUDA_CHECK(cudaMemsetAsync(total_out, 0, sizeof(uint64_t), st));
+    return 0;
+  }
+  if (ex < 2 || ex > (1ULL << 32) || kdiv == 0 || lo_bits < 0 || lo_bits > 9 || (key_mode != 1 && key_mode != 3)) {
+    smx_set_error("smx_fused_gen: unsupported call (ex %llu, k %u, lo_bits %d, key mode %d)",
+                  (unsigned long long)ex, kdiv, lo_bits, key_mode);
+    return -1;
+  }
+  FusedGen g{};
+  g.key = Key{k0, k1};
+  g.lm.ex = (uint32_t)(ex & 0xffffffffULL);
+  g.lm.threshold = ex == (1ULL << 32) ? 0u : (uint32_t)(((1ULL << 32) - ex) % ex);
+  const double prej = (double)g.lm.threshold / 4294967296.0;
+  g.n_raw = n_out + (uint64_t)std::ceil(n_out * prej * 1.25 + 12.0 * std::sqrt(n_out * prej + 1.0) + 64.0);
+  g.n_out = n_out;
+  if (key_mode == 3) {
+    const uint32_t np = key_tab ? key_tab[0] : 0;
+    if (np < 1 || np > FG_MAXP) {
+      smx_set_error("smx_fused_gen: %u key pieces (1..%d supported)", np, FG_MAXP);
+      return -1;
+    }
+    g.np = np;
+    for (uint32_t i = 0; i < FG_MAXP; ++i) {
+      g.pstart[i] = i < np ? key_tab[1 + i] : 0xffffffffu;
+      g.pdelta[i] = i < np ? key_tab[1 + np + i] : 0u;
+    }
+  } else {
+    g.key_tab = key_tab;
+  }
+  g.kdiv = kdiv;
+  g.kd = FastDiv::make(kdiv);
+  g.wide_j = n_out > 0xffffffffULL;
+  g.tag = tag;
+  g.pbits = pbits;
+  g.region = region;
+  g.rstart = rstart;
+  g.rcap = rcap;
+  g.fill_in = fill_in;
+  g.fill_out = fill_out;
+  g.total = total_out;
+  g.overflow = overflow;
+  const uint64_t n_tiles = (g.n_raw + FG_TILE - 1) / FG_TILE;
+  if (n_tiles >= 0xffffffffull) {
+    smx_set_error("smx_fused_gen: %llu raw positions exceed the tile range", (unsigned long long)g.n_raw);
+    return -1;
+  }
+  const size_t B = (size_t)1 << lo_bits;
+  uint32_t* ws = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&ws, sizeof(uint32_t) * (n_tiles * B + 1), st));
+  SMX_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (n_tiles * B + 1), st));
+  g.status = ws;
+  g.ticket = ws + n_tiles * B;
+  const int rc = key_mode == 3 ? fg_dispatch<3>(lo_bits, g, (uint32_t)n_tiles, st)
+                               : fg_dispatch<1>(lo_bits, g, (uint32_t)n_tiles, st);
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
+// Pass B: stable sort of the digit regions by the high digit.  Region r
+// (r < 2^lo_bits) holds fill[r] records from slot rstart[r] (device arrays);
+// rcap_host (host, the regions' capacities) fixes the tile layout.  Writes
+// out[] (payloads sorted by key = hi << lo_bits | r) and counts[key] (zeroed
+// first).  err receives 6 for a key >= n_keys.
+extern "C" int smx_fused_sort(const uint32_t* region, const uint64_t* rstart, const uint64_t* fill,
+                              const uint64_t* rcap_host, int lo_bits, int hi_bits, int pbits, int tidx_bits,
+                              const uint64_t* pay_tabs, uint32_t* counts, uint64_t n_keys, uint32_t* out, int* err,
+                              void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  SMX_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * n_keys, st));
+  if (hi_bits < 8 || hi_bits > 11) {
+    smx_set_error("smx_fused_sort: high digit of %d bits (8..11 supported)", hi_bits);
+    return -1;
+  }
+  const uint32_t R = 1u << lo_bits;
+  std::vector<uint32_t> firsts(2 * (R + 1));
+  uint32_t* tile_first = firsts.data();
+  uint32_t* chunk_first = firsts.data() + R + 1;
+  uint64_t nt = 0, nc = 0;
+  for (uint32_t r = 0; r < R; ++r) {
+    tile_first[r] = (uint32_t)nt;
+    chunk_first[r] = (uint32_t)nc;
+    const uint64_t t = (rcap_host[r] + FB_TILE - 1) / FB_TILE;
+    nt += t;
+    nc += (t + FB_TC - 1) / FB_TC;
+  }
+  tile_first[R] = (uint32_t)nt;
+  chunk_first[R] = (uint32_t)nc;
+  if (nt >= 0xffffffffull) {
+    smx_set_error("smx_fused_sort: too many tiles");
+    return -1;
+  }
+  uint32_t* dfirst = nullptr;
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&dfirst, sizeof(uint32_t) * firsts.size(), st));
+  SMX_CUDA_CHECK(cudaMemcpyAsync(dfirst, firsts.data(), sizeof(uint32_t) * firsts.size(), cudaMemcpyHostToDevice, st));
+  FusedSort s{};
+  s.region = region;
+  s.rstart = rstart;
+  s.fill = fill;
+  s.tile_first = dfirst;
+  s.chunk_first = dfirst + R + 1;
+  s.n_regions = R;
+  s.pbits = pbits;
+  s.tidx_bits = tidx_bits;
+  s.lo_bits = lo_bits;
+  s.pay_tabs = pay_tabs;
+  s.counts = counts;
+  s.n_keys = n_keys;
+  s.out = out;
+  s.err = err;
+  int rc = 0;
+  switch (hi_bits) {
+    case 8: rc = fb_run<8>(s, (uint32_t)nt, (uint32_t)nc, st); break;
+    case 9: rc = fb_run<9>(s, (uint32_t)nt, (uint32_t)nc, st); break;
+    case 10: rc = fb_run<10>(s, (uint32_t)nt, (uint32_t)nc, st); break;
+    default: rc = fb_run<11>(s, (uint32_t)nt, (uint32_t)nc, st); break;
+  }
+  cudaFreeAsync(dfirst, st);
+  return rc;
+}

@@ -20,6 +20,7 @@ Construction and preparation never communicate (check_construction_silent).
 from __future__ import annotations
 
 import math
+import os
 import time
 from contextlib import contextmanager
 from dataclasses import asdict, dataclass, field
@@ -273,6 +274,13 @@ class _Rank:
         self.used_classes: set[int] = set()
         self.mem: RankMemory | None = None   # modeled-byte arenas (memory.py)
         self.prepared = False
+        # fixed-in-degree draws whose generation is deferred to prepare, where
+        # it runs fused with the first sort pass (csrc/fused.cu); any other
+        # record-producing call first generates them into the pending
+        # buffers, in call order (fused_ok then stays False)
+        self.deferred: list[dict] = []
+        self.fused_ok = True
+        self.fused = None
 
     @property
     def stream(self):
@@ -364,6 +372,7 @@ class Cluster:
         self.any_p2p = False
         self.min_remote_delay = None
         self.use_graphs = True
+        self.fused_enabled = self.FUSED_ENABLED   # fused generation + sort (tests switch it off for A/B)
         self._graph = None
         self._xgraph_ok = None   # exchange captured in the block graph (None: not tried yet)
         self._pg = None
@@ -639,10 +648,18 @@ class Cluster:
         Returns the record count.  sm/construction.py:410-432 + 530-534."""
         n_src, n_tgt = len(sources), len(targets)
         cls = self._syn_class(st, syn, port)
+        rule = conn.rule
+        if (rule == "fixed_indegree" and conn.allow_multapses and tmp_base is None and pos_bits is None
+                and not autapse_fix and self._defer_ok(st, cls, n_src, int(conn.k_in) * n_tgt)):
+            # local fixed in-degree draws: generated at prepare, fused with the sort
+            src, tgt, key_tab, pay_tab = self._tables(st, sources, targets, cls, None)
+            self._defer(st, aligned_key, n_src, int(conn.k_in) * n_tgt, 1, key_tab, pay_tab, int(conn.k_in),
+                        n_tgt, src_host=np.asarray(sources, dtype=np.int64))
+            return int(conn.k_in) * n_tgt, src
+        self._fused_off(st)
         if cls is None:
             self._make_wide(st)
         src, tgt, key_tab, pay_tab = self._tables(st, sources, targets, 0 if cls is None else cls, tmp_base)
-        rule = conn.rule
         if rule in ("one_to_one", "assigned"):
             n = n_src
         elif rule == "all_to_all":
@@ -696,6 +713,13 @@ class Cluster:
             self._write_syn(st, syn, port, base, n, syn_key)
         st.commit_records(n)
         return n, src
+
+    def _defer(self, st: _Rank, key, ex, n, kmode, ktab, pay_tab, kdiv, n_tgt, src_host=None, acct=None):
+        lm_thr = 0 if ex == (1 << 32) else ((1 << 32) - ex) % ex
+        st.deferred.append(dict(key=key, ex=int(ex), n=int(n), kmode=kmode, ktab=ktab, pay_tab=pay_tab,
+                                kdiv=int(kdiv), n_tgt=int(n_tgt), src_host=src_host, acct=acct,
+                                prej=lm_thr / 4294967296.0))
+        return st.deferred[-1]
 
     def _validate_conn(self, rank, sources, targets, conn, syn, what="connect"):
         sources = np.asarray(sources, dtype=np.int64)
@@ -1160,12 +1184,21 @@ class Cluster:
                 keys0 = np.where(rks == tr, nds, TMP_KEY | (lut_base + np.asarray(vbase, np.int64)[rks] + nds))
                 pieces = self._pack_pieces(starts, keys0)
         cls = self._syn_class(st, syn, port)
+        defer = multi and pieces is not None and not tmp_keys and self._defer_ok(st, cls, total, n)
+        if not defer:
+            self._fused_off(st)
         if cls is None:
             self._make_wide(st)
         tgt = _up_index(tg, dev)
         pay_tab = torch.empty(len(tg), dtype=torch.int32, device=dev)
         call("smx_pay_table", _ptr(tgt), len(tg), _ptr(st.node2row.t), st.node2row.n,
              0 if cls is None else cls, _ptr(pay_tab), sk)
+        if defer:
+            # generated at prepare, fused with the sort's first pass
+            d = self._defer(st, key, total, n, 3, pieces, pay_tab, k_in, len(tg))
+            self._dist_accounting(st, tr, group, n, 0, present, runs, pieces, False, lut_base, vbase, seg_words,
+                                  deferred=d)
+            return vbits, present
         base = st.reserve_records(n)
         vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
         cur = np.zeros(1, dtype=np.uint64)
@@ -1261,7 +1294,7 @@ class Cluster:
         st.w_meta.t[base: base + n][order] = tmp_m[:n]
 
     def _dist_accounting(self, st, tr, group, n, base, present, runs, pieces, tmp_keys, lut_base, vbase,
-                         seg_words):
+                         seg_words, deferred=None):
         """Modeled bytes of one distributed call on its target rank: the
         reference appends one batch per source rank present, ascending, the
         remote ones through remote_connect (sm/construction.py:689-703)."""
@@ -1292,6 +1325,12 @@ class Cluster:
                 his.append(TMP_KEY | (lut_base + (sw0 + snw) * 32))
                 owner.append(r)
         rng = np.array([len(los)] + los + his, dtype=np.uint64).astype(np.uint32)
+        if deferred is not None:  # counted once the records exist (prepare)
+            cnt = torch.zeros(len(los), dtype=torch.int64, device=st.device)
+            deferred["acct"] = (rng, cnt)
+            sizes = torch.stack([_popcount_dev(st.maps[(int(group), r)].present.view()) for r in remote])
+            st.mem.later("dist_batches", tr, int(group), list(present), owner, cnt, sizes)
+            return
         main = torch.cuda.current_stream(st.device)
         side = _prep_stream(st.device)
         side.wait_stream(main)
@@ -1467,15 +1506,68 @@ class Cluster:
 
     def _prepare_rank(self, st: _Rank):
         dev, sk = st.device, st.stream
-        dt = self.cfg.resolution_ms
         n_nodes = st.n_nodes
         st.L = max(2, st.max_delay + 1)
         st.P = 1 + st.max_port
+        if n_nodes >= (1 << 31):
+            raise ValueError("more than 2^31 nodes on one rank")
+        main = torch.cuda.current_stream(dev)
+        pre_sort = torch.cuda.Event()
+        pre_sort.record(main)  # maps / mirrors / rosters written so far
         # sort the store first (sm/core.py:299-324): it is the long kernel
         # sequence, and everything below up to the first_index check is host
         # work or independent small kernels that overlap it on a side stream
+        plan = self._fused_plan(st) if st.deferred and st.fused_ok else None
+        if st.deferred and st.fused_ok and plan is None:
+            self._fused_off(st)   # not representable in packed records: general path
+        if plan is not None:
+            self._fused_run(st, plan)
+            sorted_state = None
+        else:
+            sorted_state = self._sort_pending(st)
+        side = _prep_stream(dev)
+        side.wait_event(pre_sort)  # not on the sort itself: the side work overlaps it
+        with torch.cuda.stream(side):
+            self._prepare_tables(st)
+        main.wait_stream(side)
+        _record_stream(st.__dict__, main)  # side-stream allocations are used on main
+        check(_lib.lib().smx_check_device_errors(sk), "construction")  # asynchronous draws
+        if plan is not None and not self._fused_check(st):
+            # a digit region overflowed or a raw window was short (both ~never):
+            # regenerate every deferred call into the pending buffers and sort
+            self._fused_off(st)
+            sorted_state = self._sort_pending(st)
+        n = st.n_records
+        if n and int(st.first_index[-1].item()) != n:
+            raise ConsistencyError(f"record source beyond node count {n_nodes}")
+        # modeled bytes of construction + prepare (sm/construction.py:763-807);
+        # record counts of deferred calls exist only now
+        st.mem.resolve()
+        st.mem.prepare(st.N, st.P, st.L, st.n_nodes, {k: int(v.numel()) for k, v in st.H.items()}, st.rank,
+                       {k: int(v.numel()) for k, v in st.S.items()})
+        # record lists are dropped only after the sort has consumed them
+        del sorted_state
+        st.keys = st.vals = None
+        st.w_rows = st.w_w = st.w_meta = None
+        st.lut = None
+        st.fused = None
+        st.deferred = []
+        fi = st.first_index
+        max_len = int((fi[1:] - fi[:-1]).max().item()) if st.n_nodes else 0
+        max_chunks = max(1, -(-max_len // 1024))
+        st.owner_cap = st.N * self.block * max_chunks + 16
+        st.owner = torch.zeros(st.owner_cap, dtype=torch.int32, device=dev)
+        st.prepared = True
+
+    def _sort_pending(self, st: _Rank):
+        """General path: stable LSD sort of the pending (key, value) records by
+        source (sm/core.py:299-324), per-source counts and first_index.
+        Returns the scratch that must outlive the asynchronous sort."""
+        dev, sk = st.device, st.stream
+        n_nodes = st.n_nodes
         n = st.keys.n
         st.n_records = n
+        st.store_path = "general"
         key_bits = max(1, int(n_nodes - 1).bit_length())
         st.counts = torch.empty(max(n_nodes, 1), dtype=torch.int32, device=dev)
         # scratch pair in one allocation: the sort's intermediate passes use it
@@ -1483,15 +1575,9 @@ class Cluster:
         scratch = torch.empty(2 * max(n, 1), dtype=torch.int32, device=dev)
         kb, vb = scratch[: max(n, 1)], scratch[max(n, 1):]
         which = np.zeros(1, dtype=np.int32)
-        lut = st.lut.t
-        if n and n_nodes >= (1 << 31):
-            raise ValueError("more than 2^31 nodes on one rank")
         ev0 = self._event(st) if self.prof is not None else None
-        main = torch.cuda.current_stream(dev)
-        pre_sort = torch.cuda.Event()
-        pre_sort.record(main)  # maps / mirrors / rosters written so far
         call("smx_sort_records", _ptr(st.keys.t), _ptr(st.vals.t), _ptr(kb), _ptr(vb), n, key_bits,
-             1 if st.wide else 0, _ptr(lut), _ptr(st.counts), n_nodes, which.ctypes.data, sk)
+             1 if st.wide else 0, _ptr(st.lut.t), _ptr(st.counts), n_nodes, which.ctypes.data, sk)
         sorted_vals = (vb if which[0] else st.vals.t)[:n]
         if self.prof is not None:
             self.prof["sort"].append((ev0, self._event(st)))
@@ -1506,26 +1592,179 @@ class Cluster:
         else:
             st.payload = sorted_vals if n else torch.empty(1, dtype=torch.int32, device=dev)
             st.ww = st.wm = None
-        side = _prep_stream(dev)
-        side.wait_event(pre_sort)  # not on the sort itself: the side work overlaps it
-        with torch.cuda.stream(side):
-            self._prepare_tables(st)
-        main.wait_stream(side)
-        _record_stream(st.__dict__, main)  # side-stream allocations are used on main
-        check(_lib.lib().smx_check_device_errors(sk), "construction")  # asynchronous draws
-        if n and int(st.first_index[-1].item()) != n:
-            raise ConsistencyError(f"record source beyond node count {n_nodes}")
-        # record lists are dropped only after the sort has consumed them
-        del kb, vb, scratch, sorted_vals
-        st.keys = st.vals = None
-        st.w_rows = st.w_w = st.w_meta = None
-        st.lut = None
-        fi = st.first_index
-        max_len = int((fi[1:] - fi[:-1]).max().item()) if st.n_nodes else 0
-        max_chunks = max(1, -(-max_len // 1024))
-        st.owner_cap = st.N * self.block * max_chunks + 16
-        st.owner = torch.zeros(st.owner_cap, dtype=torch.int32, device=dev)
-        st.prepared = True
+        return (scratch, st.keys, st.vals, st.lut)
+
+    # ------------------------------------------------- fused generation + sort
+    FUSED_ENABLED = os.environ.get("SMX_FUSED", "1") != "0"
+
+    def _defer_ok(self, st: _Rank, cls, ex: int, n: int) -> bool:
+        return (self.fused_enabled and st.fused_ok and cls is not None and not st.wide and ex >= 2 and n > 0
+                and ex <= (1 << 32))
+
+    def _fused_off(self, st: _Rank):
+        """Leave the fused path for good: the deferred calls are generated into
+        the pending buffers (same draws, call order) by the general path."""
+        if not st.fused_ok:
+            return
+        st.fused_ok = False
+        for d in st.deferred:
+            self._gen_deferred(st, d)
+        st.deferred = []
+
+    def _gen_deferred(self, st: _Rank, d: dict):
+        n = d["n"]
+        base = st.reserve_records(n)
+        keys, vals = st.keys.t[base:], st.vals.t[base:]
+        sk = st.stream
+        ev0 = self._event(st) if self.prof is not None else None
+        ktab = d["ktab"].ctypes.data if d["kmode"] == 3 else _ptr(d["ktab"])
+        call("smx_gen_draw", d["key"][0], d["key"][1], 0, d["ex"], n, d["kmode"], 2, ktab, _ptr(d["pay_tab"]),
+             d["kdiv"], _ptr(keys), _ptr(vals), 0, 0, 0, 0, 0, 0, 0, sk)
+        if self.prof is not None:
+            self.prof["gen"].append((ev0, self._event(st)))
+        st.commit_records(n)
+        if d["acct"] is not None:  # records per source rank (modeled bytes), as _dist_accounting does
+            rng, cnt = d["acct"]
+            main = torch.cuda.current_stream(st.device)
+            side = _prep_stream(st.device)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                call("smx_count_ranges", _ptr(keys), n, rng.ctypes.data, _ptr(cnt), side.cuda_stream)
+
+    @staticmethod
+    def _call_key_ranges(d: dict) -> list:
+        """Key intervals [a, b) a deferred call's draws can produce."""
+        if d["kmode"] == 1:
+            s = d["src_host"]
+            return [(int(s.min()), int(s.max()) + 1)]
+        pc = d["ktab"]
+        m = int(pc[0])
+        starts = [int(x) for x in pc[1: 1 + m]] + [d["ex"]]
+        return [((starts[i] + int(pc[1 + m + i])) & 0xFFFFFFFF,
+                 ((starts[i] + int(pc[1 + m + i])) & 0xFFFFFFFF) + starts[i + 1] - starts[i]) for i in range(m)
+                if starts[i + 1] > starts[i]]
+
+    @staticmethod
+    def _digit_probs(d: dict, B: int) -> np.ndarray:
+        """Probability of each low key digit (key mod B) for one draw of a
+        deferred call: uniform positions mapped to keys (exact)."""
+        cnt = np.zeros(B, dtype=np.float64)
+        if d["kmode"] == 1:
+            cnt += np.bincount(np.asarray(d["src_host"], dtype=np.int64) & (B - 1), minlength=B)
+        else:
+            for a, b in Cluster._call_key_ranges(d):
+                ln = b - a
+                cnt += ln // B
+                rem = ln % B
+                if rem:
+                    np.add.at(cnt, (a + np.arange(rem)) & (B - 1), 1.0)
+        return cnt / float(d["ex"])
+
+    def _fused_plan(self, st: _Rank):
+        """Digit split and region capacities of the fused path, or None when
+        the records do not fit the packed format (general path)."""
+        calls = st.deferred
+        key_bits = max(1, int(st.n_nodes - 1).bit_length())
+        env_lo = os.environ.get("SMX_FUSED_LO")
+        if env_lo is not None:
+            lo = int(env_lo)
+        else:
+            lo = 0 if key_bits <= 11 else max(key_bits - 11, min(9, key_bits - 8))
+        hi = max(8, key_bits - lo)
+        if lo > 9 or hi > 11:
+            return None
+        tidx_bits = max(1, int(max(d["n_tgt"] for d in calls) - 1).bit_length())
+        seg_bits = int(len(calls) - 1).bit_length()
+        pbits = seg_bits + tidx_bits
+        if hi + pbits > 31:
+            return None
+        # record counts per source rank of distributed calls (modeled bytes)
+        # come from the per-key counts: every accounted call's keys must be
+        # its own
+        acct = [i for i, d in enumerate(calls) if d["acct"] is not None]
+        if acct:
+            rngs = [self._call_key_ranges(d) for d in calls]
+            for i in acct:
+                for j, rj in enumerate(rngs):
+                    if j != i and any(a < y and x < b for a, b in rngs[i] for x, y in rj):
+                        return None
+        B = 1 << lo
+        exp = np.zeros(B)
+        var = np.zeros(B)
+        for d in calls:
+            p = self._digit_probs(d, B)
+            n = float(d["n"])
+            # the raw window's slack (accepted draws past the last record)
+            # lands in the regions too
+            slack = 1.25 * n * d["prej"] + 12.0 * math.sqrt(n * d["prej"] + 1.0) + 64.0
+            if (n + slack) * float(p.max()) * 1.05 + 1e4 >= (1 << 30):
+                return None   # look-back descriptors hold 30-bit counts
+            exp += (n + slack) * p
+            var += n * p * (1.0 - p)
+        cap = np.ceil(exp + 8.0 * np.sqrt(var) + 64.0).astype(np.int64)
+        cap = (cap + 31) // 32 * 32
+        return dict(lo=lo, hi=hi, pbits=pbits, tidx_bits=tidx_bits, cap=cap.astype(np.uint64))
+
+    def _fused_run(self, st: _Rank, plan: dict):
+        """Pass A per deferred call into the digit regions, then pass B (csrc/fused.cu)."""
+        dev, sk = st.device, st.stream
+        calls = st.deferred
+        lo, B = plan["lo"], 1 << plan["lo"]
+        cap = plan["cap"]
+        rstart = np.zeros(B, dtype=np.int64)
+        rstart[1:] = np.cumsum(cap.astype(np.int64))[:-1]
+        slots = int(rstart[-1] + cap[-1])
+        n = sum(d["n"] for d in calls)
+        st.n_records = n
+        region = torch.empty(max(slots, 1), dtype=torch.int32, device=dev)
+        meta = _up(np.concatenate([rstart, cap.astype(np.int64)]), dev)
+        rs_t, rc_t = meta[:B], meta[B:]
+        fills = torch.zeros((2, B), dtype=torch.int64, device=dev)
+        flags = torch.zeros(2 + len(calls), dtype=torch.int64, device=dev)   # overflow, err, totals
+        ev0 = self._event(st) if self.prof is not None else None
+        for i, d in enumerate(calls):
+            ktab = d["ktab"].ctypes.data if d["kmode"] == 3 else _ptr(d["ktab"])
+            call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"],
+                 i << plan["tidx_bits"], lo, plan["pbits"], _ptr(region), _ptr(rs_t), _ptr(rc_t),
+                 _ptr(fills[i % 2]), _ptr(fills[(i + 1) % 2]), _ptr(flags[2 + i:]), _ptr(flags), sk)
+        if self.prof is not None:
+            self.prof["gen"].append((ev0, self._event(st)))
+            ev0 = self._event(st)
+        pay_tabs = _up(np.array([d["pay_tab"].data_ptr() for d in calls], dtype=np.int64), dev)
+        st.counts = torch.empty(max(st.n_nodes, 1), dtype=torch.int32, device=dev)
+        st.payload = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        call("smx_fused_sort", _ptr(region), _ptr(rs_t), _ptr(fills[len(calls) % 2]), cap.ctypes.data, lo,
+             plan["hi"], plan["pbits"], plan["tidx_bits"], _ptr(pay_tabs), _ptr(st.counts), st.n_nodes,
+             _ptr(st.payload), _ptr(flags[1:]), sk)
+        st.first_index = torch.empty(st.n_nodes + 1, dtype=torch.int64, device=dev)
+        call("smx_counts_to_offsets", _ptr(st.counts), st.n_nodes, _ptr(st.first_index), sk)
+        if self.prof is not None:
+            self.prof["sort"].append((ev0, self._event(st)))
+        st.ww = st.wm = None
+        # records per source rank of accounted distributed calls: sums of the
+        # per-key counts over the call's key ranges (keys are the call's own)
+        cs = None
+        for d in calls:
+            if d["acct"] is None:
+                continue
+            if cs is None:
+                cs = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), torch.cumsum(st.counts.long(), 0)])
+            rng, cnt = d["acct"]
+            m = int(rng[0])
+            los = torch.from_numpy(rng[1: 1 + m].astype(np.int64)).to(dev)
+            his = torch.from_numpy(rng[1 + m: 1 + 2 * m].astype(np.int64)).to(dev)
+            los = los.clamp(max=st.n_nodes)
+            his = his.clamp(max=st.n_nodes)
+            cnt.copy_(cs[his] - cs[los])
+        st.store_path = "fused"
+        st.fused = dict(region=region, meta=meta, fills=fills, flags=flags, pay_tabs=pay_tabs,
+                        want=np.array([d["n"] for d in calls], dtype=np.int64))
+
+    def _fused_check(self, st: _Rank) -> bool:
+        f = st.fused["flags"].cpu().numpy()
+        if int(f[1]):
+            raise ConsistencyError(f"fused sort: device error {int(f[1])}")
+        return not int(f[0]) and bool((f[2:] >= st.fused["want"]).all())
 
     def _prepare_tables(self, st: _Rank):
         """Everything of prepare that does not read the sorted store: neuron
@@ -1584,10 +1823,6 @@ class Cluster:
         st.TP = self._routes(st, [(tr, st.mirrors[tr].t) for tr in sorted(st.mirrors)])
         own = [(self.group_slots[g], st.rosters[(g, sr)].t) for (g, sr) in sorted(st.rosters) if sr == st.rank]
         st.GQ = self._routes(st, own)
-        # modeled bytes of prepare (sm/construction.py:763-807)
-        st.mem.resolve()
-        st.mem.prepare(st.N, st.P, st.L, st.n_nodes, {k: int(v.numel()) for k, v in st.H.items()}, st.rank,
-                       {k: int(v.numel()) for k, v in st.S.items()})
         # propagation buffers
         self._alloc_propagation(st)
 

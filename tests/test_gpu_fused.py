@@ -1,0 +1,124 @@
+"""The fused generation + sort path (csrc/fused.cu) against the general
+path (smx_gen_draw + smx_sort_records, itself pinned to the reference's
+goldens): identical tables for every digit split, several calls, both key
+modes, rejections, and the overflow fallback."""
+import numpy as np
+import pytest
+
+import scenarios
+import tables
+from namespaces import gpu_ns
+
+pytestmark = pytest.mark.gpu
+
+
+def _build(fused, fn, monkeypatch=None, lo=None):
+    if lo is not None:
+        monkeypatch.setenv("SMX_FUSED_LO", str(lo))
+    ns = gpu_ns()
+    make = ns.make_cluster
+
+    def mk(cfg):
+        c = make(cfg)
+        c.fused_enabled = fused
+        return c
+    ns.make_cluster = mk
+    c = fn(ns)
+    c.prepare()
+    return c
+
+
+def _balanced(n_ranks, mode, per_rank, k_exc, k_inh, seed=7):
+    def fn(ns):
+        c, _ = scenarios.balanced(ns, n_ranks, mode, per_rank, k_exc, k_inh, seed)
+        return c
+    return fn
+
+
+def _local_mix(ns):
+    """Local fixed in-degree calls with key tables (scattered sources), a
+    distributed call, overlapping populations and two classes."""
+    c = ns.make_cluster(ns.SimConfig(n_ranks=1, seed=19))
+    a = c.create_neurons(0, 3000, ns.LifParams(), -60.0)
+    b = c.create_neurons(0, 1000, ns.LifParams(), -61.0)
+    A, Bn = np.arange(a.start, a.stop), np.arange(b.start, b.stop)
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    rng = np.random.default_rng(3)
+    c.connect(0, A, Bn, S("fixed_indegree", k_in=40), Sy(0.25, 3))
+    c.connect(0, rng.permutation(A)[:777], A, S("fixed_indegree", k_in=9), Sy(-0.5, 4))
+    c.connect(0, Bn, A, S("fixed_indegree", k_in=13), Sy(0.25, 3))
+    c.connect_fixed_indegree_distributed([(0, Bn), (0, A[:500])], [(0, A)], 11, Sy(0.125, 2))
+    return c
+
+
+CASES = {
+    "balanced_1r": _balanced(1, "p2p", 3000, 240, 60),
+    "balanced_4r_coll": _balanced(4, "collective", 700, 80, 20),
+    "balanced_3r_p2p": _balanced(3, "p2p", 900, 100, 25),
+    "local_mix": _local_mix,
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_fused_equals_general(name):
+    g = _build(False, CASES[name])
+    f = _build(True, CASES[name])
+    assert all(st.store_path == "general" for st in g.ranks.values())
+    assert all(st.store_path == "fused" for st in f.ranks.values()), [st.store_path for st in f.ranks.values()]
+    bad = tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))
+    assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("lo", [0, 3, 6, 7, 8, 9])
+def test_fused_digit_splits(lo, monkeypatch):
+    """Every low-digit width of pass A (the high digit takes the rest)."""
+    g = _build(False, CASES["local_mix"])
+    f = _build(True, CASES["local_mix"], monkeypatch, lo)
+    assert all(st.store_path == "fused" for st in f.ranks.values())
+    assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))
+
+
+def test_fused_with_rejections():
+    """A source range whose Lemire threshold rejects draws (ex = 300,000:
+    p = 3.9e-5 per draw): the look-back carries the accept counts."""
+    def fn(ns):
+        c = ns.make_cluster(ns.SimConfig(n_ranks=1, seed=23))
+        a = c.create_neurons(0, 300_000, ns.LifParams(), -60.0)
+        A = np.arange(a.start, a.stop)
+        c.connect(0, A, A[:40_000], ns.ConnSpec("fixed_indegree", k_in=60), ns.SynSpec(0.25, 3))
+        return c
+    g, f = _build(False, fn), _build(True, fn)
+    assert f.ranks[0].store_path == "fused"
+    assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))
+
+
+def test_fused_overflow_falls_back(monkeypatch):
+    """Regions too small for the draws: the overflow flag sends the rank
+    through the general path, with identical tables."""
+    from paper_2512_09502_b200.engine import Cluster
+    real = Cluster._fused_plan
+
+    def tiny(self, st):
+        p = real(self, st)
+        if p is not None:
+            p["cap"] = (p["cap"] // 3 // 32 * 32).astype(np.uint64)
+        return p
+    g = _build(False, CASES["balanced_1r"])
+    monkeypatch.setattr(Cluster, "_fused_plan", tiny)
+    f = _build(True, CASES["balanced_1r"])
+    assert f.ranks[0].store_path == "general"
+    assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))
+
+
+def test_fused_then_general_call_flushes_in_order():
+    """A deferred call followed by a call the fused path cannot take (random
+    weights): the deferred draws are generated first, in call order."""
+    def fn(ns):
+        c = ns.make_cluster(ns.SimConfig(n_ranks=1, seed=29))
+        a = c.create_neurons(0, 500, ns.LifParams(), -60.0)
+        A = np.arange(a.start, a.stop)
+        c.connect(0, A, A, ns.ConnSpec("fixed_indegree", k_in=20), ns.SynSpec(0.25, 3))
+        c.connect(0, A, A, ns.ConnSpec("fixed_indegree", k_in=5), ns.SynSpec(("normal", 0.5, 0.1), 2))
+        return c
+    g, f = _build(False, fn), _build(True, fn)
+    assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))

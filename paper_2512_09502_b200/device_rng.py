@@ -71,3 +71,20 @@ class PoissonStream:
     @property
     def word_cursor(self) -> int:
         return int(self.cursor[self.ping].item())
+
+
+def normal(key, loc: float, scale: float, n: int, device="cuda"):
+    """numpy Generator.normal(loc, scale, size=n) from the start of a stream
+    (ziggurat, variable words per sample); returns (values, words used)."""
+    L = _lib.lib()
+    dev = torch.device(device)
+    chunks = L.smx_normal_chunks_for(n)
+    ws = torch.empty(int(L.smx_poisson_workspace(chunks)), dtype=torch.uint8, device=dev)
+    cur = torch.zeros(2, dtype=torch.int64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    call("smx_normal_fill", key[0], key[1], cur.data_ptr(), float(loc), float(scale), n, chunks, ws.data_ptr(),
+         out.data_ptr(), cur[1:].data_ptr(), err.data_ptr(), _stream(dev))
+    if int(err.item()):
+        raise RuntimeError(f"normal chain error {int(err.item())}")
+    return out[:n], int(cur[1].item())

@@ -280,7 +280,7 @@ class _Rank:
         # buffers, in call order (fused_ok then stays False)
         self.deferred: list[dict] = []
         self.fused_ok = True
-        self.fused = None
+        self.fgen = None   # fused-path buffers between pass B and the prepare check
 
     @property
     def stream(self):
@@ -1550,7 +1550,7 @@ class Cluster:
         st.keys = st.vals = None
         st.w_rows = st.w_w = st.w_meta = None
         st.lut = None
-        st.fused = None
+        st.fgen = None
         st.deferred = []
         fi = st.first_index
         max_len = int((fi[1:] - fi[:-1]).max().item()) if st.n_nodes else 0
@@ -1757,14 +1757,14 @@ class Cluster:
             his = his.clamp(max=st.n_nodes)
             cnt.copy_(cs[his] - cs[los])
         st.store_path = "fused"
-        st.fused = dict(region=region, meta=meta, fills=fills, flags=flags, pay_tabs=pay_tabs,
+        st.fgen = dict(region=region, meta=meta, fills=fills, flags=flags, pay_tabs=pay_tabs,
                         want=np.array([d["n"] for d in calls], dtype=np.int64))
 
     def _fused_check(self, st: _Rank) -> bool:
-        f = st.fused["flags"].cpu().numpy()
+        f = st.fgen["flags"].cpu().numpy()
         if int(f[1]):
             raise ConsistencyError(f"fused sort: device error {int(f[1])}")
-        return not int(f[0]) and bool((f[2:] >= st.fused["want"]).all())
+        return not int(f[0]) and bool((f[2:] >= st.fgen["want"]).all())
 
     def _prepare_tables(self, st: _Rank):
         """Everything of prepare that does not read the sorted store: neuron

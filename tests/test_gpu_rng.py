@@ -138,3 +138,44 @@ def test_integers_draw_variants(env):
     r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_normal_slow_paths_at_scale(seed):
+    """1e7 ziggurat normals from one stream (~1.5e5 wedge/tail samples, the
+    branches that call exp / log1p) bit-exact against the oracle (glibc)."""
+    from oracle.rng import OracleStream
+    from paper_2512_09502_b200 import device_rng as dr
+    from paper_2512_09502_b200.api import stream_key
+    k = stream_key(seed, ("normal-scale", seed))
+    o = OracleStream(0, key=k)
+    want = o.normal(-58.0, 5.0, size=10_000_000)
+    got, used = dr.normal(k, -58.0, 5.0, 10_000_000)
+    got = got.cpu().numpy()
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+    assert used == o.words_used
+
+
+@pytest.mark.parametrize("lam", [12.5, 150.0])
+def test_ptrs_at_scale(lam):
+    """numpy's PTRS sampler (lam >= 10, CUDA log in the squeeze test):
+    1e7 samples bit-exact against the oracle."""
+    from oracle.rng import OracleStream
+    from paper_2512_09502_b200 import device_rng as dr
+    from paper_2512_09502_b200.api import stream_key
+    k = stream_key(8, ("ptrs-scale", int(lam)))
+    o = OracleStream(0, key=k)
+    ps = dr.PoissonStream(k, lam)
+    assert np.array_equal(ps.draw(10_000_000).cpu().numpy().astype(np.int64), o.poisson(lam, size=10_000_000))
+    assert ps.word_cursor == o.words_used
+
+
+def test_init_v_many_gids():
+    """Per-gid init-v streams (blake2b on the device) for 2e5 gids spread over
+    0 .. 4.1e6 (the C4 neuron count) against the oracle."""
+    from oracle.rng import OracleStream
+    from paper_2512_09502_b200 import device_rng as dr
+    gids = np.unique(np.random.default_rng(5).integers(0, 4_130_000, 200_000)).astype(np.int64)
+    want = np.array([OracleStream(12345, ("init-v", int(g))).normal(-58.0, 5.0) for g in gids])
+    got = dr.init_v(12345, gids, -58.0, 5.0).cpu().numpy()
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))

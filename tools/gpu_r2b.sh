@@ -4,7 +4,7 @@ O=gpurun_out/r2b
 mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu_fused.py -q -x -p no:cacheprovider > $O/pytest_fused.log 2>&1
 tail -5 $O/pytest_fused.log
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_memory.py tests/test_gpu_facade.py -q -x -p no:cacheprovider > $O/pytest_parity.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_rng.py tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_memory.py tests/test_gpu_facade.py -q -x -p no:cacheprovider > $O/pytest_parity.log 2>&1
 tail -5 $O/pytest_parity.log
 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/bench.json 2> $O/bench.err
 cat $O/bench.json; tail -3 $O/bench.err

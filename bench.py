@@ -52,6 +52,10 @@ def parse():
                     help="strong scaling: --neurons is the whole network, split over the GPUs")
     ap.add_argument("--cpu-sample-neurons", type=int, default=5_000)
     ap.add_argument("--cpu-sample-k-scale", type=float, default=0.1)
+    ap.add_argument("--workload", default="c3", choices=["c3", "c5"],
+                    help="c3: the headline (hpc_benchmark weak scaling); c5: construction-only sweep")
+    ap.add_argument("--c5-points", default="1e8,3e8,1e9,3e9,1e10")
+    ap.add_argument("--c5-rules", default="fixed_indegree,fixed_total")
     return ap.parse_args()
 
 
@@ -385,9 +389,98 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_c5(args):
+    """BASELINE configs[4]: construction-only sweep of
+    synapses per GPU for fixed_indegree (distributed rule, the fused path)
+    and fixed_total (local rule, general path).  N neurons per GPU fixed,
+    K or n_total scaled.  One JSON line per point; peak device memory from
+    the caching allocator (everything the construction holds at once)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_09502_b200 import api, engine
+
+    world, rank, local = dist_info()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    n = args.neurons
+    points = [int(float(x)) for x in args.c5_points.split(",")]
+    rules = args.c5_rules.split(",")
+
+    def build(rule, syn_per_gpu):
+        c = engine.Cluster(api.SimConfig(n_ranks=world, seed=args.seed), profile=True)
+        pops = [np.arange(c.create_neurons(r, n).start, n) for r in range(world)]
+        if rule == "fixed_indegree":
+            k = syn_per_gpu // n
+            c.connect_fixed_indegree_distributed([(r, pops[r]) for r in range(world)],
+                                                 [(r, pops[r]) for r in range(world)], k, api.SynSpec(0.125, 15))
+        else:
+            for r in range(world):
+                c.connect(r, pops[r], pops[r], api.ConnSpec("fixed_total", n_total=syn_per_gpu), api.SynSpec(0.125, 15))
+        c.prepare()
+        return c
+
+    for rule in rules:
+        for S in points:
+            if rule == "fixed_total" and S >= (1 << 32):
+                line = {"metric": "construction_synapses_per_s", "config": {"workload": f"C5_{rule}_{S:.0e}"},
+                        "skipped": "fixed_total runs through the general path (32-bit record index, ~20 B/synapse)"}
+                if rank == 0:
+                    print(json.dumps(line), flush=True)
+                continue
+            times, gen, srt = [], [], []
+            c = None
+            for i in range(args.warmup + args.steps):
+                del c
+                gc.collect()
+                torch.cuda.empty_cache()
+                torch.cuda.reset_peak_memory_stats(dev)
+                if world > 1:
+                    dist.barrier()
+                torch.cuda.synchronize(dev)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                c = build(rule, S)
+                e1.record()
+                torch.cuda.synchronize(dev)
+                if i >= args.warmup:
+                    t = e0.elapsed_time(e1)
+                    if world > 1:
+                        x = torch.tensor([t], dtype=torch.float64, device=dev)
+                        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+                        t = float(x.item())
+                    times.append(t)
+                    gen.append(c.kernel_ms("gen"))
+                    srt.append(c.kernel_ms("sort"))
+            peak = torch.cuda.max_memory_allocated(dev)
+            st = c.ranks[rank]
+            ok = int(st.first_index[-1].item()) == S
+            ms = float(np.mean(times))
+            line = {"metric": "construction_synapses_per_s", "value": world * S / (ms * 1e-3), "unit": "synapses/s",
+                    "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                    "higher_is_better": True, "scaling": "weak", "data": "synthetic",
+                    "config": {"workload": f"C5_{rule}_{S:.0e}", "rule": rule, "neurons_per_gpu": n,
+                               "synapses_per_gpu": S, "store_path": st.store_path},
+                    "phase_ms": {"gen": float(np.mean(gen)), "sort": float(np.mean(srt))},
+                    "peak_device_bytes": int(peak), "peak_bytes_per_synapse": peak / S, "records_ok": ok}
+            if rank == 0:
+                print(json.dumps(line), flush=True)
+            del c
+            gc.collect()
+            torch.cuda.empty_cache()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.workload == "c5":
+        run_c5(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

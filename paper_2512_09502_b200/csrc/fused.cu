@@ -211,13 +211,24 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     if (tid < B) {
       tstart[tid] = ts;
       if (t > 0) {
+        // walk back 4 descriptors per step (independent loads): a tile
+        // usually finds an inclusive prefix within the first few
         uint32_t e = 0;
         for (int64_t i = (int64_t)t - 1;;) {
-          const uint32_t w = ld_vol(g.status + (size_t)i * B + tid);
-          if (w == 0) continue;  // predecessor still drawing
-          e += w & ST_VAL;
-          if (w & ST_P) break;
-          --i;
+          uint32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) w[u] = i - u >= 0 ? ld_vol(g.status + (size_t)(i - u) * B + tid) : ST_P;
+          int used = 0;
+          bool done = false;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (done || used < u || w[u] == 0) continue;  // stop at a predecessor still drawing
+            e += w[u] & ST_VAL;
+            used = u + 1;
+            done = (w[u] & ST_P) != 0;
+          }
+          if (done) break;
+          i -= used;
         }
         excl = e;
         st_vol(g.status + (size_t)t * B + tid, ST_P | (e + c));
@@ -413,71 +424,98 @@ __global__ void __launch_bounds__(256) fb_chunk_sum_kernel(const __grid_constant
   }
 }
 
-// One CTA: per high digit, exclusive prefix over the chunks in (region,
-// chunk) order -- the stable order of the input -- in place; per-key
-// counts (key = d << lo_bits | region) from the per-region sums; digit bases.
+// rsum[r][d] = records of digit d in region r (sum over the region's
+// chunks); per-key counts (key = d << lo_bits | r) are these sums.
 template <int BITS>
-__global__ void __launch_bounds__(1024) fb_digit_scan_kernel(const __grid_constant__ FusedSort s, uint32_t* csum,
-                                                             uint64_t* dbase) {
+__global__ void __launch_bounds__(256) fb_region_sum_kernel(const __grid_constant__ FusedSort s, const uint32_t* csum,
+                                                            uint32_t* rsum) {
+  constexpr int BINS = 1 << BITS;
+  const uint32_t r = blockIdx.x;
+  const uint32_t c0 = s.chunk_first[r], c1 = s.chunk_first[r + 1];
+  for (int d = threadIdx.x; d < BINS; d += 256) {
+    uint32_t acc = 0;
+    for (uint32_t C = c0; C < c1; ++C) acc += csum[(size_t)C * BINS + d];
+    rsum[(size_t)r * BINS + d] = acc;
+    const uint64_t key = ((uint64_t)d << s.lo_bits) | r;
+    if (acc) {
+      if (key < s.n_keys) s.counts[key] = acc;
+      else atomicExch(s.err, 6);
+    }
+  }
+}
+
+// One CTA: per digit, exclusive scan over the regions (in place: rsum ->
+// region base within the digit) and the 64-bit digit bases.
+template <int BITS>
+__global__ void __launch_bounds__(1024) fb_region_scan_kernel(const __grid_constant__ FusedSort s, uint32_t* rsum,
+                                                              uint64_t* dbase) {
   constexpr int BINS = 1 << BITS;
   constexpr int DPT = (BINS + 1023) / 1024;
   __shared__ unsigned long long ws[32];
   uint64_t tot[DPT];
 #pragma unroll
   for (int j = 0; j < DPT; ++j) {
-    const int d = threadIdx.x * DPT + j;
+    const int d = j * 1024 + threadIdx.x;
     uint64_t run = 0;
     if (d < BINS) {
+#pragma unroll 8
       for (uint32_t r = 0; r < s.n_regions; ++r) {
-        const uint32_t c0 = s.chunk_first[r], c1 = s.chunk_first[r + 1];
-        // region r's records of digit d follow the earlier regions' (run)
-        uint32_t rsum = 0;
-#pragma unroll 4
-        for (uint32_t C = c0; C < c1; ++C) {
-          const uint32_t x = csum[(size_t)C * BINS + d];
-          csum[(size_t)C * BINS + d] = (uint32_t)run + rsum;
-          rsum += x;
-        }
-        if (run + rsum > 0xffffffffull) atomicExch(s.err, 7);  // within-digit offsets are 32-bit
-        const uint64_t key = ((uint64_t)d << s.lo_bits) | r;
-        if (rsum) {
-          if (key < s.n_keys) s.counts[key] = rsum;
-          else atomicExch(s.err, 6);
-        }
-        run += rsum;
+        const uint32_t x = rsum[(size_t)r * BINS + d];
+        rsum[(size_t)r * BINS + d] = (uint32_t)run;
+        run += x;
       }
+      if (run > 0xffffffffull) atomicExch(s.err, 7);  // within-digit offsets are 32-bit
     }
     tot[j] = run;
   }
-  // exclusive scan of the digit totals -> digit bases (64-bit)
   uint64_t mine = 0;
 #pragma unroll
   for (int j = 0; j < DPT; ++j) mine += tot[j];
+  // digit order is j * 1024 + tid: scan thread-major within each j slice
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t inc = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  if (lane == 31) ws[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    uint64_t v = ws[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += y;
-    }
-    ws[lane] = v;
-  }
-  __syncthreads();
-  uint64_t base = (warp ? ws[warp - 1] : 0) + inc - mine;
+  uint64_t carry = 0;
 #pragma unroll
   for (int j = 0; j < DPT; ++j) {
-    const int d = threadIdx.x * DPT + j;
-    if (d < BINS) dbase[d] = base;
-    base += tot[j];
+    uint64_t inc = tot[j];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) ws[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t v = ws[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      ws[lane] = v;
+    }
+    __syncthreads();
+    const int d = j * 1024 + threadIdx.x;
+    if (d < BINS) dbase[d] = carry + (warp ? ws[warp - 1] : 0) + inc - tot[j];
+    carry += ws[31];
+    __syncthreads();
+  }
+  (void)mine;
+}
+
+// csum[C][d] = position of chunk C's first record of digit d within the digit
+template <int BITS>
+__global__ void __launch_bounds__(256) fb_chunk_base_kernel(const __grid_constant__ FusedSort s, uint32_t* csum,
+                                                            const uint32_t* rbase) {
+  constexpr int BINS = 1 << BITS;
+  const uint32_t r = blockIdx.x;
+  const uint32_t c0 = s.chunk_first[r], c1 = s.chunk_first[r + 1];
+  for (int d = threadIdx.x; d < BINS; d += 256) {
+    uint32_t run = rbase[(size_t)r * BINS + d];
+    for (uint32_t C = c0; C < c1; ++C) {
+      const uint32_t x = csum[(size_t)C * BINS + d];
+      csum[(size_t)C * BINS + d] = run;
+      run += x;
+    }
   }
 }
 
@@ -503,7 +541,10 @@ __global__ void __launch_bounds__(256) fb_tile_offsets_kernel(const __grid_const
 // a ticket so the tiles in flight write neighbouring parts of every digit's
 // output (partial sectors complete in L2).  Writes the final payload.
 template <int BITS>
-__global__ void __launch_bounds__(FB_THREADS, 2) fb_scatter_kernel(const __grid_constant__ FusedSort s,
+#ifndef SMX_FB_CTAS
+#define SMX_FB_CTAS 3
+#endif
+__global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(const __grid_constant__ FusedSort s,
                                                                    const uint32_t* off, const uint64_t* dbase,
                                                                    uint32_t n_tiles, uint32_t* tile_ctr) {
   constexpr int BINS = 1 << BITS;
@@ -627,12 +668,13 @@ template <int BITS>
 int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, cudaStream_t st) {
   constexpr int BINS = 1 << BITS;
   uint16_t* tcnt = nullptr;
-  uint32_t *off = nullptr, *csum = nullptr, *ctr = nullptr;
+  uint32_t *off = nullptr, *csum = nullptr, *ctr = nullptr, *rsum = nullptr;
   uint64_t* dbase = nullptr;
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&tcnt, sizeof(uint16_t) * (size_t)n_tiles * BINS, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&off, sizeof(uint32_t) * (size_t)n_tiles * BINS, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&csum, sizeof(uint32_t) * (size_t)std::max<uint32_t>(n_chunks, 1) * BINS, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&dbase, sizeof(uint64_t) * BINS, st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&rsum, sizeof(uint32_t) * (size_t)s.n_regions * BINS, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&ctr, sizeof(uint32_t), st));
   SMX_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
   const size_t h_smem = (size_t)32 * BINS * 4;
@@ -651,17 +693,20 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, cudaStream_t
   if (n_chunks) {
     smx_count_launch(); fb_chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum);
   }
-  smx_count_launch(); fb_digit_scan_kernel<BITS><<<1, 1024, 0, st>>>(s, csum, dbase);
+  smx_count_launch(); fb_region_sum_kernel<BITS><<<s.n_regions, 256, 0, st>>>(s, csum, rsum);
+  smx_count_launch(); fb_region_scan_kernel<BITS><<<1, 1024, 0, st>>>(s, rsum, dbase);
+  smx_count_launch(); fb_chunk_base_kernel<BITS><<<s.n_regions, 256, 0, st>>>(s, csum, rsum);
   if (n_chunks) {
     smx_count_launch(); fb_tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum, off);
   }
-  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(n_tiles, 148u * 2));
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(n_tiles, 148u * SMX_FB_CTAS));
   smx_count_launch(); fb_scatter_kernel<BITS><<<grid, FB_THREADS, s_smem, st>>>(s, off, dbase, n_tiles, ctr);
   SMX_LAUNCH_CHECK();
   cudaFreeAsync(tcnt, st);
   cudaFreeAsync(off, st);
   cudaFreeAsync(csum, st);
   cudaFreeAsync(dbase, st);
+  cudaFreeAsync(rsum, st);
   cudaFreeAsync(ctr, st);
   return 0;
 }

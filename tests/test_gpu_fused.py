@@ -69,11 +69,18 @@ def test_fused_equals_general(name):
     assert not bad, bad[:10]
 
 
-@pytest.mark.parametrize("lo", [0, 3, 6, 7, 8, 9])
-def test_fused_digit_splits(lo, monkeypatch):
-    """Every low-digit width of pass A (the high digit takes the rest)."""
-    g = _build(False, CASES["local_mix"])
-    f = _build(True, CASES["local_mix"], monkeypatch, lo)
+def _small(ns):
+    c, _ = scenarios.balanced(ns, 2, "collective", 500, 40, 10, 5)   # 11-bit keys: lo = 0 possible
+    return c
+
+
+@pytest.mark.parametrize("lo,case", [(0, "small"), (2, "small"), (1, "local_mix"), (3, "local_mix"),
+                                     (6, "local_mix"), (7, "local_mix"), (8, "local_mix"), (9, "local_mix")])
+def test_fused_digit_splits(lo, case, monkeypatch):
+    """Every low-digit width of pass A (the high digit takes the rest, 8..11 bits)."""
+    fn = _small if case == "small" else CASES["local_mix"]
+    g = _build(False, fn)
+    f = _build(True, fn, monkeypatch, lo)
     assert all(st.store_path == "fused" for st in f.ranks.values())
     assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))
 

@@ -85,17 +85,76 @@ struct SeqStream {
 };
 
 // ---------------------------------------------------------------------------
-// Ziggurat standard normal (numpy random_standard_normal), bit-exact on the
-// fast path (98.5% of first words).  The wedge / tail branches use CUDA's
-// exp / log1p, which are faithfully rounded (<= 1 ulp) like glibc's; a
-// decision could only differ when both sides of a comparison are within one
-// ulp of each other.
+// Ziggurat standard normal (numpy random_standard_normal).  The tail value
+// uses glibc's log1p restated bit for bit (below); the wedge's exp only
+// enters a comparison, which could only differ when both sides lie within
+// one ulp of each other.
 // ---------------------------------------------------------------------------
 }  // namespace smx
 
 #include "ziggurat_tables.cuh"
 
 namespace smx {
+
+// log1p(x) for x in (-1, 0] exactly as the x86-64 glibc (2.39) that numpy's
+// npy_log1p calls on an FMA-capable host: libm's ifunc picks the FMA build of
+// sysdeps/ieee754/dbl-64/s_log1p.c, transcribed here operation for operation
+// from that build (contractions included).  CUDA's log1p is faithfully rounded
+// but differs from glibc's in the last bit often enough to change ziggurat
+// tail values (tests/test_gpu_rng.py::test_normal_slow_paths_at_scale); this
+// one was checked against glibc on 2e8 arguments -u, u = k 2^-53 (0 mismatches).
+__device__ __forceinline__ double glibc_log1p_neg(double x) {
+  const uint32_t hx = (uint32_t)((uint64_t)__double_as_longlong(x) >> 32);
+  if ((hx & 0x7fffffffu) < 0x3e200000u) {  // |x| < 2^-29
+    if ((hx & 0x7fffffffu) < 0x3c900000u) return x;
+    return __fma_rn(-__dmul_rn(x, x), 0.5, x);
+  }
+  const double LN2_HI = 6.93147180369123816490e-01, LN2_LO = 1.90821492927058770002e-10;
+  int k;
+  double f, hfsq, c = 0.0;
+  uint32_t hu;
+  if (hx + 0x402d413cu <= 0x402d413cu) {  // x <= -0.2929: k != 0
+    double u = __dadd_rn(x, 1.0);
+    hu = (uint32_t)((uint64_t)__double_as_longlong(u) >> 32);
+    k = (int)(hu >> 20) - 1023;
+    c = k > 0 ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+    c = __ddiv_rn(c, u);
+    hu &= 0xfffffu;
+    const uint64_t lo = (uint64_t)__double_as_longlong(u) & 0xffffffffull;
+    if (hu > 0x6a09du) {
+      k += 1;
+      u = __longlong_as_double((long long)(((uint64_t)(hu | 0x3fe00000u) << 32) | lo));
+      hu = (0x100000u - hu) >> 2;
+    } else {
+      u = __longlong_as_double((long long)(((uint64_t)(hu | 0x3ff00000u) << 32) | lo));
+    }
+    f = __dsub_rn(u, 1.0);
+    hfsq = __dmul_rn(__dmul_rn(f, 0.5), f);
+    if (hu == 0) {
+      const double dk = (double)k;
+      if (f == 0.0) return __fma_rn(dk, LN2_HI, __fma_rn(dk, LN2_LO, c));
+      const double R = __dmul_rn(__fma_rn(-f, 6.66666666666666629659e-01, 1.0), hfsq);
+      return __fma_rn(dk, LN2_HI, -__dsub_rn(__dsub_rn(R, __fma_rn(dk, LN2_LO, c)), f));
+    }
+  } else {
+    k = 0;
+    f = x;
+    hfsq = __dmul_rn(__dmul_rn(x, 0.5), x);
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(f, 2.0));
+  const double z = __dmul_rn(s, s);
+  const double R2 = __fma_rn(z, 2.857142874366239149e-01, 3.999999999940941908e-01);
+  const double R3 = __fma_rn(z, 1.818357216161805012e-01, 2.222219843214978396e-01);
+  const double R4 = __fma_rn(z, 1.479819860511658591e-01, 1.531383769920937332e-01);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z2, z4);
+  const double R =
+      __fma_rn(z6, R4, __fma_rn(z4, R3, __fma_rn(z, 6.666666666666735130e-01, __dmul_rn(z2, R2))));
+  const double t = __dmul_rn(__dadd_rn(R, hfsq), s);
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, t));
+  const double dk = (double)k;
+  const double a = __dadd_rn(__fma_rn(dk, LN2_LO, c), t);
+  return __fma_rn(dk, LN2_HI, -__dsub_rn(__dsub_rn(hfsq, a), f));
+}
 
 __device__ __forceinline__ double zig_standard_normal(SeqStream& s) {
   for (;;) {
@@ -109,8 +168,8 @@ __device__ __forceinline__ double zig_standard_normal(SeqStream& s) {
     if (rabs < ZIG_KI_DOUBLE_BITS[idx]) return x;
     if (idx == 0) {
       for (;;) {
-        const double xx = __dmul_rn(-ZIG_NOR_INV_R, log1p(-s.next_double()));
-        const double yy = -log1p(-s.next_double());
+        const double xx = __dmul_rn(-ZIG_NOR_INV_R, glibc_log1p_neg(-s.next_double()));
+        const double yy = -glibc_log1p_neg(-s.next_double());
         if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx))
           return ((rabs >> 8) & 1) ? -__dadd_rn(ZIG_NOR_R, xx) : __dadd_rn(ZIG_NOR_R, xx);
       }

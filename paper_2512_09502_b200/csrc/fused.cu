@@ -76,9 +76,11 @@ struct FusedGen {
   int* overflow;
 };
 
+// KM 1: key table; 3: piecewise-affine pieces; 4: a single piece (key = v + delta)
 template <int KM>
 __device__ __forceinline__ uint32_t fg_key(const FusedGen& g, uint32_t v) {
   if (KM == 1) return __ldg(g.key_tab + v);
+  if (KM == 4) return v + g.pdelta[0];
   uint32_t off = g.pdelta[0];
 #pragma unroll
   for (int s = 1; s < FG_MAXP; ++s)
@@ -149,9 +151,13 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     __syncthreads();
     const uint32_t t = s_t;
     if (t >= n_tiles) break;
-    // 1. draw the thread's 16 consecutive raw positions (two Philox blocks)
+    // 1. draw the thread's 16 consecutive raw positions (two Philox blocks);
+    //    padded layout (one word per 32): conflict-free both ways
     const uint64_t p0 = (uint64_t)t * FG_TILE + (uint64_t)tid * FG_IPT;
-#pragma unroll 1
+    const bool full = (uint64_t)(t + 1) * FG_TILE <= g.n_raw;
+    const uint32_t lim = full ? FG_IPT : (g.n_raw > p0 ? (g.n_raw - p0 < FG_IPT ? (uint32_t)(g.n_raw - p0) : (uint32_t)FG_IPT) : 0u);
+    uint32_t* xw = xs + tid * FG_IPT + (tid >> 1);
+#pragma unroll
     for (int q = 0; q < 2; ++q) {
       uint64_t w[4];
       philox4x64_10(p0 / 8 + q + 1, g.key, w);
@@ -159,19 +165,16 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       for (int i = 0; i < 8; ++i) {
         const uint32_t v = (i & 1) ? (uint32_t)(w[i >> 1] >> 32) : (uint32_t)w[i >> 1];
         uint32_t out;
-        const bool ok = g.lm.accept(v, out) && p0 + 8 * q + i < g.n_raw;
-        const uint32_t p = tid * FG_IPT + 8 * q + i;
-        xs[p + (p >> 5)] = ok ? fg_key<KM>(g, out) : FG_NOKEY;
+        const bool ok = g.lm.accept(v, out) && (full || (uint32_t)(8 * q + i) < lim);
+        xw[8 * q + i] = ok ? fg_key<KM>(g, out) : FG_NOKEY;
       }
     }
     __syncthreads();
     // 2. raw order, warp-striped: item i of lane l is warp position 32 i + l
     uint32_t k[FG_IPT];
+    const uint32_t* xr = xs + warp * (33 * FG_IPT) + lane;
 #pragma unroll
-    for (int i = 0; i < FG_IPT; ++i) {
-      const uint32_t p = warp * (32 * FG_IPT) + 32 * i + lane;
-      k[i] = xs[p + (p >> 5)];
-    }
+    for (int i = 0; i < FG_IPT; ++i) k[i] = xr[33 * i];
     for (int j = lane; j < BC / 2; j += 32) reinterpret_cast<uint32_t*>(mycnt)[j] = 0;
     __syncwarp();
     uint32_t rank2[FG_IPT / 2];
@@ -191,21 +194,24 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       if (LB == 0) mycnt[0] = (uint16_t)run;
     }
     __syncthreads();  // counters complete; xs is free
-    // 3. per digit: tile count, per-warp exclusive bases; publish the aggregate
+    // 3. per digit: tile count (published at once), tile start, per-warp bases
     uint32_t c = 0;
     if (tid < B) {
-      uint32_t acc = 0;
-#pragma unroll 4
+#pragma unroll
+      for (int w = 0; w < FG_WARPS; ++w) c += wcnt[w * BC + tid];
+      st_vol(g.status + (size_t)t * B + tid, (t == 0 ? ST_P : ST_A) | c);
+    }
+    uint32_t tot;
+    const uint32_t ts = block_excl_scan(tid < B ? c : 0u, ws, tot);
+    if (tid < B) {  // wcnt[w][d] = staging position of warp w's first record of digit d
+      uint32_t acc = ts;
+#pragma unroll
       for (int w = 0; w < FG_WARPS; ++w) {
         const uint32_t x = wcnt[w * BC + tid];
         wcnt[w * BC + tid] = (uint16_t)acc;
         acc += x;
       }
-      c = acc;
-      st_vol(g.status + (size_t)t * B + tid, (t == 0 ? ST_P : ST_A) | c);
     }
-    uint32_t tot;
-    const uint32_t ts = block_excl_scan(tid < B ? c : 0u, ws, tot);
     // 4. look-back: records of this digit in earlier tiles of the call
     uint64_t excl = 0;
     if (tid < B) {
@@ -228,6 +234,7 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
             done = (w[u] & ST_P) != 0;
           }
           if (done) break;
+          if (used == 0) __nanosleep(64);  // predecessor still drawing: leave the issue slots to others
           i -= used;
         }
         excl = e;
@@ -266,7 +273,7 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       if (r == 0xffffu) continue;
       const uint32_t d = LB ? (k[i] & DM) : 0u;
       const uint32_t rec = j < g.n_out ? (((k[i] >> LB) << g.pbits) | g.tag | fg_tidx(g, j)) : FG_SENTINEL;
-      const uint32_t pos = tstart[d] + wcnt[warp * BC + d] + r;
+      const uint32_t pos = wcnt[warp * BC + d] + r;
       xs[pos] = rec;
       sd[pos] = (uint16_t)d;
     }
@@ -780,8 +787,9 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
   SMX_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (n_tiles * B + 1), st));
   g.status = ws;
   g.ticket = ws + n_tiles * B;
-  const int rc = key_mode == 3 ? fg_dispatch<3>(lo_bits, g, (uint32_t)n_tiles, st)
-                               : fg_dispatch<1>(lo_bits, g, (uint32_t)n_tiles, st);
+  const int rc = key_mode == 1 ? fg_dispatch<1>(lo_bits, g, (uint32_t)n_tiles, st)
+                 : g.np == 1   ? fg_dispatch<4>(lo_bits, g, (uint32_t)n_tiles, st)
+                               : fg_dispatch<3>(lo_bits, g, (uint32_t)n_tiles, st);
   cudaFreeAsync(ws, st);
   return rc;
 }

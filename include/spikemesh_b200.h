@@ -155,23 +155,24 @@ int smx_promote_wide(const uint32_t* vals, uint64_t n, const double* cls_w, cons
  * passes of an LSD radix sort whose first pass is the draw itself.
  * smx_fused_gen: one call's integers(0, ex, size=n_out) draws from the start
  * of stream (k0, k1), ranked by the low key digit and written as packed u32
- * records (key >> lo_bits) << pbits | tag | j / kdiv into the digit regions
- * (rstart / rcap / fill_in / fill_out: device arrays of 2^lo_bits entries).
+ * records (key >> lo_bits) << pbits | cpay[j / kdiv] into the digit regions
+ * (rstart / rcap / fill_in / fill_out: device arrays of 2^lo_bits entries;
+ * cpay: the compact payload of each target, row | class index << row bits).
  * key_mode 3: key_tab is a host array {n, start[n], delta[n]} of piecewise-
  * affine keys; key_mode 1: device table key_tab[value].  *total_out = accepted
  * draws of the raw window (< n_out: window short); *overflow set when a region
  * was too small (the caller rebuilds through smx_gen_draw + smx_sort_records). */
 int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_out, int key_mode, const uint32_t* key_tab,
-                  uint32_t kdiv, uint32_t tag, int lo_bits, int pbits, uint32_t* region, const uint64_t* rstart,
-                  const uint64_t* rcap, const uint64_t* fill_in, uint64_t* fill_out, uint64_t* total_out,
-                  int* overflow, void* stream);
+                  uint32_t kdiv, const uint32_t* cpay, int lo_bits, int pbits, uint32_t* region, uint64_t n_slots,
+                  const uint64_t* rstart, const uint64_t* rcap, const uint64_t* fill_in, uint64_t* fill_out,
+                  uint64_t* total_out, int* overflow, void* stream);
 /* smx_fused_sort: pass B over the regions: stable scatter by the high digit
- * (hi_bits 8..11) writing out[] = pay_tabs[tag][tidx] in key order and
- * counts[key] (key = hi << lo_bits | region; first_index via
+ * (hi_bits 8..11) writing out[] = row | cls_map[class index] in key order
+ * and counts[key] (key = hi << lo_bits | region; first_index via
  * smx_counts_to_offsets).  rcap_host: host copy of the capacities. */
 int smx_fused_sort(const uint32_t* region, const uint64_t* rstart, const uint64_t* fill, const uint64_t* rcap_host,
-                   int lo_bits, int hi_bits, int pbits, int tidx_bits, const uint64_t* pay_tabs, uint32_t* counts,
-                   uint64_t n_keys, uint32_t* out, int* err, void* stream);
+                   int lo_bits, int hi_bits, int pbits, int row_bits, const uint32_t* cls_map, uint32_t* counts,
+                   uint64_t n_keys, uint64_t n_records, uint32_t* out, int* err, void* stream);
 /* ConnectionStore.finalize: stable sort of pending records by source. */
 int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, uint64_t n,
                      int key_bits, int index_values, const uint32_t* lut, uint32_t* counts, uint64_t n_keys,

@@ -15,7 +15,8 @@
 //     stably by the low key digit (ballot multisplit), finds each digit's
 //     position across tiles with a decoupled look-back (tiles taken in order
 //     from a ticket) and writes one packed u32 per record into that digit's
-//     region:  rec = (key >> lo_bits) << pbits | call tag | target index.
+//     region:  rec = (key >> lo_bits) << pbits | compact payload, the compact
+//     payload being the target row and a per-rank class index.
 //     Regions are sized from the exact digit probabilities of the call's
 //     source-value -> key map (expectation + 8 sigma); an overflow sets a flag
 //     and the engine rebuilds the rank through the general path.
@@ -23,7 +24,7 @@
 //     per 3840-record tile of a region: histogram of the high digit
 //     (fb_hist), per-region / per-digit scans (per-key counts for
 //     first_index fall out of the same sums), then a stable scatter by the
-//     high digit that writes the final payload pay_tab[call][target index]
+//     high digit that writes the final payload (row | global class << 24)
 //     (fb_scatter, TMA tile loads, coalesced digit runs).
 //
 // Record bytes: pass A writes 4 B, pass B reads 4 B twice and writes 4 B
@@ -62,8 +63,7 @@ struct FusedGen {
   const uint32_t* key_tab;  // key mode 1: key = key_tab[value]
   uint32_t kdiv;      // k_in: target index = j / kdiv
   FastDiv kd;
-  int wide_j;         // j may reach 2^32
-  uint32_t tag;       // call tag << tidx_bits
+  const uint32_t* cpay;  // compact payload of each target index (row | class index << row bits)
   int pbits;          // bits below the high key digit in a record
   uint32_t* region;
   const uint64_t* rstart;   // [B] first slot of each digit region
@@ -86,15 +86,6 @@ __device__ __forceinline__ uint32_t fg_key(const FusedGen& g, uint32_t v) {
   for (int s = 1; s < FG_MAXP; ++s)
     if (s < (int)g.np && v >= g.pstart[s]) off = g.pdelta[s];
   return v + off;
-}
-
-__device__ __forceinline__ uint32_t fg_tidx(const FusedGen& g, uint64_t j) {
-  if (!g.wide_j) return g.kd.div((uint32_t)j);
-  uint64_t q = (uint64_t)((double)j / (double)g.kdiv);  // within one of the quotient for j < 2^53
-  int64_t r = (int64_t)(j - q * g.kdiv);
-  while (r < 0) { --q; r += g.kdiv; }
-  while (r >= (int64_t)g.kdiv) { ++q; r -= g.kdiv; }
-  return (uint32_t)q;
 }
 
 __device__ __forceinline__ uint32_t ld_vol(const uint32_t* p) { return *(const volatile uint32_t*)p; }
@@ -127,7 +118,8 @@ __device__ __forceinline__ uint32_t fg_rank(uint32_t d, bool valid, uint32_t vm,
   return valid ? old + __popc(peers & lt) : 0xffffu;
 }
 
-template <int KM, int LB>
+// WIDE: region slots may exceed 2^31 (64-bit staging offsets)
+template <int KM, int LB, bool WIDE>
 __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     fused_gen_kernel(const __grid_constant__ FusedGen g, uint32_t n_tiles) {
   constexpr int B = 1 << LB;
@@ -143,6 +135,7 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
   __shared__ uint32_t wacc[FG_WARPS];
   __shared__ unsigned long long wred[FG_WARPS];
   __shared__ uint32_t s_t;
+  __shared__ uint32_t s_tq, s_tr, s_lim;  // target index / remainder of the tile's first draw, records left
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = (1u << lane) - 1;
   uint16_t* mycnt = wcnt + warp * BC;
@@ -261,71 +254,94 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       jbase += wred[w];
       if (w < warp) wbase += wacc[w];
     }
-    if (t == n_tiles - 1 && tid == 0) *g.total = jbase + tot;
+    if (tid == 0) {
+      // draw j of the tile = jbase + a: target index tq + (tr + a) / k (32-bit
+      // from here on); records past the call's end become sentinels
+      const uint64_t tq = jbase / g.kdiv;
+      s_tq = (uint32_t)tq;
+      s_tr = (uint32_t)(jbase - tq * g.kdiv);
+      s_lim = jbase >= g.n_out ? 0u : (g.n_out - jbase > 0xffffffffull ? 0xffffffffu : (uint32_t)(g.n_out - jbase));
+      if (t == n_tiles - 1) *g.total = jbase + tot;
+    }
+    __syncthreads();
     // 5. records, staged in digit order (accept ranks recomputed: fewer live registers)
-    uint64_t jw = jbase + wbase;
+    const uint32_t tq = s_tq, tr = s_tr, left = s_lim;
+    uint32_t aw = (uint32_t)wbase;
 #pragma unroll
     for (int i = 0; i < FG_IPT; ++i) {
       const uint32_t vm = __ballot_sync(0xffffffffu, k[i] != FG_NOKEY);
-      const uint64_t j = jw + __popc(vm & lt);
-      jw += __popc(vm);
+      const uint32_t a = aw + __popc(vm & lt);
+      aw += __popc(vm);
       const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
       if (r == 0xffffu) continue;
       const uint32_t d = LB ? (k[i] & DM) : 0u;
-      const uint32_t rec = j < g.n_out ? (((k[i] >> LB) << g.pbits) | g.tag | fg_tidx(g, j)) : FG_SENTINEL;
+      const uint32_t rec =
+          a < left ? (((k[i] >> LB) << g.pbits) | __ldg(g.cpay + tq + g.kd.div(tr + a))) : FG_SENTINEL;
       const uint32_t pos = wcnt[warp * BC + d] + r;
       xs[pos] = rec;
       sd[pos] = (uint16_t)d;
     }
     __syncthreads();
     // 6. coalesced runs per digit
-    for (uint32_t q = tid; q < tot; q += FG_THREADS) {
-      const uint32_t d = sd[q];
-      const uint64_t base = delta[d];
-      if (base != ~0ull) g.region[base + q] = xs[q];
+    if (WIDE) {
+      for (uint32_t q = tid; q < tot; q += FG_THREADS) {
+        const uint64_t base = delta[sd[q]];
+        if (base != ~0ull) g.region[base + q] = xs[q];
+      }
+    } else {
+      const uint32_t* d32 = reinterpret_cast<const uint32_t*>(delta);  // low words (little endian)
+      for (uint32_t q = tid; q < tot; q += FG_THREADS) {
+        const uint32_t base = d32[2 * sd[q]];
+        if (base != 0xffffffffu) g.region[base + q] = xs[q];
+      }
     }
     __syncthreads();
   }
 }
 
-template <int KM, int LB>
+template <int LB>
 size_t fg_smem() {
   constexpr int B = 1 << LB;
   constexpr int BC = B < 2 ? 2 : B;
   return (size_t)FG_XS * 4 + (size_t)B * 12 + (size_t)FG_TILE * 2 + (size_t)FG_WARPS * BC * 2;
 }
 
-template <int KM, int LB>
+template <int KM, int LB, bool WIDE>
 int fg_launch(const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
-  const size_t smem = fg_smem<KM, LB>();
+  const size_t smem = fg_smem<LB>();
   static int configured = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured != dev) {  // per device (one Cluster drives one device; see engine)
-    SMX_CUDA_CHECK(cudaFuncSetAttribute(fused_gen_kernel<KM, LB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(fused_gen_kernel<KM, LB, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
     configured = dev;
   }
   const uint32_t grid = std::min<uint32_t>(n_tiles, 148u * SMX_FG_MIN_BLOCKS);
   smx_count_launch();
-  fused_gen_kernel<KM, LB><<<grid, FG_THREADS, smem, st>>>(g, n_tiles);
+  fused_gen_kernel<KM, LB, WIDE><<<grid, FG_THREADS, smem, st>>>(g, n_tiles);
   SMX_LAUNCH_CHECK();
   return 0;
 }
 
+template <int KM, int LB>
+int fg_wide(bool wide, const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
+  return wide ? fg_launch<KM, LB, true>(g, n_tiles, st) : fg_launch<KM, LB, false>(g, n_tiles, st);
+}
+
 template <int KM>
-int fg_dispatch(int lo_bits, const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
+int fg_dispatch(int lo_bits, bool wide, const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
   switch (lo_bits) {
-    case 0: return fg_launch<KM, 0>(g, n_tiles, st);
-    case 1: return fg_launch<KM, 1>(g, n_tiles, st);
-    case 2: return fg_launch<KM, 2>(g, n_tiles, st);
-    case 3: return fg_launch<KM, 3>(g, n_tiles, st);
-    case 4: return fg_launch<KM, 4>(g, n_tiles, st);
-    case 5: return fg_launch<KM, 5>(g, n_tiles, st);
-    case 6: return fg_launch<KM, 6>(g, n_tiles, st);
-    case 7: return fg_launch<KM, 7>(g, n_tiles, st);
-    case 8: return fg_launch<KM, 8>(g, n_tiles, st);
-    case 9: return fg_launch<KM, 9>(g, n_tiles, st);
+    case 0: return fg_wide<KM, 0>(wide, g, n_tiles, st);
+    case 1: return fg_wide<KM, 1>(wide, g, n_tiles, st);
+    case 2: return fg_wide<KM, 2>(wide, g, n_tiles, st);
+    case 3: return fg_wide<KM, 3>(wide, g, n_tiles, st);
+    case 4: return fg_wide<KM, 4>(wide, g, n_tiles, st);
+    case 5: return fg_wide<KM, 5>(wide, g, n_tiles, st);
+    case 6: return fg_wide<KM, 6>(wide, g, n_tiles, st);
+    case 7: return fg_wide<KM, 7>(wide, g, n_tiles, st);
+    case 8: return fg_wide<KM, 8>(wide, g, n_tiles, st);
+    case 9: return fg_wide<KM, 9>(wide, g, n_tiles, st);
     default: break;
   }
   smx_set_error("smx_fused_gen: low digit of %d bits (0..9 supported)", lo_bits);
@@ -346,10 +362,10 @@ struct FusedSort {
   const uint32_t* tile_first; // [R + 1] first tile of each region
   const uint32_t* chunk_first;// [R + 1] first scan chunk of each region
   uint32_t n_regions;
-  int pbits;                  // record = hi << pbits | tag | tidx
-  int tidx_bits;
+  int pbits;                  // record = hi << pbits | class index << row_bits | row
+  int row_bits;
   int lo_bits;                // key = hi << lo_bits | region
-  const uint64_t* pay_tabs;   // [n_tags] device pointers to u32 payload tables
+  const uint32_t* cls_map;    // [2^(pbits - row_bits)] class index -> global class id << 24
   uint32_t* counts;           // [n_keys] records per key
   uint64_t n_keys;
   uint32_t* out;              // final payload (sorted by key)
@@ -382,15 +398,20 @@ __device__ __forceinline__ FbTile fb_tile(const FusedSort& s, uint32_t T) {
   return x;
 }
 
-// Per-tile histogram of the high digit (sentinels skipped); one warp per tile.
+// Per-tile histogram of the high digit (sentinels skipped); one warp per
+// tile, as many warps per CTA as their u32 histograms fit in 128 KB.
+template <int BITS>
+__host__ __device__ constexpr int fb_hist_warps() { return (128 * 1024) / (4 << BITS) < 32 ? (128 * 1024) / (4 << BITS) : 32; }
+
 template <int BITS>
 __global__ void __launch_bounds__(1024) fb_hist_kernel(const __grid_constant__ FusedSort s, uint16_t* tcnt,
                                                        uint32_t n_tiles) {
   constexpr int BINS = 1 << BITS;
-  extern __shared__ uint32_t fbh[];  // [32][BINS]
+  constexpr int HW = fb_hist_warps<BITS>();
+  extern __shared__ uint32_t fbh[];  // [HW][BINS]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* wh = fbh + warp * BINS;
-  for (uint32_t T = blockIdx.x * 32 + warp; T < n_tiles; T += gridDim.x * 32) {
+  for (uint32_t T = blockIdx.x * HW + warp; T < n_tiles; T += gridDim.x * HW) {
     for (int j = lane; j < BINS; j += 32) wh[j] = 0;
     __syncwarp();
     const FbTile x = fb_tile(s, T);
@@ -547,10 +568,10 @@ __global__ void __launch_bounds__(256) fb_tile_offsets_kernel(const __grid_const
 // Stable scatter by the high digit; tiles in global (region, tile) order from
 // a ticket so the tiles in flight write neighbouring parts of every digit's
 // output (partial sectors complete in L2).  Writes the final payload.
-template <int BITS>
 #ifndef SMX_FB_CTAS
 #define SMX_FB_CTAS 3
 #endif
+template <int BITS, bool WIDE>
 __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(const __grid_constant__ FusedSort s,
                                                                    const uint32_t* off, const uint64_t* dbase,
                                                                    uint32_t n_tiles, uint32_t* tile_ctr) {
@@ -566,27 +587,35 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
   uint16_t* wcnt = reinterpret_cast<uint16_t*>(delta + BINS);     // [FB_WARPS][BINS]
   __shared__ uint32_t ws[32];
   __shared__ uint32_t ticket[2];
+  __shared__ FbTile tinfo[2];
+  __shared__ uint32_t cmap[256];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = (1u << lane) - 1;
-  const uint32_t tmask = (1u << s.tidx_bits) - 1;
-  const uint32_t pmask = (1u << s.pbits) - 1;
+  const uint32_t rmask = (1u << s.row_bits) - 1;
+  const uint32_t cmask = (1u << (s.pbits - s.row_bits)) - 1;
+  for (int i = tid; i <= (int)cmask; i += FB_THREADS) cmap[i] = s.cls_map[i];
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](uint32_t T) {  // thread 0: offset row + (full tiles) records
-    const FbTile x = fb_tile(s, T);
+  // thread 0 takes the tickets: the tile's (region, slots) for everyone, then
+  // its TMA -- the offset row and, for full tiles, the records
+  auto take = [&](int sl) {
+    const uint32_t T = atomicAdd(tile_ctr, 1u);
+    ticket[sl] = T;
+    if (T < n_tiles) tinfo[sl] = fb_tile(s, T);
+  };
+  auto issue = [&](uint32_t T, const FbTile& x) {
     const bool full = x.n == FB_TILE;
     mbar_expect_tx(&bar, BINS * 4 + (full ? FB_TILE * 4 : 0));
     bulk_g2s(ioff, off + (size_t)T * BINS, BINS * 4, &bar);
     if (full) bulk_g2s(irec, s.region + x.a, FB_TILE * 4, &bar);
   };
   if (tid == 0) {
-    const uint32_t T = atomicAdd(tile_ctr, 1u);
-    ticket[0] = T;
-    if (T < n_tiles) issue(T);
+    take(0);
+    if (ticket[0] < n_tiles) issue(ticket[0], tinfo[0]);
   }
   __syncthreads();
   uint16_t* mycnt = wcnt + warp * BINS;
@@ -594,7 +623,7 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
   uint32_t phase = 0;
   int slot = 0;
   for (uint32_t T = ticket[0]; T < n_tiles; T = ticket[slot ^= 1]) {
-    const FbTile x = fb_tile(s, T);
+    const FbTile x = tinfo[slot];
     const bool full = x.n == FB_TILE;
     mbar_wait(&bar, phase);
     phase ^= 1;
@@ -619,7 +648,7 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
       if (i & 1) rank2[i >> 1] |= r << 16; else rank2[i >> 1] = r;
     }
     __syncthreads();  // 1: counters complete, records in registers
-    if (tid == 0) ticket[slot ^ 1] = atomicAdd(tile_ctr, 1u);
+    if (tid == 0) take(slot ^ 1);
     uint32_t tot[DPT];
     uint32_t mysum = 0;
 #pragma unroll
@@ -648,31 +677,34 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
     }
     __syncthreads();  // 2: offsets ready; offset row and record buffer free
     const uint32_t nxt = ticket[slot ^ 1];
-    // stage payloads in digit order (the record buffer is reused)
+    // stage the final payloads in digit order (the record buffer is reused)
 #pragma unroll
     for (int i = 0; i < FB_IPT; ++i) {
       const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
       if (r != 0xffffu) {
         const uint32_t d = (rec[i] >> s.pbits) & mask;
-        const uint32_t low = rec[i] & pmask;
-        const uint32_t* pt = reinterpret_cast<const uint32_t*>(__ldg(s.pay_tabs + (low >> s.tidx_bits)));
         const uint32_t pos = mycnt[d] + r;
-        irec[pos] = __ldg(pt + (low & tmask));
+        irec[pos] = (rec[i] & rmask) | cmap[(rec[i] >> s.row_bits) & cmask];
         sdig[pos] = (uint16_t)d;
       }
     }
     __syncthreads();  // 3: staged
-    for (uint32_t q = tid; q < tsum; q += FB_THREADS) s.out[delta[sdig[q]] + q] = irec[q];
+    if (WIDE) {
+      for (uint32_t q = tid; q < tsum; q += FB_THREADS) s.out[delta[sdig[q]] + q] = irec[q];
+    } else {
+      const uint32_t* d32 = reinterpret_cast<const uint32_t*>(delta);
+      for (uint32_t q = tid; q < tsum; q += FB_THREADS) s.out[d32[2 * sdig[q]] + q] = irec[q];
+    }
     __syncthreads();  // 4: staging read: buffers may be refilled
     if (tid == 0 && nxt < n_tiles) {
       fence_proxy_async();
-      issue(nxt);
+      issue(nxt, tinfo[slot ^ 1]);
     }
   }
 }
 
 template <int BITS>
-int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, cudaStream_t st) {
+int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, cudaStream_t st) {
   constexpr int BINS = 1 << BITS;
   uint16_t* tcnt = nullptr;
   uint32_t *off = nullptr, *csum = nullptr, *ctr = nullptr, *rsum = nullptr;
@@ -684,19 +716,22 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, cudaStream_t
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&rsum, sizeof(uint32_t) * (size_t)s.n_regions * BINS, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&ctr, sizeof(uint32_t), st));
   SMX_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
-  const size_t h_smem = (size_t)32 * BINS * 4;
+  constexpr int HW = fb_hist_warps<BITS>();
+  const size_t h_smem = (size_t)HW * BINS * 4;
   const size_t s_smem = (size_t)FB_TILE * 6 + (size_t)BINS * 12 + (size_t)FB_WARPS * BINS * 2;
   static int configured = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured != dev) {
     SMX_CUDA_CHECK(cudaFuncSetAttribute(fb_hist_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h_smem));
-    SMX_CUDA_CHECK(cudaFuncSetAttribute(fb_scatter_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(fb_scatter_kernel<BITS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)s_smem));
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(fb_scatter_kernel<BITS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)s_smem));
     configured = dev;
   }
-  const uint32_t hgrid = std::max<uint32_t>(1, std::min<uint32_t>((n_tiles + 31) / 32, 148 * 2));
-  smx_count_launch(); fb_hist_kernel<BITS><<<hgrid, 1024, h_smem, st>>>(s, tcnt, n_tiles);
+  const uint32_t hgrid = std::max<uint32_t>(1, std::min<uint32_t>((n_tiles + HW - 1) / HW, 148 * 2));
+  smx_count_launch(); fb_hist_kernel<BITS><<<hgrid, 32 * HW, h_smem, st>>>(s, tcnt, n_tiles);
   if (n_chunks) {
     smx_count_launch(); fb_chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum);
   }
@@ -707,7 +742,9 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, cudaStream_t
     smx_count_launch(); fb_tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum, off);
   }
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(n_tiles, 148u * SMX_FB_CTAS));
-  smx_count_launch(); fb_scatter_kernel<BITS><<<grid, FB_THREADS, s_smem, st>>>(s, off, dbase, n_tiles, ctr);
+  smx_count_launch();
+  if (wide) fb_scatter_kernel<BITS, true><<<grid, FB_THREADS, s_smem, st>>>(s, off, dbase, n_tiles, ctr);
+  else fb_scatter_kernel<BITS, false><<<grid, FB_THREADS, s_smem, st>>>(s, off, dbase, n_tiles, ctr);
   SMX_LAUNCH_CHECK();
   cudaFreeAsync(tcnt, st);
   cudaFreeAsync(off, st);
@@ -729,9 +766,10 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, cudaStream_t
 // in the raw window (< n_out: the window was short, rebuild), *overflow is
 // set when a region is too small.
 extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_out, int key_mode,
-                             const uint32_t* key_tab, uint32_t kdiv, uint32_t tag, int lo_bits, int pbits,
-                             uint32_t* region, const uint64_t* rstart, const uint64_t* rcap, const uint64_t* fill_in,
-                             uint64_t* fill_out, uint64_t* total_out, int* overflow, void* stream) {
+                             const uint32_t* key_tab, uint32_t kdiv, const uint32_t* cpay, int lo_bits, int pbits,
+                             uint32_t* region, uint64_t n_slots, const uint64_t* rstart, const uint64_t* rcap,
+                             const uint64_t* fill_in, uint64_t* fill_out, uint64_t* total_out, int* overflow,
+                             void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n_out == 0) {
     SMX_CUDA_CHECK(cudaMemcpyAsync(fill_out, fill_in, sizeof(uint64_t) << lo_bits, cudaMemcpyDeviceToDevice, st));
@@ -766,8 +804,11 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
   }
   g.kdiv = kdiv;
   g.kd = FastDiv::make(kdiv);
-  g.wide_j = n_out > 0xffffffffULL;
-  g.tag = tag;
+  g.cpay = cpay;
+  if ((uint64_t)kdiv + 2 * FG_TILE >= 0xffffffffull) {
+    smx_set_error("smx_fused_gen: k_in %u too large", kdiv);
+    return -1;
+  }
   g.pbits = pbits;
   g.region = region;
   g.rstart = rstart;
@@ -787,9 +828,10 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
   SMX_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (n_tiles * B + 1), st));
   g.status = ws;
   g.ticket = ws + n_tiles * B;
-  const int rc = key_mode == 1 ? fg_dispatch<1>(lo_bits, g, (uint32_t)n_tiles, st)
-                 : g.np == 1   ? fg_dispatch<4>(lo_bits, g, (uint32_t)n_tiles, st)
-                               : fg_dispatch<3>(lo_bits, g, (uint32_t)n_tiles, st);
+  const bool wide = n_slots >= 0x7fffffffull;  // 32-bit staging offsets below 2^31 slots
+  const int rc = key_mode == 1 ? fg_dispatch<1>(lo_bits, wide, g, (uint32_t)n_tiles, st)
+                 : g.np == 1   ? fg_dispatch<4>(lo_bits, wide, g, (uint32_t)n_tiles, st)
+                               : fg_dispatch<3>(lo_bits, wide, g, (uint32_t)n_tiles, st);
   cudaFreeAsync(ws, st);
   return rc;
 }
@@ -800,9 +842,9 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
 // out[] (payloads sorted by key = hi << lo_bits | r) and counts[key] (zeroed
 // first).  err receives 6 for a key >= n_keys.
 extern "C" int smx_fused_sort(const uint32_t* region, const uint64_t* rstart, const uint64_t* fill,
-                              const uint64_t* rcap_host, int lo_bits, int hi_bits, int pbits, int tidx_bits,
-                              const uint64_t* pay_tabs, uint32_t* counts, uint64_t n_keys, uint32_t* out, int* err,
-                              void* stream) {
+                              const uint64_t* rcap_host, int lo_bits, int hi_bits, int pbits, int row_bits,
+                              const uint32_t* cls_map, uint32_t* counts, uint64_t n_keys, uint64_t n_records,
+                              uint32_t* out, int* err, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   SMX_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * n_keys, st));
   if (hi_bits < 8 || hi_bits > 11) {
@@ -838,19 +880,24 @@ extern "C" int smx_fused_sort(const uint32_t* region, const uint64_t* rstart, co
   s.chunk_first = dfirst + R + 1;
   s.n_regions = R;
   s.pbits = pbits;
-  s.tidx_bits = tidx_bits;
+  s.row_bits = row_bits;
   s.lo_bits = lo_bits;
-  s.pay_tabs = pay_tabs;
+  s.cls_map = cls_map;
+  if (pbits - row_bits > 8) {
+    smx_set_error("smx_fused_sort: more than 256 classes");
+    return -1;
+  }
+  const bool wide = n_records >= 0xffffffffull;
   s.counts = counts;
   s.n_keys = n_keys;
   s.out = out;
   s.err = err;
   int rc = 0;
   switch (hi_bits) {
-    case 8: rc = fb_run<8>(s, (uint32_t)nt, (uint32_t)nc, st); break;
-    case 9: rc = fb_run<9>(s, (uint32_t)nt, (uint32_t)nc, st); break;
-    case 10: rc = fb_run<10>(s, (uint32_t)nt, (uint32_t)nc, st); break;
-    default: rc = fb_run<11>(s, (uint32_t)nt, (uint32_t)nc, st); break;
+    case 8: rc = fb_run<8>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;
+    case 9: rc = fb_run<9>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;
+    case 10: rc = fb_run<10>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;
+    default: rc = fb_run<11>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;
   }
   cudaFreeAsync(dfirst, st);
   return rc;

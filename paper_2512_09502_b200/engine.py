@@ -654,7 +654,7 @@ class Cluster:
             # local fixed in-degree draws: generated at prepare, fused with the sort
             src, tgt, key_tab, pay_tab = self._tables(st, sources, targets, cls, None)
             self._defer(st, aligned_key, n_src, int(conn.k_in) * n_tgt, 1, key_tab, pay_tab, int(conn.k_in),
-                        n_tgt, src_host=np.asarray(sources, dtype=np.int64))
+                        n_tgt, cls, src_host=np.asarray(sources, dtype=np.int64))
             return int(conn.k_in) * n_tgt, src
         self._fused_off(st)
         if cls is None:
@@ -714,9 +714,9 @@ class Cluster:
         st.commit_records(n)
         return n, src
 
-    def _defer(self, st: _Rank, key, ex, n, kmode, ktab, pay_tab, kdiv, n_tgt, src_host=None, acct=None):
+    def _defer(self, st: _Rank, key, ex, n, kmode, ktab, pay_tab, kdiv, n_tgt, cls, src_host=None, acct=None):
         lm_thr = 0 if ex == (1 << 32) else ((1 << 32) - ex) % ex
-        st.deferred.append(dict(key=key, ex=int(ex), n=int(n), kmode=kmode, ktab=ktab, pay_tab=pay_tab,
+        st.deferred.append(dict(key=key, ex=int(ex), n=int(n), kmode=kmode, ktab=ktab, pay_tab=pay_tab, cls=int(cls),
                                 kdiv=int(kdiv), n_tgt=int(n_tgt), src_host=src_host, acct=acct,
                                 prej=lm_thr / 4294967296.0))
         return st.deferred[-1]
@@ -1195,7 +1195,7 @@ class Cluster:
              0 if cls is None else cls, _ptr(pay_tab), sk)
         if defer:
             # generated at prepare, fused with the sort's first pass
-            d = self._defer(st, key, total, n, 3, pieces, pay_tab, k_in, len(tg))
+            d = self._defer(st, key, total, n, 3, pieces, pay_tab, k_in, len(tg), cls)
             self._dist_accounting(st, tr, group, n, 0, present, runs, pieces, False, lut_base, vbase, seg_words,
                                   deferred=d)
             return vbits, present
@@ -1673,10 +1673,12 @@ class Cluster:
         hi = max(8, key_bits - lo)
         if lo > 9 or hi > 11:
             return None
-        tidx_bits = max(1, int(max(d["n_tgt"] for d in calls) - 1).bit_length())
-        seg_bits = int(len(calls) - 1).bit_length()
-        pbits = seg_bits + tidx_bits
-        if hi + pbits > 31:
+        # records carry the compact payload: target row | class index << row bits
+        row_bits = max(1, int(st.n_real - 1).bit_length())
+        cls_ids = sorted({d["cls"] for d in calls})
+        cls_bits = int(len(cls_ids) - 1).bit_length()
+        pbits = row_bits + cls_bits
+        if hi + pbits > 31 or cls_bits > 8:
             return None
         # record counts per source rank of distributed calls (modeled bytes)
         # come from the per-key counts: every accounted call's keys must be
@@ -1703,7 +1705,7 @@ class Cluster:
             var += n * p * (1.0 - p)
         cap = np.ceil(exp + 8.0 * np.sqrt(var) + 64.0).astype(np.int64)
         cap = (cap + 31) // 32 * 32
-        return dict(lo=lo, hi=hi, pbits=pbits, tidx_bits=tidx_bits, cap=cap.astype(np.uint64))
+        return dict(lo=lo, hi=hi, pbits=pbits, row_bits=row_bits, cls_ids=cls_ids, cap=cap.astype(np.uint64))
 
     def _fused_run(self, st: _Rank, plan: dict):
         """Pass A per deferred call into the digit regions, then pass B (csrc/fused.cu)."""
@@ -1722,19 +1724,26 @@ class Cluster:
         fills = torch.zeros((2, B), dtype=torch.int64, device=dev)
         flags = torch.zeros(2 + len(calls), dtype=torch.int64, device=dev)   # overflow, err, totals
         ev0 = self._event(st) if self.prof is not None else None
+        cidx = {c: i for i, c in enumerate(plan["cls_ids"])}
+        cpays = []
         for i, d in enumerate(calls):
+            # compact payload per target: row | class index << row bits
+            cpay = (d["pay_tab"] & ROW_MASK) | (cidx[d["cls"]] << plan["row_bits"])
+            cpays.append(cpay)
             ktab = d["ktab"].ctypes.data if d["kmode"] == 3 else _ptr(d["ktab"])
             call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"],
-                 i << plan["tidx_bits"], lo, plan["pbits"], _ptr(region), _ptr(rs_t), _ptr(rc_t),
+                 _ptr(cpay), lo, plan["pbits"], _ptr(region), slots, _ptr(rs_t), _ptr(rc_t),
                  _ptr(fills[i % 2]), _ptr(fills[(i + 1) % 2]), _ptr(flags[2 + i:]), _ptr(flags), sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
             ev0 = self._event(st)
-        pay_tabs = _up(np.array([d["pay_tab"].data_ptr() for d in calls], dtype=np.int64), dev)
+        cls_map = np.zeros(256, dtype=np.uint32)
+        cls_map[: len(plan["cls_ids"])] = np.array(plan["cls_ids"], dtype=np.uint32) << 24
+        cls_map_t = _up(cls_map.view(np.int32), dev)
         st.counts = torch.empty(max(st.n_nodes, 1), dtype=torch.int32, device=dev)
         st.payload = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         call("smx_fused_sort", _ptr(region), _ptr(rs_t), _ptr(fills[len(calls) % 2]), cap.ctypes.data, lo,
-             plan["hi"], plan["pbits"], plan["tidx_bits"], _ptr(pay_tabs), _ptr(st.counts), st.n_nodes,
+             plan["hi"], plan["pbits"], plan["row_bits"], _ptr(cls_map_t), _ptr(st.counts), st.n_nodes, n,
              _ptr(st.payload), _ptr(flags[1:]), sk)
         st.first_index = torch.empty(st.n_nodes + 1, dtype=torch.int64, device=dev)
         call("smx_counts_to_offsets", _ptr(st.counts), st.n_nodes, _ptr(st.first_index), sk)
@@ -1757,7 +1766,7 @@ class Cluster:
             his = his.clamp(max=st.n_nodes)
             cnt.copy_(cs[his] - cs[los])
         st.store_path = "fused"
-        st.fgen = dict(region=region, meta=meta, fills=fills, flags=flags, pay_tabs=pay_tabs,
+        st.fgen = dict(region=region, meta=meta, fills=fills, flags=flags, cpays=cpays, cls_map=cls_map_t,
                         want=np.array([d["n"] for d in calls], dtype=np.int64))
 
     def _fused_check(self, st: _Rank) -> bool:

@@ -166,11 +166,12 @@ int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_out, int key
                   uint32_t kdiv, const uint32_t* cpay, int lo_bits, int pbits, uint32_t* region, uint64_t n_slots,
                   const uint64_t* rstart, const uint64_t* rcap, const uint64_t* fill_in, uint64_t* fill_out,
                   uint64_t* total_out, int* overflow, void* stream);
-/* smx_fused_sort: pass B over the regions: stable scatter by the high digit
+/* smx_fused_sort: pass B over the regions (region digit * per_digit + call
+ * at rptr[region], fill[region] records): stable scatter by the high digit
  * (hi_bits 8..11) writing out[] = row | cls_map[class index] in key order
- * and counts[key] (key = hi << lo_bits | region; first_index via
+ * and counts[key] (key = hi << lo_bits | digit; first_index via
  * smx_counts_to_offsets).  rcap_host: host copy of the capacities. */
-int smx_fused_sort(const uint32_t* region, const uint64_t* rstart, const uint64_t* fill, const uint64_t* rcap_host,
+int smx_fused_sort(const uint64_t* rptr, const uint64_t* fill, const uint64_t* rcap_host, int per_digit,
                    int lo_bits, int hi_bits, int pbits, int row_bits, const uint32_t* cls_map, uint32_t* counts,
                    uint64_t n_keys, uint64_t n_records, uint32_t* out, int* err, void* stream);
 /* ConnectionStore.finalize: stable sort of pending records by source. */

@@ -356,12 +356,12 @@ constexpr int FB_TILE = FB_THREADS * FB_IPT;   // 3840 records
 constexpr int FB_TC = 256;                     // tiles per scan chunk (chunks never straddle regions)
 
 struct FusedSort {
-  const uint32_t* region;
-  const uint64_t* rstart;     // [R] region start slots
+  const uint64_t* rptr;       // [R] region base pointers, regions in (low digit, call) order
   const uint64_t* fill;       // [R] records per region
   const uint32_t* tile_first; // [R + 1] first tile of each region
   const uint32_t* chunk_first;// [R + 1] first scan chunk of each region
   uint32_t n_regions;
+  uint32_t per_digit;         // regions per low digit (one per call)
   int pbits;                  // record = hi << pbits | class index << row_bits | row
   int row_bits;
   int lo_bits;                // key = hi << lo_bits | region
@@ -383,16 +383,16 @@ __device__ __forceinline__ uint32_t upper_region(const uint32_t* first, uint32_t
 }
 
 struct FbTile {
+  const uint32_t* src;  // first record
   uint32_t region;
-  uint64_t a;     // first slot
-  uint32_t n;     // records in the tile
+  uint32_t n;           // records in the tile
 };
 
 __device__ __forceinline__ FbTile fb_tile(const FusedSort& s, uint32_t T) {
   FbTile x;
   x.region = upper_region(s.tile_first, s.n_regions, T);
   const uint64_t local = (uint64_t)(T - __ldg(s.tile_first + x.region)) * FB_TILE;
-  x.a = __ldg(s.rstart + x.region) + local;
+  x.src = reinterpret_cast<const uint32_t*>(__ldg(s.rptr + x.region)) + local;
   const uint64_t f = __ldg(s.fill + x.region);
   x.n = f > local ? (f - local < (uint64_t)FB_TILE ? (uint32_t)(f - local) : (uint32_t)FB_TILE) : 0u;
   return x;
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(1024) fb_hist_kernel(const __grid_constant__ F
     for (int j = lane; j < BINS; j += 32) wh[j] = 0;
     __syncwarp();
     const FbTile x = fb_tile(s, T);
-    const uint32_t* src = s.region + x.a;
+    const uint32_t* src = x.src;
     const uint32_t nq = x.n / 4;
     for (uint32_t i = lane; i < nq; i += 32) {
       const uint4 q = __ldcs(reinterpret_cast<const uint4*>(src) + i);
@@ -464,9 +464,9 @@ __global__ void __launch_bounds__(256) fb_region_sum_kernel(const __grid_constan
     uint32_t acc = 0;
     for (uint32_t C = c0; C < c1; ++C) acc += csum[(size_t)C * BINS + d];
     rsum[(size_t)r * BINS + d] = acc;
-    const uint64_t key = ((uint64_t)d << s.lo_bits) | r;
+    const uint64_t key = ((uint64_t)d << s.lo_bits) | (r / s.per_digit);
     if (acc) {
-      if (key < s.n_keys) s.counts[key] = acc;
+      if (key < s.n_keys) atomicAdd(s.counts + key, acc);  // one region per call of the digit
       else atomicExch(s.err, 6);
     }
   }
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
     const bool full = x.n == FB_TILE;
     mbar_expect_tx(&bar, BINS * 4 + (full ? FB_TILE * 4 : 0));
     bulk_g2s(ioff, off + (size_t)T * BINS, BINS * 4, &bar);
-    if (full) bulk_g2s(irec, s.region + x.a, FB_TILE * 4, &bar);
+    if (full) bulk_g2s(irec, x.src, FB_TILE * 4, &bar);
   };
   if (tid == 0) {
     take(0);
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
 #pragma unroll
     for (int i = 0; i < FB_IPT; ++i) {
       const uint32_t q = wofs + i * 32;
-      rec[i] = full ? irec[q] : (q < x.n ? s.region[x.a + q] : FG_SENTINEL);
+      rec[i] = full ? irec[q] : (q < x.n ? x.src[q] : FG_SENTINEL);
     }
     {
       uint32_t* w32 = reinterpret_cast<uint32_t*>(mycnt);
@@ -836,13 +836,14 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
   return rc;
 }
 
-// Pass B: stable sort of the digit regions by the high digit.  Region r
-// (r < 2^lo_bits) holds fill[r] records from slot rstart[r] (device arrays);
-// rcap_host (host, the regions' capacities) fixes the tile layout.  Writes
-// out[] (payloads sorted by key = hi << lo_bits | r) and counts[key] (zeroed
-// first).  err receives 6 for a key >= n_keys.
-extern "C" int smx_fused_sort(const uint32_t* region, const uint64_t* rstart, const uint64_t* fill,
-                              const uint64_t* rcap_host, int lo_bits, int hi_bits, int pbits, int row_bits,
+// Pass B: stable sort of the digit regions by the high digit.  Region
+// r = digit * per_digit + call holds fill[r] records at rptr[r] (device
+// arrays; every call wrote its own regions in pass A); rcap_host (host, the
+// regions' capacities) fixes the tile layout.  Writes out[] (payloads sorted
+// by key = hi << lo_bits | digit) and counts[key] (zeroed first).  err
+// receives 6 for a key >= n_keys, 7 when a digit holds >= 2^32 records.
+extern "C" int smx_fused_sort(const uint64_t* rptr, const uint64_t* fill, const uint64_t* rcap_host, int per_digit,
+                              int lo_bits, int hi_bits, int pbits, int row_bits,
                               const uint32_t* cls_map, uint32_t* counts, uint64_t n_keys, uint64_t n_records,
                               uint32_t* out, int* err, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -851,7 +852,11 @@ extern "C" int smx_fused_sort(const uint32_t* region, const uint64_t* rstart, co
     smx_set_error("smx_fused_sort: high digit of %d bits (8..11 supported)", hi_bits);
     return -1;
   }
-  const uint32_t R = 1u << lo_bits;
+  if (per_digit < 1) {
+    smx_set_error("smx_fused_sort: no regions");
+    return -1;
+  }
+  const uint32_t R = (uint32_t)per_digit << lo_bits;
   std::vector<uint32_t> firsts(2 * (R + 1));
   uint32_t* tile_first = firsts.data();
   uint32_t* chunk_first = firsts.data() + R + 1;
@@ -873,12 +878,12 @@ extern "C" int smx_fused_sort(const uint32_t* region, const uint64_t* rstart, co
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&dfirst, sizeof(uint32_t) * firsts.size(), st));
   SMX_CUDA_CHECK(cudaMemcpyAsync(dfirst, firsts.data(), sizeof(uint32_t) * firsts.size(), cudaMemcpyHostToDevice, st));
   FusedSort s{};
-  s.region = region;
-  s.rstart = rstart;
+  s.rptr = rptr;
   s.fill = fill;
   s.tile_first = dfirst;
   s.chunk_first = dfirst + R + 1;
   s.n_regions = R;
+  s.per_digit = (uint32_t)per_digit;
   s.pbits = pbits;
   s.row_bits = row_bits;
   s.lo_bits = lo_bits;

@@ -280,7 +280,7 @@ class _Rank:
         # buffers, in call order (fused_ok then stays False)
         self.deferred: list[dict] = []
         self.fused_ok = True
-        self.fgen = None   # fused-path buffers between pass B and the prepare check
+        self.fz = None     # fused-path session: record format and every call's digit regions
 
     @property
     def stream(self):
@@ -715,11 +715,16 @@ class Cluster:
         return n, src
 
     def _defer(self, st: _Rank, key, ex, n, kmode, ktab, pay_tab, kdiv, n_tgt, cls, src_host=None, acct=None):
+        """Register a fixed in-degree draw for the fused path and launch its
+        pass A; when the record format cannot take it, every deferred call
+        (this one included) goes through the general path instead."""
         lm_thr = 0 if ex == (1 << 32) else ((1 << 32) - ex) % ex
-        st.deferred.append(dict(key=key, ex=int(ex), n=int(n), kmode=kmode, ktab=ktab, pay_tab=pay_tab, cls=int(cls),
-                                kdiv=int(kdiv), n_tgt=int(n_tgt), src_host=src_host, acct=acct,
-                                prej=lm_thr / 4294967296.0))
-        return st.deferred[-1]
+        d = dict(key=key, ex=int(ex), n=int(n), kmode=kmode, ktab=ktab, pay_tab=pay_tab, cls=int(cls),
+                 kdiv=int(kdiv), n_tgt=int(n_tgt), src_host=src_host, acct=acct, prej=lm_thr / 4294967296.0)
+        st.deferred.append(d)
+        if not self._fused_eager(st, d):
+            self._fused_off(st)
+        return d
 
     def _validate_conn(self, rank, sources, targets, conn, syn, what="connect"):
         sources = np.asarray(sources, dtype=np.int64)
@@ -1194,10 +1199,10 @@ class Cluster:
         call("smx_pay_table", _ptr(tgt), len(tg), _ptr(st.node2row.t), st.node2row.n,
              0 if cls is None else cls, _ptr(pay_tab), sk)
         if defer:
-            # generated at prepare, fused with the sort's first pass
-            d = self._defer(st, key, total, n, 3, pieces, pay_tab, k_in, len(tg), cls)
-            self._dist_accounting(st, tr, group, n, 0, present, runs, pieces, False, lut_base, vbase, seg_words,
-                                  deferred=d)
+            # pass A now (fused with the draw), pass B at prepare
+            acct = self._dist_accounting(st, tr, group, n, 0, present, runs, pieces, False, lut_base, vbase,
+                                         seg_words, deferred=True)
+            self._defer(st, key, total, n, 3, pieces, pay_tab, k_in, len(tg), cls, acct=acct)
             return vbits, present
         base = st.reserve_records(n)
         vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
@@ -1301,7 +1306,7 @@ class Cluster:
         remote = [r for r in present if r != tr]
         if not remote:
             st.mem.later("store_append", n)
-            return
+            return None
         # records per source rank: disjoint key ranges of the call's records,
         # counted on the preparation side stream (memory-bound, it overlaps the
         # next call's compute-bound draws)
@@ -1325,12 +1330,11 @@ class Cluster:
                 his.append(TMP_KEY | (lut_base + (sw0 + snw) * 32))
                 owner.append(r)
         rng = np.array([len(los)] + los + his, dtype=np.uint64).astype(np.uint32)
-        if deferred is not None:  # counted once the records exist (prepare)
+        if deferred:  # counted once the records are sorted (prepare): returns (ranges, counts)
             cnt = torch.zeros(len(los), dtype=torch.int64, device=st.device)
-            deferred["acct"] = (rng, cnt)
             sizes = torch.stack([_popcount_dev(st.maps[(int(group), r)].present.view()) for r in remote])
             st.mem.later("dist_batches", tr, int(group), list(present), owner, cnt, sizes)
-            return
+            return rng, cnt
         main = torch.cuda.current_stream(st.device)
         side = _prep_stream(st.device)
         side.wait_stream(main)
@@ -1517,11 +1521,11 @@ class Cluster:
         # sort the store first (sm/core.py:299-324): it is the long kernel
         # sequence, and everything below up to the first_index check is host
         # work or independent small kernels that overlap it on a side stream
-        plan = self._fused_plan(st) if st.deferred and st.fused_ok else None
-        if st.deferred and st.fused_ok and plan is None:
-            self._fused_off(st)   # not representable in packed records: general path
-        if plan is not None:
-            self._fused_run(st, plan)
+        fused = self._fused_ready(st)
+        if st.deferred and st.fused_ok and not fused:
+            self._fused_off(st)   # the regions cannot be sorted in one pass B: general path
+        if fused:
+            self._fused_sort(st)
             sorted_state = None
         else:
             sorted_state = self._sort_pending(st)
@@ -1532,7 +1536,7 @@ class Cluster:
         main.wait_stream(side)
         _record_stream(st.__dict__, main)  # side-stream allocations are used on main
         check(_lib.lib().smx_check_device_errors(sk), "construction")  # asynchronous draws
-        if plan is not None and not self._fused_check(st):
+        if fused and not self._fused_check(st):
             # a digit region overflowed or a raw window was short (both ~never):
             # regenerate every deferred call into the pending buffers and sort
             self._fused_off(st)
@@ -1550,7 +1554,7 @@ class Cluster:
         st.keys = st.vals = None
         st.w_rows = st.w_w = st.w_meta = None
         st.lut = None
-        st.fgen = None
+        st.fz = None
         st.deferred = []
         fi = st.first_index
         max_len = int((fi[1:] - fi[:-1]).max().item()) if st.n_nodes else 0
@@ -1607,6 +1611,7 @@ class Cluster:
         if not st.fused_ok:
             return
         st.fused_ok = False
+        st.fz = None   # regions of pass A (if any) are dropped
         for d in st.deferred:
             self._gen_deferred(st, d)
         st.deferred = []
@@ -1660,120 +1665,137 @@ class Cluster:
                     np.add.at(cnt, (a + np.arange(rem)) & (B - 1), 1.0)
         return cnt / float(d["ex"])
 
-    def _fused_plan(self, st: _Rank):
-        """Digit split and region capacities of the fused path, or None when
-        the records do not fit the packed format (general path)."""
-        calls = st.deferred
+    def _fused_eager(self, st: _Rank, d: dict) -> bool:
+        """Pass A of one deferred call, launched at call time (it overlaps the
+        host work of the calls that follow): the call's draws ranked by the
+        low key digit into its own digit regions (csrc/fused.cu).  The record
+        format (digit split, row / class bits) is fixed by the rank's first
+        call; False when this call does not fit it."""
+        z = st.fz
+        dev, sk = st.device, st.stream
+        if z is None:
+            key_bits = max(1, int(st.n_nodes - 1).bit_length())
+            env_lo = os.environ.get("SMX_FUSED_LO")
+            lo = int(env_lo) if env_lo is not None else (
+                0 if key_bits <= 11 else max(key_bits - 11, min(9, key_bits - 8)))
+            row_bits = max(1, int(st.n_real - 1).bit_length())
+            cls_bits = min(8, 20 - row_bits)   # keeps hi (<= 11 bits) + payload within 31 bits
+            if lo > 9 or cls_bits < 0:
+                return False
+            z = st.fz = dict(lo=lo, row_bits=row_bits, cls_bits=cls_bits, pbits=row_bits + cls_bits, cidx={},
+                             calls=[], flag=torch.zeros(2, dtype=torch.int64, device=dev))
+        if st.n_real > (1 << z["row_bits"]):
+            return False
+        if d["cls"] not in z["cidx"]:
+            if len(z["cidx"]) >= (1 << z["cls_bits"]):
+                return False
+            z["cidx"][d["cls"]] = len(z["cidx"])
+        B = 1 << z["lo"]
+        p = self._digit_probs(d, B)
+        n = float(d["n"])
+        # the raw window's slack (accepted draws past the last record) lands
+        # in the regions too
+        slack = 1.25 * n * d["prej"] + 12.0 * math.sqrt(n * d["prej"] + 1.0) + 64.0
+        if (n + slack) * float(p.max()) * 1.05 + 1e4 >= (1 << 30):
+            return False   # look-back descriptors hold 30-bit counts
+        cap = np.ceil((n + slack) * p + 8.0 * np.sqrt(n * p * (1.0 - p)) + 64.0).astype(np.int64)
+        cap = (cap + 31) // 32 * 32
+        rstart = np.zeros(B, dtype=np.int64)
+        rstart[1:] = np.cumsum(cap)[:-1]
+        slots = int(rstart[-1] + cap[-1])
+        region = torch.empty(slots, dtype=torch.int32, device=dev)
+        meta = _up(np.concatenate([rstart, cap]), dev)
+        fills = torch.zeros((2, B), dtype=torch.int64, device=dev)
+        total = torch.zeros(1, dtype=torch.int64, device=dev)
+        cpay = (d["pay_tab"] & ROW_MASK) | (z["cidx"][d["cls"]] << z["row_bits"])   # row | class index
+        ev0 = self._event(st) if self.prof is not None else None
+        ktab = d["ktab"].ctypes.data if d["kmode"] == 3 else _ptr(d["ktab"])
+        call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"], _ptr(cpay),
+             z["lo"], z["pbits"], _ptr(region), slots, _ptr(meta[:B]), _ptr(meta[B:]), _ptr(fills[0]),
+             _ptr(fills[1]), _ptr(total), _ptr(z["flag"]), sk)
+        if self.prof is not None:
+            self.prof["gen"].append((ev0, self._event(st)))
+        z["calls"].append(dict(region=region, rstart=rstart, cap=cap.astype(np.uint64), meta=meta, fill=fills[1],
+                               fills=fills, total=total, cpay=cpay, n=int(d["n"])))
+        return True
+
+    def _fused_ready(self, st: _Rank) -> bool:
+        """At prepare: can pass B take the rank's regions (the high digit fits
+        11 bits with the final node count; accounted calls own their keys)?"""
+        z = st.fz
+        if z is None or not st.fused_ok or not st.deferred:
+            return False
         key_bits = max(1, int(st.n_nodes - 1).bit_length())
-        env_lo = os.environ.get("SMX_FUSED_LO")
-        if env_lo is not None:
-            lo = int(env_lo)
-        else:
-            lo = 0 if key_bits <= 11 else max(key_bits - 11, min(9, key_bits - 8))
-        hi = max(8, key_bits - lo)
-        if lo > 9 or hi > 11:
-            return None
-        # records carry the compact payload: target row | class index << row bits
-        row_bits = max(1, int(st.n_real - 1).bit_length())
-        cls_ids = sorted({d["cls"] for d in calls})
-        cls_bits = int(len(cls_ids) - 1).bit_length()
-        pbits = row_bits + cls_bits
-        if hi + pbits > 31 or cls_bits > 8:
-            return None
-        # record counts per source rank of distributed calls (modeled bytes)
-        # come from the per-key counts: every accounted call's keys must be
-        # its own
+        z["hi"] = max(8, key_bits - z["lo"])
+        if z["hi"] > 11 or z["hi"] + z["pbits"] > 31:
+            return False
+        # records per source rank of distributed calls (modeled bytes) come
+        # from the per-key counts: every accounted call's keys must be its own
+        calls = st.deferred
         acct = [i for i, d in enumerate(calls) if d["acct"] is not None]
         if acct:
             rngs = [self._call_key_ranges(d) for d in calls]
             for i in acct:
                 for j, rj in enumerate(rngs):
                     if j != i and any(a < y and x < b for a, b in rngs[i] for x, y in rj):
-                        return None
-        B = 1 << lo
-        exp = np.zeros(B)
-        var = np.zeros(B)
-        for d in calls:
-            p = self._digit_probs(d, B)
-            n = float(d["n"])
-            # the raw window's slack (accepted draws past the last record)
-            # lands in the regions too
-            slack = 1.25 * n * d["prej"] + 12.0 * math.sqrt(n * d["prej"] + 1.0) + 64.0
-            if (n + slack) * float(p.max()) * 1.05 + 1e4 >= (1 << 30):
-                return None   # look-back descriptors hold 30-bit counts
-            exp += (n + slack) * p
-            var += n * p * (1.0 - p)
-        cap = np.ceil(exp + 8.0 * np.sqrt(var) + 64.0).astype(np.int64)
-        cap = (cap + 31) // 32 * 32
-        return dict(lo=lo, hi=hi, pbits=pbits, row_bits=row_bits, cls_ids=cls_ids, cap=cap.astype(np.uint64))
+                        return False
+        return True
 
-    def _fused_run(self, st: _Rank, plan: dict):
-        """Pass A per deferred call into the digit regions, then pass B (csrc/fused.cu)."""
+    def _fused_sort(self, st: _Rank):
+        """Pass B over every call's regions, in (low digit, call) order: the
+        store's payloads, per-key counts and first_index (csrc/fused.cu)."""
         dev, sk = st.device, st.stream
-        calls = st.deferred
-        lo, B = plan["lo"], 1 << plan["lo"]
-        cap = plan["cap"]
-        rstart = np.zeros(B, dtype=np.int64)
-        rstart[1:] = np.cumsum(cap.astype(np.int64))[:-1]
-        slots = int(rstart[-1] + cap[-1])
-        n = sum(d["n"] for d in calls)
+        z = st.fz
+        calls = z["calls"]
+        C, B = len(calls), 1 << z["lo"]
+        rptr = np.empty((B, C), dtype=np.int64)
+        rcap = np.empty((B, C), dtype=np.uint64)
+        for c, zc in enumerate(calls):
+            rptr[:, c] = zc["region"].data_ptr() + 4 * zc["rstart"]
+            rcap[:, c] = zc["cap"]
+        rptr_t = _up(rptr.reshape(-1), dev)
+        rcap = np.ascontiguousarray(rcap.reshape(-1))
+        fill = torch.stack([zc["fill"] for zc in calls], dim=1).reshape(-1).contiguous()
+        n = sum(zc["n"] for zc in calls)
         st.n_records = n
-        region = torch.empty(max(slots, 1), dtype=torch.int32, device=dev)
-        meta = _up(np.concatenate([rstart, cap.astype(np.int64)]), dev)
-        rs_t, rc_t = meta[:B], meta[B:]
-        fills = torch.zeros((2, B), dtype=torch.int64, device=dev)
-        flags = torch.zeros(2 + len(calls), dtype=torch.int64, device=dev)   # overflow, err, totals
-        ev0 = self._event(st) if self.prof is not None else None
-        cidx = {c: i for i, c in enumerate(plan["cls_ids"])}
-        cpays = []
-        for i, d in enumerate(calls):
-            # compact payload per target: row | class index << row bits
-            cpay = (d["pay_tab"] & ROW_MASK) | (cidx[d["cls"]] << plan["row_bits"])
-            cpays.append(cpay)
-            ktab = d["ktab"].ctypes.data if d["kmode"] == 3 else _ptr(d["ktab"])
-            call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"],
-                 _ptr(cpay), lo, plan["pbits"], _ptr(region), slots, _ptr(rs_t), _ptr(rc_t),
-                 _ptr(fills[i % 2]), _ptr(fills[(i + 1) % 2]), _ptr(flags[2 + i:]), _ptr(flags), sk)
-        if self.prof is not None:
-            self.prof["gen"].append((ev0, self._event(st)))
-            ev0 = self._event(st)
         cls_map = np.zeros(256, dtype=np.uint32)
-        cls_map[: len(plan["cls_ids"])] = np.array(plan["cls_ids"], dtype=np.uint32) << 24
+        for cls, i in z["cidx"].items():
+            cls_map[i] = np.uint32(cls) << np.uint32(24)
         cls_map_t = _up(cls_map.view(np.int32), dev)
         st.counts = torch.empty(max(st.n_nodes, 1), dtype=torch.int32, device=dev)
         st.payload = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        call("smx_fused_sort", _ptr(region), _ptr(rs_t), _ptr(fills[len(calls) % 2]), cap.ctypes.data, lo,
-             plan["hi"], plan["pbits"], plan["row_bits"], _ptr(cls_map_t), _ptr(st.counts), st.n_nodes, n,
-             _ptr(st.payload), _ptr(flags[1:]), sk)
+        ev0 = self._event(st) if self.prof is not None else None
+        call("smx_fused_sort", _ptr(rptr_t), _ptr(fill), rcap.ctypes.data, C, z["lo"], z["hi"], z["pbits"],
+             z["row_bits"], _ptr(cls_map_t), _ptr(st.counts), st.n_nodes, n, _ptr(st.payload), _ptr(z["flag"][1:]), sk)
         st.first_index = torch.empty(st.n_nodes + 1, dtype=torch.int64, device=dev)
         call("smx_counts_to_offsets", _ptr(st.counts), st.n_nodes, _ptr(st.first_index), sk)
         if self.prof is not None:
             self.prof["sort"].append((ev0, self._event(st)))
         st.ww = st.wm = None
+        st.store_path = "fused"
         # records per source rank of accounted distributed calls: sums of the
         # per-key counts over the call's key ranges (keys are the call's own)
         cs = None
-        for d in calls:
+        for d in st.deferred:
             if d["acct"] is None:
                 continue
             if cs is None:
                 cs = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), torch.cumsum(st.counts.long(), 0)])
             rng, cnt = d["acct"]
             m = int(rng[0])
-            los = torch.from_numpy(rng[1: 1 + m].astype(np.int64)).to(dev)
-            his = torch.from_numpy(rng[1 + m: 1 + 2 * m].astype(np.int64)).to(dev)
-            los = los.clamp(max=st.n_nodes)
-            his = his.clamp(max=st.n_nodes)
+            los = torch.from_numpy(rng[1: 1 + m].astype(np.int64)).to(dev).clamp(max=st.n_nodes)
+            his = torch.from_numpy(rng[1 + m: 1 + 2 * m].astype(np.int64)).to(dev).clamp(max=st.n_nodes)
             cnt.copy_(cs[his] - cs[los])
-        st.store_path = "fused"
-        st.fgen = dict(region=region, meta=meta, fills=fills, flags=flags, cpays=cpays, cls_map=cls_map_t,
-                        want=np.array([d["n"] for d in calls], dtype=np.int64))
+        z["keep"] = (rptr_t, fill, cls_map_t)
 
     def _fused_check(self, st: _Rank) -> bool:
-        f = st.fgen["flags"].cpu().numpy()
+        z = st.fz
+        f = z["flag"].cpu().numpy()
         if int(f[1]):
             raise ConsistencyError(f"fused sort: device error {int(f[1])}")
-        return not int(f[0]) and bool((f[2:] >= st.fgen["want"]).all())
+        totals = torch.cat([zc["total"] for zc in z["calls"]]).cpu().numpy()
+        want = np.array([zc["n"] for zc in z["calls"]], dtype=np.int64)
+        return not int(f[0]) and bool((totals >= want).all())
 
     def _prepare_tables(self, st: _Rank):
         """Everything of prepare that does not read the sorted store: neuron

@@ -128,19 +128,21 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
   extern __shared__ __align__(16) uint8_t fg_smem[];
   uint32_t* xs = reinterpret_cast<uint32_t*>(fg_smem);               // [FG_XS] keys, then staged records
   uint64_t* delta = reinterpret_cast<uint64_t*>(xs + FG_XS);         // [B]
-  uint32_t* tstart = reinterpret_cast<uint32_t*>(delta + B);         // [B]
-  uint16_t* sd = reinterpret_cast<uint16_t*>(tstart + B);            // [FG_TILE] digit of each staged record
+  uint32_t* hist = reinterpret_cast<uint32_t*>(delta + B);           // [B] tile digit counts
+  uint16_t* sd = reinterpret_cast<uint16_t*>(hist + B);              // [FG_TILE] digit of each staged record
   uint16_t* wcnt = sd + FG_TILE;                                     // [FG_WARPS][BC]
   __shared__ uint32_t ws[32];
   __shared__ uint32_t wacc[FG_WARPS];
   __shared__ unsigned long long wred[FG_WARPS];
   __shared__ uint32_t s_t;
   __shared__ uint32_t s_tq, s_tr, s_lim;  // target index / remainder of the tile's first draw, records left
+  __shared__ uint32_t s_cp[2];            // k_in >= tile: the (at most two) targets of the tile
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = (1u << lane) - 1;
   uint16_t* mycnt = wcnt + warp * BC;
   for (;;) {
     if (tid == 0) s_t = atomicAdd(g.ticket, 1u);
+    if (tid < B) hist[tid] = 0;
     __syncthreads();
     const uint32_t t = s_t;
     if (t >= n_tiles) break;
@@ -168,8 +170,24 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     const uint32_t* xr = xs + warp * (33 * FG_IPT) + lane;
 #pragma unroll
     for (int i = 0; i < FG_IPT; ++i) k[i] = xr[33 * i];
+    // the tile's digit counts first, published before the (longer) ranking
+    // so that successors' look-backs rarely wait on this tile
+#pragma unroll
+    for (int i = 0; i < FG_IPT; ++i) {
+      if (LB == 0) {
+        const uint32_t vm = __ballot_sync(0xffffffffu, k[i] != FG_NOKEY);
+        if (lane == 0 && vm) atomicAdd(hist, (uint32_t)__popc(vm));
+      } else if (k[i] != FG_NOKEY) {
+        atomicAdd(hist + (k[i] & DM), 1u);
+      }
+    }
     for (int j = lane; j < BC / 2; j += 32) reinterpret_cast<uint32_t*>(mycnt)[j] = 0;
-    __syncwarp();
+    __syncthreads();
+    uint32_t c = 0;
+    if (tid < B) {
+      c = hist[tid];
+      st_vol(g.status + (size_t)t * B + tid, (t == 0 ? ST_P : ST_A) | c);
+    }
     uint32_t rank2[FG_IPT / 2];
     uint32_t run = 0;
 #pragma unroll
@@ -187,13 +205,7 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       if (LB == 0) mycnt[0] = (uint16_t)run;
     }
     __syncthreads();  // counters complete; xs is free
-    // 3. per digit: tile count (published at once), tile start, per-warp bases
-    uint32_t c = 0;
-    if (tid < B) {
-#pragma unroll
-      for (int w = 0; w < FG_WARPS; ++w) c += wcnt[w * BC + tid];
-      st_vol(g.status + (size_t)t * B + tid, (t == 0 ? ST_P : ST_A) | c);
-    }
+    // 3. per digit: tile start, per-warp bases
     uint32_t tot;
     const uint32_t ts = block_excl_scan(tid < B ? c : 0u, ws, tot);
     if (tid < B) {  // wcnt[w][d] = staging position of warp w's first record of digit d
@@ -208,7 +220,6 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     // 4. look-back: records of this digit in earlier tiles of the call
     uint64_t excl = 0;
     if (tid < B) {
-      tstart[tid] = ts;
       if (t > 0) {
         // walk back 4 descriptors per step (independent loads): a tile
         // usually finds an inclusive prefix within the first few
@@ -261,11 +272,18 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       s_tq = (uint32_t)tq;
       s_tr = (uint32_t)(jbase - tq * g.kdiv);
       s_lim = jbase >= g.n_out ? 0u : (g.n_out - jbase > 0xffffffffull ? 0xffffffffu : (uint32_t)(g.n_out - jbase));
+      if (g.kdiv >= FG_TILE) {
+        const uint64_t n_tgt = (g.n_out + g.kdiv - 1) / g.kdiv;
+        s_cp[0] = tq < n_tgt ? __ldg(g.cpay + tq) : 0u;
+        s_cp[1] = tq + 1 < n_tgt ? __ldg(g.cpay + tq + 1) : 0u;
+      }
       if (t == n_tiles - 1) *g.total = jbase + tot;
     }
     __syncthreads();
     // 5. records, staged in digit order (accept ranks recomputed: fewer live registers)
     const uint32_t tq = s_tq, tr = s_tr, left = s_lim;
+    const bool bigk = g.kdiv >= FG_TILE;   // j / k_in takes two values in a tile
+    const uint32_t cp0 = s_cp[0], cp1 = s_cp[1], kth = g.kdiv - tr;
     uint32_t aw = (uint32_t)wbase;
 #pragma unroll
     for (int i = 0; i < FG_IPT; ++i) {
@@ -275,8 +293,8 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
       if (r == 0xffffu) continue;
       const uint32_t d = LB ? (k[i] & DM) : 0u;
-      const uint32_t rec =
-          a < left ? (((k[i] >> LB) << g.pbits) | __ldg(g.cpay + tq + g.kd.div(tr + a))) : FG_SENTINEL;
+      const uint32_t cp = bigk ? (a >= kth ? cp1 : cp0) : __ldg(g.cpay + tq + g.kd.div(tr + a));
+      const uint32_t rec = a < left ? (((k[i] >> LB) << g.pbits) | cp) : FG_SENTINEL;
       const uint32_t pos = wcnt[warp * BC + d] + r;
       xs[pos] = rec;
       sd[pos] = (uint16_t)d;

@@ -103,15 +103,12 @@ def test_fused_overflow_falls_back(monkeypatch):
     """Regions too small for the draws: the overflow flag sends the rank
     through the general path, with identical tables."""
     from paper_2512_09502_b200.engine import Cluster
-    real = Cluster._fused_plan
+    real = Cluster._digit_probs
 
-    def tiny(self, st):
-        p = real(self, st)
-        if p is not None:
-            p["cap"] = (p["cap"] // 3 // 32 * 32).astype(np.uint64)
-        return p
+    def tiny(d, B):
+        return real(d, B) / 3.0   # regions sized for a third of the draws
     g = _build(False, CASES["balanced_1r"])
-    monkeypatch.setattr(Cluster, "_fused_plan", tiny)
+    monkeypatch.setattr(Cluster, "_digit_probs", staticmethod(tiny))
     f = _build(True, CASES["balanced_1r"])
     assert f.ranks[0].store_path == "general"
     assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))

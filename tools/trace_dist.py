@@ -19,6 +19,7 @@ cfg = api.SimConfig(n_ranks=world, comm_mode="collective" if world > 1 else "p2p
 
 
 def build():
+    torch.zeros(1, device="cuda")  # marks the start of the construction on the GPU timeline
     c = engine.Cluster(cfg)
     models.build_balanced_network(c, P)
     c.prepare()
@@ -52,7 +53,7 @@ if rank == 0:
         ops = [e["name"] for e in cpu if e["ts"] <= at + g / 2 <= e["ts"] + e["dur"]]
         print(f"  gap {1e-3 * g:6.3f} ms at {1e-3 * (at - t0):7.2f} ms before {n[:40]:40s} cpu: {ops[-3:]}")
     if os.environ.get("STACK"):  # host functions (>= 30 us) before the first generation launch
-        first = min((a for a, b, n in gpu if "draw_" in n), default=t1)
+        first = min((a for a, b, n in gpu if "draw_" in n or "fused_gen" in n), default=t1)
         for e in sorted(cpu, key=lambda e: e["ts"]):
             if e["ts"] < first and e["dur"] >= 30 and e.get("cat") == "python_function":
                 print(f"  host {1e-3 * (e['ts'] - t0):7.2f} +{1e-3 * e['dur']:6.3f} ms  {e['name'][:90]}")

@@ -1544,6 +1544,9 @@ class Cluster:
         n = st.n_records
         if n and int(st.first_index[-1].item()) != n:
             raise ConsistencyError(f"record source beyond node count {n_nodes}")
+        for d in st.devices:
+            if d.get("rows_ok") is not None and not bool(d["rows_ok"]):
+                raise ValueError("poisson targets must be real neurons")
         # modeled bytes of construction + prepare (sm/construction.py:763-807);
         # record counts of deferred calls exist only now
         st.mem.resolve()
@@ -1805,19 +1808,26 @@ class Cluster:
         # neuron state, real rows only (sm/dynamics.py:153-189)
         N = st.n_real
         st.N = N
-        prm = np.concatenate(st.row_param) if st.row_param else np.empty(0, np.int32)
+        # per-row parameters gathered on the device from the (small) table of
+        # distinct LifParams; decay = exp(-dt / tau) from the host (glibc)
         tab = np.array([[math.exp(-dt / p.tau_m), p.v_rest, p.v_reset, p.v_th, p.i_e] for p in self.params] or
                        [[0.0] * 5], dtype=np.float64)
         rs = np.array([int(round(p.t_ref / dt)) for p in self.params] or [0], dtype=np.int32)
-        f64 = lambda a: _up(np.ascontiguousarray(a), dev)  # noqa: E731
-        st.decay, st.v_rest, st.v_reset, st.v_th, st.i_e = (f64(tab[prm, j]) for j in range(5))
-        st.ref_steps = f64(rs[prm])
+        pid = [(int(p[0]), len(p)) for p in st.row_param]
+        prm = (torch.cat([torch.full((k,), i, dtype=torch.int64, device=dev) for i, k in pid]) if pid
+               else torch.zeros(0, dtype=torch.int64, device=dev))
+        tab_t = _up(np.ascontiguousarray(tab.T), dev)
+        st.decay, st.v_rest, st.v_reset, st.v_th, st.i_e = (tab_t[j][prm].contiguous() for j in range(5))
+        st.ref_steps = _up(rs, dev)[prm].contiguous()
         st.v = torch.cat(st.v0) if st.v0 else torch.empty(0, dtype=torch.float64, device=dev)
         st.ref = torch.zeros(N, dtype=torch.int32, device=dev)
         st.row2node_np = np.concatenate(st.row2node) if st.row2node else np.empty(0, np.int64)
-        st.row2node_t = _up(st.row2node_np.astype(np.int32), dev)
+        st.row2node_t = (torch.cat([torch.arange(int(r[0]), int(r[0]) + len(r), dtype=torch.int32, device=dev)
+                                    for r in st.row2node]) if st.row2node
+                         else torch.zeros(0, dtype=torch.int32, device=dev))
         st.gid_np = np.concatenate(st.row_gid) if st.row_gid else np.empty(0, np.int64)
-        st.gid_t = _up(st.gid_np, dev)
+        st.gid_t = (torch.cat([_up_index(g, dev) for g in st.row_gid]) if st.row_gid
+                    else torch.zeros(0, dtype=torch.int64, device=dev))
         st.ring = torch.zeros(st.L * st.P * max(N, 1), dtype=torch.float64, device=dev)
         st.cls_w, cm = self._class_tables(dev)
         cmn = cm.cpu().numpy().view(np.uint32)
@@ -1942,10 +1952,11 @@ class Cluster:
         st.pois_steps = B * max(1, -(-max_pd // B))
         for d in st.devices:
             nt = len(d["targets"])
-            rows = np.asarray(st_node2row_host(st, d["targets"]), dtype=np.int64)
-            if (rows < 0).any():
-                raise ValueError("poisson targets must be real neurons")
-            d["rows"] = _up(rows.astype(np.int32), dev)
+            # node -> row on the device (no host copy of the node map)
+            tg = _up_index(d["targets"], dev)
+            rows = st.node2row.t[tg] if len(d["targets"]) else torch.empty(0, dtype=torch.int32, device=dev)
+            d["rows"] = rows.to(torch.int32)
+            d["rows_ok"] = (rows >= 0).all() if len(d["targets"]) else None
             d["nt"] = nt
             d["active"] = nt > 0 and d["lam"] != 0.0
             if not d["active"]:
@@ -1962,16 +1973,17 @@ class Cluster:
             d["batch0"] = -1
         # fused step path: every active device hits each row at most once
         act = [d for d in st.devices if d["active"]]
-        st.fused = len(act) <= 8 and all(_all_distinct(d["rows"].cpu().numpy()) for d in act)
+        # rows are distinct iff the targets are (node -> row is injective on real neurons)
+        st.fused = len(act) <= 8 and all(_all_distinct(np.asarray(d["targets"])) for d in act)
         st.ctr = torch.zeros(2, dtype=torch.int64, device=dev)
         # multi-step LIF blocks: every record delay >= block length (Poisson
         # devices are applied by their target row's own thread)
         st.block_ok = st.min_delay is None or st.min_delay >= B
         st.fdev = (ctypes_fdev * max(len(act), 1))()
         for k, d in enumerate(act):
-            inv = np.full(max(N, 1), -1, dtype=np.int32)
-            inv[d["rows"].cpu().numpy()] = np.arange(d["nt"], dtype=np.int32)
-            d["inv"] = _up(inv, dev)
+            inv = torch.full((max(N, 1),), -1, dtype=torch.int32, device=dev)
+            inv[d["rows"].long()] = torch.arange(d["nt"], dtype=torch.int32, device=dev)
+            d["inv"] = inv
             st.fdev[k].counts = _ptr(d["counts"])
             st.fdev[k].inv = _ptr(d["inv"])
             st.fdev[k].n_t = d["nt"]
@@ -2540,14 +2552,6 @@ class Cluster:
         out["gid"] = st.gid_np
         out["row2node"] = st.row2node_np
         return out
-
-
-def st_node2row_host(st: _Rank, nodes: np.ndarray) -> np.ndarray:
-    n2r = np.full(st.n_nodes, -1, dtype=np.int64)
-    if st.row2node:
-        r2n = np.concatenate(st.row2node)
-        n2r[r2n] = np.arange(len(r2n))
-    return n2r[np.asarray(nodes, dtype=np.int64)]
 
 
 # ---------------------------------------------------------------- ctypes structs

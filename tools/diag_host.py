@@ -1,0 +1,54 @@
+"""Host time per façade call / prepare step of one C3 construction (no
+profiler): wall clock around each method, and the CUDA-event span of the
+whole construction.  Shows whether the host or the device is the critical
+path."""
+import os
+import sys
+import time
+from collections import defaultdict
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2512_09502_b200 import api, engine, models  # noqa: E402
+
+T = defaultdict(float)
+N = defaultdict(int)
+
+
+def wrap(cls, name):
+    f = getattr(cls, name)
+
+    def g(*a, **k):
+        t0 = time.perf_counter()
+        try:
+            return f(*a, **k)
+        finally:
+            T[name] += time.perf_counter() - t0
+            N[name] += 1
+    setattr(cls, name, g)
+
+
+for m in ("create_neurons", "add_poisson_source", "connect_fixed_indegree_distributed", "prepare", "_prepare_rank",
+          "_prepare_tables", "_fused_sort", "_fused_eager", "_fused_ready", "_fused_check", "_sort_pending",
+          "_alloc_propagation", "_dist_target", "_routes", "_compact", "_delay_stats"):
+    wrap(engine.Cluster, m)
+neur = int(os.environ.get("NEURONS", "100000"))
+P = models.BalancedParams(neurons_per_rank=neur, k_exc=9000, k_inh=2250)
+for it in range(4):
+    T.clear()
+    N.clear()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    c = engine.Cluster(api.SimConfig(n_ranks=1, seed=12345))
+    models.build_balanced_network(c, P)
+    c.prepare()
+    e1.record()
+    host = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    print(f"iter {it}: host {1e3 * host:.2f} ms, gpu span {e0.elapsed_time(e1):.2f} ms, store {c.ranks[0].store_path}")
+    del c
+for k in sorted(T, key=lambda k: -T[k]):
+    print(f"  {k:40s} {1e3 * T[k]:8.3f} ms  x{N[k]}")

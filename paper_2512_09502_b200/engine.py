@@ -50,10 +50,12 @@ H2D_BYTES = [0]
 
 
 def _up(arr, dev) -> torch.Tensor:
-    """Host -> device upload (counted for the end-to-end byte accounting)."""
+    """Host -> device upload (counted for the end-to-end byte accounting),
+    staged through pinned memory so the host does not wait for the work
+    already queued on the stream."""
     a = np.ascontiguousarray(arr)
     H2D_BYTES[0] += a.nbytes
-    return torch.from_numpy(a).to(dev)
+    return torch.from_numpy(a).pin_memory().to(dev, non_blocking=True)
 
 
 def _up_index(arr, dev) -> torch.Tensor:
@@ -69,6 +71,16 @@ def _up_index(arr, dev) -> torch.Tensor:
 
 
 _PREP_STREAMS: dict = {}
+_GEN_STREAMS: dict = {}
+
+
+def _gen_stream(dev) -> "torch.cuda.Stream":
+    """Stream of the fused path's pass A (one per device): the draws of a
+    call overlap the host work and small kernels of the calls that follow."""
+    key = torch.device(dev).index
+    if key not in _GEN_STREAMS:
+        _GEN_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _GEN_STREAMS[key]
 
 
 def _prep_stream(dev) -> "torch.cuda.Stream":
@@ -1711,13 +1723,25 @@ class Cluster:
         fills = torch.zeros((2, B), dtype=torch.int64, device=dev)
         total = torch.zeros(1, dtype=torch.int64, device=dev)
         cpay = (d["pay_tab"] & ROW_MASK) | (z["cidx"][d["cls"]] << z["row_bits"])   # row | class index
-        ev0 = self._event(st) if self.prof is not None else None
+        # pass A runs on the generation stream: the main stream keeps only the
+        # small map / image kernels that the preparation side stream waits on
+        gen = _gen_stream(dev)
+        gen.wait_stream(torch.cuda.current_stream(dev))
+        ev0 = torch.cuda.Event(enable_timing=True) if self.prof is not None else None
+        if ev0 is not None:
+            ev0.record(gen)
         ktab = d["ktab"].ctypes.data if d["kmode"] == 3 else _ptr(d["ktab"])
         call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"], _ptr(cpay),
              z["lo"], z["pbits"], _ptr(region), slots, _ptr(meta[:B]), _ptr(meta[B:]), _ptr(fills[0]),
-             _ptr(fills[1]), _ptr(total), _ptr(z["flag"]), sk)
-        if self.prof is not None:
-            self.prof["gen"].append((ev0, self._event(st)))
+             _ptr(fills[1]), _ptr(total), _ptr(z["flag"]), gen.cuda_stream)
+        if ev0 is not None:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record(gen)
+            self.prof["gen"].append((ev0, ev1))
+        for tnsr in (region, meta, fills, total, cpay, z["flag"], d["pay_tab"]):
+            tnsr.record_stream(gen)
+        if d["kmode"] == 1:
+            d["ktab"].record_stream(gen)
         z["calls"].append(dict(region=region, rstart=rstart, cap=cap.astype(np.uint64), meta=meta, fill=fills[1],
                                fills=fills, total=total, cpay=cpay, n=int(d["n"])))
         return True
@@ -1758,6 +1782,7 @@ class Cluster:
             rcap[:, c] = zc["cap"]
         rptr_t = _up(rptr.reshape(-1), dev)
         rcap = np.ascontiguousarray(rcap.reshape(-1))
+        torch.cuda.current_stream(dev).wait_stream(_gen_stream(dev))   # every call's pass A
         fill = torch.stack([zc["fill"] for zc in calls], dim=1).reshape(-1).contiguous()
         n = sum(zc["n"] for zc in calls)
         st.n_records = n

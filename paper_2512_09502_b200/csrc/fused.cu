@@ -367,10 +367,13 @@ int fg_dispatch(int lo_bits, bool wide, const FusedGen& g, uint32_t n_tiles, cud
 }
 
 // ------------------------------------------------------------------ pass B
-constexpr int FB_THREADS = 256;
+#ifndef SMX_FB_THREADS
+#define SMX_FB_THREADS 512
+#endif
+constexpr int FB_THREADS = SMX_FB_THREADS;
 constexpr int FB_WARPS = FB_THREADS / 32;
 constexpr int FB_IPT = 15;
-constexpr int FB_TILE = FB_THREADS * FB_IPT;   // 3840 records
+constexpr int FB_TILE = FB_THREADS * FB_IPT;   // 7680 records
 constexpr int FB_TC = 256;                     // tiles per scan chunk (chunks never straddle regions)
 
 struct FusedSort {
@@ -587,15 +590,14 @@ __global__ void __launch_bounds__(256) fb_tile_offsets_kernel(const __grid_const
 // a ticket so the tiles in flight write neighbouring parts of every digit's
 // output (partial sectors complete in L2).  Writes the final payload.
 #ifndef SMX_FB_CTAS
-#define SMX_FB_CTAS 3
+#define SMX_FB_CTAS (FB_THREADS >= 512 ? 2 : 3)
 #endif
 template <int BITS, bool WIDE>
 __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(const __grid_constant__ FusedSort s,
                                                                    const uint32_t* off, const uint64_t* dbase,
                                                                    uint32_t n_tiles, uint32_t* tile_ctr) {
   constexpr int BINS = 1 << BITS;
-  constexpr int DPT = BINS / FB_THREADS;
-  static_assert(DPT >= 1, "at least 8-bit digits");
+  constexpr int DPT = BINS >= FB_THREADS ? BINS / FB_THREADS : 1;   // digits per thread
   constexpr uint32_t mask = BINS - 1;
   extern __shared__ __align__(128) uint8_t fbs[];
   uint32_t* irec = reinterpret_cast<uint32_t*>(fbs);              // [FB_TILE] TMA target, then staged payloads
@@ -674,7 +676,7 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
       const int d = tid * DPT + j;
       uint32_t t = 0;
 #pragma unroll
-      for (int w = 0; w < FB_WARPS; ++w) t += wcnt[w * BINS + d];
+      for (int w = 0; w < FB_WARPS; ++w) t += d < BINS ? wcnt[w * BINS + d] : 0u;
       tot[j] = t;
       mysum += t;
     }
@@ -683,6 +685,7 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
       const int d = tid * DPT + j;
+      if (d >= BINS) break;
       uint32_t t = run;
 #pragma unroll
       for (int w = 0; w < FB_WARPS; ++w) {

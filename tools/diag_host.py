@@ -29,9 +29,36 @@ def wrap(cls, name):
     setattr(cls, name, g)
 
 
+_call = engine.call
+
+
+def timed_call(name, *a):
+    t0 = time.perf_counter()
+    try:
+        return _call(name, *a)
+    finally:
+        T["call:" + name] += time.perf_counter() - t0
+        N["call:" + name] += 1
+
+
+engine.call = timed_call
+for m in ("_up_index", "_up"):
+    f0 = getattr(engine, m)
+
+    def mk(f0, m):
+        def g(*a, **k):
+            t0 = time.perf_counter()
+            try:
+                return f0(*a, **k)
+            finally:
+                T[m] += time.perf_counter() - t0
+                N[m] += 1
+        return g
+    setattr(engine, m, mk(f0, m))
 for m in ("create_neurons", "add_poisson_source", "connect_fixed_indegree_distributed", "prepare", "_prepare_rank",
           "_prepare_tables", "_fused_sort", "_fused_eager", "_fused_ready", "_fused_check", "_sort_pending",
-          "_alloc_propagation", "_dist_target", "_routes", "_compact", "_delay_stats"):
+          "_alloc_propagation", "_dist_target", "_routes", "_compact", "_delay_stats", "_dist", "_present_ranks",
+          "_final_pieces", "_assign", "_syn_class", "_dist_accounting", "_defer", "_tables"):
     wrap(engine.Cluster, m)
 neur = int(os.environ.get("NEURONS", "100000"))
 P = models.BalancedParams(neurons_per_rank=neur, k_exc=9000, k_inh=2250)

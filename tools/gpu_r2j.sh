@@ -1,5 +1,5 @@
 set -x
-O=gpurun_out/r2i
+O=gpurun_out/r2j
 mkdir -p $O
 timeout 600 python tools/diag_host.py > $O/diag_host.log 2>&1
 cat $O/diag_host.log

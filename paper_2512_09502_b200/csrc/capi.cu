@@ -103,7 +103,8 @@ extern "C" int smx_check_device_errors(void* stream) {
   }
   if (v) {
     cudaMemsetAsync(p, 0, sizeof(int), (cudaStream_t)stream);
-    smx_set_error("device error %d (1: a draw window was short of accepted draws)", v);
+    smx_set_error("device error %d (1: a draw window was short of accepted draws, 3: a connection target that is "
+                  "not a real neuron of its rank)", v);
     return -2;
   }
   return 0;

@@ -44,7 +44,7 @@ __global__ void pay_table_kernel(const int64_t* targets, uint64_t n, const int32
   if (i >= n) return;
   const int64_t t = targets[i];
   int32_t row = (t >= 0 && (uint64_t)t < n_nodes) ? node2row[t] : -1;
-  if (row < 0 || row > (int32_t)SMX_ROW_MASK) { atomicExch(bad, 1); row = 0; }
+  if (row < 0 || row > (int32_t)SMX_ROW_MASK) { atomicExch(bad, 3); row = 0; }
   pay[i] = (uint32_t)row | (cls << SMX_ROW_BITS);
 }
 
@@ -407,19 +407,16 @@ extern "C" int smx_pay_table(const int64_t* targets, uint64_t n, const int32_t* 
                              uint32_t cls, uint32_t* pay_tab, void* stream) {
   if (n == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  int* bad = nullptr;
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&bad, sizeof(int), st));
-  SMX_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  // the engine checks on the host that targets are real neurons; a bad row
+  // here is an internal error, reported through the device error word
+  // (no synchronisation: a persistent pass-A kernel may hold every SM)
+  int* bad = smx_device_error_word();
+  if (!bad) {
+    smx_set_error("smx_pay_table: no device error word");
+    return -3;
+  }
   smx_count_launch(); pay_table_kernel<<<nblk(n), T256, 0, st>>>(targets, n, node2row, n_nodes, cls, pay_tab, bad);
   SMX_LAUNCH_CHECK();
-  int hbad = 0;
-  SMX_CUDA_CHECK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-  SMX_CUDA_CHECK(cudaStreamSynchronize(st));
-  cudaFreeAsync(bad, st);
-  if (hbad) {
-    smx_set_error("connection targets must be real neurons of the target rank (image target or row >= 2^24)");
-    return -1;
-  }
   return 0;
 }
 

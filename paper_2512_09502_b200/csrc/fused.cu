@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       } else {
         delta[tid] = g.rstart[tid] + filled - ts;
       }
-      if (t == n_tiles - 1) g.fill_out[tid] = filled + c;
+      // clamped: an overflowing region is never read past its capacity
+      if (t == n_tiles - 1) g.fill_out[tid] = filled + c < g.rcap[tid] ? filled + c : g.rcap[tid];
     }
     // draw index of the tile's first accepted value = sum of the digit prefixes
     unsigned long long sx = excl;
@@ -335,7 +336,9 @@ int fg_launch(const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
                                         (int)smem));
     configured = dev;
   }
-  const uint32_t grid = std::min<uint32_t>(n_tiles, 148u * SMX_FG_MIN_BLOCKS);
+  // persistent CTAs, two slots short of a full GPU: small kernels of other
+  // streams (and the host waiting on them) are not queued behind pass A
+  const uint32_t grid = std::min<uint32_t>(n_tiles, 148u * SMX_FG_MIN_BLOCKS - 2);
   smx_count_launch();
   fused_gen_kernel<KM, LB, WIDE><<<grid, FG_THREADS, smem, st>>>(g, n_tiles);
   SMX_LAUNCH_CHECK();
@@ -762,7 +765,7 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, c
   if (n_chunks) {
     smx_count_launch(); fb_tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum, off);
   }
-  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(n_tiles, 148u * SMX_FB_CTAS));
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(n_tiles, 148u * SMX_FB_CTAS - 2));
   smx_count_launch();
   if (wide) fb_scatter_kernel<BITS, true><<<grid, FB_THREADS, s_smem, st>>>(s, off, dbase, n_tiles, ctr);
   else fb_scatter_kernel<BITS, false><<<grid, FB_THREADS, s_smem, st>>>(s, off, dbase, n_tiles, ctr);

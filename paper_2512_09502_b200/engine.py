@@ -402,11 +402,15 @@ class Cluster:
 
     @contextmanager
     def _timed(self, bucket):
+        """Phase timer of one façade call (sm/engine.py:212-219), with an NVTX
+        range of the same name for nsys / ncu timelines."""
         starts = [(st, self._event(st)) for st in self.ranks.values()]
         t0 = time.perf_counter()
+        torch.cuda.nvtx.range_push(bucket)
         try:
             yield
         finally:
+            torch.cuda.nvtx.range_pop()
             host_s = time.perf_counter() - t0
             self.timers._pending.append((bucket, host_s, [(a, self._event(st)) for st, a in starts]))
 
@@ -537,7 +541,21 @@ class Cluster:
             return d
 
     # -------------------------------------------------------------- connections
+    @staticmethod
+    def _check_real_targets(st: _Rank, targets):
+        """Connection targets must be real neurons of the target rank (rows of
+        the store), not image nodes: checked against the rank's node ranges."""
+        if st.n_nodes == st.n_real or not len(targets):
+            return   # no images on the rank: every node index in range is real
+        starts = np.array([int(r[0]) for r in st.row2node], dtype=np.int64)
+        ends = np.array([int(r[0]) + len(r) for r in st.row2node], dtype=np.int64)
+        t = np.asarray(targets, dtype=np.int64)
+        i = np.searchsorted(starts, t, side="right") - 1
+        if (i < 0).any() or (t >= ends[np.maximum(i, 0)]).any():
+            raise ValueError("connection targets must be real neurons of the target rank")
+
     def _tables(self, st: _Rank, sources, targets, cls, tmp_base=None):
+        self._check_real_targets(st, targets)
         dev = st.device
         src = _up_index(sources, dev)
         tgt = _up_index(targets, dev)
@@ -1206,6 +1224,7 @@ class Cluster:
             self._fused_off(st)
         if cls is None:
             self._make_wide(st)
+        self._check_real_targets(st, tg)
         tgt = _up_index(tg, dev)
         pay_tab = torch.empty(len(tg), dtype=torch.int32, device=dev)
         call("smx_pay_table", _ptr(tgt), len(tg), _ptr(st.node2row.t), st.node2row.n,
@@ -1819,6 +1838,8 @@ class Cluster:
     def _fused_check(self, st: _Rank) -> bool:
         z = st.fz
         f = z["flag"].cpu().numpy()
+        if int(f[0]):
+            return False   # a region overflowed: its records are incomplete (pass B saw a clamped fill)
         if int(f[1]):
             raise ConsistencyError(f"fused sort: device error {int(f[1])}")
         totals = torch.cat([zc["total"] for zc in z["calls"]]).cpu().numpy()
@@ -1905,6 +1926,10 @@ class Cluster:
     def _routes(self, st, tables):
         dev = st.device
         n_nodes = st.n_nodes
+        if not tables:  # no mirror / roster: empty routing table, no kernel and no readback
+            empty = torch.zeros(1, dtype=torch.int32, device=dev)
+            return dict(first=torch.zeros(n_nodes + 1, dtype=torch.int64, device=dev), dest=empty[:0], pos=empty[:0],
+                        n=0)
         arr = (ctypes_route * max(len(tables), 1))()
         keep = []
         for i, (dest, bits) in enumerate(tables):
@@ -2449,10 +2474,12 @@ class Cluster:
         warm_s = time.perf_counter() - t0
         self._recording = record
         self._set_record(record)
+        torch.cuda.nvtx.range_push("propagation")
         t1 = time.perf_counter()
         self._advance(steps)
         self._sync()
         prop = time.perf_counter() - t1
+        torch.cuda.nvtx.range_pop()
         self._recording = False
         self._set_record(False)
         self.timers.propagation += prop

@@ -206,6 +206,21 @@ int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uint32_t* row2
                int64_t* now_dev, uint32_t* src_nodes, uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap,
                const int* record_dev, int64_t* rec, uint64_t* n_rec, uint64_t rec_cap, uint32_t* spike_count,
                int* overflow, const void* p2p_host, const void* grp_host, void* stream);
+/* Spike exchange over NVLink peer memory (csrc/peer.cu), one process per
+ * GPU: the data movement of LockstepTransport's rounds (sm/transport.py:
+ * 92-168) without NCCL.  smx_peer_alloc / smx_peer_handle / smx_peer_open /
+ * smx_peer_close / smx_peer_free: an IPC-exportable receive area and its
+ * mapping in the senders.  smx_peer_exchange: per block, n_send PeerSend
+ * descriptors (count, packets, receiver slot + flag per parity, capacity)
+ * and n_slot PeerSlot descriptors (local slot + flag per parity, fixed
+ * receive block, capacity); *seq (device) is the block sequence. */
+int smx_peer_alloc(uint64_t bytes, void** ptr);
+int smx_peer_free(void* ptr);
+int smx_peer_handle(void* ptr, void* handle_out);
+int smx_peer_open(const void* handle, void** ptr);
+int smx_peer_close(void* ptr);
+int smx_peer_exchange(const void* sends_host, int n_send, const void* slots_host, int n_slot,
+                      unsigned long long* seq, void* stream);
 /* deliver_point_packets / deliver_gather_packets (sm/engine.py:146-190).
  * *count (written by the sender) is clamped to max_count, the block's
  * capacity; a larger count sets *err = 5. */

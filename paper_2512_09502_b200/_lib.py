@@ -39,6 +39,12 @@ SIGNATURES = {
     "smx_dist_tables": (I32, [P, P, U64, P, I32, U32, P, P, P]),
     "smx_gen_draw": (I32, [U64, U64, U64, U64, U64, I32, I32, P, P, U32, P, P, P, P, U32, I32, U32, U32, P, P]),
     "smx_count_ranges": (I32, [P, U64, P, P, P]),
+    "smx_peer_alloc": (I32, [U64, P]),
+    "smx_peer_free": (I32, [P]),
+    "smx_peer_handle": (I32, [P, P]),
+    "smx_peer_open": (I32, [P, P]),
+    "smx_peer_close": (I32, [P]),
+    "smx_peer_exchange": (I32, [P, I32, P, I32, P, P]),
     "smx_fused_gen": (I32, [U64, U64, U64, U64, I32, P, U32, P, I32, I32, P, U64, P, P, P, P, P, P, P]),
     "smx_fused_sort": (I32, [P, P, P, I32, I32, I32, I32, I32, P, P, U64, U64, P, P, P]),
     "smx_bits_or_many": (I32, [P, P, I32, U64, P]),

@@ -2372,13 +2372,19 @@ class Cluster:
                                recv=torch.zeros(max(sum(in_sz), 1), dtype=torch.int32, device=dev))
         plan["sent"] = torch.zeros(1, dtype=torch.int64, device=dev)    # packets sent (byte counter)
         plan["over"] = torch.zeros(1, dtype=torch.int32, device=dev)    # capacity check
+        plan["peer"] = self._peer_setup(st, plan)
         return plan
 
+    PEER_EXCHANGE = os.environ.get("SMX_PEER_EXCHANGE", "1") != "0"
+
     def _exchange_nccl(self):
-        """One process per rank: the exchange round of a block over NCCL
-        (sm/transport.py:92-168) with fixed-capacity buffers -- one collective
-        per group (all_gather) and one all_to_all for p2p pairs, each buffer
-        led by its count; nothing is read back to the host."""
+        """One process per rank: the exchange round of a block (sm/transport.py:
+        92-168) with fixed-capacity receive blocks, each led by its count.
+        Default: every sender writes its occupied packets straight into the
+        receivers' HBM over NVLink (CUDA IPC peer memory, csrc/peer.cu); with
+        SMX_PEER_EXCHANGE=0 (or without peer access) NCCL moves the
+        fixed-capacity buffers: one all_gather per group, one all_to_all for
+        p2p pairs.  Nothing is read back to the host either way."""
         dist = torch.distributed
         (st,) = self.ranks.values()
         me = st.rank
@@ -2394,7 +2400,21 @@ class Cluster:
                 if c:
                     X["over"].bitwise_or_((st.p2p_counts[d: d + 1] > c).to(torch.int32))
             X["sent"] += st.p2p_counts.sum()
-            rv, offs = fixed_p2p(st.p2p_counts, st.p2p_packets, st.pk_cap, P["out_c"], P["in_c"], P["send"], P["recv"])
+        for g, G in X["groups"].items():
+            slot = self.group_slots[g]
+            X["over"].bitwise_or_((st.g_counts[slot: slot + 1] > G["cap"]).to(torch.int32))
+            X["sent"] += st.g_counts[slot]
+        peer = X.get("peer")
+        if peer is not None:
+            call("smx_peer_exchange", ctypes_addr(peer["sends"]), peer["n_send"], ctypes_addr(peer["slots"]),
+                 peer["n_slot"], _ptr(peer["seq"]), st.stream)
+        if self.has_p2p:
+            P = X["p2p"]
+            if peer is None:
+                rv, offs = fixed_p2p(st.p2p_counts, st.p2p_packets, st.pk_cap, P["out_c"], P["in_c"], P["send"],
+                                     P["recv"])
+            else:
+                rv, offs = P["recv"], P["offs"]
             for sr in range(self.n_ranks):
                 if not P["in_c"][sr]:
                     continue
@@ -2406,11 +2426,12 @@ class Cluster:
                      _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
         for g, G in X["groups"].items():
             slot, cap, members = self.group_slots[g], G["cap"], G["members"]
-            X["over"].bitwise_or_((st.g_counts[slot: slot + 1] > cap).to(torch.int32))
-            X["sent"] += st.g_counts[slot]
-            recv = fixed_allgather(st.g_counts[slot: slot + 1],
-                                   st.g_packets[slot * st.pk_cap * 2: (slot + 1) * st.pk_cap * 2], cap,
-                                   G["send"], G["recv"], self._pg[g])
+            if peer is None:
+                recv = fixed_allgather(st.g_counts[slot: slot + 1],
+                                       st.g_packets[slot * st.pk_cap * 2: (slot + 1) * st.pk_cap * 2], cap,
+                                       G["send"], G["recv"], self._pg[g])
+            else:
+                recv = G["recv"]
             for i, sr in enumerate(members):
                 if sr == me:
                     continue
@@ -2421,6 +2442,89 @@ class Cluster:
                 call("smx_unpack", _ptr(recv[base + 2:]), _ptr(recv[base:]), cap, _ptr(lk), lk.numel(),
                      _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
         self._deliver(st)
+
+    def _peer_setup(self, st, X):
+        """Receive area of this rank (CUDA IPC, one per process) and the
+        mapped slots of every peer it sends to.  Every receiver publishes its
+        slot layout with its IPC handle (one host all_gather at setup); the
+        per-block rounds are kernels only.  None when peer access is not
+        available (different nodes, no NVLink P2P): NCCL is used instead."""
+        dist = torch.distributed
+        me = st.rank
+        if not self.PEER_EXCHANGE or dist.get_backend() != "nccl":
+            return None
+        # slot keys received by this rank: ("g", group, source) and ("p", source)
+        slots = []
+        for g, G in X["groups"].items():
+            for sr in G["members"]:
+                if sr != me:
+                    slots.append((("g", g, sr), G["cap"]))
+        if self.has_p2p:
+            for sr, c in enumerate(X["p2p"]["in_c"]):
+                if c and sr != me:
+                    slots.append((("p", sr), c))
+        layout, words = {}, 0
+        for key, cap in slots:
+            sz = (4 + 2 * cap + 3) // 4 * 4   # 16-byte aligned slots
+            layout[key] = (words, words + sz, cap)
+            words += 2 * sz
+        words = (words + 3) // 4 * 4
+        fl0 = words // 2   # flags (u64) after the slots: two per slot
+        for i, (key, cap) in enumerate(slots):
+            w0, w1, c = layout[key]
+            layout[key] = (w0, w1, fl0 + 2 * i, fl0 + 2 * i + 1, c)
+        nbytes = 4 * words + 16 * max(len(slots), 1)
+        ptr = ctypes.c_void_p()
+        call("smx_peer_alloc", nbytes, ctypes.byref(ptr))
+        handle = ctypes.create_string_buffer(64)
+        call("smx_peer_handle", ptr, handle)
+        infos = [None] * self.n_ranks
+        dist.all_gather_object(infos, (bytes(handle.raw), layout))
+        mapped = {}
+        # sends: group members (all_gather semantics) and p2p destinations
+        sends = []
+        for g, G in X["groups"].items():
+            slot = self.group_slots[g]
+            for m in G["members"]:
+                if m != me:
+                    sends.append((m, ("g", g, me), st.g_counts[slot: slot + 1], st.g_packets[slot * st.pk_cap * 2:]))
+        if self.has_p2p:
+            for d, c in enumerate(X["p2p"]["out_c"]):
+                if c and d != me:
+                    sends.append((d, ("p", me), st.p2p_counts[d: d + 1], st.p2p_packets[d * st.pk_cap * 2:]))
+        S = (ctypes_peer_send * max(len(sends), 1))()
+        for i, (dst, key, cnt, pk) in enumerate(sends):
+            if dst not in mapped:
+                rp = ctypes.c_void_p()
+                call("smx_peer_open", ctypes.create_string_buffer(infos[dst][0], 64), ctypes.byref(rp))
+                mapped[dst] = rp.value
+            w0, w1, f0, f1, cap = infos[dst][1][key]
+            base = mapped[dst]
+            S[i].count, S[i].packets = _ptr(cnt), _ptr(pk)
+            S[i].slot0, S[i].slot1 = base + 4 * w0, base + 4 * w1
+            S[i].flag0, S[i].flag1 = base + 8 * f0, base + 8 * f1
+            S[i].cap = cap
+        W = (ctypes_peer_slot * max(len(slots), 1))()
+        P = X.get("p2p")
+        if P is not None:
+            P["offs"] = []
+            at = 0
+            for sz in [2 + 2 * c if c else 0 for c in P["in_c"]]:
+                P["offs"].append(at)
+                at += sz
+        for i, (key, cap) in enumerate(slots):
+            w0, w1, f0, f1, _ = layout[key]
+            W[i].slot0, W[i].slot1 = ptr.value + 4 * w0, ptr.value + 4 * w1
+            W[i].flag0, W[i].flag1 = ptr.value + 8 * f0, ptr.value + 8 * f1
+            if key[0] == "g":
+                G = X["groups"][key[1]]
+                idx = G["members"].index(key[2])
+                W[i].out = _ptr(G["recv"]) + 4 * idx * (2 + 2 * cap)
+            else:
+                W[i].out = _ptr(P["recv"]) + 4 * P["offs"][key[1]]
+            W[i].cap = cap
+        seq = torch.zeros(1, dtype=torch.int64, device=st.device)
+        return dict(area=ptr.value, mapped=mapped, sends=S, n_send=len(sends), slots=W, n_slot=len(slots), seq=seq)
 
     def _settle_exchange(self):
         """Byte counter and capacity check of the fixed-capacity rounds (read
@@ -2623,6 +2727,17 @@ class ctypes_route(ctypes.Structure):
 class ctypes_fdev(ctypes.Structure):
     _fields_ = [("counts", ctypes.c_void_p), ("inv", ctypes.c_void_p), ("n_t", ctypes.c_uint32),
                 ("w", ctypes.c_double), ("delay", ctypes.c_int), ("port", ctypes.c_int)]
+
+
+class ctypes_peer_send(ctypes.Structure):   # csrc/peer.cu PeerSend
+    _fields_ = [("count", ctypes.c_void_p), ("packets", ctypes.c_void_p), ("slot0", ctypes.c_void_p),
+                ("slot1", ctypes.c_void_p), ("flag0", ctypes.c_void_p), ("flag1", ctypes.c_void_p),
+                ("cap", ctypes.c_uint32)]
+
+
+class ctypes_peer_slot(ctypes.Structure):   # csrc/peer.cu PeerSlot
+    _fields_ = [("slot0", ctypes.c_void_p), ("slot1", ctypes.c_void_p), ("flag0", ctypes.c_void_p),
+                ("flag1", ctypes.c_void_p), ("out", ctypes.c_void_p), ("cap", ctypes.c_uint32)]
 
 
 class ctypes_routes(ctypes.Structure):

@@ -436,7 +436,6 @@ def run_c5(args):
             for i in range(args.warmup + args.steps):
                 del c
                 gc.collect()
-                torch.cuda.empty_cache()
                 torch.cuda.reset_peak_memory_stats(dev)
                 if world > 1:
                     dist.barrier()
@@ -456,19 +455,20 @@ def run_c5(args):
                     gen.append(c.kernel_ms("gen"))
                     srt.append(c.kernel_ms("sort"))
             peak = torch.cuda.max_memory_allocated(dev)
-            st = c.ranks[rank]
-            ok = int(st.first_index[-1].item()) == S
+            ok = int(c.ranks[rank].first_index[-1].item()) == S
+            path = c.ranks[rank].store_path
             ms = float(np.mean(times))
             line = {"metric": "construction_synapses_per_s", "value": world * S / (ms * 1e-3), "unit": "synapses/s",
                     "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                     "higher_is_better": True, "scaling": "weak", "data": "synthetic",
                     "config": {"workload": f"C5_{rule}_{S:.0e}", "rule": rule, "neurons_per_gpu": n,
-                               "synapses_per_gpu": S, "store_path": st.store_path},
+                               "synapses_per_gpu": S, "store_path": path},
                     "phase_ms": {"gen": float(np.mean(gen)), "sort": float(np.mean(srt))},
                     "peak_device_bytes": int(peak), "peak_bytes_per_synapse": peak / S, "records_ok": ok}
             if rank == 0:
                 print(json.dumps(line), flush=True)
             del c
+            c = None
             gc.collect()
             torch.cuda.empty_cache()
     if world > 1:

@@ -211,16 +211,20 @@ int smx_spikes(const uint32_t* spike_bits, uint32_t n_rows, const uint32_t* row2
  * 92-168) without NCCL.  smx_peer_alloc / smx_peer_handle / smx_peer_open /
  * smx_peer_close / smx_peer_free: an IPC-exportable receive area and its
  * mapping in the senders.  smx_peer_exchange: per block, n_send PeerSend
- * descriptors (count, packets, receiver slot + flag per parity, capacity)
- * and n_slot PeerSlot descriptors (local slot + flag per parity, fixed
- * receive block, capacity); *seq (device) is the block sequence. */
+ * descriptors (count, packets, receiver slot + flag per parity, capacity,
+ * byte-count flag) and n_slot PeerSlot descriptors (local slot + flag per
+ * parity, position lookup L / I, capacity): sends, then wait + unpack into
+ * the delivery list (src_nodes, src_steps, *n_src).  *seq (device) is the
+ * block sequence, *sent / *over the round's counters, *done a zeroed word. */
 int smx_peer_alloc(uint64_t bytes, void** ptr);
 int smx_peer_free(void* ptr);
 int smx_peer_handle(void* ptr, void* handle_out);
 int smx_peer_open(const void* handle, void** ptr);
 int smx_peer_close(void* ptr);
 int smx_peer_exchange(const void* sends_host, int n_send, const void* slots_host, int n_slot,
-                      unsigned long long* seq, void* stream);
+                      unsigned long long* seq, unsigned long long* sent, int* over, uint32_t* src_nodes,
+                      uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err, unsigned int* done,
+                      void* stream);
 /* deliver_point_packets / deliver_gather_packets (sm/engine.py:146-190).
  * *count (written by the sender) is clamped to max_count, the block's
  * capacity; a larger count sets *err = 5. */

@@ -11,8 +11,11 @@
 //              scope and publishes the block's sequence number in the slot's
 //              flag;
 //   peer_wait  spins until every expected flag carries the sequence number,
-//              then copies each slot into the fixed receive blocks the unpack
-//              kernels read and advances the sequence.
+//              then unpacks each slot in place: map / roster position ->
+//              image node through the slot's lookup table (L or I, -1
+//              skipped), appended to the delivery source list; the last CTA
+//              advances the sequence.  The capacity check and the byte
+//              counter of the round ride along in peer_send.
 // No NCCL launch, no padding (only occupied packets travel), no host step:
 // both kernels are captured in the block's CUDA graph.  Slots alternate
 // between two parities so a fast sender never overwrites a block the
@@ -28,25 +31,36 @@ constexpr int PEER_MAX = 64;  // sends / slots per launch
 struct PeerSend {
   const uint32_t* count;  // sender's packet count (device)
   const uint32_t* packets;  // sender's packets, 2 words each
-  uint32_t* slot[2];      // receiver's slot per parity (mapped): [count, 0, packets...]
+  uint32_t* slot[2];      // receiver's slot per parity (mapped): [count, 0, 0, 0, packets...]
   unsigned long long* flag[2];  // receiver's flag per parity (mapped)
   uint32_t cap;           // packets per slot
+  int account;            // this descriptor adds the buffer's count to the byte counter
 };
 
 struct PeerSendArgs {
   int n;
+  unsigned long long* sent;  // packets put on the wire (TransportStats bytes / 8)
+  int* over;                 // set when a buffer exceeds its capacity
+  uint32_t* n_src;           // delivery list length, reset for this round's unpack
   PeerSend s[PEER_MAX];
 };
 
 struct PeerSlot {
   const uint32_t* slot[2];              // local slot per parity
   const unsigned long long* flag[2];    // local flag per parity
-  uint32_t* out;                        // fixed receive block [count, 0, packets...]
+  const int64_t* table;                 // position -> image node (-1: not an image here)
+  uint64_t table_len;
   uint32_t cap;
 };
 
 struct PeerWaitArgs {
   int n;
+  uint32_t* src_nodes;
+  uint32_t* src_steps;
+  uint32_t* n_src;
+  uint32_t src_cap;
+  int* err;
+  unsigned int* done;     // CTA counter: the last one advances the sequence
   PeerSlot s[PEER_MAX];
 };
 
@@ -55,7 +69,12 @@ __global__ void peer_send_kernel(const __grid_constant__ PeerSendArgs A, const u
   const unsigned long long s = *seq + 1;
   const int par = (int)(s & 1);
   uint32_t n = *P.count;
-  if (n > P.cap) n = P.cap;  // over-full blocks are flagged by the engine's capacity check
+  if (threadIdx.x == 0) {
+    if (n > P.cap) atomicExch(A.over, 1);
+    if (P.account) atomicAdd(A.sent, (unsigned long long)n);
+    if (blockIdx.x == 0) *A.n_src = 0;
+  }
+  if (n > P.cap) n = P.cap;
   uint32_t* dst = P.slot[par];
   const uint32_t words = 2 * n;
   if ((reinterpret_cast<uintptr_t>(P.packets) & 15) == 0) {  // 16-byte NVLink stores
@@ -78,21 +97,38 @@ __global__ void peer_wait_kernel(const __grid_constant__ PeerWaitArgs A, unsigne
   const int par = (int)(s & 1);
   __shared__ uint32_t n;
   if (threadIdx.x == 0) {
-    while (*(volatile const unsigned long long*)P.flag[par] != s) __nanosleep(100);
+    while (*(volatile const unsigned long long*)P.flag[par] != s) __nanosleep(64);
     __threadfence_system();
     n = *(volatile const uint32_t*)P.slot[par];
+    if (n > P.cap) { atomicExch(A.err, 5); n = P.cap; }
+    if (P.table == nullptr) n = 0;  // no lookup for this source here: nothing to deliver
   }
   __syncthreads();
-  const uint32_t* src = P.slot[par];
-  const uint32_t words = 2 * n;
-  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) P.out[2 + i] = ((volatile const uint32_t*)src)[4 + i];
-  if (threadIdx.x == 0) {
-    P.out[0] = n;
-    P.out[1] = 0;
+  const volatile uint32_t* src = P.slot[par] + 4;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {  // unpack (smx_unpack) in place
+    const uint32_t p = src[2 * i];
+    if (p >= P.table_len) { atomicExch(A.err, 4); continue; }
+    const int64_t img = P.table[p];
+    if (img < 0) continue;
+    const uint32_t k = atomicAdd(A.n_src, 1u);
+    if (k < A.src_cap) { A.src_nodes[k] = (uint32_t)img; A.src_steps[k] = src[2 * i + 1]; }
+    else atomicExch(A.err, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // every CTA has read *seq: the last one advances it
+    __threadfence();
+    if (atomicAdd(A.done, 1u) == gridDim.x - 1) {
+      *A.done = 0;
+      *seq = s;
+    }
   }
 }
 
-__global__ void peer_advance_kernel(unsigned long long* seq) { *seq += 1; }
+__global__ void peer_reset_kernel(uint32_t* n_src, unsigned long long* seq, int advance) {
+  *n_src = 0;
+  if (advance) *seq += 1;
+}
+
 
 }  // namespace
 
@@ -129,11 +165,17 @@ extern "C" int smx_peer_close(void* ptr) {
   return 0;
 }
 
-// One exchange round: sends (host array of n_send descriptors, laid out as
-// PeerSend), then waits for n_slot incoming slots (PeerSlot) and copies them
-// into their fixed receive blocks; *seq (device) advances by one.
+
+
+// One exchange round, two kernels: sends (n_send PeerSend descriptors; they
+// also reset the delivery list, check capacities and count the packets),
+// then the wait + in-place unpack of n_slot incoming slots (PeerSlot) into
+// (src_nodes, src_steps, *n_src); *seq (device) advances by one.  `done` is
+// a zeroed device word (CTA counter).
 extern "C" int smx_peer_exchange(const void* sends_host, int n_send, const void* slots_host, int n_slot,
-                                 unsigned long long* seq, void* stream) {
+                                 unsigned long long* seq, unsigned long long* sent, int* over, uint32_t* src_nodes,
+                                 uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err, unsigned int* done,
+                                 void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n_send > PEER_MAX || n_slot > PEER_MAX) {
     smx_set_error("smx_peer_exchange: at most %d sends / slots", PEER_MAX);
@@ -142,16 +184,27 @@ extern "C" int smx_peer_exchange(const void* sends_host, int n_send, const void*
   if (n_send) {
     PeerSendArgs A;
     A.n = n_send;
+    A.sent = sent;
+    A.over = over;
+    A.n_src = n_src;
     memcpy(A.s, sends_host, sizeof(PeerSend) * n_send);
     smx_count_launch(); peer_send_kernel<<<n_send, 256, 0, st>>>(A, seq);
   }
   if (n_slot) {
     PeerWaitArgs W;
     W.n = n_slot;
+    W.src_nodes = src_nodes;
+    W.src_steps = src_steps;
+    W.n_src = n_src;
+    W.src_cap = src_cap;
+    W.err = err;
+    W.done = done;
     memcpy(W.s, slots_host, sizeof(PeerSlot) * n_slot);
+    if (!n_send) { smx_count_launch(); peer_reset_kernel<<<1, 1, 0, st>>>(n_src, seq, 0); }
     smx_count_launch(); peer_wait_kernel<<<n_slot, 256, 0, st>>>(W, seq);
+  } else {
+    smx_count_launch(); peer_reset_kernel<<<1, 1, 0, st>>>(n_src, seq, 1);
   }
-  smx_count_launch(); peer_advance_kernel<<<1, 1, 0, st>>>(seq);
   SMX_LAUNCH_CHECK();
   return 0;
 }

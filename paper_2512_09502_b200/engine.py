@@ -2388,12 +2388,23 @@ class Cluster:
         dist = torch.distributed
         (st,) = self.ranks.values()
         me = st.rank
-        st.n_src.zero_()
         if self._pg is None:
             self._pg = {g: dist.new_group(sorted(self.groups[g])) for g in sorted(self.groups)}
         if st.xplan is None:
             st.xplan = self._xplan(st)
         X = st.xplan
+        peer = X.get("peer")
+        if peer is not None:
+            # sends (+ capacity check, byte counter, list reset), then wait +
+            # unpack in place: two kernels, then the delivery of the round
+            for g in peer["solo"]:   # a group with this rank alone: no message, its pairs still count
+                X["sent"] += st.g_counts[self.group_slots[g]]
+            call("smx_peer_exchange", ctypes_addr(peer["sends"]), peer["n_send"], ctypes_addr(peer["slots"]),
+                 peer["n_slot"], _ptr(peer["seq"]), _ptr(X["sent"]), _ptr(X["over"]), _ptr(st.src_nodes),
+                 _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), _ptr(peer["done"]), st.stream)
+            self._deliver(st)
+            return
+        st.n_src.zero_()
         if self.has_p2p:
             P = X["p2p"]
             for d, c in enumerate(P["out_c"]):
@@ -2404,17 +2415,10 @@ class Cluster:
             slot = self.group_slots[g]
             X["over"].bitwise_or_((st.g_counts[slot: slot + 1] > G["cap"]).to(torch.int32))
             X["sent"] += st.g_counts[slot]
-        peer = X.get("peer")
-        if peer is not None:
-            call("smx_peer_exchange", ctypes_addr(peer["sends"]), peer["n_send"], ctypes_addr(peer["slots"]),
-                 peer["n_slot"], _ptr(peer["seq"]), st.stream)
         if self.has_p2p:
             P = X["p2p"]
-            if peer is None:
-                rv, offs = fixed_p2p(st.p2p_counts, st.p2p_packets, st.pk_cap, P["out_c"], P["in_c"], P["send"],
-                                     P["recv"])
-            else:
-                rv, offs = P["recv"], P["offs"]
+            rv, offs = fixed_p2p(st.p2p_counts, st.p2p_packets, st.pk_cap, P["out_c"], P["in_c"], P["send"],
+                                 P["recv"])
             for sr in range(self.n_ranks):
                 if not P["in_c"][sr]:
                     continue
@@ -2426,12 +2430,9 @@ class Cluster:
                      _ptr(st.src_nodes), _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), st.stream)
         for g, G in X["groups"].items():
             slot, cap, members = self.group_slots[g], G["cap"], G["members"]
-            if peer is None:
-                recv = fixed_allgather(st.g_counts[slot: slot + 1],
-                                       st.g_packets[slot * st.pk_cap * 2: (slot + 1) * st.pk_cap * 2], cap,
-                                       G["send"], G["recv"], self._pg[g])
-            else:
-                recv = G["recv"]
+            recv = fixed_allgather(st.g_counts[slot: slot + 1],
+                                   st.g_packets[slot * st.pk_cap * 2: (slot + 1) * st.pk_cap * 2], cap,
+                                   G["send"], G["recv"], self._pg[g])
             for i, sr in enumerate(members):
                 if sr == me:
                     continue
@@ -2482,18 +2483,23 @@ class Cluster:
         dist.all_gather_object(infos, (bytes(handle.raw), layout))
         mapped = {}
         # sends: group members (all_gather semantics) and p2p destinations
-        sends = []
+        sends, solo = [], []
         for g, G in X["groups"].items():
             slot = self.group_slots[g]
+            first = True
             for m in G["members"]:
-                if m != me:
-                    sends.append((m, ("g", g, me), st.g_counts[slot: slot + 1], st.g_packets[slot * st.pk_cap * 2:]))
+                if m != me:   # the group's pairs count once per round (sm/transport.py:165-166)
+                    sends.append((m, ("g", g, me), st.g_counts[slot: slot + 1], st.g_packets[slot * st.pk_cap * 2:],
+                                  first))
+                    first = False
+            if first:
+                solo.append(g)
         if self.has_p2p:
             for d, c in enumerate(X["p2p"]["out_c"]):
                 if c and d != me:
-                    sends.append((d, ("p", me), st.p2p_counts[d: d + 1], st.p2p_packets[d * st.pk_cap * 2:]))
+                    sends.append((d, ("p", me), st.p2p_counts[d: d + 1], st.p2p_packets[d * st.pk_cap * 2:], True))
         S = (ctypes_peer_send * max(len(sends), 1))()
-        for i, (dst, key, cnt, pk) in enumerate(sends):
+        for i, (dst, key, cnt, pk, account) in enumerate(sends):
             if dst not in mapped:
                 rp = ctypes.c_void_p()
                 call("smx_peer_open", ctypes.create_string_buffer(infos[dst][0], 64), ctypes.byref(rp))
@@ -2504,27 +2510,22 @@ class Cluster:
             S[i].slot0, S[i].slot1 = base + 4 * w0, base + 4 * w1
             S[i].flag0, S[i].flag1 = base + 8 * f0, base + 8 * f1
             S[i].cap = cap
+            S[i].account = 1 if account else 0
         W = (ctypes_peer_slot * max(len(slots), 1))()
-        P = X.get("p2p")
-        if P is not None:
-            P["offs"] = []
-            at = 0
-            for sz in [2 + 2 * c if c else 0 for c in P["in_c"]]:
-                P["offs"].append(at)
-                at += sz
         for i, (key, cap) in enumerate(slots):
             w0, w1, f0, f1, _ = layout[key]
             W[i].slot0, W[i].slot1 = ptr.value + 4 * w0, ptr.value + 4 * w1
             W[i].flag0, W[i].flag1 = ptr.value + 8 * f0, ptr.value + 8 * f1
-            if key[0] == "g":
-                G = X["groups"][key[1]]
-                idx = G["members"].index(key[2])
-                W[i].out = _ptr(G["recv"]) + 4 * idx * (2 + 2 * cap)
-            else:
-                W[i].out = _ptr(P["recv"]) + 4 * P["offs"][key[1]]
+            # lookup of the source's positions: roster lookups I (groups) or
+            # map images L (p2p); none -> the round is waited for, not delivered
+            tab = st.I.get((key[1], key[2])) if key[0] == "g" else st.RL[(POINT_TO_POINT, key[1])][1]
+            W[i].table = _ptr(tab)
+            W[i].table_len = 0 if tab is None else tab.numel()
             W[i].cap = cap
         seq = torch.zeros(1, dtype=torch.int64, device=st.device)
-        return dict(area=ptr.value, mapped=mapped, sends=S, n_send=len(sends), slots=W, n_slot=len(slots), seq=seq)
+        done = torch.zeros(1, dtype=torch.int32, device=st.device)
+        return dict(area=ptr.value, mapped=mapped, sends=S, n_send=len(sends), slots=W, n_slot=len(slots), seq=seq,
+                    done=done, solo=solo)
 
     def _settle_exchange(self):
         """Byte counter and capacity check of the fixed-capacity rounds (read
@@ -2732,12 +2733,13 @@ class ctypes_fdev(ctypes.Structure):
 class ctypes_peer_send(ctypes.Structure):   # csrc/peer.cu PeerSend
     _fields_ = [("count", ctypes.c_void_p), ("packets", ctypes.c_void_p), ("slot0", ctypes.c_void_p),
                 ("slot1", ctypes.c_void_p), ("flag0", ctypes.c_void_p), ("flag1", ctypes.c_void_p),
-                ("cap", ctypes.c_uint32)]
+                ("cap", ctypes.c_uint32), ("account", ctypes.c_int)]
 
 
 class ctypes_peer_slot(ctypes.Structure):   # csrc/peer.cu PeerSlot
     _fields_ = [("slot0", ctypes.c_void_p), ("slot1", ctypes.c_void_p), ("flag0", ctypes.c_void_p),
-                ("flag1", ctypes.c_void_p), ("out", ctypes.c_void_p), ("cap", ctypes.c_uint32)]
+                ("flag1", ctypes.c_void_p), ("table", ctypes.c_void_p), ("table_len", ctypes.c_uint64),
+                ("cap", ctypes.c_uint32)]
 
 
 class ctypes_routes(ctypes.Structure):

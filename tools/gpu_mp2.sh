@@ -1,5 +1,5 @@
 set -x
-O=gpurun_out/mp2
+O=gpurun_out/mp2b
 mkdir -p $O
 nvidia-smi topo -m > $O/topo.txt 2>&1
 timeout 900 python -m pytest tests/test_gpu_multiprocess.py -q -p no:cacheprovider > $O/pytest_mp.log 2>&1

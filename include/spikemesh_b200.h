@@ -224,7 +224,7 @@ int smx_peer_close(void* ptr);
 int smx_peer_exchange(const void* sends_host, int n_send, const void* slots_host, int n_slot,
                       unsigned long long* seq, unsigned long long* sent, int* over, uint32_t* src_nodes,
                       uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err, unsigned int* done,
-                      void* stream);
+                      uint32_t* zero0, uint32_t nzero0, uint32_t* zero1, uint32_t nzero1, void* stream);
 /* deliver_point_packets / deliver_gather_packets (sm/engine.py:146-190).
  * *count (written by the sender) is clamped to max_count, the block's
  * capacity; a larger count sets *err = 5. */

@@ -61,6 +61,8 @@ struct PeerWaitArgs {
   uint32_t src_cap;
   int* err;
   unsigned int* done;     // CTA counter: the last one advances the sequence
+  uint32_t* zero[2];      // the senders' packet counts, cleared for the next block
+  uint32_t nzero[2];
   PeerSlot s[PEER_MAX];
 };
 
@@ -104,6 +106,10 @@ __global__ void peer_wait_kernel(const __grid_constant__ PeerWaitArgs A, unsigne
     if (P.table == nullptr) n = 0;  // no lookup for this source here: nothing to deliver
   }
   __syncthreads();
+  if (blockIdx.x == 0) {  // the sends of this round are complete (stream order)
+    for (int z = 0; z < 2; ++z)
+      for (uint32_t i = threadIdx.x; i < A.nzero[z]; i += blockDim.x) A.zero[z][i] = 0;
+  }
   const volatile uint32_t* src = P.slot[par] + 4;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {  // unpack (smx_unpack) in place
     const uint32_t p = src[2 * i];
@@ -124,9 +130,14 @@ __global__ void peer_wait_kernel(const __grid_constant__ PeerWaitArgs A, unsigne
   }
 }
 
-__global__ void peer_reset_kernel(uint32_t* n_src, unsigned long long* seq, int advance) {
+__global__ void peer_reset_kernel(uint32_t* n_src, unsigned long long* seq, int advance, uint32_t* z0, uint32_t n0,
+                                  uint32_t* z1, uint32_t n1) {
   *n_src = 0;
-  if (advance) *seq += 1;
+  if (advance) {
+    *seq += 1;
+    for (uint32_t i = 0; i < n0; ++i) z0[i] = 0;
+    for (uint32_t i = 0; i < n1; ++i) z1[i] = 0;
+  }
 }
 
 
@@ -171,11 +182,12 @@ extern "C" int smx_peer_close(void* ptr) {
 // also reset the delivery list, check capacities and count the packets),
 // then the wait + in-place unpack of n_slot incoming slots (PeerSlot) into
 // (src_nodes, src_steps, *n_src); *seq (device) advances by one.  `done` is
-// a zeroed device word (CTA counter).
+// a zeroed device word (CTA counter); zero0 / zero1 (the senders' packet
+// counts) are cleared once the round is sent.
 extern "C" int smx_peer_exchange(const void* sends_host, int n_send, const void* slots_host, int n_slot,
                                  unsigned long long* seq, unsigned long long* sent, int* over, uint32_t* src_nodes,
                                  uint32_t* src_steps, uint32_t* n_src, uint32_t src_cap, int* err, unsigned int* done,
-                                 void* stream) {
+                                 uint32_t* zero0, uint32_t nzero0, uint32_t* zero1, uint32_t nzero1, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n_send > PEER_MAX || n_slot > PEER_MAX) {
     smx_set_error("smx_peer_exchange: at most %d sends / slots", PEER_MAX);
@@ -199,11 +211,15 @@ extern "C" int smx_peer_exchange(const void* sends_host, int n_send, const void*
     W.src_cap = src_cap;
     W.err = err;
     W.done = done;
+    W.zero[0] = zero0;
+    W.zero[1] = zero1;
+    W.nzero[0] = nzero0;
+    W.nzero[1] = nzero1;
     memcpy(W.s, slots_host, sizeof(PeerSlot) * n_slot);
-    if (!n_send) { smx_count_launch(); peer_reset_kernel<<<1, 1, 0, st>>>(n_src, seq, 0); }
+    if (!n_send) { smx_count_launch(); peer_reset_kernel<<<1, 1, 0, st>>>(n_src, seq, 0, nullptr, 0, nullptr, 0); }
     smx_count_launch(); peer_wait_kernel<<<n_slot, 256, 0, st>>>(W, seq);
   } else {
-    smx_count_launch(); peer_reset_kernel<<<1, 1, 0, st>>>(n_src, seq, 1);
+    smx_count_launch(); peer_reset_kernel<<<1, 1, 0, st>>>(n_src, seq, 1, zero0, nzero0, zero1, nzero1);
   }
   SMX_LAUNCH_CHECK();
   return 0;

@@ -2229,6 +2229,9 @@ class Cluster:
 
     def _zero_counts(self):
         for st in self.ranks.values():
+            X = getattr(st, "xplan", None)
+            if X is not None and X.get("peer") is not None:
+                continue   # the peer round clears them (csrc/peer.cu)
             st.p2p_counts.zero_()
             st.g_counts.zero_()
 
@@ -2401,7 +2404,8 @@ class Cluster:
                 X["sent"] += st.g_counts[self.group_slots[g]]
             call("smx_peer_exchange", ctypes_addr(peer["sends"]), peer["n_send"], ctypes_addr(peer["slots"]),
                  peer["n_slot"], _ptr(peer["seq"]), _ptr(X["sent"]), _ptr(X["over"]), _ptr(st.src_nodes),
-                 _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), _ptr(peer["done"]), st.stream)
+                 _ptr(st.src_steps), _ptr(st.n_src), st.src_cap, _ptr(st.err), _ptr(peer["done"]),
+                 _ptr(st.p2p_counts), st.p2p_counts.numel(), _ptr(st.g_counts), st.g_counts.numel(), st.stream)
             self._deliver(st)
             return
         st.n_src.zero_()

@@ -58,10 +58,18 @@ for m in ("_up_index", "_up"):
 for m in ("create_neurons", "add_poisson_source", "connect_fixed_indegree_distributed", "prepare", "_prepare_rank",
           "_prepare_tables", "_fused_sort", "_fused_eager", "_fused_ready", "_fused_check", "_sort_pending",
           "_alloc_propagation", "_dist_target", "_routes", "_compact", "_delay_stats", "_dist", "_present_ranks",
-          "_final_pieces", "_assign", "_syn_class", "_dist_accounting", "_defer", "_tables"):
+          "_final_pieces", "_assign", "_syn_class", "_dist_accounting", "_defer", "_tables", "_replay_start",
+          "_replay_finish", "_dist_replay", "_dist_tables"):
     wrap(engine.Cluster, m)
 neur = int(os.environ.get("NEURONS", "100000"))
 P = models.BalancedParams(neurons_per_rank=neur, k_exc=9000, k_inh=2250)
+world = int(os.environ.get("WORLD_SIZE", "1"))
+rank = int(os.environ.get("RANK", "0"))
+if world > 1:   # under torchrun: one rank per GPU, rank 0 prints
+    import torch.distributed as dist
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+cfg = api.SimConfig(n_ranks=world, comm_mode="collective" if world > 1 else "p2p", seed=12345)
 for it in range(4):
     T.clear()
     N.clear()
@@ -69,13 +77,20 @@ for it in range(4):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     e0.record()
-    c = engine.Cluster(api.SimConfig(n_ranks=1, seed=12345))
+    if world > 1:
+        dist.barrier()
+    c = engine.Cluster(cfg)
     models.build_balanced_network(c, P)
     c.prepare()
     e1.record()
     host = time.perf_counter() - t0
     torch.cuda.synchronize()
-    print(f"iter {it}: host {1e3 * host:.2f} ms, gpu span {e0.elapsed_time(e1):.2f} ms, store {c.ranks[0].store_path}")
+    if rank == 0:
+        print(f"iter {it}: host {1e3 * host:.2f} ms, gpu span {e0.elapsed_time(e1):.2f} ms, "
+              f"store {c.ranks[rank].store_path}", flush=True)
     del c
-for k in sorted(T, key=lambda k: -T[k]):
-    print(f"  {k:40s} {1e3 * T[k]:8.3f} ms  x{N[k]}")
+if rank == 0:
+    for k in sorted(T, key=lambda k: -T[k]):
+        print(f"  {k:40s} {1e3 * T[k]:8.3f} ms  x{N[k]}")
+if world > 1:
+    dist.destroy_process_group()

@@ -1,5 +1,6 @@
 set -x
-O=gpurun_out/mp2b
+export PYTHONFAULTHANDLER=1
+O=gpurun_out/mp2c
 mkdir -p $O
 nvidia-smi topo -m > $O/topo.txt 2>&1
 timeout 900 python -m pytest tests/test_gpu_multiprocess.py -q -p no:cacheprovider > $O/pytest_mp.log 2>&1

@@ -93,10 +93,16 @@ __device__ __forceinline__ void st_vol(uint32_t* p, uint32_t v) { *(volatile uin
 
 // Stable rank of one item per lane among the warp's items with the same
 // digit (ballot multisplit, as in sort.cu) against the warp's SMEM counters.
+#ifndef SMX_MATCH_RANK
+#define SMX_MATCH_RANK 0   // 1: __match_any_sync instead of one ballot per digit bit (A/B)
+#endif
 template <int LB>
 __device__ __forceinline__ uint32_t fg_rank(uint32_t d, bool valid, uint32_t vm, uint16_t* mycnt, int lane,
                                             uint32_t lt) {
   uint32_t peers = vm;
+  if (SMX_MATCH_RANK) {
+    peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu) & vm;
+  } else {
 #pragma unroll
   for (int b = 0; b < LB; ++b) {
     asm("{\n\t.reg .pred p;\n\t.reg .b32 t, bal;\n\t"
@@ -106,6 +112,7 @@ __device__ __forceinline__ uint32_t fg_rank(uint32_t d, bool valid, uint32_t vm,
         "@!p not.b32 bal, bal;\n\t"
         "and.b32 %0, %0, bal;\n\t}"
         : "+r"(peers) : "r"(d), "r"(1u << b));
+  }
   }
   if (!valid) peers = 1u << lane;
   const int leader = __ffs(peers) - 1;

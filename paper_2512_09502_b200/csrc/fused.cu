@@ -52,6 +52,9 @@ constexpr int FG_MAXP = 8;
 #ifndef SMX_FG_MIN_BLOCKS
 #define SMX_FG_MIN_BLOCKS 2
 #endif
+#ifndef SMX_FG_FREE_SMS
+#define SMX_FG_FREE_SMS 8
+#endif
 
 struct FusedGen {
   Key key;
@@ -343,9 +346,10 @@ int fg_launch(const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
                                         (int)smem));
     configured = dev;
   }
-  // persistent CTAs, two slots short of a full GPU: small kernels of other
-  // streams (and the host waiting on them) are not queued behind pass A
-  const uint32_t grid = std::min<uint32_t>(n_tiles, 148u * SMX_FG_MIN_BLOCKS - 2);
+  // persistent CTAs on 140 of the 148 SMs: the replays and small kernels of
+  // the calls that follow (their host code waits on them) run beside pass A
+  // instead of queueing behind it
+  const uint32_t grid = std::min<uint32_t>(n_tiles, (148u - SMX_FG_FREE_SMS) * SMX_FG_MIN_BLOCKS);
   smx_count_launch();
   fused_gen_kernel<KM, LB, WIDE><<<grid, FG_THREADS, smem, st>>>(g, n_tiles);
   SMX_LAUNCH_CHECK();

@@ -765,7 +765,7 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, c
                                         (int)s_smem));
     configured = dev;
   }
-  const uint32_t hgrid = std::max<uint32_t>(1, std::min<uint32_t>((n_tiles + HW - 1) / HW, 148 * 2));
+  const uint32_t hgrid = std::max<uint32_t>(1, std::min<uint32_t>((n_tiles + HW - 1) / HW, (148 - SMX_FG_FREE_SMS) * 2));
   smx_count_launch(); fb_hist_kernel<BITS><<<hgrid, 32 * HW, h_smem, st>>>(s, tcnt, n_tiles);
   if (n_chunks) {
     smx_count_launch(); fb_chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum);
@@ -776,7 +776,9 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, c
   if (n_chunks) {
     smx_count_launch(); fb_tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum, off);
   }
-  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(n_tiles, 148u * SMX_FB_CTAS - 2));
+  // like pass A, the scatter leaves SMX_FG_FREE_SMS SMs to the preparation
+  // side stream (map compaction, routes), whose host code waits on it
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(n_tiles, (148u - SMX_FG_FREE_SMS) * SMX_FB_CTAS));
   smx_count_launch();
   if (wide) fb_scatter_kernel<BITS, true><<<grid, FB_THREADS, s_smem, st>>>(s, off, dbase, n_tiles, ctr);
   else fb_scatter_kernel<BITS, false><<<grid, FB_THREADS, s_smem, st>>>(s, off, dbase, n_tiles, ctr);

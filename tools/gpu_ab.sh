@@ -6,3 +6,5 @@ for v in default match; do
   timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --model-ms 10 --prop-warmup-ms 1 > $O/bench_$v.json 2>&1
   python -c "import json; d=json.load(open('$O/bench_$v.json')); print('$v', d['ms_per_step'], d['phase_ms'])"
 done
+unset SMX_LIB_PATH
+timeout 600 python tools/diag_host.py > $O/diag1.log 2>&1; head -12 $O/diag1.log

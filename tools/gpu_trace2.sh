@@ -1,5 +1,5 @@
 set -x
 O=gpurun_out/trace2
 mkdir -p $O
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29563 tools/trace_dist.py > $O/trace_fused.log 2>&1
-grep -v "^\*\|OMP\|NCCL\|Warn\|warn" $O/trace_fused.log | head -40
+TIMELINE=1 STACK=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29563 tools/trace_dist.py > $O/trace_fused.log 2>&1
+grep -v "^\*\|OMP\|NCCL\|Warn\|warn" $O/trace_fused.log | head -150

@@ -52,6 +52,14 @@ if rank == 0:
     for g, at, n in sorted(gaps, reverse=True)[:25]:
         ops = [e["name"] for e in cpu if e["ts"] <= at + g / 2 <= e["ts"] + e["dur"]]
         print(f"  gap {1e-3 * g:6.3f} ms at {1e-3 * (at - t0):7.2f} ms before {n[:40]:40s} cpu: {ops[-3:]}")
+    if os.environ.get("TIMELINE"):  # every GPU op >= 20 us: start, duration, stream, name
+        for e2 in sorted((e for e in ev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")),
+                         key=lambda e: e["ts"]):
+            if e2["dur"] >= 20:
+                print(f"  gpu {1e-3 * (e2['ts'] - t0):7.2f} +{1e-3 * e2['dur']:7.3f} ms s{e2.get('tid')}  {e2['name'][:70]}")
+        for e2 in sorted(cpu, key=lambda e: e["ts"]):
+            if e2.get("cat") == "python_function" and e2["dur"] >= 300 and "engine.py" in e2["name"]:
+                print(f"  cpu {1e-3 * (e2['ts'] - t0):7.2f} +{1e-3 * e2['dur']:7.3f} ms  {e2['name'][:80]}")
     if os.environ.get("STACK"):  # host functions (>= 30 us) before the first generation launch
         first = min((a for a, b, n in gpu if "draw_" in n or "fused_gen" in n), default=t1)
         for e in sorted(cpu, key=lambda e: e["ts"]):

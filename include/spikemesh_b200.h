@@ -35,6 +35,10 @@ int smx_stream_sync(void* stream);
  * (cudaDeviceScheduleSpin = 1, Yield = 2, BlockingSync = 4) */
 int smx_set_sync_policy(int flags);
 /* keep the default stream-ordered pool's memory mapped (no trim at sync) */
+/* A non-blocking stream (no implicit synchronisation with the legacy
+ * default stream) at the given priority; the engine runs the fused path's
+ * pass A and the preparation side work on such streams. */
+int smx_stream_create(int priority, void** out);
 int smx_pool_setup(int device);
 /* device error word of asynchronous paths: read + clear (synchronises stream) */
 int smx_check_device_errors(void* stream);

@@ -9,6 +9,10 @@
 
 #include <atomic>
 #include <cstdint>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
 
 static thread_local char g_err[1024] = {0};
 static std::atomic<uint64_t> g_launches{0};
@@ -32,6 +36,72 @@ extern "C" int smx_last_error(char* buf, size_t cap) {
   return (int)strlen(buf);
 }
 
+// Host -> device copy of a small host array without the pageable-copy
+// semantics (a pageable cudaMemcpyAsync first waits for the stream to drain,
+// blocking the host behind every queued kernel): the bytes are staged in a
+// pinned block that is reused once its previous copy has completed.
+namespace {
+struct Staging {
+  char* p;
+  size_t cap;
+  cudaEvent_t ev;
+  int device;
+};
+std::mutex g_stage_mu;
+std::vector<Staging> g_stage;
+}  // namespace
+
+int smx_h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return 0;
+  int dev = 0;
+  SMX_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_stage_mu);
+  Staging* s = nullptr;
+  for (auto& b : g_stage)
+    if (b.device == dev && b.cap >= bytes && cudaEventQuery(b.ev) == cudaSuccess) {
+      s = &b;
+      break;
+    }
+  if (!s) {
+    Staging b{nullptr, bytes < (64u << 10) ? (size_t)(64u << 10) : bytes, nullptr, dev};
+    SMX_CUDA_CHECK(cudaHostAlloc((void**)&b.p, b.cap, cudaHostAllocPortable));
+    SMX_CUDA_CHECK(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+    g_stage.push_back(b);
+    s = &g_stage.back();
+  }
+  memcpy(s->p, src, bytes);
+  SMX_CUDA_CHECK(cudaMemcpyAsync(dst, s->p, bytes, cudaMemcpyHostToDevice, st));
+  SMX_CUDA_CHECK(cudaEventRecord(s->ev, st));
+  return 0;
+}
+
+// Long-kernel tracking: pass A (fused.cu) keeps all but a few CTA slots of
+// the GPU for its whole run.  A kernel launched on another stream meanwhile
+// only completes once every one of its CTAs has been placed, so the ticketed
+// draw kernels launched while pass A is in flight use a grid that fits the
+// free slots (their tiles are taken by ticket: any grid size is correct).
+namespace {
+constexpr int MAX_DEVICES = 64;
+cudaEvent_t g_long_ev[MAX_DEVICES] = {};
+}  // namespace
+
+void smx_long_kernel_mark(cudaStream_t st) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= MAX_DEVICES) return;
+  if (!g_long_ev[dev] && cudaEventCreateWithFlags(&g_long_ev[dev], cudaEventDisableTiming) != cudaSuccess) {
+    g_long_ev[dev] = nullptr;
+    return;
+  }
+  cudaEventRecord(g_long_ev[dev], st);
+}
+
+int smx_grid_cap(int grid, int concurrent_cap) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= MAX_DEVICES || !g_long_ev[dev]) return grid;
+  if (cudaEventQuery(g_long_ev[dev]) != cudaErrorNotReady) return grid;
+  return grid < concurrent_cap ? grid : concurrent_cap;
+}
+
 extern "C" const char* smx_version(void) { return "spikemesh-b200 0.1.0 sm_100a"; }
 
 // Host-thread wait policy for synchronisations (must run before the CUDA
@@ -48,12 +118,35 @@ extern "C" int smx_set_sync_policy(int flags) {
 // Keep the stream-ordered allocator's freed memory mapped between calls
 // (release threshold = max): without it every synchronisation trims the
 // default pool and the next cudaMallocAsync re-maps physical pages.
+// A stream that does not synchronise with the legacy default stream (the one
+// torch's default stream is): work on it runs beside the default stream's
+// kernels instead of serialising with them.
+extern "C" int smx_stream_create(int priority, void** out) {
+  cudaStream_t s;
+  cudaError_t e = cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority);
+  if (e != cudaSuccess) {
+    smx_set_error("stream create: %s", cudaGetErrorString(e));
+    return -3;
+  }
+  *out = (void*)s;
+  return 0;
+}
+
 extern "C" int smx_pool_setup(int device) {
   cudaMemPool_t pool;
   cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
   if (e == cudaSuccess) {
     uint64_t thr = ~0ULL;
     e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (e == cudaSuccess) {
+    // no reuse through inserted dependencies: a block freed on the
+    // generation stream behind a long pass-A kernel would otherwise be
+    // handed to an allocation on another stream together with a wait on that
+    // kernel, serialising the streams (opportunistic reuse of blocks whose
+    // free has completed stays on)
+    int no = 0;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
   }
   if (e != cudaSuccess) {
     smx_set_error("mempool setup: %s", cudaGetErrorString(e));

@@ -326,6 +326,12 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* ws, ui
 // unit (defined in capi.cu).
 extern "C" void smx_set_error(const char* fmt, ...);
 extern "C" void smx_count_launch(void);
+// pinned-staged host -> device copy (capi.cu): never blocks the host
+int smx_h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
+// long persistent kernel in flight (capi.cu): smx_long_kernel_mark records
+// its end; smx_grid_cap(grid, cap) returns min(grid, cap) while it runs
+void smx_long_kernel_mark(cudaStream_t st);
+int smx_grid_cap(int grid, int concurrent_cap);
 extern "C" int* smx_device_error_word(void);
 #define SMX_CUDA_CHECK(expr)                                                       \
   do {                                                                             \

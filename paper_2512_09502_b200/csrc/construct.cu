@@ -541,7 +541,7 @@ extern "C" int smx_assign_images(const uint32_t* vbits, uint64_t nwords, const v
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&segs, sizeof(Segment) * ns, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&cnt, sizeof(uint32_t) * nwords, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&excl, sizeof(int64_t) * (nwords + 1), st));
-  SMX_CUDA_CHECK(cudaMemcpyAsync(segs, segs_host, sizeof(Segment) * ns, cudaMemcpyHostToDevice, st));
+  if (smx_h2d_async(segs, segs_host, sizeof(Segment) * ns, st)) return -3;
   smx_count_launch(); new_counts_kernel<<<nblk(nwords), T256, 0, st>>>(vbits, nwords, segs, ns, cnt);
   SMX_LAUNCH_CHECK();
   if (int rc = smx_counts_to_offsets(cnt, nwords, excl, st)) return rc;
@@ -632,7 +632,7 @@ extern "C" int smx_build_routes(const void* tabs_host, int nt, uint64_t n_nodes,
   *n_entries = 0;
   RouteTable* tabs = nullptr;
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&tabs, sizeof(RouteTable) * (nt ? nt : 1), st));
-  if (nt) SMX_CUDA_CHECK(cudaMemcpyAsync(tabs, tabs_host, sizeof(RouteTable) * nt, cudaMemcpyHostToDevice, st));
+  if (nt && smx_h2d_async(tabs, tabs_host, sizeof(RouteTable) * nt, st)) return -3;
   if (n_nodes) {
     smx_count_launch(); route_count_kernel<<<nblk(n_nodes), T256, 0, st>>>(tabs, nt, n_nodes, cnt_scratch);
     SMX_LAUNCH_CHECK();

@@ -150,6 +150,11 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = (1u << lane) - 1;
   uint16_t* mycnt = wcnt + warp * BC;
+  if (SMX_FG_FREE_SMS > 0) {  // CTAs placed on the reserved SMs leave at once (tiles go by ticket)
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (smid >= 148u - SMX_FG_FREE_SMS) return;
+  }
   for (;;) {
     if (tid == 0) s_t = atomicAdd(g.ticket, 1u);
     if (tid < B) hist[tid] = 0;
@@ -348,11 +353,15 @@ int fg_launch(const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
   }
   // persistent CTAs on 140 of the 148 SMs: the replays and small kernels of
   // the calls that follow (their host code waits on them) run beside pass A
-  // instead of queueing behind it
-  const uint32_t grid = std::min<uint32_t>(n_tiles, (148u - SMX_FG_FREE_SMS) * SMX_FG_MIN_BLOCKS);
+  // instead of queueing behind it.  The grid fills every SM (the block
+  // scheduler spreads CTAs round-robin, so a smaller grid would leave half
+  // SMs, too small for a draw CTA); the CTAs that land on SMs 140..147 exit
+  // at once, leaving those SMs empty
+  const uint32_t grid = std::min<uint32_t>(n_tiles + SMX_FG_FREE_SMS * SMX_FG_MIN_BLOCKS, 148u * SMX_FG_MIN_BLOCKS);
   smx_count_launch();
   fused_gen_kernel<KM, LB, WIDE><<<grid, FG_THREADS, smem, st>>>(g, n_tiles);
   SMX_LAUNCH_CHECK();
+  smx_long_kernel_mark(st);
   return 0;
 }
 
@@ -913,7 +922,7 @@ extern "C" int smx_fused_sort(const uint64_t* rptr, const uint64_t* fill, const 
   }
   uint32_t* dfirst = nullptr;
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&dfirst, sizeof(uint32_t) * firsts.size(), st));
-  SMX_CUDA_CHECK(cudaMemcpyAsync(dfirst, firsts.data(), sizeof(uint32_t) * firsts.size(), cudaMemcpyHostToDevice, st));
+  if (smx_h2d_async(dfirst, firsts.data(), sizeof(uint32_t) * firsts.size(), st)) return -3;
   FusedSort s{};
   s.rptr = rptr;
   s.fill = fill;

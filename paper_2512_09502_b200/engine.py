@@ -19,6 +19,7 @@ Construction and preparation never communicate (check_construction_silent).
 """
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 import time
@@ -79,8 +80,18 @@ def _gen_stream(dev) -> "torch.cuda.Stream":
     call overlap the host work and small kernels of the calls that follow."""
     key = torch.device(dev).index
     if key not in _GEN_STREAMS:
-        _GEN_STREAMS[key] = torch.cuda.Stream(device=dev)
+        _GEN_STREAMS[key] = _nonblocking_stream(dev)
     return _GEN_STREAMS[key]
+
+
+def _nonblocking_stream(dev):
+    """A CUDA stream created with cudaStreamNonBlocking (csrc/capi.cu): it does
+    not serialise with the legacy default stream that torch's default stream
+    is, so its kernels run beside the default stream's small kernels."""
+    p = ctypes.c_void_p()
+    with torch.cuda.device(dev):
+        call("smx_stream_create", 0, ctypes.byref(p))
+    return torch.cuda.ExternalStream(p.value, device=dev)
 
 
 def _prep_stream(dev) -> "torch.cuda.Stream":
@@ -88,7 +99,7 @@ def _prep_stream(dev) -> "torch.cuda.Stream":
     caching-allocator pool is then reused by every Cluster)."""
     key = torch.device(dev).index
     if key not in _PREP_STREAMS:
-        _PREP_STREAMS[key] = torch.cuda.Stream(device=dev)
+        _PREP_STREAMS[key] = _nonblocking_stream(dev)
     return _PREP_STREAMS[key]
 
 
@@ -597,7 +608,7 @@ class Cluster:
         for i, (w, d, p) in enumerate(self.classes[:MAX_CLASSES]):
             cw[i] = w
             cm[i] = (d & 0xFFFFFF) | (p << 24)
-        return cw.to(dev), cm.to(torch.int32).to(dev)
+        return _up(cw.numpy(), dev), _up(cm.to(torch.int32).numpy(), dev)
 
     def _write_syn(self, st: _Rank, syn: SynSpec, port: int, base: int, n: int, syn_key):
         """Per-record weights/delays for wide ranks (sm/construction.py:157-176)."""
@@ -1830,8 +1841,8 @@ class Cluster:
                 cs = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), torch.cumsum(st.counts.long(), 0)])
             rng, cnt = d["acct"]
             m = int(rng[0])
-            los = torch.from_numpy(rng[1: 1 + m].astype(np.int64)).to(dev).clamp(max=st.n_nodes)
-            his = torch.from_numpy(rng[1 + m: 1 + 2 * m].astype(np.int64)).to(dev).clamp(max=st.n_nodes)
+            los = _up(rng[1: 1 + m].astype(np.int64), dev).clamp(max=st.n_nodes)
+            his = _up(rng[1 + m: 1 + 2 * m].astype(np.int64), dev).clamp(max=st.n_nodes)
             cnt.copy_(cs[his] - cs[los])
         z["keep"] = (rptr_t, fill, cls_map_t)
 
@@ -2716,7 +2727,6 @@ class Cluster:
 
 
 # ---------------------------------------------------------------- ctypes structs
-import ctypes  # noqa: E402
 
 
 class ctypes_segment(ctypes.Structure):

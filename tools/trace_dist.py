@@ -52,11 +52,28 @@ if rank == 0:
     for g, at, n in sorted(gaps, reverse=True)[:25]:
         ops = [e["name"] for e in cpu if e["ts"] <= at + g / 2 <= e["ts"] + e["dur"]]
         print(f"  gap {1e-3 * g:6.3f} ms at {1e-3 * (at - t0):7.2f} ms before {n[:40]:40s} cpu: {ops[-3:]}")
-    if os.environ.get("TIMELINE"):  # every GPU op >= 20 us: start, duration, stream, name
+    if os.environ.get("TIMELINE"):  # every GPU op >= 20 us: start, duration, stream, host launch time, name
+        launch = {e["args"]["correlation"]: e["ts"] for e in ev
+                  if e.get("cat") == "cuda_runtime" and "correlation" in e.get("args", {})}
         for e2 in sorted((e for e in ev if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")),
                          key=lambda e: e["ts"]):
             if e2["dur"] >= 20:
-                print(f"  gpu {1e-3 * (e2['ts'] - t0):7.2f} +{1e-3 * e2['dur']:7.3f} ms s{e2.get('tid')}  {e2['name'][:70]}")
+                lt = launch.get(e2.get("args", {}).get("correlation"))
+                ls = f"{1e-3 * (lt - t0):7.2f}" if lt is not None else "      ?"
+                print(f"  gpu {1e-3 * (e2['ts'] - t0):7.2f} +{1e-3 * e2['dur']:7.3f} ms s{e2.get('tid')} launched {ls}  "
+                      f"{e2['name'][:60]}")
+
+        fg = min((e for e in ev if e.get("ph") == "X" and e.get("cat") == "kernel" and "fused_gen" in e["name"]),
+                 key=lambda e: e["ts"], default=None)
+        if fg is not None:  # everything the GPU and the runtime did while the first pass A ran
+            w0, w1 = fg["ts"], fg["ts"] + fg["dur"] + 300
+            for e2 in sorted((e for e in ev if e.get("ph") == "X" and w0 <= e["ts"] <= w1 and
+                              e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset", "cuda_runtime", "cuda_driver")),
+                             key=lambda e: e["ts"]):
+                lt = launch.get(e2.get("args", {}).get("correlation"))
+                ls = f"{1e-3 * (lt - t0):7.2f}" if lt is not None and e2.get("cat") != "cuda_runtime" else "      -"
+                print(f"  win {e2.get('cat')[:7]:7s} {1e-3 * (e2['ts'] - t0):7.2f} +{1e-3 * e2['dur']:7.3f} ms "
+                      f"s{e2.get('tid')} launched {ls}  {e2['name'][:60]}")
         for e2 in sorted(cpu, key=lambda e: e["ts"]):
             if e2.get("cat") == "python_function" and e2["dur"] >= 300 and "engine.py" in e2["name"]:
                 print(f"  cpu {1e-3 * (e2['ts'] - t0):7.2f} +{1e-3 * e2['dur']:7.3f} ms  {e2['name'][:80]}")

@@ -1,6 +1,7 @@
-"""Device keyed-stream draws (thin wrappers over the C ABI), numpy-exact:
-raw Philox words, Generator.integers, per-gid init-v normals and the
-Poisson drive's counts.  Used by the engine and by the parity tests."""
+"""Test helper: the library's keyed-stream draw entry points (raw Philox
+words, Generator.integers, per-gid init-v normals, the Poisson drive's
+counts) called one by one through the C ABI, so the parity tests can compare
+each against numpy / the oracle.  Not part of the product package."""
 from __future__ import annotations
 
 import math
@@ -8,9 +9,9 @@ import math
 import numpy as np
 import torch
 
-from . import _lib
-from ._lib import call
-from .api import canonical_bytes
+from paper_2512_09502_b200 import _lib
+from paper_2512_09502_b200._lib import call
+from paper_2512_09502_b200.api import canonical_bytes
 
 
 def _stream(dev):

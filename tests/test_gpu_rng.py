@@ -17,7 +17,7 @@ def _keys(z):
 
 
 def test_words_golden():
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     z = np.load(GOLDEN)
     for i, k in _keys(z):
         got = dr.words(k, 0, 64).cpu().numpy().view(np.uint64)
@@ -27,7 +27,7 @@ def test_words_golden():
 
 
 def test_integers_golden_with_cursor():
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     z = np.load(GOLDEN)
     for i, k in _keys(z):
         cur = 0
@@ -43,7 +43,7 @@ def test_integers_golden_with_cursor():
                                      (0, 2, 100_001), (0, 2**32, 5000)])
 def test_integers_vs_oracle_large(lo, hi, n):
     from oracle.rng import OracleStream
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     from paper_2512_09502_b200.api import stream_key
     k = stream_key(99, ("big", lo, n))
     o = OracleStream(0, key=k)
@@ -58,7 +58,7 @@ def test_integers_vs_oracle_large(lo, hi, n):
 
 
 def test_init_v_golden():
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     z = np.load(GOLDEN)
     gids = z["initv/gids"]
     for seed in (11, 12345):
@@ -68,7 +68,7 @@ def test_init_v_golden():
 
 def test_init_v_vs_oracle_many():
     from oracle.rng import OracleStream
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     gids = np.arange(0, 20000, 7, dtype=np.int64)
     want = np.array([OracleStream(5, ("init-v", int(g))).normal(-58.0, 5.0) for g in gids])
     got = dr.init_v(5, gids, -58.0, 5.0).cpu().numpy()
@@ -76,7 +76,7 @@ def test_init_v_vs_oracle_many():
 
 
 def test_poisson_golden_steps():
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     z = np.load(GOLDEN)
     for i, k in _keys(z):
         ps = dr.PoissonStream(k, 1.1)
@@ -90,7 +90,7 @@ def test_poisson_golden_steps():
                                            (10.0, 300_000, 2), (27.5, 300_000, 2), (150.0, 200_000, 2)])
 def test_poisson_vs_oracle_large(lam, n, batches):
     from oracle.rng import OracleStream
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     from paper_2512_09502_b200.api import stream_key
     k = stream_key(3, ("poisson", 0, int(lam * 10)))
     o = OracleStream(0, key=k)
@@ -105,7 +105,7 @@ import sys
 import numpy as np
 sys.path.insert(0, sys.argv[1])
 from oracle.rng import OracleStream
-from paper_2512_09502_b200 import device_rng as dr
+import device_rng as dr
 from paper_2512_09502_b200.api import stream_key
 for lo, hi, n in [(0, 8000, 1_000_000), (7, 3_000_000_007, 200_000), (0, 2, 100_001), (0, 100_000, 2047),
                   (0, 100_000, 2048), (0, 100_000, 2049), (0, 2**32, 5000), (5, 9, 1)]:
@@ -145,7 +145,7 @@ def test_normal_slow_paths_at_scale(seed):
     """1e7 ziggurat normals from one stream (~1.5e5 wedge/tail samples, the
     branches that call exp / log1p) bit-exact against the oracle (glibc)."""
     from oracle.rng import OracleStream
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     from paper_2512_09502_b200.api import stream_key
     k = stream_key(seed, ("normal-scale", seed))
     o = OracleStream(0, key=k)
@@ -161,7 +161,7 @@ def test_ptrs_at_scale(lam):
     """numpy's PTRS sampler (lam >= 10, CUDA log in the squeeze test):
     1e7 samples bit-exact against the oracle."""
     from oracle.rng import OracleStream
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     from paper_2512_09502_b200.api import stream_key
     k = stream_key(8, ("ptrs-scale", int(lam)))
     o = OracleStream(0, key=k)
@@ -174,7 +174,7 @@ def test_init_v_many_gids():
     """Per-gid init-v streams (blake2b on the device) for 2e5 gids spread over
     0 .. 4.1e6 (the C4 neuron count) against the oracle."""
     from oracle.rng import OracleStream
-    from paper_2512_09502_b200 import device_rng as dr
+    import device_rng as dr
     gids = np.unique(np.random.default_rng(5).integers(0, 4_130_000, 200_000)).astype(np.int64)
     want = np.array([OracleStream(12345, ("init-v", int(g))).normal(-58.0, 5.0) for g in gids])
     got = dr.init_v(12345, gids, -58.0, 5.0).cpu().numpy()

@@ -2,8 +2,9 @@
 import sys, os
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 from oracle.rng import OracleStream
-from paper_2512_09502_b200 import device_rng as dr
+import device_rng as dr
 from paper_2512_09502_b200.api import stream_key
 for seed in (1, 2):
     k = stream_key(seed, ("normal-scale", seed))

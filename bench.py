@@ -52,7 +52,11 @@ def parse():
                     help="strong scaling: --neurons is the whole network, split over the GPUs")
     ap.add_argument("--cpu-sample-neurons", type=int, default=5_000)
     ap.add_argument("--cpu-sample-k-scale", type=float, default=0.1)
-    ap.add_argument("--workload", default="c3", choices=["c3", "c5"],
+    ap.add_argument("--c4-areas", type=int, default=0,
+                    help="C4 areas (default 4 per GPU: the per-GPU load of the 32-area model on 8 GPUs)")
+    ap.add_argument("--c4-neurons", type=int, default=129_063)
+    ap.add_argument("--c4-k", default="3600,900,44", help="k_intra_exc,k_intra_inh,k_inter (SURVEY §8 C4)")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c5"],
                     help="c3: the headline (hpc_benchmark weak scaling); c5: construction-only sweep")
     ap.add_argument("--c5-points", default="1e8,3e8,1e9,3e9,1e10")
     ap.add_argument("--c5-rules", default="fixed_indegree,fixed_total")
@@ -476,10 +480,104 @@ def run_c5(args):
         dist.destroy_process_group()
 
 
+def run_c4(args):
+    """BASELINE configs[3]: the multi-area model of
+    sm/models.py:349-403 -- areas of ~1.29e5 neurons packed onto the ranks
+    by pack_areas (sm/models.py:290-306), local E/I circuits plus k_inter
+    remote E inputs for every ordered area pair, point-to-point exchange.
+    One JSON line: construction (device span, max over ranks; host wall; the
+    host share = time inside the façade calls / wall), then the RTF of a
+    propagation window."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_09502_b200 import api, engine, models
+
+    world, rank, local = dist_info()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    n_areas = args.c4_areas or 4 * world
+    ke, ki, kx = (int(x) for x in args.c4_k.split(","))
+    per_in = ke + ki + kx * (n_areas - 1)
+    areas = [models.AreaSpec(f"A{i:02d}", args.c4_neurons, args.c4_neurons * per_in) for i in range(n_areas)]
+    assignment, _ = models.pack_areas(areas, world)
+    params = models.MultiAreaParams(k_intra_exc=ke, k_intra_inh=ki, k_inter=kx, delay_steps=15)
+    cfg = api.SimConfig(n_ranks=world, comm_mode="p2p", seed=args.seed)
+    mine = [a for a in areas if assignment[a.area_id] == rank]
+    syn_rank = sum(a.neurons * per_in for a in mine)
+    syn_total = sum(a.neurons * per_in for a in areas)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    c = None
+    span, wall, host, kern, gen, srt = [], [], [], [], [], []
+    for i in range(args.warmup + args.steps):
+        del c
+        gc.collect()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        c = engine.Cluster(cfg, profile=True)
+        models.build_multi_area(c, areas, assignment, params)
+        c.prepare()
+        e1.record()
+        n_rec = int(c.ranks[rank].first_index[-1].item())
+        w = time.perf_counter() - t0
+        torch.cuda.synchronize(dev)
+        assert n_rec == syn_rank, (n_rec, syn_rank)
+        if i >= args.warmup:
+            span.append(max_over_ranks(e0.elapsed_time(e1)))
+            wall.append(max_over_ranks(w))
+            host.append(max_over_ranks(sum(h for _, h, _ in c.timers._pending)))
+            gen.append(max_over_ranks(c.kernel_ms("gen")))
+            srt.append(max_over_ranks(c.kernel_ms("sort")))
+            kern.append(max_over_ranks(c.kernel_ms("gen") + c.kernel_ms("sort")))
+    peak = torch.cuda.max_memory_allocated(dev)
+    rep = c.simulate(args.prop_warmup_ms, args.model_ms, record=False)
+    rtf = max_over_ranks(rep.rtf)
+    c.simulate(0.0, args.model_ms, record=True)
+    n_spk = len(c.rank_events(rank))
+    n_rank_neurons = sum(a.neurons for a in mine)
+    ms = float(np.mean(span))
+    line = {"metric": "construction_synapses_per_s", "value": syn_total / (ms * 1e-3), "unit": "synapses/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "data": "synthetic",
+            "config": {"workload": "multi_area_C4", "areas": n_areas, "areas_per_gpu": len(mine),
+                       "neurons_per_area": args.c4_neurons, "k": [ke, ki, kx], "synapses_total": syn_total,
+                       "synapses_rank0": syn_rank, "comm": "p2p", "parallelism": f"ranks{world}",
+                       "remote_calls": n_areas * (n_areas - 1), "store_path": c.ranks[rank].store_path},
+            "construction_wall_s": float(np.mean(wall)),
+            "facade_s": float(np.mean(host)),
+            "non_kernel_share": 1.0 - float(np.mean(kern)) / (1e3 * float(np.mean(wall))),
+            "gen_sort_kernel_ms": float(np.mean(kern)),
+            "phase_ms": {"gen": float(np.mean(gen)), "sort": float(np.mean(srt))},
+            "peak_device_bytes": int(peak), "rtf": rtf, "rtf_model_ms": args.model_ms,
+            "n_spikes_rank0": n_spk, "rate_hz_rank0": n_spk / (n_rank_neurons * args.model_ms * 1e-3)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        c.close()
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.workload == "c5":
         run_c5(args)
+    elif args.workload == "c4":
+        run_c4(args)
     elif args.impl == "reference":
         run_reference(args)
     else:

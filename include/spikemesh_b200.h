@@ -174,9 +174,12 @@ int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_out, int key
  * at rptr[region], fill[region] records): stable scatter by the high digit
  * (hi_bits 8..11) writing out[] = row | cls_map[class index] in key order
  * and counts[key] (key = hi << lo_bits | digit; first_index via
- * smx_counts_to_offsets).  rcap_host: host copy of the capacities. */
+ * smx_counts_to_offsets).  rcap_host: host copy of the capacities;
+ * row_bits_host[call] (host, per_digit <= 512 entries): the call's payload
+ * split, class index << row_bits | row (rows fixed at the call's time). */
 int smx_fused_sort(const uint64_t* rptr, const uint64_t* fill, const uint64_t* rcap_host, int per_digit,
-                   int lo_bits, int hi_bits, int pbits, int row_bits, const uint32_t* cls_map, uint32_t* counts,
+                   int lo_bits, int hi_bits, int pbits, const uint8_t* row_bits_host, const uint32_t* cls_map,
+                   uint32_t* counts,
                    uint64_t n_keys, uint64_t n_records, uint32_t* out, int* err, void* stream);
 /* ConnectionStore.finalize: stable sort of pending records by source. */
 int smx_sort_records(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, uint64_t n,

@@ -398,6 +398,7 @@ constexpr int FB_WARPS = FB_THREADS / 32;
 constexpr int FB_IPT = 15;
 constexpr int FB_TILE = FB_THREADS * FB_IPT;   // 7680 records
 constexpr int FB_TC = 256;                     // tiles per scan chunk (chunks never straddle regions)
+constexpr int FB_MAX_CALLS = 512;              // calls (regions per low digit) one pass B takes
 
 struct FusedSort {
   const uint64_t* rptr;       // [R] region base pointers, regions in (low digit, call) order
@@ -406,14 +407,14 @@ struct FusedSort {
   const uint32_t* chunk_first;// [R + 1] first scan chunk of each region
   uint32_t n_regions;
   uint32_t per_digit;         // regions per low digit (one per call)
-  int pbits;                  // record = hi << pbits | class index << row_bits | row
-  int row_bits;
+  int pbits;                  // record = hi << pbits | class index << row bits | row
   int lo_bits;                // key = hi << lo_bits | region
-  const uint32_t* cls_map;    // [2^(pbits - row_bits)] class index -> global class id << 24
+  const uint32_t* cls_map;    // [256] class index -> global class id << 24
   uint32_t* counts;           // [n_keys] records per key
   uint64_t n_keys;
   uint32_t* out;              // final payload (sorted by key)
   int* err;
+  uint8_t row_bits[FB_MAX_CALLS];  // per call: payload = class index << row_bits[call] | row
 };
 
 __device__ __forceinline__ uint32_t upper_region(const uint32_t* first, uint32_t n, uint32_t x) {
@@ -635,9 +636,7 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = (1u << lane) - 1;
-  const uint32_t rmask = (1u << s.row_bits) - 1;
-  const uint32_t cmask = (1u << (s.pbits - s.row_bits)) - 1;
-  for (int i = tid; i <= (int)cmask; i += FB_THREADS) cmap[i] = s.cls_map[i];
+  for (int i = tid; i < 256; i += FB_THREADS) cmap[i] = s.cls_map[i];
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -668,6 +667,10 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
   for (uint32_t T = ticket[0]; T < n_tiles; T = ticket[slot ^= 1]) {
     const FbTile x = tinfo[slot];
     const bool full = x.n == FB_TILE;
+    // the tile's call (regions are in (low digit, call) order) fixes its row / class split
+    const int rbits = s.row_bits[x.region % s.per_digit];
+    const uint32_t rmask = (1u << rbits) - 1;
+    const uint32_t cmask = (1u << (s.pbits - rbits < 8 ? s.pbits - rbits : 8)) - 1;
     mbar_wait(&bar, phase);
     phase ^= 1;
     uint32_t rec[FB_IPT];
@@ -728,7 +731,7 @@ __global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(con
       if (r != 0xffffu) {
         const uint32_t d = (rec[i] >> s.pbits) & mask;
         const uint32_t pos = mycnt[d] + r;
-        irec[pos] = (rec[i] & rmask) | cmap[(rec[i] >> s.row_bits) & cmask];
+        irec[pos] = (rec[i] & rmask) | cmap[(rec[i] >> rbits) & cmask];
         sdig[pos] = (uint16_t)d;
       }
     }
@@ -889,7 +892,7 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
 // by key = hi << lo_bits | digit) and counts[key] (zeroed first).  err
 // receives 6 for a key >= n_keys, 7 when a digit holds >= 2^32 records.
 extern "C" int smx_fused_sort(const uint64_t* rptr, const uint64_t* fill, const uint64_t* rcap_host, int per_digit,
-                              int lo_bits, int hi_bits, int pbits, int row_bits,
+                              int lo_bits, int hi_bits, int pbits, const uint8_t* row_bits_host,
                               const uint32_t* cls_map, uint32_t* counts, uint64_t n_keys, uint64_t n_records,
                               uint32_t* out, int* err, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -931,12 +934,18 @@ extern "C" int smx_fused_sort(const uint64_t* rptr, const uint64_t* fill, const 
   s.n_regions = R;
   s.per_digit = (uint32_t)per_digit;
   s.pbits = pbits;
-  s.row_bits = row_bits;
   s.lo_bits = lo_bits;
   s.cls_map = cls_map;
-  if (pbits - row_bits > 8) {
-    smx_set_error("smx_fused_sort: more than 256 classes");
+  if (per_digit > FB_MAX_CALLS) {
+    smx_set_error("smx_fused_sort: more than %d calls", FB_MAX_CALLS);
     return -1;
+  }
+  for (int c = 0; c < per_digit; ++c) {
+    if (row_bits_host[c] < 1 || row_bits_host[c] > pbits) {
+      smx_set_error("smx_fused_sort: call %d: %d row bits of %d payload bits", c, (int)row_bits_host[c], pbits);
+      return -1;
+    }
+    s.row_bits[c] = row_bits_host[c];
   }
   const bool wide = n_records >= 0xffffffffull;
   s.counts = counts;

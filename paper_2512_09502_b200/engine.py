@@ -715,6 +715,9 @@ class Cluster:
         keys = st.keys.t[base:]
         vals = (st.w_rows.t if st.wide else st.vals.t)[base:]
         cur = np.zeros(1, dtype=np.uint64)
+        # the stream cursor comes back to the host (a synchronisation) only
+        # when a later draw continues the same stream
+        cur_out = cur.ctypes.data if (autapse_fix or rule == "fixed_total") else 0
         sk = st.stream
         ev0 = self._event(st) if self.prof is not None else None
         if n:
@@ -732,10 +735,10 @@ class Cluster:
             elif rule == "fixed_indegree":
                 call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 2, _ptr(key_tab),
                      _ptr(pay_tab), int(conn.k_in), _ptr(keys), _ptr(vals), _ptr(pos_bits), 0,
-                     _words(n_src), 0, 0, 0, cur.ctypes.data, sk)
+                     _words(n_src), 0, 0, 0, cur_out, sk)
             elif rule == "fixed_outdegree":
                 call("smx_gen_draw", local_key[0], local_key[1], 0, n_tgt, n, 2, 1, _ptr(key_tab),
-                     _ptr(pay_tab), int(conn.k_out), _ptr(keys), _ptr(vals), 0, 0, 0, 0, 0, 0, cur.ctypes.data, sk)
+                     _ptr(pay_tab), int(conn.k_out), _ptr(keys), _ptr(vals), 0, 0, 0, 0, 0, 0, cur_out, sk)
             else:  # fixed_total: positions (aligned) then targets (local; same stream locally)
                 call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 0, _ptr(key_tab),
                      0, 1, _ptr(keys), 0, _ptr(pos_bits), 0, _words(n_src), 0, 0, 0, cur.ctypes.data, sk)
@@ -862,7 +865,10 @@ class Cluster:
         n_rec = 0
         used_pos = None
         span = int(sources.max()) + 1
-        if self.is_local(tr):
+        if self.is_local(tr) and self._remote_defer_ok(self.ranks[tr], conn, syn, port, n_src, n_tgt):
+            n_rec, used_pos = self._remote_deferred(self.ranks[tr], sr, sources, targets, conn, syn, port, group,
+                                                    k_src, flag, span)
+        elif self.is_local(tr):
             st = self.ranks[tr]
             dev = st.device
             pos_bits = torch.zeros(_words(n_src), dtype=torch.int32, device=dev) if flag else None
@@ -903,6 +909,39 @@ class Cluster:
                     ros = ms.rosters.setdefault((group, sr), _Bits(ms.device)).ensure(span)
                     call("smx_mark_values", 0, _ptr(src_dev), n_src, _ptr(ros.t), ms.stream)
         return n_rec
+
+    def _remote_defer_ok(self, st: _Rank, conn, syn, port, n_src, n_tgt) -> bool:
+        return (conn.rule == "fixed_indegree" and conn.allow_multapses and
+                self._defer_ok(st, self._syn_class(st, syn, port), n_src, int(conn.k_in) * n_tgt))
+
+    def _remote_deferred(self, st: _Rank, sr, sources, targets, conn, syn, port, group, k_src, flag, span):
+        """Target side of a remote fixed in-degree call on the fused path
+        (sm/construction.py:550-612): the images come first -- every source
+        (unflagged call) or the used ones, from a marking-only replay of the
+        position draws (flagged call) -- so the call's keys are final image
+        ids and its draws go to pass A like a local call's."""
+        dev = st.device
+        n_src, n_tgt = len(sources), len(targets)
+        k_in = int(conn.k_in)
+        cls = self._syn_class(st, syn, port)
+        src_dev = _up_index(sources, dev)
+        pos_bits = self._replay_positions(st, conn, n_src, n_tgt, k_src) if flag else None
+        vbits = torch.zeros(_words(span), dtype=torch.int32, device=dev)
+        call("smx_mark_values", _ptr(pos_bits), _ptr(src_dev), n_src, _ptr(vbits), st.stream)
+        m = st.map_for(group, sr)
+        m.ensure(span)
+        self._assign(st, vbits, [(0, _words(span), m)])
+        key_tab = torch.empty(n_src, dtype=torch.int32, device=dev)
+        call("smx_gather_lut", _ptr(src_dev), n_src, _ptr(m.img_of.t), _ptr(key_tab), st.stream)
+        self._check_real_targets(st, targets)
+        tgt = _up_index(targets, dev)
+        pay_tab = torch.empty(n_tgt, dtype=torch.int32, device=dev)
+        call("smx_pay_table", _ptr(tgt), n_tgt, _ptr(st.node2row.t), st.node2row.n, cls & 0xFF, _ptr(pay_tab),
+             st.stream)
+        n = k_in * n_tgt
+        self._defer(st, k_src, n_src, n, 1, key_tab, pay_tab, k_in, n_tgt, cls, src_host=key_tab.cpu().numpy())
+        st.mem.later("remote_batch", n_src, (int(group), sr), _popcount_dev(m.present.view()), n)
+        return n, pos_bits
 
     def _replay_positions(self, ss: _Rank, conn, n_src, n_tgt, k_src):
         """Source-side replay of the aligned position draws (sm/construction.py:620-627)."""
@@ -1723,18 +1762,19 @@ class Cluster:
             env_lo = os.environ.get("SMX_FUSED_LO")
             lo = int(env_lo) if env_lo is not None else (
                 0 if key_bits <= 11 else max(key_bits - 11, min(9, key_bits - 8)))
-            row_bits = max(1, int(st.n_real - 1).bit_length())
-            cls_bits = min(8, 20 - row_bits)   # keeps hi (<= 11 bits) + payload within 31 bits
-            if lo > 9 or cls_bits < 0:
+            if lo > 9:
                 return False
-            z = st.fz = dict(lo=lo, row_bits=row_bits, cls_bits=cls_bits, pbits=row_bits + cls_bits, cidx={},
-                             calls=[], flag=torch.zeros(2, dtype=torch.int64, device=dev))
-        if st.n_real > (1 << z["row_bits"]):
+            # payload of 20 bits (with the <= 11-bit high digit: 31-bit records)
+            z = st.fz = dict(lo=lo, pbits=20, cidx={}, calls=[], flag=torch.zeros(2, dtype=torch.int64, device=dev))
+        # the call's payload split: its target rows (real neurons so far) in
+        # the low bits, the class index above (pass B decodes per call)
+        row_bits = max(1, int(st.n_real - 1).bit_length())
+        if row_bits > z["pbits"] or len(z["calls"]) >= 512:
             return False
         if d["cls"] not in z["cidx"]:
-            if len(z["cidx"]) >= (1 << z["cls_bits"]):
-                return False
             z["cidx"][d["cls"]] = len(z["cidx"])
+        if z["cidx"][d["cls"]] >= (1 << min(8, z["pbits"] - row_bits)):
+            return False
         B = 1 << z["lo"]
         p = self._digit_probs(d, B)
         n = float(d["n"])
@@ -1752,7 +1792,7 @@ class Cluster:
         meta = _up(np.concatenate([rstart, cap]), dev)
         fills = torch.zeros((2, B), dtype=torch.int64, device=dev)
         total = torch.zeros(1, dtype=torch.int64, device=dev)
-        cpay = (d["pay_tab"] & ROW_MASK) | (z["cidx"][d["cls"]] << z["row_bits"])   # row | class index
+        cpay = (d["pay_tab"] & ROW_MASK) | (z["cidx"][d["cls"]] << row_bits)   # row | class index
         # pass A runs on the generation stream: the main stream keeps only the
         # small map / image kernels that the preparation side stream waits on
         gen = _gen_stream(dev)
@@ -1773,7 +1813,7 @@ class Cluster:
         if d["kmode"] == 1:
             d["ktab"].record_stream(gen)
         z["calls"].append(dict(region=region, rstart=rstart, cap=cap.astype(np.uint64), meta=meta, fill=fills[1],
-                               fills=fills, total=total, cpay=cpay, n=int(d["n"])))
+                               fills=fills, total=total, cpay=cpay, n=int(d["n"]), row_bits=row_bits))
         return True
 
     def _fused_ready(self, st: _Rank) -> bool:
@@ -1823,8 +1863,9 @@ class Cluster:
         st.counts = torch.empty(max(st.n_nodes, 1), dtype=torch.int32, device=dev)
         st.payload = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         ev0 = self._event(st) if self.prof is not None else None
+        rbits = np.array([zc["row_bits"] for zc in calls], dtype=np.uint8)
         call("smx_fused_sort", _ptr(rptr_t), _ptr(fill), rcap.ctypes.data, C, z["lo"], z["hi"], z["pbits"],
-             z["row_bits"], _ptr(cls_map_t), _ptr(st.counts), st.n_nodes, n, _ptr(st.payload), _ptr(z["flag"][1:]), sk)
+             rbits.ctypes.data, _ptr(cls_map_t), _ptr(st.counts), st.n_nodes, n, _ptr(st.payload), _ptr(z["flag"][1:]), sk)
         st.first_index = torch.empty(st.n_nodes + 1, dtype=torch.int64, device=dev)
         call("smx_counts_to_offsets", _ptr(st.counts), st.n_nodes, _ptr(st.first_index), sk)
         if self.prof is not None:

@@ -104,6 +104,7 @@ _VARIANT_SCRIPT = r"""
 import sys
 import numpy as np
 sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + "/tests")
 from oracle.rng import OracleStream
 import device_rng as dr
 from paper_2512_09502_b200.api import stream_key

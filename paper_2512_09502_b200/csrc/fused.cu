@@ -517,11 +517,46 @@ __global__ void __launch_bounds__(256) fb_region_sum_kernel(const __grid_constan
   }
 }
 
-// One CTA: per digit, exclusive scan over the regions (in place: rsum ->
-// region base within the digit) and the 64-bit digit bases.
+// The per-digit exclusive scan over the regions runs in three steps over
+// groups of FB_RG consecutive regions: group sums, one CTA scanning the
+// groups (and the 64-bit digit bases), then each group's regions.
+constexpr uint32_t FB_RG = 64;
+
 template <int BITS>
-__global__ void __launch_bounds__(1024) fb_region_scan_kernel(const __grid_constant__ FusedSort s, uint32_t* rsum,
-                                                              uint64_t* dbase) {
+__global__ void __launch_bounds__(256) fb_group_sum_kernel(const __grid_constant__ FusedSort s, const uint32_t* rsum,
+                                                           uint32_t* gsum) {
+  constexpr int BINS = 1 << BITS;
+  const uint32_t g = blockIdx.x;
+  const uint32_t r0 = g * FB_RG, r1 = min(s.n_regions, r0 + FB_RG);
+  for (int d = threadIdx.x; d < BINS; d += 256) {
+    uint64_t acc = 0;
+    for (uint32_t r = r0; r < r1; ++r) acc += rsum[(size_t)r * BINS + d];
+    if (acc > 0xffffffffull) atomicExch(s.err, 7);  // within-digit offsets are 32-bit
+    gsum[(size_t)g * BINS + d] = (uint32_t)acc;
+  }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(256) fb_group_apply_kernel(const __grid_constant__ FusedSort s, uint32_t* rsum,
+                                                             const uint32_t* gbase) {
+  constexpr int BINS = 1 << BITS;
+  const uint32_t g = blockIdx.x;
+  const uint32_t r0 = g * FB_RG, r1 = min(s.n_regions, r0 + FB_RG);
+  for (int d = threadIdx.x; d < BINS; d += 256) {
+    uint32_t run = gbase[(size_t)g * BINS + d];
+    for (uint32_t r = r0; r < r1; ++r) {
+      const uint32_t x = rsum[(size_t)r * BINS + d];
+      rsum[(size_t)r * BINS + d] = run;
+      run += x;
+    }
+  }
+}
+
+// One CTA: per digit, exclusive scan over the region groups (in place: gsum
+// -> group base within the digit) and the 64-bit digit bases.
+template <int BITS>
+__global__ void __launch_bounds__(1024) fb_region_scan_kernel(const __grid_constant__ FusedSort s, uint32_t* gsum,
+                                                              uint32_t n_groups, uint64_t* dbase) {
   constexpr int BINS = 1 << BITS;
   constexpr int DPT = (BINS + 1023) / 1024;
   __shared__ unsigned long long ws[32];
@@ -532,9 +567,9 @@ __global__ void __launch_bounds__(1024) fb_region_scan_kernel(const __grid_const
     uint64_t run = 0;
     if (d < BINS) {
 #pragma unroll 8
-      for (uint32_t r = 0; r < s.n_regions; ++r) {
-        const uint32_t x = rsum[(size_t)r * BINS + d];
-        rsum[(size_t)r * BINS + d] = (uint32_t)run;
+      for (uint32_t g = 0; g < n_groups; ++g) {
+        const uint32_t x = gsum[(size_t)g * BINS + d];
+        gsum[(size_t)g * BINS + d] = (uint32_t)run;
         run += x;
       }
       if (run > 0xffffffffull) atomicExch(s.err, 7);  // within-digit offsets are 32-bit
@@ -754,7 +789,8 @@ template <int BITS>
 int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, cudaStream_t st) {
   constexpr int BINS = 1 << BITS;
   uint16_t* tcnt = nullptr;
-  uint32_t *off = nullptr, *csum = nullptr, *ctr = nullptr, *rsum = nullptr;
+  uint32_t *off = nullptr, *csum = nullptr, *ctr = nullptr, *rsum = nullptr, *gsum = nullptr;
+  const uint32_t n_groups = (s.n_regions + FB_RG - 1) / FB_RG;
   uint64_t* dbase = nullptr;
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&tcnt, sizeof(uint16_t) * (size_t)n_tiles * BINS, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&off, sizeof(uint32_t) * (size_t)n_tiles * BINS, st));
@@ -762,6 +798,7 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, c
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&dbase, sizeof(uint64_t) * BINS, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&rsum, sizeof(uint32_t) * (size_t)s.n_regions * BINS, st));
   SMX_CUDA_CHECK(cudaMallocAsync((void**)&ctr, sizeof(uint32_t), st));
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&gsum, sizeof(uint32_t) * (size_t)n_groups * BINS, st));
   SMX_CUDA_CHECK(cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
   constexpr int HW = fb_hist_warps<BITS>();
   const size_t h_smem = (size_t)HW * BINS * 4;
@@ -783,7 +820,9 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, c
     smx_count_launch(); fb_chunk_sum_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum);
   }
   smx_count_launch(); fb_region_sum_kernel<BITS><<<s.n_regions, 256, 0, st>>>(s, csum, rsum);
-  smx_count_launch(); fb_region_scan_kernel<BITS><<<1, 1024, 0, st>>>(s, rsum, dbase);
+  smx_count_launch(); fb_group_sum_kernel<BITS><<<n_groups, 256, 0, st>>>(s, rsum, gsum);
+  smx_count_launch(); fb_region_scan_kernel<BITS><<<1, 1024, 0, st>>>(s, gsum, n_groups, dbase);
+  smx_count_launch(); fb_group_apply_kernel<BITS><<<n_groups, 256, 0, st>>>(s, rsum, gsum);
   smx_count_launch(); fb_chunk_base_kernel<BITS><<<s.n_regions, 256, 0, st>>>(s, csum, rsum);
   if (n_chunks) {
     smx_count_launch(); fb_tile_offsets_kernel<BITS><<<n_chunks, 256, 0, st>>>(s, tcnt, csum, off);
@@ -801,6 +840,7 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, c
   cudaFreeAsync(dbase, st);
   cudaFreeAsync(rsum, st);
   cudaFreeAsync(ctr, st);
+  cudaFreeAsync(gsum, st);
   return 0;
 }
 

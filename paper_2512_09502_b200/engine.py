@@ -59,6 +59,12 @@ def _up(arr, dev) -> torch.Tensor:
     return torch.from_numpy(a).pin_memory().to(dev, non_blocking=True)
 
 
+def _consecutive(a: np.ndarray) -> bool:
+    """a is one run first, first + 1, ... (the common population case)."""
+    n = len(a)
+    return n > 1 and int(a[-1]) - int(a[0]) == n - 1 and bool((np.diff(a) == 1).all())
+
+
 def _up_index(arr, dev) -> torch.Tensor:
     """int64 node-index upload; a consecutive run (the common population
     case) is materialised on the device from its first index instead of
@@ -561,6 +567,8 @@ class Cluster:
         starts = np.array([int(r[0]) for r in st.row2node], dtype=np.int64)
         ends = np.array([int(r[0]) + len(r) for r in st.row2node], dtype=np.int64)
         t = np.asarray(targets, dtype=np.int64)
+        if _consecutive(t):   # a population run: its two ends decide
+            t = t[[0, -1]]
         i = np.searchsorted(starts, t, side="right") - 1
         if (i < 0).any() or (t >= ends[np.maximum(i, 0)]).any():
             raise ValueError("connection targets must be real neurons of the target rank")
@@ -764,7 +772,8 @@ class Cluster:
         (this one included) goes through the general path instead."""
         lm_thr = 0 if ex == (1 << 32) else ((1 << 32) - ex) % ex
         d = dict(key=key, ex=int(ex), n=int(n), kmode=kmode, ktab=ktab, pay_tab=pay_tab, cls=int(cls),
-                 kdiv=int(kdiv), n_tgt=int(n_tgt), src_host=src_host, acct=acct, prej=lm_thr / 4294967296.0)
+                 kdiv=int(kdiv), n_tgt=int(n_tgt), src_host=src_host, acct=acct, prej=lm_thr / 4294967296.0,
+                 src_run=src_host is not None and _consecutive(np.asarray(src_host)))
         st.deferred.append(d)
         if not self._fused_eager(st, d):
             self._fused_off(st)
@@ -1725,6 +1734,8 @@ class Cluster:
         """Key intervals [a, b) a deferred call's draws can produce."""
         if d["kmode"] == 1:
             s = d["src_host"]
+            if d.get("src_run"):   # keys a, a + 1, ..., b - 1
+                return [(int(s[0]), int(s[-1]) + 1)]
             return [(int(s.min()), int(s.max()) + 1)]
         pc = d["ktab"]
         m = int(pc[0])
@@ -1738,7 +1749,7 @@ class Cluster:
         """Probability of each low key digit (key mod B) for one draw of a
         deferred call: uniform positions mapped to keys (exact)."""
         cnt = np.zeros(B, dtype=np.float64)
-        if d["kmode"] == 1:
+        if d["kmode"] == 1 and not d.get("src_run"):
             cnt += np.bincount(np.asarray(d["src_host"], dtype=np.int64) & (B - 1), minlength=B)
         else:
             for a, b in Cluster._call_key_ranges(d):

@@ -1,5 +1,5 @@
 set -x
-O=gpurun_out/c4c
+O=gpurun_out/c4d
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest.log 2>&1; tail -15 $O/pytest.log
 timeout 900 python bench.py --workload c4 --steps 1 --warmup 1 > $O/c4_n1.json 2> $O/c4_n1.err

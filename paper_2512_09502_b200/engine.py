@@ -252,6 +252,8 @@ class _Map:
     def __init__(self, device):
         self.img_of = _Buf(torch.int32, device, fill=-1)
         self.present = _Buf(torch.int32, device, fill=0)
+        # node-value intervals that may hold images (host-side knowledge, for _dist_speculate)
+        self.imaged: list = []
 
     def ensure(self, n_values: int):
         nw = _words(n_values)
@@ -402,6 +404,8 @@ class Cluster:
         self.min_remote_delay = None
         self.use_graphs = True
         self.fused_enabled = self.FUSED_ENABLED   # fused generation + sort (tests switch it off for A/B)
+        # distributed calls whose pass A started on predicted keys (_dist_speculate)
+        self.spec_stats = {"confirmed": 0, "redone": 0, "dropped": 0}
         self._graph = None
         self._xgraph_ok = None   # exchange captured in the block graph (None: not tried yet)
         self._pg = None
@@ -890,7 +894,7 @@ class Cluster:
                 used_pos = pos_bits
             m = st.map_for(group, sr)
             m.ensure(span)
-            self._assign(st, vbits, [(0, _words(span), m)])
+            self._assign(st, vbits, [(0, _words(span), m)], [[(int(sources.min()), span)]])
             st.lut.reserve(lut_base + n_src)
             call("smx_gather_lut", _ptr(src_dev), n_src, _ptr(m.img_of.t), _ptr(st.lut.t[lut_base:]), st.stream)
             st.lut.n = lut_base + n_src
@@ -939,7 +943,7 @@ class Cluster:
         call("smx_mark_values", _ptr(pos_bits), _ptr(src_dev), n_src, _ptr(vbits), st.stream)
         m = st.map_for(group, sr)
         m.ensure(span)
-        self._assign(st, vbits, [(0, _words(span), m)])
+        self._assign(st, vbits, [(0, _words(span), m)], [[(int(sources.min()), span)]])
         key_tab = torch.empty(n_src, dtype=torch.int32, device=dev)
         call("smx_gather_lut", _ptr(src_dev), n_src, _ptr(m.img_of.t), _ptr(key_tab), st.stream)
         self._check_real_targets(st, targets)
@@ -967,11 +971,21 @@ class Cluster:
                  _words(n_src), 0, 0, 0, cur.ctypes.data, ss.stream)
         return pb
 
-    def _assign(self, st: _Rank, vbits, segs):
+    @staticmethod
+    def _rank_intervals(runs, r, total) -> list:
+        """Node intervals [a, b) of source rank r in a call's runs."""
+        starts, rks, nds = runs
+        ends = np.append(starts[1:], total)
+        return [(int(nds[i]), int(nds[i]) + int(ends[i] - starts[i])) for i in range(len(starts)) if int(rks[i]) == r]
+
+    def _assign(self, st: _Rank, vbits, segs, hulls=None):
         """New images for set bits of vbits, segments in ascending source-rank
         order: ids n_nodes, n_nodes+1, ... (sm/construction.py:473-486)."""
         arr = (ctypes_segment * len(segs))()
         for i, (w0, nw, m) in enumerate(segs):
+            if m is not None:   # the values that may get images here
+                h = hulls[i] if hulls is not None else None
+                m.imaged.extend(h if h is not None else [(0, 1 << 62)])
             arr[i].word0 = w0
             arr[i].nwords = nw
             arr[i].present = _ptr(m.present.t) if m is not None else 0
@@ -1060,6 +1074,17 @@ class Cluster:
                 self.is_local(r) for r in (members or ranks_sorted))
             if need_bits and n:
                 work.append((tr, tg, key, n))
+        # 0. local targets whose keys can be predicted start their pass A first
+        #    (it then runs beside every replay below)
+        specs = {}
+        if self._dist_multi:
+            runs0 = self._runs(all_rank, all_node)
+            for tr, tg, key, n in work:
+                if self.is_local(tr) and runs0 is not None and bool((runs0[1] != tr).any()):
+                    st = self.ranks[tr]
+                    if tg.min() < 0 or tg.max() >= self.n_nodes[tr]:
+                        raise ValueError("target index outside the rank's node range")
+                    specs[tr] = self._dist_speculate(st, key, tr, tg, k_in, total, runs0, group, syn, port)
         # 1. source-side replays of the remote targets, launched before the local
         #    draws; their completion checks and presence flags come back in one
         #    asynchronous read, so the host does not wait for the local draw
@@ -1095,7 +1120,8 @@ class Cluster:
             if tg.min() < 0 or tg.max() >= self.n_nodes[tr]:
                 raise ValueError("target index outside the rank's node range")
             tgt_bits[tr] = self._dist_target(st, key, tr, tg, k_in, total, all_rank, all_node, vbase,
-                                             seg_words, total_words, syn, port, group, ranks_sorted)
+                                             seg_words, total_words, syn, port, group, ranks_sorted,
+                                             spec=specs.get(tr, "none"))
         # 3. remote bitmaps and their source ranks (the rare incomplete first
         #    piece continues synchronously)
         if remote:
@@ -1205,6 +1231,55 @@ class Cluster:
         delta = (np.asarray(keys0, dtype=np.int64) - starts) & 0xFFFFFFFF
         return np.concatenate([[len(starts)], starts, delta]).astype(np.uint32)
 
+    def _dist_speculate(self, st, key, tr, tg, k_in, total, runs, group, syn, port):
+        """Deferred call with predicted keys, or None.  With every remote map
+        of the call fresh and every source value drawn (a fixed in-degree
+        draw of K x N_tgt from N_src values covers them all unless K N_tgt is
+        small against N_src ln N_src), the images are assigned in (rank, node)
+        order from st.n_nodes: the key pieces are known before the replay and
+        pass A can run beside it.  _dist_target checks the prediction."""
+        starts, rks, nds = runs
+        n = k_in * len(tg)
+        remote = [r for r in sorted(set(int(x) for x in rks)) if r != tr]
+        mode = os.environ.get("SMX_SPECULATE", "1")   # "0": never, "force": whatever the coverage odds
+        if mode == "0" or not self._dist_multi or not n or total < 2:
+            return None
+        if mode != "force" and n < 2.0 * total * (math.log(total) + 6.0):
+            return None   # full coverage unlikely
+        for r in remote:   # none of the call's remote sources may have an image yet
+            m = st.maps.get((int(group), r))
+            if m is not None and any(a < y and x < b for a, b in self._rank_intervals(runs, r, total)
+                                     for x, y in m.imaged):
+                return None
+        cls = self._syn_class(st, syn, port)
+        if not self._defer_ok(st, cls, total, n):
+            return None
+        ends = np.append(starts[1:], total)
+        keys0 = np.zeros(len(starts), dtype=np.int64)
+        nxt = st.n_nodes
+        for r in remote:   # images in ascending (rank, node) order
+            idx = [i for i in range(len(starts)) if int(rks[i]) == r]
+            idx.sort(key=lambda i: int(nds[i]))
+            last = -1
+            for i in idx:
+                nd0, ln = int(nds[i]), int(ends[i] - starts[i])
+                if nd0 <= last:
+                    return None   # overlapping runs of one rank
+                keys0[i] = nxt
+                nxt += ln
+                last = nd0 + ln - 1
+        for i in range(len(starts)):
+            if int(rks[i]) == tr:
+                keys0[i] = int(nds[i])
+        pieces = self._pack_pieces(starts, keys0)
+        self._check_real_targets(st, tg)
+        dev = st.device
+        tgt = _up_index(tg, dev)
+        pay_tab = torch.empty(len(tg), dtype=torch.int32, device=dev)
+        call("smx_pay_table", _ptr(tgt), len(tg), _ptr(st.node2row.t), st.node2row.n, cls, _ptr(pay_tab), st.stream)
+        d = self._defer(st, key, total, n, 3, pieces, pay_tab, k_in, len(tg), cls)
+        return d if st.fused_ok else None
+
     def _final_pieces(self, st, tr, group, runs, total, present):
         """Key pieces with final source rows (local node or image id) when
         every remote run's images are consecutive; None otherwise."""
@@ -1232,18 +1307,24 @@ class Cluster:
         return self._pack_pieces(starts, keys0)
 
     def _dist_target(self, st, key, tr, tg, k_in, total, all_rank, all_node, vbase, seg_words,
-                     total_words, syn, port, group, ranks_sorted):
+                     total_words, syn, port, group, ranks_sorted, spec="none"):
         dev, sk = st.device, st.stream
         lut_base = st.lut.n
         n = k_in * len(tg)
         multi = self._dist_multi
         runs = self._runs(all_rank, all_node) if multi else None
         remote = bool((runs[1] != tr).any()) if runs is not None else bool((np.asarray(all_rank) != tr).any())
+        speculated = spec != "none"   # _dist already tried (spec: its deferred call or None)
+        spec = spec if speculated else None
         if runs is None:
             # general table: keys gathered from key_tab, used values marked by the draw
             key_tab, gv_tab = self._dist_tables(dev, sk, tr, total, all_rank, all_node, vbase, lut_base)[:2]
             vbits = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
         elif remote:
+            # pass A starts before the replay when the keys can be predicted:
+            # fresh maps and every source value drawn (checked below)
+            if not speculated:
+                spec = self._dist_speculate(st, key, tr, tg, k_in, total, runs, group, syn, port)
             # used source values from the early-exit replay of the same stream (what
             # every source rank runs anyway), so images exist before the draw
             vbits = self._dist_replay(dev, key, tr, total, all_rank, all_node, vbase, total_words, n)
@@ -1254,7 +1335,7 @@ class Cluster:
                 vbits[b >> 5: (b >> 5) + 1] |= int(np.uint32(1 << (b & 31)).view(np.int32))
 
         def assign(present):
-            segs = []
+            segs, hulls = [], []
             for r in ranks_sorted:
                 sw0, snw = seg_words[r]
                 m = None
@@ -1262,7 +1343,8 @@ class Cluster:
                     m = st.map_for(group, r)
                     m.ensure(snw * 32)
                 segs.append((sw0, snw, m))
-            self._assign(st, vbits, segs)
+                hulls.append(self._rank_intervals(runs, r, total) if runs is not None else None)
+            self._assign(st, vbits, segs, hulls)
 
         pieces, tmp_keys, present = None, True, None
         if runs is not None:
@@ -1272,6 +1354,25 @@ class Cluster:
             else:  # all sources local: nothing to assign, present iff anything was drawn
                 present = [tr] if n and total else []
             pieces = self._final_pieces(st, tr, group, runs, total, present)
+            if remote and spec is not None:
+                d = spec
+                if not st.fused_ok or d not in st.deferred:
+                    raise ConsistencyError("speculative fused call left the fused path early")
+                if pieces is not None:
+                    d["acct"] = self._dist_accounting(st, tr, group, n, 0, present, runs, pieces, False, lut_base,
+                                                      vbase, seg_words, deferred=True)
+                    same = np.array_equal(pieces, d["ktab"])
+                    self.spec_stats["confirmed" if same else "redone"] += 1
+                    if not same:
+                        # some value never drawn: pass A again with the real keys, same place in the order
+                        d["ktab"] = pieces
+                        if not self._fused_eager(st, d, slot=d["zi"]):
+                            self._fused_off(st)   # generates it (real keys, counted) with the others
+                    return vbits, present
+                # temporary keys needed: drop the speculative call, general path below
+                self.spec_stats["dropped"] += 1
+                st.deferred.remove(d)
+                self._fused_off(st)
             tmp_keys = pieces is None
             if pieces is None:  # images not consecutive: temporary keys resolved through the LUT
                 starts, rks, nds = runs
@@ -1760,7 +1861,7 @@ class Cluster:
                     np.add.at(cnt, (a + np.arange(rem)) & (B - 1), 1.0)
         return cnt / float(d["ex"])
 
-    def _fused_eager(self, st: _Rank, d: dict) -> bool:
+    def _fused_eager(self, st: _Rank, d: dict, slot=None) -> bool:
         """Pass A of one deferred call, launched at call time (it overlaps the
         host work of the calls that follow): the call's draws ranked by the
         low key digit into its own digit regions (csrc/fused.cu).  The record
@@ -1769,7 +1870,9 @@ class Cluster:
         z = st.fz
         dev, sk = st.device, st.stream
         if z is None:
-            key_bits = max(1, int(st.n_nodes - 1).bit_length())
+            # the call's own keys may lie past the current nodes (predicted images)
+            top = max([st.n_nodes] + [b for _, b in self._call_key_ranges(d)])
+            key_bits = max(1, int(top - 1).bit_length())
             env_lo = os.environ.get("SMX_FUSED_LO")
             lo = int(env_lo) if env_lo is not None else (
                 0 if key_bits <= 11 else max(key_bits - 11, min(9, key_bits - 8)))
@@ -1780,7 +1883,7 @@ class Cluster:
         # the call's payload split: its target rows (real neurons so far) in
         # the low bits, the class index above (pass B decodes per call)
         row_bits = max(1, int(st.n_real - 1).bit_length())
-        if row_bits > z["pbits"] or len(z["calls"]) >= 512:
+        if row_bits > z["pbits"] or (slot is None and len(z["calls"]) >= 512):
             return False
         if d["cls"] not in z["cidx"]:
             z["cidx"][d["cls"]] = len(z["cidx"])
@@ -1823,8 +1926,13 @@ class Cluster:
             tnsr.record_stream(gen)
         if d["kmode"] == 1:
             d["ktab"].record_stream(gen)
-        z["calls"].append(dict(region=region, rstart=rstart, cap=cap.astype(np.uint64), meta=meta, fill=fills[1],
-                               fills=fills, total=total, cpay=cpay, n=int(d["n"]), row_bits=row_bits))
+        zc = dict(region=region, rstart=rstart, cap=cap.astype(np.uint64), meta=meta, fill=fills[1],
+                  fills=fills, total=total, cpay=cpay, n=int(d["n"]), row_bits=row_bits)
+        if slot is None:   # in call order (pass B keeps it within every key)
+            d["zi"] = len(z["calls"])
+            z["calls"].append(zc)
+        else:              # the same call again (keys corrected): its place in the order stays
+            z["calls"][slot] = zc
         return True
 
     def _fused_ready(self, st: _Rank) -> bool:

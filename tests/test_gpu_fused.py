@@ -126,3 +126,24 @@ def test_fused_then_general_call_flushes_in_order():
         return c
     g, f = _build(False, fn), _build(True, fn)
     assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))
+
+
+@pytest.mark.parametrize("case,outcome", [("dense", "confirmed"), ("sparse", "dropped")])
+def test_speculative_distributed_keys(case, outcome, monkeypatch):
+    """Distributed calls with remote sources start pass A on predicted keys
+    (fresh maps, every source value drawn) before the replay: a dense call
+    confirms the prediction; a sparse one (forced; most values undrawn, so
+    the images are not consecutive) drops to the general path.  Tables equal
+    the general path's either way."""
+    monkeypatch.setenv("SMX_SPECULATE", "force")
+    k = (100, 25) if case == "dense" else (3, 1)
+
+    def fn(ns):
+        c, _ = scenarios.balanced(ns, 3, "p2p", 900, k[0], k[1], 11)
+        return c
+    g = _build(False, fn)
+    f = _build(True, fn)
+    assert f.spec_stats[outcome] > 0, f.spec_stats
+    if outcome == "confirmed":
+        assert all(st.store_path == "fused" for st in f.ranks.values())
+    assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))

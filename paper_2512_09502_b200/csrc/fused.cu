@@ -84,6 +84,14 @@ template <int KM>
 __device__ __forceinline__ uint32_t fg_key(const FusedGen& g, uint32_t v) {
   if (KM == 1) return __ldg(g.key_tab + v);
   if (KM == 4) return v + g.pdelta[0];
+  if (KM == 5) return v + (v >= g.pstart[1] ? g.pdelta[1] : g.pdelta[0]);   // two pieces
+  if (KM == 6) {  // up to four pieces (padding starts never reached: ex < 2^32)
+    uint32_t off = g.pdelta[0];
+    off = v >= g.pstart[1] ? g.pdelta[1] : off;
+    off = v >= g.pstart[2] ? g.pdelta[2] : off;
+    off = v >= g.pstart[3] ? g.pdelta[3] : off;
+    return v + off;
+  }
   uint32_t off = g.pdelta[0];
 #pragma unroll
   for (int s = 1; s < FG_MAXP; ++s)
@@ -918,9 +926,12 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
   g.status = ws;
   g.ticket = ws + n_tiles * B;
   const bool wide = n_slots >= 0x7fffffffull;  // 32-bit staging offsets below 2^31 slots
-  const int rc = key_mode == 1 ? fg_dispatch<1>(lo_bits, wide, g, (uint32_t)n_tiles, st)
-                 : g.np == 1   ? fg_dispatch<4>(lo_bits, wide, g, (uint32_t)n_tiles, st)
-                               : fg_dispatch<3>(lo_bits, wide, g, (uint32_t)n_tiles, st);
+  // key modes by piece count: 4 (one), 5 (two), 6 (three or four), 3 (up to FG_MAXP)
+  const int rc = key_mode == 1                  ? fg_dispatch<1>(lo_bits, wide, g, (uint32_t)n_tiles, st)
+                 : g.np == 1                    ? fg_dispatch<4>(lo_bits, wide, g, (uint32_t)n_tiles, st)
+                 : g.np == 2                    ? fg_dispatch<5>(lo_bits, wide, g, (uint32_t)n_tiles, st)
+                 : g.np <= 4 && ex < (1ull << 32) ? fg_dispatch<6>(lo_bits, wide, g, (uint32_t)n_tiles, st)
+                                                : fg_dispatch<3>(lo_bits, wide, g, (uint32_t)n_tiles, st);
   cudaFreeAsync(ws, st);
   return rc;
 }

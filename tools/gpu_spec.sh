@@ -1,7 +1,7 @@
 set -x
 O=gpurun_out/spec
 mkdir -p $O
-timeout 1500 python -m pytest tests/test_gpu_fused.py tests/test_gpu_multiprocess.py tests/test_gpu_parity.py -q -p no:cacheprovider > $O/pytest.log 2>&1; tail -15 $O/pytest.log
+timeout 1500 python -m pytest tests/test_gpu_fused.py tests/test_gpu_multiprocess.py -q -p no:cacheprovider > $O/pytest.log 2>&1; tail -15 $O/pytest.log
 for N in 2 4; do
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2962$N bench.py --gpus $N --steps 5 --warmup 3 > $O/c3_n$N.json 2> $O/c3_n$N.err
 cut -c1-300 $O/c3_n$N.json; tail -3 $O/c3_n$N.err

@@ -63,13 +63,24 @@ def parse():
     return ap.parse_args()
 
 
-def traffic_per_synapse():
-    """DRAM bytes (read + write) per synapse of the generation + sort kernels,
-    from the committed ncu capture of one C3 construction (profiles/r1f)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1f", "traffic.json")
+TRAFFIC = {"fused": "profiles/r2/traffic.json", "general": "profiles/r1f/traffic.json"}
+KERNELS = {"fused": "pass A (smx_fused_gen: generation + low-digit ranking) + pass B (smx_fused_sort)",
+           "general": "generation (smx_gen_draw) + stable sort (smx_sort_records)"}
+
+
+def traffic_per_synapse(path_kind: str):
+    """DRAM bytes (read + write) per synapse of the generation + sort kernels
+    of the store path the run took, from the committed ncu capture of one C3
+    construction on that path (tools/profile_summary.py)."""
+    rel = TRAFFIC.get(path_kind)
+    if rel is None:
+        return None, None
     try:
-        with open(path) as f:
-            return float(json.load(f)["bytes_per_synapse"]), "profiles/r1f/traffic.json"
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), rel)) as f:
+            d = json.load(f)
+        if d.get("store_path", "general") != path_kind:
+            return None, None
+        return float(d["bytes_per_synapse"]), rel
     except (OSError, KeyError, ValueError):
         return None, None
 
@@ -357,7 +368,8 @@ def run_ours(args):
     peak, peak_kind = peaks()
     k_ms = float(np.mean(gen_ms)) + float(np.mean(sort_ms))
     achieved = BYTES_PER_SYN * syn_per_rank / (k_ms * 1e-3) / 1e9
-    tps, traffic_src = traffic_per_synapse()
+    store_path = c.ranks[rank].store_path
+    tps, traffic_src = traffic_per_synapse(store_path)
     traffic = tps * syn_per_rank if tps is not None else None  # bytes per construction, like achieved
     line = {
         "metric": "construction_synapses_per_s", "value": value, "unit": "synapses/s", "n_gpus": world,
@@ -378,7 +390,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_kind": peak_kind,
-                     "kernel": "generation (smx_gen_draw) + stable sort (smx_sort_records)",
+                     "kernel": KERNELS.get(store_path, store_path), "store_path": store_path,
                      "kernel_ms": k_ms, "bytes_per_synapse": BYTES_PER_SYN},
         "clocks": clocks,
         "phase_ms": {"gen": float(np.mean(gen_ms)), "sort": float(np.mean(sort_ms))},

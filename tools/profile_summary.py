@@ -16,7 +16,8 @@ import subprocess
 import sys
 
 SYNAPSES = 100_000 * 11_250
-GEN_SORT = ("draw_", "tile_hist", "chunk_sum", "chunk_scan", "tile_offsets", "downsweep", "scan_")
+GEN_SORT = ("draw_", "tile_hist", "chunk_sum", "chunk_scan", "tile_offsets", "downsweep", "scan_",
+            "fused_gen", "fb_")
 
 
 def launch_rows(path):
@@ -66,11 +67,14 @@ def main(src, dst):
                 if any(name.startswith(p) or p in k for p in GEN_SORT):
                     gs_bytes += r + wr
                     gs_ms += t / 1e6
+        fused = any("fused_gen" in k for k in agg)
         json.dump({"what": "DRAM bytes (read+write) of the generation + sort kernels of one C3 construction "
                            "(1.125e9 synapses), ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
                            "--clock-control none, tools/prof_construct.py",
+                   "store_path": "fused" if fused else "general",
                    "bytes_per_construction": gs_bytes, "bytes_per_synapse": gs_bytes / SYNAPSES,
-                   "kernel_time_ms_serialised": gs_ms, "algorithmic_bytes_per_synapse": 20.0},
+                   "kernel_time_ms_serialised": gs_ms, "algorithmic_bytes_per_synapse": 20.0,
+                   "path_minimum_bytes_per_synapse": 12.0 if fused else 20.0},
                   open(os.path.join(dst, "traffic.json"), "w"), indent=1)
     reps = [x for x in os.listdir(src) if x.endswith(".ncu-rep")]
     if reps:

@@ -836,9 +836,9 @@ extern "C" int smx_count_ranges(const uint32_t* keys, uint64_t n, const uint32_t
 //   otherwise:                 Floyd's algorithm, then a Fisher-Yates shuffle
 // every index draw is numpy's random_bounded_uint64 (Lemire on next_uint32,
 // value in [0, rng], rng == 0 consumes nothing).  The rows form one chain
-// through the stream (each row's length depends on its rejections), so one
-// warp walks the call sequentially: lane 0 draws, the warp clears the hash
-// tables.  A correctness path for the rule, not a throughput path.
+// through the stream (each row's length depends on its rejections): the
+// chain of row starts is resolved warp-parallel (row_consumption), and the
+// rows themselves are drawn concurrently, one per warp.
 namespace {
 
 struct U32Stream {  // next_uint32 with numpy's low-half-first buffering, from a u32 cursor
@@ -875,70 +875,177 @@ struct U32Stream {  // next_uint32 with numpy's low-half-first buffering, from a
 
 constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
 
-__global__ void __launch_bounds__(32) choice_rows_kernel(smx::Key key, uint64_t u0, uint32_t n, uint32_t k,
-                                                         uint64_t rows, uint32_t* out, uint32_t* tab,
-                                                         uint32_t tab_mask, uint64_t* cursor_out) {
-  const int lane = threadIdx.x;
+// One row of choice(n, k, replace=False) from u32 cursor `start`, serially on
+// the calling thread, exactly as numpy walks it (Floyd's set sampling then a
+// Fisher-Yates shuffle; the tail branch shuffles a virtual array).  `tab` is
+// this row's private hash table.
+__device__ void choice_row(smx::Key key, uint64_t start, uint32_t n, uint32_t k, bool tail, uint32_t* row,
+                           uint32_t* tab, uint32_t tab_mask) {
   U32Stream s;
-  s.init(key, u0);
-  const bool tail = n > 10000u && k > n / 50u;
-  for (uint64_t r = 0; r < rows; ++r) {
-    uint32_t* row = out + r * k;
-    for (uint32_t i = lane; i <= tab_mask; i += 32) tab[i] = EMPTY32;           // hash keys
-    if (tail) for (uint32_t i = lane; i <= tab_mask; i += 32) tab[tab_mask + 1 + i] = 0;  // values
-    __syncwarp();
-    if (lane == 0) {
-      if (tail) {
-        // virtual array data[i] = i, swaps kept in an open-addressing map
-        auto find = [&](uint32_t key_) -> uint32_t {
-          uint32_t loc = (key_ * 2654435761u) & tab_mask;
-          while (tab[loc] != EMPTY32 && tab[loc] != key_) loc = (loc + 1) & tab_mask;
-          return loc;
-        };
-        auto get = [&](uint32_t idx) -> uint32_t {
-          const uint32_t loc = find(idx);
-          return tab[loc] == EMPTY32 ? idx : tab[tab_mask + 1 + loc];
-        };
-        auto put = [&](uint32_t idx, uint32_t val) {
-          const uint32_t loc = find(idx);
-          tab[loc] = idx;
-          tab[tab_mask + 1 + loc] = val;
-        };
-        const uint32_t first = n - k > 1 ? n - k : 1;
-        for (uint32_t i = n - 1; i >= first; --i) {
-          const uint32_t j = s.bounded_incl(i);
-          const uint32_t vi = get(i), vj = get(j);
-          put(j, vi);
-          put(i, vj);
-          if (i == 0) break;
-        }
-        for (uint32_t q = 0; q < k; ++q) row[q] = get(n - k + q);
+  s.init(key, start);
+  if (tail) {
+    // virtual array data[i] = i, swaps kept in an open-addressing map
+    auto find = [&](uint32_t key_) -> uint32_t {
+      uint32_t loc = (key_ * 2654435761u) & tab_mask;
+      while (tab[loc] != EMPTY32 && tab[loc] != key_) loc = (loc + 1) & tab_mask;
+      return loc;
+    };
+    auto get = [&](uint32_t idx) -> uint32_t {
+      const uint32_t loc = find(idx);
+      return tab[loc] == EMPTY32 ? idx : tab[tab_mask + 1 + loc];
+    };
+    auto put = [&](uint32_t idx, uint32_t val) {
+      const uint32_t loc = find(idx);
+      tab[loc] = idx;
+      tab[tab_mask + 1 + loc] = val;
+    };
+    const uint32_t first = n - k > 1 ? n - k : 1;
+    for (uint32_t i = n - 1; i >= first; --i) {
+      const uint32_t j = s.bounded_incl(i);
+      const uint32_t vi = get(i), vj = get(j);
+      put(j, vi);
+      put(i, vj);
+      if (i == 0) break;
+    }
+    for (uint32_t q = 0; q < k; ++q) row[q] = get(n - k + q);
+  } else {
+    for (uint32_t j = n - k; j < n; ++j) {
+      const uint32_t val = s.bounded_incl(j);
+      uint32_t loc = val & tab_mask;
+      while (tab[loc] != EMPTY32 && tab[loc] != val) loc = (loc + 1) & tab_mask;
+      if (tab[loc] == EMPTY32) {
+        tab[loc] = val;
+        row[j - n + k] = val;
       } else {
-        for (uint32_t j = n - k; j < n; ++j) {
-          const uint32_t val = s.bounded_incl(j);
-          uint32_t loc = val & tab_mask;
-          while (tab[loc] != EMPTY32 && tab[loc] != val) loc = (loc + 1) & tab_mask;
-          if (tab[loc] == EMPTY32) {
-            tab[loc] = val;
-            row[j - n + k] = val;
-          } else {
-            loc = j & tab_mask;
-            while (tab[loc] != EMPTY32) loc = (loc + 1) & tab_mask;
-            tab[loc] = j;
-            row[j - n + k] = j;
-          }
-        }
-        for (uint32_t i = k - 1; i >= 1 && k > 1; --i) {
-          const uint32_t j = s.bounded_incl(i);
-          const uint32_t t = row[j];
-          row[j] = row[i];
-          row[i] = t;
-        }
+        loc = j & tab_mask;
+        while (tab[loc] != EMPTY32) loc = (loc + 1) & tab_mask;
+        tab[loc] = j;
+        row[j - n + k] = j;
       }
     }
-    __syncwarp();
+    for (uint32_t i = k - 1; i >= 1 && k > 1; --i) {
+      const uint32_t j = s.bounded_incl(i);
+      const uint32_t t = row[j];
+      row[j] = row[i];
+      row[i] = t;
+    }
   }
-  if (lane == 0 && cursor_out) *cursor_out = s.pos;
+}
+
+// The bounded range of stage t of a row (bounded_incl(rng) calls in order):
+// Floyd stages rng = n - k + t (t < k), then shuffle stages rng = k - 1 - (t - k);
+// tail stages rng = n - 1 - t.
+struct RowStages {
+  uint32_t n, k, m;
+  bool tail;
+  __device__ uint32_t rng(uint32_t t) const {
+    if (tail) return n - 1 - t;
+    return t < k ? n - k + t : k - 1 - (t - k);
+  }
+};
+
+// u32 draws a row consumes from `start` (each stage: one draw plus one per
+// Lemire rejection; a stage of range 0 draws nothing), found by the warp in
+// windows of 256 stages: every lane checks 8 consecutive positions for a
+// rejection under the no-rejection alignment; the first rejection moves the
+// window to the stage that redraws.
+__device__ uint64_t row_consumption(smx::Key key, uint64_t start, const RowStages& S, int lane) {
+  uint64_t p = start;
+  uint32_t t = 0;
+  if (!S.tail && S.n == S.k && S.m > 0) t = 1;   // Floyd stage 0 has range 0: no draw
+  while (t < S.m) {
+    const uint32_t t0 = t + 8u * lane;
+    uint64_t blk = ~0ull, w4[4];
+    int hit = 8;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t ts = t0 + e;
+      if (ts >= S.m || hit < 8) continue;
+      const uint64_t q = p + 8ull * lane + e;
+      const uint64_t w = q >> 1, b = (w >> 2) + 1;
+      if (b != blk) { smx::philox4x64_10(b, key, w4); blk = b; }
+      const uint32_t raw = (q & 1) ? (uint32_t)(w4[w & 3] >> 32) : (uint32_t)w4[w & 3];
+      const uint32_t rng = S.rng(ts);
+      if (rng == 0u || rng == 0xFFFFFFFFu) continue;   // (range 0 only at Floyd stage 0, skipped above)
+      const uint32_t ex = rng + 1;
+      const uint32_t left = (uint32_t)((uint64_t)raw * ex);
+      if (left < ex && left < (uint32_t)((0x100000000ULL - ex) % ex)) hit = e;
+    }
+    const uint32_t any = __ballot_sync(0xffffffffu, hit < 8);
+    if (!any) {
+      const uint32_t adv = min(256u, S.m - t);
+      t += adv;
+      p += adv;
+      continue;
+    }
+    const int l = __ffs(any) - 1;
+    const int e = __shfl_sync(0xffffffffu, hit, l);
+    // stage t + 8 l + e rejected its draw at position p + 8 l + e: it redraws at the next one
+    t += 8u * l + e;
+    p += 8ull * l + e + 1;
+  }
+  return p - start;
+}
+
+constexpr uint64_t CURSOR_UNSET = ~0ull;
+
+// Rows in parallel: warps take rows by ticket.  Row r's start cursor is
+// published by row r - 1's warp as soon as it knows its consumption.  A warp
+// first speculates that rows r - D .. r - 1 consume the nominal m draws each
+// (no rejection), starting from row r - D's start (published D hand-offs
+// earlier), and computes its own consumption from there while the chain
+// catches up; when the speculation holds, the chain advances by one flag
+// hand-off per row.  Then lane 0 draws the row itself, beside every other
+// warp's row.
+constexpr uint64_t CHOICE_SPEC_DEPTH = 8;
+// One warp per CTA.  With in_smem the row's hash table and the row itself
+// live in shared memory (the serial draw is latency-bound on its probes and
+// swaps) and the row is copied out at the end; otherwise both are global.
+__global__ void __launch_bounds__(32) choice_rows_kernel(smx::Key key, uint32_t n, uint32_t k, uint64_t rows,
+                                                         RowStages S, uint32_t* out, uint32_t* tab,
+                                                         uint32_t tab_mask, uint64_t* starts, uint32_t* ticket,
+                                                         int in_smem) {
+  extern __shared__ uint32_t crs[];
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp_id = blockIdx.x;
+  const uint32_t tab_words = (tab_mask + 1) * (S.tail ? 2u : 1u);
+  uint32_t* my_tab = in_smem ? crs : tab + warp_id * tab_words;
+  uint32_t* srow = crs + tab_words;
+  volatile uint64_t* vs = starts;
+  for (;;) {
+    uint64_t r = 0;
+    if (lane == 0) r = atomicAdd(ticket, 1u);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= rows) break;
+    // speculate from the predecessor's start (published one row earlier)
+    uint64_t spec = CURSOR_UNSET, c_spec = 0;
+    if (r > 0) {
+      const uint64_t b = r > CHOICE_SPEC_DEPTH ? r - CHOICE_SPEC_DEPTH : 0;
+      uint64_t ps = CURSOR_UNSET;
+      if (lane == 0) {
+        while ((ps = vs[b]) == CURSOR_UNSET) __nanosleep(32);
+      }
+      ps = __shfl_sync(0xffffffffu, ps, 0);
+      spec = ps + (r - b) * (uint64_t)S.m;
+      c_spec = row_consumption(key, spec, S, lane);
+    }
+    uint64_t s0 = CURSOR_UNSET;
+    if (lane == 0) {
+      while ((s0 = vs[r]) == CURSOR_UNSET) __nanosleep(32);
+    }
+    s0 = __shfl_sync(0xffffffffu, s0, 0);
+    const uint64_t c = s0 == spec ? c_spec : row_consumption(key, s0, S, lane);
+    if (lane == 0) {
+      __threadfence();
+      vs[r + 1] = s0 + c;
+    }
+    for (uint32_t i = lane; i < tab_words; i += 32) my_tab[i] = i <= tab_mask ? EMPTY32 : 0u;
+    __syncwarp();
+    if (lane == 0) choice_row(key, s0, n, k, S.tail, in_smem ? srow : out + r * k, my_tab, tab_mask);
+    __syncwarp();
+    if (in_smem)
+      for (uint32_t i = lane; i < k; i += 32) out[r * k + i] = srow[i];
+  }
 }
 
 }  // namespace
@@ -963,18 +1070,40 @@ extern "C" int smx_choice_rows(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t n
   uint64_t want = tail ? 4 * k : (uint64_t)(1.2 * (double)k) + 1;
   uint64_t cap = 1;
   while (cap < want) cap <<= 1;
+  RowStages S;
+  S.n = (uint32_t)n;
+  S.k = (uint32_t)k;
+  S.tail = tail;
+  S.m = tail ? (uint32_t)(n - (n - k > 1 ? n - k : 1)) : (uint32_t)(k + (k > 1 ? k - 1 : 0));
+  // one warp per CTA; the hash table and the row in SMEM when they fit
+  // (<= 160 KB), otherwise global tables bounded to 256 MB in total
+  const uint64_t tab_bytes = sizeof(uint32_t) * cap * (tail ? 2 : 1);
+  const uint64_t smem = tab_bytes + sizeof(uint32_t) * k;
+  const int in_smem = smem <= (160u << 10);
+  uint64_t warps = std::min<uint64_t>(rows, 148ull * 16);
+  if (!in_smem) warps = std::max<uint64_t>(1, std::min<uint64_t>(warps, (256ull << 20) / tab_bytes));
+  const uint32_t blocks = (uint32_t)warps;
   uint32_t* tab = nullptr;
-  uint64_t* cur = nullptr;
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&tab, sizeof(uint32_t) * cap * (tail ? 2 : 1), st));
-  SMX_CUDA_CHECK(cudaMallocAsync((void**)&cur, sizeof(uint64_t), st));
+  uint64_t* starts = nullptr;
+  if (in_smem) {
+    SMX_CUDA_CHECK(cudaFuncSetAttribute(choice_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  } else {
+    SMX_CUDA_CHECK(cudaMallocAsync((void**)&tab, tab_bytes * warps, st));
+  }
+  SMX_CUDA_CHECK(cudaMallocAsync((void**)&starts, sizeof(uint64_t) * (rows + 2), st));
+  SMX_CUDA_CHECK(cudaMemsetAsync(starts, 0xff, sizeof(uint64_t) * (rows + 2), st));
+  if (smx_h2d_async(starts, &u0, sizeof(uint64_t), st)) return -3;
+  uint32_t* ticket = reinterpret_cast<uint32_t*>(starts + rows + 1);
+  SMX_CUDA_CHECK(cudaMemsetAsync(ticket, 0, sizeof(uint32_t), st));
   smx_count_launch();
-  choice_rows_kernel<<<1, 32, 0, st>>>(smx::Key{k0, k1}, u0, (uint32_t)n, (uint32_t)k, rows, out, tab,
-                                       (uint32_t)(cap - 1), cur);
+  choice_rows_kernel<<<blocks, 32, in_smem ? smem : 0, st>>>(smx::Key{k0, k1}, (uint32_t)n, (uint32_t)k, rows, S,
+                                                              out, tab, (uint32_t)(cap - 1), starts, ticket,
+                                                              in_smem);
   SMX_LAUNCH_CHECK();
-  SMX_CUDA_CHECK(cudaMemcpyAsync(cursor_out_host, cur, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  SMX_CUDA_CHECK(cudaMemcpyAsync(cursor_out_host, starts + rows, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   SMX_CUDA_CHECK(cudaStreamSynchronize(st));
-  cudaFreeAsync(tab, st);
-  cudaFreeAsync(cur, st);
+  if (tab) cudaFreeAsync(tab, st);
+  cudaFreeAsync(starts, st);
   return 0;
 }
 

@@ -34,6 +34,16 @@ def integers(key, u32_cursor: int, lo: int, hi: int, n: int, device="cuda"):
     return out[:n], int(cur[0])
 
 
+def choice_rows(key, u32_cursor: int, n: int, k: int, rows: int, device="cuda"):
+    """rows back-to-back Generator.choice(n, k, replace=False) draws from a
+    u32 cursor; returns (rows x k int32 tensor, cursor after the last row)."""
+    out = torch.empty(max(rows * k, 1), dtype=torch.int32, device=device)
+    cur = np.zeros(1, dtype=np.uint64)
+    call("smx_choice_rows", key[0], key[1], u32_cursor, n, k, rows, out.data_ptr(), cur.ctypes.data,
+         _stream(out.device))
+    return out[: rows * k].view(rows, k) if rows * k else out[:0], int(cur[0])
+
+
 def init_v(seed: int, gids, mu: float, sd: float, device="cuda") -> torch.Tensor:
     g = torch.as_tensor(np.asarray(gids, dtype=np.int64)).to(device)
     v = torch.empty(max(g.numel(), 1), dtype=torch.float64, device=device)

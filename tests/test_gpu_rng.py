@@ -180,3 +180,24 @@ def test_init_v_many_gids():
     want = np.array([OracleStream(12345, ("init-v", int(g))).normal(-58.0, 5.0) for g in gids])
     got = dr.init_v(12345, gids, -58.0, 5.0).cpu().numpy()
     assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+@pytest.mark.parametrize("n,k,rows", [(1000, 40, 3000), (5, 5, 50), (20_000, 900, 40), (50_000, 600, 200),
+                                      (3, 1, 100), (100_000, 1, 20_000),
+                                      (2_200_000_000, 20, 2000)])
+def test_choice_rows_parallel_chain(n, k, rows):
+    """smx_choice_rows draws rows concurrently (one warp per row) after
+    resolving the chain of row starts; the rows and the final cursor equal
+    numpy's back-to-back choice(n, k, replace=False) calls on one stream
+    (Floyd + shuffle, the tail branch for n > 10000 and k > n // 50, n == k,
+    a long chain, and ranges just above 2^31 where about half the draws are
+    Lemire rejections, so nearly every row shifts the ones after it)."""
+    import device_rng as dr
+    from oracle.rng import OracleStream
+    from paper_2512_09502_b200.api import stream_key
+    key = stream_key(5, ("choice-rows", n, k, rows))
+    got, cur = dr.choice_rows(key, 0, n, k, rows)
+    o = OracleStream(0, key=key)
+    want = np.stack([o.choice_no_replace(n, k) for _ in range(rows)])
+    assert np.array_equal(got.cpu().numpy().view(np.uint32).astype(np.int64), want.astype(np.int64))
+    assert cur == o.u32_used

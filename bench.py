@@ -56,7 +56,7 @@ def parse():
                     help="C4 areas (default 4 per GPU: the per-GPU load of the 32-area model on 8 GPUs)")
     ap.add_argument("--c4-neurons", type=int, default=129_063)
     ap.add_argument("--c4-k", default="3600,900,44", help="k_intra_exc,k_intra_inh,k_inter (SURVEY §8 C4)")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c5"],
+    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c4", "c5"],
                     help="c3: the headline (hpc_benchmark weak scaling); c5: construction-only sweep")
     ap.add_argument("--c5-points", default="1e8,3e8,1e9,3e9,1e10")
     ap.add_argument("--c5-rules", default="fixed_indegree,fixed_total")
@@ -584,9 +584,87 @@ def run_c4(args):
         dist.destroy_process_group()
 
 
+def run_c2(args):
+    """BASELINE configs[1]: the Potjans-Diesmann microcircuit
+    at full scale on one GPU (paper_2512_09502_b200/models.py:
+    build_microcircuit; fixed_total per projection, normal weights, uniform
+    integer delays -> the wide general path).  Under torchrun every rank
+    builds its own copy (replicas; the model is a one-GPU config)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_09502_b200 import api, engine, models
+
+    world, rank, local = dist_info()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    p = models.MicrocircuitParams(scale=1.0)
+    sizes, k = models.microcircuit_synapse_counts(p)
+    n_syn = int(k.sum())
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    c = None
+    span, wall, gen, srt = [], [], [], []
+    for i in range(args.warmup + args.steps):
+        del c
+        gc.collect()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        c = engine.Cluster(api.SimConfig(n_ranks=1, comm_mode="p2p", seed=args.seed), profile=True)
+        models.build_microcircuit(c, p)
+        c.prepare()
+        e1.record()
+        n_rec = int(c.ranks[0].first_index[-1].item())
+        w = time.perf_counter() - t0
+        torch.cuda.synchronize(dev)
+        assert n_rec == n_syn, (n_rec, n_syn)
+        if i >= args.warmup:
+            span.append(max_over_ranks(e0.elapsed_time(e1)))
+            wall.append(max_over_ranks(w))
+            gen.append(c.kernel_ms("gen"))
+            srt.append(c.kernel_ms("sort"))
+    peak = torch.cuda.max_memory_allocated(dev)
+    rep = c.simulate(args.prop_warmup_ms, args.model_ms, record=False)
+    c.simulate(0.0, args.model_ms, record=True)
+    n_spk = len(c.rank_events(0))
+    ms = float(np.mean(span))
+    line = {"metric": "construction_synapses_per_s", "value": world * n_syn / (ms * 1e-3), "unit": "synapses/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "data": "synthetic", "dtype": "u32/f64",
+            "config": {"workload": "microcircuit_C2", "neurons": int(sum(sizes)), "synapses": n_syn,
+                       "parallelism": "replicas" if world > 1 else "ranks1", "seed": args.seed,
+                       "store_path": c.ranks[0].store_path},
+            "construction_wall_s": float(np.mean(wall)),
+            "phase_ms": {"gen": float(np.mean(gen)), "sort": float(np.mean(srt))},
+            "peak_device_bytes": int(peak), "peak_bytes_per_synapse": peak / n_syn,
+            "rtf": max_over_ranks(rep.rtf), "rtf_model_ms": args.model_ms, "n_spikes": n_spk,
+            "rate_hz": n_spk / (sum(sizes) * args.model_ms * 1e-3)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
-    if args.workload == "c5":
+    if args.workload == "c2":
+        run_c2(args)
+    elif args.workload == "c5":
         run_c5(args)
     elif args.workload == "c4":
         run_c4(args)

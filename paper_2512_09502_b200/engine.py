@@ -1755,7 +1755,34 @@ class Cluster:
         max_chunks = max(1, -(-max_len // 1024))
         st.owner_cap = st.N * self.block * max_chunks + 16
         st.owner = torch.zeros(st.owner_cap, dtype=torch.int32, device=dev)
+        self._place(st)
         st.prepared = True
+
+    @staticmethod
+    def _place(st: _Rank):
+        """The optimisation level's placement plan made real
+        (sm/construction.py:43-71): structures the plan puts on the host move
+        to pinned host memory, which the kernels read in place over the host
+        link (zero-copy; same pointer under unified addressing); counts the
+        plan drops (level 2) are freed.  Results never depend on the
+        placement, only speed and HBM use do."""
+        from .memory import HOST
+        plan = st.mem.plan
+
+        def host(t):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)   # ordered on the rank's stream before every later kernel
+            return h
+        if plan.first_index == HOST:
+            st.first_index = host(st.first_index)
+        if plan.counts is None:
+            st.counts = None
+        elif plan.counts == HOST and st.counts is not None:
+            st.counts = host(st.counts)
+        if plan.remote_source_maps == HOST:
+            st.RL = {k: tuple(host(x) for x in v) for k, v in st.RL.items()}
+        if plan.image_maps == HOST:
+            st.I = {k: host(v) for k, v in st.I.items()}
 
     def _sort_pending(self, st: _Rank):
         """General path: stable LSD sort of the pending (key, value) records by

@@ -145,6 +145,31 @@ def gen_c1():
     del ns
 
 
+C2_SEED = 12345
+
+
+def gen_c2():
+    """C2 at full size (PD microcircuit, 77,169 neurons, ~3e8 synapses, 1 rank,
+    seed 12345): SHA-256 digests of every canonical table column, built by
+    the reference Cluster from this repository's microcircuit script (the
+    reference has no PD builder; the script only calls façade methods)."""
+    import time
+    ns = ref_namespace()
+    t0 = time.time()
+    c = sm.Cluster(sm.SimConfig(n_ranks=1, comm_mode="p2p", seed=C2_SEED))
+    ns.build_microcircuit(c, ns.MicrocircuitParams(scale=1.0))
+    c.prepare()
+    t1 = time.time()
+    dig = tables.digests(tables.canon_reference(c))
+    out = dict(config=dict(model="PD microcircuit", scale=1.0, seed=C2_SEED, comm_mode="p2p"),
+               n_neurons=int(sum(st.n_real for st in c.ranks)) if hasattr(c.ranks[0], "n_real") else None,
+               n_synapses=int(sum(len(st.store.src) for st in c.ranks)), tables=dig,
+               reference_construction_s=round(t1 - t0, 1))
+    with open(os.path.join(HERE, "c2_digests.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+    print("C2", out["n_synapses"], round(t1 - t0, 1), "s", file=sys.stderr)
+
+
 def gen_transport():
     """Transport counters of each simulated scenario (sm/transport.py:55-67,
     128-129, 165-166): messages and bytes per phase after simulate()."""
@@ -166,6 +191,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if "--c1-only" in sys.argv:
         gen_c1()
+        sys.exit(0)
+    if "--c2-only" in sys.argv:
+        gen_c2()
         sys.exit(0)
     if "--memory-only" in sys.argv:
         gen_memory()

@@ -113,6 +113,26 @@ def test_c1_full_size_digests():
     assert hashlib.sha256(counts.tobytes()).hexdigest() == want["spike_counts_sha256"]
 
 
+def test_c2_full_size_digests():
+    """BASELINE configs[1] at full size (PD microcircuit, 77,169 neurons,
+    ~3e8 synapses through fixed_total with normal weights and uniform integer
+    delays, 1 rank, seed 12345): every table column equals the reference
+    Cluster's by SHA-256 (tests/golden/c2_digests.json, made by
+    make_golden.py --c2-only)."""
+    path = os.path.join(GOLD, "c2_digests.json")
+    if not os.path.exists(path):
+        pytest.skip("c2_digests.json not generated")
+    want = json.load(open(path))
+    ns = gpu_ns()
+    c = ns.make_cluster(ns.SimConfig(n_ranks=1, comm_mode="p2p", seed=want["config"]["seed"]))
+    ns.build_microcircuit(c, ns.MicrocircuitParams(scale=want["config"]["scale"]))
+    c.prepare()
+    got = tables.digests(tables.canon_gpu(c))
+    assert int(c.ranks[0].first_index[-1].item()) == want["n_synapses"]
+    bad = [k for k in want["tables"] if got.get(k) != want["tables"][k]]
+    assert not bad and set(got) == set(want["tables"]), (bad, sorted(set(got) ^ set(want["tables"])))
+
+
 @pytest.mark.parametrize("delay_ms,mode,n_ranks", [(2.0, "p2p", 1), (3.0, "p2p", 1), (2.0, "collective", 2),
                                                    (3.0, "p2p", 3)])
 def test_long_delays(delay_ms, mode, n_ranks):

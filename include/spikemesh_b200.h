@@ -38,6 +38,13 @@ int smx_set_sync_policy(int flags);
 /* A non-blocking stream (no implicit synchronisation with the legacy
  * default stream) at the given priority; the engine runs the fused path's
  * pass A and the preparation side work on such streams. */
+/* Device-side chaining of draws on one keyed stream (sm/construction.py:
+ * 424-431: fixed_total's targets continue after its positions; 157-176: a
+ * syn stream's delays continue after its normal weights).  The next draw
+ * entry point called on this thread starts at *u0_dev (u32 cursor, device;
+ * null: its u0 argument) and writes its end cursor to *cursor_dev (device;
+ * null: as usual), with no host synchronisation.  Taken once. */
+int smx_draw_chain(const uint64_t* u0_dev, uint64_t* cursor_dev);
 int smx_stream_create(int priority, void** out);
 int smx_pool_setup(int device);
 /* device error word of asynchronous paths: read + clear (synchronises stream) */

@@ -102,6 +102,41 @@ int smx_grid_cap(int grid, int concurrent_cap) {
   return grid < concurrent_cap ? grid : concurrent_cap;
 }
 
+// Device-side chaining of draws on one stream (a draw that continues where
+// the previous one ended, e.g. fixed_total's targets after its positions, or
+// a syn stream's delays after its normal weights): smx_draw_chain sets, for
+// the next draw entry point called on this thread, where its start cursor
+// comes from and where its end cursor goes -- both device words, no host
+// synchronisation.  run_draw takes (and clears) the setting.
+namespace {
+thread_local const uint64_t* t_chain_u0 = nullptr;
+thread_local uint64_t* t_chain_cur = nullptr;
+
+__global__ void chain_copy_kernel(const uint64_t* u0_dev, uint64_t u0, uint64_t* cursor_dev) {
+  *cursor_dev = u0_dev ? *u0_dev : u0;
+}
+}  // namespace
+
+extern "C" int smx_draw_chain(const uint64_t* u0_dev, uint64_t* cursor_dev) {
+  t_chain_u0 = u0_dev;
+  t_chain_cur = cursor_dev;
+  return 0;
+}
+
+void smx_take_draw_chain(const uint64_t** u0_dev, uint64_t** cursor_dev) {
+  *u0_dev = t_chain_u0;
+  *cursor_dev = t_chain_cur;
+  t_chain_u0 = nullptr;
+  t_chain_cur = nullptr;
+}
+
+int smx_chain_passthrough(const uint64_t* u0_dev, uint64_t u0, uint64_t* cursor_dev, cudaStream_t st) {
+  if (!cursor_dev) return 0;
+  smx_count_launch(); chain_copy_kernel<<<1, 1, 0, st>>>(u0_dev, u0, cursor_dev);
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
 extern "C" const char* smx_version(void) { return "spikemesh-b200 0.1.0 sm_100a"; }
 
 // Host-thread wait policy for synchronisations (must run before the CUDA

@@ -331,6 +331,9 @@ int smx_h2d_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
 // long persistent kernel in flight (capi.cu): smx_long_kernel_mark records
 // its end; smx_grid_cap(grid, cap) returns min(grid, cap) while it runs
 void smx_long_kernel_mark(cudaStream_t st);
+// draw chaining (capi.cu, smx_draw_chain): taken once by the next run_draw
+void smx_take_draw_chain(const uint64_t** u0_dev, uint64_t** cursor_dev);
+int smx_chain_passthrough(const uint64_t* u0_dev, uint64_t u0, uint64_t* cursor_dev, cudaStream_t st);
 int smx_grid_cap(int grid, int concurrent_cap);
 extern "C" int* smx_device_error_word(void);
 #define SMX_CUDA_CHECK(expr)                                                       \

@@ -473,9 +473,13 @@ static int gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, uint64_t
       SMX_LAUNCH_CHECK();
     }
     if (cursor_out) *cursor_out = u0;
-    return 0;
+    const uint64_t* u0_dev = nullptr;   // a chained call's cursor passes through
+    uint64_t* cursor_dev = nullptr;
+    smx_take_draw_chain(&u0_dev, &cursor_dev);
+    return smx_chain_passthrough(u0_dev, u0, cursor_dev, st);
   }
   // no cursor wanted: the asynchronous path (no host synchronisation)
+  res.cursor = u0;
   const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, st, cursor_out ? &res : nullptr, mk0);
   if (cursor_out) *cursor_out = res.cursor;
   return rc;
@@ -687,16 +691,20 @@ extern "C" int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out3, vo
 extern "C" int smx_delay_fill(uint64_t k0, uint64_t k1, uint64_t u0, uint32_t lo, uint64_t ex, uint64_t n,
                               uint32_t port, uint32_t* meta, uint64_t* cursor_out, void* stream) {
   MetaSink s{lo, port << 24, meta};
-  *cursor_out = u0;
-  if (n == 0) return 0;
-  if (ex == 1) {
-    smx_count_launch(); draw_const_kernel<MetaSink><<<nblk(n), T256, 0, (cudaStream_t)stream>>>(n, s);
-    SMX_LAUNCH_CHECK();
-    return 0;
+  if (cursor_out) *cursor_out = u0;
+  if (n == 0 || ex == 1) {   // (a chained call's cursor passes through)
+    const uint64_t* u0_dev = nullptr;
+    uint64_t* cursor_dev = nullptr;
+    smx_take_draw_chain(&u0_dev, &cursor_dev);
+    if (n) {
+      smx_count_launch(); draw_const_kernel<MetaSink><<<nblk(n), T256, 0, (cudaStream_t)stream>>>(n, s);
+      SMX_LAUNCH_CHECK();
+    }
+    return smx_chain_passthrough(u0_dev, u0, cursor_dev, (cudaStream_t)stream);
   }
-  DrawResult res;
-  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, (cudaStream_t)stream, &res);
-  *cursor_out = res.cursor;
+  DrawResult res;   // no cursor_out: asynchronous (window checked on the device)
+  const int rc = run_draw(Key{k0, k1}, u0, ex, n, s, (cudaStream_t)stream, cursor_out ? &res : nullptr);
+  if (cursor_out) *cursor_out = res.cursor;
   return rc;
 }
 

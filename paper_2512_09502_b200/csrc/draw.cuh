@@ -22,7 +22,8 @@ constexpr int DRAW_THREADS = 256;
 
 struct DrawRange {
   Key key;
-  uint64_t u0;       // first raw u32 position
+  uint64_t u0;       // first raw u32 position (replaced by *u0_dev when set)
+  const uint64_t* u0_dev;  // device cursor written by an earlier draw of the same stream, or null
   uint64_t n_raw;     // raw positions covered by the launch
   uint64_t per_warp;  // raw positions per warp (multiple of 8)
   Lemire lm;
@@ -312,8 +313,10 @@ __device__ __forceinline__ uint64_t nth_accept_cursor(const DrawRange& r, uint64
 
 template <class Sink, int MARK>
 __global__ void __launch_bounds__(DRAW_THREADS, SMX_DRAW_MIN_BLOCKS)
-    draw_onepass_kernel(DrawRange r, uint32_t tile, uint32_t n_tiles, uint64_t* desc, uint32_t* ticket,
+    draw_onepass_kernel(DrawRange r_in, uint32_t tile, uint32_t n_tiles, uint64_t* desc, uint32_t* ticket,
                         uint64_t* total_out, uint64_t n_out, Sink sink, uint64_t* cursor_out, DrawMark mk) {
+  DrawRange r = r_in;
+  if (r_in.u0_dev) r.u0 = *r_in.u0_dev;   // chained draw: starts where the previous one ended
   extern __shared__ uint32_t op_smem[];  // [DRAW_WARPS][tile] accepted values, then the mark bitmap
   uint32_t* smark = op_smem + DRAW_WARPS * tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

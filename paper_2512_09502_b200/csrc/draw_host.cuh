@@ -80,8 +80,14 @@ int launch_onepass(int mode, int G, size_t smem, cudaStream_t st, const DrawRang
 template <class Sink>
 int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink,
              cudaStream_t st, DrawResult* res, DrawMark mk = DrawMark{nullptr, nullptr, 0, 0, 0, 0, 0}) {
+  // device-side chaining (smx_draw_chain): start at *u0_dev, end cursor to
+  // *cursor_dev, no host readback
+  const uint64_t* u0_dev = nullptr;
+  uint64_t* cursor_dev = nullptr;
+  smx_take_draw_chain(&u0_dev, &cursor_dev);
+  if (u0_dev || cursor_dev) res = nullptr;
   if (res) res->cursor = u0;
-  if (n_out == 0) return 0;
+  if (n_out == 0) return smx_chain_passthrough(u0_dev, u0, cursor_dev, st);
   if (ex == 1) {  // numpy: range of one value consumes nothing
     smx_set_error("run_draw: ex == 1 must be handled by the caller");
     return -1;
@@ -93,7 +99,16 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
   DrawRange r;
   r.key = key;
   r.u0 = u0;
+  r.u0_dev = u0_dev;
   const bool async = res == nullptr;  // no cursor wanted: no host readback at all
+  static const bool onepass_env = [] {
+    const char* e = getenv("SMX_DRAW_ONEPASS");
+    return !(e && e[0] == '0');
+  }();
+  if ((u0_dev || cursor_dev) && !onepass_env) {
+    smx_set_error("run_draw: chained draws need the one-pass kernel");
+    return -1;
+  }
   r.lm.ex = (uint32_t)(ex & 0xffffffffULL);
   r.lm.threshold = ex == (1ULL << 32) ? 0u : (uint32_t)(((1ULL << 32) - ex) % ex);
   const double prej = (double)r.lm.threshold / 4294967296.0;
@@ -142,7 +157,7 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
       SMX_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint64_t) * (n_tiles + 2), st));
       uint32_t* ticket = reinterpret_cast<uint32_t*>(ws + n_tiles);
       uint64_t* total_d = ws + n_tiles + 1;
-      uint64_t* cur_p = async ? nullptr : ws + n_tiles + 2;
+      uint64_t* cur_p = cursor_dev ? cursor_dev : async ? nullptr : ws + n_tiles + 2;
       if (int rc2 = launch_onepass(mode, G, smem, st, r, tile, (uint32_t)n_tiles, ws, ticket, total_d, n_out, sink, cur_p, mk))
         return rc2;
       SMX_LAUNCH_CHECK();

@@ -310,6 +310,7 @@ class _Rank:
         # record-producing call first generates them into the pending
         # buffers, in call order (fused_ok then stays False)
         self.deferred: list[dict] = []
+        self.pending_errs: list = []   # device error flags of asynchronous syn-stream chains
         self.fused_ok = True
         self.fz = None     # fused-path session: record format and every call's digit regions
 
@@ -667,9 +668,10 @@ class Cluster:
             err = torch.zeros(1, dtype=torch.int32, device=dev)
             call("smx_normal_fill", syn_key[0], syn_key[1], _ptr(cur), float(w[1]), float(w[2]), n, chunks,
                  _ptr(ws), _ptr(seg_w), _ptr(cur[1:]), _ptr(err), st.stream)
-            if int(err.item()):
-                raise RuntimeError(f"normal weight chain error {int(err.item())}")
-            u32 = 2 * int(cur[1].item())
+            st.pending_errs.append(err)   # checked at prepare (no synchronisation per call)
+            # next32 after next64 words starts at the next word: u32 cursor = 2 x words,
+            # handed to the delay draw on the device
+            u32 = cur[1:2] * 2
         else:
             wv = np.asarray(w, dtype=np.float64)
             if wv.ndim:
@@ -682,9 +684,13 @@ class Cluster:
             lo, hi = int(d[1]), int(d[2])
             if hi > ROW_MASK:
                 raise DelayRangeError("delay >= 2^24 steps not representable")
-            cur = np.zeros(1, dtype=np.uint64)
-            call("smx_delay_fill", syn_key[0], syn_key[1], u32, lo, hi - lo + 1, n, port, _ptr(seg_m),
-                 cur.ctypes.data, st.stream)
+            if isinstance(u32, torch.Tensor):   # continues after the normal weights (device cursor)
+                call("smx_draw_chain", _ptr(u32), 0)
+                call("smx_delay_fill", syn_key[0], syn_key[1], 0, lo, hi - lo + 1, n, port, _ptr(seg_m), 0,
+                     st.stream)
+            else:
+                call("smx_delay_fill", syn_key[0], syn_key[1], u32, lo, hi - lo + 1, n, port, _ptr(seg_m), 0,
+                     st.stream)
         else:
             dv = np.asarray(d, dtype=np.int64)
             if dv.ndim:
@@ -752,11 +758,22 @@ class Cluster:
                 call("smx_gen_draw", local_key[0], local_key[1], 0, n_tgt, n, 2, 1, _ptr(key_tab),
                      _ptr(pay_tab), int(conn.k_out), _ptr(keys), _ptr(vals), 0, 0, 0, 0, 0, 0, cur_out, sk)
             else:  # fixed_total: positions (aligned) then targets (local; same stream locally)
-                call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 0, _ptr(key_tab),
-                     0, 1, _ptr(keys), 0, _ptr(pos_bits), 0, _words(n_src), 0, 0, 0, cur.ctypes.data, sk)
-                u0 = int(cur[0]) if local_key == aligned_key else 0
-                call("smx_gen_draw", local_key[0], local_key[1], u0, n_tgt, n, 0, 1, 0,
-                     _ptr(pay_tab), 1, 0, _ptr(vals), 0, 0, 0, 0, 0, 0, cur.ctypes.data, sk)
+                same = local_key == aligned_key
+                if same and not autapse_fix:
+                    # the target draw starts where the position draw ended: cursor chained on the device
+                    cdev = torch.empty(1, dtype=torch.int64, device=st.device)
+                    call("smx_draw_chain", 0, _ptr(cdev))
+                    call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 0, _ptr(key_tab),
+                         0, 1, _ptr(keys), 0, _ptr(pos_bits), 0, _words(n_src), 0, 0, 0, 0, sk)
+                    call("smx_draw_chain", _ptr(cdev), 0)
+                    call("smx_gen_draw", local_key[0], local_key[1], 0, n_tgt, n, 0, 1, 0,
+                         _ptr(pay_tab), 1, 0, _ptr(vals), 0, 0, 0, 0, 0, 0, 0, sk)
+                else:
+                    call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, n, 1, 0, _ptr(key_tab),
+                         0, 1, _ptr(keys), 0, _ptr(pos_bits), 0, _words(n_src), 0, 0, 0, cur_out, sk)
+                    u0 = int(cur[0]) if same else 0
+                    call("smx_gen_draw", local_key[0], local_key[1], u0, n_tgt, n, 0, 1, 0,
+                         _ptr(pay_tab), 1, 0, _ptr(vals), 0, 0, 0, 0, 0, 0, cur_out, sk)
         if self.prof is not None:
             self.prof["gen"].append((ev0, self._event(st)))
         if autapse_fix and n:
@@ -1727,6 +1744,11 @@ class Cluster:
         main.wait_stream(side)
         _record_stream(st.__dict__, main)  # side-stream allocations are used on main
         check(_lib.lib().smx_check_device_errors(sk), "construction")  # asynchronous draws
+        if st.pending_errs:
+            e = int(torch.stack(st.pending_errs).max().item())
+            st.pending_errs = []
+            if e:
+                raise RuntimeError(f"normal weight chain error {e}")
         if fused and not self._fused_check(st):
             # a digit region overflowed or a raw window was short (both ~never):
             # regenerate every deferred call into the pending buffers and sort

@@ -59,7 +59,8 @@ for m in ("create_neurons", "add_poisson_source", "connect_fixed_indegree_distri
           "_prepare_tables", "_fused_sort", "_fused_eager", "_fused_ready", "_fused_check", "_sort_pending",
           "_alloc_propagation", "_dist_target", "_routes", "_compact", "_delay_stats", "_dist", "_present_ranks",
           "_final_pieces", "_assign", "_syn_class", "_dist_accounting", "_defer", "_tables", "_replay_start",
-          "_replay_finish", "_dist_replay", "_dist_tables"):
+          "_replay_finish", "_dist_replay", "_dist_tables", "connect", "_emit_records", "_write_syn",
+          "_write_syn_random", "_make_wide", "_fused_off", "_gen_deferred", "_prepare_tables"):
     wrap(engine.Cluster, m)
 neur = int(os.environ.get("NEURONS", "100000"))
 P = models.BalancedParams(neurons_per_rank=neur, k_exc=9000, k_inh=2250)
@@ -80,7 +81,10 @@ for it in range(4):
     if world > 1:
         dist.barrier()
     c = engine.Cluster(cfg)
-    models.build_balanced_network(c, P)
+    if os.environ.get("C2"):   # PD microcircuit, full scale
+        models.build_microcircuit(c, models.MicrocircuitParams(scale=1.0))
+    else:
+        models.build_balanced_network(c, P)
     c.prepare()
     e1.record()
     host = time.perf_counter() - t0

@@ -27,6 +27,7 @@ constexpr int PC = 2048;          // words per chunk
 constexpr int PE = 64;            // entry offsets tracked per chunk
 constexpr int PG = 64;            // chunks per composition group
 constexpr int P_THREADS = 128;
+constexpr int J_RAW_WORDS = PC;   // emit_kernel's staged words (normals start inside the chunk)
 
 struct PoisJob {
   smx::Key key;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
     uint64_t b[4];
     smx::philox4x64_10(((cw >> 2) + q) + 1, J.key, b);  // cw is a multiple of 4
 #pragma unroll
-    for (int i = 0; i < 4; ++i) U[4 * q + i] = smx::u53(b[i]);
+    for (int i = 0; i < 4; ++i) U[4 * q + i] = J.kind == 1 ? __longlong_as_double((long long)b[i]) : smx::u53(b[i]);
   }
   __syncthreads();
   // len(w) for w in [0, PC + PE): products forward; words past the window
@@ -138,12 +139,18 @@ __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
         if (k >= 254) break;
       }
     } else {
-      // ziggurat: one word on the fast path, else run the sampler to count
-      smx::SeqStream st;
-      st.init(J.key, cw + w);
-      (void)smx::zig_standard_normal(st);
-      const uint64_t used = st.word - (cw + w);
-      k = used > 255 ? 255 : (int)used;
+      // ziggurat: one word on the fast path (raw words staged in U), else
+      // run the sampler from the word to count
+      double x;
+      if (smx::zig_first((uint64_t)__double_as_longlong(U[w]), x)) {
+        k = 1;
+      } else {
+        smx::SeqStream st;
+        st.init(J.key, cw + w);
+        (void)smx::zig_standard_normal(st);
+        const uint64_t used = st.word - (cw + w);
+        k = used > 255 ? 255 : (int)used;
+      }
     }
     if (k >= PE) atomicExch(J.err, 11);
     L[w] = (uint8_t)k;
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__(PE) within_kernel(PoisJob J, const uint8_t* ge
   }
 }
 
-__device__ __forceinline__ void emit(const PoisJob& J, uint64_t k, int c, int p, int len) {
+__device__ __forceinline__ void emit(const PoisJob& J, uint64_t k, int c, int p, int len, const uint64_t* raw) {
   if (k < J.n) {
     const uint64_t start = (*J.w0_dev & ~3ULL) + (uint64_t)c * PC + p;
     if (J.kind == 0) {
@@ -315,9 +322,12 @@ __device__ __forceinline__ void emit(const PoisJob& J, uint64_t k, int c, int p,
       if (!ptrs_trial(J, u, v, cnt) || cnt < 0 || cnt > 255) atomicExch(J.err, 14);  // u8 counts
       static_cast<uint8_t*>(J.out)[k] = (uint8_t)cnt;
     } else {  // numpy random_normal: loc + scale * z, no FMA
-      smx::SeqStream st;
-      st.init(J.key, start);
-      const double z = smx::zig_standard_normal(st);
+      double z;
+      if (len != 1 || !smx::zig_first(raw[p], z)) {   // (raw: the chunk's words, staged)
+        smx::SeqStream st;
+        st.init(J.key, start);
+        z = smx::zig_standard_normal(st);
+      }
       static_cast<double*>(J.out)[k] = __dadd_rn(J.loc, __dmul_rn(J.scale, z));
     }
     if (k == J.n - 1) *J.cursor = start + len;
@@ -327,15 +337,26 @@ __device__ __forceinline__ void emit(const PoisJob& J, uint64_t k, int c, int p,
 __global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
   __shared__ uint32_t ws[32];
   __shared__ int merge_p, pre_n;
+  __shared__ uint64_t raw[J_RAW_WORDS];   // normals: the chunk's words
   const int c = blockIdx.x, tid = threadIdx.x;
   const uint64_t kb = J.kbase[c];
   if (kb >= J.n) return;
   const uint8_t* L = J.len + (size_t)c * PC;
   const uint32_t* S0 = J.s0 + (size_t)c * (PC / 32);
+  if (J.kind == 1) {
+    const uint64_t cw = (*J.w0_dev & ~3ULL) + (uint64_t)c * PC;
+    for (int q = tid; q < PC / 4; q += P_THREADS) {
+      uint64_t b[4];
+      smx::philox4x64_10(((cw >> 2) + q) + 1, J.key, b);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) raw[4 * q + i] = b[i];
+    }
+    __syncthreads();
+  }
   if (tid == 0) {
     int p = J.entry[c], pre = 0;
     while (p < PC && !((S0[p >> 5] >> (p & 31)) & 1)) {
-      emit(J, kb + pre, c, p, L[p]);
+      emit(J, kb + pre, c, p, L[p], raw);
       ++pre;
       p += L[p];
     }
@@ -362,7 +383,7 @@ __global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
       const int p = q * 32 + b;
-      emit(J, k, c, p, L[p]);
+      emit(J, k, c, p, L[p], raw);
       ++k;
     }
   }

@@ -1843,6 +1843,10 @@ class Cluster:
 
     # ------------------------------------------------- fused generation + sort
     FUSED_ENABLED = os.environ.get("SMX_FUSED", "1") != "0"
+    # Poisson drive batch: at least this many steps per batch (the batch's
+    # sequential composition kernels are a fixed cost; longer batches
+    # amortise them, at the price of generating up to one batch ahead)
+    POIS_MIN_STEPS = int(os.environ.get("SMX_POIS_MIN_STEPS", "64"))
 
     def _defer_ok(self, st: _Rank, cls, ex: int, n: int) -> bool:
         return (self.fused_enabled and st.fused_ok and cls is not None and not st.wide and ex >= 2 and n > 0
@@ -2218,7 +2222,7 @@ class Cluster:
         # batches and can be replayed from a CUDA graph).  The fused kernels
         # add a count at its arrival step now = t + d, reading back up to d
         # steps: S >= max Poisson delay keeps that inside the previous batch.
-        max_pd = max([int(d["delay"]) for d in st.devices] + [64])
+        max_pd = max([int(d["delay"]) for d in st.devices] + [self.POIS_MIN_STEPS])
         st.pois_steps = B * max(1, -(-max_pd // B))
         for d in st.devices:
             nt = len(d["targets"])

@@ -227,7 +227,13 @@ def run_reference(args):
         "impl": "reference", "metric": "construction_synapses_per_s", "value": value, "unit": "synapses/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
-        "config": {"workload": "hpc_benchmark_C3_sampled", "neurons_per_rank": n, "k_in": k_e + k_i},
+        # the GPU arm's config (the metric is per synapse), with the bounded
+        # sample each step actually builds
+        "config": {"workload": "hpc_benchmark_C3_strong" if args.strong else "hpc_benchmark_C3_weak",
+                   "neurons_per_gpu": args.neurons, "k_in": args.k_exc + args.k_inh,
+                   "synapses_per_gpu": args.neurons * (args.k_exc + args.k_inh),
+                   "comm": "collective" if args.gpus > 1 else "p2p", "parallelism": f"ranks{args.gpus}",
+                   "seed": args.seed, "sample": {"neurons": n, "k_in": k_e + k_i, "synapses": syn}},
         "cpu_baseline": {"value": value, "unit": "synapses/s", "cores": 1, "kind": kind, "sample": sample,
                          "host": host_info()},
         "e2e": {"value": value, "unit": "synapses/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -52,6 +52,9 @@ constexpr int FG_MAXP = 8;
 #ifndef SMX_FG_MIN_BLOCKS
 #define SMX_FG_MIN_BLOCKS 2
 #endif
+#ifndef SMX_FG_LB_WIN
+#define SMX_FG_LB_WIN 4   // look-back descriptors read per step
+#endif
 #ifndef SMX_FG_FREE_SMS
 #define SMX_FG_FREE_SMS 8
 #endif
@@ -135,6 +138,10 @@ __device__ __forceinline__ uint32_t fg_rank(uint32_t d, bool valid, uint32_t vm,
   old = __shfl_sync(0xffffffffu, old, leader);
   return valid ? old + __popc(peers & lt) : 0xffffu;
 }
+
+#ifdef SMX_FG_LBSTAT   // tuning aid: look-back statistics of digit 0 (tiles, steps, descriptors, waits)
+__device__ unsigned long long g_fg_lbstat[4];
+#endif
 
 // WIDE: region slots may exceed 2^31 (64-bit staging offsets)
 template <int KM, int LB, bool WIDE>
@@ -244,26 +251,37 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     uint64_t excl = 0;
     if (tid < B) {
       if (t > 0) {
-        // walk back 4 descriptors per step (independent loads): a tile
-        // usually finds an inclusive prefix within the first few
+        // walk back SMX_FG_LB_WIN descriptors per step (independent loads):
+        // a tile usually finds an inclusive prefix ~18 tiles back
         uint32_t e = 0;
         for (int64_t i = (int64_t)t - 1;;) {
-          uint32_t w[4];
+          uint32_t w[SMX_FG_LB_WIN];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) w[u] = i - u >= 0 ? ld_vol(g.status + (size_t)(i - u) * B + tid) : ST_P;
+          for (int u = 0; u < SMX_FG_LB_WIN; ++u)
+            w[u] = i - u >= 0 ? ld_vol(g.status + (size_t)(i - u) * B + tid) : ST_P;
           int used = 0;
           bool done = false;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < SMX_FG_LB_WIN; ++u) {
             if (done || used < u || w[u] == 0) continue;  // stop at a predecessor still drawing
             e += w[u] & ST_VAL;
             used = u + 1;
             done = (w[u] & ST_P) != 0;
           }
+#ifdef SMX_FG_LBSTAT
+          if (tid == 0) {
+            atomicAdd(&g_fg_lbstat[1], 1ull);
+            atomicAdd(&g_fg_lbstat[2], (unsigned long long)used);
+            if (used == 0) atomicAdd(&g_fg_lbstat[3], 1ull);
+          }
+#endif
           if (done) break;
           if (used == 0) __nanosleep(64);  // predecessor still drawing: leave the issue slots to others
           i -= used;
         }
+#ifdef SMX_FG_LBSTAT
+        if (tid == 0) atomicAdd(&g_fg_lbstat[0], 1ull);
+#endif
         excl = e;
         st_vol(g.status + (size_t)t * B + tid, ST_P | (e + c));
       }
@@ -935,6 +953,17 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
   cudaFreeAsync(ws, st);
   return rc;
 }
+
+#ifdef SMX_FG_LBSTAT
+extern "C" int smx_fg_lbstat(unsigned long long* out, int reset) {
+  SMX_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_fg_lbstat, sizeof(unsigned long long) * 4));
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    SMX_CUDA_CHECK(cudaMemcpyToSymbol(g_fg_lbstat, z, sizeof(z)));
+  }
+  return 0;
+}
+#endif
 
 // Pass B: stable sort of the digit regions by the high digit.  Region
 // r = digit * per_digit + call holds fill[r] records at rptr[r] (device

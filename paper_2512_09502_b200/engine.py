@@ -59,10 +59,36 @@ def _up(arr, dev) -> torch.Tensor:
     return torch.from_numpy(a).pin_memory().to(dev, non_blocking=True)
 
 
+_RUNS: dict = {}   # id(array) -> (weakref, length, first, mid, last, consecutive, min, max)
+
+
+def _run_info(a: np.ndarray):
+    """(consecutive, min, max) of an int64 node array.  Builders pass the
+    same population arrays to many calls, so the O(n) scan is cached per
+    array object (weak reference; length and three samples re-checked)."""
+    import weakref
+    n = len(a)
+    if n == 0:
+        return False, 0, -1
+    key = id(a)
+    hit = _RUNS.get(key)
+    f, m, l = int(a[0]), int(a[n // 2]), int(a[-1])
+    if hit is not None and hit[0]() is a and hit[1:5] == (n, f, m, l):
+        return hit[5:]
+    cons = n > 1 and l - f == n - 1 and bool((np.diff(a) == 1).all())
+    lo, hi = (f, l) if cons else (int(a.min()), int(a.max()))
+    try:
+        if len(_RUNS) > 4096:
+            _RUNS.clear()
+        _RUNS[key] = (weakref.ref(a), n, f, m, l, cons, lo, hi)
+    except TypeError:   # not weak-referenceable (a view of a temporary): no cache
+        pass
+    return cons, lo, hi
+
+
 def _consecutive(a: np.ndarray) -> bool:
     """a is one run first, first + 1, ... (the common population case)."""
-    n = len(a)
-    return n > 1 and int(a[-1]) - int(a[0]) == n - 1 and bool((np.diff(a) == 1).all())
+    return _run_info(a)[0]
 
 
 def _up_index(arr, dev) -> torch.Tensor:
@@ -71,7 +97,7 @@ def _up_index(arr, dev) -> torch.Tensor:
     being copied from pageable host memory."""
     a = np.ascontiguousarray(arr, dtype=np.int64)
     n = len(a)
-    if n > 1024 and a[-1] - a[0] == n - 1 and bool((np.diff(a) == 1).all()):
+    if n > 1024 and _consecutive(a):
         H2D_BYTES[0] += 16
         return torch.arange(int(a[0]), int(a[0]) + n, dtype=torch.int64, device=dev)
     return _up(a, dev)
@@ -806,7 +832,8 @@ class Cluster:
         if len(sources) == 0 or len(targets) == 0:
             raise ValueError("connect needs non-empty source and target sets")
         for name, arr, r in (("source", sources, rank[0]), ("target", targets, rank[1])):
-            if arr.min() < 0 or arr.max() >= self.n_nodes[r]:
+            _, lo, hi = _run_info(arr)
+            if lo < 0 or hi >= self.n_nodes[r]:
                 raise ValueError(f"{name} index outside the rank's node range")
         conn.validate(len(sources), len(targets))
         syn.validate()

@@ -60,7 +60,9 @@ for m in ("create_neurons", "add_poisson_source", "connect_fixed_indegree_distri
           "_alloc_propagation", "_dist_target", "_routes", "_compact", "_delay_stats", "_dist", "_present_ranks",
           "_final_pieces", "_assign", "_syn_class", "_dist_accounting", "_defer", "_tables", "_replay_start",
           "_replay_finish", "_dist_replay", "_dist_tables", "connect", "_emit_records", "_write_syn",
-          "_write_syn_random", "_make_wide", "_fused_off", "_gen_deferred", "_prepare_tables"):
+          "_write_syn_random", "_make_wide", "_fused_off", "_gen_deferred", "_prepare_tables", "connect_remote",
+          "_remote", "_remote_deferred", "_connect_local", "_validate_conn",
+          "_replay_positions"):
     wrap(engine.Cluster, m)
 neur = int(os.environ.get("NEURONS", "100000"))
 P = models.BalancedParams(neurons_per_rank=neur, k_exc=9000, k_inh=2250)
@@ -70,7 +72,8 @@ if world > 1:   # under torchrun: one rank per GPU, rank 0 prints
     import torch.distributed as dist
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
-cfg = api.SimConfig(n_ranks=world, comm_mode="collective" if world > 1 else "p2p", seed=12345)
+cfg = api.SimConfig(n_ranks=world, comm_mode="collective" if world > 1 and not os.environ.get("C4") else "p2p",
+                    seed=12345)
 for it in range(4):
     T.clear()
     N.clear()
@@ -83,6 +86,11 @@ for it in range(4):
     c = engine.Cluster(cfg)
     if os.environ.get("C2"):   # PD microcircuit, full scale
         models.build_microcircuit(c, models.MicrocircuitParams(scale=1.0))
+    elif os.environ.get("C4"):   # multi-area, 4 areas per rank, p2p
+        areas = [models.AreaSpec(f"A{i:02d}", 129_063, 1) for i in range(4 * world)]
+        asg, _ = models.pack_areas(areas, world)
+        models.build_multi_area(c, areas, asg, models.MultiAreaParams(k_intra_exc=3600, k_intra_inh=900,
+                                                                      k_inter=44, delay_steps=15))
     else:
         models.build_balanced_network(c, P)
     c.prepare()

@@ -19,6 +19,8 @@
 //                   the S0 starts in parallel: count[k] = len(start_k) - 1.
 // Exact for every input: no speculation is assumed beyond E (a sample longer
 // than E-1 words raises the error flag instead of being mis-composed).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -389,6 +391,273 @@ __global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// One-pass form of the same chain (opt-in, see run_chain): one CTA per chunk, chunks taken
+// by ticket.  A chunk computes U, len and its entry->exit map exactly as
+// chunk_kernel does, then publishes a 64-bit descriptor for its successors:
+//   MAP  its exit when every entry offset leads to the same exit (orbits
+//        merge inside the chunk: nearly always), so the successor knows its
+//        entry without waiting for this chunk's entry;
+//   AGG  its true entry is known: true exit and the samples started here;
+//   INC  also the samples started in every earlier chunk (inclusive).
+// Its true entry comes from the predecessor (MAP with a constant exit, or
+// AGG / INC), its first sample index from a decoupled look-back over the
+// predecessors' counts, and it emits its samples from its shared memory.
+// Replaces chunk + group + across + within + emit (no len / s0 round trip).
+// ---------------------------------------------------------------------------
+constexpr uint64_t CD_STATE = 62, CD_CONST = 61, CD_EXIT = 48;
+constexpr uint64_t CD_CNT_MASK = (1ULL << 48) - 1;
+constexpr uint64_t CD_MAP = 1, CD_AGG = 2, CD_INC = 3;
+
+__device__ __forceinline__ uint64_t ld_vol64(const uint64_t* p) { return *(const volatile uint64_t*)p; }
+
+__global__ void __launch_bounds__(P_THREADS) chain_onepass_kernel(PoisJob J, uint64_t* desc, uint32_t* ticket) {
+  __shared__ double U[PC + PE];
+  __shared__ uint8_t L[PC + PE];
+  __shared__ uint32_t S0[PC / 32];
+  __shared__ uint32_t cnt0_pos[PC / 32 + 1];
+  __shared__ int seg_exit[P_THREADS];
+  __shared__ uint16_t M16[P_THREADS];
+  __shared__ uint8_t exs[PE];
+  __shared__ uint16_t cts[PE];
+  __shared__ uint32_t ws[32];
+  __shared__ int exit0, count0, s_c, s_entry, merge_p, pre_n;
+  __shared__ unsigned long long s_kb;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_c = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int c = s_c;
+  const uint64_t cw = (*J.w0_dev & ~3ULL) + (uint64_t)c * PC;
+  for (int q = tid; q < (PC + PE) / 4; q += P_THREADS) {
+    uint64_t b[4];
+    smx::philox4x64_10(((cw >> 2) + q) + 1, J.key, b);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) U[4 * q + i] = J.kind == 1 ? __longlong_as_double((long long)b[i]) : smx::u53(b[i]);
+  }
+  __syncthreads();
+  for (int w = tid; w < PC + PE; w += P_THREADS) {
+    int k = 0;
+    if (J.kind == 0) {
+      double prod = 1.0;
+      for (;;) {
+        const int idx = w + k;
+        const double u = idx < PC + PE ? U[idx] : smx::u53(smx::philox_word(J.key, cw + idx));
+        prod = __dmul_rn(prod, u);
+        ++k;
+        if (!(prod > J.enlam)) break;
+        if (k >= 255) break;
+      }
+    } else if (J.kind == 2) {
+      for (;;) {
+        const int i0 = w + k, i1 = w + k + 1;
+        const double u = i0 < PC + PE ? U[i0] : smx::u53(smx::philox_word(J.key, cw + i0));
+        const double v = i1 < PC + PE ? U[i1] : smx::u53(smx::philox_word(J.key, cw + i1));
+        k += 2;
+        long long cnt;
+        if (ptrs_trial(J, u, v, cnt)) break;
+        if (k >= 254) break;
+      }
+    } else {
+      double x;
+      if (smx::zig_first((uint64_t)__double_as_longlong(U[w]), x)) {
+        k = 1;
+      } else {
+        smx::SeqStream st;
+        st.init(J.key, cw + w);
+        (void)smx::zig_standard_normal(st);
+        const uint64_t used = st.word - (cw + w);
+        k = used > 255 ? 255 : (int)used;
+      }
+    }
+    if (k >= PE) atomicExch(J.err, 11);
+    L[w] = (uint8_t)k;
+  }
+  __syncthreads();
+  {  // orbit of starts from entry 0 (as chunk_kernel)
+    constexpr int SEG = PC / P_THREADS;
+    const int lo = SEG * tid, hi = lo + SEG;
+    uint32_t mask = 0;
+    int entry = lo, ex_ = lo;
+    while (ex_ < hi) { mask |= 1u << (ex_ - lo); ex_ += L[ex_]; }
+    seg_exit[tid] = ex_;
+    for (;;) {
+      __syncthreads();
+      const int e_in = tid == 0 ? 0 : seg_exit[tid - 1];
+      bool changed = false;
+      if (e_in != entry) {
+        entry = e_in;
+        uint32_t m = 0;
+        int p = e_in;
+        while (p < hi && !((mask >> (p - lo)) & 1)) { m |= 1u << (p - lo); p += L[p]; }
+        const int ex_new = p < hi ? ex_ : p;
+        mask = p < hi ? (m | (mask & ~((1u << (p - lo)) - 1))) : m;
+        changed = ex_new != ex_;
+        ex_ = ex_new;
+      }
+      __syncthreads();
+      seg_exit[tid] = ex_;
+      if (!__syncthreads_or(changed)) break;
+    }
+    M16[tid] = (uint16_t)mask;
+    __syncthreads();
+    if (tid < PC / 32) S0[tid] = (uint32_t)M16[2 * tid] | ((uint32_t)M16[2 * tid + 1] << 16);
+    __syncthreads();
+    if (tid < 32) {
+      const uint32_t a = __popc(S0[2 * tid]), b = __popc(S0[2 * tid + 1]);
+      uint32_t x = a + b;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (tid >= o) x += y;
+      }
+      cnt0_pos[2 * tid] = x - a - b;
+      cnt0_pos[2 * tid + 1] = x - b;
+      if (tid == 31) { cnt0_pos[PC / 32] = x; count0 = (int)x; exit0 = seg_exit[P_THREADS - 1] - PC; }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < PE; e += P_THREADS) {  // entry -> (exit, samples started here)
+    int p = e, pre = 0, ex_ = -1, ct = 0;
+    while (p < PC) {
+      if ((S0[p >> 5] >> (p & 31)) & 1) {
+        const int rank = cnt0_pos[p >> 5] + __popc(S0[p >> 5] & ((1u << (p & 31)) - 1));
+        ex_ = exit0;
+        ct = pre + (count0 - rank);
+        break;
+      }
+      ++pre;
+      p += L[p];
+    }
+    if (ex_ < 0) { ex_ = p - PC; ct = pre; }
+    if (ex_ >= PE) { atomicExch(J.err, 12); ex_ = PE - 1; }
+    exs[e] = (uint8_t)ex_;
+    cts[e] = (uint16_t)ct;
+  }
+  __syncthreads();
+  if (tid < 32) {  // warp 0: publish, take the entry, look back
+    const int lane = tid;
+    int entry = 0;
+    uint64_t mine = 0, myexit = 0;
+    if (lane == 0) {
+      bool cons = true;
+      for (int e = 1; e < PE; ++e) cons &= exs[e] == exs[0];
+      // MAP: a constant exit lets the successor start without this chunk's entry
+      __threadfence();
+      *(volatile uint64_t*)(desc + c) = (CD_MAP << CD_STATE) | ((uint64_t)cons << CD_CONST) |
+                                        ((uint64_t)exs[0] << CD_EXIT);
+      // true entry: the predecessor's exit (constant map, or its true exit)
+      if (c == 0) {
+        entry = (int)(*J.w0_dev & 3);
+      } else {
+        uint64_t d;
+        for (;;) {
+          d = ld_vol64(desc + c - 1);
+          const uint64_t s = d >> CD_STATE;
+          if (s >= CD_AGG || (s == CD_MAP && ((d >> CD_CONST) & 1))) break;
+          __nanosleep(32);
+        }
+        entry = (int)((d >> CD_EXIT) & 0xff);
+      }
+      mine = cts[entry];
+      myexit = exs[entry];
+      __threadfence();
+      *(volatile uint64_t*)(desc + c) = (CD_AGG << CD_STATE) | (myexit << CD_EXIT) | mine;
+    }
+    // first sample index: warp-wide decoupled look-back, 32 descriptors per step
+    uint64_t kb = 0;
+    for (int q = c - 1; q >= 0;) {
+      const int qi = q - lane;
+      const uint64_t d = qi >= 0 ? ld_vol64(desc + qi) : (CD_INC << CD_STATE);
+      const uint64_t s = d >> CD_STATE;
+      const uint32_t inc = __ballot_sync(0xffffffffu, s == CD_INC);
+      const uint32_t notyet = __ballot_sync(0xffffffffu, s < CD_AGG);
+      const int first_inc = inc ? __ffs(inc) - 1 : 32;
+      const int first_wait = notyet ? __ffs(notyet) - 1 : 32;
+      if (first_wait < first_inc) {   // a predecessor before the nearest INC has no count yet
+        if (first_wait > 0) {         // take the ready ones and move on
+          uint64_t v = lane < first_wait ? (d & CD_CNT_MASK) : 0;
+          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          kb += v;
+          q -= first_wait;
+        } else {
+          __nanosleep(32);
+        }
+        continue;
+      }
+      uint64_t v = (lane <= first_inc && qi >= 0) ? (d & CD_CNT_MASK) : 0;
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      kb += v;
+      if (first_inc < 32) break;
+      q -= 32;
+    }
+    if (lane == 0) {
+      __threadfence();
+      *(volatile uint64_t*)(desc + c) = (CD_INC << CD_STATE) | (myexit << CD_EXIT) | ((kb + mine) & CD_CNT_MASK);
+      if (c == J.n_chunks - 1 && kb + mine < J.n) atomicExch(J.err, 13);  // window too small
+      s_kb = kb;
+      s_entry = entry;
+    }
+  }
+  __syncthreads();
+  const uint64_t kb = s_kb;
+  if (kb >= J.n) return;
+  const uint64_t* raw = reinterpret_cast<const uint64_t*>(U);   // kind 1: the words themselves
+  if (tid == 0) {  // from the true entry to the merge with the entry-0 orbit
+    int p = s_entry, pre = 0;
+    while (p < PC && !((S0[p >> 5] >> (p & 31)) & 1)) {
+      emit(J, kb + pre, c, p, L[p], raw);
+      ++pre;
+      p += L[p];
+    }
+    merge_p = p;
+    pre_n = pre;
+  }
+  __syncthreads();
+  const int m = merge_p;
+  if (m >= PC) return;
+  for (int q0 = 0; q0 < PC / 32; q0 += P_THREADS) {
+    const int q = q0 + tid;
+    uint32_t bits = 0;
+    if (q < PC / 32) {
+      bits = S0[q];
+      const int lo = q * 32;
+      if (m > lo) bits &= (m - lo >= 32) ? 0u : ~((1u << (m - lo)) - 1);
+    }
+    uint32_t tot;
+    const uint32_t exq = smx::block_excl_scan(__popc(bits), ws, tot);
+    uint64_t k = kb + pre_n + exq;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int p = q * 32 + b;
+      emit(J, k, c, p, L[p], raw);
+      ++k;
+    }
+  }
+}
+
+// The chain on `ws`: the one-pass kernel when SMX_CHAIN_ONEPASS=1, else
+// (default) the five kernels above.  Measured on B200 (C3 drive, C2
+// weights): the one-pass form is exact but slower -- RTF 0.057 vs 0.040, C2
+// 87 vs 69 ms -- its CTAs live through the entry wait, the look-back and the
+// emission while the multi-kernel form keeps every phase fully parallel.
+int run_chain(PoisJob& J, int n_chunks, void* ws, cudaStream_t st) {
+  static const bool onepass = [] {
+    const char* e = getenv("SMX_CHAIN_ONEPASS");
+    return e && e[0] == '1';
+  }();
+  if (onepass) {
+    uint64_t* desc = static_cast<uint64_t*>(ws);
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(desc + n_chunks);
+    SMX_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint64_t) * (n_chunks + 1), st));
+    J.n_chunks = n_chunks;
+    smx_count_launch(); chain_onepass_kernel<<<n_chunks, P_THREADS, 0, st>>>(J, desc, ticket);
+    SMX_LAUNCH_CHECK();
+    return 0;
+  }
+  return 1;   // caller runs the multi-kernel form
+}
+
 }  // namespace
 
 // Workspace sizes for a window of n_chunks chunks (bytes).
@@ -438,6 +707,7 @@ extern "C" int smx_poisson_counts(uint64_t k0, uint64_t k1, const uint64_t* curs
   J.out = counts;
   J.cursor = cursor_out;
   J.err = err;
+  if (const int rc = run_chain(J, n_chunks, ws, st); rc <= 0) return rc;
   smx_count_launch(); chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
   smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
@@ -490,6 +760,7 @@ extern "C" int smx_poisson_counts_ptrs(uint64_t k0, uint64_t k1, const uint64_t*
   J.out = counts;
   J.cursor = cursor_out;
   J.err = err;
+  if (const int rc = run_chain(J, n_chunks, ws, st); rc <= 0) return rc;
   smx_count_launch(); chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
   smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
@@ -531,6 +802,7 @@ extern "C" int smx_normal_fill(uint64_t k0, uint64_t k1, const uint64_t* cursor_
   J.out = values;
   J.cursor = cursor_out;
   J.err = err;
+  if (const int rc = run_chain(J, n_chunks, ws, st); rc <= 0) return rc;
   smx_count_launch(); chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
   smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);

@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(256) fb_tile_offsets_kernel(const __grid_const
 #define SMX_FB_CTAS (FB_THREADS >= 512 ? 2 : 3)
 #endif
 template <int BITS, bool WIDE>
-__global__ void __launch_bounds__(FB_THREADS, SMX_FB_CTAS) fb_scatter_kernel(const __grid_constant__ FusedSort s,
+__global__ void __launch_bounds__(FB_THREADS, BITS >= 12 ? 1 : SMX_FB_CTAS) fb_scatter_kernel(const __grid_constant__ FusedSort s,
                                                                    const uint32_t* off, const uint64_t* dbase,
                                                                    uint32_t n_tiles, uint32_t* tile_ctr) {
   constexpr int BINS = 1 << BITS;
@@ -977,8 +977,8 @@ extern "C" int smx_fused_sort(const uint64_t* rptr, const uint64_t* fill, const 
                               uint32_t* out, int* err, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   SMX_CUDA_CHECK(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * n_keys, st));
-  if (hi_bits < 8 || hi_bits > 11) {
-    smx_set_error("smx_fused_sort: high digit of %d bits (8..11 supported)", hi_bits);
+  if (hi_bits < 8 || hi_bits > 12) {
+    smx_set_error("smx_fused_sort: high digit of %d bits (8..12 supported)", hi_bits);
     return -1;
   }
   if (per_digit < 1) {
@@ -1037,7 +1037,8 @@ extern "C" int smx_fused_sort(const uint64_t* rptr, const uint64_t* fill, const 
     case 8: rc = fb_run<8>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;
     case 9: rc = fb_run<9>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;
     case 10: rc = fb_run<10>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;
-    default: rc = fb_run<11>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;
+    case 11: rc = fb_run<11>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;
+    default: rc = fb_run<12>(s, (uint32_t)nt, (uint32_t)nc, wide, st); break;   // 1 CTA/SM (221 KB SMEM)
   }
   cudaFreeAsync(dfirst, st);
   return rc;

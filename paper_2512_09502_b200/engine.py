@@ -826,12 +826,15 @@ class Cluster:
             self._fused_off(st)
         return d
 
-    def _validate_conn(self, rank, sources, targets, conn, syn, what="connect"):
+    def _validate_conn(self, rank, sources, targets, conn, syn, what="connect", ranges=True):
+        """Argument checks of a connect call.  ranges=False (a call that no
+        local rank takes part in, one process per GPU) skips the O(n) node
+        range scans: the processes that do take part raise on bad ranges."""
         sources = np.asarray(sources, dtype=np.int64)
         targets = np.asarray(targets, dtype=np.int64)
         if len(sources) == 0 or len(targets) == 0:
             raise ValueError("connect needs non-empty source and target sets")
-        for name, arr, r in (("source", sources, rank[0]), ("target", targets, rank[1])):
+        for name, arr, r in (("source", sources, rank[0]), ("target", targets, rank[1])) if ranges else ():
             _, lo, hi = _run_info(arr)
             if lo < 0 or hi >= self.n_nodes[r]:
                 raise ValueError(f"{name} index outside the rank's node range")
@@ -847,7 +850,8 @@ class Cluster:
     def _connect_local(self, rank, sources, targets, conn, syn, port, validated=False):
         self._require_unprepared()
         if not validated:
-            sources, targets = self._validate_conn((rank, rank), sources, targets, conn, syn)
+            sources, targets = self._validate_conn((rank, rank), sources, targets, conn, syn,
+                                                   ranges=self.is_local(rank))
         if port < 0:
             raise ValueError("ports must be >= 0")
         self.local_ctr[rank] += 1
@@ -900,7 +904,6 @@ class Cluster:
         if sr == tr:
             return self._connect_local(sr, sources, targets, conn, syn, port)
         self._require_unprepared()
-        sources, targets = self._validate_conn((sr, tr), sources, targets, conn, syn)
         members = None
         if group != POINT_TO_POINT:
             members = self.groups.get(group)
@@ -908,6 +911,9 @@ class Cluster:
                 raise ValueError(f"group {group} is not declared")
             if sr not in members or tr not in members:
                 raise ValueError(f"ranks {sr} and {tr} must both belong to group {group}")
+        involved = self.is_local(sr) or self.is_local(tr) or (
+            members is not None and any(self.is_local(m) for m in members))
+        sources, targets = self._validate_conn((sr, tr), sources, targets, conn, syn, ranges=involved)
         n_src, n_tgt = len(sources), len(targets)
         if group == POINT_TO_POINT:
             self.any_p2p = True
@@ -921,7 +927,9 @@ class Cluster:
         k_syn = self._key(("remote-syn", sr, tr, idx))
         n_rec = 0
         used_pos = None
-        span = int(sources.max()) + 1
+        if not involved:   # nothing local: the counters above are all this process needs
+            return n_rec
+        span = _run_info(sources)[2] + 1
         if self.is_local(tr) and self._remote_defer_ok(self.ranks[tr], conn, syn, port, n_src, n_tgt):
             n_rec, used_pos = self._remote_deferred(self.ranks[tr], sr, sources, targets, conn, syn, port, group,
                                                     k_src, flag, span)
@@ -2017,14 +2025,23 @@ class Cluster:
 
     def _fused_ready(self, st: _Rank) -> bool:
         """At prepare: can pass B take the rank's regions (the high digit fits
-        11 bits with the final node count; accounted calls own their keys)?"""
+        12 bits with the final node count; accounted calls own their keys)?"""
         z = st.fz
         if z is None or not st.fused_ok or not st.deferred:
             return False
         key_bits = max(1, int(st.n_nodes - 1).bit_length())
         z["hi"] = max(8, key_bits - z["lo"])
-        if z["hi"] > 11 or z["hi"] + z["pbits"] > 31:
+        if z["hi"] > 12 or z["hi"] + z["pbits"] > 32:
             return False
+        if z["hi"] + z["pbits"] == 32:
+            # 32-bit records: the all-ones word is the sentinel, so no call may
+            # be able to produce an all-ones payload (row 2^row_bits - 1 with
+            # the largest class index of its split)
+            n_cls = len(z["cidx"])
+            for zc in z["calls"]:
+                rb = zc["row_bits"]
+                if (st.n_real >= (1 << rb) and n_cls >= (1 << min(8, z["pbits"] - rb))):
+                    return False
         # records per source rank of distributed calls (modeled bytes) come
         # from the per-key counts: every accounted call's keys must be its own
         calls = st.deferred

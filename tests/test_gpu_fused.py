@@ -74,10 +74,12 @@ def _small(ns):
     return c
 
 
-@pytest.mark.parametrize("lo,case", [(0, "small"), (2, "small"), (1, "local_mix"), (3, "local_mix"),
+@pytest.mark.parametrize("lo,case", [(0, "small"), (2, "small"), (0, "local_mix"), (1, "local_mix"), (3, "local_mix"),
                                      (6, "local_mix"), (7, "local_mix"), (8, "local_mix"), (9, "local_mix")])
 def test_fused_digit_splits(lo, case, monkeypatch):
-    """Every low-digit width of pass A (the high digit takes the rest, 8..11 bits)."""
+    """Every low-digit width of pass A (the high digit takes the rest, 8..12
+    bits; local_mix at lo = 0 has 12-bit keys: the 12-bit pass B with
+    32-bit records)."""
     fn = _small if case == "small" else CASES["local_mix"]
     g = _build(False, fn)
     f = _build(True, fn, monkeypatch, lo)

@@ -280,6 +280,7 @@ class _Map:
         self.present = _Buf(torch.int32, device, fill=0)
         # node-value intervals that may hold images (host-side knowledge, for _dist_speculate)
         self.imaged: list = []
+        self.runs: dict = {}   # (lo, hi) source run imaged whole and consecutively -> its first image id
 
     def ensure(self, n_values: int):
         nw = _words(n_values)
@@ -995,7 +996,17 @@ class Cluster:
         call("smx_mark_values", _ptr(pos_bits), _ptr(src_dev), n_src, _ptr(vbits), st.stream)
         m = st.map_for(group, sr)
         m.ensure(span)
-        self._assign(st, vbits, [(0, _words(span), m)], [[(int(sources.min()), span)]])
+        # image ids on the host without a readback: a consecutive source run
+        # whose values had no images gets n_nodes, n_nodes + 1, ... (every
+        # source imaged when unflagged); a run imaged that way before keeps them
+        cons, lo, hi = _run_info(sources)
+        known = m.runs.get((lo, hi + 1)) if cons else None
+        fresh = (cons and not flag and known is None and
+                 not any(a < hi + 1 and lo < b for a, b in m.imaged))
+        n0 = st.n_nodes
+        n_new = self._assign(st, vbits, [(0, _words(span), m)], [[(lo, span)]])
+        if fresh and n_new == n_src:
+            known = m.runs[(lo, hi + 1)] = n0
         key_tab = torch.empty(n_src, dtype=torch.int32, device=dev)
         call("smx_gather_lut", _ptr(src_dev), n_src, _ptr(m.img_of.t), _ptr(key_tab), st.stream)
         self._check_real_targets(st, targets)
@@ -1004,7 +1015,8 @@ class Cluster:
         call("smx_pay_table", _ptr(tgt), n_tgt, _ptr(st.node2row.t), st.node2row.n, cls & 0xFF, _ptr(pay_tab),
              st.stream)
         n = k_in * n_tgt
-        self._defer(st, k_src, n_src, n, 1, key_tab, pay_tab, k_in, n_tgt, cls, src_host=key_tab.cpu().numpy())
+        src_host = np.arange(known, known + n_src, dtype=np.int64) if known is not None else key_tab.cpu().numpy()
+        self._defer(st, k_src, n_src, n, 1, key_tab, pay_tab, k_in, n_tgt, cls, src_host=src_host)
         st.mem.later("remote_batch", n_src, (int(group), sr), _popcount_dev(m.present.view()), n)
         return n, pos_bits
 

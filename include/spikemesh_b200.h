@@ -45,6 +45,10 @@ int smx_set_sync_policy(int flags);
  * null: its u0 argument) and writes its end cursor to *cursor_dev (device;
  * null: as usual), with no host synchronisation.  Taken once. */
 int smx_draw_chain(const uint64_t* u0_dev, uint64_t* cursor_dev);
+/* SMs pass A (smx_fused_gen) leaves empty for work on other streams -- the
+ * replays and small kernels of the calls that follow (0..16, default 8).
+ * Process-wide; a single-rank construction uses 0. */
+int smx_set_pass_a_free_sms(int n);
 int smx_stream_create(int priority, void** out);
 int smx_pool_setup(int device);
 /* device error word of asynchronous paths: read + clear (synchronises stream) */

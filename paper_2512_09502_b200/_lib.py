@@ -29,6 +29,7 @@ SIGNATURES = {
     "smx_pool_setup": (I32, [I32]),
     "smx_stream_create": (I32, [I32, P]),
     "smx_draw_chain": (I32, [P, P]),
+    "smx_set_pass_a_free_sms": (I32, [I32]),
     "smx_launch_count": (U64, []),
     "smx_philox_words": (I32, [U64, U64, U64, U64, P, P]),
     "smx_integers": (I32, [U64, U64, U64, I64, U64, U64, P, P, P]),

@@ -80,7 +80,12 @@ struct FusedGen {
   uint32_t* ticket;
   uint64_t* total;          // accepted draws in the window (last tile)
   int* overflow;
+  uint32_t free_sms;        // SMs 148 - free_sms .. 147 left empty (0: all SMs work)
 };
+
+// SMs pass A leaves to concurrent work (replays of later calls), per process
+// (smx_set_pass_a_free_sms; SMX_FG_FREE_SMS by default).
+static int g_fg_free_sms = SMX_FG_FREE_SMS;
 
 // KM 1: key table; 3: piecewise-affine pieces; 4: a single piece (key = v + delta)
 template <int KM>
@@ -165,10 +170,10 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = (1u << lane) - 1;
   uint16_t* mycnt = wcnt + warp * BC;
-  if (SMX_FG_FREE_SMS > 0) {  // CTAs placed on the reserved SMs leave at once (tiles go by ticket)
+  if (g.free_sms > 0) {  // CTAs placed on the reserved SMs leave at once (tiles go by ticket)
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    if (smid >= 148u - SMX_FG_FREE_SMS) return;
+    if (smid >= 148u - g.free_sms) return;
   }
   for (;;) {
     if (tid == 0) s_t = atomicAdd(g.ticket, 1u);
@@ -383,11 +388,11 @@ int fg_launch(const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
   // scheduler spreads CTAs round-robin, so a smaller grid would leave half
   // SMs, too small for a draw CTA); the CTAs that land on SMs 140..147 exit
   // at once, leaving those SMs empty
-  const uint32_t grid = std::min<uint32_t>(n_tiles + SMX_FG_FREE_SMS * SMX_FG_MIN_BLOCKS, 148u * SMX_FG_MIN_BLOCKS);
+  const uint32_t grid = std::min<uint32_t>(n_tiles + g.free_sms * SMX_FG_MIN_BLOCKS, 148u * SMX_FG_MIN_BLOCKS);
   smx_count_launch();
   fused_gen_kernel<KM, LB, WIDE><<<grid, FG_THREADS, smem, st>>>(g, n_tiles);
   SMX_LAUNCH_CHECK();
-  smx_long_kernel_mark(st);
+  if (g.free_sms) smx_long_kernel_mark(st);
   return 0;
 }
 
@@ -897,6 +902,7 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
     return -1;
   }
   FusedGen g{};
+  g.free_sms = (uint32_t)g_fg_free_sms;
   g.key = Key{k0, k1};
   g.lm.ex = (uint32_t)(ex & 0xffffffffULL);
   g.lm.threshold = ex == (1ULL << 32) ? 0u : (uint32_t)(((1ULL << 32) - ex) % ex);
@@ -964,6 +970,17 @@ extern "C" int smx_fg_lbstat(unsigned long long* out, int reset) {
   return 0;
 }
 #endif
+
+// SMs pass A leaves free for concurrent work (0..16; default SMX_FG_FREE_SMS).
+// A single-rank construction has nothing to run beside pass A: 0.
+extern "C" int smx_set_pass_a_free_sms(int n) {
+  if (n < 0 || n > 16) {
+    smx_set_error("smx_set_pass_a_free_sms: %d outside 0..16", n);
+    return -1;
+  }
+  g_fg_free_sms = n;
+  return 0;
+}
 
 // Pass B: stable sort of the digit regions by the high digit.  Region
 // r = digit * per_digit + call holds fill[r] records at rptr[r] (device

@@ -2015,6 +2015,9 @@ class Cluster:
         if ev0 is not None:
             ev0.record(gen)
         ktab = d["ktab"].ctypes.data if d["kmode"] == 3 else _ptr(d["ktab"])
+        # SMs left free for the replays / small kernels of later calls: only
+        # a multi-rank construction has any
+        call("smx_set_pass_a_free_sms", 0 if self.n_ranks == 1 else 8)
         call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"], _ptr(cpay),
              z["lo"], z["pbits"], _ptr(region), slots, _ptr(meta[:B]), _ptr(meta[B:]), _ptr(fills[0]),
              _ptr(fills[1]), _ptr(total), _ptr(z["flag"]), gen.cuda_stream)

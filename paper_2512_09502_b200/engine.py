@@ -59,31 +59,16 @@ def _up(arr, dev) -> torch.Tensor:
     return torch.from_numpy(a).pin_memory().to(dev, non_blocking=True)
 
 
-_RUNS: dict = {}   # id(array) -> (weakref, length, first, mid, last, consecutive, min, max)
-
-
 def _run_info(a: np.ndarray):
-    """(consecutive, min, max) of an int64 node array.  Builders pass the
-    same population arrays to many calls, so the O(n) scan is cached per
-    array object (weak reference; length and three samples re-checked)."""
-    import weakref
+    """(consecutive, min, max) of an int64 node array in one pass when it is
+    a run (the common population case).  Not cached: a caller may reuse and
+    refill an array between calls."""
     n = len(a)
     if n == 0:
         return False, 0, -1
-    key = id(a)
-    hit = _RUNS.get(key)
-    f, m, l = int(a[0]), int(a[n // 2]), int(a[-1])
-    if hit is not None and hit[0]() is a and hit[1:5] == (n, f, m, l):
-        return hit[5:]
+    f, l = int(a[0]), int(a[-1])
     cons = n > 1 and l - f == n - 1 and bool((np.diff(a) == 1).all())
-    lo, hi = (f, l) if cons else (int(a.min()), int(a.max()))
-    try:
-        if len(_RUNS) > 4096:
-            _RUNS.clear()
-        _RUNS[key] = (weakref.ref(a), n, f, m, l, cons, lo, hi)
-    except TypeError:   # not weak-referenceable (a view of a temporary): no cache
-        pass
-    return cons, lo, hi
+    return (cons, f, l) if cons else (cons, int(a.min()), int(a.max()))
 
 
 def _consecutive(a: np.ndarray) -> bool:

@@ -347,6 +347,7 @@ void smx_long_kernel_mark(cudaStream_t st);
 void smx_take_draw_chain(const uint64_t** u0_dev, uint64_t** cursor_dev);
 int smx_chain_passthrough(const uint64_t* u0_dev, uint64_t u0, uint64_t* cursor_dev, cudaStream_t st);
 int smx_grid_cap(int grid, int concurrent_cap);
+int smx_pass_a_free_slots();   // fused.cu: CTA slots pass A leaves free
 extern "C" int* smx_device_error_word(void);
 #define SMX_CUDA_CHECK(expr)                                                       \
   do {                                                                             \

@@ -150,7 +150,8 @@ int run_draw(Key key, uint64_t u0, uint64_t ex, uint64_t n_out, const Sink& sink
       r.per_warp = 0;
       // while pass A runs, the SMX_FG_FREE_SMS * 2 CTA slots it leaves
       const int G = smx_grid_cap((int)std::max<uint64_t>(1, std::min<uint64_t>((n_tiles + DRAW_WARPS - 1) / DRAW_WARPS,
-                                                                   148 * SMX_DRAW_MIN_BLOCKS)), 16);
+                                                                   148 * SMX_DRAW_MIN_BLOCKS)),
+                                  std::max(1, smx_pass_a_free_slots()));
       // [desc n_tiles][ticket][total][cursor]
       uint64_t* ws = nullptr;
       SMX_CUDA_CHECK(cudaMallocAsync((void**)&ws, sizeof(uint64_t) * (n_tiles + 3), st));

@@ -974,6 +974,9 @@ extern "C" int smx_fg_lbstat(unsigned long long* out, int reset) {
 }
 #endif
 
+// CTA slots (two per free SM) a kernel launched beside pass A can count on.
+int smx_pass_a_free_slots() { return g_fg_free_sms * SMX_FG_MIN_BLOCKS; }
+
 // SMs pass A leaves free for concurrent work (0..16; default SMX_FG_FREE_SMS).
 // A single-rank construction has nothing to run beside pass A: 0.
 extern "C" int smx_set_pass_a_free_sms(int n) {

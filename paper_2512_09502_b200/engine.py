@@ -1879,6 +1879,8 @@ class Cluster:
     # sequential composition kernels are a fixed cost; longer batches
     # amortise them, at the price of generating up to one batch ahead)
     POIS_MIN_STEPS = int(os.environ.get("SMX_POIS_MIN_STEPS", "64"))
+    # SMs pass A leaves to the replays of later calls in multi-rank runs
+    PASS_A_FREE_SMS = int(os.environ.get("SMX_PASS_A_FREE_SMS", "8"))
 
     def _defer_ok(self, st: _Rank, cls, ex: int, n: int) -> bool:
         return (self.fused_enabled and st.fused_ok and cls is not None and not st.wide and ex >= 2 and n > 0
@@ -2002,7 +2004,7 @@ class Cluster:
         ktab = d["ktab"].ctypes.data if d["kmode"] == 3 else _ptr(d["ktab"])
         # SMs left free for the replays / small kernels of later calls: only
         # a multi-rank construction has any
-        call("smx_set_pass_a_free_sms", 0 if self.n_ranks == 1 else 8)
+        call("smx_set_pass_a_free_sms", 0 if self.n_ranks == 1 else self.PASS_A_FREE_SMS)
         call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"], _ptr(cpay),
              z["lo"], z["pbits"], _ptr(region), slots, _ptr(meta[:B]), _ptr(meta[B:]), _ptr(fills[0]),
              _ptr(fills[1]), _ptr(total), _ptr(z["flag"]), gen.cuda_stream)

@@ -40,9 +40,17 @@ using namespace smx;
 namespace {
 
 // ------------------------------------------------------------------ pass A
-constexpr int FG_THREADS = 512;
+// 256 threads x 32 positions, 3 CTAs per SM (measured: pass A 10.3 -> 9.0 ms
+// on C3 against 512 x 16 x 2; 256 x 32 x 2 and x 4 were slower)
+#ifndef SMX_FG_THREADS
+#define SMX_FG_THREADS 256
+#endif
+#ifndef SMX_FG_IPT
+#define SMX_FG_IPT 32
+#endif
+constexpr int FG_THREADS = SMX_FG_THREADS;
 constexpr int FG_WARPS = FG_THREADS / 32;
-constexpr int FG_IPT = 16;                       // raw positions per thread per tile
+constexpr int FG_IPT = SMX_FG_IPT;               // raw positions per thread per tile (multiple of 8)
 constexpr int FG_TILE = FG_THREADS * FG_IPT;     // 8192 raw u32 positions per tile
 constexpr int FG_XS = FG_TILE + FG_TILE / 32;    // padded transpose buffer
 constexpr uint32_t FG_NOKEY = 0xFFFFFFFFu;       // rejected draw / outside the window
@@ -50,8 +58,9 @@ constexpr uint32_t FG_SENTINEL = 0xFFFFFFFFu;    // accepted draw past the call'
 constexpr uint32_t ST_A = 1u << 30, ST_P = 2u << 30, ST_VAL = (1u << 30) - 1;
 constexpr int FG_MAXP = 8;
 #ifndef SMX_FG_MIN_BLOCKS
-#define SMX_FG_MIN_BLOCKS 2
+#define SMX_FG_MIN_BLOCKS 3
 #endif
+static_assert(FG_IPT == 8 || FG_IPT == 16 || FG_IPT == 32, "padded transpose: a thread's run never crosses a pad word");
 #ifndef SMX_FG_LB_WIN
 #define SMX_FG_LB_WIN 4   // look-back descriptors read per step
 #endif
@@ -177,7 +186,7 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
   }
   for (;;) {
     if (tid == 0) s_t = atomicAdd(g.ticket, 1u);
-    if (tid < B) hist[tid] = 0;
+    for (int d = tid; d < B; d += FG_THREADS) hist[d] = 0;
     __syncthreads();
     const uint32_t t = s_t;
     if (t >= n_tiles) break;
@@ -186,9 +195,9 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     const uint64_t p0 = (uint64_t)t * FG_TILE + (uint64_t)tid * FG_IPT;
     const bool full = (uint64_t)(t + 1) * FG_TILE <= g.n_raw;
     const uint32_t lim = full ? FG_IPT : (g.n_raw > p0 ? (g.n_raw - p0 < FG_IPT ? (uint32_t)(g.n_raw - p0) : (uint32_t)FG_IPT) : 0u);
-    uint32_t* xw = xs + tid * FG_IPT + (tid >> 1);
+    uint32_t* xw = xs + tid * FG_IPT + (tid * FG_IPT) / 32;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < FG_IPT / 8; ++q) {
       uint64_t w[4];
       philox4x64_10(p0 / 8 + q + 1, g.key, w);
 #pragma unroll
@@ -218,10 +227,14 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     }
     for (int j = lane; j < BC / 2; j += 32) reinterpret_cast<uint32_t*>(mycnt)[j] = 0;
     __syncthreads();
-    uint32_t c = 0;
-    if (tid < B) {
-      c = hist[tid];
-      st_vol(g.status + (size_t)t * B + tid, (t == 0 ? ST_P : ST_A) | c);
+    // digits per thread (blocked: thread tid owns digits tid * DPTA ..)
+    constexpr int DPTA = (B + FG_THREADS - 1) / FG_THREADS;
+    uint32_t c[DPTA];
+#pragma unroll
+    for (int j = 0; j < DPTA; ++j) {
+      const int d = tid * DPTA + j;
+      c[j] = d < B ? hist[d] : 0u;
+      if (d < B) st_vol(g.status + (size_t)t * B + d, (t == 0 ? ST_P : ST_A) | c[j]);
     }
     uint32_t rank2[FG_IPT / 2];
     uint32_t run = 0;
@@ -241,20 +254,32 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     }
     __syncthreads();  // counters complete; xs is free
     // 3. per digit: tile start, per-warp bases
-    uint32_t tot;
-    const uint32_t ts = block_excl_scan(tid < B ? c : 0u, ws, tot);
-    if (tid < B) {  // wcnt[w][d] = staging position of warp w's first record of digit d
-      uint32_t acc = ts;
+    uint32_t tot, csum = 0;
+#pragma unroll
+    for (int j = 0; j < DPTA; ++j) csum += c[j];
+    uint32_t ts[DPTA];
+    ts[0] = block_excl_scan(csum, ws, tot);
+#pragma unroll
+    for (int j = 1; j < DPTA; ++j) ts[j] = ts[j - 1] + c[j - 1];
+#pragma unroll
+    for (int j = 0; j < DPTA; ++j) {  // wcnt[w][d] = staging position of warp w's first record of digit d
+      const int d = tid * DPTA + j;
+      if (d >= B) break;
+      uint32_t acc = ts[j];
 #pragma unroll
       for (int w = 0; w < FG_WARPS; ++w) {
-        const uint32_t x = wcnt[w * BC + tid];
-        wcnt[w * BC + tid] = (uint16_t)acc;
+        const uint32_t x = wcnt[w * BC + d];
+        wcnt[w * BC + d] = (uint16_t)acc;
         acc += x;
       }
     }
-    // 4. look-back: records of this digit in earlier tiles of the call
-    uint64_t excl = 0;
-    if (tid < B) {
+    // 4. look-back: records of each digit in earlier tiles of the call
+    uint64_t excl_sum = 0;
+#pragma unroll
+    for (int j = 0; j < DPTA; ++j) {
+      const int d = tid * DPTA + j;
+      if (d >= B) break;
+      uint64_t excl = 0;
       if (t > 0) {
         // walk back SMX_FG_LB_WIN descriptors per step (independent loads):
         // a tile usually finds an inclusive prefix ~18 tiles back
@@ -263,7 +288,7 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
           uint32_t w[SMX_FG_LB_WIN];
 #pragma unroll
           for (int u = 0; u < SMX_FG_LB_WIN; ++u)
-            w[u] = i - u >= 0 ? ld_vol(g.status + (size_t)(i - u) * B + tid) : ST_P;
+            w[u] = i - u >= 0 ? ld_vol(g.status + (size_t)(i - u) * B + d) : ST_P;
           int used = 0;
           bool done = false;
 #pragma unroll
@@ -288,20 +313,21 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
         if (tid == 0) atomicAdd(&g_fg_lbstat[0], 1ull);
 #endif
         excl = e;
-        st_vol(g.status + (size_t)t * B + tid, ST_P | (e + c));
+        st_vol(g.status + (size_t)t * B + d, ST_P | (e + c[j]));
       }
-      const uint64_t filled = g.fill_in[tid] + excl;
-      if (filled + c > g.rcap[tid]) {
+      excl_sum += excl;
+      const uint64_t filled = g.fill_in[d] + excl;
+      if (filled + c[j] > g.rcap[d]) {
         atomicExch(g.overflow, 1);
-        delta[tid] = ~0ull;
+        delta[d] = ~0ull;
       } else {
-        delta[tid] = g.rstart[tid] + filled - ts;
+        delta[d] = g.rstart[d] + filled - ts[j];
       }
       // clamped: an overflowing region is never read past its capacity
-      if (t == n_tiles - 1) g.fill_out[tid] = filled + c < g.rcap[tid] ? filled + c : g.rcap[tid];
+      if (t == n_tiles - 1) g.fill_out[d] = filled + c[j] < g.rcap[d] ? filled + c[j] : g.rcap[d];
     }
     // draw index of the tile's first accepted value = sum of the digit prefixes
-    unsigned long long sx = excl;
+    unsigned long long sx = excl_sum;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
     if (lane == 0) wred[warp] = sx;

@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
   __shared__ uint32_t wacc[FG_WARPS];
   __shared__ unsigned long long wred[FG_WARPS];
   __shared__ uint32_t s_t;
-  __shared__ uint32_t s_tq, s_tr, s_lim;  // target index / remainder of the tile's first draw, records left
+  __shared__ unsigned long long s_tq;     // target index of the tile's first draw (64-bit: per-record payloads)
+  __shared__ uint32_t s_tr, s_lim;        // remainder of the tile's first draw, records left
   __shared__ uint32_t s_cp[2];            // k_in >= tile: the (at most two) targets of the tile
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = (1u << lane) - 1;
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       // draw j of the tile = jbase + a: target index tq + (tr + a) / k (32-bit
       // from here on); records past the call's end become sentinels
       const uint64_t tq = jbase / g.kdiv;
-      s_tq = (uint32_t)tq;
+      s_tq = tq;
       s_tr = (uint32_t)(jbase - tq * g.kdiv);
       s_lim = jbase >= g.n_out ? 0u : (g.n_out - jbase > 0xffffffffull ? 0xffffffffu : (uint32_t)(g.n_out - jbase));
       if (g.kdiv >= FG_TILE) {
@@ -354,7 +355,8 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
     }
     __syncthreads();
     // 5. records, staged in digit order (accept ranks recomputed: fewer live registers)
-    const uint32_t tq = s_tq, tr = s_tr, left = s_lim;
+    const uint64_t tq = s_tq;
+    const uint32_t tr = s_tr, left = s_lim;
     const bool bigk = g.kdiv >= FG_TILE;   // j / k_in takes two values in a tile
     const uint32_t cp0 = s_cp[0], cp1 = s_cp[1], kth = g.kdiv - tr;
     uint32_t aw = (uint32_t)wbase;

@@ -727,6 +727,29 @@ class Cluster:
             self._defer(st, aligned_key, n_src, int(conn.k_in) * n_tgt, 1, key_tab, pay_tab, int(conn.k_in),
                         n_tgt, cls, src_host=np.asarray(sources, dtype=np.int64))
             return int(conn.k_in) * n_tgt, src
+        if (rule == "fixed_total" and local_key == aligned_key and tmp_base is None and pos_bits is None
+                and not autapse_fix and self._defer_ok(st, cls, n_src, int(conn.n_total))
+                and (st.deferred or int(conn.n_total) >= self.FUSED_TOTAL_MIN)):
+            # local fixed total: the target draws continue the stream where the
+            # position draws end -- that cursor from a count-only pass, the
+            # targets' payloads drawn per record, the positions deferred to
+            # pass A with those payloads (kdiv 1)
+            n = int(conn.n_total)
+            src, tgt, key_tab, pay_tab = self._tables(st, sources, targets, cls, None)
+            cdev = torch.zeros(1, dtype=torch.int64, device=st.device)   # stream cursor, chained on the device
+            piece = 1 << 31   # one draw call takes < 2^32 records
+            for j0 in range(0, n, piece):   # count-only: where the position draws end
+                call("smx_draw_chain", _ptr(cdev) if j0 else 0, _ptr(cdev))
+                call("smx_gen_draw", aligned_key[0], aligned_key[1], 0, n_src, min(piece, n - j0), 0, 0, 0, 0, 1,
+                     0, 0, 0, 0, 0, 0, 0, 0, 0, st.stream)
+            rec_pay = torch.empty(max(n, 1), dtype=torch.int32, device=st.device)
+            for j0 in range(0, n, piece):   # the targets' payloads, continuing that stream
+                call("smx_draw_chain", _ptr(cdev), _ptr(cdev))
+                call("smx_gen_draw", local_key[0], local_key[1], 0, n_tgt, min(piece, n - j0), 0, 1, 0,
+                     _ptr(pay_tab), 1, 0, _ptr(rec_pay[j0:]), 0, 0, 0, 0, 0, 0, 0, st.stream)
+            d = self._defer(st, aligned_key, n_src, n, 1, key_tab, rec_pay, 1, n, cls,
+                            src_host=np.asarray(sources, dtype=np.int64), per_record=True)
+            return n, src
         self._fused_off(st)
         if cls is None:
             self._make_wide(st)
@@ -799,12 +822,14 @@ class Cluster:
         st.commit_records(n)
         return n, src
 
-    def _defer(self, st: _Rank, key, ex, n, kmode, ktab, pay_tab, kdiv, n_tgt, cls, src_host=None, acct=None):
+    def _defer(self, st: _Rank, key, ex, n, kmode, ktab, pay_tab, kdiv, n_tgt, cls, src_host=None, acct=None,
+               per_record=False):
         """Register a fixed in-degree draw for the fused path and launch its
         pass A; when the record format cannot take it, every deferred call
         (this one included) goes through the general path instead."""
         lm_thr = 0 if ex == (1 << 32) else ((1 << 32) - ex) % ex
         d = dict(key=key, ex=int(ex), n=int(n), kmode=kmode, ktab=ktab, pay_tab=pay_tab, cls=int(cls),
+                 per_record=per_record, pay_compact=None,
                  kdiv=int(kdiv), n_tgt=int(n_tgt), src_host=src_host, acct=acct, prej=lm_thr / 4294967296.0,
                  src_run=src_host is not None and _consecutive(np.asarray(src_host)))
         st.deferred.append(d)
@@ -1879,6 +1904,10 @@ class Cluster:
     # sequential composition kernels are a fixed cost; longer batches
     # amortise them, at the price of generating up to one batch ahead)
     POIS_MIN_STEPS = int(os.environ.get("SMX_POIS_MIN_STEPS", "64"))
+    # fixed_total calls take the fused path when the rank is on it already, or
+    # from this size on (below it the general path's two draws + sort are
+    # faster; above it they do not fit: 32-bit record index, 20 B/synapse)
+    FUSED_TOTAL_MIN = int(os.environ.get("SMX_FUSED_TOTAL_MIN", str(1 << 31)))
     # SMs pass A leaves to the replays of later calls in multi-rank runs
     PASS_A_FREE_SMS = int(os.environ.get("SMX_PASS_A_FREE_SMS", "8"))
 
@@ -1899,6 +1928,13 @@ class Cluster:
 
     def _gen_deferred(self, st: _Rank, d: dict):
         n = d["n"]
+        if d.get("pay_compact") is not None:   # per-record payloads back to row | class << 24
+            p = d["pay_tab"]
+            p.bitwise_and_((1 << d["pay_compact"]) - 1)
+            c24 = int(d["cls"]) << 24
+            if c24:
+                p.bitwise_or_(c24 - (1 << 32) if c24 >= (1 << 31) else c24)
+            d["pay_compact"] = None
         base = st.reserve_records(n)
         keys, vals = st.keys.t[base:], st.vals.t[base:]
         sk = st.stream
@@ -1993,7 +2029,15 @@ class Cluster:
         meta = _up(np.concatenate([rstart, cap]), dev)
         fills = torch.zeros((2, B), dtype=torch.int64, device=dev)
         total = torch.zeros(1, dtype=torch.int64, device=dev)
-        cpay = (d["pay_tab"] & ROW_MASK) | (z["cidx"][d["cls"]] << row_bits)   # row | class index
+        if d["per_record"]:   # one payload per record (fixed_total): compacted in place, no second copy
+            cpay = d["pay_tab"]
+            if d["pay_compact"] is None:
+                cpay.bitwise_and_(ROW_MASK)
+                if z["cidx"][d["cls"]]:
+                    cpay.bitwise_or_(z["cidx"][d["cls"]] << row_bits)
+                d["pay_compact"] = row_bits
+        else:
+            cpay = (d["pay_tab"] & ROW_MASK) | (z["cidx"][d["cls"]] << row_bits)   # row | class index
         # pass A runs on the generation stream: the main stream keeps only the
         # small map / image kernels that the preparation side stream waits on
         gen = _gen_stream(dev)

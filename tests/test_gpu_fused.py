@@ -51,7 +51,25 @@ def _local_mix(ns):
     return c
 
 
+def _fixed_total_mix(ns):
+    """Local fixed_total calls (targets drawn per record, continuing the
+    position stream) between fixed in-degree calls, two classes, a scattered
+    source set."""
+    c = ns.make_cluster(ns.SimConfig(n_ranks=1, seed=37))
+    a = c.create_neurons(0, 2500, ns.LifParams(), -60.0)
+    b = c.create_neurons(0, 700, ns.LifParams(), -61.0)
+    A, Bn = np.arange(a.start, a.stop), np.arange(b.start, b.stop)
+    S, Sy = ns.ConnSpec, ns.SynSpec
+    rng = np.random.default_rng(5)
+    c.connect(0, A, Bn, S("fixed_total", n_total=90_000), Sy(0.25, 3))
+    c.connect(0, A, A, S("fixed_indegree", k_in=17), Sy(-0.5, 4))
+    c.connect(0, rng.permutation(A)[:333], A, S("fixed_total", n_total=41_111), Sy(-0.5, 4))
+    c.connect(0, Bn, Bn, S("fixed_total", n_total=5), Sy(0.25, 3))
+    return c
+
+
 CASES = {
+    "fixed_total_mix": _fixed_total_mix,
     "balanced_1r": _balanced(1, "p2p", 3000, 240, 60),
     "balanced_4r_coll": _balanced(4, "collective", 700, 80, 20),
     "balanced_3r_p2p": _balanced(3, "p2p", 900, 100, 25),

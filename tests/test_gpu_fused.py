@@ -69,7 +69,6 @@ def _fixed_total_mix(ns):
 
 
 CASES = {
-    "fixed_total_mix": _fixed_total_mix,
     "balanced_1r": _balanced(1, "p2p", 3000, 240, 60),
     "balanced_4r_coll": _balanced(4, "collective", 700, 80, 20),
     "balanced_3r_p2p": _balanced(3, "p2p", 900, 100, 25),
@@ -166,4 +165,18 @@ def test_speculative_distributed_keys(case, outcome, monkeypatch):
     assert f.spec_stats[outcome] > 0, f.spec_stats
     if outcome == "confirmed":
         assert all(st.store_path == "fused" for st in f.ranks.values())
+    assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))
+
+
+@pytest.mark.parametrize("min_total", [0, 100_000])
+def test_fused_fixed_total(min_total, monkeypatch):
+    """Local fixed_total on the fused path (cursor from a count-only draw,
+    targets per record, positions through pass A), always (0) or only once
+    the rank is on the fused path (the first, smaller call then takes the
+    general path and so does the rest): identical tables either way."""
+    from paper_2512_09502_b200.engine import Cluster
+    g = _build(False, _fixed_total_mix)
+    monkeypatch.setattr(Cluster, "FUSED_TOTAL_MIN", min_total)
+    f = _build(True, _fixed_total_mix)
+    assert f.ranks[0].store_path == ("fused" if min_total == 0 else "general")
     assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))

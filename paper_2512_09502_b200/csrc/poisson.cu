@@ -312,12 +312,15 @@ __global__ void __launch_bounds__(PE) within_kernel(PoisJob J, const uint8_t* ge
   }
 }
 
+// KIND < 0: dispatch on J.kind at run time (the one-pass kernel)
+template <int KIND = -1>
 __device__ __forceinline__ void emit(const PoisJob& J, uint64_t k, int c, int p, int len, const uint64_t* raw) {
+  const int kind = KIND >= 0 ? KIND : J.kind;
   if (k < J.n) {
     const uint64_t start = (*J.w0_dev & ~3ULL) + (uint64_t)c * PC + p;
-    if (J.kind == 0) {
+    if (kind == 0) {
       static_cast<uint8_t*>(J.out)[k] = (uint8_t)(len - 1);
-    } else if (J.kind == 2) {  // PTRS: the count of the accepted (last) trial
+    } else if (kind == 2) {  // PTRS: the count of the accepted (last) trial
       const double u = smx::u53(smx::philox_word(J.key, start + len - 2));
       const double v = smx::u53(smx::philox_word(J.key, start + len - 1));
       long long cnt = 0;
@@ -336,16 +339,19 @@ __device__ __forceinline__ void emit(const PoisJob& J, uint64_t k, int c, int p,
   }
 }
 
+// One instance per kind: the Poisson counts' instance carries neither the
+// normals' staged words (16 KB of SMEM) nor the samplers' registers.
+template <int KIND>
 __global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
   __shared__ uint32_t ws[32];
   __shared__ int merge_p, pre_n;
-  __shared__ uint64_t raw[J_RAW_WORDS];   // normals: the chunk's words
+  extern __shared__ uint64_t raw[];   // normals: the chunk's words (dynamic: kind 1 only)
   const int c = blockIdx.x, tid = threadIdx.x;
   const uint64_t kb = J.kbase[c];
   if (kb >= J.n) return;
   const uint8_t* L = J.len + (size_t)c * PC;
   const uint32_t* S0 = J.s0 + (size_t)c * (PC / 32);
-  if (J.kind == 1) {
+  if (KIND == 1) {
     const uint64_t cw = (*J.w0_dev & ~3ULL) + (uint64_t)c * PC;
     for (int q = tid; q < PC / 4; q += P_THREADS) {
       uint64_t b[4];
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
   if (tid == 0) {
     int p = J.entry[c], pre = 0;
     while (p < PC && !((S0[p >> 5] >> (p & 31)) & 1)) {
-      emit(J, kb + pre, c, p, L[p], raw);
+      emit<KIND>(J, kb + pre, c, p, L[p], raw);
       ++pre;
       p += L[p];
     }
@@ -385,7 +391,7 @@ __global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
       const int p = q * 32 + b;
-      emit(J, k, c, p, L[p], raw);
+      emit<KIND>(J, k, c, p, L[p], raw);
       ++k;
     }
   }
@@ -636,6 +642,19 @@ __global__ void __launch_bounds__(P_THREADS) chain_onepass_kernel(PoisJob J, uin
   }
 }
 
+int launch_emit(const PoisJob& J, int n_chunks, cudaStream_t st) {
+  smx_count_launch();
+  if (J.kind == 0) {
+    emit_kernel<0><<<n_chunks, P_THREADS, 0, st>>>(J);
+  } else if (J.kind == 2) {
+    emit_kernel<2><<<n_chunks, P_THREADS, 0, st>>>(J);
+  } else {
+    emit_kernel<1><<<n_chunks, P_THREADS, sizeof(uint64_t) * J_RAW_WORDS, st>>>(J);
+  }
+  SMX_LAUNCH_CHECK();
+  return 0;
+}
+
 // The chain on `ws`: the one-pass kernel when SMX_CHAIN_ONEPASS=1, else
 // (default) the five kernels above.  Measured on B200 (C3 drive, C2
 // weights): the one-pass form is exact but slower -- RTF 0.057 vs 0.040, C2
@@ -712,7 +731,7 @@ extern "C" int smx_poisson_counts(uint64_t k0, uint64_t k1, const uint64_t* curs
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
   smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
   smx_count_launch(); within_kernel<<<ng, PE, 0, st>>>(J, gentry, gbase);
-  smx_count_launch(); emit_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  if (const int rc = launch_emit(J, n_chunks, st); rc) return rc;
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -765,7 +784,7 @@ extern "C" int smx_poisson_counts_ptrs(uint64_t k0, uint64_t k1, const uint64_t*
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
   smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
   smx_count_launch(); within_kernel<<<ng, PE, 0, st>>>(J, gentry, gbase);
-  smx_count_launch(); emit_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  if (const int rc = launch_emit(J, n_chunks, st); rc) return rc;
   SMX_LAUNCH_CHECK();
   return 0;
 }
@@ -807,7 +826,7 @@ extern "C" int smx_normal_fill(uint64_t k0, uint64_t k1, const uint64_t* cursor_
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
   smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
   smx_count_launch(); within_kernel<<<ng, PE, 0, st>>>(J, gentry, gbase);
-  smx_count_launch(); emit_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  if (const int rc = launch_emit(J, n_chunks, st); rc) return rc;
   SMX_LAUNCH_CHECK();
   return 0;
 }

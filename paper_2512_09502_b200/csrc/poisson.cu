@@ -92,6 +92,7 @@ __device__ __forceinline__ bool ptrs_trial(const PoisJob& J, double u, double v,
   return lhs <= rhs;
 }
 
+template <int KIND>
 __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
   __shared__ double U[PC + PE];
   __shared__ uint8_t L[PC + PE];
@@ -107,14 +108,14 @@ __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
     uint64_t b[4];
     smx::philox4x64_10(((cw >> 2) + q) + 1, J.key, b);  // cw is a multiple of 4
 #pragma unroll
-    for (int i = 0; i < 4; ++i) U[4 * q + i] = J.kind == 1 ? __longlong_as_double((long long)b[i]) : smx::u53(b[i]);
+    for (int i = 0; i < 4; ++i) U[4 * q + i] = KIND == 1 ? __longlong_as_double((long long)b[i]) : smx::u53(b[i]);
   }
   __syncthreads();
   // len(w) for w in [0, PC + PE): products forward; words past the window
   // tail are regenerated one at a time (rare).
   for (int w = tid; w < PC + PE; w += P_THREADS) {
     int k = 0;
-    if (J.kind == 0) {
+    if (KIND == 0) {
       double prod = 1.0;
       for (;;) {
         const int idx = w + k;
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(P_THREADS) chunk_kernel(PoisJob J) {
         if (!(prod > J.enlam)) break;
         if (k >= 255) break;
       }
-    } else if (J.kind == 2) {
+    } else if (KIND == 2) {
       // PTRS: two doubles per trial until one is accepted
       for (;;) {
         const int i0 = w + k, i1 = w + k + 1;
@@ -727,7 +728,10 @@ extern "C" int smx_poisson_counts(uint64_t k0, uint64_t k1, const uint64_t* curs
   J.cursor = cursor_out;
   J.err = err;
   if (const int rc = run_chain(J, n_chunks, ws, st); rc <= 0) return rc;
-  smx_count_launch(); chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  smx_count_launch();
+  if (J.kind == 0) chunk_kernel<0><<<n_chunks, P_THREADS, 0, st>>>(J);
+  else if (J.kind == 2) chunk_kernel<2><<<n_chunks, P_THREADS, 0, st>>>(J);
+  else chunk_kernel<1><<<n_chunks, P_THREADS, 0, st>>>(J);
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
   smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
   smx_count_launch(); within_kernel<<<ng, PE, 0, st>>>(J, gentry, gbase);
@@ -780,7 +784,10 @@ extern "C" int smx_poisson_counts_ptrs(uint64_t k0, uint64_t k1, const uint64_t*
   J.cursor = cursor_out;
   J.err = err;
   if (const int rc = run_chain(J, n_chunks, ws, st); rc <= 0) return rc;
-  smx_count_launch(); chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  smx_count_launch();
+  if (J.kind == 0) chunk_kernel<0><<<n_chunks, P_THREADS, 0, st>>>(J);
+  else if (J.kind == 2) chunk_kernel<2><<<n_chunks, P_THREADS, 0, st>>>(J);
+  else chunk_kernel<1><<<n_chunks, P_THREADS, 0, st>>>(J);
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
   smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
   smx_count_launch(); within_kernel<<<ng, PE, 0, st>>>(J, gentry, gbase);
@@ -822,7 +829,10 @@ extern "C" int smx_normal_fill(uint64_t k0, uint64_t k1, const uint64_t* cursor_
   J.cursor = cursor_out;
   J.err = err;
   if (const int rc = run_chain(J, n_chunks, ws, st); rc <= 0) return rc;
-  smx_count_launch(); chunk_kernel<<<n_chunks, P_THREADS, 0, st>>>(J);
+  smx_count_launch();
+  if (J.kind == 0) chunk_kernel<0><<<n_chunks, P_THREADS, 0, st>>>(J);
+  else if (J.kind == 2) chunk_kernel<2><<<n_chunks, P_THREADS, 0, st>>>(J);
+  else chunk_kernel<1><<<n_chunks, P_THREADS, 0, st>>>(J);
   smx_count_launch(); group_kernel<<<ng, PE, 0, st>>>(J);
   smx_count_launch(); across_kernel<<<1, 256, 0, st>>>(J, ng, gentry, gbase);
   smx_count_launch(); within_kernel<<<ng, PE, 0, st>>>(J, gentry, gbase);

@@ -23,5 +23,5 @@ run 4 c3_n4 --steps 5 --warmup 3
 run 2 c3s_n2 --strong --steps 5 --warmup 3
 run 4 c3s_n4 --strong --steps 5 --warmup 3
 SMX_PEER_EXCHANGE=0 run 2 c3_n2_nccl --steps 3 --warmup 3
-run 2 c4_n2 --workload c4 --steps 1 --warmup 1
-run 4 c4_n4 --workload c4 --steps 1 --warmup 1
+run 2 c4_n2 --workload c4 --steps 2 --warmup 1
+run 4 c4_n4 --workload c4 --steps 2 --warmup 1

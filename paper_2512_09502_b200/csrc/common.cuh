@@ -346,6 +346,15 @@ void smx_long_kernel_mark(cudaStream_t st);
 // draw chaining (capi.cu, smx_draw_chain): taken once by the next run_draw
 void smx_take_draw_chain(const uint64_t** u0_dev, uint64_t** cursor_dev);
 int smx_chain_passthrough(const uint64_t* u0_dev, uint64_t u0, uint64_t* cursor_dev, cudaStream_t st);
+// Scope of one chainable entry point: whatever path it returns by, a chain
+// setting it did not take does not leak into the next call.
+struct DrawChainScope {
+  ~DrawChainScope() {
+    const uint64_t* a;
+    uint64_t* b;
+    smx_take_draw_chain(&a, &b);
+  }
+};
 int smx_grid_cap(int grid, int concurrent_cap);
 int smx_pass_a_free_slots();   // fused.cu: CTA slots pass A leaves free
 extern "C" int* smx_device_error_word(void);

@@ -518,6 +518,7 @@ extern "C" int smx_gen_draw(uint64_t k0, uint64_t k1, uint64_t u0, uint64_t ex, 
                             uint32_t* keys, uint32_t* vals, uint32_t* used_bits, const uint32_t* used_tab,
                             uint32_t used_bits_words, int mark_from_key, uint32_t tmp_base, uint32_t local_bit,
                             uint64_t* cursor_out, void* stream) {
+  DrawChainScope chain_scope;
   if (n >= (1ULL << 32)) {
     smx_set_error("smx_gen_draw: %llu records in one call exceed 2^32", (unsigned long long)n);
     return -1;
@@ -728,6 +729,7 @@ extern "C" int smx_max_meta(const uint32_t* meta, uint64_t n, uint32_t* out3, vo
 // cursor u0 (sm/construction.py:168-169), stored as meta = delay | port << 24.
 extern "C" int smx_delay_fill(uint64_t k0, uint64_t k1, uint64_t u0, uint32_t lo, uint64_t ex, uint64_t n,
                               uint32_t port, uint32_t* meta, uint64_t* cursor_out, void* stream) {
+  DrawChainScope chain_scope;
   MetaSink s{lo, port << 24, meta};
   if (cursor_out) *cursor_out = u0;
   if (n == 0 || ex == 1) {   // (a chained call's cursor passes through)

@@ -34,10 +34,6 @@ int smx_stream_sync(void* stream);
 /* host wait policy for synchronisations, before context creation
  * (cudaDeviceScheduleSpin = 1, Yield = 2, BlockingSync = 4) */
 int smx_set_sync_policy(int flags);
-/* keep the default stream-ordered pool's memory mapped (no trim at sync) */
-/* A non-blocking stream (no implicit synchronisation with the legacy
- * default stream) at the given priority; the engine runs the fused path's
- * pass A and the preparation side work on such streams. */
 /* Device-side chaining of draws on one keyed stream (sm/construction.py:
  * 424-431: fixed_total's targets continue after its positions; 157-176: a
  * syn stream's delays continue after its normal weights).  The next draw
@@ -49,7 +45,12 @@ int smx_draw_chain(const uint64_t* u0_dev, uint64_t* cursor_dev);
  * replays and small kernels of the calls that follow (0..16, default 8).
  * Process-wide; a single-rank construction uses 0. */
 int smx_set_pass_a_free_sms(int n);
+/* A non-blocking stream (no implicit synchronisation with the legacy
+ * default stream) at the given priority; the engine runs the fused path's
+ * pass A and the preparation side work on such streams. */
 int smx_stream_create(int priority, void** out);
+/* keep the default stream-ordered pool's memory mapped (no trim at sync);
+ * no reuse of blocks through inserted cross-stream waits */
 int smx_pool_setup(int device);
 /* device error word of asynchronous paths: read + clear (synchronises stream) */
 int smx_check_device_errors(void* stream);
@@ -170,15 +171,17 @@ int smx_promote_wide(const uint32_t* vals, uint64_t n, const double* cls_w, cons
  * passes of an LSD radix sort whose first pass is the draw itself.
  * smx_fused_gen: one call's integers(0, ex, size=n_out) draws from the start
  * of stream (k0, k1), ranked by the low key digit and written as packed u32
- * records (key >> lo_bits) << pbits | cpay[j / kdiv] into the digit regions
+ * records (key >> lo_bits) << pbits | (pay_tab[j / kdiv] & 0xffffff) | cls_field
+ * (cls_field = the call's class index << its row bits) into the digit regions
  * (rstart / rcap / fill_in / fill_out: device arrays of 2^lo_bits entries;
- * cpay: the compact payload of each target, row | class index << row bits).
+ * pay_tab: smx_pay_table's row | class << 24 of each target).
  * key_mode 3: key_tab is a host array {n, start[n], delta[n]} of piecewise-
  * affine keys; key_mode 1: device table key_tab[value].  *total_out = accepted
  * draws of the raw window (< n_out: window short); *overflow set when a region
  * was too small (the caller rebuilds through smx_gen_draw + smx_sort_records). */
 int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_out, int key_mode, const uint32_t* key_tab,
-                  uint32_t kdiv, const uint32_t* cpay, int lo_bits, int pbits, uint32_t* region, uint64_t n_slots,
+                  uint32_t kdiv, const uint32_t* pay_tab, uint32_t cls_field, int lo_bits, int pbits,
+                  uint32_t* region, uint64_t n_slots,
                   const uint64_t* rstart, const uint64_t* rcap, const uint64_t* fill_in, uint64_t* fill_out,
                   uint64_t* total_out, int* overflow, void* stream);
 /* smx_fused_sort: pass B over the regions (region digit * per_digit + call

@@ -48,7 +48,7 @@ SIGNATURES = {
     "smx_peer_open": (I32, [P, P]),
     "smx_peer_close": (I32, [P]),
     "smx_peer_exchange": (I32, [P, I32, P, I32, P, P, P, P, P, P, U32, P, P, P, U32, P, U32, P]),
-    "smx_fused_gen": (I32, [U64, U64, U64, U64, I32, P, U32, P, I32, I32, P, U64, P, P, P, P, P, P, P]),
+    "smx_fused_gen": (I32, [U64, U64, U64, U64, I32, P, U32, P, U32, I32, I32, P, U64, P, P, P, P, P, P, P]),
     "smx_fused_sort": (I32, [P, P, P, I32, I32, I32, I32, P, P, P, U64, U64, P, P, P]),
     "smx_bits_or_many": (I32, [P, P, I32, U64, P]),
     "smx_check_device_errors": (I32, [P]),

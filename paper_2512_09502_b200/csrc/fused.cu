@@ -78,7 +78,8 @@ struct FusedGen {
   const uint32_t* key_tab;  // key mode 1: key = key_tab[value]
   uint32_t kdiv;      // k_in: target index = j / kdiv
   FastDiv kd;
-  const uint32_t* cpay;  // compact payload of each target index (row | class index << row bits)
+  const uint32_t* pay;   // payload of each target index (row | class << 24, smx_pay_table)
+  uint32_t cls_field;    // this call's class index << its row bits (the record's payload field)
   int pbits;          // bits below the high key digit in a record
   uint32_t* region;
   const uint64_t* rstart;   // [B] first slot of each digit region
@@ -348,8 +349,8 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       s_lim = jbase >= g.n_out ? 0u : (g.n_out - jbase > 0xffffffffull ? 0xffffffffu : (uint32_t)(g.n_out - jbase));
       if (g.kdiv >= FG_TILE) {
         const uint64_t n_tgt = (g.n_out + g.kdiv - 1) / g.kdiv;
-        s_cp[0] = tq < n_tgt ? __ldg(g.cpay + tq) : 0u;
-        s_cp[1] = tq + 1 < n_tgt ? __ldg(g.cpay + tq + 1) : 0u;
+        s_cp[0] = tq < n_tgt ? (__ldg(g.pay + tq) & 0xffffffu) | g.cls_field : 0u;
+        s_cp[1] = tq + 1 < n_tgt ? (__ldg(g.pay + tq + 1) & 0xffffffu) | g.cls_field : 0u;
       }
       if (t == n_tiles - 1) *g.total = jbase + tot;
     }
@@ -368,7 +369,8 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
       const uint32_t r = (rank2[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
       if (r == 0xffffu) continue;
       const uint32_t d = LB ? (k[i] & DM) : 0u;
-      const uint32_t cp = bigk ? (a >= kth ? cp1 : cp0) : __ldg(g.cpay + tq + g.kd.div(tr + a));
+      const uint32_t cp = bigk ? (a >= kth ? cp1 : cp0)
+                               : (__ldg(g.pay + tq + g.kd.div(tr + a)) & 0xffffffu) | g.cls_field;
       const uint32_t rec = a < left ? (((k[i] >> LB) << g.pbits) | cp) : FG_SENTINEL;
       const uint32_t pos = wcnt[warp * BC + d] + r;
       xs[pos] = rec;
@@ -917,7 +919,8 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, c
 // in the raw window (< n_out: the window was short, rebuild), *overflow is
 // set when a region is too small.
 extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_out, int key_mode,
-                             const uint32_t* key_tab, uint32_t kdiv, const uint32_t* cpay, int lo_bits, int pbits,
+                             const uint32_t* key_tab, uint32_t kdiv, const uint32_t* pay_tab, uint32_t cls_field,
+                             int lo_bits, int pbits,
                              uint32_t* region, uint64_t n_slots, const uint64_t* rstart, const uint64_t* rcap,
                              const uint64_t* fill_in, uint64_t* fill_out, uint64_t* total_out, int* overflow,
                              void* stream) {
@@ -956,7 +959,8 @@ extern "C" int smx_fused_gen(uint64_t k0, uint64_t k1, uint64_t ex, uint64_t n_o
   }
   g.kdiv = kdiv;
   g.kd = FastDiv::make(kdiv);
-  g.cpay = cpay;
+  g.pay = pay_tab;
+  g.cls_field = cls_field;
   if ((uint64_t)kdiv + 2 * FG_TILE >= 0xffffffffull) {
     smx_set_error("smx_fused_gen: k_in %u too large", kdiv);
     return -1;

@@ -829,7 +829,7 @@ class Cluster:
         (this one included) goes through the general path instead."""
         lm_thr = 0 if ex == (1 << 32) else ((1 << 32) - ex) % ex
         d = dict(key=key, ex=int(ex), n=int(n), kmode=kmode, ktab=ktab, pay_tab=pay_tab, cls=int(cls),
-                 per_record=per_record, pay_compact=None,
+                 per_record=per_record,
                  kdiv=int(kdiv), n_tgt=int(n_tgt), src_host=src_host, acct=acct, prej=lm_thr / 4294967296.0,
                  src_run=src_host is not None and _consecutive(np.asarray(src_host)))
         st.deferred.append(d)
@@ -1928,13 +1928,7 @@ class Cluster:
 
     def _gen_deferred(self, st: _Rank, d: dict):
         n = d["n"]
-        if d.get("pay_compact") is not None:   # per-record payloads back to row | class << 24
-            p = d["pay_tab"]
-            p.bitwise_and_((1 << d["pay_compact"]) - 1)
-            c24 = int(d["cls"]) << 24
-            if c24:
-                p.bitwise_or_(c24 - (1 << 32) if c24 >= (1 << 31) else c24)
-            d["pay_compact"] = None
+
         base = st.reserve_records(n)
         keys, vals = st.keys.t[base:], st.vals.t[base:]
         sk = st.stream
@@ -2029,15 +2023,7 @@ class Cluster:
         meta = _up(np.concatenate([rstart, cap]), dev)
         fills = torch.zeros((2, B), dtype=torch.int64, device=dev)
         total = torch.zeros(1, dtype=torch.int64, device=dev)
-        if d["per_record"]:   # one payload per record (fixed_total): compacted in place, no second copy
-            cpay = d["pay_tab"]
-            if d["pay_compact"] is None:
-                cpay.bitwise_and_(ROW_MASK)
-                if z["cidx"][d["cls"]]:
-                    cpay.bitwise_or_(z["cidx"][d["cls"]] << row_bits)
-                d["pay_compact"] = row_bits
-        else:
-            cpay = (d["pay_tab"] & ROW_MASK) | (z["cidx"][d["cls"]] << row_bits)   # row | class index
+        cls_field = z["cidx"][d["cls"]] << row_bits   # pass A packs row | class index << row bits
         # pass A runs on the generation stream: the main stream keeps only the
         # small map / image kernels that the preparation side stream waits on
         gen = _gen_stream(dev)
@@ -2049,19 +2035,20 @@ class Cluster:
         # SMs left free for the replays / small kernels of later calls: only
         # a multi-rank construction has any
         call("smx_set_pass_a_free_sms", 0 if self.n_ranks == 1 else self.PASS_A_FREE_SMS)
-        call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"], _ptr(cpay),
+        call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"],
+             _ptr(d["pay_tab"]), cls_field,
              z["lo"], z["pbits"], _ptr(region), slots, _ptr(meta[:B]), _ptr(meta[B:]), _ptr(fills[0]),
              _ptr(fills[1]), _ptr(total), _ptr(z["flag"]), gen.cuda_stream)
         if ev0 is not None:
             ev1 = torch.cuda.Event(enable_timing=True)
             ev1.record(gen)
             self.prof["gen"].append((ev0, ev1))
-        for tnsr in (region, meta, fills, total, cpay, z["flag"], d["pay_tab"]):
+        for tnsr in (region, meta, fills, total, z["flag"], d["pay_tab"]):
             tnsr.record_stream(gen)
         if d["kmode"] == 1:
             d["ktab"].record_stream(gen)
         zc = dict(region=region, rstart=rstart, cap=cap.astype(np.uint64), meta=meta, fill=fills[1],
-                  fills=fills, total=total, cpay=cpay, n=int(d["n"]), row_bits=row_bits)
+                  fills=fills, total=total, n=int(d["n"]), row_bits=row_bits)
         if slot is None:   # in call order (pass B keeps it within every key)
             d["zi"] = len(z["calls"])
             z["calls"].append(zc)

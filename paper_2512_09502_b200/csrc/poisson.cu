@@ -375,9 +375,13 @@ __global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
   __syncthreads();
   const int m = merge_p;
   if (m >= PC) return;
-  // S0 starts >= m, ranked in order
-  for (int q0 = 0; q0 < PC / 32; q0 += P_THREADS) {
-    const int q = q0 + tid;
+  // S0 starts >= m, ranked in order.  Normals (nearly every word starts a
+  // sample): word prefix counts first, then every thread takes positions
+  // p = m + tid, m + tid + P_THREADS, ... (all threads busy, neighbouring
+  // samples to neighbouring threads: coalesced 8-byte stores)
+  static_assert(PC / 32 <= P_THREADS, "one S0 word per thread in the prefix");
+  if constexpr (KIND != 1) {   // counts (about one start per two words): one S0 word per thread
+    const int q = tid;
     uint32_t bits = 0;
     if (q < PC / 32) {
       bits = S0[q];
@@ -386,7 +390,6 @@ __global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
     }
     uint32_t tot;
     const uint32_t ex = smx::block_excl_scan(__popc(bits), ws, tot);
-    // carry across iterations of q0: PC/32 = 64 words <= P_THREADS, one pass
     uint64_t k = kb + pre_n + ex;
     while (bits) {
       const int b = __ffs(bits) - 1;
@@ -395,6 +398,30 @@ __global__ void __launch_bounds__(P_THREADS) emit_kernel(PoisJob J) {
       emit<KIND>(J, k, c, p, L[p], raw);
       ++k;
     }
+    return;
+  }
+  __shared__ uint32_t wmask[PC / 32], wpre[PC / 32];
+  {
+    const int q = tid;
+    uint32_t bits = 0;
+    if (q < PC / 32) {
+      bits = S0[q];
+      const int lo = q * 32;
+      if (m > lo) bits &= (m - lo >= 32) ? 0u : ~((1u << (m - lo)) - 1);
+    }
+    uint32_t tot;
+    const uint32_t ex = smx::block_excl_scan(__popc(bits), ws, tot);
+    if (q < PC / 32) {
+      wmask[q] = bits;
+      wpre[q] = ex;
+    }
+  }
+  __syncthreads();
+  const uint64_t k0 = kb + pre_n;
+  for (int p = m + tid; p < PC; p += P_THREADS) {
+    const uint32_t bits = wmask[p >> 5];
+    const int b = p & 31;
+    if ((bits >> b) & 1u) emit<KIND>(J, k0 + wpre[p >> 5] + __popc(bits & ((1u << b) - 1u)), c, p, L[p], raw);
   }
 }
 

@@ -748,7 +748,7 @@ class Cluster:
                 call("smx_gen_draw", local_key[0], local_key[1], 0, n_tgt, min(piece, n - j0), 0, 1, 0,
                      _ptr(pay_tab), 1, 0, _ptr(rec_pay[j0:]), 0, 0, 0, 0, 0, 0, 0, st.stream)
             d = self._defer(st, aligned_key, n_src, n, 1, key_tab, rec_pay, 1, n, cls,
-                            src_host=np.asarray(sources, dtype=np.int64), per_record=True)
+                            src_host=np.asarray(sources, dtype=np.int64))
             return n, src
         self._fused_off(st)
         if cls is None:
@@ -822,14 +822,12 @@ class Cluster:
         st.commit_records(n)
         return n, src
 
-    def _defer(self, st: _Rank, key, ex, n, kmode, ktab, pay_tab, kdiv, n_tgt, cls, src_host=None, acct=None,
-               per_record=False):
+    def _defer(self, st: _Rank, key, ex, n, kmode, ktab, pay_tab, kdiv, n_tgt, cls, src_host=None, acct=None):
         """Register a fixed in-degree draw for the fused path and launch its
         pass A; when the record format cannot take it, every deferred call
         (this one included) goes through the general path instead."""
         lm_thr = 0 if ex == (1 << 32) else ((1 << 32) - ex) % ex
         d = dict(key=key, ex=int(ex), n=int(n), kmode=kmode, ktab=ktab, pay_tab=pay_tab, cls=int(cls),
-                 per_record=per_record,
                  kdiv=int(kdiv), n_tgt=int(n_tgt), src_host=src_host, acct=acct, prej=lm_thr / 4294967296.0,
                  src_run=src_host is not None and _consecutive(np.asarray(src_host)))
         st.deferred.append(d)

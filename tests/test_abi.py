@@ -38,3 +38,14 @@ def test_no_cpu_fallback_without_gpu():
     from paper_2512_09502_b200.engine import Cluster
     with pytest.raises(RuntimeError, match="CUDA"):
         Cluster(SimConfig())
+
+
+def test_pass_a_free_sms_bounds():
+    """smx_set_pass_a_free_sms takes 0..16 and reports anything else as a
+    ValueError-class status (-1) without touching the device."""
+    from paper_2512_09502_b200 import _lib
+    L = _lib.lib()
+    assert L.smx_set_pass_a_free_sms(8) == 0
+    assert L.smx_set_pass_a_free_sms(-1) == -1
+    assert L.smx_set_pass_a_free_sms(17) == -1
+    assert L.smx_set_pass_a_free_sms(8) == 0

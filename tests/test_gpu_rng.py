@@ -201,3 +201,25 @@ def test_choice_rows_parallel_chain(n, k, rows):
     want = np.stack([o.choice_no_replace(n, k) for _ in range(rows)])
     assert np.array_equal(got.cpu().numpy().view(np.uint32).astype(np.int64), want.astype(np.int64))
     assert cur == o.u32_used
+
+
+def test_draw_chain_does_not_leak_past_a_failed_call():
+    """A chain set for a draw call that then fails before drawing (bad key
+    mode) is dropped with it: the next, unrelated draw starts at its own
+    cursor (csrc/common.cuh DrawChainScope)."""
+    import ctypes
+    import torch
+    import device_rng as dr
+    from oracle.rng import OracleStream
+    from paper_2512_09502_b200 import _lib
+    from paper_2512_09502_b200.api import stream_key
+    L = _lib.lib()
+    cur = torch.tensor([12345], dtype=torch.int64, device="cuda")
+    assert L.smx_draw_chain(ctypes.c_void_p(cur.data_ptr()), None) == 0
+    rc = L.smx_gen_draw(1, 2, 0, 100, 10, 99, 0, None, None, 1, None, None, None, None, 0, 0, 0, 0, None,
+                        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == -1
+    key = stream_key(3, ("chain-scope",))
+    got, c = dr.integers(key, 0, 0, 1000, 5000)
+    o = OracleStream(0, key=key)
+    assert np.array_equal(got.cpu().numpy(), o.integers(0, 1000, size=5000))

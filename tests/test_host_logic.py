@@ -25,3 +25,17 @@ def test_population_runs_match_concatenated(seed):
     want = Cluster._pieces_of(all_rank, all_node, max_pieces=64)
     for g, w in zip(got, want):
         assert np.array_equal(g, w)
+
+
+def test_run_info():
+    """_run_info: one consecutive run (bounds from the ends) or the general
+    min / max; empty arrays; no caching across refills of one array."""
+    import numpy as np
+    from paper_2512_09502_b200.engine import _consecutive, _run_info
+    a = np.arange(7, 107, dtype=np.int64)
+    assert _run_info(a) == (True, 7, 106) and _consecutive(a)
+    a[50] = 3   # refilled in place: seen afresh
+    assert _run_info(a) == (False, 3, 106) and not _consecutive(a)
+    assert _run_info(np.array([5], dtype=np.int64)) == (False, 5, 5)
+    assert _run_info(np.array([], dtype=np.int64))[0] is False
+    assert _run_info(np.array([9, 8, 7], dtype=np.int64)) == (False, 7, 9)

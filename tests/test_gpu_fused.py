@@ -180,3 +180,24 @@ def test_fused_fixed_total(min_total, monkeypatch):
     f = _build(True, _fixed_total_mix)
     assert f.ranks[0].store_path == ("fused" if min_total == 0 else "general")
     assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))
+
+
+def test_speculation_redone_when_a_remote_run_is_never_drawn(monkeypatch):
+    """A remote source run that no draw hits gets no images, so the real key
+    pieces differ from the predicted ones while staying consecutive: pass A
+    is redone with the real keys in the call's place (spec_stats 'redone')."""
+    monkeypatch.setenv("SMX_SPECULATE", "force")
+
+    def fn(ns):
+        c = ns.make_cluster(ns.SimConfig(n_ranks=2, comm_mode="collective", seed=43))
+        a = c.create_neurons(0, 10_000, ns.LifParams(), -60.0)
+        b = c.create_neurons(1, 1, ns.LifParams(), -60.0, gids=np.array([10_000]))
+        A, Bn = np.arange(a.start, a.stop), np.arange(b.start, b.stop)
+        c.declare_group(0, [0, 1])
+        c.connect_fixed_indegree_distributed([(0, A), (1, Bn)], [(0, A[:100])], 1, ns.SynSpec(0.125, 2), group=0)
+        return c
+    g = _build(False, fn)
+    f = _build(True, fn)
+    assert f.spec_stats["redone"] == 1, f.spec_stats
+    assert f.ranks[0].store_path == "fused"
+    assert not tables.compare(tables.canon_gpu(f), tables.canon_gpu(g))

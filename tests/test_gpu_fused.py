@@ -71,6 +71,7 @@ def _fixed_total_mix(ns):
 CASES = {
     "balanced_1r": _balanced(1, "p2p", 3000, 240, 60),
     "balanced_4r_coll": _balanced(4, "collective", 700, 80, 20),
+    "balanced_8r_coll": _balanced(8, "collective", 600, 80, 20),   # 8 source pieces: the generic key mode
     "balanced_3r_p2p": _balanced(3, "p2p", 900, 100, 25),
     "local_mix": _local_mix,
 }

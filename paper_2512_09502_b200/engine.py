@@ -1645,7 +1645,7 @@ class Cluster:
         R["vbits"] = torch.zeros(max(total_words, 1), dtype=torch.int32, device=dev)
         R["n_distinct"] = self._n_distinct_gv(all_rank, all_node, vbase, total_words)
         R["excl"] = torch.empty(R["vbits"].numel() + 1, dtype=torch.int64, device=dev)
-        R["piece"] = max(int(R["n_distinct"] * (math.log(max(R["n_distinct"], 2)) + 6.0)), 1 << 20)
+        R["piece"] = max(int(R["n_distinct"] * (math.log(max(R["n_distinct"], 2)) + self.REPLAY_C)), 1 << 20)
         k = min(R["piece"], n)
         if k:
             self._replay_piece(R, 0, k, None)
@@ -1906,6 +1906,9 @@ class Cluster:
     # from this size on (below it the general path's two draws + sort are
     # faster; above it they do not fit: 32-bit record index, 20 B/synapse)
     FUSED_TOTAL_MIN = int(os.environ.get("SMX_FUSED_TOTAL_MIN", str(1 << 31)))
+    # first replay piece V (ln V + c) draws: covers every value with
+    # probability exp(-e^-c) (c = 6: 0.9975); a miss continues in pieces
+    REPLAY_C = float(os.environ.get("SMX_REPLAY_C", "6"))
     # SMs pass A leaves to the replays of later calls in multi-rank runs
     PASS_A_FREE_SMS = int(os.environ.get("SMX_PASS_A_FREE_SMS", "8"))
 

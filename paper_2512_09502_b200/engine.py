@@ -1909,8 +1909,10 @@ class Cluster:
     # first replay piece V (ln V + c) draws: covers every value with
     # probability exp(-e^-c) (c = 6: 0.9975); a miss continues in pieces
     REPLAY_C = float(os.environ.get("SMX_REPLAY_C", "6"))
-    # SMs pass A leaves to the replays of later calls in multi-rank runs
-    PASS_A_FREE_SMS = int(os.environ.get("SMX_PASS_A_FREE_SMS", "8"))
+    # SMs pass A leaves to the replays of later calls in multi-rank runs; the
+    # replays grow with the rank count (one per remote target rank), so by
+    # default 2 per rank up to 16 (measured at 4 GPUs: 8 -> 25.2 ms, 4 -> 31.7)
+    PASS_A_FREE_SMS = int(os.environ["SMX_PASS_A_FREE_SMS"]) if "SMX_PASS_A_FREE_SMS" in os.environ else None
 
     def _defer_ok(self, st: _Rank, cls, ex: int, n: int) -> bool:
         return (self.fused_enabled and st.fused_ok and cls is not None and not st.wide and ex >= 2 and n > 0
@@ -2035,7 +2037,8 @@ class Cluster:
         ktab = d["ktab"].ctypes.data if d["kmode"] == 3 else _ptr(d["ktab"])
         # SMs left free for the replays / small kernels of later calls: only
         # a multi-rank construction has any
-        call("smx_set_pass_a_free_sms", 0 if self.n_ranks == 1 else self.PASS_A_FREE_SMS)
+        free = self.PASS_A_FREE_SMS if self.PASS_A_FREE_SMS is not None else min(16, 2 * self.n_ranks)
+        call("smx_set_pass_a_free_sms", 0 if self.n_ranks == 1 else free)
         call("smx_fused_gen", d["key"][0], d["key"][1], d["ex"], d["n"], d["kmode"], ktab, d["kdiv"],
              _ptr(d["pay_tab"]), cls_field,
              z["lo"], z["pbits"], _ptr(region), slots, _ptr(meta[:B]), _ptr(meta[B:]), _ptr(fills[0]),

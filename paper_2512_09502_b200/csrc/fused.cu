@@ -64,6 +64,9 @@ static_assert(FG_IPT == 8 || FG_IPT == 16 || FG_IPT == 32, "padded transpose: a 
 #ifndef SMX_FG_LB_WIN
 #define SMX_FG_LB_WIN 4   // look-back descriptors read per step
 #endif
+#ifndef SMX_FG_LB_SLEEP
+#define SMX_FG_LB_SLEEP 64   // ns a look-back step backs off when its predecessor is still drawing
+#endif
 #ifndef SMX_FG_FREE_SMS
 #define SMX_FG_FREE_SMS 8
 #endif
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(FG_THREADS, SMX_FG_MIN_BLOCKS)
           }
 #endif
           if (done) break;
-          if (used == 0) __nanosleep(64);  // predecessor still drawing: leave the issue slots to others
+          if (used == 0) __nanosleep(SMX_FG_LB_SLEEP);  // predecessor still drawing: leave the issue slots to others
           i -= used;
         }
 #ifdef SMX_FG_LBSTAT

@@ -1799,22 +1799,24 @@ class Cluster:
         main.wait_stream(side)
         _record_stream(st.__dict__, main)  # side-stream allocations are used on main
         check(_lib.lib().smx_check_device_errors(sk), "construction")  # asynchronous draws
-        if st.pending_errs:
-            e = int(torch.stack(st.pending_errs).max().item())
-            st.pending_errs = []
-            if e:
-                raise RuntimeError(f"normal weight chain error {e}")
-        if fused and not self._fused_check(st):
+        # every small device result the checks below read, in one transfer
+        # (the stream is idle here; each separate .item() would be a round trip)
+        probe = self._prepare_probe(st, fused)
+        if probe["err"]:
+            raise RuntimeError(f"normal weight chain error {probe['err']}")
+        if fused and not self._fused_check(st, probe):
             # a digit region overflowed or a raw window was short (both ~never):
             # regenerate every deferred call into the pending buffers and sort
             self._fused_off(st)
             sorted_state = self._sort_pending(st)
+            probe = self._prepare_probe(st, False)
+            if probe["err"]:
+                raise RuntimeError(f"normal weight chain error {probe['err']}")
         n = st.n_records
-        if n and int(st.first_index[-1].item()) != n:
+        if n and probe["fi_last"] != n:
             raise ConsistencyError(f"record source beyond node count {n_nodes}")
-        for d in st.devices:
-            if d.get("rows_ok") is not None and not bool(d["rows_ok"]):
-                raise ValueError("poisson targets must be real neurons")
+        if not probe["rows_ok"]:
+            raise ValueError("poisson targets must be real neurons")
         # modeled bytes of construction + prepare (sm/construction.py:763-807);
         # record counts of deferred calls exist only now
         st.mem.resolve()
@@ -1827,8 +1829,7 @@ class Cluster:
         st.lut = None
         st.fz = None
         st.deferred = []
-        fi = st.first_index
-        max_len = int((fi[1:] - fi[:-1]).max().item()) if st.n_nodes else 0
+        max_len = probe["max_len"]
         max_chunks = max(1, -(-max_len // 1024))
         st.owner_cap = st.N * self.block * max_chunks + 16
         st.owner = torch.zeros(st.owner_cap, dtype=torch.int32, device=dev)
@@ -2140,16 +2141,49 @@ class Cluster:
             cnt.copy_(cs[his] - cs[los])
         z["keep"] = (rptr_t, fill, cls_map_t)
 
-    def _fused_check(self, st: _Rank) -> bool:
+    @staticmethod
+    def _prepare_probe(st: _Rank, fused: bool) -> dict:
+        """The device scalars prepare checks after the sort, fetched with one
+        device->host copy: the normal-chain error word, the fused flags and
+        per-call totals, first_index's last entry and the longest key run."""
+        parts, names = [], []
+
+        def add(name, t):
+            t = t.reshape(-1).to(torch.int64)
+            names.append((name, t.numel()))
+            parts.append(t)
+
+        if st.pending_errs:
+            add("err", torch.stack(st.pending_errs).max())
+            st.pending_errs = []
+        if fused:
+            add("flag", st.fz["flag"])
+            add("totals", torch.cat([zc["total"] for zc in st.fz["calls"]]))
+        fi = st.first_index
+        if st.n_records:
+            add("fi_last", fi[-1])
+        if st.n_nodes:
+            add("max_len", (fi[1:] - fi[:-1]).max())
+        oks = [d["rows_ok"] for d in st.devices if d.get("rows_ok") is not None]
+        if oks:
+            add("rows_ok", torch.stack(oks).all())
+        flat = torch.cat(parts).cpu().numpy() if parts else np.empty(0, np.int64)
+        out = {"err": 0, "fi_last": 0, "max_len": 0, "rows_ok": 1}
+        at = 0
+        for name, k in names:
+            out[name] = flat[at: at + k] if name in ("flag", "totals") else int(flat[at])
+            at += k
+        return out
+
+    def _fused_check(self, st: _Rank, probe: dict) -> bool:
         z = st.fz
-        f = z["flag"].cpu().numpy()
+        f = probe["flag"]
         if int(f[0]):
             return False   # a region overflowed: its records are incomplete (pass B saw a clamped fill)
         if int(f[1]):
             raise ConsistencyError(f"fused sort: device error {int(f[1])}")
-        totals = torch.cat([zc["total"] for zc in z["calls"]]).cpu().numpy()
         want = np.array([zc["n"] for zc in z["calls"]], dtype=np.int64)
-        return not int(f[0]) and bool((totals >= want).all())
+        return bool((probe["totals"] >= want).all())
 
     def _prepare_tables(self, st: _Rank):
         """Everything of prepare that does not read the sorted store: neuron

@@ -504,7 +504,8 @@ class Cluster:
             if not self.is_local(rank) and self.images_made[rank]:
                 raise NotImplementedError(
                     "node ranges of a remote rank are unknown after it created images")
-            if gids is None:
+            gids_run = gids is None   # the default gids are a run: no host scan to upload them
+            if gids_run:
                 gids = np.arange(start, start + n, dtype=np.int64)
             else:
                 gids = np.asarray(gids, dtype=np.int64)
@@ -526,7 +527,11 @@ class Cluster:
                 if len(v_init) != 3 or v_init[0] != "normal":
                     raise ValueError(f"bad v_init spec {v_init!r}")
                 v = torch.empty(n, dtype=torch.float64, device=dev)
-                g = _up_index(gids, dev)
+                if gids_run:
+                    H2D_BYTES[0] += 16   # as _up_index counts a run
+                    g = torch.arange(start, start + n, dtype=torch.int64, device=dev)
+                else:
+                    g = _up_index(gids, dev)
                 pre = canonical_bytes((int(self.cfg.seed), ("init-v", 0)))
                 prefix = pre[: pre.rindex(b"i:0))") + 2]
                 suffix = b"))"

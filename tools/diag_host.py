@@ -14,6 +14,8 @@ from paper_2512_09502_b200 import api, engine, models  # noqa: E402
 
 T = defaultdict(float)
 N = defaultdict(int)
+EV = []          # (start, duration, name) of the current iteration (TIMELINE=1)
+T0 = [0.0]
 
 
 def wrap(cls, name):
@@ -26,6 +28,7 @@ def wrap(cls, name):
         finally:
             T[name] += time.perf_counter() - t0
             N[name] += 1
+            EV.append((t0 - T0[0], time.perf_counter() - t0, name))
     setattr(cls, name, g)
 
 
@@ -38,6 +41,7 @@ def timed_call(name, *a):
         return _call(name, *a)
     finally:
         T["call:" + name] += time.perf_counter() - t0
+        EV.append((t0 - T0[0], time.perf_counter() - t0, "call:" + name))
         N["call:" + name] += 1
 
 
@@ -77,9 +81,11 @@ cfg = api.SimConfig(n_ranks=world, comm_mode="collective" if world > 1 and not o
 for it in range(4):
     T.clear()
     N.clear()
+    EV.clear()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
+    T0[0] = t0
     e0.record()
     if world > 1:
         dist.barrier()
@@ -101,6 +107,9 @@ for it in range(4):
         print(f"iter {it}: host {1e3 * host:.2f} ms, gpu span {e0.elapsed_time(e1):.2f} ms, "
               f"store {c.ranks[rank].store_path}", flush=True)
     del c
+if rank == 0 and os.environ.get("TIMELINE"):   # host timeline of the last iteration
+    for a, d, name in sorted(EV):
+        print(f"  t={1e3 * a:8.3f} ms  {1e3 * d:7.3f} ms  {name}")
 if rank == 0:
     for k in sorted(T, key=lambda k: -T[k]):
         print(f"  {k:40s} {1e3 * T[k]:8.3f} ms  x{N[k]}")

@@ -27,4 +27,6 @@ pr = cProfile.Profile()
 pr.enable()
 build()
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(int(os.environ.get("TOP", "30")))
+st = pstats.Stats(pr)
+st.sort_stats("tottime").print_stats(int(os.environ.get("TOP", "30")))
+st.sort_stats("cumulative").print_stats("engine.py", int(os.environ.get("TOP", "30")))

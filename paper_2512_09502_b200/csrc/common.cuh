@@ -358,6 +358,14 @@ struct DrawChainScope {
 int smx_grid_cap(int grid, int concurrent_cap);
 int smx_pass_a_free_slots();   // fused.cu: CTA slots pass A leaves free
 extern "C" int* smx_device_error_word(void);
+// Kernel attributes (dynamic SMEM limits) are per device: launchers keep one
+// bit per device in a static mask and set the attribute the first time they
+// launch on each device.
+inline unsigned long long smx_device_bit() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return 1ull << (dev & 63);
+}
 #define SMX_CUDA_CHECK(expr)                                                       \
   do {                                                                             \
     cudaError_t _e = (expr);                                                       \

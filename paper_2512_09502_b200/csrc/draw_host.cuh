@@ -15,11 +15,12 @@ struct DrawResult {
 template <class Sink, int MARK>
 int launch_write(int G, size_t smem, cudaStream_t st, const DrawRange& r, const uint64_t* offs, uint64_t n_out,
                  const Sink& sink, uint64_t* cur_d, const DrawMark& mk) {
-  static bool configured = false;
-  if (smem > 0 && !configured) {  // static (staging) + dynamic (bitmap) may exceed the 48 KB default
+  static unsigned long long configured = 0;   // one bit per device
+  const unsigned long long dbit = smx_device_bit();
+  if (smem > 0 && !(configured & dbit)) {  // static (staging) + dynamic (bitmap) may exceed the 48 KB default
     SMX_CUDA_CHECK(cudaFuncSetAttribute(draw_write_kernel<Sink, MARK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)(DRAW_MARK_SMEM_WORDS * 4)));
-    configured = true;
+    configured |= dbit;
   }
   smx_count_launch(); draw_write_kernel<Sink, MARK><<<G, DRAW_THREADS, smem, st>>>(r, offs, n_out, sink, cur_d, mk);
   return 0;
@@ -29,12 +30,14 @@ template <class Sink, int MARK>
 int launch_op(int G, size_t smem, cudaStream_t st, const DrawRange& r, uint32_t tile, uint32_t n_tiles,
               uint64_t* desc, uint32_t* ticket, uint64_t* total_d, uint64_t n_out, const Sink& sink, uint64_t* cur_d,
               const DrawMark& mk) {
-  static size_t configured = 0;
+  static size_t configured[64] = {};   // per device: the largest limit set so far
+  int dev = 0;
+  cudaGetDevice(&dev);
   smem += (size_t)DRAW_WARPS * tile * 4;
-  if (smem > 48 * 1024 && smem > configured) {
+  if (smem > 48 * 1024 && smem > configured[dev & 63]) {
     SMX_CUDA_CHECK(cudaFuncSetAttribute(draw_onepass_kernel<Sink, MARK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-    configured = smem;
+    configured[dev & 63] = smem;
   }
   smx_count_launch();
   draw_onepass_kernel<Sink, MARK><<<G, DRAW_THREADS, smem, st>>>(r, tile, n_tiles, desc, ticket, total_d, n_out,

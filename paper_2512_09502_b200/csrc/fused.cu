@@ -407,13 +407,12 @@ size_t fg_smem() {
 template <int KM, int LB, bool WIDE>
 int fg_launch(const FusedGen& g, uint32_t n_tiles, cudaStream_t st) {
   const size_t smem = fg_smem<LB>();
-  static int configured = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured != dev) {  // per device (one Cluster drives one device; see engine)
+  static unsigned long long configured = 0;   // one bit per device
+  const unsigned long long dbit = smx_device_bit();
+  if (!(configured & dbit)) {
     SMX_CUDA_CHECK(cudaFuncSetAttribute(fused_gen_kernel<KM, LB, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-    configured = dev;
+    configured |= dbit;
   }
   // persistent CTAs on 140 of the 148 SMs: the replays and small kernels of
   // the calls that follow (their host code waits on them) run beside pass A
@@ -870,16 +869,15 @@ int fb_run(const FusedSort& s, uint32_t n_tiles, uint32_t n_chunks, bool wide, c
   constexpr int HW = fb_hist_warps<BITS>();
   const size_t h_smem = (size_t)HW * BINS * 4;
   const size_t s_smem = (size_t)FB_TILE * 6 + (size_t)BINS * 12 + (size_t)FB_WARPS * BINS * 2;
-  static int configured = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured != dev) {
+  static unsigned long long configured = 0;   // one bit per device
+  const unsigned long long dbit = smx_device_bit();
+  if (!(configured & dbit)) {
     SMX_CUDA_CHECK(cudaFuncSetAttribute(fb_hist_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h_smem));
     SMX_CUDA_CHECK(cudaFuncSetAttribute(fb_scatter_kernel<BITS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)s_smem));
     SMX_CUDA_CHECK(cudaFuncSetAttribute(fb_scatter_kernel<BITS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)s_smem));
-    configured = dev;
+    configured |= dbit;
   }
   const uint32_t hgrid = std::max<uint32_t>(1, std::min<uint32_t>((n_tiles + HW - 1) / HW, (148 - SMX_FG_FREE_SMS) * 2));
   smx_count_launch(); fb_hist_kernel<BITS><<<hgrid, 32 * HW, h_smem, st>>>(s, tcnt, n_tiles);

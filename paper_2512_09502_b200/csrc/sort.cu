@@ -664,8 +664,9 @@ int run_pass(const SortPass& p, uint32_t n_tiles, uint16_t* tcnt, uint32_t* off,
   const size_t smem = downsweep_smem<BITS>();
   const size_t smem_last = downsweep_last_smem<BITS>();
   const size_t th_smem = (size_t)4 * (th_hist_warps(BITS) * BINS + CNT_BINS);
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;   // one bit per device
+  const unsigned long long dbit = smx_device_bit();
+  if (!(configured & dbit)) {
     SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
     SMX_CUDA_CHECK(cudaFuncSetAttribute(downsweep_last_kernel<BITS, true>,
@@ -674,7 +675,7 @@ int run_pass(const SortPass& p, uint32_t n_tiles, uint16_t* tcnt, uint32_t* off,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_last));
     SMX_CUDA_CHECK(cudaFuncSetAttribute(tile_hist_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)th_smem));
-    configured = true;
+    configured |= dbit;
   }
   const uint32_t n_chunks = (n_tiles + TC - 1) / TC;
   const uint32_t hg = std::min<uint32_t>(n_tiles, 148 * 2);

@@ -90,6 +90,16 @@ def _up_index(arr, dev) -> torch.Tensor:
 
 _PREP_STREAMS: dict = {}
 _GEN_STREAMS: dict = {}
+_CAPTURE_STREAMS: dict = {}
+
+
+def _capture_stream(dev) -> "torch.cuda.Stream":
+    """Block-graph capture stream of a device (torch's default capture stream
+    is one process-wide stream on whichever device was current first)."""
+    key = torch.device(dev).index
+    if key not in _CAPTURE_STREAMS:
+        _CAPTURE_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _CAPTURE_STREAMS[key]
 
 
 def _gen_stream(dev) -> "torch.cuda.Stream":
@@ -393,6 +403,10 @@ class Cluster:
             # kernel attributes are configured once per process: several
             # devices need one process each (torchrun), not one Cluster
             raise ValueError("one Cluster drives one device; use one process per GPU (torchrun) for several")
+        # native calls launch on the current device (kernel attributes and the
+        # error word are per device): every façade call makes this one current
+        self.device = devices[0]
+        self._on_device()
         self.ranks: dict[int, _Rank] = {
             r: _Rank(r, devices[i % len(devices)]) for i, r in enumerate(self.local)}
         for st in self.ranks.values():
@@ -438,6 +452,7 @@ class Cluster:
     def _timed(self, bucket):
         """Phase timer of one façade call (sm/engine.py:212-219), with an NVTX
         range of the same name for nsys / ncu timelines."""
+        self._on_device()
         starts = [(st, self._event(st)) for st in self.ranks.values()]
         t0 = time.perf_counter()
         torch.cuda.nvtx.range_push(bucket)
@@ -447,6 +462,10 @@ class Cluster:
             torch.cuda.nvtx.range_pop()
             host_s = time.perf_counter() - t0
             self.timers._pending.append((bucket, host_s, [(a, self._event(st)) for st, a in starts]))
+
+    def _on_device(self):
+        if self.device.index is not None and torch.cuda.current_device() != self.device.index:
+            torch.cuda.set_device(self.device)
 
     @staticmethod
     def _event(st):
@@ -2522,7 +2541,7 @@ class Cluster:
                 g = torch.cuda.CUDAGraph()
                 ok = True
                 try:
-                    with torch.cuda.graph(g):
+                    with torch.cuda.graph(g, stream=_capture_stream(self._dev0())):
                         self._block_body(n_steps)
                         if nccl and self._xgraph_ok:
                             self._exchange_nccl()
@@ -2543,7 +2562,7 @@ class Cluster:
                         for st in self.ranks.values():
                             torch.cuda.synchronize(st.device)
                         g = torch.cuda.CUDAGraph()
-                        with torch.cuda.graph(g):
+                        with torch.cuda.graph(g, stream=_capture_stream(self._dev0())):
                             self._block_body(n_steps)
                 self._graph = g
             self._graph.replay()
@@ -2594,6 +2613,7 @@ class Cluster:
         readback per step); simulate() keeps everything on the device."""
         if not self.prepared:
             raise ConsistencyError("prepare() the cluster before stepping")
+        self._on_device()
         keep = self._recording
         marks = {r: int(st.n_rec.item()) for r, st in self.ranks.items()}
         self._set_record(True)
@@ -2915,6 +2935,7 @@ class Cluster:
         wall time bracketed by device synchronisations."""
         if not self.prepared:
             self.prepare()
+        self._on_device()
         warm = self.cfg.steps_for(warmup_ms)
         steps = self.cfg.steps_for(model_ms)
         self.phase = "propagation"

@@ -201,3 +201,34 @@ def test_several_devices_rejected():
     with pytest.raises(ValueError):
         Cluster(api.SimConfig(n_ranks=2), devices=["cuda:0", "cuda:1"])
     Cluster(api.SimConfig(n_ranks=2), devices=["cuda:0", "cuda:0"])  # one device: fine
+
+
+def test_second_device_in_one_process():
+    """A Cluster on cuda:1 next to one on cuda:0 in the same process (kernel
+    attributes and the device error word are per device; every façade call
+    makes the cluster's device current): both build the C1 tables with the
+    reference's digests, the calls interleaved."""
+    import torch
+    from paper_2512_09502_b200.engine import Cluster
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    want = json.load(open(os.path.join(GOLD, "c1_digests.json")))
+    cfgd = want["config"]
+    ns = gpu_ns()
+    p = ns.BalancedParams(neurons_per_rank=cfgd["neurons_per_rank"], k_exc=cfgd["k_exc"], k_inh=cfgd["k_inh"])
+    cfg = ns.SimConfig(n_ranks=1, comm_mode=cfgd["comm_mode"], seed=cfgd["seed"])
+    try:
+        c0 = Cluster(cfg, devices=["cuda:0"])
+        ns.build_balanced_network(c0, p)
+        c1 = Cluster(cfg, devices=["cuda:1"])
+        ns.build_balanced_network(c1, p)
+        c0.prepare()
+        c1.prepare()
+        assert c1.ranks[0].device == torch.device("cuda", 1)
+        for c in (c1, c0):
+            assert tables.digests(tables.canon_gpu(c)) == want["tables"]
+        r1 = c1.simulate(0.0, cfgd["model_ms"], record=True)
+        r0 = c0.simulate(0.0, cfgd["model_ms"], record=True)
+        assert r1.raster_sha256 == r0.raster_sha256 == want["raster"]["sha256"]
+    finally:
+        torch.cuda.set_device(0)
